@@ -1,0 +1,147 @@
+/*
+ * quik_b200.h — C ABI of the B200-native QUIK hybrid W4A4 / W8A8 linear layer.
+ *
+ * Drop-in boundary for the reference's C++ layer API (namespace quik, in
+ * /root/reference/proj). Each entry point names the reference interface it
+ * replaces. Plain pointers and sizes only; no exceptions cross this boundary:
+ * every call returns a quik_status and quik_last_error() holds the message
+ * (thread-local). The C++ facade in quik_b200.hpp rethrows them as the
+ * reference's exception types (std::invalid_argument, std::out_of_range,
+ * quik::NumericalError).
+ *
+ * Memory: unless stated otherwise pointers are DEVICE pointers owned by the
+ * caller, and calls are asynchronous on `stream` (a cudaStream_t, NULL = legacy
+ * default stream). Non-finite activations raise a device flag which the next
+ * quik_ctx_sync() reports as QUIK_ERR_NUMERICAL (reference runtime.cpp:52).
+ *
+ * Threading: a layer handle is immutable after creation; forwards on the same
+ * layer may run concurrently from different contexts (SPEC.md "forward passes
+ * are pure and may run concurrently"). A context owns scratch memory and must
+ * not be used from two host threads at once.
+ */
+#ifndef QUIK_B200_H_
+#define QUIK_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QUIK_B200_ABI_VERSION 1
+
+typedef enum quik_status {
+  QUIK_OK = 0,
+  QUIK_ERR_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+  QUIK_ERR_OUT_OF_RANGE = 2,     /* reference: std::out_of_range (pack range errors) */
+  QUIK_ERR_NUMERICAL = 3,        /* reference: quik::NumericalError (non-finite activations) */
+  QUIK_ERR_CUDA = 4,             /* CUDA runtime / driver failure, or no sm_100 device */
+  QUIK_ERR_NCCL = 5,             /* reserved: collective failure */
+  QUIK_ERR_UNSUPPORTED = 6
+} quik_status;
+
+/* Element types of activation / output buffers. */
+typedef enum quik_dtype { QUIK_F16 = 0, QUIK_F32 = 1 } quik_dtype;
+
+/* reference: quik::PipelineVariant (runtime.hpp:31). All three are bit-identical. */
+typedef enum quik_variant { QUIK_V1_UNFUSED = 0, QUIK_V2_FUSED_QUANT = 1, QUIK_V3_FUSED_EPILOGUE = 2 } quik_variant;
+
+typedef struct quik_ctx_s* quik_ctx_t;
+typedef struct quik_layer_s* quik_layer_t;
+
+const char* quik_last_error(void);
+const char* quik_status_string(quik_status s);
+int quik_abi_version(void);
+
+/* Context: device binding, scratch memory, device error flag. */
+quik_status quik_ctx_create(int device, quik_ctx_t* out);
+quik_status quik_ctx_destroy(quik_ctx_t ctx);
+/* Synchronises `stream`, then reports (and clears) the non-finite-input flag. */
+quik_status quik_ctx_sync(quik_ctx_t ctx, void* stream);
+
+/*
+ * Layer weights, HOST memory, in the reference's formats.
+ * reference: quik::QuantizedWeights (quantizer.hpp:48-58), quik::OutlierSet
+ * (calibration.hpp:37-48), quik::QuikLinearLayer (runtime.hpp:33-44).
+ *   base            packed [out_features][row_bytes]: bits 4 -> i4p (low nibble = even
+ *                   column, stored = v + 8, packed.hpp:11-16), bits 8 -> two's complement
+ *   scales          [out_features] per-row symmetric weight scales
+ *   wreduced        [out_features] scale[r] * sum_j q[r][j] (quantizer.cpp:159-165)
+ *   outlier_weights [out_features][n_outlier] f32 (rounded to f16 on the device)
+ *   outlier_indices [n_outlier] sorted, unique, in [0, in_features)
+ *   bias            [out_features] or NULL
+ *   row_begin/row_end: optional output-row shard [row_begin, row_end) of the layer
+ *                   (multi-GPU column sharding); 0/0 = all rows.
+ */
+typedef struct quik_weights_desc {
+  int64_t in_features;
+  int64_t out_features;
+  int bits;     /* base weight bits: 4 or 8 */
+  int act_bits; /* activation bits; must equal bits (runtime.cpp:162-164) */
+  const uint8_t* base;
+  const float* scales;
+  const float* wreduced;
+  const float* outlier_weights;
+  const int64_t* outlier_indices;
+  int64_t n_outlier;
+  const float* bias;
+  int64_t row_begin;
+  int64_t row_end;
+} quik_weights_desc;
+
+/* Uploads and repacks the weights into the device GEMM layout.
+ * Replaces QuikLinearLayer::validate (runtime.cpp:150-167) + per-call unpack_int4
+ * of the weights (packed.cpp:110-111), which the device path does once here. */
+quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* desc, quik_layer_t* out);
+quik_status quik_layer_destroy(quik_layer_t layer);
+quik_status quik_layer_info(quik_layer_t layer, int64_t* in_features, int64_t* out_features,
+                            int64_t* n_outlier, int* bits);
+
+/*
+ * K1 fused quantizer. reference: quantize_activations_fused (runtime.hpp:55-56,
+ * runtime.cpp:199-220). x: [M][in_features] (x_dtype). Outputs in the reference
+ * formats: packed [M][row_bytes(K_b)] (i4p or i8), scale[M], zero[M] (row min),
+ * x_outlier [M][n_outlier] f32. Any output pointer may be NULL.
+ */
+quik_status quik_quantize_activations_fused(quik_ctx_t ctx, quik_layer_t layer, const void* x, quik_dtype x_dtype,
+                                            int64_t M, uint8_t* packed, float* scale, float* zero,
+                                            float* x_outlier, void* stream);
+
+/* Unfused quantizer of an already-split base matrix [M][K].
+ * reference: quantize_activations (runtime.hpp:51, runtime.cpp:188-197). */
+quik_status quik_quantize_activations(quik_ctx_t ctx, const void* x_base, quik_dtype x_dtype, int64_t M, int64_t K,
+                                      int bits, uint8_t* packed, float* scale, float* zero, void* stream);
+
+/* Exact INT32 GEMM of two packed operands, out[i][j] = sum_k x[i][k] * w[j][k].
+ * reference: int_matmul (packed.hpp:58, packed.cpp:93-132), same argument checks. */
+quik_status quik_int_matmul(quik_ctx_t ctx, const uint8_t* x_packed, int64_t x_rows, int64_t x_cols, int x_bits,
+                            const uint8_t* w_packed, int64_t w_rows, int64_t w_cols, int w_bits, int32_t* out,
+                            void* stream);
+
+/* out[t][r] = acc[t][r]*sa[t]*sw[r] + (za[t] + half_range*sa[t]) * wreduced[r], f32.
+ * reference: dequantize_epilogue (runtime.hpp:66-68, runtime.cpp:222-244), bit-exact. */
+quik_status quik_dequantize_epilogue(quik_ctx_t ctx, const int32_t* acc, int64_t M, int64_t N,
+                                     const float* scale_act, const float* zero_act, int half_range,
+                                     const float* weight_scales, const float* wreduced, float* out, void* stream);
+
+/* The hot path: y[M][out_features] = quik_matmul(layer, x).
+ * reference: quik_matmul (runtime.hpp:85-87, runtime.cpp:246-318), LayerMode::Quik.
+ * x_dtype/y_dtype: QUIK_F16 (hot) or QUIK_F32. V3 runs two kernels: K1 and the
+ * fused tcgen05 GEMM + epilogue. V1/V2 run the unfused stages for debugging. */
+quik_status quik_linear_forward(quik_ctx_t ctx, quik_layer_t layer, const void* x, quik_dtype x_dtype, int64_t M,
+                                void* y, quik_dtype y_dtype, quik_variant variant, void* stream);
+
+/* Same, writing into a column slice of a wider output: y + col_offset with row
+ * pitch ldy elements (used by sharded layers to place their shard in place). */
+quik_status quik_linear_forward_strided(quik_ctx_t ctx, quik_layer_t layer, const void* x, quik_dtype x_dtype,
+                                        int64_t M, void* y, quik_dtype y_dtype, int64_t ldy, quik_variant variant,
+                                        void* stream);
+
+/* Number of device kernels quik_linear_forward launches for (variant) — the
+ * bench reports it as gpu_launches. */
+int quik_linear_forward_launches(quik_variant variant);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QUIK_B200_H_ */

@@ -1,0 +1,251 @@
+// ref_shim.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// extern "C" wrapper around the reference's own C++ implementation so the test
+// suite (and bench.py's reference / cpu_baseline leg) can call it from Python.
+// Compiled together with the UNMODIFIED reference sources
+//   /root/reference/proj/src/{packed,calibration,quantizer,runtime}.cpp
+// into oracle/_ref/libquik_ref.so by paper_2310_09259_b200/build.py
+// (flags: the reference's Release flags, proj/CMakeLists.txt:11-13).
+// Nothing here re-implements the algorithm; it only marshals plain arrays.
+#include <chrono>
+#include <cstring>
+#include <random>
+#include <stdexcept>
+#include <vector>
+
+#include "quik/calibration.hpp"
+#include "quik/packed.hpp"
+#include "quik/quantizer.hpp"
+#include "quik/runtime.hpp"
+
+namespace {
+
+int status_of(const std::exception_ptr& e) {
+  try {
+    std::rethrow_exception(e);
+  } catch (const quik::NumericalError&) {
+    return 3;
+  } catch (const std::out_of_range&) {
+    return 2;
+  } catch (const std::invalid_argument&) {
+    return 1;
+  } catch (...) {
+    return 9;
+  }
+}
+
+quik::FpMatrix to_fp(const float* p, int64_t r, int64_t c) {
+  quik::FpMatrix m(r, c);
+  if (r * c) std::memcpy(m.data.data(), p, sizeof(float) * r * c);
+  return m;
+}
+
+quik::PackedIntMatrix to_packed(const uint8_t* p, int64_t r, int64_t c, int bits) {
+  quik::PackedIntMatrix m;
+  m.rows = r;
+  m.cols = c;
+  m.bits = bits;
+  m.data.assign(p, p + r * m.row_bytes());
+  return m;
+}
+
+struct Layer {
+  quik::QuikLinearLayer layer;
+};
+
+quik::QuikLinearLayer make_layer(int64_t in, int64_t out, int bits, int act_bits, const uint8_t* base,
+                                 const float* scales, const float* wreduced, const float* ow, const int64_t* idx,
+                                 int64_t n_out, const float* bias) {
+  quik::QuikLinearLayer L;
+  L.outliers = quik::OutlierSet::from_indices(in, std::vector<int64_t>(idx, idx + n_out));
+  L.weights.base = to_packed(base, out, in - n_out, bits);
+  L.weights.scales.assign(scales, scales + out);
+  L.weights.wreduced.assign(wreduced, wreduced + out);
+  L.weights.outlier_weights = to_fp(ow, out, n_out);
+  if (bias) L.bias.assign(bias, bias + out);
+  L.act_bits = act_bits;
+  return L;
+}
+
+}  // namespace
+
+extern "C" {
+
+int qr_pack(const int8_t* vals, int64_t rows, int64_t cols, int bits, uint8_t* out) {
+  try {
+    auto m = quik::pack_values(std::span<const int8_t>(vals, rows * cols), rows, cols, bits);
+    std::memcpy(out, m.data.data(), m.data.size());
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
+int qr_unpack(const uint8_t* packed, int64_t rows, int64_t cols, int bits, int8_t* out) {
+  try {
+    auto v = quik::unpack_values(to_packed(packed, rows, cols, bits));
+    std::memcpy(out, v.data(), v.size());
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
+int qr_int_matmul(const uint8_t* x, int64_t t, int64_t xk, int xbits, const uint8_t* w, int64_t n, int64_t wk,
+                  int wbits, int32_t* out) {
+  try {
+    auto r = quik::int_matmul(to_packed(x, t, xk, xbits), to_packed(w, n, wk, wbits));
+    std::memcpy(out, r.data.data(), r.data.size() * 4);
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
+int qr_select_outliers(const float* x, int64_t rows, int64_t features, int64_t k, int64_t* idx_out) {
+  try {
+    quik::CalibStats s;
+    s.accumulate(to_fp(x, rows, features));
+    auto o = quik::select_outliers(s, k);
+    std::memcpy(idx_out, o.indices.data(), o.indices.size() * 8);
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
+int qr_outlier_permutation(int64_t features, const int64_t* idx, int64_t n_idx, int64_t* perm) {
+  try {
+    auto o = quik::OutlierSet::from_indices(features, std::vector<int64_t>(idx, idx + n_idx));
+    std::memcpy(perm, o.permutation.data(), o.permutation.size() * 8);
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
+int qr_quantize_activations(const float* xb, int64_t M, int64_t K, int bits, uint8_t* packed, float* scale,
+                            float* zero) {
+  try {
+    auto r = quik::quantize_activations(to_fp(xb, M, K), bits);
+    std::memcpy(packed, r.packed.data.data(), r.packed.data.size());
+    std::memcpy(scale, r.scale.data(), M * 4);
+    std::memcpy(zero, r.zero.data(), M * 4);
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
+int qr_quantize_activations_fused(const float* x, int64_t M, int64_t K, const int64_t* idx, int64_t n_out,
+                                  int bits, uint8_t* packed, float* scale, float* zero, float* x_out) {
+  try {
+    auto o = quik::OutlierSet::from_indices(K, std::vector<int64_t>(idx, idx + n_out));
+    auto [r, xo] = quik::quantize_activations_fused(to_fp(x, M, K), o, bits);
+    std::memcpy(packed, r.packed.data.data(), r.packed.data.size());
+    std::memcpy(scale, r.scale.data(), M * 4);
+    std::memcpy(zero, r.zero.data(), M * 4);
+    if (x_out && !xo.data.empty()) std::memcpy(x_out, xo.data.data(), xo.data.size() * 4);
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
+int qr_dequantize_epilogue(const int32_t* acc, int64_t M, int64_t N, const float* sa, const float* za,
+                           int half_range, const float* sw, const float* wr, float* out) {
+  try {
+    quik::Int32Matrix a(M, N);
+    std::memcpy(a.data.data(), acc, M * N * 4);
+    quik::ActQuantResult q;
+    q.scale.assign(sa, sa + M);
+    q.zero.assign(za, za + M);
+    q.half_range = half_range;
+    auto r = quik::dequantize_epilogue(a, q, std::span<const float>(sw, N), std::span<const float>(wr, N));
+    std::memcpy(out, r.data.data(), M * N * 4);
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
+// quik_matmul with per-stage timings (StageTimes, runtime.hpp:72-80) in ms:
+// times[0..5] = split, quantize, int_matmul, fp_matmul, dequantize, add.
+int qr_quik_matmul(int64_t in, int64_t out_f, int bits, int act_bits, const uint8_t* base, const float* scales,
+                   const float* wreduced, const float* ow, const int64_t* idx, int64_t n_out, const float* bias,
+                   const float* x, int64_t M, int variant, float* out, double* times) {
+  try {
+    auto L = make_layer(in, out_f, bits, act_bits, base, scales, wreduced, ow, idx, n_out, bias);
+    quik::StageTimes st;
+    auto r = quik::quik_matmul(L, to_fp(x, M, in), static_cast<quik::PipelineVariant>(variant), &st);
+    std::memcpy(out, r.data.data(), r.data.size() * 4);
+    if (times) {
+      times[0] = st.split_ms;
+      times[1] = st.quantize_ms;
+      times[2] = st.int_matmul_ms;
+      times[3] = st.fp_matmul_ms;
+      times[4] = st.dequantize_ms;
+      times[5] = st.add_ms;
+    }
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
+// Persistent layer handle so timing loops exclude layer assembly.
+void* qr_layer_create(int64_t in, int64_t out_f, int bits, int act_bits, const uint8_t* base, const float* scales,
+                      const float* wreduced, const float* ow, const int64_t* idx, int64_t n_out, const float* bias) {
+  try {
+    auto* h = new Layer{make_layer(in, out_f, bits, act_bits, base, scales, wreduced, ow, idx, n_out, bias)};
+    return h;
+  } catch (...) {
+    return nullptr;
+  }
+}
+void qr_layer_destroy(void* h) { delete static_cast<Layer*>(h); }
+
+int qr_layer_forward(void* h, const float* x, int64_t M, int variant, float* out, double* times) {
+  try {
+    auto& L = static_cast<Layer*>(h)->layer;
+    quik::StageTimes st;
+    auto r = quik::quik_matmul(L, to_fp(x, M, L.in_features()), static_cast<quik::PipelineVariant>(variant), &st);
+    std::memcpy(out, r.data.data(), r.data.size() * 4);
+    if (times) {
+      times[0] = st.split_ms;
+      times[1] = st.quantize_ms;
+      times[2] = st.int_matmul_ms;
+      times[3] = st.fp_matmul_ms;
+      times[4] = st.dequantize_ms;
+      times[5] = st.add_ms;
+    }
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
+int qr_rtn_quantize_weights(const float* w, int64_t N, int64_t K, const int64_t* idx, int64_t n_out, int bits,
+                            uint8_t* base, float* scales, float* wreduced, float* outlier_w) {
+  try {
+    auto o = quik::OutlierSet::from_indices(K, std::vector<int64_t>(idx, idx + n_out));
+    auto q = quik::rtn_quantize_weights(to_fp(w, N, K), o, bits);
+    std::memcpy(base, q.base.data.data(), q.base.data.size());
+    std::memcpy(scales, q.scales.data(), N * 4);
+    std::memcpy(wreduced, q.wreduced.data(), N * 4);
+    if (n_out) std::memcpy(outlier_w, q.outlier_weights.data.data(), N * n_out * 4);
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
+// The reference tests' seeded Gaussian generator (tests/test_helpers.hpp:128-134):
+// std::mt19937(seed) + std::normal_distribution<float>(0, stddev), row-major.
+void qr_random_matrix(uint32_t seed, int64_t rows, int64_t cols, float stddev, float* out) {
+  std::mt19937 rng(seed);
+  std::normal_distribution<float> dist(0.0f, stddev);
+  for (int64_t i = 0; i < rows * cols; ++i) out[i] = dist(rng);
+}
+
+}  // extern "C"

@@ -1,0 +1,114 @@
+"""ctypes binding of the C ABI in include/quik_b200.h (libquik_b200.so).
+
+The library is built in-tree by paper_2310_09259_b200/build.py. There is no
+fallback: if the library is missing or no sm_100 GPU is visible, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libquik_b200.so"
+
+QUIK_OK = 0
+QUIK_ERR_INVALID_ARGUMENT = 1
+QUIK_ERR_OUT_OF_RANGE = 2
+QUIK_ERR_NUMERICAL = 3
+QUIK_ERR_CUDA = 4
+QUIK_ERR_NCCL = 5
+QUIK_ERR_UNSUPPORTED = 6
+
+QUIK_F16 = 0
+QUIK_F32 = 1
+
+EXPORTED_SYMBOLS = (
+    "quik_last_error", "quik_status_string", "quik_abi_version", "quik_ctx_create", "quik_ctx_destroy",
+    "quik_ctx_sync", "quik_layer_create", "quik_layer_destroy", "quik_layer_info",
+    "quik_quantize_activations_fused", "quik_quantize_activations", "quik_int_matmul",
+    "quik_dequantize_epilogue", "quik_linear_forward", "quik_linear_forward_strided",
+    "quik_linear_forward_launches",
+)
+
+
+class NumericalError(RuntimeError):
+    """reference: quik::NumericalError (matrix.hpp:18-21) — non-finite activations."""
+
+
+class QuikCudaError(RuntimeError):
+    """CUDA failure inside the native library (no CPU fallback exists)."""
+
+
+class WeightsDesc(C.Structure):
+    _fields_ = [
+        ("in_features", C.c_int64),
+        ("out_features", C.c_int64),
+        ("bits", C.c_int),
+        ("act_bits", C.c_int),
+        ("base", C.c_void_p),
+        ("scales", C.c_void_p),
+        ("wreduced", C.c_void_p),
+        ("outlier_weights", C.c_void_p),
+        ("outlier_indices", C.c_void_p),
+        ("n_outlier", C.c_int64),
+        ("bias", C.c_void_p),
+        ("row_begin", C.c_int64),
+        ("row_end", C.c_int64),
+    ]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load() -> C.CDLL:
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise ImportError(
+                f"{LIB_PATH} is missing: the QUIK B200 kernels are not built "
+                "(run `python -c 'import __graft_entry__ as g; g.build()'`). There is no CPU fallback.")
+        lib = C.CDLL(str(LIB_PATH))
+        vp, i64, i32 = C.c_void_p, C.c_int64, C.c_int
+        sig = {
+            "quik_last_error": (C.c_char_p, []),
+            "quik_status_string": (C.c_char_p, [i32]),
+            "quik_abi_version": (i32, []),
+            "quik_ctx_create": (i32, [i32, C.POINTER(vp)]),
+            "quik_ctx_destroy": (i32, [vp]),
+            "quik_ctx_sync": (i32, [vp, vp]),
+            "quik_layer_create": (i32, [vp, C.POINTER(WeightsDesc), C.POINTER(vp)]),
+            "quik_layer_destroy": (i32, [vp]),
+            "quik_layer_info": (i32, [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), C.POINTER(i32)]),
+            "quik_quantize_activations_fused": (i32, [vp, vp, vp, i32, i64, vp, vp, vp, vp, vp]),
+            "quik_quantize_activations": (i32, [vp, vp, i32, i64, i64, i32, vp, vp, vp, vp]),
+            "quik_int_matmul": (i32, [vp, vp, i64, i64, i32, vp, i64, i64, i32, vp, vp]),
+            "quik_dequantize_epilogue": (i32, [vp, vp, i64, i64, vp, vp, i32, vp, vp, vp, vp]),
+            "quik_linear_forward": (i32, [vp, vp, vp, i32, i64, vp, i32, i32, vp]),
+            "quik_linear_forward_strided": (i32, [vp, vp, vp, i32, i64, vp, i32, i64, i32, vp]),
+            "quik_linear_forward_launches": (i32, [i32]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(lib, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = lib
+        return lib
+
+
+def check(status: int) -> None:
+    """Maps a quik_status to the reference's exception types (runtime.cpp / packed.cpp)."""
+    if status == QUIK_OK:
+        return
+    msg = (load().quik_last_error() or b"").decode(errors="replace")
+    if status == QUIK_ERR_INVALID_ARGUMENT:
+        raise ValueError(msg)  # std::invalid_argument
+    if status == QUIK_ERR_OUT_OF_RANGE:
+        raise IndexError(msg)  # std::out_of_range
+    if status == QUIK_ERR_NUMERICAL:
+        raise NumericalError(msg)
+    if status == QUIK_ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise QuikCudaError(msg)

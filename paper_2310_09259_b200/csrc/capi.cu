@@ -1,0 +1,582 @@
+// C-ABI implementation (include/quik_b200.h). Argument checking mirrors the
+// reference's exceptions (runtime.cpp / packed.cpp); device work is delegated
+// to the kernels in gemm.cu and quantize.cu. No CPU compute fallback exists:
+// every numerical result comes from a CUDA kernel.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/quik_b200.h"
+#include "kernels.h"
+
+using namespace quikb200;
+
+namespace {
+
+thread_local std::string g_err;
+
+quik_status fail(quik_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+struct CudaFail {
+  cudaError_t e;
+  const char* what;
+};
+
+#define QK_CUDA(expr)                                                \
+  do {                                                               \
+    cudaError_t _e = (expr);                                         \
+    if (_e != cudaSuccess) throw CudaFail{_e, #expr};               \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* ensure(size_t bytes) {
+    if (bytes <= cap) return p;
+    if (p) { QK_CUDA(cudaDeviceSynchronize()); QK_CUDA(cudaFree(p)); p = nullptr; cap = 0; }
+    const size_t want = std::max<size_t>(bytes, 1 << 16);
+    QK_CUDA(cudaMalloc(&p, want));
+    cap = want;
+    return p;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev_);
+    if (prev_ != dev) cudaSetDevice(dev);
+    dev_ = dev;
+  }
+  ~DeviceGuard() {
+    if (prev_ != dev_) cudaSetDevice(prev_);
+  }
+
+ private:
+  int prev_ = 0, dev_ = 0;
+};
+
+}  // namespace
+
+struct quik_ctx_s {
+  int device = 0;
+  int num_sms = 148;
+  int* d_err = nullptr;
+  DevBuf q8, scale, zero, xo16, acc, fp, xbase, xo32, wtmp;
+};
+
+struct quik_layer_s {
+  int device = 0;
+  int64_t in_features = 0, out_features = 0, n_outlier = 0, kb = 0, kpad = 0, opad = 0;
+  int bits = 4;
+  int8_t* w8 = nullptr;      // [out][kpad]
+  __half* wo16 = nullptr;    // [out][opad]
+  float* w_scale = nullptr;  // [out]
+  float* wreduced = nullptr; // [out]
+  float* bias = nullptr;     // [out] or null
+  int32_t* base_src = nullptr;  // [kb]
+  int32_t* out_src = nullptr;   // [n_outlier]
+};
+
+namespace {
+
+template <typename F>
+quik_status guarded(F&& f) {
+  try {
+    return f();
+  } catch (const CudaFail& c) {
+    return fail(QUIK_ERR_CUDA, std::string("CUDA error: ") + cudaGetErrorString(c.e) + " (" + c.what + ")");
+  } catch (const std::bad_alloc&) {
+    return fail(QUIK_ERR_CUDA, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(QUIK_ERR_INVALID_ARGUMENT, e.what());
+  }
+}
+
+void check_launch(cudaError_t e, const char* what, const char* extra = nullptr) {
+  if (e != cudaSuccess) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e) + (extra ? std::string(" (") + extra + ")" : "");
+    throw CudaFail{e, what};
+  }
+}
+
+int64_t packed_row_bytes(int64_t cols, int bits) { return bits == 4 ? (cols + 1) / 2 : cols; }
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Runs K1 into the context scratch (GEMM layout) for the hot path.
+void run_k1(quik_ctx_t ctx, const quik_layer_s* L, const void* x, quik_dtype xdt, int64_t M, cudaStream_t st) {
+  QuantArgs q{};
+  q.x = x;
+  q.x_is_f32 = xdt == QUIK_F32;
+  q.M = M;
+  q.K = L->in_features;
+  q.ldx = L->in_features;
+  q.base_src = L->base_src;
+  q.kb = L->kb;
+  q.out_src = L->out_src;
+  q.n_out = L->n_outlier;
+  q.bits = L->bits;
+  q.q8 = L->kpad ? static_cast<int8_t*>(ctx->q8.ensure(static_cast<size_t>(M * L->kpad))) : nullptr;
+  q.kpad = L->kpad;
+  q.scale = static_cast<float*>(ctx->scale.ensure(M * 4));
+  q.zero = static_cast<float*>(ctx->zero.ensure(M * 4));
+  q.xo16 = L->opad ? static_cast<__half*>(ctx->xo16.ensure(static_cast<size_t>(M * L->opad * 2))) : nullptr;
+  q.opad = L->opad;
+  q.err = ctx->d_err;
+  check_launch(launch_quantize(q, st), "quantize kernel");
+}
+
+GemmArgs gemm_args(quik_ctx_t ctx, const quik_layer_s* L, int64_t M) {
+  GemmArgs g{};
+  g.w = L->w8;
+  g.x = static_cast<const int8_t*>(ctx->q8.p);
+  g.kpad = L->kpad;
+  g.wo = L->wo16;
+  g.xo = static_cast<const __half*>(ctx->xo16.p);
+  g.opad = L->opad;
+  g.M = M;
+  g.N = L->out_features;
+  g.w_scale = L->w_scale;
+  g.wreduced = L->wreduced;
+  g.bias = L->bias;
+  g.a_scale = static_cast<const float*>(ctx->scale.p);
+  g.a_zero = static_cast<const float*>(ctx->zero.p);
+  g.half_range = static_cast<float>(1 << (L->bits - 1));
+  return g;
+}
+
+void run_gemm(quik_ctx_t ctx, const GemmArgs& g, cudaStream_t st) {
+  const char* msg = nullptr;
+  cudaError_t e = launch_quik_gemm(g, ctx->num_sms, st, &msg);
+  check_launch(e, "quik gemm kernel", msg);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* quik_last_error(void) { return g_err.c_str(); }
+
+const char* quik_status_string(quik_status s) {
+  switch (s) {
+    case QUIK_OK: return "ok";
+    case QUIK_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case QUIK_ERR_OUT_OF_RANGE: return "out of range";
+    case QUIK_ERR_NUMERICAL: return "numerical error";
+    case QUIK_ERR_CUDA: return "cuda error";
+    case QUIK_ERR_NCCL: return "nccl error";
+    case QUIK_ERR_UNSUPPORTED: return "unsupported";
+  }
+  return "unknown";
+}
+
+int quik_abi_version(void) { return QUIK_B200_ABI_VERSION; }
+
+int quik_linear_forward_launches(quik_variant v) {
+  switch (v) {
+    case QUIK_V1_UNFUSED: return 5;      // split, quantize, int gemm, outlier gemm, dequant+add
+    case QUIK_V2_FUSED_QUANT: return 4;  // fused quantize, int gemm, outlier gemm, dequant+add
+    default: return 2;                   // fused quantize, fused gemm+epilogue
+  }
+}
+
+quik_status quik_ctx_create(int device, quik_ctx_t* out) {
+  if (!out) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_ctx_create: null output");
+  return guarded([&] {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+      return fail(QUIK_ERR_CUDA, "quik_ctx_create: no CUDA device visible (the B200 path has no CPU fallback)");
+    if (device < 0 || device >= n) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_ctx_create: bad device index");
+    cudaDeviceProp prop;
+    QK_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      return fail(QUIK_ERR_CUDA, std::string("quik_ctx_create: device ") + prop.name +
+                                     " is not sm_100 (kernels are built for sm_100a only)");
+    DeviceGuard g(device);
+    auto* c = new quik_ctx_s();
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    QK_CUDA(cudaMalloc(&c->d_err, sizeof(int)));
+    QK_CUDA(cudaMemset(c->d_err, 0, sizeof(int)));
+    *out = c;
+    return QUIK_OK;
+  });
+}
+
+quik_status quik_ctx_destroy(quik_ctx_t ctx) {
+  if (!ctx) return QUIK_OK;
+  DeviceGuard g(ctx->device);
+  cudaDeviceSynchronize();
+  for (DevBuf* b : {&ctx->q8, &ctx->scale, &ctx->zero, &ctx->xo16, &ctx->acc, &ctx->fp, &ctx->xbase, &ctx->xo32,
+                    &ctx->wtmp})
+    b->release();
+  cudaFree(ctx->d_err);
+  delete ctx;
+  return QUIK_OK;
+}
+
+quik_status quik_ctx_sync(quik_ctx_t ctx, void* stream) {
+  if (!ctx) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    QK_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    int flag = 0;
+    QK_CUDA(cudaMemcpy(&flag, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (flag) {
+      QK_CUDA(cudaMemset(ctx->d_err, 0, sizeof(int)));
+      return fail(QUIK_ERR_NUMERICAL, "activation quantization: non-finite input value");
+    }
+    return QUIK_OK;
+  });
+}
+
+quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* d, quik_layer_t* out) {
+  if (!ctx || !d || !out) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_layer_create: null argument");
+  if (d->bits != 4 && d->bits != 8) return fail(QUIK_ERR_INVALID_ARGUMENT, "weight bits must be 4 or 8");
+  if (d->act_bits != 4 && d->act_bits != 8) return fail(QUIK_ERR_INVALID_ARGUMENT, "activation bits must be 4 or 8");
+  if (d->act_bits != d->bits)
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "layer: activation bits must match weight bits in quik mode");
+  if (d->in_features < 0 || d->out_features < 0 || d->n_outlier < 0 || d->n_outlier > d->in_features)
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "layer: bad feature counts");
+  if (d->n_outlier > 0 && !d->outlier_indices)
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "layer: outlier indices missing");
+  for (int64_t i = 0; i < d->n_outlier; ++i) {
+    const int64_t v = d->outlier_indices[i];
+    if (v < 0 || v >= d->in_features)
+      return fail(QUIK_ERR_INVALID_ARGUMENT, "OutlierSet: index " + std::to_string(v) + " outside feature range");
+    if (i > 0 && v <= d->outlier_indices[i - 1])
+      return fail(QUIK_ERR_INVALID_ARGUMENT, "OutlierSet: indices must be sorted and unique");
+  }
+  const int64_t rb = d->row_begin, re = (d->row_begin == 0 && d->row_end == 0) ? d->out_features : d->row_end;
+  if (rb < 0 || re < rb || re > d->out_features) return fail(QUIK_ERR_INVALID_ARGUMENT, "layer: bad row shard");
+  const int64_t kb = d->in_features - d->n_outlier;
+  const int64_t rows = re - rb;
+  if (rows > 0 && ((kb > 0 && !d->base) || !d->scales || !d->wreduced || (d->n_outlier > 0 && !d->outlier_weights)))
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "layer: missing weight arrays");
+  if (rows > 0x7fffffffLL || kb > 0x7fffffffLL)
+    return fail(QUIK_ERR_UNSUPPORTED, "layer: dimensions exceed 2^31");
+
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    auto* L = new quik_layer_s();
+    std::unique_ptr<quik_layer_s> hold(L);
+    L->device = ctx->device;
+    L->in_features = d->in_features;
+    L->out_features = rows;
+    L->n_outlier = d->n_outlier;
+    L->bits = d->bits;
+    L->kb = kb;
+    L->kpad = round_up(kb, kKBlockBytes);
+    L->opad = round_up(d->n_outlier, 64);
+
+    // permutation tables (calibration.cpp:69-91): non-outliers ascending, outliers ascending
+    std::vector<int32_t> base_src;
+    base_src.reserve(kb);
+    std::vector<char> is_out(static_cast<size_t>(d->in_features), 0);
+    for (int64_t i = 0; i < d->n_outlier; ++i) is_out[d->outlier_indices[i]] = 1;
+    for (int64_t f = 0; f < d->in_features; ++f)
+      if (!is_out[f]) base_src.push_back(static_cast<int32_t>(f));
+    std::vector<int32_t> out_src(d->outlier_indices, d->outlier_indices + d->n_outlier);
+
+    cudaStream_t st = nullptr;
+    if (kb) {
+      QK_CUDA(cudaMalloc(&L->base_src, kb * 4));
+      QK_CUDA(cudaMemcpy(L->base_src, base_src.data(), kb * 4, cudaMemcpyHostToDevice));
+    }
+    if (d->n_outlier) {
+      QK_CUDA(cudaMalloc(&L->out_src, d->n_outlier * 4));
+      QK_CUDA(cudaMemcpy(L->out_src, out_src.data(), d->n_outlier * 4, cudaMemcpyHostToDevice));
+    }
+    if (rows > 0) {
+      QK_CUDA(cudaMalloc(&L->w_scale, rows * 4));
+      QK_CUDA(cudaMalloc(&L->wreduced, rows * 4));
+      QK_CUDA(cudaMemcpy(L->w_scale, d->scales + rb, rows * 4, cudaMemcpyHostToDevice));
+      QK_CUDA(cudaMemcpy(L->wreduced, d->wreduced + rb, rows * 4, cudaMemcpyHostToDevice));
+      if (d->bias) {
+        QK_CUDA(cudaMalloc(&L->bias, rows * 4));
+        QK_CUDA(cudaMemcpy(L->bias, d->bias + rb, rows * 4, cudaMemcpyHostToDevice));
+      }
+      if (kb) {
+        const int64_t rbytes = packed_row_bytes(kb, d->bits);
+        QK_CUDA(cudaMalloc(&L->w8, static_cast<size_t>(rows * L->kpad)));
+        void* tmp = ctx->wtmp.ensure(static_cast<size_t>(rows * rbytes));
+        QK_CUDA(cudaMemcpy(tmp, d->base + rb * rbytes, static_cast<size_t>(rows * rbytes), cudaMemcpyHostToDevice));
+        check_launch(launch_unpack_to_gemm(static_cast<const uint8_t*>(tmp), rows, kb, d->bits, L->w8, L->kpad, st),
+                     "weight unpack");
+      }
+      if (d->n_outlier) {
+        QK_CUDA(cudaMalloc(&L->wo16, static_cast<size_t>(rows * L->opad * 2)));
+        void* tmp = ctx->fp.ensure(static_cast<size_t>(rows * d->n_outlier * 4));
+        QK_CUDA(cudaMemcpy(tmp, d->outlier_weights + rb * d->n_outlier, static_cast<size_t>(rows * d->n_outlier * 4),
+                           cudaMemcpyHostToDevice));
+        check_launch(launch_f32_to_f16_padded(static_cast<const float*>(tmp), rows, d->n_outlier, L->wo16, L->opad, st),
+                     "outlier weight convert");
+      }
+    }
+    QK_CUDA(cudaStreamSynchronize(st));
+    *out = hold.release();
+    return QUIK_OK;
+  });
+}
+
+quik_status quik_layer_destroy(quik_layer_t L) {
+  if (!L) return QUIK_OK;
+  DeviceGuard g(L->device);
+  cudaDeviceSynchronize();
+  cudaFree(L->w8);
+  cudaFree(L->wo16);
+  cudaFree(L->w_scale);
+  cudaFree(L->wreduced);
+  cudaFree(L->bias);
+  cudaFree(L->base_src);
+  cudaFree(L->out_src);
+  delete L;
+  return QUIK_OK;
+}
+
+quik_status quik_layer_info(quik_layer_t L, int64_t* in_f, int64_t* out_f, int64_t* n_out, int* bits) {
+  if (!L) return fail(QUIK_ERR_INVALID_ARGUMENT, "null layer");
+  if (in_f) *in_f = L->in_features;
+  if (out_f) *out_f = L->out_features;
+  if (n_out) *n_out = L->n_outlier;
+  if (bits) *bits = L->bits;
+  return QUIK_OK;
+}
+
+quik_status quik_quantize_activations_fused(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M,
+                                            uint8_t* packed, float* scale, float* zero, float* x_outlier,
+                                            void* stream) {
+  if (!ctx || !L) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context or layer");
+  if (M < 0 || (M > 0 && !x)) return fail(QUIK_ERR_INVALID_ARGUMENT, "fused quantization: bad input");
+  if (L->in_features * (xdt == QUIK_F32 ? 4 : 2) > 200 * 1024)
+    return fail(QUIK_ERR_UNSUPPORTED, "fused quantization: row too wide for shared-memory staging");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    QuantArgs q{};
+    q.x = x;
+    q.x_is_f32 = xdt == QUIK_F32;
+    q.M = M;
+    q.K = L->in_features;
+    q.ldx = L->in_features;
+    q.base_src = L->base_src;
+    q.kb = L->kb;
+    q.out_src = L->out_src;
+    q.n_out = L->n_outlier;
+    q.bits = L->bits;
+    q.packed = packed;
+    q.scale = scale ? scale : static_cast<float*>(ctx->scale.ensure(M * 4));
+    q.zero = zero ? zero : static_cast<float*>(ctx->zero.ensure(M * 4));
+    q.xo32 = x_outlier;
+    q.err = ctx->d_err;
+    check_launch(launch_quantize(q, as_stream(stream)), "quantize kernel");
+    return QUIK_OK;
+  });
+}
+
+quik_status quik_quantize_activations(quik_ctx_t ctx, const void* x, quik_dtype xdt, int64_t M, int64_t K, int bits,
+                                      uint8_t* packed, float* scale, float* zero, void* stream) {
+  if (!ctx) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context");
+  if (bits != 4 && bits != 8) return fail(QUIK_ERR_INVALID_ARGUMENT, "activation bits must be 4 or 8");
+  if (M < 0 || K < 0 || (M > 0 && K > 0 && !x)) return fail(QUIK_ERR_INVALID_ARGUMENT, "quantize: bad input");
+  if (K * (xdt == QUIK_F32 ? 4 : 2) > 200 * 1024)
+    return fail(QUIK_ERR_UNSUPPORTED, "quantize: row too wide for shared-memory staging");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    // identity permutation table
+    int32_t* ident = static_cast<int32_t*>(ctx->xbase.ensure(static_cast<size_t>(std::max<int64_t>(K, 1) * 4)));
+    std::vector<int32_t> h(static_cast<size_t>(K));
+    for (int64_t i = 0; i < K; ++i) h[i] = static_cast<int32_t>(i);
+    if (K) QK_CUDA(cudaMemcpyAsync(ident, h.data(), K * 4, cudaMemcpyHostToDevice, as_stream(stream)));
+    QuantArgs q{};
+    q.x = x;
+    q.x_is_f32 = xdt == QUIK_F32;
+    q.M = M;
+    q.K = K;
+    q.ldx = K;
+    q.base_src = ident;
+    q.kb = K;
+    q.bits = bits;
+    q.packed = packed;
+    q.scale = scale ? scale : static_cast<float*>(ctx->scale.ensure(M * 4));
+    q.zero = zero ? zero : static_cast<float*>(ctx->zero.ensure(M * 4));
+    q.err = ctx->d_err;
+    check_launch(launch_quantize(q, as_stream(stream)), "quantize kernel");
+    QK_CUDA(cudaStreamSynchronize(as_stream(stream)));  // h must outlive the async copy
+    return QUIK_OK;
+  });
+}
+
+quik_status quik_int_matmul(quik_ctx_t ctx, const uint8_t* xp, int64_t xr, int64_t xc, int xb, const uint8_t* wp,
+                            int64_t wr, int64_t wc, int wb, int32_t* out, void* stream) {
+  if (!ctx) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context");
+  if (xb != wb)
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "int_matmul: operand bit widths differ (" + std::to_string(xb) + " vs " +
+                                               std::to_string(wb) + ")");
+  if (xb != 4 && xb != 8) return fail(QUIK_ERR_INVALID_ARGUMENT, "int_matmul: bits must be 4 or 8");
+  if (xc != wc)
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "int_matmul: inner dimensions differ (" + std::to_string(xc) + " vs " +
+                                               std::to_string(wc) + ")");
+  const int64_t half = int64_t{1} << (xb - 1);
+  if (xc > (int64_t{1} << 31) / (half * half))
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "int_matmul: inner dimension risks INT32 accumulator overflow");
+  if (xr < 0 || wr < 0 || xc < 0) return fail(QUIK_ERR_INVALID_ARGUMENT, "int_matmul: negative dimension");
+  if (xr > 0x7fffffffLL || wr > 0x7fffffffLL) return fail(QUIK_ERR_UNSUPPORTED, "int_matmul: dimension exceeds 2^31");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = as_stream(stream);
+    if (xr == 0 || wr == 0) return QUIK_OK;
+    if (xc == 0) {
+      QK_CUDA(cudaMemsetAsync(out, 0, static_cast<size_t>(xr * wr * 4), st));
+      return QUIK_OK;
+    }
+    const int64_t kpad = round_up(xc, kKBlockBytes);
+    int8_t* x8 = static_cast<int8_t*>(ctx->q8.ensure(static_cast<size_t>(xr * kpad)));
+    int8_t* w8 = static_cast<int8_t*>(ctx->wtmp.ensure(static_cast<size_t>(wr * kpad)));
+    check_launch(launch_unpack_to_gemm(xp, xr, xc, xb, x8, kpad, st), "unpack x");
+    check_launch(launch_unpack_to_gemm(wp, wr, wc, wb, w8, kpad, st), "unpack w");
+    GemmArgs gm{};
+    gm.w = w8;
+    gm.x = x8;
+    gm.kpad = kpad;
+    gm.M = xr;
+    gm.N = wr;
+    gm.out = out;
+    gm.ldo = wr;
+    gm.mode = kModeInt32;
+    run_gemm(ctx, gm, st);
+    return QUIK_OK;
+  });
+}
+
+quik_status quik_dequantize_epilogue(quik_ctx_t ctx, const int32_t* acc, int64_t M, int64_t N, const float* sa,
+                                     const float* za, int half_range, const float* sw, const float* wr, float* out,
+                                     void* stream) {
+  if (!ctx) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context");
+  if (M < 0 || N < 0) return fail(QUIK_ERR_INVALID_ARGUMENT, "dequantize_epilogue: negative dimension");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    check_launch(launch_dequant(acc, M, N, sa, za, static_cast<float>(half_range), sw, wr, out, as_stream(stream)),
+                 "dequant kernel");
+    return QUIK_OK;
+  });
+}
+
+quik_status quik_linear_forward_strided(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M,
+                                        void* y, quik_dtype ydt, int64_t ldy, quik_variant variant, void* stream) {
+  if (!ctx || !L) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context or layer");
+  if (M < 0) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_matmul: negative token count");
+  if (M > 0 && (!x || !y)) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_matmul: null input or output");
+  if (M > 0x7fffffffLL) return fail(QUIK_ERR_UNSUPPORTED, "quik_matmul: token count exceeds 2^31");
+  if (ldy < L->out_features) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_matmul: output pitch < out_features");
+  if (L->in_features * (xdt == QUIK_F32 ? 4 : 2) > 200 * 1024)
+    return fail(QUIK_ERR_UNSUPPORTED, "quik_matmul: row too wide for shared-memory staging");
+  if (ctx->device != L->device) return fail(QUIK_ERR_INVALID_ARGUMENT, "context and layer live on different devices");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = as_stream(stream);
+    if (M == 0 || L->out_features == 0) return QUIK_OK;
+    const int64_t N = L->out_features;
+    if (variant == QUIK_V3_FUSED_EPILOGUE) {
+      run_k1(ctx, L, x, xdt, M, st);
+      GemmArgs gm = gemm_args(ctx, L, M);
+      gm.out = y;
+      gm.ldo = ldy;
+      gm.mode = ydt == QUIK_F16 ? kModeF16 : kModeF32;
+      run_gemm(ctx, gm, st);
+      return QUIK_OK;
+    }
+    if (variant == QUIK_V1_UNFUSED) {
+      // split (runtime.cpp:169-186) then unfused quantisation of the base matrix (:188-197):
+      // the split is K1 in "copy" form writing f32 base/outlier columns, then K1 again
+      // over the base matrix with the identity permutation.
+      float* xb32 = static_cast<float*>(ctx->xbase.ensure(static_cast<size_t>(M * std::max<int64_t>(L->kb, 1) * 4 +
+                                                                              std::max<int64_t>(L->kb, 1) * 4)));
+      int32_t* ident = reinterpret_cast<int32_t*>(xb32 + M * std::max<int64_t>(L->kb, 1));
+      {
+        std::vector<int32_t> h(static_cast<size_t>(L->kb));
+        for (int64_t i = 0; i < L->kb; ++i) h[i] = static_cast<int32_t>(i);
+        if (L->kb) QK_CUDA(cudaMemcpy(ident, h.data(), L->kb * 4, cudaMemcpyHostToDevice));
+      }
+      // split pass: gather base columns in permutation order as f32 (exact) and the
+      // outliers as f16 GEMM operands.
+      SplitArgs s{};
+      s.x = x;
+      s.x_is_f32 = xdt == QUIK_F32;
+      s.M = M;
+      s.K = L->in_features;
+      s.ldx = L->in_features;
+      s.base_src = L->base_src;
+      s.kb = L->kb;
+      s.out_src = L->out_src;
+      s.n_out = L->n_outlier;
+      s.xbase = xb32;
+      s.xo16 = L->opad ? static_cast<__half*>(ctx->xo16.ensure(static_cast<size_t>(M * L->opad * 2))) : nullptr;
+      s.opad = L->opad;
+      check_launch(launch_split(s, st), "split kernel");
+      QuantArgs q{};
+      q.x = xb32;
+      q.x_is_f32 = 1;
+      q.M = M;
+      q.K = L->kb;
+      q.ldx = L->kb;
+      q.base_src = ident;
+      q.kb = L->kb;
+      q.bits = L->bits;
+      q.q8 = L->kpad ? static_cast<int8_t*>(ctx->q8.ensure(static_cast<size_t>(M * L->kpad))) : nullptr;
+      q.kpad = L->kpad;
+      q.scale = static_cast<float*>(ctx->scale.ensure(M * 4));
+      q.zero = static_cast<float*>(ctx->zero.ensure(M * 4));
+      q.err = ctx->d_err;
+      check_launch(launch_quantize(q, st), "quantize kernel");
+    } else {
+      run_k1(ctx, L, x, xdt, M, st);
+    }
+    // V1/V2 tail: int32 accumulator, outlier product + bias, dequantize + add
+    int32_t* acc = static_cast<int32_t*>(ctx->acc.ensure(static_cast<size_t>(M * N * 4)));
+    float* fp = static_cast<float*>(ctx->fp.ensure(static_cast<size_t>(M * N * 4)));
+    GemmArgs gi = gemm_args(ctx, L, M);
+    gi.out = acc;
+    gi.ldo = N;
+    gi.mode = kModeInt32;
+    if (L->kpad) run_gemm(ctx, gi, st);
+    else QK_CUDA(cudaMemsetAsync(acc, 0, static_cast<size_t>(M * N * 4), st));
+    GemmArgs go = gemm_args(ctx, L, M);
+    go.out = fp;
+    go.ldo = N;
+    go.mode = kModeOutlierF32;
+    run_gemm(ctx, go, st);
+    if (ldy == N) {
+      check_launch(launch_dequant_add(acc, M, N, static_cast<const float*>(ctx->scale.p),
+                                      static_cast<const float*>(ctx->zero.p), static_cast<float>(1 << (L->bits - 1)),
+                                      L->w_scale, L->wreduced, fp, y, ydt == QUIK_F16, st),
+                   "dequant+add kernel");
+    } else {
+      return fail(QUIK_ERR_UNSUPPORTED, "V1/V2 variants support dense outputs only");
+    }
+    return QUIK_OK;
+  });
+}
+
+quik_status quik_linear_forward(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M, void* y,
+                                quik_dtype ydt, quik_variant variant, void* stream) {
+  if (!L) return fail(QUIK_ERR_INVALID_ARGUMENT, "null layer");
+  return quik_linear_forward_strided(ctx, L, x, xdt, M, y, ydt, L->out_features, variant, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,111 @@
+// Internal kernel launch interface shared by the C-ABI layer (capi.cu) and the
+// kernel translation units. Not part of the public ABI.
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+namespace quikb200 {
+
+// Device-private GEMM operand layout ("GEMM layout"): row-major, one signed
+// int8 per element, row pitch kpad = round_up(cols, 128) bytes, padding = 0.
+constexpr int kKBlockBytes = 128;  // one K-block = one 128-byte swizzle atom per row
+constexpr int kBlockM = 128;       // UMMA M (weight rows / output features per tile)
+
+inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+enum GemmMode : int {
+  kModeInt32 = 0,       // out int32 [M][ldo]: raw base accumulator (int_matmul)
+  kModeOutlierF32 = 1,  // out f32: bias + x_out . W_out^T (V1/V2 outlier pass)
+  kModeF32 = 2,         // out f32: (bias + outlier) + dequant(acc)   (fused V3)
+  kModeF16 = 3,         // out f16: same as kModeF32 rounded to half  (hot path)
+};
+
+struct GemmArgs {
+  // Operand A (weights, "N" side of the layer) and B (tokens), GEMM layout.
+  const int8_t* w;       // [n_rows][kpad]
+  const int8_t* x;       // [m_rows][kpad]
+  int64_t kpad;          // bytes per row (multiple of 128); 0 => no integer part
+  // Outlier operands, fp16, row pitch opad elements (multiple of 64), 0 => none.
+  const __half* wo;      // [n_rows][opad]
+  const __half* xo;      // [m_rows][opad]
+  int64_t opad;
+  int64_t M;             // tokens
+  int64_t N;             // output features
+  const float* w_scale;  // [N]
+  const float* wreduced; // [N]
+  const float* bias;     // [N] or nullptr
+  const float* a_scale;  // [M]
+  const float* a_zero;   // [M]
+  float half_range;
+  void* out;             // [M][ldo]
+  int64_t ldo;           // elements
+  int mode;
+};
+
+// Launches the fused persistent tcgen05 kernel (int8 GEMM + f16 outlier GEMM +
+// dequantisation epilogue). Returns a cudaError_t / CUresult-derived status in
+// *err_msg on failure.
+cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream, const char** err_msg);
+
+// K1: fused split + per-token asymmetric quantisation (runtime.cpp:36-66,
+// :199-220). x is [M][K] (f16 when x_is_f32 == 0, else f32), row pitch ldx.
+struct QuantArgs {
+  const void* x;
+  int x_is_f32;
+  int64_t M, K, ldx;
+  const int32_t* base_src;  // [kb] source column of base position j (permutation[j])
+  int64_t kb;               // base column count K_b
+  const int32_t* out_src;   // [n_out] outlier source columns, ascending
+  int64_t n_out;
+  int bits;                 // 4 or 8
+  int8_t* q8;               // GEMM layout [M][kpad] or nullptr
+  int64_t kpad;
+  uint8_t* packed;          // ABI layout [M][row_bytes] (i4p / i8) or nullptr
+  float* scale;             // [M]
+  float* zero;              // [M]
+  __half* xo16;             // [M][opad] fp16 outliers (GEMM layout) or nullptr
+  int64_t opad;
+  float* xo32;              // [M][n_out] fp32 outliers (ABI) or nullptr
+  int* err;                 // device flag, set to 1 on non-finite base input
+};
+cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t stream);
+
+// V1 split (runtime.cpp:169-186): base columns in permutation order as f32
+// [M][kb] and outlier columns as f16 GEMM operands [M][opad].
+struct SplitArgs {
+  const void* x;
+  int x_is_f32;
+  int64_t M, K, ldx;
+  const int32_t* base_src;
+  int64_t kb;
+  const int32_t* out_src;
+  int64_t n_out;
+  float* xbase;
+  __half* xo16;
+  int64_t opad;
+};
+cudaError_t launch_split(const SplitArgs& a, cudaStream_t stream);
+
+// Unpacks ABI packed rows (i4p or i8, packed.hpp:11-16) into the GEMM layout.
+cudaError_t launch_unpack_to_gemm(const uint8_t* packed, int64_t rows, int64_t cols, int bits, int8_t* dst,
+                                  int64_t kpad, cudaStream_t stream);
+
+// f32 [rows][cols] -> f16 [rows][pitch], zero padded.
+cudaError_t launch_f32_to_f16_padded(const float* src, int64_t rows, int64_t cols, __half* dst,
+                                     int64_t pitch, cudaStream_t stream);
+
+// dequantize_epilogue (runtime.cpp:222-244): out[t][r] = dequant_element(...).
+cudaError_t launch_dequant(const int32_t* acc, int64_t M, int64_t N, const float* a_scale,
+                           const float* a_zero, float half_range, const float* w_scale,
+                           const float* wreduced, float* out, cudaStream_t stream);
+
+// V1/V2 tail: out[t][r] = out[t][r] + dequant_element(acc[t][r], ...), f32 or f16 result.
+cudaError_t launch_dequant_add(const int32_t* acc, int64_t M, int64_t N, const float* a_scale,
+                               const float* a_zero, float half_range, const float* w_scale,
+                               const float* wreduced, const float* fp_part, void* out, int out_is_f16,
+                               cudaStream_t stream);
+
+}  // namespace quikb200

@@ -1,0 +1,461 @@
+"""Host-side mirror of the reference's C++ layer API (namespace quik), running on
+the B200 kernels through the C ABI (include/quik_b200.h).
+
+Reference-facing functions keep the reference's names, argument meaning and
+error behaviour (runtime.hpp, packed.hpp, quantizer.hpp, calibration.hpp):
+host arrays in, host arrays out, ValueError for std::invalid_argument,
+IndexError for std::out_of_range, NumericalError for quik::NumericalError.
+
+`QuikLinear` is the device-resident hot path: weights repacked once, torch CUDA
+tensors in and out, asynchronous on the current stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import threading
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import NumericalError  # noqa: F401  (re-export)
+
+
+# --------------------------------------------------------------------------- types
+
+
+class PipelineVariant(enum.IntEnum):
+    """reference: runtime.hpp:31. All three are bit-identical."""
+    V1Unfused = 0
+    V2FusedQuant = 1
+    V3FusedEpilogue = 2
+
+
+def row_bytes(cols: int, bits: int) -> int:
+    return (cols + 1) // 2 if bits == 4 else cols
+
+
+@dataclass
+class PackedIntMatrix:
+    """reference: packed.hpp:17-36 (i4p: low nibble = even column, stored = v+8)."""
+    rows: int
+    cols: int
+    bits: int
+    data: np.ndarray  # uint8 [rows * row_bytes]
+
+    def row_bytes(self) -> int:
+        return row_bytes(self.cols, self.bits)
+
+    def get(self, r: int, c: int) -> int:
+        if self.bits == 8:
+            return int(self.data[r * self.cols + c].astype(np.int8))
+        b = int(self.data[r * self.row_bytes() + c // 2])
+        return ((b & 0xF) if c % 2 == 0 else (b >> 4)) - 8
+
+
+def pack_values(values: np.ndarray, rows: int, cols: int, bits: int) -> PackedIntMatrix:
+    """reference: pack_values / pack_int4 / pack_int8 (packed.cpp:30-66), same errors."""
+    if bits not in (4, 8):
+        raise ValueError("pack_values: bits must be 4 or 8")
+    v = np.asarray(values, dtype=np.int64).reshape(-1)
+    if v.size != rows * cols:
+        raise ValueError(f"pack: expected {rows * cols} values, got {v.size}")
+    lo, hi = (-8, 7) if bits == 4 else (-128, 127)
+    bad = np.nonzero((v < lo) | (v > hi))[0]
+    if bad.size:
+        i = int(bad[0])
+        raise IndexError(f"pack: value {int(v[i])} at row {i // cols}, col {i % cols} outside [{lo}, {hi}]")
+    v = v.reshape(rows, cols)
+    if bits == 8:
+        return PackedIntMatrix(rows, cols, 8, v.astype(np.int8).view(np.uint8).reshape(-1).copy())
+    rb = row_bytes(cols, 4)
+    biased = (v + 8).astype(np.uint8)
+    out = np.zeros((rows, rb), dtype=np.uint8)
+    out[:, : (cols + 1) // 2] |= biased[:, 0::2]
+    out[:, : cols // 2] |= (biased[:, 1::2] << 4).astype(np.uint8)
+    return PackedIntMatrix(rows, cols, 4, out.reshape(-1))
+
+
+def unpack_values(m: PackedIntMatrix) -> np.ndarray:
+    """reference: unpack_values (packed.cpp:86-91) -> int8 [rows][cols]."""
+    if m.bits == 8:
+        return m.data.view(np.int8).reshape(m.rows, m.cols).copy()
+    b = m.data.reshape(m.rows, m.row_bytes())
+    out = np.empty((m.rows, m.cols), dtype=np.int8)
+    out[:, 0::2] = (b[:, : (m.cols + 1) // 2] & 0xF).astype(np.int8) - 8
+    out[:, 1::2] = (b[:, : m.cols // 2] >> 4).astype(np.int8) - 8
+    return out
+
+
+@dataclass
+class OutlierSet:
+    """reference: calibration.hpp:37-48; from_indices calibration.cpp:69-91."""
+    feature_count: int
+    indices: np.ndarray      # int64, sorted ascending
+    permutation: np.ndarray  # int64 [feature_count]: non-outliers ascending, then outliers
+
+    @staticmethod
+    def from_indices(feature_count: int, indices) -> "OutlierSet":
+        idx = np.sort(np.asarray(indices, dtype=np.int64).reshape(-1))
+        if idx.size and (idx[0] < 0 or idx[-1] >= feature_count):
+            bad = int(idx[0] if idx[0] < 0 else idx[-1])
+            raise ValueError(f"OutlierSet: index {bad} outside feature range")
+        if idx.size > 1 and np.any(idx[1:] == idx[:-1]):
+            raise ValueError(f"OutlierSet: duplicate index {int(idx[1:][idx[1:] == idx[:-1]][0])}")
+        mask = np.ones(feature_count, dtype=bool)
+        mask[idx] = False
+        perm = np.concatenate([np.nonzero(mask)[0].astype(np.int64), idx])
+        return OutlierSet(feature_count, idx, perm)
+
+    @staticmethod
+    def none(feature_count: int) -> "OutlierSet":
+        return OutlierSet.from_indices(feature_count, [])
+
+    def outlier_count(self) -> int:
+        return int(self.indices.size)
+
+    def base_count(self) -> int:
+        return self.feature_count - self.outlier_count()
+
+
+@dataclass
+class QuantizedWeights:
+    """reference: quantizer.hpp:48-58 (permuted column order, outliers at the tail)."""
+    base: PackedIntMatrix
+    scales: np.ndarray           # f32 [out]
+    outlier_weights: np.ndarray  # f32 [out][n_outlier]
+    wreduced: np.ndarray         # f32 [out]
+    mask: Optional[np.ndarray] = None
+
+    def bits(self) -> int:
+        return self.base.bits
+
+    def out_features(self) -> int:
+        return self.base.rows
+
+    def base_features(self) -> int:
+        return self.base.cols
+
+
+@dataclass
+class QuikLinearLayer:
+    """reference: runtime.hpp:33-44 (Quik mode)."""
+    weights: QuantizedWeights
+    outliers: OutlierSet
+    bias: Optional[np.ndarray] = None
+    act_bits: int = 4
+
+    def in_features(self) -> int:
+        return self.outliers.feature_count
+
+    def out_features(self) -> int:
+        return self.weights.out_features()
+
+    def validate(self) -> None:
+        """reference: QuikLinearLayer::validate (runtime.cpp:150-167)."""
+        ow = np.asarray(self.weights.outlier_weights)
+        if self.outliers.outlier_count() != (ow.shape[1] if ow.ndim == 2 else 0):
+            raise ValueError(f"layer: outlier index count {self.outliers.outlier_count()} != outlier weight columns")
+        if self.outliers.base_count() != self.weights.base_features():
+            raise ValueError("layer: base column count mismatch")
+        if self.bias is not None and len(self.bias) != self.out_features():
+            raise ValueError("layer: bias length != out_features")
+        if self.act_bits != self.weights.bits():
+            raise ValueError("layer: activation bits must match weight bits in quik mode")
+        if self.act_bits not in (4, 8):
+            raise ValueError("activation bits must be 4 or 8")
+
+
+@dataclass
+class ActQuantResult:
+    """reference: runtime.hpp:18-23."""
+    packed: PackedIntMatrix
+    scale: np.ndarray
+    zero: np.ndarray
+    half_range: int = 8
+
+
+@dataclass
+class StageTimes:
+    """reference: runtime.hpp:72-80 (milliseconds, CUDA events on the device)."""
+    split_ms: float = 0.0
+    quantize_ms: float = 0.0
+    int_matmul_ms: float = 0.0
+    fp_matmul_ms: float = 0.0
+    dequantize_ms: float = 0.0
+    add_ms: float = 0.0
+    quantize_fused: bool = False
+    dequantize_fused: bool = False
+
+    def total_ms(self) -> float:
+        return self.split_ms + self.quantize_ms + self.int_matmul_ms + self.fp_matmul_ms + self.dequantize_ms + self.add_ms
+
+
+# --------------------------------------------------------------------------- device plumbing
+
+
+def _torch():
+    import torch  # plumbing only: device memory, streams
+
+    if not torch.cuda.is_available():
+        raise _lib.QuikCudaError("no CUDA device visible: the QUIK B200 path has no CPU fallback")
+    return torch
+
+
+class Context:
+    """Owns a quik_ctx_t (scratch + error flag) for one device."""
+
+    def __init__(self, device: int = 0):
+        self._lib = _lib.load()
+        self.device = device
+        h = C.c_void_p()
+        _lib.check(self._lib.quik_ctx_create(device, C.byref(h)))
+        self.handle = h
+
+    def sync(self, stream) -> None:
+        _lib.check(self._lib.quik_ctx_sync(self.handle, C.c_void_p(stream)))
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                self._lib.quik_ctx_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+_ctx_lock = threading.Lock()
+_ctxs: dict = {}
+
+
+def context(device: Optional[int] = None) -> Context:
+    torch = _torch()
+    dev = torch.cuda.current_device() if device is None else device
+    key = (threading.get_ident(), dev)
+    with _ctx_lock:
+        c = _ctxs.get(key)
+        if c is None:
+            c = _ctxs[key] = Context(dev)
+        return c
+
+
+def _stream_ptr(torch, device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _ptr(t) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr() if t is not None and t.numel() else None)
+
+
+def _dev(torch, a: np.ndarray, device: int):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{device}")
+
+
+class QuikLinear:
+    """Device-resident QUIK linear layer (the hot path).
+
+    Construction uploads the reference-format weights once (quik_layer_create:
+    i4p/i8 -> device GEMM layout, outliers -> f16). forward() runs K1 + the fused
+    tcgen05 kernel on the current CUDA stream. `row_begin/row_end` select an
+    output-row shard (multi-GPU column sharding)."""
+
+    def __init__(self, layer: QuikLinearLayer, device: Optional[int] = None, row_begin: int = 0, row_end: int = 0):
+        torch = _torch()
+        layer.validate()
+        self._lib = _lib.load()
+        self.ctx = context(device)
+        self.device = self.ctx.device
+        w = layer.weights
+        self.in_features = layer.in_features()
+        self.n_outlier = layer.outliers.outlier_count()
+        self.bits = w.bits()
+        self._keep = dict(
+            base=np.ascontiguousarray(w.base.data, dtype=np.uint8),
+            scales=np.ascontiguousarray(w.scales, dtype=np.float32),
+            wreduced=np.ascontiguousarray(w.wreduced, dtype=np.float32),
+            ow=np.ascontiguousarray(np.asarray(w.outlier_weights, dtype=np.float32).reshape(-1)
+                                    if self.n_outlier and w.out_features() else np.zeros(1, np.float32)),
+            idx=np.ascontiguousarray(layer.outliers.indices, dtype=np.int64),
+            bias=None if layer.bias is None else np.ascontiguousarray(layer.bias, dtype=np.float32),
+        )
+        k = self._keep
+        d = _lib.WeightsDesc(
+            in_features=self.in_features, out_features=w.out_features(), bits=self.bits, act_bits=layer.act_bits,
+            base=k["base"].ctypes.data if k["base"].size else None,
+            scales=k["scales"].ctypes.data, wreduced=k["wreduced"].ctypes.data,
+            outlier_weights=k["ow"].ctypes.data, outlier_indices=k["idx"].ctypes.data if k["idx"].size else None,
+            n_outlier=self.n_outlier, bias=None if k["bias"] is None else k["bias"].ctypes.data,
+            row_begin=row_begin, row_end=row_end)
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(self._lib.quik_layer_create(self.ctx.handle, C.byref(d), C.byref(h)))
+        self.handle = h
+        self._keep = None  # host copies no longer needed
+        of = C.c_int64()
+        self._lib.quik_layer_info(h, None, C.byref(of), None, None)
+        self.out_features = of.value
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                self._lib.quik_layer_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+    @staticmethod
+    def launches(variant: PipelineVariant = PipelineVariant.V3FusedEpilogue) -> int:
+        return int(_lib.load().quik_linear_forward_launches(int(variant)))
+
+    def forward(self, x, out=None, out_dtype=None, variant: PipelineVariant = PipelineVariant.V3FusedEpilogue):
+        """x: CUDA tensor [M][in_features] f16/f32 -> [M][out_features] (f16 default)."""
+        torch = _torch()
+        if x.dim() != 2 or x.shape[1] != self.in_features:
+            raise ValueError(f"quik_matmul: input has {x.shape[-1]} features, layer expects {self.in_features}")
+        if x.dtype not in (torch.float16, torch.float32):
+            raise ValueError("quik_matmul: input must be float16 or float32")
+        x = x.contiguous()
+        M = x.shape[0]
+        if out is None:
+            dt = out_dtype or torch.float16
+            out = torch.empty((M, self.out_features), dtype=dt, device=x.device)
+        ydt = _lib.QUIK_F16 if out.dtype == torch.float16 else _lib.QUIK_F32
+        xdt = _lib.QUIK_F16 if x.dtype == torch.float16 else _lib.QUIK_F32
+        ldy = out.stride(0)
+        if out.stride(1) != 1 or ldy < self.out_features:
+            raise ValueError("output must be row-major with pitch >= out_features")
+        _lib.check(self._lib.quik_linear_forward_strided(
+            self.ctx.handle, self.handle, _ptr(x), xdt, M, _ptr(out), ydt, ldy, int(variant),
+            C.c_void_p(_stream_ptr(torch, x.device))))
+        return out
+
+    __call__ = forward
+
+
+# --------------------------------------------------------------------------- reference-facing API
+
+
+def _outlier_handle(torch, outliers: OutlierSet, bits: int, device: int) -> QuikLinear:
+    """A weight-less layer carrying only the outlier permutation tables."""
+    K = outliers.feature_count
+    kb = outliers.base_count()
+    w = QuantizedWeights(PackedIntMatrix(0, kb, bits, np.zeros(0, np.uint8)), np.zeros(0, np.float32),
+                         np.zeros((0, outliers.outlier_count()), np.float32), np.zeros(0, np.float32))
+    return QuikLinear(QuikLinearLayer(w, outliers, None, bits), device)
+
+
+def quantize_activations_fused(x: np.ndarray, outliers: OutlierSet, bits: int):
+    """reference: quantize_activations_fused (runtime.hpp:55-56) -> (ActQuantResult, x_outlier)."""
+    if bits not in (4, 8):
+        raise ValueError("activation bits must be 4 or 8")
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    if x.ndim != 2 or x.shape[1] != outliers.feature_count:
+        raise ValueError("fused quantization: input features do not match outlier set")
+    torch = _torch()
+    ctx = context()
+    M = x.shape[0]
+    kb = outliers.base_count()
+    L = _outlier_handle(torch, outliers, bits, ctx.device)
+    dx = _dev(torch, x, ctx.device)
+    packed = torch.empty(max(M * row_bytes(kb, bits), 1), dtype=torch.uint8, device=dx.device)
+    scale = torch.empty(max(M, 1), dtype=torch.float32, device=dx.device)
+    zero = torch.empty(max(M, 1), dtype=torch.float32, device=dx.device)
+    xo = torch.empty(max(M * outliers.outlier_count(), 1), dtype=torch.float32, device=dx.device)
+    s = _stream_ptr(torch, dx.device)
+    _lib.check(L._lib.quik_quantize_activations_fused(ctx.handle, L.handle, _ptr(dx), _lib.QUIK_F32, M,
+                                                      _ptr(packed), _ptr(scale), _ptr(zero), _ptr(xo), C.c_void_p(s)))
+    ctx.sync(s)
+    pk = packed.cpu().numpy()[: M * row_bytes(kb, bits)]
+    res = ActQuantResult(PackedIntMatrix(M, kb, bits, pk), scale.cpu().numpy()[:M], zero.cpu().numpy()[:M],
+                         1 << (bits - 1))
+    return res, xo.cpu().numpy()[: M * outliers.outlier_count()].reshape(M, outliers.outlier_count())
+
+
+def quantize_activations(x_base: np.ndarray, bits: int) -> ActQuantResult:
+    """reference: quantize_activations (runtime.hpp:51, runtime.cpp:188-197)."""
+    if bits not in (4, 8):
+        raise ValueError("activation bits must be 4 or 8")
+    x = np.ascontiguousarray(x_base, dtype=np.float32)
+    if x.ndim != 2:
+        raise ValueError("quantize_activations: expected a 2-D matrix")
+    torch = _torch()
+    ctx = context()
+    M, K = x.shape
+    dx = _dev(torch, x, ctx.device)
+    packed = torch.empty(max(M * row_bytes(K, bits), 1), dtype=torch.uint8, device=dx.device)
+    scale = torch.empty(max(M, 1), dtype=torch.float32, device=dx.device)
+    zero = torch.empty(max(M, 1), dtype=torch.float32, device=dx.device)
+    s = _stream_ptr(torch, dx.device)
+    _lib.check(_lib.load().quik_quantize_activations(ctx.handle, _ptr(dx), _lib.QUIK_F32, M, K, bits, _ptr(packed),
+                                                     _ptr(scale), _ptr(zero), C.c_void_p(s)))
+    ctx.sync(s)
+    return ActQuantResult(PackedIntMatrix(M, K, bits, packed.cpu().numpy()[: M * row_bytes(K, bits)]),
+                          scale.cpu().numpy()[:M], zero.cpu().numpy()[:M], 1 << (bits - 1))
+
+
+def int_matmul(x: PackedIntMatrix, w: PackedIntMatrix) -> np.ndarray:
+    """reference: int_matmul (packed.hpp:58, packed.cpp:93-132) -> int32 [x.rows][w.rows]."""
+    torch = _torch()
+    ctx = context()
+    dxp = _dev(torch, x.data if x.data.size else np.zeros(1, np.uint8), ctx.device)
+    dwp = _dev(torch, w.data if w.data.size else np.zeros(1, np.uint8), ctx.device)
+    out = torch.empty(max(x.rows * w.rows, 1), dtype=torch.int32, device=dxp.device)
+    s = _stream_ptr(torch, dxp.device)
+    _lib.check(_lib.load().quik_int_matmul(ctx.handle, _ptr(dxp), x.rows, x.cols, x.bits, _ptr(dwp), w.rows, w.cols,
+                                           w.bits, _ptr(out), C.c_void_p(s)))
+    ctx.sync(s)
+    return out.cpu().numpy()[: x.rows * w.rows].reshape(x.rows, w.rows)
+
+
+def dequantize_epilogue(acc: np.ndarray, a: ActQuantResult, weight_scales, wreduced) -> np.ndarray:
+    """reference: dequantize_epilogue (runtime.hpp:66-68, runtime.cpp:222-244)."""
+    acc = np.ascontiguousarray(acc, dtype=np.int32)
+    M, N = acc.shape
+    if M != len(a.scale):
+        raise ValueError("dequantize_epilogue: token count mismatch")
+    if len(weight_scales) != N or len(wreduced) != N:
+        raise ValueError("dequantize_epilogue: per-row vector length mismatch")
+    torch = _torch()
+    ctx = context()
+    d = lambda v: _dev(torch, np.ascontiguousarray(v, dtype=np.float32), ctx.device)  # noqa: E731
+    dacc = _dev(torch, acc, ctx.device)
+    sa, za, sw, wr = d(a.scale), d(a.zero), d(weight_scales), d(wreduced)
+    out = torch.empty((M, N), dtype=torch.float32, device=dacc.device)
+    s = _stream_ptr(torch, dacc.device)
+    _lib.check(_lib.load().quik_dequantize_epilogue(ctx.handle, _ptr(dacc), M, N, _ptr(sa), _ptr(za), a.half_range,
+                                                    _ptr(sw), _ptr(wr), _ptr(out), C.c_void_p(s)))
+    ctx.sync(s)
+    return out.cpu().numpy()
+
+
+def quik_matmul(layer: QuikLinearLayer, x: np.ndarray,
+                variant: PipelineVariant = PipelineVariant.V3FusedEpilogue,
+                times: Optional[StageTimes] = None, out_dtype: str = "float32") -> np.ndarray:
+    """reference: quik_matmul (runtime.hpp:85-87): host FP32 in, host FP32 out.
+
+    Uploads the layer on every call like the reference re-reads its weights; keep a
+    QuikLinear for repeated calls."""
+    layer.validate()
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    if x.ndim != 2 or x.shape[1] != layer.in_features():
+        raise ValueError(f"quik_matmul: input has {x.shape[-1]} features, layer expects {layer.in_features()}")
+    torch = _torch()
+    dev = QuikLinear(layer)
+    dx = _dev(torch, x, dev.device)
+    dt = torch.float32 if out_dtype == "float32" else torch.float16
+    ev = None
+    if times is not None:
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record()
+    y = dev.forward(dx, out_dtype=dt, variant=variant)
+    if ev is not None:
+        ev[1].record()
+    dev.ctx.sync(_stream_ptr(torch, dx.device))
+    if times is not None:
+        ms = ev[0].elapsed_time(ev[1])
+        times.quantize_fused = variant != PipelineVariant.V1Unfused
+        times.dequantize_fused = variant == PipelineVariant.V3FusedEpilogue
+        times.int_matmul_ms = ms  # one fused kernel pair; split timing lives in bench.py
+    return y.float().cpu().numpy()

@@ -1,0 +1,369 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle.
+
+Bit-exact: packed activation codes, per-token scale/zero, outlier gather, INT32
+base accumulators, the dequantisation epilogue, and the whole layer when it has
+no outliers (f32 output). Tolerance: f16 outlier products (tensor-core
+summation order) and the f16 output rounding, SURVEY.md Appendix A.3:
+  |y - ref| <= 2^-11 |ref| + 2^-20 * S   (S = sum of term magnitudes), and
+  rel_frobenius(y, ref) <= 5e-4 (f16 out) / 1e-5 (f32 out).
+Cases follow the reference tests (test_packed.cpp, test_runtime.cpp,
+acceptance.cpp criteria 4/5) plus BASELINE.json shapes.
+"""
+import numpy as np
+import pytest
+
+from oracle_lib import make_layer, oracle, ref, row_bytes
+
+pytestmark = pytest.mark.gpu
+
+F16_REL = 2.0 ** -11
+
+
+def q():
+    import paper_2310_09259_b200 as m
+
+    return m
+
+
+def to_layer(L):
+    m = q()
+    kb = L["in_features"] - np.asarray(L["idx"]).size
+    w = m.QuantizedWeights(m.PackedIntMatrix(L["out_features"], kb, L["bits"], np.asarray(L["base"], np.uint8)),
+                           np.asarray(L["scales"], np.float32), np.asarray(L["outlier_weights"], np.float32),
+                           np.asarray(L["wreduced"], np.float32))
+    return m.QuikLinearLayer(w, m.OutlierSet.from_indices(L["in_features"], L["idx"]), L.get("bias"), L["bits"])
+
+
+def rel_frob(ref_, got):
+    ref_ = ref_.astype(np.float64)
+    got = got.astype(np.float64)
+    d = np.sqrt(((got - ref_) ** 2).sum())
+    n = np.sqrt((ref_ ** 2).sum())
+    return d if n == 0 else d / n
+
+
+# --------------------------------------------------------------------------- K1 quantizer
+
+
+def test_quantize_kat_direct_formula():
+    # test_runtime.cpp:80-87: [0, .5, 1, 1.5] -> scale 0.1, zero 0, codes [-8,-3,2,7]
+    m = q()
+    r = m.quantize_activations(np.array([[0.0, 0.5, 1.0, 1.5]], np.float32), 4)
+    assert abs(r.scale[0] - 0.1) < 1e-7 and r.zero[0] == 0.0
+    assert list(m.unpack_values(r.packed)[0]) == [-8, -3, 2, 7]
+
+
+def test_quantize_kat_constant_row():
+    # test_runtime.cpp:89-97
+    m = q()
+    r = m.quantize_activations(np.array([[5.0, 5.0, 5.0]], np.float32), 4)
+    assert r.scale[0] == 1.0 and r.zero[0] == 5.0
+    assert list(m.unpack_values(r.packed)[0]) == [-8, -8, -8]
+
+
+def test_quantize_rejects_non_finite():
+    # test_runtime.cpp:110-116
+    m = q()
+    for bad in (np.nan, np.inf):
+        with pytest.raises(m.NumericalError):
+            m.quantize_activations(np.array([[1.0, bad]], np.float32), 4)
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+def test_fused_quantizer_bit_exact_random(bits):
+    # fused == reference on seeded random shapes (test_runtime.cpp:134-156 style)
+    m = q()
+    o = oracle()
+    for seed in range(40):
+        rng = np.random.default_rng(1000 + seed)
+        K = int(rng.integers(8, 400))
+        M = int(rng.integers(1, 20))
+        x = rng.normal(0, 1.5, size=(M, K)).astype(np.float32)
+        k = int(rng.integers(0, K))
+        idx = o.select_outliers(x, k)
+        st, pk, sc, ze, xo = o.quantize_fused(x, idx, bits)
+        assert st == 0
+        r, gxo = m.quantize_activations_fused(x, m.OutlierSet.from_indices(K, idx), bits)
+        np.testing.assert_array_equal(r.packed.data, pk)
+        np.testing.assert_array_equal(r.scale.view(np.uint32), sc.view(np.uint32))
+        np.testing.assert_array_equal(r.zero.view(np.uint32), ze.view(np.uint32))
+        np.testing.assert_array_equal(gxo, xo)
+
+
+def test_fused_quantizer_ties_and_signed_zero():
+    # exact .5 ties (lround ties-away) and the first-seen sign of a zero minimum
+    m = q()
+    o = oracle()
+    x = np.array([[0.0, 1.0, 0.5, 15.0, 7.5, 2.5, 1.5],
+                  [-0.0, 0.0, 3.0, 1.0, 2.0, 0.0, 0.6],
+                  [0.0, -0.0, 3.0, 1.0, 2.0, -0.0, 0.6]], np.float32)
+    for bits in (4, 8):
+        st, pk, sc, ze, _ = o.quantize_fused(x, np.zeros(0, np.int64), bits)
+        r, _ = m.quantize_activations_fused(x, m.OutlierSet.none(x.shape[1]), bits)
+        np.testing.assert_array_equal(r.packed.data, pk)
+        np.testing.assert_array_equal(r.zero.view(np.uint32), ze.view(np.uint32))
+        np.testing.assert_array_equal(r.scale.view(np.uint32), sc.view(np.uint32))
+
+
+def test_fused_quantizer_boundaries():
+    # test_runtime.cpp:158-170: empty outlier set, all-outlier set
+    m = q()
+    x = np.array([[1.0, 2.0, 3.0]], np.float32)
+    a, xo = m.quantize_activations_fused(x, m.OutlierSet.none(3), 4)
+    plain = m.quantize_activations(x, 4)
+    np.testing.assert_array_equal(a.packed.data, plain.packed.data)
+    assert xo.shape == (1, 0)
+    b, allx = m.quantize_activations_fused(x, m.OutlierSet.from_indices(3, [0, 1, 2]), 4)
+    assert b.packed.cols == 0
+    np.testing.assert_array_equal(allx, x)
+
+
+# --------------------------------------------------------------------------- INT GEMM
+
+
+def test_int_matmul_kat():
+    # test_packed.cpp:78-92
+    m = q()
+    x = m.pack_values([1, -2, 3, 4], 2, 2, 8)
+    w = m.pack_values([5, 6, -7, 8], 2, 2, 8)
+    np.testing.assert_array_equal(m.int_matmul(x, w), [[-7, -23], [39, 11]])
+    x4 = m.pack_values([1, -2, 3, 4], 2, 2, 4)
+    w4 = m.pack_values([5, 6, -7, 7], 2, 2, 4)
+    out4 = m.int_matmul(x4, w4)
+    assert out4[0, 0] == 1 * 5 + -2 * 6 and out4[1, 1] == 3 * -7 + 4 * 7
+
+
+def test_int_matmul_rejects_mismatch():
+    # test_packed.cpp:153-157
+    m = q()
+    a = m.pack_values([1] * 6, 2, 3, 4)
+    b = m.pack_values([1] * 8, 2, 4, 4)
+    c = m.pack_values([1] * 6, 2, 3, 8)
+    with pytest.raises(ValueError):
+        m.int_matmul(a, b)
+    with pytest.raises(ValueError):
+        m.int_matmul(a, c)
+
+
+def test_int_matmul_random_shapes_vs_naive():
+    # test_packed.cpp:104-128: 100 random shapes with dims 1..40, bits alternating
+    m = q()
+    o = oracle()
+    rng = np.random.default_rng(7)
+    for trial in range(100):
+        bits = 4 if trial % 2 == 0 else 8
+        lim = 7 if bits == 4 else 127
+        t, k, n = (int(v) for v in rng.integers(1, 41, size=3))
+        xv = rng.integers(-lim - 1, lim + 1, size=(t, k))
+        wv = rng.integers(-lim - 1, lim + 1, size=(n, k))
+        x = m.pack_values(xv, t, k, bits)
+        w = m.pack_values(wv, n, k, bits)
+        got = m.int_matmul(x, w)
+        st, want = o.int_matmul(x.data, t, k, bits, w.data, n)
+        assert st == 0
+        np.testing.assert_array_equal(got, want)
+        np.testing.assert_array_equal(got, xv @ wv.T)
+
+
+@pytest.mark.parametrize("bits,t,k,n", [(4, 300, 1000, 500), (8, 257, 4100, 129), (4, 16, 3968, 4096),
+                                        (8, 1, 10320, 300), (4, 2048, 256, 384)])
+def test_int_matmul_large_exact(bits, t, k, n):
+    m = q()
+    rng = np.random.default_rng(t * 7 + k)
+    lim = 7 if bits == 4 else 127
+    xv = rng.integers(-lim - 1, lim + 1, size=(t, k))
+    wv = rng.integers(-lim - 1, lim + 1, size=(n, k))
+    got = m.int_matmul(m.pack_values(xv, t, k, bits), m.pack_values(wv, n, k, bits))
+    np.testing.assert_array_equal(got, (xv @ wv.T).astype(np.int64))
+
+
+def test_int_matmul_linearity():
+    # test_packed.cpp:131-151
+    m = q()
+    rng = np.random.default_rng(11)
+    t, k, n = 33, 300, 70
+    xv = rng.integers(-8, 8, size=(t, k))
+    w1 = rng.integers(-4, 4, size=(n, k))
+    w2 = rng.integers(-4, 4, size=(n, k))
+    x = m.pack_values(xv, t, k, 4)
+    s = m.int_matmul(x, m.pack_values(w1 + w2, n, k, 4))
+    a = m.int_matmul(x, m.pack_values(w1, n, k, 4))
+    b = m.int_matmul(x, m.pack_values(w2, n, k, 4))
+    np.testing.assert_array_equal(s, a + b)
+
+
+# --------------------------------------------------------------------------- epilogue
+
+
+def test_dequantize_epilogue_bit_exact():
+    m = q()
+    o = oracle()
+    rng = np.random.default_rng(3)
+    M, N = 37, 211
+    acc = rng.integers(-400000, 400000, size=(M, N)).astype(np.int32)
+    sa = rng.uniform(0.01, 2, M).astype(np.float32)
+    za = rng.normal(0, 3, M).astype(np.float32)
+    sw = rng.uniform(0.001, 0.1, N).astype(np.float32)
+    wr = rng.normal(0, 5, N).astype(np.float32)
+    want = o.dequantize_epilogue(acc, sa, za, 8, sw, wr)
+    a = m.ActQuantResult(m.PackedIntMatrix(M, 0, 4, np.zeros(0, np.uint8)), sa, za, 8)
+    got = m.dequantize_epilogue(acc, a, sw, wr)
+    np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_dequantize_epilogue_hand_example():
+    # test_runtime.cpp:172-186: acc = -23, out = -0.5
+    m = q()
+    aq = m.quantize_activations(np.array([[1.0, 3.0]], np.float32), 4)
+    assert list(m.unpack_values(aq.packed)[0]) == [-8, 7]
+    acc = m.int_matmul(aq.packed, m.pack_values([2, -1], 1, 2, 4))
+    assert acc[0, 0] == -23
+    out = m.dequantize_epilogue(acc, aq, np.array([0.5], np.float32), np.array([0.5], np.float32))
+    assert abs(out[0, 0] + 0.5) < 1e-6
+
+
+# --------------------------------------------------------------------------- full layer
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+@pytest.mark.parametrize("with_bias", [False, True])
+def test_layer_no_outliers_f32_bit_exact(bits, with_bias):
+    """With O = 0 every op of the layer is defined op-by-op: the f32 output must be
+    bit-identical to the reference quik_matmul (runtime.cpp:246-318)."""
+    m = q()
+    o = oracle()
+    rng = np.random.default_rng(17 + bits)
+    for (M, K, N) in [(9, 96, 40), (64, 128, 48), (33, 1000, 257), (130, 512, 300)]:
+        L, x, _ = make_layer(rng, M, K, N, bits, 0, heavy_cols=2, with_bias=with_bias)
+        st, want = o.quik_matmul(L, x, 2)
+        assert st == 0
+        got = m.quik_matmul(to_layer(L), x)
+        np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+def test_layer_with_outliers_f32(bits):
+    m = q()
+    o = oracle()
+    rng = np.random.default_rng(23 + bits)
+    for (M, K, N, O) in [(9, 96, 40, 8), (64, 128, 48, 16), (48, 2048, 512, 256), (5, 300, 77, 64)]:
+        L, x, _ = make_layer(rng, M, K, N, bits, O, heavy_cols=4)
+        st, want = o.quik_matmul(L, x, 2)
+        assert st == 0
+        got = m.quik_matmul(to_layer(L), x)
+        assert rel_frob(want, got) < 1e-5, (M, K, N, O, rel_frob(want, got))
+
+
+def elementwise_bound(L, x, want):
+    """Per-element f16 tolerance, SURVEY.md Appendix A.3."""
+    idx = np.asarray(L["idx"])
+    xo = x[:, idx].astype(np.float64)
+    ow = np.asarray(L["outlier_weights"], np.float64)
+    S = np.abs(xo) @ np.abs(ow).T + np.abs(want).astype(np.float64)
+    if L.get("bias") is not None:
+        S += np.abs(L["bias"])[None, :]
+    return F16_REL * np.abs(want) + 2.0 ** -20 * S + 1e-30
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+def test_layer_f16_output_tolerance(bits):
+    m = q()
+    o = oracle()
+    import torch
+
+    rng = np.random.default_rng(29 + bits)
+    for (M, K, N, O) in [(16, 512, 384, 128), (200, 1024, 640, 64), (3, 640, 128, 0)]:
+        L, x, _ = make_layer(rng, M, K, N, bits, O, heavy_cols=4)
+        st, want = o.quik_matmul(L, x, 2)
+        dev = m.QuikLinear(to_layer(L))
+        y = dev(torch.from_numpy(x).half().cuda()).float().cpu().numpy()
+        err = np.abs(y - want)
+        assert np.all(err <= elementwise_bound(L, x, want) * 2 + 6.2e-5 * np.abs(want)), float(err.max())
+        assert rel_frob(want, y) <= 5e-4
+
+
+def test_variants_bit_identical():
+    # test_runtime.cpp:270-281 / acceptance criterion 5
+    m = q()
+    import torch
+
+    rng = np.random.default_rng(31)
+    for trial in range(6):
+        bits = 4 if trial % 2 == 0 else 8
+        L, x, _ = make_layer(rng, 5 + 13 * trial, 48 + 40 * trial, 24 + 50 * trial, bits, 8 * (trial % 3), 1)
+        dev = m.QuikLinear(to_layer(L))
+        xt = torch.from_numpy(x).cuda()
+        outs = [dev(xt, out_dtype=torch.float32, variant=v).cpu().numpy() for v in m.PipelineVariant]
+        np.testing.assert_array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+        np.testing.assert_array_equal(outs[0].view(np.uint32), outs[2].view(np.uint32))
+
+
+def test_layer_matches_compiled_reference():
+    """Same seeded layer through the reference sources themselves (oracle/_ref)."""
+    m = q()
+    r = ref()
+    rng = np.random.default_rng(37)
+    L, x, _ = make_layer(rng, 24, 640, 200, 4, 0, heavy_cols=3, checker=r)
+    st, want = r.quik_matmul(L, x, 2)
+    assert st == 0
+    got = m.quik_matmul(to_layer(L), x)
+    np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_cfg1_oracle_shape():
+    """BASELINE configs[0]: 16 tokens x 4096 -> 4096, 128 outliers, W4A4."""
+    m = q()
+    o = oracle()
+    import torch
+
+    rng = np.random.default_rng(41)
+    L, x, _ = make_layer(rng, 16, 4096, 4096, 4, 128, heavy_cols=128)
+    st, want = o.quik_matmul(L, x, 2)
+    dev = m.QuikLinear(to_layer(L))
+    y32 = dev(torch.from_numpy(x).cuda(), out_dtype=torch.float32).cpu().numpy()
+    assert rel_frob(want, y32) < 1e-5
+    y16 = dev(torch.from_numpy(x).half().cuda()).float().cpu().numpy()
+    assert rel_frob(want, y16) < 5e-4
+
+
+def test_large_layer_token_subset_exact():
+    """Full-size property: tokens and output rows are independent, so the oracle on a
+    subset of tokens and rows checks the full-size device run exactly (O = 0, f32)."""
+    m = q()
+    o = oracle()
+    import torch
+
+    rng = np.random.default_rng(43)
+    M, K, N = 1024, 8192, 4096
+    L, x, _ = make_layer(rng, M, K, N, 4, 0, heavy_cols=0)
+    dev = m.QuikLinear(to_layer(L))
+    y = dev(torch.from_numpy(x).cuda(), out_dtype=torch.float32).cpu().numpy()
+    toks = np.sort(rng.choice(M, 6, replace=False))
+    rows = np.sort(rng.choice(N, 300, replace=False))
+    rb = row_bytes(K, 4)
+    sub = dict(L)
+    sub["out_features"] = rows.size
+    sub["base"] = np.asarray(L["base"]).reshape(N, rb)[rows].reshape(-1)
+    sub["scales"] = L["scales"][rows]
+    sub["wreduced"] = L["wreduced"][rows]
+    sub["outlier_weights"] = np.zeros((rows.size, 0), np.float32)
+    sub["bias"] = L["bias"][rows]
+    st, want = o.quik_matmul(sub, x[toks], 2)
+    np.testing.assert_array_equal(y[np.ix_(toks, rows)].view(np.uint32), want.view(np.uint32))
+
+
+def test_non_finite_input_flags_numerical_error():
+    m = q()
+    import torch
+
+    rng = np.random.default_rng(47)
+    L, x, _ = make_layer(rng, 4, 64, 32, 4, 4)
+    lay = to_layer(L)
+    dev = m.QuikLinear(lay)
+    base_col = int(lay.outliers.permutation[0])
+    x[2, base_col] = np.nan
+    dev(torch.from_numpy(x).cuda())
+    with pytest.raises(m.NumericalError):
+        dev.ctx.sync(torch.cuda.current_stream().cuda_stream)
+    with pytest.raises(m.NumericalError):
+        m.quik_matmul(lay, x)
