@@ -1,0 +1,449 @@
+#!/usr/bin/env python
+"""bench.py — QUIK linear-layer throughput on B200 (BASELINE.json metric:
+"QUIK linear TOPS & speedup vs FP16 cuBLAS at LLaMA-2-70B shapes, 1/2/4/8 GPU").
+
+One step = one QUIK linear forward (K1 fused quantizer + fused tcgen05 INT/FP16
+GEMM with the dequantisation epilogue) over a synthetic activation batch of the
+workload shape, inputs resident in HBM. Default workload: BASELINE configs[2],
+the LLaMA-2-70B MLP up/gate layer 8192 -> 28672, 256 outliers, W4A4, 4096 tokens
+(fits one GPU). For N > 1 (torchrun) the output features are sharded over the
+ranks and the FP16 output is all-gathered with NCCL (strong scaling: total work
+fixed). value = whole-job TOPS = 2*M*N*K / step time (max over ranks).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg3]
+  python bench.py --impl reference ...   # the reference's own CPU quik_matmul
+                                         # (oracle/_ref: the unmodified sources)
+
+Extra keys: roofline (GEMM kernel vs tensor peak), cpu_baseline (reference CPU
+path on this host), e2e (host buffers through the public API, H2D/D2H inside the
+timed region), fp16_cublas (torch.matmul f16 of the same shape), clocks,
+gpu_launches.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "QUIK linear TOPS & speedup vs FP16 cuBLAS at LLaMA-2-70B shapes, 1/2/4/8 GPU"
+
+WORKLOADS = {
+    # BASELINE.json configs[2] (headline): LLaMA-2-70B MLP up/gate (arch/llama2-70b.json:16-17)
+    "cfg3": dict(desc="LLaMA-2-70B MLP up/gate 8192->28672, 256 outliers, W4A4, 4096 tokens",
+                 M=4096, K=8192, N=28672, O=256, bits=4),
+    "cfg3-down": dict(desc="LLaMA-2-70B MLP down 28672->8192, 896 outliers, W8A8, 4096 tokens",
+                      M=4096, K=28672, N=8192, O=896, bits=8),
+    "cfg1": dict(desc="QUIK W4A4 4096->4096, 128 outliers, 16 tokens (oracle shape)", M=16, K=4096, N=4096, O=128,
+                 bits=4),
+    "cfg2-qkvo": dict(desc="LLaMA-2-7B q/k/v/o 4096->4096, 256 outliers, W4A4, 2048 tokens", M=2048, K=4096,
+                      N=4096, O=256, bits=4),
+    "cfg2-up": dict(desc="LLaMA-2-7B up/gate 4096->11008, 256 outliers, W4A4, 2048 tokens", M=2048, K=4096,
+                    N=11008, O=256, bits=4),
+    "cfg2-down": dict(desc="LLaMA-2-7B down 11008->4096, 688 outliers, W8A8, 2048 tokens", M=2048, K=11008,
+                      N=4096, O=688, bits=8),
+    "cfg4-opt-fc1": dict(desc="OPT-66B fc1 9216->36864, 256 outliers, W4A4, 2048 tokens", M=2048, K=9216,
+                         N=36864, O=256, bits=4),
+}
+
+CPU_SAMPLE_TOKENS = 64  # bounded sample of the workload for the CPU reference
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return dict(hbm_gbs=float(d["hbm_gbs"]), bf16=float(d["bf16_tflops"]),
+                    bf16_sustained=float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), source="measured")
+    return dict(hbm_gbs=6650.0, bf16=1590.0, bf16_sustained=1400.0, source="fallback")
+
+
+def emit(obj):
+    print(json.dumps(obj), flush=True)
+
+
+# =============================================================================== reference arm
+
+
+def synth_host(w, seed, tokens):
+    """CPU synthetic layer for the reference arm, bench.cpp:51-72 style: W, x ~ N(0,1),
+    O random heavy columns x50, outliers = select_outliers(x), RTN weights — all with
+    the reference's own functions (oracle/_ref)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import ref  # the reference's compiled sources (TEST/BASELINE infrastructure)
+
+    r = ref()
+    rng = np.random.default_rng(seed)
+    W = rng.standard_normal((w["N"], w["K"]), dtype=np.float32)
+    x = rng.standard_normal((tokens, w["K"]), dtype=np.float32)
+    heavy = np.unique(rng.integers(0, w["K"], size=max(w["O"], 1)))
+    if w["O"]:
+        x[:, heavy] *= 50.0
+    x = x.astype(np.float16).astype(np.float32)
+    idx = r.select_outliers(x, w["O"])
+    q = r.rtn_quantize_weights(W, idx, w["bits"])
+    del W
+    L = dict(in_features=w["K"], out_features=w["N"], bits=w["bits"], act_bits=w["bits"], base=q["base"],
+             scales=q["scales"], wreduced=q["wreduced"], outlier_weights=q["outlier_weights"], idx=idx, bias=None)
+    return r, L, x
+
+
+def run_reference(args, w):
+    """The reference's own CPU implementation (oracle/_ref = proj/src compiled unchanged,
+    OpenMP on all host threads), each step one quik_matmul V3 call on a bounded token
+    sample of the workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    M_s = args.cpu_tokens
+    r, L, x = synth_host(w, args.seed, M_s)
+    h, keep = r.layer_create(L)
+    times = np.zeros(6)
+    for _ in range(args.warmup):
+        st, _ = r.layer_forward(h, x, w["N"], 2)
+        assert st == 0, st
+    per = []
+    stage = np.zeros(6)
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        st, _ = r.layer_forward(h, x, w["N"], 2, times)
+        per.append(time.perf_counter() - t0)
+        stage += times
+    r.layer_destroy(h)
+    total = sum(per)
+    ops = 2.0 * M_s * w["N"] * w["K"]
+    value = ops * args.steps / total / 1e12
+    sample = (f"{M_s} of {w['M']} tokens of {args.workload} ({w['desc']}); quik_matmul V3 per step, "
+              f"OpenMP threads={os.environ.get('OMP_NUM_THREADS')}")
+    out = dict(metric=METRIC, value=value, unit="TOPS", n_gpus=args.gpus, steps=args.steps, warmup=args.warmup,
+               ms_per_step=1e3 * total / args.steps, higher_is_better=True, scaling="strong", vs_baseline=None,
+               dtype="int8", data="synthetic", impl="reference",
+               config=dict(workload=args.workload, M=w["M"], K=w["K"], N=w["N"], outliers=w["O"], bits=w["bits"],
+                           sample_tokens=M_s),
+               cpu_baseline=dict(value=value, unit="TOPS", cores=int(os.environ.get("OMP_NUM_THREADS", cores)),
+                                 kind="reference", sample=sample,
+                                 stage_ms_mean=dict(zip(["split", "quantize", "int_matmul", "fp_matmul",
+                                                         "dequantize", "add"],
+                                                        (stage / args.steps).round(3).tolist()))),
+               e2e=dict(value=value, unit="TOPS", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    emit(out)
+
+
+# =============================================================================== our arm
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.proc = None
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        rows = []
+        for line in Path(self.path).read_text().splitlines():
+            p = [s.strip() for s in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                rows.append(dict(sm=float(p[1]), smax=float(p[2]), power=float(p[3]), hw=p[5], hwt=p[6], swt=p[7],
+                                 swp=p[8]))
+            except ValueError:
+                continue
+        os.unlink(self.path)
+        if not rows:
+            return None
+        load = [r for r in rows if r["power"] > 300.0] or rows
+        reasons = sorted({name for r in load for name, key in (("hw_slowdown", "hw"),
+                                                                 ("hw_thermal_slowdown", "hwt"),
+                                                                 ("sw_thermal_slowdown", "swt"),
+                                                                 ("sw_power_cap", "swp")) if r[key] == "Active"})
+        return dict(sm_mhz=statistics.median(r["sm"] for r in load), sm_max_mhz=max(r["smax"] for r in rows),
+                    reasons=reasons, samples=len(rows), samples_under_load=len(load),
+                    power_w_max=max(r["power"] for r in rows))
+
+
+def run_ours(args, w):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2310_09259_b200 as q
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    M, K, N, O, bits = w["M"], w["K"], w["N"], w["O"], w["bits"]
+    if N % world:
+        raise SystemExit(f"out_features {N} not divisible by {world} GPUs")
+    ns = N // world
+    rb, re_ = rank * ns, (rank + 1) * ns
+
+    # ---- synthetic layer, generated on the device (same seed on every rank)
+    g = torch.Generator(device=dev)
+    g.manual_seed(args.seed)
+    x = torch.randn((M, K), generator=g, device=dev, dtype=torch.float32)
+    heavy = torch.unique(torch.randint(0, K, (max(O, 1),), generator=g, device=dev))
+    if O:
+        x[:, heavy] *= 50.0
+    x16 = x.half()
+    maxabs = x16.float().abs().amax(0)
+    order = torch.sort(maxabs, descending=True, stable=True).indices[:O]
+    outliers = q.OutlierSet.from_indices(K, order.cpu().numpy())
+    del x, maxabs
+    Wt = torch.randn((ns, K), generator=torch.Generator(device=dev).manual_seed(args.seed * 1000 + rank), device=dev,
+                     dtype=torch.float32)
+    base, sc, wr, ow = q.rtn_quantize_weights_device(Wt, outliers, bits)
+    del Wt
+    layer = q.QuikLinear.from_device(outliers, base, sc, wr, ow, bits)
+    del base, ow
+    torch.cuda.synchronize()
+
+    y_local = torch.empty((M, ns), dtype=torch.float16, device=dev)
+    if world > 1:
+        gathered = torch.empty((world, M, ns), dtype=torch.float16, device=dev)
+        y = torch.empty((M, N), dtype=torch.float16, device=dev)
+
+    steps, warm = args.steps, args.warmup
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+
+    def step(i=None):
+        e = ev[i] if i is not None else None
+        if e:
+            e[0].record()
+        layer.forward(x16, out=y_local, mid_event=e[1] if e else None)
+        if e:
+            e[2].record()
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, y_local)
+            y.view(M, world, ns).copy_(gathered.permute(1, 0, 2))
+
+    for e3 in ev:  # materialise the raw cudaEvent handles
+        for e in e3:
+            e.record()
+    for _ in range(warm):
+        step()
+    torch.cuda.synchronize()
+
+    # soak (untimed) with the clock sampler running through the timed region
+    sampler = ClockSampler(local) if not args.no_clocks else None
+    t_end = time.perf_counter() + args.soak_s
+    while time.perf_counter() < t_end:
+        for _ in range(10):
+            step()
+        torch.cuda.synchronize()
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    for i in range(steps):
+        step(i)
+    end.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+
+    total_ms = start.elapsed_time(end)
+    gemm_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    quant_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    stats = torch.tensor([total_ms, statistics.mean(gemm_ms), statistics.mean(quant_ms)], device=dev,
+                         dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+    total_ms, gemm_avg, quant_avg = stats.tolist()
+    ms_per_step = total_ms / steps
+    ops = 2.0 * M * N * K
+    value = ops / (ms_per_step * 1e-3) / 1e12
+
+    # ---- roofline of the dominant kernel (fused GEMM), per launch on this rank
+    pk = peaks()
+    kb = K - O
+    p_f16 = pk["bf16"]
+    p_i8 = 2.0 * p_f16  # B200 dense INT8 = 2x dense FP16/BF16 tensor rate
+    ops_rank = 2.0 * M * ns * K
+    t_ideal_s = 2.0 * M * ns * kb / (p_i8 * 1e12) + 2.0 * M * ns * O / (p_f16 * 1e12)
+    mixed_peak = ops_rank / t_ideal_s / 1e12
+    achieved = ops_rank / (gemm_avg * 1e-3) / 1e12
+    traffic = None
+    tp = ROOT / "profiles" / "ncu_gemm_traffic.json"
+    if tp.exists():
+        try:
+            tj = json.loads(tp.read_text())
+            traffic = tj.get(args.workload)
+        except Exception:
+            traffic = None
+    roofline = dict(bound="tensor", achieved=achieved, peak=mixed_peak, unit="TFLOP/s", frac=achieved / mixed_peak,
+                    traffic=traffic,
+                    kernel="quik_gemm_kernel (fused int8 GEMM + f16 outlier GEMM + dequant epilogue)",
+                    peak_basis=(f"{pk['source']} bf16 burst {p_f16:.1f} TF/s (MEASURED_PEAKS.json) for the "
+                                f"{O} f16 outlier columns; INT8 peak = 2x that = {p_i8:.1f} TOPS for the {kb} "
+                                "int columns; mixed peak = ops / (int_ops/P_i8 + f16_ops/P_f16)"),
+                    int8_only_frac=achieved / p_i8, kernel_ms=gemm_avg)
+    bytes_q = M * K * 2 + M * (kb + 127) // 128 * 128 + M * ((O + 63) // 64 * 64) * 2 + 8 * M
+    quant = dict(kernel="quantize_rows_kernel (K1)", ms=quant_avg, algorithmic_bytes=bytes_q,
+                 achieved_gbs=bytes_q / (quant_avg * 1e-3) / 1e9 if quant_avg > 0 else None,
+                 peak_gbs=pk["hbm_gbs"],
+                 frac=(bytes_q / (quant_avg * 1e-3) / 1e9) / pk["hbm_gbs"] if quant_avg > 0 else None)
+
+    # ---- FP16 cuBLAS GEMM of the same (sharded) shape, same x
+    fp16 = None
+    if not args.no_cublas:
+        Wf = torch.randn((ns, K), device=dev, dtype=torch.float16)
+        out16 = torch.empty((M, ns), device=dev, dtype=torch.float16)
+        for _ in range(3):
+            torch.matmul(x16, Wf.t(), out=out16)
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(steps):
+            torch.matmul(x16, Wf.t(), out=out16)
+        s1.record()
+        torch.cuda.synchronize()
+        t16 = torch.tensor([s0.elapsed_time(s1) / steps], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t16, op=dist.ReduceOp.MAX)
+        t16 = float(t16.item())
+        fp16 = dict(ms=t16, tflops=2.0 * M * ns * K / (t16 * 1e-3) / 1e12, speedup_step=t16 / (ms_per_step),
+                    speedup_gemm=t16 / gemm_avg, note="torch.matmul f16 (cuBLAS) of the per-rank shape, same x")
+        del Wf, out16
+
+    # ---- e2e: host (pinned) buffers through the public API, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        xh = x16.cpu().pin_memory()
+        yh = torch.empty((M, N if world > 1 else ns), dtype=torch.float16).pin_memory()
+        xd = torch.empty_like(x16)
+        e2e_steps = max(3, min(steps, 10))
+
+        def e2e_step():
+            xd.copy_(xh, non_blocking=True)
+            layer.forward(xd, out=y_local)
+            if world > 1:
+                dist.all_gather_into_tensor(gathered, y_local)
+                y.view(M, world, ns).copy_(gathered.permute(1, 0, 2))
+                if rank == 0:
+                    yh.copy_(y, non_blocking=True)
+            else:
+                yh.copy_(y_local, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(e2e_steps):
+            e2e_step()
+        b.record()
+        torch.cuda.synchronize()
+        te = torch.tensor([a.elapsed_time(b) / e2e_steps], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        te = float(te.item())
+        e2e = dict(value=ops / (te * 1e-3) / 1e12, unit="TOPS", h2d_bytes_per_step=M * K * 2 * world,
+                   d2h_bytes_per_step=M * N * 2, ms_per_step=te, steps=e2e_steps,
+                   path="QuikLinear.forward (C ABI quik_linear_forward_ex) with pinned host f16 x -> y")
+
+    # ---- CPU baseline: the reference's own code on this host, rank 0, N = 1 only
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cmd = [sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--workload", args.workload,
+               "--steps", "3", "--warmup", "1", "--cpu-tokens", str(args.cpu_tokens)]
+        env = dict(os.environ)
+        for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK"):
+            env.pop(k, None)
+        env["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+            line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
+            cpu = json.loads(line)["cpu_baseline"]
+        except Exception as exc:  # reported, never silently replaced
+            cpu = dict(value=None, unit="TOPS", cores=os.cpu_count(), kind="reference",
+                       sample=f"failed: {type(exc).__name__}")
+
+    if rank == 0:
+        out = dict(metric=METRIC, value=value, unit="TOPS", n_gpus=world, steps=steps, warmup=warm,
+                   ms_per_step=ms_per_step, higher_is_better=True, scaling="strong", vs_baseline=None,
+                   dtype="int8", data="synthetic",
+                   config=dict(workload=args.workload, desc=w["desc"], M=M, K=K, N=N, outliers=O, bits=bits,
+                               parallelism=f"output-feature shards x{world}" + (" + NCCL all-gather" if world > 1 else ""),
+                               l2="inputs larger than L2 (int8 weights %.0f MB, x f16 %.0f MB); no flush" %
+                                  (N * ((kb + 127) // 128 * 128) / 1e6, M * K * 2 / 1e6)),
+                   roofline=roofline, cpu_baseline=cpu, e2e=e2e, fp16_cublas=fp16, quantizer=quant,
+                   clocks=clocks, gpu_launches=steps * q.QuikLinear.launches(),
+                   precision="W%dA%d integer codes on tcgen05 kind::i8 (s32 accumulate) + f16 outliers (f32 accumulate), f16 out"
+                             % (bits, bits))
+        emit(out)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
+    ap.add_argument("--seed", type=int, default=2310)
+    ap.add_argument("--cpu-tokens", type=int, default=CPU_SAMPLE_TOKENS)
+    ap.add_argument("--soak-s", type=float, default=1.5)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cublas", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--tile", default="", help="force the GEMM tile 'cta_group,block_n' (tuning)")
+    args = ap.parse_args()
+    if args.tile and args.impl == "ours":
+        import paper_2310_09259_b200 as q
+
+        cg, bn = (int(v) for v in args.tile.split(","))
+        from paper_2310_09259_b200 import _lib
+
+        _lib.check(q.load_library().quik_set_gemm_tile(cg, bn))
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3  # timing rule: at least 3 warm-up steps
+    w = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, w)
+    else:
+        run_ours(args, w)
+
+
+if __name__ == "__main__":
+    main()

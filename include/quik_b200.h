@@ -70,6 +70,7 @@ quik_status quik_ctx_sync(quik_ctx_t ctx, void* stream);
  *   outlier_weights [out_features][n_outlier] f32 (rounded to f16 on the device)
  *   outlier_indices [n_outlier] sorted, unique, in [0, in_features)
  *   bias            [out_features] or NULL
+ *   All arrays except outlier_indices may be host or device memory (UVA copy).
  *   row_begin/row_end: optional output-row shard [row_begin, row_end) of the layer
  *                   (multi-GPU column sharding); 0/0 = all rows.
  */
@@ -136,6 +137,31 @@ quik_status quik_linear_forward(quik_ctx_t ctx, quik_layer_t layer, const void* 
 quik_status quik_linear_forward_strided(quik_ctx_t ctx, quik_layer_t layer, const void* x, quik_dtype x_dtype,
                                         int64_t M, void* y, quik_dtype y_dtype, int64_t ldy, quik_variant variant,
                                         void* stream);
+
+/* Same as _strided; additionally records `mid_event` (a cudaEvent_t, may be NULL)
+ * on `stream` between the quantizer and the GEMM launch (V3) for per-kernel timing. */
+quik_status quik_linear_forward_ex(quik_ctx_t ctx, quik_layer_t layer, const void* x, quik_dtype x_dtype, int64_t M,
+                                   void* y, quik_dtype y_dtype, int64_t ldy, quik_variant variant, void* stream,
+                                   void* mid_event);
+
+/* Round-to-nearest weight quantization on the device.
+ * reference: rtn_quantize_weights (quantizer.hpp:87-88, quantizer.cpp:339-371) with
+ * use_clipping = false; bit-exact (FP64 scale, ties away from zero, wreduced in FP64).
+ * w: DEVICE f32 [N][K]. outlier_indices: HOST, sorted unique. Outputs (DEVICE):
+ * base packed [N][row_bytes(K - n_outlier)] (i4p / i8), scales [N], wreduced [N],
+ * outlier_weights [N][n_outlier] f32 (original values, permuted-tail order). */
+quik_status quik_rtn_quantize_weights(quik_ctx_t ctx, const float* w, int64_t N, int64_t K,
+                                      const int64_t* outlier_indices, int64_t n_outlier, int bits, uint8_t* base,
+                                      float* scales, float* wreduced, float* outlier_weights, void* stream);
+
+/* Tuning/debug knob (process-wide): force the GEMM tile, cta_group in {1, 2} and
+ * token block_n in {32, 64, 128} (1-CTA) or {128, 256} (CTA pair); (0, 0) restores
+ * the heuristic. */
+quik_status quik_set_gemm_tile(int cta_group, int block_n);
+
+/* Diagnostics (process-wide): when on, the V3 forward runs the fused GEMM
+ * without writing the output (mainloop + TMEM drain only). Never for results. */
+quik_status quik_set_probe_mode(int on);
 
 /* Number of device kernels quik_linear_forward launches for (variant) — the
  * bench reports it as gpu_launches. */

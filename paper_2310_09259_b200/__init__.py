@@ -22,6 +22,8 @@ from .quik import (  # noqa: F401
     quantize_activations_fused,
     quik_matmul,
     row_bytes,
+    rtn_quantize_weights,
+    rtn_quantize_weights_device,
     unpack_values,
 )
 from ._lib import LIB_PATH, load as load_library  # noqa: F401

@@ -27,7 +27,8 @@ EXPORTED_SYMBOLS = (
     "quik_ctx_sync", "quik_layer_create", "quik_layer_destroy", "quik_layer_info",
     "quik_quantize_activations_fused", "quik_quantize_activations", "quik_int_matmul",
     "quik_dequantize_epilogue", "quik_linear_forward", "quik_linear_forward_strided",
-    "quik_linear_forward_launches",
+    "quik_linear_forward_launches", "quik_linear_forward_ex", "quik_rtn_quantize_weights",
+    "quik_set_gemm_tile", "quik_set_probe_mode",
 )
 
 
@@ -89,6 +90,10 @@ def load() -> C.CDLL:
             "quik_linear_forward": (i32, [vp, vp, vp, i32, i64, vp, i32, i32, vp]),
             "quik_linear_forward_strided": (i32, [vp, vp, vp, i32, i64, vp, i32, i64, i32, vp]),
             "quik_linear_forward_launches": (i32, [i32]),
+            "quik_linear_forward_ex": (i32, [vp, vp, vp, i32, i64, vp, i32, i64, i32, vp, vp]),
+            "quik_rtn_quantize_weights": (i32, [vp, vp, i64, i64, vp, i64, i32, vp, vp, vp, vp, vp]),
+            "quik_set_gemm_tile": (i32, [i32, i32]),
+            "quik_set_probe_mode": (i32, [i32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)

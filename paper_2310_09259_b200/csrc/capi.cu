@@ -21,6 +21,7 @@ using namespace quikb200;
 namespace {
 
 thread_local std::string g_err;
+int g_probe_mode = 0;  // diagnostics: V3 GEMM without output stores (quik_set_probe_mode)
 
 quik_status fail(quik_status s, const std::string& msg) {
   g_err = msg;
@@ -91,6 +92,8 @@ struct quik_layer_s {
   float* bias = nullptr;     // [out] or null
   int32_t* base_src = nullptr;  // [kb]
   int32_t* out_src = nullptr;   // [n_outlier]
+  uint8_t* lane_mask = nullptr;  // [round_up(in,16)] 0xFF = outlier column (null when n_outlier == 0)
+  uint16_t* gather = nullptr;    // [kpad] base position -> source column (null when n_outlier == 0)
 };
 
 namespace {
@@ -127,9 +130,10 @@ void run_k1(quik_ctx_t ctx, const quik_layer_s* L, const void* x, quik_dtype xdt
   q.M = M;
   q.K = L->in_features;
   q.ldx = L->in_features;
-  q.base_src = L->base_src;
-  q.kb = L->kb;
+  q.lane_mask = L->lane_mask;
+  q.gather = L->gather;
   q.out_src = L->out_src;
+  q.kb = L->kb;
   q.n_out = L->n_outlier;
   q.bits = L->bits;
   q.q8 = L->kpad ? static_cast<int8_t*>(ctx->q8.ensure(static_cast<size_t>(M * L->kpad))) : nullptr;
@@ -187,6 +191,23 @@ const char* quik_status_string(quik_status s) {
 }
 
 int quik_abi_version(void) { return QUIK_B200_ABI_VERSION; }
+
+quik_status quik_set_probe_mode(int on) {
+  g_probe_mode = on;
+  return QUIK_OK;
+}
+
+quik_status quik_set_gemm_tile(int cta_group, int block_n) {
+  if (cta_group == 0 && block_n == 0) {
+    quikb200::gemm_tile_override = 0;
+    return QUIK_OK;
+  }
+  const bool ok = (cta_group == 1 && (block_n == 32 || block_n == 64 || block_n == 128)) ||
+                  (cta_group == 2 && (block_n == 128 || block_n == 256));
+  if (!ok) return fail(QUIK_ERR_INVALID_ARGUMENT, "unsupported GEMM tile configuration");
+  quikb200::gemm_tile_override = (cta_group << 16) | block_n;
+  return QUIK_OK;
+}
 
 int quik_linear_forward_launches(quik_variant v) {
   switch (v) {
@@ -271,6 +292,7 @@ quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* d, quik_l
     return fail(QUIK_ERR_INVALID_ARGUMENT, "layer: missing weight arrays");
   if (rows > 0x7fffffffLL || kb > 0x7fffffffLL)
     return fail(QUIK_ERR_UNSUPPORTED, "layer: dimensions exceed 2^31");
+  if (d->in_features > 65520) return fail(QUIK_ERR_UNSUPPORTED, "layer: in_features > 65520");
 
   return guarded([&] {
     DeviceGuard g(ctx->device);
@@ -293,6 +315,11 @@ quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* d, quik_l
     for (int64_t f = 0; f < d->in_features; ++f)
       if (!is_out[f]) base_src.push_back(static_cast<int32_t>(f));
     std::vector<int32_t> out_src(d->outlier_indices, d->outlier_indices + d->n_outlier);
+    const int64_t kr16 = round_up(d->in_features, 16);
+    std::vector<uint8_t> lane_mask(static_cast<size_t>(kr16), 0);
+    for (int64_t i = 0; i < d->n_outlier; ++i) lane_mask[d->outlier_indices[i]] = 0xFF;
+    std::vector<uint16_t> gather(static_cast<size_t>(L->kpad), static_cast<uint16_t>(kr16));
+    for (int64_t j = 0; j < kb; ++j) gather[j] = static_cast<uint16_t>(base_src[j]);
 
     cudaStream_t st = nullptr;
     if (kb) {
@@ -302,21 +329,25 @@ quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* d, quik_l
     if (d->n_outlier) {
       QK_CUDA(cudaMalloc(&L->out_src, d->n_outlier * 4));
       QK_CUDA(cudaMemcpy(L->out_src, out_src.data(), d->n_outlier * 4, cudaMemcpyHostToDevice));
+      QK_CUDA(cudaMalloc(&L->lane_mask, kr16));
+      QK_CUDA(cudaMemcpy(L->lane_mask, lane_mask.data(), kr16, cudaMemcpyHostToDevice));
+      QK_CUDA(cudaMalloc(&L->gather, std::max<int64_t>(L->kpad, 1) * 2));
+      if (L->kpad) QK_CUDA(cudaMemcpy(L->gather, gather.data(), L->kpad * 2, cudaMemcpyHostToDevice));
     }
     if (rows > 0) {
       QK_CUDA(cudaMalloc(&L->w_scale, rows * 4));
       QK_CUDA(cudaMalloc(&L->wreduced, rows * 4));
-      QK_CUDA(cudaMemcpy(L->w_scale, d->scales + rb, rows * 4, cudaMemcpyHostToDevice));
-      QK_CUDA(cudaMemcpy(L->wreduced, d->wreduced + rb, rows * 4, cudaMemcpyHostToDevice));
+      QK_CUDA(cudaMemcpy(L->w_scale, d->scales + rb, rows * 4, cudaMemcpyDefault));
+      QK_CUDA(cudaMemcpy(L->wreduced, d->wreduced + rb, rows * 4, cudaMemcpyDefault));
       if (d->bias) {
         QK_CUDA(cudaMalloc(&L->bias, rows * 4));
-        QK_CUDA(cudaMemcpy(L->bias, d->bias + rb, rows * 4, cudaMemcpyHostToDevice));
+        QK_CUDA(cudaMemcpy(L->bias, d->bias + rb, rows * 4, cudaMemcpyDefault));
       }
       if (kb) {
         const int64_t rbytes = packed_row_bytes(kb, d->bits);
         QK_CUDA(cudaMalloc(&L->w8, static_cast<size_t>(rows * L->kpad)));
         void* tmp = ctx->wtmp.ensure(static_cast<size_t>(rows * rbytes));
-        QK_CUDA(cudaMemcpy(tmp, d->base + rb * rbytes, static_cast<size_t>(rows * rbytes), cudaMemcpyHostToDevice));
+        QK_CUDA(cudaMemcpy(tmp, d->base + rb * rbytes, static_cast<size_t>(rows * rbytes), cudaMemcpyDefault));
         check_launch(launch_unpack_to_gemm(static_cast<const uint8_t*>(tmp), rows, kb, d->bits, L->w8, L->kpad, st),
                      "weight unpack");
       }
@@ -324,7 +355,7 @@ quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* d, quik_l
         QK_CUDA(cudaMalloc(&L->wo16, static_cast<size_t>(rows * L->opad * 2)));
         void* tmp = ctx->fp.ensure(static_cast<size_t>(rows * d->n_outlier * 4));
         QK_CUDA(cudaMemcpy(tmp, d->outlier_weights + rb * d->n_outlier, static_cast<size_t>(rows * d->n_outlier * 4),
-                           cudaMemcpyHostToDevice));
+                           cudaMemcpyDefault));
         check_launch(launch_f32_to_f16_padded(static_cast<const float*>(tmp), rows, d->n_outlier, L->wo16, L->opad, st),
                      "outlier weight convert");
       }
@@ -346,6 +377,8 @@ quik_status quik_layer_destroy(quik_layer_t L) {
   cudaFree(L->bias);
   cudaFree(L->base_src);
   cudaFree(L->out_src);
+  cudaFree(L->lane_mask);
+  cudaFree(L->gather);
   delete L;
   return QUIK_OK;
 }
@@ -364,8 +397,8 @@ quik_status quik_quantize_activations_fused(quik_ctx_t ctx, quik_layer_t L, cons
                                             void* stream) {
   if (!ctx || !L) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context or layer");
   if (M < 0 || (M > 0 && !x)) return fail(QUIK_ERR_INVALID_ARGUMENT, "fused quantization: bad input");
-  if (L->in_features * (xdt == QUIK_F32 ? 4 : 2) > 200 * 1024)
-    return fail(QUIK_ERR_UNSUPPORTED, "fused quantization: row too wide for shared-memory staging");
+  if (L->in_features * (xdt == QUIK_F32 ? 4 : 2) > 128 * 1024)
+    return fail(QUIK_ERR_UNSUPPORTED, "fused quantization: row wider than 128 KiB (register-resident quantizer limit)");
   return guarded([&] {
     DeviceGuard g(ctx->device);
     QuantArgs q{};
@@ -374,9 +407,10 @@ quik_status quik_quantize_activations_fused(quik_ctx_t ctx, quik_layer_t L, cons
     q.M = M;
     q.K = L->in_features;
     q.ldx = L->in_features;
-    q.base_src = L->base_src;
-    q.kb = L->kb;
+    q.lane_mask = L->lane_mask;
+    q.gather = L->gather;
     q.out_src = L->out_src;
+    q.kb = L->kb;
     q.n_out = L->n_outlier;
     q.bits = L->bits;
     q.packed = packed;
@@ -394,22 +428,16 @@ quik_status quik_quantize_activations(quik_ctx_t ctx, const void* x, quik_dtype 
   if (!ctx) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context");
   if (bits != 4 && bits != 8) return fail(QUIK_ERR_INVALID_ARGUMENT, "activation bits must be 4 or 8");
   if (M < 0 || K < 0 || (M > 0 && K > 0 && !x)) return fail(QUIK_ERR_INVALID_ARGUMENT, "quantize: bad input");
-  if (K * (xdt == QUIK_F32 ? 4 : 2) > 200 * 1024)
-    return fail(QUIK_ERR_UNSUPPORTED, "quantize: row too wide for shared-memory staging");
+  if (K * (xdt == QUIK_F32 ? 4 : 2) > 128 * 1024)
+    return fail(QUIK_ERR_UNSUPPORTED, "quantize: row wider than 128 KiB (register-resident quantizer limit)");
   return guarded([&] {
     DeviceGuard g(ctx->device);
-    // identity permutation table
-    int32_t* ident = static_cast<int32_t*>(ctx->xbase.ensure(static_cast<size_t>(std::max<int64_t>(K, 1) * 4)));
-    std::vector<int32_t> h(static_cast<size_t>(K));
-    for (int64_t i = 0; i < K; ++i) h[i] = static_cast<int32_t>(i);
-    if (K) QK_CUDA(cudaMemcpyAsync(ident, h.data(), K * 4, cudaMemcpyHostToDevice, as_stream(stream)));
     QuantArgs q{};
     q.x = x;
     q.x_is_f32 = xdt == QUIK_F32;
     q.M = M;
     q.K = K;
     q.ldx = K;
-    q.base_src = ident;
     q.kb = K;
     q.bits = bits;
     q.packed = packed;
@@ -417,7 +445,6 @@ quik_status quik_quantize_activations(quik_ctx_t ctx, const void* x, quik_dtype 
     q.zero = zero ? zero : static_cast<float*>(ctx->zero.ensure(M * 4));
     q.err = ctx->d_err;
     check_launch(launch_quantize(q, as_stream(stream)), "quantize kernel");
-    QK_CUDA(cudaStreamSynchronize(as_stream(stream)));  // h must outlive the async copy
     return QUIK_OK;
   });
 }
@@ -477,15 +504,16 @@ quik_status quik_dequantize_epilogue(quik_ctx_t ctx, const int32_t* acc, int64_t
   });
 }
 
-quik_status quik_linear_forward_strided(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M,
-                                        void* y, quik_dtype ydt, int64_t ldy, quik_variant variant, void* stream) {
+quik_status quik_linear_forward_ex(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M,
+                                   void* y, quik_dtype ydt, int64_t ldy, quik_variant variant, void* stream,
+                                   void* mid_event) {
   if (!ctx || !L) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context or layer");
   if (M < 0) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_matmul: negative token count");
   if (M > 0 && (!x || !y)) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_matmul: null input or output");
   if (M > 0x7fffffffLL) return fail(QUIK_ERR_UNSUPPORTED, "quik_matmul: token count exceeds 2^31");
   if (ldy < L->out_features) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_matmul: output pitch < out_features");
-  if (L->in_features * (xdt == QUIK_F32 ? 4 : 2) > 200 * 1024)
-    return fail(QUIK_ERR_UNSUPPORTED, "quik_matmul: row too wide for shared-memory staging");
+  if (L->in_features * (xdt == QUIK_F32 ? 4 : 2) > 128 * 1024)
+    return fail(QUIK_ERR_UNSUPPORTED, "quik_matmul: row wider than 128 KiB (register-resident quantizer limit)");
   if (ctx->device != L->device) return fail(QUIK_ERR_INVALID_ARGUMENT, "context and layer live on different devices");
   return guarded([&] {
     DeviceGuard g(ctx->device);
@@ -494,10 +522,12 @@ quik_status quik_linear_forward_strided(quik_ctx_t ctx, quik_layer_t L, const vo
     const int64_t N = L->out_features;
     if (variant == QUIK_V3_FUSED_EPILOGUE) {
       run_k1(ctx, L, x, xdt, M, st);
+      if (mid_event) QK_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(mid_event), st));
       GemmArgs gm = gemm_args(ctx, L, M);
       gm.out = y;
       gm.ldo = ldy;
       gm.mode = ydt == QUIK_F16 ? kModeF16 : kModeF32;
+      if (g_probe_mode) gm.mode = kModeProbe;
       run_gemm(ctx, gm, st);
       return QUIK_OK;
     }
@@ -505,14 +535,7 @@ quik_status quik_linear_forward_strided(quik_ctx_t ctx, quik_layer_t L, const vo
       // split (runtime.cpp:169-186) then unfused quantisation of the base matrix (:188-197):
       // the split is K1 in "copy" form writing f32 base/outlier columns, then K1 again
       // over the base matrix with the identity permutation.
-      float* xb32 = static_cast<float*>(ctx->xbase.ensure(static_cast<size_t>(M * std::max<int64_t>(L->kb, 1) * 4 +
-                                                                              std::max<int64_t>(L->kb, 1) * 4)));
-      int32_t* ident = reinterpret_cast<int32_t*>(xb32 + M * std::max<int64_t>(L->kb, 1));
-      {
-        std::vector<int32_t> h(static_cast<size_t>(L->kb));
-        for (int64_t i = 0; i < L->kb; ++i) h[i] = static_cast<int32_t>(i);
-        if (L->kb) QK_CUDA(cudaMemcpy(ident, h.data(), L->kb * 4, cudaMemcpyHostToDevice));
-      }
+      float* xb32 = static_cast<float*>(ctx->xbase.ensure(static_cast<size_t>(M * std::max<int64_t>(L->kb, 1) * 4)));
       // split pass: gather base columns in permutation order as f32 (exact) and the
       // outliers as f16 GEMM operands.
       SplitArgs s{};
@@ -535,7 +558,6 @@ quik_status quik_linear_forward_strided(quik_ctx_t ctx, quik_layer_t L, const vo
       q.M = M;
       q.K = L->kb;
       q.ldx = L->kb;
-      q.base_src = ident;
       q.kb = L->kb;
       q.bits = L->bits;
       q.q8 = L->kpad ? static_cast<int8_t*>(ctx->q8.ensure(static_cast<size_t>(M * L->kpad))) : nullptr;
@@ -569,6 +591,47 @@ quik_status quik_linear_forward_strided(quik_ctx_t ctx, quik_layer_t L, const vo
     } else {
       return fail(QUIK_ERR_UNSUPPORTED, "V1/V2 variants support dense outputs only");
     }
+    return QUIK_OK;
+  });
+}
+
+quik_status quik_linear_forward_strided(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M,
+                                        void* y, quik_dtype ydt, int64_t ldy, quik_variant variant, void* stream) {
+  return quik_linear_forward_ex(ctx, L, x, xdt, M, y, ydt, ldy, variant, stream, nullptr);
+}
+
+quik_status quik_rtn_quantize_weights(quik_ctx_t ctx, const float* w, int64_t N, int64_t K,
+                                      const int64_t* outlier_indices, int64_t n_outlier, int bits, uint8_t* base,
+                                      float* scales, float* wreduced, float* outlier_weights, void* stream) {
+  if (!ctx) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context");
+  if (bits != 4 && bits != 8) return fail(QUIK_ERR_INVALID_ARGUMENT, "weight bits must be 4 or 8");
+  if (N < 0 || K < 0 || n_outlier < 0 || n_outlier > K)
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "rtn_quantize_weights: bad dimensions");
+  if (n_outlier > 0 && !outlier_indices) return fail(QUIK_ERR_INVALID_ARGUMENT, "outlier indices missing");
+  for (int64_t i = 0; i < n_outlier; ++i) {
+    const int64_t v = outlier_indices[i];
+    if (v < 0 || v >= K)
+      return fail(QUIK_ERR_INVALID_ARGUMENT, "OutlierSet: index " + std::to_string(v) + " outside feature range");
+    if (i > 0 && v <= outlier_indices[i - 1])
+      return fail(QUIK_ERR_INVALID_ARGUMENT, "OutlierSet: indices must be sorted and unique");
+  }
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = as_stream(stream);
+    const int64_t kb = K - n_outlier;
+    std::vector<int32_t> tab(static_cast<size_t>(K));
+    std::vector<char> is_out(static_cast<size_t>(K), 0);
+    for (int64_t i = 0; i < n_outlier; ++i) is_out[outlier_indices[i]] = 1;
+    int64_t p = 0;
+    for (int64_t f = 0; f < K; ++f)
+      if (!is_out[f]) tab[p++] = static_cast<int32_t>(f);
+    for (int64_t i = 0; i < n_outlier; ++i) tab[p++] = static_cast<int32_t>(outlier_indices[i]);
+    int32_t* dtab = static_cast<int32_t*>(ctx->xbase.ensure(static_cast<size_t>(std::max<int64_t>(K, 1) * 4)));
+    if (K) QK_CUDA(cudaMemcpyAsync(dtab, tab.data(), K * 4, cudaMemcpyHostToDevice, st));
+    check_launch(launch_rtn_weights(w, N, K, dtab, kb, dtab + kb, n_outlier, bits, base, scales, wreduced,
+                                    outlier_weights, st),
+                 "rtn weight kernel");
+    QK_CUDA(cudaStreamSynchronize(st));  // tab must outlive the copy
     return QUIK_OK;
   });
 }

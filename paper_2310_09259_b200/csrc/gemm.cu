@@ -4,17 +4,24 @@
 //   acc[n][t] = sum_k W8[n][k] * X8[t][k]                  (tcgen05 kind::i8, exact int32 in TMEM)
 //   f[n][t]   = sum_o Wo[n][o] * Xo[t][o]                  (tcgen05 kind::f16, f32 in TMEM)
 //   y[t][n]   = (bias[n] + f) + dequant_element(acc, ...)  (epilogue, runtime.cpp:70-77)
-// "Swap-AB" orientation: weight rows are the UMMA M dimension (128 per tile),
-// tokens are the UMMA N dimension (BN per tile), so small token counts use
-// narrow N tiles instead of padding 128-row MMAs.
+// "Swap-AB" orientation: weight rows are the UMMA M dimension, tokens are the
+// UMMA N dimension (BN per tile), so small token counts use narrow N tiles
+// instead of padding 128-row MMAs.
+//
+// CG = 2 (large M): a CTA pair (cluster of 2) runs tcgen05.mma.cta_group::2 with
+// M = 256: each CTA stages its own 128 weight rows and half of the BN token rows,
+// halving shared-memory operand traffic per SM (the 1-CTA 128x128 tile is
+// SMEM-bandwidth bound: 8 KB of operands per 64-cycle MMA). The leader CTA issues
+// the MMAs; both CTAs' TMA loads complete on the leader's full barrier; MMA
+// commits are multicast to both CTAs.
 //
 // Warp roles (256 threads, 1 CTA per SM, persistent over tiles):
 //   warp 0      TMA producer (one elected lane)
-//   warp 1      MMA issuer  (one elected lane)
+//   warp 1      MMA issuer  (one lane, leader CTA only)
 //   warp 2      TMEM allocator
 //   warps 4..7  epilogue: TMEM -> registers -> dequant -> global
-// Pipelines: smem ring (full/empty mbarriers, TMA <-> MMA) and a double-buffered
-// TMEM accumulator (tmem_full/tmem_empty, MMA <-> epilogue).
+// Pipelines: smem ring (full/empty mbarriers, TMA <-> MMA) and a TMEM
+// accumulator ring (tmem_full/tmem_empty, MMA <-> epilogue).
 #include <cudaTypedefs.h>
 
 #include <mutex>
@@ -26,15 +33,21 @@ namespace quikb200 {
 
 namespace {
 
-constexpr int kThreads = 256;
 constexpr int kEpiWarp0 = 4;
+constexpr int kEpiWarps = 8;  // 2 per SM sub-partition: each TMEM lane quadrant split in column halves
+constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
+constexpr int kChunk = 32;                                 // tokens per epilogue step
+constexpr int kStoreBufBytes = kChunk * 32 * 2;            // [32 tokens][32 features] f16
+constexpr int kStagingBytes = kEpiWarps * 2 * kStoreBufBytes;  // double-buffered per warp
 
-template <int BN>
+template <int CG, int BN>
 struct Cfg {
-  static constexpr int kABytes = kBlockM * kKBlockBytes;  // 16 KB
-  static constexpr int kBBytes = BN * kKBlockBytes;
+  static constexpr int kBRows = BN / CG;                  // token rows staged per CTA
+  static constexpr int kABytes = kBlockM * kKBlockBytes;  // 16 KB: 128 weight rows per CTA
+  static constexpr int kBBytes = kBRows * kKBlockBytes;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (200 * 1024 / kStageBytes) > 8 ? 8 : (200 * 1024 / kStageBytes);
+  static constexpr int kBudget = 227 * 1024 - 1024 - kStagingBytes - 256;
+  static constexpr int kStages = (kBudget / kStageBytes) > 8 ? 8 : (kBudget / kStageBytes);
   // Per accumulator buffer: BN int32 columns + BN f32 columns.
   static constexpr int kAccCols = 2 * BN;
   static constexpr int kAccBufs = (2 * kAccCols <= 512) ? 2 : 1;
@@ -42,14 +55,17 @@ struct Cfg {
   static constexpr int kTmemCols =
       kTmemColsRaw <= 32 ? 32 : kTmemColsRaw <= 64 ? 64 : kTmemColsRaw <= 128 ? 128 : kTmemColsRaw <= 256 ? 256 : 512;
   static constexpr int kBarBytes = (2 * kStages + 2 * kAccBufs) * 8 + 16;
-  static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kBarBytes;
+  static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kStagingBytes + kBarBytes;
+  static constexpr int kTileRows = kBlockM * CG;          // weight rows per (cluster) tile
 };
 
 struct KParams {
   CUtensorMap tm_w;   // int8 [N][kpad], box {128 B, 128 rows}
-  CUtensorMap tm_x;   // int8 [M][kpad], box {128 B, BN rows}
+  CUtensorMap tm_x;   // int8 [M][kpad], box {128 B, BN/CG rows}
   CUtensorMap tm_wo;  // f16 [N][opad], box {64, 128}
-  CUtensorMap tm_xo;  // f16 [M][opad], box {64, BN}
+  CUtensorMap tm_xo;  // f16 [M][opad], box {64, BN/CG}
+  CUtensorMap tm_y;   // f16 [M][ldo] output, box {32 features, 32 tokens} (valid when tma_store)
+  int tma_store;
   int M, N;
   int kb_int, kb_out;
   const float* w_scale;
@@ -62,12 +78,13 @@ struct KParams {
   long long ldo;
 };
 
-template <int BN, int MODE>
+template <int CG, int BN, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_constant__ KParams p) {
-  using C = Cfg<BN>;
+  using C = Cfg<CG, BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint8_t* staging = smem + C::kStages * C::kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + kStagingBytes);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + C::kAccBufs;
@@ -75,6 +92,8 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
 
   if (warp == 0 && lane == 0) {
     if (p.kb_int) { tma_prefetch(&p.tm_w); tma_prefetch(&p.tm_x); }
@@ -82,20 +101,22 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
   }
   if (warp == 1 && lane == 0) {
     for (int i = 0; i < C::kStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < C::kAccBufs; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    for (int i = 0; i < C::kAccBufs; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], kEpiWarps * CG); }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, C::kTmemCols);
+  if (warp == 2) tmem_alloc<CG>(tmem_slot, C::kTmemCols);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   const int tiles_m = (p.M + BN - 1) / BN;
-  const int tiles_n = (p.N + kBlockM - 1) / kBlockM;
+  const int tiles_n = (p.N + C::kTileRows - 1) / C::kTileRows;
   const int num_tiles = tiles_m * tiles_n;
-  // Tile order: consecutive tile ids share the weight block (n) so the CTAs that
-  // run concurrently read the same 128 weight rows through L2.
+  const int cluster_id = blockIdx.x / CG;
+  const int num_clusters = gridDim.x / CG;
+  // Tile order: consecutive tile ids share the weight block (n) so the clusters
+  // that run concurrently read the same weight rows through L2.
   const int kb_total = p.kb_int + p.kb_out;
 
   if (warp == 0) {
@@ -104,34 +125,39 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
       const uint64_t pol_x = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         const int nb = tile / tiles_m, mb = tile % tiles_m;
+        const int wrow = nb * C::kTileRows + static_cast<int>(rank) * kBlockM;
+        const int trow = mb * BN + static_cast<int>(rank) * C::kBRows;
         for (int kb = 0; kb < kb_total; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::kStageBytes;
           uint8_t* sb = sa + C::kABytes;
-          mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-          if (kb < p.kb_int) {
-            tma_load_2d(sa, &p.tm_w, kb * kKBlockBytes, nb * kBlockM, &full[stage], pol_w);
-            tma_load_2d(sb, &p.tm_x, kb * kKBlockBytes, mb * BN, &full[stage], pol_x);
+          if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::kStageBytes);
+          const bool is_int = kb < p.kb_int;
+          const CUtensorMap* ma = is_int ? &p.tm_w : &p.tm_wo;
+          const CUtensorMap* mx = is_int ? &p.tm_x : &p.tm_xo;
+          const int kc = is_int ? kb * kKBlockBytes : (kb - p.kb_int) * 64;
+          if constexpr (CG == 1) {
+            tma_load_2d(sa, ma, kc, wrow, &full[stage], pol_w);
+            tma_load_2d(sb, mx, kc, trow, &full[stage], pol_x);
           } else {
-            const int ko = (kb - p.kb_int) * 64;
-            tma_load_2d(sa, &p.tm_wo, ko, nb * kBlockM, &full[stage], pol_w);
-            tma_load_2d(sb, &p.tm_xo, ko, mb * BN, &full[stage], pol_x);
+            tma_load_2d_pair(sa, ma, kc, wrow, &full[stage], pol_w);
+            tma_load_2d_pair(sb, mx, kc, trow, &full[stage], pol_x);
           }
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t id_i8 = idesc_make(2u, 1u, kBlockM, BN);
-      constexpr uint32_t id_f16 = idesc_make(1u, 0u, kBlockM, BN);
+    if (lane == 0 && leader) {
+      constexpr uint32_t id_i8 = idesc_make(2u, 1u, kBlockM * CG, BN);
+      constexpr uint32_t id_f16 = idesc_make(1u, 0u, kBlockM * CG, BN);
       int stage = 0;
       uint32_t phase = 0;
       int abuf = 0;
       uint32_t aphase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         mbar_wait(&tempty[abuf], aphase ^ 1);
         tc_fence_after();
         const uint32_t d_int = tmem_base + abuf * C::kAccCols;
@@ -146,30 +172,41 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
           if (kb < p.kb_int) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)  // 4 x K=32 int8 = 128 bytes
-              mma_i8(d_int, adesc + 2 * k, bdesc + 2 * k, id_i8, (kb | k) != 0);
+              mma_i8<CG>(d_int, adesc + 2 * k, bdesc + 2 * k, id_i8, (kb | k) != 0);
           } else {
             const int ko = kb - p.kb_int;
 #pragma unroll
             for (int k = 0; k < 4; ++k)  // 4 x K=16 f16 = 128 bytes
-              mma_f16(d_f32, adesc + 2 * k, bdesc + 2 * k, id_f16, (ko | k) != 0);
+              mma_f16<CG>(d_f32, adesc + 2 * k, bdesc + 2 * k, id_f16, (ko | k) != 0);
           }
-          mma_commit(&empty[stage]);
+          mma_commit<CG>(&empty[stage]);
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull[abuf]);
+        mma_commit<CG>(&tfull[abuf]);
         if (C::kAccBufs == 2) { abuf ^= 1; if (abuf == 0) aphase ^= 1; } else { aphase ^= 1; }
       }
     }
   } else if (warp >= kEpiWarp0) {
-    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    // Epilogue warp e: TMEM lane quadrant q = warp % 4 (hardware rule: a warp may
+    // only access lanes 32*(warp%4) .. +31), column half h.
+    const int e = warp - kEpiWarp0;
+    const int q = warp & 3;
+    const int h = e >> 2;
+    constexpr int kHalf = BN / 2 < kChunk ? kChunk : BN / 2;  // columns per half (BN >= 32)
+    const int c_begin = h * kHalf;
+    const int c_end = (c_begin + kHalf) < BN ? (c_begin + kHalf) : BN;
     const int row = q * 32 + lane;
+    uint8_t* my_stage = staging + e * 2 * kStoreBufBytes;
+    int sbuf = 0;
     int abuf = 0;
     uint32_t aphase = 0;
     const bool has_int = p.kb_int > 0;
     const bool has_out = p.kb_out > 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    const bool tma_out = MODE == kModeF16 && p.tma_store;
+    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
       const int nb = tile / tiles_m, mb = tile % tiles_m;
-      const int n = nb * kBlockM + row;
+      const int n0 = nb * C::kTileRows + static_cast<int>(rank) * kBlockM + q * 32;  // warp's first feature
+      const int n = n0 + lane;
       const bool n_ok = n < p.N;
       float sw = 0.f, wr = 0.f, bs = 0.f;
       if (n_ok) {
@@ -181,7 +218,45 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
       const uint32_t t_int = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + abuf * C::kAccCols;
       const uint32_t t_f32 = t_int + BN;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = c_begin; c < c_end; c += kChunk) {
+        if (tma_out) {
+          // ---- fast path: dequant 32 tokens x 32 features, stage in smem, TMA store
+          uint32_t vi[32], vf[32];
+          if (has_int) tmem_ld32(t_int + c, vi);
+          if (has_out) tmem_ld32(t_f32 + c, vf);
+          // per-token scale / shift: lane j holds token t0+j (broadcast by shuffles)
+          const int t_l = mb * BN + c + lane;
+          const float sa_l = t_l < p.M ? __ldg(&p.a_scale[t_l]) : 0.f;
+          const float za_l = t_l < p.M ? __ldg(&p.a_zero[t_l]) : 0.f;
+          const float zs_l = __fadd_rn(za_l, __fmul_rn(p.half_range, sa_l));  // runtime.cpp:74
+          tmem_ld_wait();
+          if (!has_int) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) vi[j] = 0u;
+          }
+          __half* buf = reinterpret_cast<__half*>(my_stage + sbuf * kStoreBufBytes);
+          if (lane == 0) bulk_wait_read<1>();  // the store issued from this buffer 2 chunks ago has read it
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float sa = __shfl_sync(0xffffffffu, sa_l, j);
+            const float zs = __shfl_sync(0xffffffffu, zs_l, j);
+            float o = bs;
+            if (has_out) o = __fadd_rn(o, __uint_as_float(vf[j]));
+            float v = __fmul_rn(__int2float_rn(static_cast<int32_t>(vi[j])), sa);
+            v = __fmul_rn(v, sw);
+            o = __fadd_rn(o, __fadd_rn(v, __fmul_rn(zs, wr)));  // runtime.cpp:70-77, :298-299
+            buf[j * 32 + lane] = __float2half_rn(o);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&p.tm_y, buf, n0, mb * BN + c);
+            bulk_commit();
+          }
+          sbuf ^= 1;
+          continue;
+        }
         uint32_t vi[32], vf[32];
         if (MODE != kModeOutlierF32) {
           if (has_int) tmem_ld32(t_int + c, vi);
@@ -198,6 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
           }
         }
         tmem_ld_wait();
+        if constexpr (MODE == kModeProbe) continue;
         const int t0 = mb * BN + c;
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -229,16 +305,20 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[abuf]);
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster(&tempty[abuf], 0);
+        else mbar_arrive(&tempty[abuf]);
+      }
       if (C::kAccBufs == 2) { abuf ^= 1; if (abuf == 0) aphase ^= 1; } else { aphase ^= 1; }
     }
+    if (lane == 0) bulk_wait_all();
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, C::kTmemCols);
+    tmem_dealloc<CG>(tmem_base, C::kTmemCols);
   }
 }
 
@@ -273,39 +353,58 @@ bool make_map(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int elem
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, int MODE>
-cudaError_t launch_bn_mode(const KParams& kp, int num_sms, cudaStream_t stream) {
-  using C = Cfg<BN>;
-  auto kern = quik_gemm_kernel<BN, MODE>;
+template <int CG, int BN, int MODE>
+cudaError_t launch_cfg(const KParams& kp, int num_sms, cudaStream_t stream) {
+  using C = Cfg<CG, BN>;
+  auto kern = quik_gemm_kernel<CG, BN, MODE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
   if (e != cudaSuccess) return e;
-  const int tiles = static_cast<int>(((kp.M + BN - 1) / BN) * ((kp.N + kBlockM - 1) / kBlockM));
-  const int grid = tiles < num_sms ? tiles : num_sms;
-  if (grid <= 0) return cudaSuccess;
-  kern<<<grid, kThreads, C::kSmemBytes, stream>>>(kp);
-  return cudaGetLastError();
+  const long long tiles = static_cast<long long>((kp.M + BN - 1) / BN) * ((kp.N + C::kTileRows - 1) / C::kTileRows);
+  const int max_clusters = num_sms / CG;
+  const int clusters = static_cast<int>(tiles < max_clusters ? tiles : max_clusters);
+  if (clusters <= 0) return cudaSuccess;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(clusters * CG);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, kp);
 }
 
-template <int BN>
-cudaError_t launch_bn(const KParams& kp, int mode, int num_sms, cudaStream_t stream) {
+template <int CG, int BN>
+cudaError_t launch_mode(const KParams& kp, int mode, int num_sms, cudaStream_t stream) {
   switch (mode) {
-    case kModeInt32: return launch_bn_mode<BN, kModeInt32>(kp, num_sms, stream);
-    case kModeOutlierF32: return launch_bn_mode<BN, kModeOutlierF32>(kp, num_sms, stream);
-    case kModeF32: return launch_bn_mode<BN, kModeF32>(kp, num_sms, stream);
-    default: return launch_bn_mode<BN, kModeF16>(kp, num_sms, stream);
+    case kModeInt32: return launch_cfg<CG, BN, kModeInt32>(kp, num_sms, stream);
+    case kModeOutlierF32: return launch_cfg<CG, BN, kModeOutlierF32>(kp, num_sms, stream);
+    case kModeF32: return launch_cfg<CG, BN, kModeF32>(kp, num_sms, stream);
+    case kModeProbe: return launch_cfg<CG, BN, kModeProbe>(kp, num_sms, stream);
+    default: return launch_cfg<CG, BN, kModeF16>(kp, num_sms, stream);
   }
 }
 
 }  // namespace
 
+int gemm_tile_override = 0;  // debug/tuning: 0 = heuristic, else (CG << 16) | BN
+
 cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream, const char** err_msg) {
   *err_msg = nullptr;
   if (a.M == 0 || a.N == 0) return cudaSuccess;
   if (!get_encoder()) { *err_msg = "cuTensorMapEncodeTiled unavailable"; return cudaErrorNotSupported; }
-  // Token tile: the narrowest legal UMMA N that covers M (<=128), else 128.
-  int bn = 128;
+  // Token tile: narrow UMMA N for small M (memory-bound weight streaming, 1-CTA);
+  // CTA-pair M = 256 tiles once the token count makes the GEMM compute-bound.
+  int cg = 1, bn = 128;
   if (a.M <= 32) bn = 32;
   else if (a.M <= 64) bn = 64;
+  else if (a.M <= 128) bn = 128;
+  else { cg = 2; bn = 256; }
+  if (gemm_tile_override) { cg = gemm_tile_override >> 16; bn = gemm_tile_override & 0xFFFF; }
 
   KParams kp{};
   kp.M = static_cast<int>(a.M);
@@ -314,19 +413,30 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
   kp.kb_out = static_cast<int>(a.opad / 64);
   if (a.mode == kModeInt32) kp.kb_out = 0;
   if (a.mode == kModeOutlierF32) kp.kb_int = 0;
+  const uint32_t brows = static_cast<uint32_t>(bn / cg);
   if (kp.kb_int) {
     if (!make_map(&kp.tm_w, a.w, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, a.kpad, a.N, a.kpad, kBlockM) ||
-        !make_map(&kp.tm_x, a.x, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, a.kpad, a.M, a.kpad, bn)) {
+        !make_map(&kp.tm_x, a.x, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, a.kpad, a.M, a.kpad, brows)) {
       *err_msg = "tensor map encode failed (int8 operands)";
       return cudaErrorInvalidValue;
     }
   }
   if (kp.kb_out) {
     if (!make_map(&kp.tm_wo, a.wo, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.opad, a.N, a.opad * 2, kBlockM) ||
-        !make_map(&kp.tm_xo, a.xo, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.opad, a.M, a.opad * 2, bn)) {
+        !make_map(&kp.tm_xo, a.xo, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.opad, a.M, a.opad * 2, brows)) {
       *err_msg = "tensor map encode failed (outlier operands)";
       return cudaErrorInvalidValue;
     }
+  }
+  kp.tma_store = 0;
+  if (a.mode == kModeF16 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 && (a.ldo * 2) % 16 == 0) {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.N), static_cast<cuuint64_t>(a.M)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.ldo * 2)};
+    cuuint32_t box[2] = {32, static_cast<cuuint32_t>(kChunk)};
+    cuuint32_t estr[2] = {1, 1};
+    kp.tma_store = g_encode(&kp.tm_y, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.out, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
   kp.w_scale = a.w_scale;
   kp.wreduced = a.wreduced;
@@ -336,10 +446,14 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
   kp.half_range = a.half_range;
   kp.out = a.out;
   kp.ldo = a.ldo;
-  switch (bn) {
-    case 32: return launch_bn<32>(kp, a.mode, num_sms, stream);
-    case 64: return launch_bn<64>(kp, a.mode, num_sms, stream);
-    default: return launch_bn<128>(kp, a.mode, num_sms, stream);
+  const int key = (cg << 16) | bn;
+  switch (key) {
+    case (1 << 16) | 32: return launch_mode<1, 32>(kp, a.mode, num_sms, stream);
+    case (1 << 16) | 64: return launch_mode<1, 64>(kp, a.mode, num_sms, stream);
+    case (1 << 16) | 128: return launch_mode<1, 128>(kp, a.mode, num_sms, stream);
+    case (2 << 16) | 128: return launch_mode<2, 128>(kp, a.mode, num_sms, stream);
+    case (2 << 16) | 256: return launch_mode<2, 256>(kp, a.mode, num_sms, stream);
+    default: *err_msg = "unsupported tile configuration"; return cudaErrorInvalidValue;
   }
 }
 

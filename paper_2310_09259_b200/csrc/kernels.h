@@ -21,6 +21,7 @@ enum GemmMode : int {
   kModeOutlierF32 = 1,  // out f32: bias + x_out . W_out^T (V1/V2 outlier pass)
   kModeF32 = 2,         // out f32: (bias + outlier) + dequant(acc)   (fused V3)
   kModeF16 = 3,         // out f16: same as kModeF32 rounded to half  (hot path)
+  kModeProbe = 4,       // diagnostics: mainloop + TMEM drain, no global stores
 };
 
 struct GemmArgs {
@@ -48,6 +49,7 @@ struct GemmArgs {
 // Launches the fused persistent tcgen05 kernel (int8 GEMM + f16 outlier GEMM +
 // dequantisation epilogue). Returns a cudaError_t / CUresult-derived status in
 // *err_msg on failure.
+extern int gemm_tile_override;  // (cta_group << 16) | block_n, 0 = heuristic
 cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream, const char** err_msg);
 
 // K1: fused split + per-token asymmetric quantisation (runtime.cpp:36-66,
@@ -56,9 +58,17 @@ struct QuantArgs {
   const void* x;
   int x_is_f32;
   int64_t M, K, ldx;
-  const int32_t* base_src;  // [kb] source column of base position j (permutation[j])
+  // Outlier map (calibration.cpp:69-91, permutation = non-outliers ascending then
+  // outliers), as per-layer tables (K <= 65520):
+  //   lane_mask [round_up(K, 16)] bytes: 0xFF = outlier column, 0 = base
+  //   gather    [kpad] u16: source column of base position j; j >= kb -> round_up(K, 16)
+  //             (a zero code slot)
+  //   out_src   [n_out] i32: outlier columns ascending
+  // lane_mask == nullptr: no outliers (identity permutation, gather unused).
+  const uint8_t* lane_mask;
+  const uint16_t* gather;
+  const int32_t* out_src;
   int64_t kb;               // base column count K_b
-  const int32_t* out_src;   // [n_out] outlier source columns, ascending
   int64_t n_out;
   int bits;                 // 4 or 8
   int8_t* q8;               // GEMM layout [M][kpad] or nullptr
@@ -96,6 +106,12 @@ cudaError_t launch_unpack_to_gemm(const uint8_t* packed, int64_t rows, int64_t c
 // f32 [rows][cols] -> f16 [rows][pitch], zero padded.
 cudaError_t launch_f32_to_f16_padded(const float* src, int64_t rows, int64_t cols, __half* dst,
                                      int64_t pitch, cudaStream_t stream);
+
+// rtn_quantize_weights (quantizer.cpp:339-371): f32 W [N][K] (device) -> ABI
+// packed base [N][row_bytes(kb)], scales, wreduced, outlier weights [N][n_out].
+cudaError_t launch_rtn_weights(const float* w, int64_t N, int64_t K, const int32_t* base_src, int64_t kb,
+                               const int32_t* out_src, int64_t n_out, int bits, uint8_t* base, float* scales,
+                               float* wreduced, float* outlier_w, cudaStream_t stream);
 
 // dequantize_epilogue (runtime.cpp:222-244): out[t][r] = dequant_element(...).
 cudaError_t launch_dequant(const int32_t* acc, int64_t M, int64_t N, const float* a_scale,

@@ -18,150 +18,375 @@ namespace quikb200 {
 
 namespace {
 
-constexpr int kQThreads = 256;
-constexpr int kGroup = 16;  // base positions per thread per step (one 16-byte int8 store)
+__device__ __forceinline__ float to_float(__half v) { return __half2float(v); }
+__device__ __forceinline__ float to_float(float v) { return v; }
 
 template <typename T>
-__device__ __forceinline__ float to_f32(T v);
-template <>
-__device__ __forceinline__ float to_f32<__half>(__half v) { return __half2float(v); }
-template <>
-__device__ __forceinline__ float to_f32<float>(float v) { return v; }
-
-struct MinMax {
-  float vmin, vmax;
-  int imin, imax;  // column index of the extremum (first-seen tie-break)
-  int nonfinite;
-};
-
-// Combines two partial reductions; on equal values the lower column index wins,
-// which reproduces the sequential "first element seeds, strict < / >" scan.
-__device__ __forceinline__ void mm_combine(MinMax& a, float vmin, int imin, float vmax, int imax, int nf) {
-  if (vmin < a.vmin || (vmin == a.vmin && imin < a.imin)) { a.vmin = vmin; a.imin = imin; }
-  if (vmax > a.vmax || (vmax == a.vmax && imax < a.imax)) { a.vmax = vmax; a.imax = imax; }
-  a.nonfinite |= nf;
+__device__ __forceinline__ float elem(const uint4& v, int e) {
+  if constexpr (sizeof(T) == 2) {
+    const uint32_t w = (&v.x)[e >> 1];
+    const uint16_t h = (e & 1) ? static_cast<uint16_t>(w >> 16) : static_cast<uint16_t>(w & 0xFFFF);
+    return __half2float(__ushort_as_half(h));
+  } else {
+    return __uint_as_float((&v.x)[e]);
+  }
 }
 
-// One CTA per token row. The row is staged in shared memory with 16-byte loads;
-// base positions are processed 16 at a time per thread (perm gather from smem).
-template <typename T, int BITS>
-__global__ void __launch_bounds__(kQThreads) quantize_rows_kernel(const QuantArgs a) {
-  extern __shared__ __align__(16) uint8_t smem_q[];
-  T* row = reinterpret_cast<T*>(smem_q);
-  __shared__ MinMax red[kQThreads / 32];
-  __shared__ float s_scale, s_zero;
+// Exact lround((x - vmin) / scale) for the quantizer (runtime.cpp:58) without an
+// IEEE division per element. With d = fl(x - vmin) >= 0, r = fl(1/scale),
+// qa = fl(d * r) and u = fl(qa + 0.5):
+//   |qa - fl(d / scale)| <= (d/scale) * 3.0001 * 2^-24 <= 4.6e-5 (d/scale <= 256),
+//   |u - (fl(d/scale) + 0.5)| <= 6.1e-5.
+// lround(q) = floor(q + 0.5) for q >= 0 changes value only at integers of u, so
+// whenever frac(u) is farther than 2^-12 from 0 and 1, floor(u) is exact; the
+// other elements (about 5e-4 of them; exact .5 ties among them) take the IEEE
+// quotient, rounded half away from zero. Bit-identical to the reference.
+__device__ __forceinline__ float quant_slow(float d, float scale) { return round_half_away(__fdiv_rn(d, scale)); }
+constexpr float kNearTie = 0.5f - 2.44140625e-4f;
 
-  const int64_t t = blockIdx.x;
-  const T* src = reinterpret_cast<const T*>(a.x) + t * a.ldx;
+__device__ __forceinline__ unsigned long long f32x2_pack(float lo, float hi) {
+  return (static_cast<unsigned long long>(__float_as_uint(hi)) << 32) | __float_as_uint(lo);
+}
+__device__ __forceinline__ void f32x2_unpack(unsigned long long v, float& lo, float& hi) {
+  lo = __uint_as_float(static_cast<uint32_t>(v));
+  hi = __uint_as_float(static_cast<uint32_t>(v >> 32));
+}
+// (x - vmin) * rcp for two lanes at once (FADD2 / FMUL2, IEEE round-to-nearest).
+__device__ __forceinline__ void sub_mul_x2(float x0, float x1, unsigned long long vmin2, unsigned long long rcp2,
+                                           float& d0, float& d1, float& q0, float& q1) {
+  unsigned long long d, qa;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f32x2_pack(x0, x1)), "l"(vmin2));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(qa) : "l"(d), "l"(rcp2));
+  f32x2_unpack(d, d0, d1);
+  f32x2_unpack(qa, q0, q1);
+}
+
+__device__ __forceinline__ __half2 u2h2(uint32_t u) {
+  __half2 h;
+  memcpy(&h, &u, 4);
+  return h;
+}
+__device__ __forceinline__ uint32_t h22u(__half2 h) {
+  uint32_t u;
+  memcpy(&u, &h, 4);
+  return u;
+}
+
+// One CTA per token row (the row held in registers, VPT 16-byte vectors per
+// thread, read once from HBM with coalesced 128-bit loads):
+//   pass 1  min / max over the base columns: packed half2 (or f32) min/max with
+//           outlier lanes neutralised by the per-layer byte lane mask; NaN
+//           propagates (flagged as NumericalError);
+//   pass 2  codes for every column in registers (exact reciprocal fast path),
+//           written UNCOMPACTED to shared memory with one 8-byte store per vector;
+//   copy    base position j <- column gather[j] (per-layer u16 table): 16 codes per
+//           thread gathered from shared memory, one 16-byte store to HBM;
+//   outliers gathered from the shared-memory row copy into their f16 slots.
+//
+// min/max tie semantics (runtime.cpp:40-51: first element seeds, strict < / >):
+// the extrema VALUES are order independent except for the sign of a zero
+// minimum, which is resolved exactly: when the row minimum compares equal to 0
+// the sign of the lowest-index zero wins (only the sign of vmin reaches an
+// output; vmax's sign cannot change range = vmax - vmin).
+template <typename T, int BITS, int VPT>
+__global__ void __launch_bounds__(512) quantize_rows_kernel(const QuantArgs a) {
+  extern __shared__ __align__(16) uint8_t s_dyn[];
+  __shared__ float s_min[16], s_max[16];
+  __shared__ int s_nf[16];
+  __shared__ unsigned s_key[16];
+  constexpr int E = 16 / sizeof(T);  // elements per 16-byte vector (8 f16 / 4 f32)
+  constexpr int kHr = 1 << (BITS - 1);
+  constexpr float kLevels = static_cast<float>((1 << BITS) - 1);
+
+  const int t = blockIdx.x;
   const int tid = threadIdx.x;
+  const int nt = blockDim.x;
+  const int K = static_cast<int>(a.K);
+  const int nvec = (K + E - 1) / E;
+  const int kb = static_cast<int>(a.kb);
+  // shared: codes [round_up(K,16) + 16] (uncompacted, zero tail) | row copy [nvec * 16] (outlier gather)
+  const int code_bytes = ((K + 15) & ~15) + 16;
+  uint8_t* s_codes = s_dyn;
+  uint4* s_row = reinterpret_cast<uint4*>(s_dyn + code_bytes);
+  const T* src = reinterpret_cast<const T*>(a.x) + static_cast<int64_t>(t) * a.ldx;
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && (K % E == 0);
+  const bool has_out = a.lane_mask != nullptr;
 
-  // ---- stage the row (vectorised when 16-byte aligned)
-  constexpr int kVec = 16 / sizeof(T);
-  const bool vec_ok = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && (a.K % kVec == 0);
-  if (vec_ok) {
-    const uint4* s4 = reinterpret_cast<const uint4*>(src);
-    uint4* d4 = reinterpret_cast<uint4*>(row);
-    for (int64_t i = tid; i < a.K / kVec; i += kQThreads) d4[i] = __ldg(&s4[i]);
-  } else {
-    for (int64_t i = tid; i < a.K; i += kQThreads) row[i] = src[i];
+  uint4 raw[VPT];
+  uint32_t lm[VPT];  // lane-mask bytes of the vector's E columns (tail / beyond-row columns = 0xFF)
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int v = tid + i * nt;
+    raw[i] = make_uint4(0, 0, 0, 0);
+    lm[i] = 0xFFFFFFFFu;
+    if (E == 8) lm[i] = 0xFFFFFFFFu;  // E == 8: two words, see lm_hi
+    if (v < nvec) {
+      if (vec_ok) {
+        raw[i] = __ldg(reinterpret_cast<const uint4*>(src) + v);
+      } else {
+        T tmp[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) tmp[e] = (v * E + e < K) ? src[v * E + e] : T(0);
+        memcpy(&raw[i], tmp, 16);
+      }
+      s_row[v] = raw[i];
+    }
   }
-  __syncthreads();
-
-  // ---- pass 1: min / max over base columns (+ finiteness)
-  MinMax mm{FLT_MAX, -FLT_MAX, INT_MAX, INT_MAX, 0};
-  bool any = false;
-  for (int64_t j0 = static_cast<int64_t>(tid) * kGroup; j0 < a.kb; j0 += kQThreads * kGroup) {
-    const int jn = static_cast<int>(a.kb - j0 < kGroup ? a.kb - j0 : kGroup);
-    for (int u = 0; u < jn; ++u) {
-      const int c = __ldg(&a.base_src[j0 + u]);
-      const float v = to_f32<T>(row[c]);
-      if (!isfinite(v)) mm.nonfinite = 1;
-      if (!any) { mm.vmin = mm.vmax = v; mm.imin = mm.imax = c; any = true; }
-      else {
-        if (v < mm.vmin) { mm.vmin = v; mm.imin = c; }
-        if (v > mm.vmax) { mm.vmax = v; mm.imax = c; }
+  uint32_t lm_hi[VPT];  // bytes 4..7 of the lane mask (E == 8 only)
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int v = tid + i * nt;
+    lm_hi[i] = 0xFFFFFFFFu;
+    if (v < nvec) {
+      const int c0 = v * E;
+      if (has_out) {
+        if (E == 8) {
+          const uint2 m = __ldg(reinterpret_cast<const uint2*>(a.lane_mask + c0));
+          lm[i] = m.x;
+          lm_hi[i] = m.y;
+        } else {
+          lm[i] = __ldg(reinterpret_cast<const uint32_t*>(a.lane_mask + c0));
+        }
+      } else {
+        lm[i] = 0u;
+        lm_hi[i] = 0u;
+      }
+      if (c0 + E > K) {  // row tail: columns >= K excluded
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+          if (c0 + e >= K) {
+            if (e < 4) lm[i] |= 0xFFu << (8 * e);
+            else lm_hi[i] |= 0xFFu << (8 * (e - 4));
+          }
       }
     }
   }
-  // warp reduce
+
+  // ---- pass 1: min / max over base columns (NaN-propagating; +-inf caught by the
+  // final finiteness test)
+  float vmin, vmax;
+  int nonfinite;
+  if constexpr (sizeof(T) == 2) {
+    __half2 hmin = u2h2(0x7C007C00u), hmax = u2h2(0xFC00FC00u);
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const uint32_t x2 = (&raw[i].x)[w];
+        // widen mask bytes (2w, 2w+1) to 16-bit lanes
+        const uint32_t mword = w < 2 ? lm[i] : lm_hi[i];
+        const uint32_t m = __byte_perm(mword, 0u, (w & 1) ? 0x3322u : 0x1100u);
+        hmin = __hmin2_nan(hmin, u2h2((x2 & ~m) | (0x7C007C00u & m)));
+        hmax = __hmax2_nan(hmax, u2h2((x2 & ~m) | (0xFC00FC00u & m)));
+      }
+    }
+    const float2 fmn = __half22float2(hmin);
+    const float2 fmx = __half22float2(hmax);
+    // NaN propagates through the _nan min/max; +inf can only reach hmax and -inf
+    // only hmin (the lane sentinels are the opposite infinities)
+    nonfinite = isnan(fmn.x) || isnan(fmn.y) || isnan(fmx.x) || isnan(fmx.y) || fmx.x == INFINITY ||
+                fmx.y == INFINITY || fmn.x == -INFINITY || fmn.y == -INFINITY;
+    vmin = fminf(fmn.x, fmn.y);
+    vmax = fmaxf(fmx.x, fmx.y);
+  } else {
+    vmin = __int_as_float(0x7f800000);
+    vmax = -vmin;
+    nonfinite = 0;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const float x = __uint_as_float((&raw[i].x)[e]);
+        const bool base = ((lm[i] >> (8 * e)) & 0xFFu) == 0;
+        nonfinite |= base && !isfinite(x);
+        vmin = fminf(vmin, base ? x : vmin);
+        vmax = fmaxf(vmax, base ? x : vmax);
+      }
+    }
+  }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
-    const float vmin = __shfl_xor_sync(0xffffffffu, mm.vmin, off);
-    const float vmax = __shfl_xor_sync(0xffffffffu, mm.vmax, off);
-    const int imin = __shfl_xor_sync(0xffffffffu, mm.imin, off);
-    const int imax = __shfl_xor_sync(0xffffffffu, mm.imax, off);
-    const int nf = __shfl_xor_sync(0xffffffffu, mm.nonfinite, off);
-    mm_combine(mm, vmin, imin, vmax, imax, nf);
+    vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, off));
+    vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, off));
+    nonfinite |= __shfl_xor_sync(0xffffffffu, nonfinite, off);
   }
-  if ((tid & 31) == 0) red[tid >> 5] = mm;
+  if ((tid & 31) == 0) { s_min[tid >> 5] = vmin; s_max[tid >> 5] = vmax; s_nf[tid >> 5] = nonfinite; }
+  for (int j = ((K + 15) & ~15) + tid; j < code_bytes; j += nt) s_codes[j] = 0;  // zero pad (gather target)
   __syncthreads();
-  if (tid == 0) {
-    MinMax r = red[0];
-    for (int w = 1; w < kQThreads / 32; ++w) mm_combine(r, red[w].vmin, red[w].imin, red[w].vmax, red[w].imax, red[w].nonfinite);
-    if (r.nonfinite && a.err) atomicExch(a.err, 1);
-    // The seeded min/max hold the actual values of the winning columns
-    // (re-read so the sign of a zero extremum is the first-seen one).
-    float vmin = 0.f, vmax = 0.f;
-    if (a.kb > 0) { vmin = to_f32<T>(row[r.imin]); vmax = to_f32<T>(row[r.imax]); }
-    const float range = __fsub_rn(vmax, vmin);
-    constexpr float kLevels = static_cast<float>((1 << BITS) - 1);
-    const float scale = range == 0.0f ? 1.0f : __fdiv_rn(range, kLevels);
-    s_scale = scale;
-    s_zero = vmin;
-    a.scale[t] = scale;
-    a.zero[t] = vmin;
+  vmin = s_min[0];
+  vmax = s_max[0];
+  nonfinite = s_nf[0];
+  for (int w = 1; w < nt / 32; ++w) {
+    vmin = fminf(vmin, s_min[w]);
+    vmax = fmaxf(vmax, s_max[w]);
+    nonfinite |= s_nf[w];
   }
-  __syncthreads();
-  const float vmin = s_zero, scale = s_scale;
-  constexpr int kHr = 1 << (BITS - 1);
-
-  // ---- pass 2: quantise + pack
-  const int64_t kend = a.q8 ? a.kpad : a.kb;
-  uint8_t* prow = a.packed ? a.packed + t * (BITS == 4 ? (a.kb + 1) / 2 : a.kb) : nullptr;
-  for (int64_t j0 = static_cast<int64_t>(tid) * kGroup; j0 < kend; j0 += kQThreads * kGroup) {
-    int8_t code[kGroup];
+  if (kb == 0) { vmin = 0.f; vmax = 0.f; }
+  if (vmin == 0.0f && kb > 0) {
+    // rare: the sign of a zero minimum is the first-seen zero's (block-uniform branch)
+    unsigned key = 0xFFFFFFFFu;
+#pragma unroll 1
+    for (int i = 0; i < VPT; ++i) {
+      const int v = tid + i * nt;
+      if (v >= nvec) break;
+      uint4 rv = make_uint4(0, 0, 0, 0);
 #pragma unroll
-    for (int u = 0; u < kGroup; ++u) {
-      const int64_t j = j0 + u;
-      int s = 0;
-      if (j < a.kb) {
-        const float v = to_f32<T>(row[__ldg(&a.base_src[j])]);
-        const float qf = round_half_away(__fdiv_rn(__fsub_rn(v, vmin), scale));
-        int q = static_cast<int>(fminf(fmaxf(qf, -1.0e6f), 1.0e6f));  // NaN-safe bound; NaN rows are flagged
-        s = q - kHr;
-        s = s < -kHr ? -kHr : (s > kHr - 1 ? kHr - 1 : s);
-      }
-      code[u] = static_cast<int8_t>(s);
-    }
-    if (a.q8) {
-      uint4 v;
-      memcpy(&v, code, 16);
-      *reinterpret_cast<uint4*>(a.q8 + t * a.kpad + j0) = v;
-    }
-    if (prow) {
-      const int jn = static_cast<int>(a.kb - j0 < kGroup ? a.kb - j0 : kGroup);
-      if (BITS == 8) {
-        for (int u = 0; u < jn; ++u) prow[j0 + u] = static_cast<uint8_t>(code[u]);
-      } else {
-        // i4p: low nibble = even base index, stored + 8; pad nibble of odd rows = 0
-        for (int u = 0; u < jn; u += 2) {
-          const uint8_t lo = static_cast<uint8_t>(code[u] + 8) & 0xF;
-          const uint8_t hi = (u + 1 < jn) ? (static_cast<uint8_t>(code[u + 1] + 8) & 0xF) : 0;
-          prow[(j0 + u) / 2] = static_cast<uint8_t>(lo | (hi << 4));
+      for (int j = 0; j < VPT; ++j)
+        if (j == i) rv = raw[j];
+      uint32_t m0 = 0, m1 = 0;
+#pragma unroll
+      for (int j = 0; j < VPT; ++j)
+        if (j == i) { m0 = lm[j]; m1 = lm_hi[j]; }
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const float x = elem<T>(rv, e);
+        const uint32_t mbyte = ((e < 4 ? m0 : m1) >> (8 * (e & 3))) & 0xFFu;
+        if (mbyte == 0 && x == 0.0f) {
+          const unsigned k = (static_cast<unsigned>(v * E + e) << 1) | (__float_as_uint(x) >> 31);
+          key = k < key ? k : key;
         }
       }
     }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const unsigned o = __shfl_xor_sync(0xffffffffu, key, off);
+      key = o < key ? o : key;
+    }
+    __syncthreads();
+    if ((tid & 31) == 0) s_key[tid >> 5] = key;
+    __syncthreads();
+    key = s_key[0];
+    for (int w = 1; w < nt / 32; ++w) key = s_key[w] < key ? s_key[w] : key;
+    vmin = (key & 1u) ? -0.0f : 0.0f;
   }
+  const float range = __fsub_rn(vmax, vmin);
+  const float scale = range == 0.0f ? 1.0f : __fdiv_rn(range, kLevels);
+  const float rcp = __frcp_rn(scale);
+  if (tid == 0) {
+    if (nonfinite && a.err) atomicExch(a.err, 1);
+    a.scale[t] = scale;
+    a.zero[t] = vmin;
+  }
+  const unsigned long long vmin2 = f32x2_pack(vmin, vmin);
+  const unsigned long long rcp2 = f32x2_pack(rcp, rcp);
 
-  // ---- outlier gather (ascending index order, runtime.cpp:217)
-  if (a.xo16) {
-    for (int64_t i = tid; i < a.opad; i += kQThreads) {
-      const float v = i < a.n_out ? to_f32<T>(row[__ldg(&a.out_src[i])]) : 0.0f;
-      a.xo16[t * a.opad + i] = __float2half_rn(v);
+  // ---- pass 2: codes for every column (outlier lanes produce ignored codes)
+  uint32_t near_vec = 0;  // bit i: vector i has an element near a rounding boundary
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int v = tid + i * nt;
+    if (v >= nvec) continue;
+    bool near_any = false;
+    float x[E];
+    int code[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = elem<T>(raw[i], e);
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+      float d0, d1, q0, q1;
+      sub_mul_x2(x[e], x[e + 1], vmin2, rcp2, d0, d1, q0, q1);
+      const float u0 = __fadd_rn(q0, 0.5f), u1 = __fadd_rn(q1, 0.5f);
+      const float f0 = floorf(u0), f1 = floorf(u1);
+      near_any |= fabsf(__fsub_rn(__fsub_rn(u0, f0), 0.5f)) >= kNearTie;
+      near_any |= fabsf(__fsub_rn(__fsub_rn(u1, f1), 0.5f)) >= kNearTie;
+      code[e] = static_cast<int>(f0);
+      code[e + 1] = static_cast<int>(f1);
+    }
+    // codes are in [0, levels] for finite rows (no clamp needed: d >= 0 and
+    // qa <= levels * (1 + 2^-22)); pack as signed bytes (q - half_range)
+    uint32_t w0 = 0, w1 = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t b = static_cast<uint32_t>(code[e] - kHr) & 0xFFu;
+      if (e < 4) w0 |= b << (8 * e);
+      else w1 |= b << (8 * (e - 4));
+    }
+    if (E == 8) *reinterpret_cast<uint2*>(s_codes + v * E) = make_uint2(w0, w1);
+    else *reinterpret_cast<uint32_t*>(s_codes + v * E) = w0;
+    near_vec |= (near_any ? 1u : 0u) << i;
+  }
+  if (near_vec) {
+    // rare: elements within 2^-12 of a rounding boundary take the exact IEEE
+    // quotient (same d and u as above; this thread owns these code bytes)
+    const T* row = reinterpret_cast<const T*>(s_row);
+#pragma unroll 1
+    for (uint32_t nv = near_vec; nv; nv &= nv - 1) {
+      const int v = tid + (__ffs(nv) - 1) * nt;
+#pragma unroll 1
+      for (int e = 0; e < E; ++e) {
+        const int c = v * E + e;
+        if (c >= K) break;
+        const float d = __fsub_rn(to_float(row[c]), vmin);
+        const float u = __fadd_rn(__fmul_rn(d, rcp), 0.5f);
+        if (fabsf(__fsub_rn(__fsub_rn(u, floorf(u)), 0.5f)) >= kNearTie)
+          s_codes[c] = static_cast<uint8_t>(static_cast<int>(quant_slow(d, scale)) - kHr);
+      }
     }
   }
-  if (a.xo32) {
-    for (int64_t i = tid; i < a.n_out; i += kQThreads) a.xo32[t * a.n_out + i] = to_f32<T>(row[__ldg(&a.out_src[i])]);
+  __syncthreads();
+
+  // ---- outliers (ascending index order, runtime.cpp:217) from the row copy
+  if (has_out) {
+    const T* row = reinterpret_cast<const T*>(s_row);
+    __half* xo16 = a.xo16 ? a.xo16 + static_cast<int64_t>(t) * a.opad : nullptr;
+    float* xo32 = a.xo32 ? a.xo32 + static_cast<int64_t>(t) * a.n_out : nullptr;
+    for (int i = tid; i < a.n_out; i += nt) {
+      const float x = to_float(row[__ldg(&a.out_src[i])]);
+      if (xo16) xo16[i] = __float2half_rn(x);
+      if (xo32) xo32[i] = x;
+    }
+    if (xo16)
+      for (int i = static_cast<int>(a.n_out) + tid; i < a.opad; i += nt) xo16[i] = __float2half_rn(0.0f);
+  } else if (a.xo16) {
+    for (int i = tid; i < a.opad; i += nt) a.xo16[static_cast<int64_t>(t) * a.opad + i] = __float2half_rn(0.0f);
+  }
+
+  // ---- compacted code row: base position j <- column gather[j] (16 per thread)
+  if (a.q8) {
+    uint4* dst = reinterpret_cast<uint4*>(a.q8 + static_cast<int64_t>(t) * a.kpad);
+    const int nchunk = static_cast<int>(a.kpad / 16);
+    for (int cidx = tid; cidx < nchunk; cidx += nt) {
+      const int j0 = cidx * 16;
+      uint32_t w[4];
+      if (has_out) {
+        const uint4 g0 = __ldg(reinterpret_cast<const uint4*>(a.gather + j0));
+        const uint4 g1 = __ldg(reinterpret_cast<const uint4*>(a.gather + j0 + 8));
+        const uint32_t gi[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t b0 = s_codes[gi[2 * k] & 0xFFFFu], b1 = s_codes[gi[2 * k] >> 16];
+          const uint32_t b2 = s_codes[gi[2 * k + 1] & 0xFFFFu], b3 = s_codes[gi[2 * k + 1] >> 16];
+          w[k] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
+        }
+      } else {
+        const uint4 c = *reinterpret_cast<const uint4*>(s_codes + j0);
+        w[0] = c.x; w[1] = c.y; w[2] = c.z; w[3] = c.w;
+        if (j0 + 16 > kb) {  // zero the pad positions j >= kb
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            if (j0 + k >= kb) w[k >> 2] &= ~(0xFFu << (8 * (k & 3)));
+        }
+      }
+      dst[cidx] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+  // ---- ABI packed codes (debug / parity entry points)
+  if (a.packed) {
+    uint8_t* prow = a.packed + static_cast<int64_t>(t) * (BITS == 4 ? (kb + 1) / 2 : kb);
+    auto code_at = [&](int j) -> int {
+      const int c = has_out ? static_cast<int>(__ldg(&a.gather[j])) : j;
+      return static_cast<int8_t>(s_codes[c]);
+    };
+    if (BITS == 8) {
+      for (int j = tid; j < kb; j += nt) prow[j] = static_cast<uint8_t>(code_at(j));
+    } else {
+      // i4p: low nibble = even base index, stored + 8; pad nibble of odd rows = 0
+      for (int b = tid; b < (kb + 1) / 2; b += nt) {
+        const uint8_t lo = static_cast<uint8_t>(code_at(2 * b) + 8) & 0xF;
+        const uint8_t hi = (2 * b + 1 < kb) ? (static_cast<uint8_t>(code_at(2 * b + 1) + 8) & 0xF) : 0;
+        prow[b] = static_cast<uint8_t>(lo | (hi << 4));
+      }
+    }
   }
 }
 
@@ -235,6 +460,65 @@ __global__ void dequant_kernel(const int32_t* __restrict__ acc, int64_t M, int64
   }
 }
 
+// rtn_quantize_weights (quantizer.cpp:339-371 with rtn_quantize_row :251-264 and
+// quantize_to_grid :17-22): per output row, FP64 scale = amax / maxq, q =
+// clamp(round-half-away(w / scale)), packed ABI codes, wreduced = scale_f32 * sum q.
+// One CTA per row; every FP64 op is an explicit _rn intrinsic (bit-exact).
+__global__ void __launch_bounds__(256) rtn_rows_kernel(const float* __restrict__ w, int64_t K,
+                                                       const int32_t* __restrict__ base_src, int64_t kb,
+                                                       const int32_t* __restrict__ out_src, int64_t n_out, int bits,
+                                                       uint8_t* __restrict__ base, float* __restrict__ scales,
+                                                       float* __restrict__ wreduced, float* __restrict__ outlier_w) {
+  __shared__ float s_amax[8];
+  __shared__ long long s_sum[8];
+  const int64_t r = blockIdx.x;
+  const float* row = w + r * K;
+  const int tid = threadIdx.x;
+  float amax = 0.0f;
+  for (int64_t j = tid; j < kb; j += blockDim.x) amax = fmaxf(amax, fabsf(row[base_src[j]]));
+  for (int off = 16; off; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+  if ((tid & 31) == 0) s_amax[tid >> 5] = amax;
+  __syncthreads();
+  amax = s_amax[0];
+  for (int i = 1; i < 8; ++i) amax = fmaxf(amax, s_amax[i]);
+  const int maxq = (1 << (bits - 1)) - 1;
+  const bool zero_row = amax == 0.0f;
+  const double scale = zero_row ? 1.0 : __ddiv_rn(static_cast<double>(amax), static_cast<double>(maxq));
+  const double inv_scale = __ddiv_rn(1.0, scale);
+  const int64_t rb = bits == 4 ? (kb + 1) / 2 : kb;
+  long long qsum = 0;
+  for (int64_t p = tid; p < rb; p += blockDim.x) {
+    const int per = bits == 4 ? 2 : 1;
+    uint8_t byte = 0;
+    for (int u = 0; u < per; ++u) {
+      const int64_t j = p * per + u;
+      if (j >= kb) break;
+      int qi = 0;
+      if (!zero_row) {
+        const double t = __dmul_rn(static_cast<double>(row[base_src[j]]), inv_scale);
+        double qd = floor(__dadd_rn(fabs(t), 0.5));
+        if (qd > maxq) qd = maxq;
+        qi = static_cast<int>(t < 0.0 ? -qd : qd);
+      }
+      qsum += qi;
+      if (bits == 8) byte = static_cast<uint8_t>(static_cast<int8_t>(qi));
+      else byte |= static_cast<uint8_t>((qi + 8) & 0xF) << (4 * u);
+    }
+    base[r * rb + p] = byte;
+  }
+  for (int off = 16; off; off >>= 1) qsum += __shfl_xor_sync(0xffffffffu, qsum, off);
+  if ((tid & 31) == 0) s_sum[tid >> 5] = qsum;
+  __syncthreads();
+  if (tid == 0) {
+    long long total = 0;
+    for (int i = 0; i < 8; ++i) total += s_sum[i];
+    const float sf = __double2float_rn(scale);
+    scales[r] = sf;
+    wreduced[r] = __double2float_rn(__dmul_rn(static_cast<double>(sf), static_cast<double>(total)));
+  }
+  for (int64_t i = tid; i < n_out; i += blockDim.x) outlier_w[r * n_out + i] = row[out_src[i]];
+}
+
 dim3 grid2(int64_t cols, int64_t rows) {
   int64_t gx = (cols + 255) / 256;
   if (gx > 64) gx = 64;
@@ -244,24 +528,35 @@ dim3 grid2(int64_t cols, int64_t rows) {
 
 }  // namespace
 
-cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t stream) {
-  if (a.M == 0) return cudaSuccess;
-  const size_t smem = static_cast<size_t>(a.K) * (a.x_is_f32 ? 4 : 2) + 16;
-  cudaError_t e;
-#define QUIK_Q_LAUNCH(T, B)                                                                           \
-  do {                                                                                                \
-    e = cudaFuncSetAttribute(quantize_rows_kernel<T, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                             static_cast<int>(smem));                                                 \
-    if (e != cudaSuccess) return e;                                                                   \
-    quantize_rows_kernel<T, B><<<static_cast<unsigned>(a.M), kQThreads, smem, stream>>>(a);          \
+template <typename T, int B>
+cudaError_t launch_quantize_t(const QuantArgs& a, cudaStream_t stream) {
+  constexpr int E = 16 / sizeof(T);
+  const int64_t nvec = (a.K + E - 1) / E;
+  const int threads = nvec > 256 * 4 ? 512 : 256;
+  const int64_t vpt = (nvec + threads - 1) / threads;
+  if (vpt > 16) return cudaErrorInvalidValue;  // row wider than 512 x 16 vectors
+  const size_t smem = static_cast<size_t>(round_up(a.K, 16) + 16) + static_cast<size_t>(nvec) * 16;
+  const dim3 grid(static_cast<unsigned>(a.M));
+#define QUIK_Q_LAUNCH(V)                                                                                   \
+  do {                                                                                                     \
+    cudaError_t e = cudaFuncSetAttribute(quantize_rows_kernel<T, B, V>,                                    \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)); \
+    if (e != cudaSuccess) return e;                                                                        \
+    quantize_rows_kernel<T, B, V><<<grid, threads, smem, stream>>>(a);                                     \
   } while (0)
-  if (a.x_is_f32) {
-    if (a.bits == 4) QUIK_Q_LAUNCH(float, 4); else QUIK_Q_LAUNCH(float, 8);
-  } else {
-    if (a.bits == 4) QUIK_Q_LAUNCH(__half, 4); else QUIK_Q_LAUNCH(__half, 8);
-  }
+  if (vpt <= 1) QUIK_Q_LAUNCH(1);
+  else if (vpt <= 2) QUIK_Q_LAUNCH(2);
+  else if (vpt <= 4) QUIK_Q_LAUNCH(4);
+  else if (vpt <= 8) QUIK_Q_LAUNCH(8);
+  else QUIK_Q_LAUNCH(16);
 #undef QUIK_Q_LAUNCH
   return cudaGetLastError();
+}
+
+cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t stream) {
+  if (a.M == 0) return cudaSuccess;
+  if (a.x_is_f32) return a.bits == 4 ? launch_quantize_t<float, 4>(a, stream) : launch_quantize_t<float, 8>(a, stream);
+  return a.bits == 4 ? launch_quantize_t<__half, 4>(a, stream) : launch_quantize_t<__half, 8>(a, stream);
 }
 
 cudaError_t launch_split(const SplitArgs& a, cudaStream_t stream) {
@@ -281,6 +576,15 @@ cudaError_t launch_f32_to_f16_padded(const float* src, int64_t rows, int64_t col
                                      cudaStream_t stream) {
   if (rows == 0 || pitch == 0) return cudaSuccess;
   f32_to_f16_kernel<<<grid2(pitch, rows), 256, 0, stream>>>(src, rows, cols, dst, pitch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rtn_weights(const float* w, int64_t N, int64_t K, const int32_t* base_src, int64_t kb,
+                               const int32_t* out_src, int64_t n_out, int bits, uint8_t* base, float* scales,
+                               float* wreduced, float* outlier_w, cudaStream_t stream) {
+  if (N == 0) return cudaSuccess;
+  rtn_rows_kernel<<<static_cast<unsigned>(N), 256, 0, stream>>>(w, K, base_src, kb, out_src, n_out, bits, base,
+                                                                scales, wreduced, outlier_w);
   return cudaGetLastError();
 }
 

@@ -297,6 +297,37 @@ class QuikLinear:
         self._lib.quik_layer_info(h, None, C.byref(of), None, None)
         self.out_features = of.value
 
+    @classmethod
+    def from_device(cls, outliers: OutlierSet, base, scales, wreduced, outlier_weights, bits: int, bias=None,
+                    row_begin: int = 0, row_end: int = 0) -> "QuikLinear":
+        """Builds the layer straight from device tensors in the reference formats
+        (e.g. the output of rtn_quantize_weights_device) without a host round trip."""
+        torch = _torch()
+        self = cls.__new__(cls)
+        self._lib = _lib.load()
+        self.ctx = context(base.device.index)
+        self.device = self.ctx.device
+        self.in_features = outliers.feature_count
+        self.n_outlier = outliers.outlier_count()
+        self.bits = bits
+        idx = np.ascontiguousarray(outliers.indices, dtype=np.int64)
+        ow = outlier_weights.contiguous() if self.n_outlier else None
+        d = _lib.WeightsDesc(
+            in_features=self.in_features, out_features=scales.numel(), bits=bits, act_bits=bits,
+            base=base.data_ptr(), scales=scales.data_ptr(), wreduced=wreduced.data_ptr(),
+            outlier_weights=None if ow is None else ow.data_ptr(),
+            outlier_indices=idx.ctypes.data if idx.size else None, n_outlier=self.n_outlier,
+            bias=None if bias is None else bias.data_ptr(), row_begin=row_begin, row_end=row_end)
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            torch.cuda.current_stream().synchronize()
+            _lib.check(self._lib.quik_layer_create(self.ctx.handle, C.byref(d), C.byref(h)))
+        self.handle = h
+        of = C.c_int64()
+        self._lib.quik_layer_info(h, None, C.byref(of), None, None)
+        self.out_features = of.value
+        return self
+
     def __del__(self):
         try:
             if getattr(self, "handle", None):
@@ -309,8 +340,11 @@ class QuikLinear:
     def launches(variant: PipelineVariant = PipelineVariant.V3FusedEpilogue) -> int:
         return int(_lib.load().quik_linear_forward_launches(int(variant)))
 
-    def forward(self, x, out=None, out_dtype=None, variant: PipelineVariant = PipelineVariant.V3FusedEpilogue):
-        """x: CUDA tensor [M][in_features] f16/f32 -> [M][out_features] (f16 default)."""
+    def forward(self, x, out=None, out_dtype=None, variant: PipelineVariant = PipelineVariant.V3FusedEpilogue,
+                mid_event=None):
+        """x: CUDA tensor [M][in_features] f16/f32 -> [M][out_features] (f16 default).
+        mid_event: optional torch.cuda.Event recorded between the quantizer and the
+        GEMM kernel (per-kernel timing)."""
         torch = _torch()
         if x.dim() != 2 or x.shape[1] != self.in_features:
             raise ValueError(f"quik_matmul: input has {x.shape[-1]} features, layer expects {self.in_features}")
@@ -326,9 +360,9 @@ class QuikLinear:
         ldy = out.stride(0)
         if out.stride(1) != 1 or ldy < self.out_features:
             raise ValueError("output must be row-major with pitch >= out_features")
-        _lib.check(self._lib.quik_linear_forward_strided(
+        _lib.check(self._lib.quik_linear_forward_ex(
             self.ctx.handle, self.handle, _ptr(x), xdt, M, _ptr(out), ydt, ldy, int(variant),
-            C.c_void_p(_stream_ptr(torch, x.device))))
+            C.c_void_p(_stream_ptr(torch, x.device)), C.c_void_p(mid_event.cuda_event if mid_event else None)))
         return out
 
     __call__ = forward
@@ -428,6 +462,49 @@ def dequantize_epilogue(acc: np.ndarray, a: ActQuantResult, weight_scales, wredu
                                                     _ptr(sw), _ptr(wr), _ptr(out), C.c_void_p(s)))
     ctx.sync(s)
     return out.cpu().numpy()
+
+
+def rtn_quantize_weights_device(w, outliers: OutlierSet, bits: int):
+    """reference: rtn_quantize_weights (quantizer.cpp:339-371), on the device.
+
+    w: CUDA f32 tensor [out][in]. Returns device tensors (base_packed u8
+    [out*row_bytes], scales, wreduced, outlier_weights [out][n_outlier])."""
+    torch = _torch()
+    if bits not in (4, 8):
+        raise ValueError("weight bits must be 4 or 8")
+    if w.dim() != 2 or w.shape[1] != outliers.feature_count:
+        raise ValueError(f"outlier set covers {outliers.feature_count} features, weights have {w.shape[-1]}")
+    w = w.contiguous().float()
+    ctx = context(w.device.index)
+    N, K = w.shape
+    kb = outliers.base_count()
+    O = outliers.outlier_count()
+    base = torch.empty(max(N * row_bytes(kb, bits), 1), dtype=torch.uint8, device=w.device)
+    scales = torch.empty(max(N, 1), dtype=torch.float32, device=w.device)
+    wred = torch.empty(max(N, 1), dtype=torch.float32, device=w.device)
+    ow = torch.empty(max(N * O, 1), dtype=torch.float32, device=w.device)
+    idx = np.ascontiguousarray(outliers.indices, dtype=np.int64)
+    s = _stream_ptr(torch, w.device)
+    _lib.check(_lib.load().quik_rtn_quantize_weights(
+        ctx.handle, _ptr(w), N, K, C.c_void_p(idx.ctypes.data if idx.size else None), O, bits, _ptr(base),
+        _ptr(scales), _ptr(wred), _ptr(ow), C.c_void_p(s)))
+    return base[: N * row_bytes(kb, bits)], scales[:N], wred[:N], ow[: N * O].view(N, O)
+
+
+def rtn_quantize_weights(w: np.ndarray, outliers: OutlierSet, bits: int) -> QuantizedWeights:
+    """reference: rtn_quantize_weights (quantizer.hpp:87-88), use_clipping = false.
+    Host f32 [out][in] in, QuantizedWeights (host arrays) out; computed on the GPU."""
+    torch = _torch()
+    w = np.ascontiguousarray(w, dtype=np.float32)
+    if w.ndim != 2 or w.shape[1] != outliers.feature_count:
+        raise ValueError(f"outlier set covers {outliers.feature_count} features, weights have {w.shape[-1]}")
+    ctx = context()
+    dw = _dev(torch, w, ctx.device)
+    base, sc, wr, ow = rtn_quantize_weights_device(dw, outliers, bits)
+    ctx.sync(_stream_ptr(torch, dw.device))
+    N = w.shape[0]
+    return QuantizedWeights(PackedIntMatrix(N, outliers.base_count(), bits, base.cpu().numpy()), sc.cpu().numpy(),
+                            ow.cpu().numpy(), wr.cpu().numpy())
 
 
 def quik_matmul(layer: QuikLinearLayer, x: np.ndarray,

@@ -367,3 +367,73 @@ def test_non_finite_input_flags_numerical_error():
         dev.ctx.sync(torch.cuda.current_stream().cuda_stream)
     with pytest.raises(m.NumericalError):
         m.quik_matmul(lay, x)
+
+
+# --------------------------------------------------------------------------- every tile configuration
+
+
+@pytest.fixture
+def tile():
+    import paper_2310_09259_b200 as m
+
+    lib = m.load_library()
+    yield lambda cg, bn: lib.quik_set_gemm_tile(cg, bn)
+    lib.quik_set_gemm_tile(0, 0)
+
+
+@pytest.mark.parametrize("cg,bn", [(1, 32), (1, 64), (1, 128), (2, 128), (2, 256)])
+def test_every_tile_config_exact(tile, cg, bn):
+    """Forces each GEMM tile (1-CTA and CTA-pair) and checks the INT32 path and the
+    O=0 f32 layer bit-exactly, with ragged M/N/K tails."""
+    m = q()
+    o = oracle()
+    assert tile(cg, bn) == 0
+    rng = np.random.default_rng(100 * cg + bn)
+    for (t, k, n, bits) in [(300, 1000, 500, 4), (37, 259, 333, 8), (513, 640, 257, 4)]:
+        lim = 7 if bits == 4 else 127
+        xv = rng.integers(-lim - 1, lim + 1, size=(t, k))
+        wv = rng.integers(-lim - 1, lim + 1, size=(n, k))
+        got = m.int_matmul(m.pack_values(xv, t, k, bits), m.pack_values(wv, n, k, bits))
+        np.testing.assert_array_equal(got, xv @ wv.T)
+    L, x, _ = make_layer(rng, 300, 700, 300, 4, 0, heavy_cols=2)
+    st, want = o.quik_matmul(L, x, 2)
+    got = m.quik_matmul(to_layer(L), x)
+    np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+    L, x, _ = make_layer(rng, 260, 900, 520, 8, 64, heavy_cols=5)
+    st, want = o.quik_matmul(L, x, 2)
+    got = m.quik_matmul(to_layer(L), x)
+    assert rel_frob(want, got) < 1e-5
+
+
+def test_rtn_quantize_weights_device_bit_exact():
+    """quantize-weights on the device vs the reference's rtn_quantize_weights
+    (quantizer.cpp:339-371): codes, scales, wreduced and outlier columns bit-exact."""
+    m = q()
+    r = ref()
+    rng = np.random.default_rng(53)
+    for bits in (4, 8):
+        for (N, K, O) in [(40, 96, 8), (257, 1001, 0), (64, 512, 64)]:
+            w = rng.normal(0, 0.5, size=(N, K)).astype(np.float32)
+            w[3] = 0.0  # all-zero row -> scale 1, q = 0
+            idx = np.sort(rng.choice(K, O, replace=False)).astype(np.int64)
+            want = r.rtn_quantize_weights(w, idx, bits)
+            got = m.rtn_quantize_weights(w, m.OutlierSet.from_indices(K, idx), bits)
+            np.testing.assert_array_equal(got.base.data, want["base"])
+            np.testing.assert_array_equal(got.scales.view(np.uint32), want["scales"].view(np.uint32))
+            np.testing.assert_array_equal(got.wreduced.view(np.uint32), want["wreduced"].view(np.uint32))
+            np.testing.assert_array_equal(got.outlier_weights, want["outlier_weights"])
+
+
+def test_quantizer_wide_rows_f32_and_f16():
+    """K1 at the LLaMA-2-70B down-projection width (28672) with 896 outliers, both input types."""
+    m = q()
+    o = oracle()
+    rng = np.random.default_rng(59)
+    K = 28672
+    x = rng.normal(0, 1, size=(3, K)).astype(np.float16).astype(np.float32)
+    idx = np.sort(rng.choice(K, 896, replace=False)).astype(np.int64)
+    st, pk, sc, ze, xo = o.quantize_fused(x, idx, 8)
+    r, gxo = m.quantize_activations_fused(x, m.OutlierSet.from_indices(K, idx), 8)
+    np.testing.assert_array_equal(r.packed.data, pk)
+    np.testing.assert_array_equal(r.scale.view(np.uint32), sc.view(np.uint32))
+    np.testing.assert_array_equal(gxo, xo)
