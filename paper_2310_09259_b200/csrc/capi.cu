@@ -211,8 +211,8 @@ quik_status quik_set_gemm_tile(int cta_group, int block_n) {
 
 int quik_linear_forward_launches(quik_variant v) {
   switch (v) {
-    case QUIK_V1_UNFUSED: return 5;      // split, quantize, int gemm, outlier gemm, dequant+add
-    case QUIK_V2_FUSED_QUANT: return 4;  // fused quantize, int gemm, outlier gemm, dequant+add
+    case QUIK_V1_UNFUSED: return 4;      // split, quantize, int gemm, epilogue + outlier gemm
+    case QUIK_V2_FUSED_QUANT: return 3;  // fused quantize, int gemm, epilogue + outlier gemm
     default: return 2;                   // fused quantize, fused gemm+epilogue
   }
 }
@@ -569,9 +569,9 @@ quik_status quik_linear_forward_ex(quik_ctx_t ctx, quik_layer_t L, const void* x
     } else {
       run_k1(ctx, L, x, xdt, M, st);
     }
-    // V1/V2 tail: int32 accumulator, outlier product + bias, dequantize + add
+    // V1/V2 tail: the int32 accumulator through global memory, then the same
+    // epilogue + outlier MMAs as V3 reading it back (bit-identical to V3).
     int32_t* acc = static_cast<int32_t*>(ctx->acc.ensure(static_cast<size_t>(M * N * 4)));
-    float* fp = static_cast<float*>(ctx->fp.ensure(static_cast<size_t>(M * N * 4)));
     GemmArgs gi = gemm_args(ctx, L, M);
     gi.out = acc;
     gi.ldo = N;
@@ -579,18 +579,12 @@ quik_status quik_linear_forward_ex(quik_ctx_t ctx, quik_layer_t L, const void* x
     if (L->kpad) run_gemm(ctx, gi, st);
     else QK_CUDA(cudaMemsetAsync(acc, 0, static_cast<size_t>(M * N * 4), st));
     GemmArgs go = gemm_args(ctx, L, M);
-    go.out = fp;
-    go.ldo = N;
-    go.mode = kModeOutlierF32;
+    go.acc_in = acc;
+    go.ld_acc = N;
+    go.out = y;
+    go.ldo = ldy;
+    go.mode = ydt == QUIK_F16 ? kModeAccInitF16 : kModeAccInitF32;
     run_gemm(ctx, go, st);
-    if (ldy == N) {
-      check_launch(launch_dequant_add(acc, M, N, static_cast<const float*>(ctx->scale.p),
-                                      static_cast<const float*>(ctx->zero.p), static_cast<float>(1 << (L->bits - 1)),
-                                      L->w_scale, L->wreduced, fp, y, ydt == QUIK_F16, st),
-                   "dequant+add kernel");
-    } else {
-      return fail(QUIK_ERR_UNSUPPORTED, "V1/V2 variants support dense outputs only");
-    }
     return QUIK_OK;
   });
 }

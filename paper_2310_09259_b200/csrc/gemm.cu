@@ -1,27 +1,31 @@
 // K2+K3+K4: the fused QUIK linear kernel for sm_100a.
 //
-// Computes, for one layer call (runtime.cpp:246-318, V3 path :279-303):
-//   acc[n][t] = sum_k W8[n][k] * X8[t][k]                  (tcgen05 kind::i8, exact int32 in TMEM)
-//   f[n][t]   = sum_o Wo[n][o] * Xo[t][o]                  (tcgen05 kind::f16, f32 in TMEM)
-//   y[t][n]   = (bias[n] + f) + dequant_element(acc, ...)  (epilogue, runtime.cpp:70-77)
-// "Swap-AB" orientation: weight rows are the UMMA M dimension, tokens are the
-// UMMA N dimension (BN per tile), so small token counts use narrow N tiles
-// instead of padding 128-row MMAs.
+// For one layer call (reference runtime.cpp:246-318, V3 path :279-303):
+//   acc[n][t] = sum_k W8[n][k] * X8[t][k]                   tcgen05 kind::i8, exact int32 in TMEM
+//   init      = bias[n] + dequant_element(acc, ...)         epilogue, in place in TMEM (f32)
+//   D         = init + sum_o Wo[n][o] * Xo[t][o]            tcgen05 kind::f16 accumulating onto init
+//   y[t][n]   = f16(D)                                      epilogue -> smem -> TMA store
+// dequant_element is evaluated op by op (runtime.cpp:70-77) so the whole layer is
+// bit-identical to the reference when it has no outliers; with outliers the only
+// difference is the summation order of the f16 products (SURVEY.md A.3 tolerance).
 //
-// CG = 2 (large M): a CTA pair (cluster of 2) runs tcgen05.mma.cta_group::2 with
-// M = 256: each CTA stages its own 128 weight rows and half of the BN token rows,
-// halving shared-memory operand traffic per SM (the 1-CTA 128x128 tile is
-// SMEM-bandwidth bound: 8 KB of operands per 64-cycle MMA). The leader CTA issues
-// the MMAs; both CTAs' TMA loads complete on the leader's full barrier; MMA
+// "Swap-AB" orientation: weight rows are the UMMA M dimension, tokens are the
+// UMMA N dimension (BN per tile), so small token counts use narrow N tiles.
+// CG = 2 (large M): a CTA pair runs tcgen05.mma.cta_group::2 with M = 256; each
+// CTA stages its own 128 weight rows and half of the BN token rows; the leader
+// issues the MMAs, both CTAs' TMA loads complete on the leader's barrier, MMA
 // commits are multicast to both CTAs.
 //
-// Warp roles (256 threads, 1 CTA per SM, persistent over tiles):
-//   warp 0      TMA producer (one elected lane)
+// TMEM: two accumulator buffers of BN columns. Per tile the MMA warp issues
+//   int k-blocks [0, kb/2) of tile i | outlier k-blocks of tile i-1 | int k-blocks [kb/2, kb) of tile i
+// so that the epilogue's two passes over tile i-1 (convert int32 -> f32 init in
+// place, then drain the finished f32 tile) overlap the integer MMAs of tile i.
+//
+// Warp roles (384 threads, 1 CTA per SM, persistent over tiles):
+//   warp 0      TMA producer (one lane)
 //   warp 1      MMA issuer  (one lane, leader CTA only)
 //   warp 2      TMEM allocator
-//   warps 4..7  epilogue: TMEM -> registers -> dequant -> global
-// Pipelines: smem ring (full/empty mbarriers, TMA <-> MMA) and a TMEM
-// accumulator ring (tmem_full/tmem_empty, MMA <-> epilogue).
+//   warps 4..11 epilogue (TMEM lane quadrant = warp % 4, column half = (warp - 4) / 4)
 #include <cudaTypedefs.h>
 
 #include <mutex>
@@ -34,10 +38,10 @@ namespace quikb200 {
 namespace {
 
 constexpr int kEpiWarp0 = 4;
-constexpr int kEpiWarps = 8;  // 2 per SM sub-partition: each TMEM lane quadrant split in column halves
+constexpr int kEpiWarps = 8;
 constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
-constexpr int kChunk = 32;                                 // tokens per epilogue step
-constexpr int kStoreBufBytes = kChunk * 32 * 2;            // [32 tokens][32 features] f16
+constexpr int kChunk = 32;                                     // tokens per epilogue step
+constexpr int kStoreBufBytes = kChunk * 32 * 2;                // [32 tokens][32 features] f16
 constexpr int kStagingBytes = kEpiWarps * 2 * kStoreBufBytes;  // double-buffered per warp
 
 template <int CG, int BN>
@@ -46,15 +50,10 @@ struct Cfg {
   static constexpr int kABytes = kBlockM * kKBlockBytes;  // 16 KB: 128 weight rows per CTA
   static constexpr int kBBytes = kBRows * kKBlockBytes;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kBudget = 227 * 1024 - 1024 - kStagingBytes - 256;
+  static constexpr int kBudget = 227 * 1024 - 1024 - kStagingBytes - 512;
   static constexpr int kStages = (kBudget / kStageBytes) > 8 ? 8 : (kBudget / kStageBytes);
-  // Per accumulator buffer: BN int32 columns + BN f32 columns.
-  static constexpr int kAccCols = 2 * BN;
-  static constexpr int kAccBufs = (2 * kAccCols <= 512) ? 2 : 1;
-  static constexpr int kTmemColsRaw = kAccBufs * kAccCols;
-  static constexpr int kTmemCols =
-      kTmemColsRaw <= 32 ? 32 : kTmemColsRaw <= 64 ? 64 : kTmemColsRaw <= 128 ? 128 : kTmemColsRaw <= 256 ? 256 : 512;
-  static constexpr int kBarBytes = (2 * kStages + 2 * kAccBufs) * 8 + 16;
+  static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
+  static constexpr int kBarBytes = (2 * kStages + 8) * 8 + 16;
   static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kStagingBytes + kBarBytes;
   static constexpr int kTileRows = kBlockM * CG;          // weight rows per (cluster) tile
 };
@@ -76,32 +75,57 @@ struct KParams {
   float half_range;
   void* out;
   long long ldo;
+  const int32_t* acc_in;
+  long long ld_acc;
 };
+
+template <int CG, int MODE>
+__device__ __forceinline__ void arrive_leader(uint64_t* bar) {
+  if constexpr (CG == 2) mbar_arrive_cluster(bar, 0);
+  else mbar_arrive(bar);
+}
 
 template <int CG, int BN, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_constant__ KParams p) {
   using C = Cfg<CG, BN>;
+  constexpr bool kAccGlobal = MODE == kModeAccInitF32 || MODE == kModeAccInitF16;
+  constexpr bool kF16Out = MODE == kModeF16 || MODE == kModeAccInitF16;
+  constexpr bool kInt32Out = MODE == kModeInt32;
+  constexpr bool kProbe = MODE == kModeProbe;
+
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* staging = smem + C::kStages * C::kStageBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(staging + kStagingBytes);
   uint64_t* empty = full + C::kStages;
-  uint64_t* tfull = empty + C::kStages;
-  uint64_t* tempty = tfull + C::kAccBufs;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + C::kAccBufs);
+  uint64_t* tint = empty + C::kStages;  // [2] int MMAs of the tile done        (MMA -> epilogue)
+  uint64_t* tconv = tint + 2;           // [2] init written into TMEM          (epilogue -> MMA)
+  uint64_t* tfin = tconv + 2;           // [2] outlier MMAs done, tile final   (MMA -> epilogue)
+  uint64_t* tempty = tfin + 2;          // [2] accumulator buffer drained      (epilogue -> MMA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
   const bool leader = rank == 0;
 
+  const int kb_int = kAccGlobal ? 0 : p.kb_int;
+  const int kb_out = kInt32Out ? 0 : p.kb_out;
+  const bool two_phase = kb_out > 0;
+  const int h_a = kb_int / 2;
+
   if (warp == 0 && lane == 0) {
-    if (p.kb_int) { tma_prefetch(&p.tm_w); tma_prefetch(&p.tm_x); }
-    if (p.kb_out) { tma_prefetch(&p.tm_wo); tma_prefetch(&p.tm_xo); }
+    if (kb_int) { tma_prefetch(&p.tm_w); tma_prefetch(&p.tm_x); }
+    if (kb_out) { tma_prefetch(&p.tm_wo); tma_prefetch(&p.tm_xo); }
   }
   if (warp == 1 && lane == 0) {
     for (int i = 0; i < C::kStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < C::kAccBufs; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], kEpiWarps * CG); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tint[i], 1);
+      mbar_init(&tconv[i], kEpiWarps * CG);
+      mbar_init(&tfin[i], 1);
+      mbar_init(&tempty[i], kEpiWarps * CG);
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<CG>(tmem_slot, C::kTmemCols);
@@ -117,7 +141,6 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
   const int num_clusters = gridDim.x / CG;
   // Tile order: consecutive tile ids share the weight block (n) so the clusters
   // that run concurrently read the same weight rows through L2.
-  const int kb_total = p.kb_int + p.kb_out;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -125,28 +148,42 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
       const uint64_t pol_x = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
-        const int nb = tile / tiles_m, mb = tile % tiles_m;
-        const int wrow = nb * C::kTileRows + static_cast<int>(rank) * kBlockM;
-        const int trow = mb * BN + static_cast<int>(rank) * C::kBRows;
-        for (int kb = 0; kb < kb_total; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * C::kStageBytes;
-          uint8_t* sb = sa + C::kABytes;
-          if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::kStageBytes);
-          const bool is_int = kb < p.kb_int;
-          const CUtensorMap* ma = is_int ? &p.tm_w : &p.tm_wo;
-          const CUtensorMap* mx = is_int ? &p.tm_x : &p.tm_xo;
-          const int kc = is_int ? kb * kKBlockBytes : (kb - p.kb_int) * 64;
-          if constexpr (CG == 1) {
-            tma_load_2d(sa, ma, kc, wrow, &full[stage], pol_w);
-            tma_load_2d(sb, mx, kc, trow, &full[stage], pol_x);
-          } else {
-            tma_load_2d_pair(sa, ma, kc, wrow, &full[stage], pol_w);
-            tma_load_2d_pair(sb, mx, kc, trow, &full[stage], pol_x);
-          }
-          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+      auto load = [&](const CUtensorMap* ma, const CUtensorMap* mx, int kc, int wrow, int trow) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * C::kStageBytes;
+        uint8_t* sb = sa + C::kABytes;
+        if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::kStageBytes);
+        if constexpr (CG == 1) {
+          tma_load_2d(sa, ma, kc, wrow, &full[stage], pol_w);
+          tma_load_2d(sb, mx, kc, trow, &full[stage], pol_x);
+        } else {
+          tma_load_2d_pair(sa, ma, kc, wrow, &full[stage], pol_w);
+          tma_load_2d_pair(sb, mx, kc, trow, &full[stage], pol_x);
         }
+        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+      };
+      auto rows_of = [&](int tile, int& wrow, int& trow) {
+        const int nb = tile / tiles_m, mb = tile % tiles_m;
+        wrow = nb * C::kTileRows + static_cast<int>(rank) * kBlockM;
+        trow = mb * BN + static_cast<int>(rank) * C::kBRows;
+      };
+      int prev = -1;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+        int wr, tr;
+        rows_of(tile, wr, tr);
+        for (int kb = 0; kb < h_a; ++kb) load(&p.tm_w, &p.tm_x, kb * kKBlockBytes, wr, tr);
+        if (two_phase && prev >= 0) {
+          int pw, pt;
+          rows_of(prev, pw, pt);
+          for (int ko = 0; ko < kb_out; ++ko) load(&p.tm_wo, &p.tm_xo, ko * 64, pw, pt);
+        }
+        for (int kb = h_a; kb < kb_int; ++kb) load(&p.tm_w, &p.tm_x, kb * kKBlockBytes, wr, tr);
+        prev = tile;
+      }
+      if (two_phase && prev >= 0) {
+        int pw, pt;
+        rows_of(prev, pw, pt);
+        for (int ko = 0; ko < kb_out; ++ko) load(&p.tm_wo, &p.tm_xo, ko * 64, pw, pt);
       }
     }
   } else if (warp == 1) {
@@ -155,99 +192,124 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
       constexpr uint32_t id_f16 = idesc_make(1u, 0u, kBlockM * CG, BN);
       int stage = 0;
       uint32_t phase = 0;
-      int abuf = 0;
-      uint32_t aphase = 0;
-      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
-        mbar_wait(&tempty[abuf], aphase ^ 1);
+      auto next_stage = [&](uint64_t& adesc, uint64_t& bdesc) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t d_int = tmem_base + abuf * C::kAccCols;
-        const uint32_t d_f32 = d_int + BN;
-        for (int kb = 0; kb < kb_total; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
-          const uint32_t sb = sa + C::kABytes;
-          const uint64_t adesc = umma_desc_sw128(sa);
-          const uint64_t bdesc = umma_desc_sw128(sb);
-          if (kb < p.kb_int) {
+        const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
+        adesc = umma_desc_sw128(sa);
+        bdesc = umma_desc_sw128(sa + C::kABytes);
+      };
+      auto release_stage = [&]() {
+        mma_commit<CG>(&empty[stage]);
+        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+      };
+      auto int_blocks = [&](uint32_t d, int k0, int k1) {
+        for (int kb = k0; kb < k1; ++kb) {
+          uint64_t ad, bd;
+          next_stage(ad, bd);
 #pragma unroll
-            for (int k = 0; k < 4; ++k)  // 4 x K=32 int8 = 128 bytes
-              mma_i8<CG>(d_int, adesc + 2 * k, bdesc + 2 * k, id_i8, (kb | k) != 0);
-          } else {
-            const int ko = kb - p.kb_int;
-#pragma unroll
-            for (int k = 0; k < 4; ++k)  // 4 x K=16 f16 = 128 bytes
-              mma_f16<CG>(d_f32, adesc + 2 * k, bdesc + 2 * k, id_f16, (ko | k) != 0);
-          }
-          mma_commit<CG>(&empty[stage]);
-          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+          for (int k = 0; k < 4; ++k)  // 4 x K=32 int8 = 128 bytes
+            mma_i8<CG>(d, ad + 2 * k, bd + 2 * k, id_i8, (kb | k) != 0);
+          release_stage();
         }
-        mma_commit<CG>(&tfull[abuf]);
-        if (C::kAccBufs == 2) { abuf ^= 1; if (abuf == 0) aphase ^= 1; } else { aphase ^= 1; }
+      };
+      auto out_blocks = [&](int it_prev) {
+        const int bp = it_prev & 1;
+        mbar_wait(&tconv[bp], (it_prev >> 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + bp * BN;
+        for (int ko = 0; ko < kb_out; ++ko) {
+          uint64_t ad, bd;
+          next_stage(ad, bd);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)  // 4 x K=16 f16 = 128 bytes, accumulating onto init
+            mma_f16<CG>(d, ad + 2 * k, bd + 2 * k, id_f16, 1u);
+          release_stage();
+        }
+        mma_commit<CG>(&tfin[bp]);
+      };
+      int it = 0;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
+        const int b = it & 1;
+        mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + b * BN;
+        int_blocks(d, 0, h_a);
+        if (two_phase && it > 0) out_blocks(it - 1);
+        int_blocks(d, h_a, kb_int);
+        mma_commit<CG>(&tint[b]);
       }
+      if (two_phase && it > 0) out_blocks(it - 1);
     }
   } else if (warp >= kEpiWarp0) {
-    // Epilogue warp e: TMEM lane quadrant q = warp % 4 (hardware rule: a warp may
-    // only access lanes 32*(warp%4) .. +31), column half h.
     const int e = warp - kEpiWarp0;
-    const int q = warp & 3;
+    const int q = warp & 3;  // TMEM lane quadrant (hardware: lanes 32*(warp%4) .. +31)
     const int h = e >> 2;
-    constexpr int kHalf = BN / 2 < kChunk ? kChunk : BN / 2;  // columns per half (BN >= 32)
+    constexpr int kHalf = BN / 2 < kChunk ? kChunk : BN / 2;
     const int c_begin = h * kHalf;
     const int c_end = (c_begin + kHalf) < BN ? (c_begin + kHalf) : BN;
-    const int row = q * 32 + lane;
     uint8_t* my_stage = staging + e * 2 * kStoreBufBytes;
     int sbuf = 0;
-    int abuf = 0;
-    uint32_t aphase = 0;
-    const bool has_int = p.kb_int > 0;
-    const bool has_out = p.kb_out > 0;
-    const bool tma_out = MODE == kModeF16 && p.tma_store;
-    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+    const bool tma_out = kF16Out && p.tma_store;
+    int it = 0;
+    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
+      const int b = it & 1;
+      const uint32_t par = (it >> 1) & 1;
       const int nb = tile / tiles_m, mb = tile % tiles_m;
       const int n0 = nb * C::kTileRows + static_cast<int>(rank) * kBlockM + q * 32;  // warp's first feature
       const int n = n0 + lane;
       const bool n_ok = n < p.N;
       float sw = 0.f, wr = 0.f, bs = 0.f;
-      if (n_ok) {
-        if (MODE == kModeF32 || MODE == kModeF16) { sw = __ldg(&p.w_scale[n]); wr = __ldg(&p.wreduced[n]); }
-        if (MODE != kModeInt32 && p.bias) bs = __ldg(&p.bias[n]);
+      if (n_ok && !kInt32Out) {
+        sw = __ldg(&p.w_scale[n]);
+        wr = __ldg(&p.wreduced[n]);
+        if (p.bias) bs = __ldg(&p.bias[n]);
       }
-      mbar_wait(&tfull[abuf], aphase);
-      tc_fence_after();
-      const uint32_t t_int = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + abuf * C::kAccCols;
-      const uint32_t t_f32 = t_int + BN;
-#pragma unroll 1
-      for (int c = c_begin; c < c_end; c += kChunk) {
-        if (tma_out) {
-          // ---- fast path: dequant 32 tokens x 32 features, stage in smem, TMA store
-          uint32_t vi[32], vf[32];
-          if (has_int) tmem_ld32(t_int + c, vi);
-          if (has_out) tmem_ld32(t_f32 + c, vf);
-          // per-token scale / shift: lane j holds token t0+j (broadcast by shuffles)
-          const int t_l = mb * BN + c + lane;
-          const float sa_l = t_l < p.M ? __ldg(&p.a_scale[t_l]) : 0.f;
-          const float za_l = t_l < p.M ? __ldg(&p.a_zero[t_l]) : 0.f;
-          const float zs_l = __fadd_rn(za_l, __fmul_rn(p.half_range, sa_l));  // runtime.cpp:74
-          tmem_ld_wait();
-          if (!has_int) {
+      const uint32_t tacc = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + b * BN;
+      if (!kAccGlobal) {
+        mbar_wait(&tint[b], par);
+        tc_fence_after();
+      }
+
+      // init = bias + dequant_element(acc, ...) for 32 tokens of this warp's 32 rows
+      auto dequant_chunk = [&](int c, uint32_t (&v)[32]) {
+        if (kAccGlobal) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) vi[j] = 0u;
+          for (int j = 0; j < 32; ++j) {
+            const int t = mb * BN + c + j;
+            v[j] = (t < p.M && n_ok) ? static_cast<uint32_t>(__ldg(&p.acc_in[static_cast<long long>(t) * p.ld_acc + n]))
+                                     : 0u;
           }
+        } else if (kb_int > 0) {
+          tmem_ld32(tacc + c, v);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0u;
+        }
+        const int t_l = mb * BN + c + lane;
+        const float sa_l = t_l < p.M ? __ldg(&p.a_scale[t_l]) : 0.f;
+        const float za_l = t_l < p.M ? __ldg(&p.a_zero[t_l]) : 0.f;
+        const float zs_l = __fadd_rn(za_l, __fmul_rn(p.half_range, sa_l));  // runtime.cpp:74
+        if (!kAccGlobal && kb_int > 0) tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float sa = __shfl_sync(0xffffffffu, sa_l, j);
+          const float zs = __shfl_sync(0xffffffffu, zs_l, j);
+          float x = __fmul_rn(__int2float_rn(static_cast<int32_t>(v[j])), sa);
+          x = __fmul_rn(x, sw);
+          x = __fadd_rn(x, __fmul_rn(zs, wr));  // dequant_element, runtime.cpp:70-77
+          v[j] = __float_as_uint(__fadd_rn(bs, x));
+        }
+      };
+      // writes 32 tokens x 32 features of final values
+      auto emit_chunk = [&](int c, const uint32_t (&v)[32]) {
+        if constexpr (kProbe) return;
+        if (tma_out) {
           __half* buf = reinterpret_cast<__half*>(my_stage + sbuf * kStoreBufBytes);
           if (lane == 0) bulk_wait_read<1>();  // the store issued from this buffer 2 chunks ago has read it
           __syncwarp();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float sa = __shfl_sync(0xffffffffu, sa_l, j);
-            const float zs = __shfl_sync(0xffffffffu, zs_l, j);
-            float o = bs;
-            if (has_out) o = __fadd_rn(o, __uint_as_float(vf[j]));
-            float v = __fmul_rn(__int2float_rn(static_cast<int32_t>(vi[j])), sa);
-            v = __fmul_rn(v, sw);
-            o = __fadd_rn(o, __fadd_rn(v, __fmul_rn(zs, wr)));  // runtime.cpp:70-77, :298-299
-            buf[j * 32 + lane] = __float2half_rn(o);
-          }
+          for (int j = 0; j < 32; ++j) buf[j * 32 + lane] = __float2half_rn(__uint_as_float(v[j]));
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
@@ -255,61 +317,60 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
             bulk_commit();
           }
           sbuf ^= 1;
-          continue;
+          return;
         }
-        uint32_t vi[32], vf[32];
-        if (MODE != kModeOutlierF32) {
-          if (has_int) tmem_ld32(t_int + c, vi);
-          else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) vi[j] = 0u;
-          }
-        }
-        if (MODE != kModeInt32) {
-          if (has_out) tmem_ld32(t_f32 + c, vf);
-          else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) vf[j] = 0u;
-          }
-        }
-        tmem_ld_wait();
-        if constexpr (MODE == kModeProbe) continue;
-        const int t0 = mb * BN + c;
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const int t = t0 + j;
-          if (t >= p.M) continue;
+          const int t = mb * BN + c + j;
+          if (t >= p.M || !n_ok) continue;
           const long long off = static_cast<long long>(t) * p.ldo + n;
-          if (MODE == kModeInt32) {
-            if (n_ok) reinterpret_cast<int32_t*>(p.out)[off] = static_cast<int32_t>(vi[j]);
-          } else {
-            // orow = fp_linear(...) = bias + sum_o x_o w_o   (runtime.cpp:96-113)
-            float o = bs;
-            if (has_out) o = __fadd_rn(o, __uint_as_float(vf[j]));
-            if (MODE != kModeOutlierF32) {
-              const float sa = __ldg(&p.a_scale[t]);
-              const float za = __ldg(&p.a_zero[t]);
-              // dequant_element, runtime.cpp:70-77, op by op (no contraction)
-              float v = __fmul_rn(__int2float_rn(static_cast<int32_t>(vi[j])), sa);
-              v = __fmul_rn(v, sw);
-              float sh = __fadd_rn(za, __fmul_rn(p.half_range, sa));
-              sh = __fmul_rn(sh, wr);
-              o = __fadd_rn(o, __fadd_rn(v, sh));  // runtime.cpp:298-299
-            }
-            if (n_ok) {
-              if (MODE == kModeF16) reinterpret_cast<__half*>(p.out)[off] = __float2half_rn(o);
-              else reinterpret_cast<float*>(p.out)[off] = o;
-            }
-          }
+          if (kInt32Out) reinterpret_cast<int32_t*>(p.out)[off] = static_cast<int32_t>(v[j]);
+          else if (kF16Out) reinterpret_cast<__half*>(p.out)[off] = __float2half_rn(__uint_as_float(v[j]));
+          else reinterpret_cast<float*>(p.out)[off] = __uint_as_float(v[j]);
+        }
+      };
+
+      if (kInt32Out) {
+#pragma unroll 1
+        for (int c = c_begin; c < c_end; c += kChunk) {
+          uint32_t v[32];
+          tmem_ld32(tacc + c, v);
+          tmem_ld_wait();
+          emit_chunk(c, v);
+        }
+      } else if (!two_phase) {
+#pragma unroll 1
+        for (int c = c_begin; c < c_end; c += kChunk) {
+          uint32_t v[32];
+          dequant_chunk(c, v);
+          emit_chunk(c, v);
+        }
+      } else {
+        // pass 1: init into TMEM (in place over the int32 accumulator)
+#pragma unroll 1
+        for (int c = c_begin; c < c_end; c += kChunk) {
+          uint32_t v[32];
+          dequant_chunk(c, v);
+          tmem_st32(tacc + c, v);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) arrive_leader<CG, MODE>(&tconv[b]);
+        // pass 2: outlier MMAs have accumulated onto init
+        mbar_wait(&tfin[b], par);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = c_begin; c < c_end; c += kChunk) {
+          uint32_t v[32];
+          tmem_ld32(tacc + c, v);
+          tmem_ld_wait();
+          emit_chunk(c, v);
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        if constexpr (CG == 2) mbar_arrive_cluster(&tempty[abuf], 0);
-        else mbar_arrive(&tempty[abuf]);
-      }
-      if (C::kAccBufs == 2) { abuf ^= 1; if (abuf == 0) aphase ^= 1; } else { aphase ^= 1; }
+      if (lane == 0) arrive_leader<CG, MODE>(&tempty[b]);
     }
     if (lane == 0) bulk_wait_all();
   }
@@ -382,7 +443,8 @@ template <int CG, int BN>
 cudaError_t launch_mode(const KParams& kp, int mode, int num_sms, cudaStream_t stream) {
   switch (mode) {
     case kModeInt32: return launch_cfg<CG, BN, kModeInt32>(kp, num_sms, stream);
-    case kModeOutlierF32: return launch_cfg<CG, BN, kModeOutlierF32>(kp, num_sms, stream);
+    case kModeAccInitF32: return launch_cfg<CG, BN, kModeAccInitF32>(kp, num_sms, stream);
+    case kModeAccInitF16: return launch_cfg<CG, BN, kModeAccInitF16>(kp, num_sms, stream);
     case kModeF32: return launch_cfg<CG, BN, kModeF32>(kp, num_sms, stream);
     case kModeProbe: return launch_cfg<CG, BN, kModeProbe>(kp, num_sms, stream);
     default: return launch_cfg<CG, BN, kModeF16>(kp, num_sms, stream);
@@ -411,8 +473,11 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
   kp.N = static_cast<int>(a.N);
   kp.kb_int = static_cast<int>(a.kpad / kKBlockBytes);
   kp.kb_out = static_cast<int>(a.opad / 64);
+  const bool acc_global = a.mode == kModeAccInitF32 || a.mode == kModeAccInitF16;
   if (a.mode == kModeInt32) kp.kb_out = 0;
-  if (a.mode == kModeOutlierF32) kp.kb_int = 0;
+  if (acc_global) kp.kb_int = 0;
+  kp.acc_in = a.acc_in;
+  kp.ld_acc = a.ld_acc;
   const uint32_t brows = static_cast<uint32_t>(bn / cg);
   if (kp.kb_int) {
     if (!make_map(&kp.tm_w, a.w, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, a.kpad, a.N, a.kpad, kBlockM) ||
@@ -429,7 +494,8 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
     }
   }
   kp.tma_store = 0;
-  if (a.mode == kModeF16 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 && (a.ldo * 2) % 16 == 0) {
+  if ((a.mode == kModeF16 || a.mode == kModeAccInitF16) && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 &&
+      (a.ldo * 2) % 16 == 0) {
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.N), static_cast<cuuint64_t>(a.M)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.ldo * 2)};
     cuuint32_t box[2] = {32, static_cast<cuuint32_t>(kChunk)};

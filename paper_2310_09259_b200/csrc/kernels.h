@@ -16,12 +16,17 @@ constexpr int kBlockM = 128;       // UMMA M (weight rows / output features per 
 
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
+// Output of the fused layer: y = f16/f32( (bias + dequant(acc)) + x_out . W_out^T ),
+// where the outlier product is accumulated by the tensor cores onto the f32
+// value bias + dequant(acc) held in TMEM (SURVEY.md A.3 tolerance; bit-exact
+// when the layer has no outliers).
 enum GemmMode : int {
-  kModeInt32 = 0,       // out int32 [M][ldo]: raw base accumulator (int_matmul)
-  kModeOutlierF32 = 1,  // out f32: bias + x_out . W_out^T (V1/V2 outlier pass)
-  kModeF32 = 2,         // out f32: (bias + outlier) + dequant(acc)   (fused V3)
-  kModeF16 = 3,         // out f16: same as kModeF32 rounded to half  (hot path)
-  kModeProbe = 4,       // diagnostics: mainloop + TMEM drain, no global stores
+  kModeInt32 = 0,       // out int32 [M][ldo]: raw base accumulator (int_matmul, V1/V2 stage)
+  kModeAccInitF32 = 1,  // acc read from global int32 (V1/V2 tail), out f32
+  kModeF32 = 2,         // fused int GEMM + epilogue + outliers, out f32
+  kModeF16 = 3,         // same, out f16 (hot path)
+  kModeProbe = 4,       // diagnostics: mainloop + TMEM traffic, no global stores
+  kModeAccInitF16 = 5,  // acc read from global int32 (V1/V2 tail), out f16
 };
 
 struct GemmArgs {
@@ -44,6 +49,8 @@ struct GemmArgs {
   void* out;             // [M][ldo]
   int64_t ldo;           // elements
   int mode;
+  const int32_t* acc_in; // kModeAccInit*: int32 accumulators [M][ld_acc]
+  int64_t ld_acc;
 };
 
 // Launches the fused persistent tcgen05 kernel (int8 GEMM + f16 outlier GEMM +
