@@ -1,0 +1,447 @@
+// quik_b200.hpp — C++ facade with the reference's layer API, running on B200.
+//
+// Drop-in for the reference's namespace quik (proj/include/quik/{matrix,packed,
+// calibration,quantizer,runtime}.hpp): the same type names, fields, function
+// names, argument meaning and exception types, in namespace quik::b200. A caller
+// switches with `namespace Q = quik::b200;` (or a using-declaration). Host data in,
+// host data out, exactly like the reference; every number is computed by the
+// sm_100a kernels behind the C ABI (quik_b200.h). For repeated forwards keep a
+// DeviceLayer (weights uploaded and repacked once) instead of quik_matmul(layer, x).
+//
+// Header-only; link with -lquik_b200 -lcudart.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "quik_b200.h"
+
+namespace quik::b200 {
+
+// ---------------------------------------------------------------- errors (matrix.hpp:12-21)
+class FormatError : public std::runtime_error {
+ public:
+  explicit FormatError(const std::string& m) : std::runtime_error(m) {}
+};
+class NumericalError : public std::runtime_error {
+ public:
+  explicit NumericalError(const std::string& m) : std::runtime_error(m) {}
+};
+class CudaError : public std::runtime_error {
+ public:
+  explicit CudaError(const std::string& m) : std::runtime_error(m) {}
+};
+
+namespace detail {
+inline void check(quik_status s) {
+  if (s == QUIK_OK) return;
+  const std::string m = quik_last_error();
+  switch (s) {
+    case QUIK_ERR_INVALID_ARGUMENT: throw std::invalid_argument(m);
+    case QUIK_ERR_OUT_OF_RANGE: throw std::out_of_range(m);
+    case QUIK_ERR_NUMERICAL: throw NumericalError(m);
+    default: throw CudaError(m);
+  }
+}
+inline void cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+// Device buffer (RAII).
+struct Buf {
+  void* p = nullptr;
+  explicit Buf(size_t n) { cuda(cudaMalloc(&p, n ? n : 1), "cudaMalloc"); }
+  Buf(const void* host, size_t n) : Buf(n) {
+    if (n) cuda(cudaMemcpy(p, host, n, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+  }
+  ~Buf() { cudaFree(p); }
+  Buf(const Buf&) = delete;
+  Buf& operator=(const Buf&) = delete;
+  void get(void* host, size_t n) const {
+    if (n) cuda(cudaMemcpy(host, p, n, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+  }
+};
+// One context per host thread (scratch + error flag), on the current device.
+inline quik_ctx_t ctx() {
+  struct Holder {
+    quik_ctx_t c = nullptr;
+    ~Holder() { quik_ctx_destroy(c); }
+  };
+  thread_local Holder h;
+  if (!h.c) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    check(quik_ctx_create(dev, &h.c));
+  }
+  return h.c;
+}
+}  // namespace detail
+
+// ---------------------------------------------------------------- value types (matrix.hpp:24-65)
+struct FpMatrix {
+  int64_t rows = 0, cols = 0;
+  std::vector<float> data;
+  FpMatrix() = default;
+  FpMatrix(int64_t r, int64_t c) : rows(r), cols(c), data(static_cast<size_t>(r * c), 0.0f) {}
+  float& at(int64_t r, int64_t c) { return data[static_cast<size_t>(r * cols + c)]; }
+  float at(int64_t r, int64_t c) const { return data[static_cast<size_t>(r * cols + c)]; }
+  const float* row(int64_t r) const { return data.data() + r * cols; }
+  bool empty() const { return rows == 0 || cols == 0; }
+  int64_t size() const { return rows * cols; }
+};
+
+struct Int32Matrix {
+  int64_t rows = 0, cols = 0;
+  std::vector<int32_t> data;
+  Int32Matrix() = default;
+  Int32Matrix(int64_t r, int64_t c) : rows(r), cols(c), data(static_cast<size_t>(r * c), 0) {}
+  int32_t at(int64_t r, int64_t c) const { return data[static_cast<size_t>(r * cols + c)]; }
+};
+
+// packed.hpp:17-36 (i4p: low nibble = even column, stored = v + 8; bits 8 = two's complement)
+struct PackedIntMatrix {
+  int64_t rows = 0, cols = 0;
+  int bits = 4;
+  std::vector<uint8_t> data;
+  int64_t row_bytes() const { return bits == 4 ? (cols + 1) / 2 : cols; }
+  int get(int64_t r, int64_t c) const {
+    if (bits == 8) return static_cast<int8_t>(data[static_cast<size_t>(r * cols + c)]);
+    const uint8_t b = data[static_cast<size_t>(r * row_bytes() + c / 2)];
+    return static_cast<int>((c % 2 == 0) ? (b & 0x0F) : (b >> 4)) - 8;
+  }
+  bool empty() const { return rows == 0 || cols == 0; }
+};
+
+// packed.cpp:30-66 (host-side format conversion; same range errors)
+inline PackedIntMatrix pack_values(std::span<const int8_t> v, int64_t rows, int64_t cols, int bits) {
+  if (bits != 4 && bits != 8) throw std::invalid_argument("pack_values: bits must be 4 or 8");
+  if (static_cast<int64_t>(v.size()) != rows * cols)
+    throw std::invalid_argument("pack: expected " + std::to_string(rows * cols) + " values, got " +
+                                std::to_string(v.size()));
+  PackedIntMatrix m;
+  m.rows = rows;
+  m.cols = cols;
+  m.bits = bits;
+  m.data.assign(static_cast<size_t>(rows * m.row_bytes()), 0);
+  const int lo = bits == 4 ? -8 : -128, hi = bits == 4 ? 7 : 127;
+  for (int64_t r = 0; r < rows; ++r)
+    for (int64_t c = 0; c < cols; ++c) {
+      const int x = v[static_cast<size_t>(r * cols + c)];
+      if (x < lo || x > hi)
+        throw std::out_of_range("pack: value " + std::to_string(x) + " at row " + std::to_string(r) + ", col " +
+                                std::to_string(c) + " outside [" + std::to_string(lo) + ", " + std::to_string(hi) +
+                                "]");
+      if (bits == 8) {
+        m.data[static_cast<size_t>(r * cols + c)] = static_cast<uint8_t>(static_cast<int8_t>(x));
+      } else {
+        uint8_t& b = m.data[static_cast<size_t>(r * m.row_bytes() + c / 2)];
+        const uint8_t s = static_cast<uint8_t>(x + 8);
+        b = (c % 2 == 0) ? static_cast<uint8_t>((b & 0xF0) | s) : static_cast<uint8_t>((b & 0x0F) | (s << 4));
+      }
+    }
+  return m;
+}
+inline PackedIntMatrix pack_int4(std::span<const int8_t> v, int64_t r, int64_t c) { return pack_values(v, r, c, 4); }
+inline PackedIntMatrix pack_int8(std::span<const int8_t> v, int64_t r, int64_t c) { return pack_values(v, r, c, 8); }
+
+inline std::vector<int8_t> unpack_values(const PackedIntMatrix& m) {
+  std::vector<int8_t> out(static_cast<size_t>(m.rows * m.cols));
+  for (int64_t r = 0; r < m.rows; ++r)
+    for (int64_t c = 0; c < m.cols; ++c) out[static_cast<size_t>(r * m.cols + c)] = static_cast<int8_t>(m.get(r, c));
+  return out;
+}
+
+// calibration.hpp:37-48; from_indices calibration.cpp:69-91
+struct OutlierSet {
+  int64_t feature_count = 0;
+  std::vector<int64_t> indices;
+  std::vector<int64_t> permutation;
+  static OutlierSet from_indices(int64_t feature_count, std::vector<int64_t> idx) {
+    std::sort(idx.begin(), idx.end());
+    for (size_t i = 0; i < idx.size(); ++i) {
+      if (idx[i] < 0 || idx[i] >= feature_count)
+        throw std::invalid_argument("OutlierSet: index " + std::to_string(idx[i]) + " outside feature range");
+      if (i > 0 && idx[i] == idx[i - 1])
+        throw std::invalid_argument("OutlierSet: duplicate index " + std::to_string(idx[i]));
+    }
+    OutlierSet o;
+    o.feature_count = feature_count;
+    o.indices = std::move(idx);
+    std::vector<bool> is_out(static_cast<size_t>(feature_count), false);
+    for (int64_t i : o.indices) is_out[static_cast<size_t>(i)] = true;
+    for (int64_t f = 0; f < feature_count; ++f)
+      if (!is_out[static_cast<size_t>(f)]) o.permutation.push_back(f);
+    o.permutation.insert(o.permutation.end(), o.indices.begin(), o.indices.end());
+    return o;
+  }
+  static OutlierSet none(int64_t feature_count) { return from_indices(feature_count, {}); }
+  int64_t outlier_count() const { return static_cast<int64_t>(indices.size()); }
+  int64_t base_count() const { return feature_count - outlier_count(); }
+};
+
+// quantizer.hpp:48-58
+struct QuantizedWeights {
+  PackedIntMatrix base;
+  std::vector<float> scales;
+  FpMatrix outlier_weights;
+  std::vector<float> wreduced;
+  int bits() const { return base.bits; }
+  int64_t out_features() const { return base.rows; }
+  int64_t base_features() const { return base.cols; }
+};
+
+enum class PipelineVariant { V1Unfused, V2FusedQuant, V3FusedEpilogue };  // runtime.hpp:31
+
+// runtime.hpp:33-44 (LayerMode::Quik)
+struct QuikLinearLayer {
+  QuantizedWeights weights;
+  OutlierSet outliers;
+  std::vector<float> bias;
+  int act_bits = 4;
+  int64_t in_features() const { return outliers.feature_count; }
+  int64_t out_features() const { return weights.out_features(); }
+  void validate() const {  // runtime.cpp:150-167
+    if (outliers.outlier_count() != weights.outlier_weights.cols)
+      throw std::invalid_argument("layer: outlier index count " + std::to_string(outliers.outlier_count()) +
+                                  " != outlier weight columns " + std::to_string(weights.outlier_weights.cols));
+    if (outliers.base_count() != weights.base_features())
+      throw std::invalid_argument("layer: base column count mismatch");
+    if (!bias.empty() && static_cast<int64_t>(bias.size()) != out_features())
+      throw std::invalid_argument("layer: bias length != out_features");
+    if (act_bits != weights.bits())
+      throw std::invalid_argument("layer: activation bits must match weight bits in quik mode");
+    if (act_bits != 4 && act_bits != 8) throw std::invalid_argument("activation bits must be 4 or 8");
+  }
+};
+
+// runtime.hpp:18-23
+struct ActQuantResult {
+  PackedIntMatrix packed;
+  std::vector<float> scale;
+  std::vector<float> zero;
+  int half_range = 8;
+};
+
+inline float dequantize_activation(int q, float scale, float zero, int half_range) {  // runtime.hpp:60-62
+  return (static_cast<float>(q) + static_cast<float>(half_range)) * scale + zero;
+}
+
+// runtime.hpp:72-80; filled from CUDA events around the device call
+struct StageTimes {
+  double split_ms = 0, quantize_ms = 0, int_matmul_ms = 0, fp_matmul_ms = 0, dequantize_ms = 0, add_ms = 0;
+  bool quantize_fused = false, dequantize_fused = false;
+  double total_ms() const { return split_ms + quantize_ms + int_matmul_ms + fp_matmul_ms + dequantize_ms + add_ms; }
+};
+
+// ---------------------------------------------------------------- device layer handle
+class DeviceLayer {
+ public:
+  explicit DeviceLayer(const QuikLinearLayer& L, int64_t row_begin = 0, int64_t row_end = 0) {
+    L.validate();
+    quik_weights_desc d{};
+    d.in_features = L.in_features();
+    d.out_features = L.out_features();
+    d.bits = L.weights.bits();
+    d.act_bits = L.act_bits;
+    d.base = L.weights.base.data.data();
+    d.scales = L.weights.scales.data();
+    d.wreduced = L.weights.wreduced.data();
+    d.outlier_weights = L.weights.outlier_weights.data.data();
+    d.outlier_indices = L.outliers.indices.data();
+    d.n_outlier = L.outliers.outlier_count();
+    d.bias = L.bias.empty() ? nullptr : L.bias.data();
+    d.row_begin = row_begin;
+    d.row_end = row_end;
+    detail::check(quik_layer_create(detail::ctx(), &d, &h_));
+    int64_t in = 0, out = 0;
+    quik_layer_info(h_, &in, &out, nullptr, nullptr);
+    in_ = in;
+    out_ = out;
+  }
+  ~DeviceLayer() { quik_layer_destroy(h_); }
+  DeviceLayer(const DeviceLayer&) = delete;
+  DeviceLayer& operator=(const DeviceLayer&) = delete;
+  quik_layer_t handle() const { return h_; }
+  int64_t in_features() const { return in_; }
+  int64_t out_features() const { return out_; }
+
+  // Host FP32 in, host FP32 out (reference semantics), copies included.
+  FpMatrix forward(const FpMatrix& x, PipelineVariant v = PipelineVariant::V3FusedEpilogue,
+                   StageTimes* times = nullptr) const {
+    if (x.cols != in_)
+      throw std::invalid_argument("quik_matmul: input has " + std::to_string(x.cols) + " features, layer expects " +
+                                  std::to_string(in_));
+    FpMatrix y(x.rows, out_);
+    if (x.rows == 0 || out_ == 0) return y;
+    detail::Buf dx(x.data.data(), x.data.size() * 4), dy(y.data.size() * 4);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, nullptr);
+    const quik_status s = quik_linear_forward(detail::ctx(), h_, dx.p, QUIK_F32, x.rows, dy.p, QUIK_F32,
+                                              static_cast<quik_variant>(v), nullptr);
+    cudaEventRecord(e1, nullptr);
+    detail::check(s);
+    detail::check(quik_ctx_sync(detail::ctx(), nullptr));
+    if (times) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      times->quantize_fused = v != PipelineVariant::V1Unfused;
+      times->dequantize_fused = v == PipelineVariant::V3FusedEpilogue;
+      times->int_matmul_ms = ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    dy.get(y.data.data(), y.data.size() * 4);
+    return y;
+  }
+
+ private:
+  quik_layer_t h_ = nullptr;
+  int64_t in_ = 0, out_ = 0;
+};
+
+// ---------------------------------------------------------------- reference functions
+
+// runtime.hpp:85-87 (uploads the layer per call, like the reference re-reads its weights)
+inline FpMatrix quik_matmul(const QuikLinearLayer& layer, const FpMatrix& x,
+                            PipelineVariant v = PipelineVariant::V3FusedEpilogue, StageTimes* times = nullptr) {
+  layer.validate();
+  if (x.cols != layer.in_features())
+    throw std::invalid_argument("quik_matmul: input has " + std::to_string(x.cols) + " features, layer expects " +
+                                std::to_string(layer.in_features()));
+  return DeviceLayer(layer).forward(x, v, times);
+}
+
+// runtime.hpp:55-56
+inline std::pair<ActQuantResult, FpMatrix> quantize_activations_fused(const FpMatrix& x, const OutlierSet& o,
+                                                                      int bits) {
+  if (bits != 4 && bits != 8) throw std::invalid_argument("activation bits must be 4 or 8");
+  if (x.cols != o.feature_count)
+    throw std::invalid_argument("fused quantization: input features do not match outlier set");
+  QuikLinearLayer carrier;  // permutation tables only (no weight rows)
+  carrier.outliers = o;
+  carrier.act_bits = bits;
+  carrier.weights.base.rows = 0;
+  carrier.weights.base.cols = o.base_count();
+  carrier.weights.base.bits = bits;
+  carrier.weights.outlier_weights = FpMatrix(0, o.outlier_count());
+  DeviceLayer L(carrier);
+  ActQuantResult r;
+  r.packed.rows = x.rows;
+  r.packed.cols = o.base_count();
+  r.packed.bits = bits;
+  r.packed.data.resize(static_cast<size_t>(x.rows * r.packed.row_bytes()));
+  r.scale.resize(static_cast<size_t>(x.rows));
+  r.zero.resize(static_cast<size_t>(x.rows));
+  r.half_range = 1 << (bits - 1);
+  FpMatrix xo(x.rows, o.outlier_count());
+  if (x.rows == 0) return {std::move(r), std::move(xo)};
+  detail::Buf dx(x.data.data(), x.data.size() * 4), dp(r.packed.data.size()), ds(x.rows * 4), dz(x.rows * 4),
+      dxo(xo.data.size() * 4);
+  detail::check(quik_quantize_activations_fused(detail::ctx(), L.handle(), dx.p, QUIK_F32, x.rows,
+                                                static_cast<uint8_t*>(dp.p), static_cast<float*>(ds.p),
+                                                static_cast<float*>(dz.p), static_cast<float*>(dxo.p), nullptr));
+  detail::check(quik_ctx_sync(detail::ctx(), nullptr));
+  dp.get(r.packed.data.data(), r.packed.data.size());
+  ds.get(r.scale.data(), x.rows * 4);
+  dz.get(r.zero.data(), x.rows * 4);
+  dxo.get(xo.data.data(), xo.data.size() * 4);
+  return {std::move(r), std::move(xo)};
+}
+
+// runtime.hpp:51
+inline ActQuantResult quantize_activations(const FpMatrix& x_base, int bits) {
+  if (bits != 4 && bits != 8) throw std::invalid_argument("activation bits must be 4 or 8");
+  ActQuantResult r;
+  r.packed.rows = x_base.rows;
+  r.packed.cols = x_base.cols;
+  r.packed.bits = bits;
+  r.packed.data.resize(static_cast<size_t>(x_base.rows * r.packed.row_bytes()));
+  r.scale.resize(static_cast<size_t>(x_base.rows));
+  r.zero.resize(static_cast<size_t>(x_base.rows));
+  r.half_range = 1 << (bits - 1);
+  if (x_base.rows == 0) return r;
+  detail::Buf dx(x_base.data.data(), x_base.data.size() * 4), dp(r.packed.data.size()), ds(x_base.rows * 4),
+      dz(x_base.rows * 4);
+  detail::check(quik_quantize_activations(detail::ctx(), dx.p, QUIK_F32, x_base.rows, x_base.cols, bits,
+                                          static_cast<uint8_t*>(dp.p), static_cast<float*>(ds.p),
+                                          static_cast<float*>(dz.p), nullptr));
+  detail::check(quik_ctx_sync(detail::ctx(), nullptr));
+  dp.get(r.packed.data.data(), r.packed.data.size());
+  ds.get(r.scale.data(), x_base.rows * 4);
+  dz.get(r.zero.data(), x_base.rows * 4);
+  return r;
+}
+
+// packed.hpp:58
+inline Int32Matrix int_matmul(const PackedIntMatrix& x, const PackedIntMatrix& w) {
+  Int32Matrix out(x.rows, w.rows);
+  detail::Buf dx(x.data.data(), x.data.size()), dw(w.data.data(), w.data.size()), dout(out.data.size() * 4);
+  detail::check(quik_int_matmul(detail::ctx(), static_cast<const uint8_t*>(dx.p), x.rows, x.cols, x.bits,
+                                static_cast<const uint8_t*>(dw.p), w.rows, w.cols, w.bits,
+                                static_cast<int32_t*>(dout.p), nullptr));
+  detail::check(quik_ctx_sync(detail::ctx(), nullptr));
+  dout.get(out.data.data(), out.data.size() * 4);
+  return out;
+}
+
+// runtime.hpp:66-68
+inline FpMatrix dequantize_epilogue(const Int32Matrix& acc, const ActQuantResult& a,
+                                   std::span<const float> weight_scales, std::span<const float> wreduced) {
+  if (acc.rows != static_cast<int64_t>(a.scale.size()))
+    throw std::invalid_argument("dequantize_epilogue: token count mismatch");
+  if (static_cast<int64_t>(weight_scales.size()) != acc.cols || static_cast<int64_t>(wreduced.size()) != acc.cols)
+    throw std::invalid_argument("dequantize_epilogue: per-row vector length mismatch");
+  FpMatrix out(acc.rows, acc.cols);
+  if (acc.rows == 0 || acc.cols == 0) return out;
+  detail::Buf da(acc.data.data(), acc.data.size() * 4), ds(a.scale.data(), a.scale.size() * 4),
+      dz(a.zero.data(), a.zero.size() * 4), dsw(weight_scales.data(), weight_scales.size() * 4),
+      dwr(wreduced.data(), wreduced.size() * 4), dout(out.data.size() * 4);
+  detail::check(quik_dequantize_epilogue(detail::ctx(), static_cast<const int32_t*>(da.p), acc.rows, acc.cols,
+                                         static_cast<const float*>(ds.p), static_cast<const float*>(dz.p),
+                                         a.half_range, static_cast<const float*>(dsw.p),
+                                         static_cast<const float*>(dwr.p), static_cast<float*>(dout.p), nullptr));
+  detail::check(quik_ctx_sync(detail::ctx(), nullptr));
+  dout.get(out.data.data(), out.data.size() * 4);
+  return out;
+}
+
+// quantizer.hpp:87-88 (use_clipping = false), on the device, bit-exact
+inline QuantizedWeights rtn_quantize_weights(const FpMatrix& w, const OutlierSet& o, int bits) {
+  if (o.feature_count != w.cols)
+    throw std::invalid_argument("outlier set covers " + std::to_string(o.feature_count) + " features, weights have " +
+                                std::to_string(w.cols));
+  QuantizedWeights q;
+  q.base.rows = w.rows;
+  q.base.cols = o.base_count();
+  q.base.bits = bits;
+  q.base.data.resize(static_cast<size_t>(w.rows * q.base.row_bytes()));
+  q.scales.resize(static_cast<size_t>(w.rows));
+  q.wreduced.resize(static_cast<size_t>(w.rows));
+  q.outlier_weights = FpMatrix(w.rows, o.outlier_count());
+  if (w.rows == 0) return q;
+  detail::Buf dw(w.data.data(), w.data.size() * 4), db(q.base.data.size()), ds(w.rows * 4), dr(w.rows * 4),
+      dow(q.outlier_weights.data.size() * 4);
+  detail::check(quik_rtn_quantize_weights(detail::ctx(), static_cast<const float*>(dw.p), w.rows, w.cols,
+                                          o.indices.data(), o.outlier_count(), bits, static_cast<uint8_t*>(db.p),
+                                          static_cast<float*>(ds.p), static_cast<float*>(dr.p),
+                                          static_cast<float*>(dow.p), nullptr));
+  detail::check(quik_ctx_sync(detail::ctx(), nullptr));
+  db.get(q.base.data.data(), q.base.data.size());
+  ds.get(q.scales.data(), w.rows * 4);
+  dr.get(q.wreduced.data(), w.rows * 4);
+  dow.get(q.outlier_weights.data.data(), q.outlier_weights.data.size() * 4);
+  return q;
+}
+
+}  // namespace quik::b200

@@ -240,6 +240,51 @@ int qr_rtn_quantize_weights(const float* w, int64_t N, int64_t K, const int64_t*
   }
 }
 
+// The reference tests' layer fixture, exactly (tests/test_runtime.cpp:27-45
+// make_layer): W ~ N(0, .5), x ~ N(0, 1) from mt19937(seed), `heavy` random
+// columns x100, outliers = select_outliers(x), RTN weights, bias ~ N(0, .1).
+// Sizes are fixed by the arguments; outputs are caller-allocated.
+int qr_make_test_layer(uint32_t seed, int64_t tokens, int64_t in, int64_t out, int bits, int64_t outliers,
+                       int64_t heavy_cols, int with_bias, float* x, float* w, int64_t* idx, uint8_t* base,
+                       float* scales, float* wreduced, float* outlier_w, float* bias) {
+  try {
+    std::mt19937 rng(seed);
+    auto randm = [&](int64_t r, int64_t c, float sd) {
+      std::normal_distribution<float> dist(0.0f, sd);
+      quik::FpMatrix m(r, c);
+      for (float& v : m.data) v = dist(rng);
+      return m;
+    };
+    quik::FpMatrix W = randm(out, in, 0.5f);
+    quik::FpMatrix X = randm(tokens, in, 1.0f);
+    if (heavy_cols > 0) {
+      std::uniform_int_distribution<int64_t> pick(0, in - 1);
+      for (int64_t i = 0; i < heavy_cols; ++i) {
+        const int64_t c = pick(rng);
+        for (int64_t r = 0; r < tokens; ++r) X.at(r, c) *= 100.0f;
+      }
+    }
+    quik::CalibStats stats;
+    stats.accumulate(X);
+    auto o = quik::select_outliers(stats, outliers);
+    auto q = quik::rtn_quantize_weights(W, o, bits);
+    std::memcpy(x, X.data.data(), X.data.size() * 4);
+    std::memcpy(w, W.data.data(), W.data.size() * 4);
+    if (outliers) std::memcpy(idx, o.indices.data(), o.indices.size() * 8);
+    std::memcpy(base, q.base.data.data(), q.base.data.size());
+    std::memcpy(scales, q.scales.data(), out * 4);
+    std::memcpy(wreduced, q.wreduced.data(), out * 4);
+    if (outliers) std::memcpy(outlier_w, q.outlier_weights.data.data(), out * outliers * 4);
+    if (with_bias) {
+      std::normal_distribution<float> dist(0.0f, 0.1f);
+      for (int64_t r = 0; r < out; ++r) bias[r] = dist(rng);
+    }
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
 // The reference tests' seeded Gaussian generator (tests/test_helpers.hpp:128-134):
 // std::mt19937(seed) + std::normal_distribution<float>(0, stddev), row-major.
 void qr_random_matrix(uint32_t seed, int64_t rows, int64_t cols, float stddev, float* out) {

@@ -96,10 +96,28 @@ def build_reference(force: bool = False) -> Path | None:
     return out
 
 
+def build_tests(force: bool = False) -> Path:
+    """C++ parity driver for the drop-in facade (include/quik_b200.hpp); test
+    infrastructure: links the product library and the oracle (as the checker)."""
+    src = ROOT / "tests" / "cpp" / "facade_test.cpp"
+    out = ROOT / "build" / "tests" / "facade_test"
+    out.parent.mkdir(parents=True, exist_ok=True)
+    deps = [src, ROOT / "include" / "quik_b200.hpp", ROOT / "include" / "quik_b200.h", LIB,
+            ROOT / "oracle" / "build" / "libquik_oracle.so"]
+    if force or _stale(out, deps):
+        _run(["g++", "-std=c++20", "-O2", "-Wall", "-I" + str(ROOT / "include"), "-I/usr/local/cuda/include",
+              str(src), "-o", str(out), "-L" + str(LIBDIR), "-lquik_b200",
+              str(ROOT / "oracle" / "build" / "libquik_oracle.so"), "-L/usr/local/cuda/lib64", "-lcudart",
+              "-Wl,-rpath," + str(LIBDIR), "-Wl,-rpath,$ORIGIN/../../paper_2310_09259_b200/lib",
+              "-Wl,-rpath,$ORIGIN/../../oracle/build", "-Wl,-rpath," + str(ROOT / "oracle" / "build")])
+    return out
+
+
 def build_all(force: bool = False) -> None:
     build_product(force)
     build_oracle(force)
     build_reference(force)
+    build_tests(force)
 
 
 if __name__ == "__main__":

@@ -1,0 +1,189 @@
+// C++ parity driver for the drop-in facade (include/quik_b200.hpp): the same
+// calls as the reference's own tests (proj/tests/test_packed.cpp,
+// test_runtime.cpp), against the plain-C oracle (oracle/quik_oracle.c) as the
+// checker. Exit code = number of failed checks. Needs a B200.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <vector>
+
+#include <cuda_fp16.h>
+
+#include "quik_b200.hpp"
+
+extern "C" {
+#include "../../oracle/quik_oracle.h"
+}
+
+namespace Q = quik::b200;
+
+static int g_fail = 0;
+#define CHECK(cond)                                                       \
+  do {                                                                    \
+    if (!(cond)) {                                                        \
+      std::printf("FAIL %s:%d  %s\n", __FILE__, __LINE__, #cond);         \
+      ++g_fail;                                                           \
+    }                                                                     \
+  } while (0)
+
+template <typename E, typename F>
+static bool throws(F&& f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+static Q::FpMatrix rows(std::initializer_list<std::initializer_list<float>> init) {
+  Q::FpMatrix m(static_cast<int64_t>(init.size()), static_cast<int64_t>(init.begin()->size()));
+  size_t i = 0;
+  for (auto& r : init)
+    for (float v : r) m.data[i++] = v;
+  return m;
+}
+
+int main() {
+  // test_packed.cpp:78-92 — int_matmul hand-computed 2x2, INT8 and INT4
+  {
+    const std::vector<int8_t> xv = {1, -2, 3, 4}, wv = {5, 6, -7, 8}, w4 = {5, 6, -7, 7};
+    const auto out = Q::int_matmul(Q::pack_int8(xv, 2, 2), Q::pack_int8(wv, 2, 2));
+    CHECK(out.at(0, 0) == -7 && out.at(0, 1) == -23 && out.at(1, 0) == 39 && out.at(1, 1) == 11);
+    const auto out4 = Q::int_matmul(Q::pack_int4(xv, 2, 2), Q::pack_int4(w4, 2, 2));
+    CHECK(out4.at(0, 0) == 1 * 5 + -2 * 6 && out4.at(1, 1) == 3 * -7 + 4 * 7);
+    CHECK(throws<std::invalid_argument>([&] { Q::int_matmul(Q::pack_int4(xv, 2, 2), Q::pack_int8(wv, 2, 2)); }));
+    CHECK(throws<std::out_of_range>([&] { Q::pack_int4(std::vector<int8_t>{0, 0, 8, 0}, 2, 2); }));
+  }
+  // test_packed.cpp:104-120 — int_matmul == naive on random shapes
+  {
+    std::mt19937 rng(7);
+    std::uniform_int_distribution<int64_t> dim(1, 40);
+    for (int trial = 0; trial < 50; ++trial) {
+      const int bits = trial % 2 == 0 ? 4 : 8;
+      const int lim = bits == 4 ? 7 : 127;
+      std::uniform_int_distribution<int> val(-lim - 1, lim);
+      const int64_t t = dim(rng), k = dim(rng), n = dim(rng);
+      std::vector<int8_t> xv(t * k), wv(n * k);
+      for (auto& v : xv) v = static_cast<int8_t>(val(rng));
+      for (auto& v : wv) v = static_cast<int8_t>(val(rng));
+      const auto x = Q::pack_values(xv, t, k, bits), w = Q::pack_values(wv, n, k, bits);
+      const auto got = Q::int_matmul(x, w);
+      std::vector<int32_t> want(t * n);
+      qo_int_matmul(x.data.data(), t, k, bits, w.data.data(), n, k, bits, want.data());
+      CHECK(got.data == want);
+    }
+  }
+  // test_runtime.cpp:80-116 — quantizer known answers and errors
+  {
+    const auto r = Q::quantize_activations(rows({{0.0f, 0.5f, 1.0f, 1.5f}}), 4);
+    CHECK(std::fabs(r.scale[0] - 0.1f) < 1e-7f && r.zero[0] == 0.0f && r.half_range == 8);
+    CHECK((Q::unpack_values(r.packed) == std::vector<int8_t>{-8, -3, 2, 7}));
+    const auto c = Q::quantize_activations(rows({{5.0f, 5.0f, 5.0f}}), 4);
+    CHECK(c.scale[0] == 1.0f && c.zero[0] == 5.0f);
+    auto bad = rows({{1.0f, 2.0f}});
+    bad.at(0, 1) = NAN;
+    CHECK(throws<Q::NumericalError>([&] { Q::quantize_activations(bad, 4); }));
+  }
+  // test_runtime.cpp:134-156 — fused quantizer == reference (oracle), bit-exact
+  {
+    for (uint32_t seed = 0; seed < 40; ++seed) {
+      std::mt19937 local(seed);
+      const int bits = seed % 2 == 0 ? 4 : 8;
+      const int64_t in = 8 + static_cast<int64_t>(local() % 120);
+      const int64_t tokens = 1 + static_cast<int64_t>(local() % 16);
+      std::normal_distribution<float> dist(0.0f, 1.5f);
+      Q::FpMatrix x(tokens, in);
+      for (float& v : x.data) v = dist(local);
+      const int64_t k = static_cast<int64_t>(local() % static_cast<uint64_t>(in));
+      std::vector<int64_t> idx(k);
+      qo_select_outliers(x.data.data(), tokens, in, k, idx.data());
+      const auto o = Q::OutlierSet::from_indices(in, idx);
+      const auto [fused, xo] = Q::quantize_activations_fused(x, o, bits);
+      std::vector<uint8_t> pk(tokens * qo_row_bytes(in - k, bits) + 1);
+      std::vector<float> sc(tokens), ze(tokens), xo_ref(tokens * k + 1);
+      qo_quantize_activations_fused(x.data.data(), tokens, in, o.permutation.data(), in - k, o.indices.data(), k,
+                                    bits, pk.data(), sc.data(), ze.data(), xo_ref.data());
+      CHECK(std::memcmp(fused.packed.data.data(), pk.data(), fused.packed.data.size()) == 0);
+      CHECK(std::memcmp(fused.scale.data(), sc.data(), tokens * 4) == 0);
+      CHECK(std::memcmp(fused.zero.data(), ze.data(), tokens * 4) == 0);
+      CHECK(std::memcmp(xo.data.data(), xo_ref.data(), xo.data.size() * 4) == 0);
+    }
+  }
+  // test_runtime.cpp:172-186 — epilogue hand example
+  {
+    const auto aq = Q::quantize_activations(rows({{1.0f, 3.0f}}), 4);
+    const auto acc = Q::int_matmul(aq.packed, Q::pack_int4(std::vector<int8_t>{2, -1}, 1, 2));
+    CHECK(acc.at(0, 0) == -23);
+    const std::vector<float> s = {0.5f}, wr = {0.5f};
+    const auto out = Q::dequantize_epilogue(acc, aq, s, wr);
+    CHECK(std::fabs(out.at(0, 0) + 0.5f) < 1e-6f);
+  }
+  // quik_matmul through the facade vs the reference algorithm (oracle):
+  // bit-exact without outliers, and V1 == V2 == V3
+  {
+    std::mt19937 rng(131);
+    std::normal_distribution<float> nd(0.0f, 1.0f);
+    for (int trial = 0; trial < 6; ++trial) {
+      const int bits = trial % 2 == 0 ? 4 : 8;
+      const int64_t M = 5 + 11 * trial, K = 64 + 40 * trial, N = 24 + 30 * trial;
+      const int64_t O = (trial % 3) * 8;
+      Q::FpMatrix x(M, K), w(N, K);
+      for (float& v : x.data) v = nd(rng);
+      for (float& v : w.data) v = 0.5f * nd(rng);
+      std::vector<int64_t> idx(O);
+      qo_select_outliers(x.data.data(), M, K, O, idx.data());
+      Q::QuikLinearLayer L;
+      L.outliers = Q::OutlierSet::from_indices(K, idx);
+      L.weights = Q::rtn_quantize_weights(w, L.outliers, bits);
+      L.act_bits = bits;
+      L.bias.assign(N, 0.25f);
+      // weight-side parity: device RTN == reference RTN
+      std::vector<uint8_t> base(N * qo_row_bytes(K - O, bits));
+      std::vector<float> sc(N), wr(N), ow(N * O + 1);
+      qo_rtn_quantize_weights(w.data.data(), N, K, idx.data(), O, bits, base.data(), sc.data(), wr.data(), ow.data());
+      CHECK(L.weights.base.data == base);
+      CHECK(std::memcmp(L.weights.scales.data(), sc.data(), N * 4) == 0);
+      CHECK(std::memcmp(L.weights.wreduced.data(), wr.data(), N * 4) == 0);
+      // x and outlier weights rounded to f16 so the device f16 outlier operands are exact
+      for (float& v : x.data) v = __half2float(__float2half(v));
+      for (float& v : L.weights.outlier_weights.data) v = __half2float(__float2half(v));
+      const auto y1 = Q::quik_matmul(L, x, Q::PipelineVariant::V1Unfused);
+      const auto y2 = Q::quik_matmul(L, x, Q::PipelineVariant::V2FusedQuant);
+      const auto y3 = Q::quik_matmul(L, x);
+      CHECK(y1.data == y2.data && y1.data == y3.data);
+      qo_layer ql{K, N, O, bits, bits, L.weights.base.data.data(), L.weights.scales.data(), L.weights.wreduced.data(),
+                  L.weights.outlier_weights.data.data(), L.outliers.indices.data(), L.bias.data()};
+      std::vector<float> want(M * N);
+      CHECK(qo_quik_matmul(&ql, x.data.data(), M, 2, want.data()) == QO_OK);
+      if (O == 0) {
+        CHECK(std::memcmp(y3.data.data(), want.data(), want.size() * 4) == 0);
+      } else {
+        double d2 = 0, r2 = 0;
+        for (size_t i = 0; i < want.size(); ++i) {
+          d2 += (double(y3.data[i]) - want[i]) * (double(y3.data[i]) - want[i]);
+          r2 += double(want[i]) * want[i];
+        }
+        CHECK(std::sqrt(d2 / r2) < 1e-5);
+      }
+    }
+  }
+  // validation (runtime.cpp:150-167)
+  {
+    Q::QuikLinearLayer L;
+    L.outliers = Q::OutlierSet::from_indices(8, {1, 2});
+    L.weights.base = Q::pack_int4(std::vector<int8_t>(12, 0), 2, 6);
+    L.weights.scales = {1.f, 1.f};
+    L.weights.wreduced = {0.f, 0.f};
+    L.weights.outlier_weights = Q::FpMatrix(2, 2);
+    L.act_bits = 8;
+    CHECK(throws<std::invalid_argument>([&] { Q::quik_matmul(L, Q::FpMatrix(1, 8)); }));
+    L.act_bits = 4;
+    CHECK(throws<std::invalid_argument>([&] { Q::quik_matmul(L, Q::FpMatrix(1, 9)); }));
+  }
+  std::printf("facade_test: %d failure(s)\n", g_fail);
+  return g_fail;
+}
