@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -17,6 +19,23 @@
 #include "kernels.h"
 
 using namespace quikb200;
+
+namespace quikb200 {
+// cudaFuncSetAttribute once per (kernel, device, size): a host call per launch
+// otherwise, which shows up as GPU idle time at small token counts.
+cudaError_t ensure_smem_attr_impl(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = done.find({kernel, dev});
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done[{kernel, dev}] = bytes;
+  return e;
+}
+}  // namespace quikb200
 
 namespace {
 

@@ -28,6 +28,7 @@
 //   warps 4..11 epilogue (TMEM lane quadrant = warp % 4, column half = (warp - 4) / 4)
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "kernels.h"
@@ -65,6 +66,7 @@ struct KParams {
   CUtensorMap tm_xo;  // f16 [M][opad], box {64, BN/CG}
   CUtensorMap tm_y;   // f16 [M][ldo] output, box {32 features, 32 tokens} (valid when tma_store)
   int tma_store;
+  int w_policy;  // L2 policy of the weight tiles: 0 normal, 1 evict_first, 2 evict_last
   int M, N;
   int kb_int, kb_out;
   const float* w_scale;
@@ -133,6 +135,9 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: everything above overlapped the previous
+  // kernel (the quantizer); wait for its results before touching them.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   const int tiles_m = (p.M + BN - 1) / BN;
   const int tiles_n = (p.N + C::kTileRows - 1) / C::kTileRows;
@@ -144,7 +149,8 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_w =
+          p.w_policy == 1 ? policy_evict_first() : (p.w_policy == 2 ? policy_evict_last() : policy_evict_normal());
       const uint64_t pol_x = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
@@ -251,6 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
     uint8_t* my_stage = staging + e * 2 * kStoreBufBytes;
     int sbuf = 0;
     const bool tma_out = kF16Out && p.tma_store;
+    const uint64_t pol_y = policy_evict_first();  // the output is not re-read by this kernel
     int it = 0;
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
       const int b = it & 1;
@@ -313,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&p.tm_y, buf, n0, mb * BN + c);
+            tma_store_2d(&p.tm_y, buf, n0, mb * BN + c, pol_y);
             bulk_commit();
           }
           sbuf ^= 1;
@@ -418,7 +425,7 @@ template <int CG, int BN, int MODE>
 cudaError_t launch_cfg(const KParams& kp, int num_sms, cudaStream_t stream) {
   using C = Cfg<CG, BN>;
   auto kern = quik_gemm_kernel<CG, BN, MODE>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  cudaError_t e = ensure_smem_attr(kern, C::kSmemBytes);
   if (e != cudaSuccess) return e;
   const long long tiles = static_cast<long long>((kp.M + BN - 1) / BN) * ((kp.N + C::kTileRows - 1) / C::kTileRows);
   const int max_clusters = num_sms / CG;
@@ -429,13 +436,15 @@ cudaError_t launch_cfg(const KParams& kp, int num_sms, cudaStream_t stream) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = C::kSmemBytes;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (kernel waits via griddepcontrol)
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kern, kp);
 }
 
@@ -493,6 +502,11 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
       return cudaErrorInvalidValue;
     }
   }
+  static const int w_policy = [] {
+    const char* e = getenv("QUIK_W_L2_POLICY");
+    return e ? atoi(e) : 0;
+  }();
+  kp.w_policy = w_policy;
   kp.tma_store = 0;
   if ((a.mode == kModeF16 || a.mode == kModeAccInitF16) && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 &&
       (a.ldo * 2) % 16 == 0) {

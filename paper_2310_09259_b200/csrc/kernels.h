@@ -16,6 +16,14 @@ constexpr int kBlockM = 128;       // UMMA M (weight rows / output features per 
 
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and device
+// (it is a host-side call per launch otherwise, visible at small M).
+cudaError_t ensure_smem_attr_impl(const void* kernel, int bytes);  // capi.cu
+template <typename K>
+cudaError_t ensure_smem_attr(K kernel, int bytes) {
+  return ensure_smem_attr_impl(reinterpret_cast<const void*>(kernel), bytes);
+}
+
 // Output of the fused layer: y = f16/f32( (bias + dequant(acc)) + x_out . W_out^T ),
 // where the outlier product is accumulated by the tensor cores onto the f32
 // value bias + dequant(acc) held in TMEM (SURVEY.md A.3 tolerance; bit-exact

@@ -42,6 +42,8 @@ __device__ __forceinline__ float elem(const uint4& v, int e) {
 // other elements (about 5e-4 of them; exact .5 ties among them) take the IEEE
 // quotient, rounded half away from zero. Bit-identical to the reference.
 __device__ __forceinline__ float quant_slow(float d, float scale) { return round_half_away(__fdiv_rn(d, scale)); }
+// |qa - round(qa)| >= kNearTie  <=>  qa within 2^-12 of a half-integer (a rounding
+// boundary of lround); such elements take the exact IEEE quotient.
 constexpr float kNearTie = 0.5f - 2.44140625e-4f;
 
 __device__ __forceinline__ unsigned long long f32x2_pack(float lo, float hi) {
@@ -88,7 +90,9 @@ __device__ __forceinline__ uint32_t h22u(__half2 h) {
 // minimum, which is resolved exactly: when the row minimum compares equal to 0
 // the sign of the lowest-index zero wins (only the sign of vmin reaches an
 // output; vmax's sign cannot change range = vmax - vmin).
-template <typename T, int BITS, int VPT>
+// FULL: nvec == blockDim * VPT, K % E == 0 and the row is 16-byte aligned (host
+// checked): no bounds checks or tails in the unrolled register code.
+template <typename T, int BITS, int VPT, bool FULL>
 __global__ void __launch_bounds__(512) quantize_rows_kernel(const QuantArgs a) {
   extern __shared__ __align__(16) uint8_t s_dyn[];
   __shared__ float s_min[16], s_max[16];
@@ -98,6 +102,9 @@ __global__ void __launch_bounds__(512) quantize_rows_kernel(const QuantArgs a) {
   constexpr int kHr = 1 << (BITS - 1);
   constexpr float kLevels = static_cast<float>((1 << BITS) - 1);
 
+  // let the dependent GEMM launch and run its prologue while this grid finishes
+  // (it waits for this grid's completion with griddepcontrol.wait)
+  asm volatile("griddepcontrol.launch_dependents;");
   const int t = blockIdx.x;
   const int tid = threadIdx.x;
   const int nt = blockDim.x;
@@ -109,7 +116,7 @@ __global__ void __launch_bounds__(512) quantize_rows_kernel(const QuantArgs a) {
   uint8_t* s_codes = s_dyn;
   uint4* s_row = reinterpret_cast<uint4*>(s_dyn + code_bytes);
   const T* src = reinterpret_cast<const T*>(a.x) + static_cast<int64_t>(t) * a.ldx;
-  const bool vec_ok = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && (K % E == 0);
+  const bool vec_ok = FULL || (((reinterpret_cast<uintptr_t>(src) & 15) == 0) && (K % E == 0));
   const bool has_out = a.lane_mask != nullptr;
 
   uint4 raw[VPT];
@@ -120,7 +127,7 @@ __global__ void __launch_bounds__(512) quantize_rows_kernel(const QuantArgs a) {
     raw[i] = make_uint4(0, 0, 0, 0);
     lm[i] = 0xFFFFFFFFu;
     if (E == 8) lm[i] = 0xFFFFFFFFu;  // E == 8: two words, see lm_hi
-    if (v < nvec) {
+    if (FULL || v < nvec) {
       if (vec_ok) {
         raw[i] = __ldg(reinterpret_cast<const uint4*>(src) + v);
       } else {
@@ -137,7 +144,7 @@ __global__ void __launch_bounds__(512) quantize_rows_kernel(const QuantArgs a) {
   for (int i = 0; i < VPT; ++i) {
     const int v = tid + i * nt;
     lm_hi[i] = 0xFFFFFFFFu;
-    if (v < nvec) {
+    if (FULL || v < nvec) {
       const int c0 = v * E;
       if (has_out) {
         if (E == 8) {
@@ -151,13 +158,27 @@ __global__ void __launch_bounds__(512) quantize_rows_kernel(const QuantArgs a) {
         lm[i] = 0u;
         lm_hi[i] = 0u;
       }
-      if (c0 + E > K) {  // row tail: columns >= K excluded
+      if (!FULL && c0 + E > K) {  // row tail: columns >= K excluded
 #pragma unroll
         for (int e = 0; e < E; ++e)
           if (c0 + e >= K) {
             if (e < 4) lm[i] |= 0xFFu << (8 * e);
             else lm_hi[i] |= 0xFFu << (8 * (e - 4));
           }
+      }
+    }
+  }
+
+  // prefetch the gather-table entries of this thread's first two output chunks
+  const int nchunk = a.q8 ? static_cast<int>(a.kpad / 16) : 0;
+  uint4 gpre[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+  if (has_out) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int cidx = tid + k * nt;
+      if (cidx < nchunk) {
+        gpre[2 * k] = __ldg(reinterpret_cast<const uint4*>(a.gather + cidx * 16));
+        gpre[2 * k + 1] = __ldg(reinterpret_cast<const uint4*>(a.gather + cidx * 16 + 8));
       }
     }
   }
@@ -228,7 +249,7 @@ __global__ void __launch_bounds__(512) quantize_rows_kernel(const QuantArgs a) {
 #pragma unroll 1
     for (int i = 0; i < VPT; ++i) {
       const int v = tid + i * nt;
-      if (v >= nvec) break;
+      if (!FULL && v >= nvec) break;
       uint4 rv = make_uint4(0, 0, 0, 0);
 #pragma unroll
       for (int j = 0; j < VPT; ++j)
@@ -269,40 +290,52 @@ __global__ void __launch_bounds__(512) quantize_rows_kernel(const QuantArgs a) {
   }
   const unsigned long long vmin2 = f32x2_pack(vmin, vmin);
   const unsigned long long rcp2 = f32x2_pack(rcp, rcp);
+  constexpr float kMagic = 12582912.0f - static_cast<float>(kHr);  // 1.5 * 2^23 - half_range
+  const unsigned long long magic2 = f32x2_pack(kMagic, kMagic);
 
   // ---- pass 2: codes for every column (outlier lanes produce ignored codes)
   uint32_t near_vec = 0;  // bit i: vector i has an element near a rounding boundary
 #pragma unroll
   for (int i = 0; i < VPT; ++i) {
     const int v = tid + i * nt;
-    if (v >= nvec) continue;
-    bool near_any = false;
+    if (!FULL && v >= nvec) continue;
+    // qa = (x - vmin) * fl(1/scale) (FADD2/FMUL2); t = qa + (1.5*2^23 - hr) rounds qa
+    // to the nearest integer inside the mantissa, whose low byte is then the signed
+    // code (q - hr) directly; r = qa - round(qa) tells how close qa is to a
+    // rounding boundary (see quant_q / kNearTie). No float->int conversions.
+    // ptxas may contract the packed mul+add into FFMA2 (t = rn(d*rcp + magic)); the
+    // exactness argument holds either way: the unrounded product is even closer to
+    // d/scale (<= 3.1e-5 at the top of the range) than fl(d*rcp), and the margin to
+    // kNearTie is 2^-12, so an element is either flagged or its rounding is exact.
     float x[E];
-    int code[E];
+    uint32_t tb[E];
+    float rmax = 0.0f;
 #pragma unroll
     for (int e = 0; e < E; ++e) x[e] = elem<T>(raw[i], e);
 #pragma unroll
     for (int e = 0; e < E; e += 2) {
-      float d0, d1, q0, q1;
-      sub_mul_x2(x[e], x[e + 1], vmin2, rcp2, d0, d1, q0, q1);
-      const float u0 = __fadd_rn(q0, 0.5f), u1 = __fadd_rn(q1, 0.5f);
-      const float f0 = floorf(u0), f1 = floorf(u1);
-      near_any |= fabsf(__fsub_rn(__fsub_rn(u0, f0), 0.5f)) >= kNearTie;
-      near_any |= fabsf(__fsub_rn(__fsub_rn(u1, f1), 0.5f)) >= kNearTie;
-      code[e] = static_cast<int>(f0);
-      code[e + 1] = static_cast<int>(f1);
+      unsigned long long d2, qa2, t2, rq2, r2;
+      asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d2) : "l"(f32x2_pack(x[e], x[e + 1])), "l"(vmin2));
+      asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(qa2) : "l"(d2), "l"(rcp2));
+      asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t2) : "l"(qa2), "l"(magic2));
+      asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(rq2) : "l"(t2), "l"(magic2));
+      asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r2) : "l"(qa2), "l"(rq2));
+      float r0, r1;
+      f32x2_unpack(r2, r0, r1);
+      rmax = fmaxf(rmax, fmaxf(fabsf(r0), fabsf(r1)));
+      tb[e] = static_cast<uint32_t>(t2);
+      tb[e + 1] = static_cast<uint32_t>(t2 >> 32);
     }
-    // codes are in [0, levels] for finite rows (no clamp needed: d >= 0 and
-    // qa <= levels * (1 + 2^-22)); pack as signed bytes (q - half_range)
-    uint32_t w0 = 0, w1 = 0;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const uint32_t b = static_cast<uint32_t>(code[e] - kHr) & 0xFFu;
-      if (e < 4) w0 |= b << (8 * e);
-      else w1 |= b << (8 * (e - 4));
+    const bool near_any = !(rmax < kNearTie);  // also catches NaN (flagged rows)
+    // codes are in [0, levels] for finite rows (d >= 0, qa <= levels * (1 + 2^-22))
+    const uint32_t w0 = __byte_perm(__byte_perm(tb[0], tb[1], 0x0040), __byte_perm(tb[2], tb[3], 0x0040), 0x5410);
+    if (E == 8) {
+      const uint32_t w1 =
+          __byte_perm(__byte_perm(tb[4 % E], tb[5 % E], 0x0040), __byte_perm(tb[6 % E], tb[7 % E], 0x0040), 0x5410);
+      *reinterpret_cast<uint2*>(s_codes + v * E) = make_uint2(w0, w1);
+    } else {
+      *reinterpret_cast<uint32_t*>(s_codes + v * E) = w0;
     }
-    if (E == 8) *reinterpret_cast<uint2*>(s_codes + v * E) = make_uint2(w0, w1);
-    else *reinterpret_cast<uint32_t*>(s_codes + v * E) = w0;
     near_vec |= (near_any ? 1u : 0u) << i;
   }
   if (near_vec) {
@@ -317,8 +350,9 @@ __global__ void __launch_bounds__(512) quantize_rows_kernel(const QuantArgs a) {
         const int c = v * E + e;
         if (c >= K) break;
         const float d = __fsub_rn(to_float(row[c]), vmin);
-        const float u = __fadd_rn(__fmul_rn(d, rcp), 0.5f);
-        if (fabsf(__fsub_rn(__fsub_rn(u, floorf(u)), 0.5f)) >= kNearTie)
+        const float qa = __fmul_rn(d, rcp);
+        const float r = __fsub_rn(qa, __fsub_rn(__fadd_rn(qa, kMagic), kMagic));
+        if (!(fabsf(r) < kNearTie))
           s_codes[c] = static_cast<uint8_t>(static_cast<int>(quant_slow(d, scale)) - kHr);
       }
     }
@@ -341,30 +375,36 @@ __global__ void __launch_bounds__(512) quantize_rows_kernel(const QuantArgs a) {
     for (int i = tid; i < a.opad; i += nt) a.xo16[static_cast<int64_t>(t) * a.opad + i] = __float2half_rn(0.0f);
   }
 
-  // ---- compacted code row: base position j <- column gather[j] (16 per thread)
+  // ---- compacted code row: base position j <- column gather[j] (16 per thread;
+  // the first two chunks' gather entries were prefetched at kernel start)
   if (a.q8) {
     uint4* dst = reinterpret_cast<uint4*>(a.q8 + static_cast<int64_t>(t) * a.kpad);
-    const int nchunk = static_cast<int>(a.kpad / 16);
-    for (int cidx = tid; cidx < nchunk; cidx += nt) {
+#pragma unroll 1
+    for (int k = 0, cidx = tid; cidx < nchunk; ++k, cidx += nt) {
       const int j0 = cidx * 16;
       uint32_t w[4];
       if (has_out) {
-        const uint4 g0 = __ldg(reinterpret_cast<const uint4*>(a.gather + j0));
-        const uint4 g1 = __ldg(reinterpret_cast<const uint4*>(a.gather + j0 + 8));
+        uint4 g0, g1;
+        if (k == 0) { g0 = gpre[0]; g1 = gpre[1]; }
+        else if (k == 1) { g0 = gpre[2]; g1 = gpre[3]; }
+        else {
+          g0 = __ldg(reinterpret_cast<const uint4*>(a.gather + j0));
+          g1 = __ldg(reinterpret_cast<const uint4*>(a.gather + j0 + 8));
+        }
         const uint32_t gi[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t b0 = s_codes[gi[2 * k] & 0xFFFFu], b1 = s_codes[gi[2 * k] >> 16];
-          const uint32_t b2 = s_codes[gi[2 * k + 1] & 0xFFFFu], b3 = s_codes[gi[2 * k + 1] >> 16];
-          w[k] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint32_t b0 = s_codes[gi[2 * kk] & 0xFFFFu], b1 = s_codes[gi[2 * kk] >> 16];
+          const uint32_t b2 = s_codes[gi[2 * kk + 1] & 0xFFFFu], b3 = s_codes[gi[2 * kk + 1] >> 16];
+          w[kk] = __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
         }
       } else {
         const uint4 c = *reinterpret_cast<const uint4*>(s_codes + j0);
         w[0] = c.x; w[1] = c.y; w[2] = c.z; w[3] = c.w;
         if (j0 + 16 > kb) {  // zero the pad positions j >= kb
 #pragma unroll
-          for (int k = 0; k < 16; ++k)
-            if (j0 + k >= kb) w[k >> 2] &= ~(0xFFu << (8 * (k & 3)));
+          for (int kk = 0; kk < 16; ++kk)
+            if (j0 + kk >= kb) w[kk >> 2] &= ~(0xFFu << (8 * (kk & 3)));
         }
       }
       dst[cidx] = make_uint4(w[0], w[1], w[2], w[3]);
@@ -532,17 +572,36 @@ template <typename T, int B>
 cudaError_t launch_quantize_t(const QuantArgs& a, cudaStream_t stream) {
   constexpr int E = 16 / sizeof(T);
   const int64_t nvec = (a.K + E - 1) / E;
-  const int threads = nvec > 256 * 4 ? 512 : 256;
-  const int64_t vpt = (nvec + threads - 1) / threads;
+  int threads = nvec > 256 * 4 ? 512 : 256;
+  int64_t vpt = (nvec + threads - 1) / threads;
   if (vpt > 16) return cudaErrorInvalidValue;  // row wider than 512 x 16 vectors
+  // exact fit (no bounds checks): threads * vpt == nvec with 16-byte aligned rows
+  bool full = false;
+  const bool aligned = (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && (a.ldx * static_cast<int64_t>(sizeof(T))) % 16 == 0 &&
+                       a.K % E == 0;
+  if (aligned) {
+    for (int v : {4, 8, 2, 1}) {
+      if (nvec % v == 0 && (nvec / v) % 32 == 0 && nvec / v >= 64 && nvec / v <= 512) {
+        threads = static_cast<int>(nvec / v);
+        vpt = v;
+        full = true;
+        break;
+      }
+    }
+  }
   const size_t smem = static_cast<size_t>(round_up(a.K, 16) + 16) + static_cast<size_t>(nvec) * 16;
   const dim3 grid(static_cast<unsigned>(a.M));
 #define QUIK_Q_LAUNCH(V)                                                                                   \
   do {                                                                                                     \
-    cudaError_t e = cudaFuncSetAttribute(quantize_rows_kernel<T, B, V>,                                    \
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)); \
-    if (e != cudaSuccess) return e;                                                                        \
-    quantize_rows_kernel<T, B, V><<<grid, threads, smem, stream>>>(a);                                     \
+    if (full && V <= 8) {                                                                                  \
+      cudaError_t e = ensure_smem_attr(quantize_rows_kernel<T, B, V, true>, static_cast<int>(smem));       \
+      if (e != cudaSuccess) return e;                                                                      \
+      quantize_rows_kernel<T, B, V, true><<<grid, threads, smem, stream>>>(a);                            \
+    } else {                                                                                               \
+      cudaError_t e = ensure_smem_attr(quantize_rows_kernel<T, B, V, false>, static_cast<int>(smem));      \
+      if (e != cudaSuccess) return e;                                                                      \
+      quantize_rows_kernel<T, B, V, false><<<grid, threads, smem, stream>>>(a);                           \
+    }                                                                                                      \
   } while (0)
   if (vpt <= 1) QUIK_Q_LAUNCH(1);
   else if (vpt <= 2) QUIK_Q_LAUNCH(2);

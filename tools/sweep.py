@@ -1,0 +1,102 @@
+"""Shape sweep on one GPU: QUIK layer step time (K1 + fused GEMM) vs cuBLAS f16 of
+the same shape, for the BASELINE.json configs and the cfg4 token sweep.
+
+  python tools/sweep.py [--quick] > sweep.json
+"""
+import argparse
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import torch
+
+import paper_2310_09259_b200 as q
+
+SHAPES = [
+    # name, M, K, N, O, bits
+    ("cfg1 oracle 4096->4096", 16, 4096, 4096, 128, 4),
+    ("cfg2 7B qkvo", 2048, 4096, 4096, 256, 4),
+    ("cfg2 7B up/gate", 2048, 4096, 11008, 256, 4),
+    ("cfg2 7B down W8A8", 2048, 11008, 4096, 688, 8),
+    ("cfg3 70B up/gate", 4096, 8192, 28672, 256, 4),
+    ("cfg3 70B down W8A8", 4096, 28672, 8192, 896, 8),
+    ("cfg5-shape 13B up", 2048, 5120, 13824, 256, 4),
+]
+OPT_FC1 = [(m, 9216, 36864, 256, 4) for m in (1, 16, 64, 128, 256, 512, 1024, 2048, 4096, 8192)]
+
+
+def timeit(fn, iters=20, warm=5):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / iters
+
+
+def run(name, M, K, N, O, bits, layers):
+    dev = torch.device("cuda", 0)
+    key = (K, N, O, bits)
+    if key not in layers:
+        layers.clear()
+        torch.cuda.empty_cache()
+        g = torch.Generator(device=dev).manual_seed(7)
+        idx = torch.randperm(K, generator=g, device=dev)[:O].sort().values.cpu().numpy()
+        outl = q.OutlierSet.from_indices(K, idx)
+        W = torch.randn(N, K, device=dev, generator=g)
+        base, sc, wr, ow = q.rtn_quantize_weights_device(W, outl, bits)
+        del W
+        layers[key] = (q.QuikLinear.from_device(outl, base, sc, wr, ow, bits),
+                       torch.randn(N, K, device=dev, dtype=torch.float16))
+    layer, W16 = layers[key]
+    x = torch.randn(M, K, device=dev, dtype=torch.float16)
+    y = torch.empty(M, N, device=dev, dtype=torch.float16)
+    mid = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    for e in mid:  # materialise the raw cudaEvent handles
+        e.record()
+    t_step_eager = timeit(lambda: layer.forward(x, out=y))
+    # CUDA graph of the forward (removes host launch overhead, visible at small M)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        layer.forward(x, out=y)
+    t_step = timeit(g.replay)
+    # kernel split from one instrumented call
+    for _ in range(3):
+        mid[0].record()
+        layer.forward(x, out=y, mid_event=mid[1])
+        mid[2].record()
+    torch.cuda.synchronize()
+    t_k1, t_gemm = mid[0].elapsed_time(mid[1]), mid[1].elapsed_time(mid[2])
+    out16 = torch.empty(M, N, device=dev, dtype=torch.float16)
+    g16 = torch.cuda.CUDAGraph()
+    torch.matmul(x, W16.t(), out=out16)
+    with torch.cuda.graph(g16):
+        torch.matmul(x, W16.t(), out=out16)
+    t16 = timeit(g16.replay)
+    ops = 2.0 * M * N * K
+    return dict(name=name, M=M, K=K, N=N, O=O, bits=bits, step_ms=t_step, step_eager_ms=t_step_eager,
+                k1_ms=t_k1, gemm_ms=t_gemm,
+                tops=ops / t_step / 1e9, cublas_f16_ms=t16, speedup_vs_f16=t16 / t_step)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--quick", action="store_true")
+    args = ap.parse_args()
+    layers = {}
+    res = []
+    for s in SHAPES:
+        res.append(run(*s, layers))
+    for m, K, N, O, bits in (OPT_FC1[::3] if args.quick else OPT_FC1):
+        res.append(run(f"cfg4 OPT-66B fc1 M={m}", m, K, N, O, bits, layers))
+    for r in res:
+        print(json.dumps(r), flush=True)
+
+
+if __name__ == "__main__":
+    main()
