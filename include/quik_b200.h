@@ -108,6 +108,14 @@ quik_status quik_quantize_activations_fused(quik_ctx_t ctx, quik_layer_t layer, 
                                             int64_t M, uint8_t* packed, float* scale, float* zero,
                                             float* x_outlier, void* stream);
 
+/* K1 exactly as the hot path runs it, into caller buffers in the device GEMM
+ * layout (diagnostics / parity): codes int8 [M][kpad] (kpad = round_up(K_b, 128),
+ * signed stored codes in permuted base order, zero padded), scale[M], zero[M],
+ * x_outlier16 f16 [M][opad] (opad = round_up(n_outlier, 64), zero padded). */
+quik_status quik_quantize_activations_gemm(quik_ctx_t ctx, quik_layer_t layer, const void* x, quik_dtype x_dtype,
+                                           int64_t M, int8_t* codes, float* scale, float* zero, void* x_outlier16,
+                                           void* stream);
+
 /* Unfused quantizer of an already-split base matrix [M][K].
  * reference: quantize_activations (runtime.hpp:51, runtime.cpp:188-197). */
 quik_status quik_quantize_activations(quik_ctx_t ctx, const void* x_base, quik_dtype x_dtype, int64_t M, int64_t K,
@@ -143,6 +151,17 @@ quik_status quik_linear_forward_strided(quik_ctx_t ctx, quik_layer_t layer, cons
 quik_status quik_linear_forward_ex(quik_ctx_t ctx, quik_layer_t layer, const void* x, quik_dtype x_dtype, int64_t M,
                                    void* y, quik_dtype y_dtype, int64_t ldy, quik_variant variant, void* stream,
                                    void* mid_event);
+
+/* The hot path with HOST activations and outputs: what the reference's
+ * quik_matmul(layer, FpMatrix) call (runtime.hpp:85-87) does with host data.
+ * x_host [M][in_features] and y_host [M][out_features] are host memory (page-locked
+ * for full overlap). The token rows are processed in chunks of `chunk_tokens`
+ * (0 = automatic, about 8 chunks of multiples of 256): the host->device copy of
+ * chunk c+1, the V3 kernels of chunk c and the device->host copy of chunk c-1 run
+ * concurrently on context-owned copy streams. Asynchronous on `stream`: y_host is
+ * complete once `stream` reaches this point (synchronise or use quik_ctx_sync). */
+quik_status quik_linear_forward_host(quik_ctx_t ctx, quik_layer_t layer, const void* x_host, quik_dtype x_dtype,
+                                     int64_t M, void* y_host, quik_dtype y_dtype, int64_t chunk_tokens, void* stream);
 
 /* Round-to-nearest weight quantization on the device.
  * reference: rtn_quantize_weights (quantizer.hpp:87-88, quantizer.cpp:339-371) with

@@ -282,6 +282,13 @@ class DeviceLayer {
                                   std::to_string(in_));
     FpMatrix y(x.rows, out_);
     if (x.rows == 0 || out_ == 0) return y;
+    if (v == PipelineVariant::V3FusedEpilogue && !times) {
+      // host buffers straight through the chunked copy/compute pipeline
+      detail::check(quik_linear_forward_host(detail::ctx(), h_, x.data.data(), QUIK_F32, x.rows, y.data.data(),
+                                             QUIK_F32, 0, nullptr));
+      detail::check(quik_ctx_sync(detail::ctx(), nullptr));
+      return y;
+    }
     detail::Buf dx(x.data.data(), x.data.size() * 4), dy(y.data.size() * 4);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);

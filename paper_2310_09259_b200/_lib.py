@@ -28,7 +28,8 @@ EXPORTED_SYMBOLS = (
     "quik_quantize_activations_fused", "quik_quantize_activations", "quik_int_matmul",
     "quik_dequantize_epilogue", "quik_linear_forward", "quik_linear_forward_strided",
     "quik_linear_forward_launches", "quik_linear_forward_ex", "quik_rtn_quantize_weights",
-    "quik_set_gemm_tile", "quik_set_probe_mode",
+    "quik_set_gemm_tile", "quik_set_probe_mode", "quik_linear_forward_host",
+    "quik_quantize_activations_gemm",
 )
 
 
@@ -94,6 +95,8 @@ def load() -> C.CDLL:
             "quik_rtn_quantize_weights": (i32, [vp, vp, i64, i64, vp, i64, i32, vp, vp, vp, vp, vp]),
             "quik_set_gemm_tile": (i32, [i32, i32]),
             "quik_set_probe_mode": (i32, [i32]),
+            "quik_linear_forward_host": (i32, [vp, vp, vp, i32, i64, vp, i32, i64, vp]),
+            "quik_quantize_activations_gemm": (i32, [vp, vp, vp, i32, i64, vp, vp, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)

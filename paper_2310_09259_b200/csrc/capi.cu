@@ -93,11 +93,30 @@ class DeviceGuard {
 
 }  // namespace
 
+constexpr int kMaxHostChunks = 32;
+
 struct quik_ctx_s {
   int device = 0;
   int num_sms = 148;
   int* d_err = nullptr;
   DevBuf q8, scale, zero, xo16, acc, fp, xbase, xo32, wtmp;
+  // host-buffer forward (quik_linear_forward_host): copy-in / copy-out streams and
+  // per-chunk events, created on first use; device staging for x and y.
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_done = nullptr;
+  cudaEvent_t ev_in[kMaxHostChunks] = {}, ev_out[kMaxHostChunks] = {};
+  DevBuf xdev, ydev;
+  void ensure_pipeline() {
+    if (s_in) return;
+    QK_CUDA(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
+    QK_CUDA(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+    QK_CUDA(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+    QK_CUDA(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
+    for (int i = 0; i < kMaxHostChunks; ++i) {
+      QK_CUDA(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
+      QK_CUDA(cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming));
+    }
+  }
 };
 
 struct quik_layer_s {
@@ -112,7 +131,10 @@ struct quik_layer_s {
   int32_t* base_src = nullptr;  // [kb]
   int32_t* out_src = nullptr;   // [n_outlier]
   uint8_t* lane_mask = nullptr;  // [round_up(in,16)] 0xFF = outlier column (null when n_outlier == 0)
-  uint16_t* gather = nullptr;    // [kpad] base position -> source column (null when n_outlier == 0)
+  uint16_t* gather = nullptr;    // [kpad] base position -> source column; >= kb -> zero slot
+  uint32_t* chunk_desc = nullptr;  // [kpad / 16] x uint4 hot-quantizer compaction descriptors
+  uint16_t* gen_chunk = nullptr;   // [n_gen] chunks gathered per byte
+  int n_gen = 0;
 };
 
 namespace {
@@ -151,6 +173,9 @@ void run_k1(quik_ctx_t ctx, const quik_layer_s* L, const void* x, quik_dtype xdt
   q.ldx = L->in_features;
   q.lane_mask = L->lane_mask;
   q.gather = L->gather;
+  q.chunk_desc = L->chunk_desc;
+  q.gen_chunk = L->gen_chunk;
+  q.n_gen = L->n_gen;
   q.out_src = L->out_src;
   q.kb = L->kb;
   q.n_out = L->n_outlier;
@@ -264,8 +289,18 @@ quik_status quik_ctx_destroy(quik_ctx_t ctx) {
   DeviceGuard g(ctx->device);
   cudaDeviceSynchronize();
   for (DevBuf* b : {&ctx->q8, &ctx->scale, &ctx->zero, &ctx->xo16, &ctx->acc, &ctx->fp, &ctx->xbase, &ctx->xo32,
-                    &ctx->wtmp})
+                    &ctx->wtmp, &ctx->xdev, &ctx->ydev})
     b->release();
+  if (ctx->s_in) {
+    cudaStreamDestroy(ctx->s_in);
+    cudaStreamDestroy(ctx->s_out);
+    cudaEventDestroy(ctx->ev_start);
+    cudaEventDestroy(ctx->ev_done);
+    for (int i = 0; i < kMaxHostChunks; ++i) {
+      cudaEventDestroy(ctx->ev_in[i]);
+      cudaEventDestroy(ctx->ev_out[i]);
+    }
+  }
   cudaFree(ctx->d_err);
   delete ctx;
   return QUIK_OK;
@@ -350,8 +385,48 @@ quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* d, quik_l
       QK_CUDA(cudaMemcpy(L->out_src, out_src.data(), d->n_outlier * 4, cudaMemcpyHostToDevice));
       QK_CUDA(cudaMalloc(&L->lane_mask, kr16));
       QK_CUDA(cudaMemcpy(L->lane_mask, lane_mask.data(), kr16, cudaMemcpyHostToDevice));
-      QK_CUDA(cudaMalloc(&L->gather, std::max<int64_t>(L->kpad, 1) * 2));
-      if (L->kpad) QK_CUDA(cudaMemcpy(L->gather, gather.data(), L->kpad * 2, cudaMemcpyHostToDevice));
+    }
+    if (L->kpad) {
+      // compaction tables of the hot quantizer (also for outlier-free layers: identity).
+      // Chunk c covers base positions 16c .. 16c+15; src[p] = code-row byte of position
+      // p (pads past kb read the zero bytes at kr16 + q).
+      const int64_t nch = L->kpad / 16;
+      std::vector<uint32_t> desc(static_cast<size_t>(nch * 4), 0u);
+      std::vector<uint16_t> gen;
+      for (int64_t c = 0; c < nch; ++c) {
+        int64_t src[16];
+        for (int p = 0; p < 16; ++p) {
+          const int64_t j = 16 * c + p;
+          src[p] = j < kb ? gather[j] : kr16 + (j - std::max<int64_t>(kb, 16 * c));
+        }
+        int len1 = 1;
+        while (len1 < 16 && src[len1] == src[0] + len1) ++len1;
+        bool ok = true;
+        for (int p = len1 + 1; p < 16; ++p) ok = ok && src[p] == src[len1] + (p - len1);
+        uint32_t* dd = &desc[static_cast<size_t>(4 * c)];
+        if (!ok) {
+          dd[0] = 0xFFFFFFFFu;
+          gen.push_back(static_cast<uint16_t>(c));
+          continue;
+        }
+        const int64_t sa = src[0], sb = len1 < 16 ? src[len1] - len1 : src[0];
+        dd[0] = static_cast<uint32_t>(sa & ~int64_t{3}) | ((0x3210u + 0x1111u * static_cast<uint32_t>(sa & 3)) << 16);
+        dd[1] = static_cast<uint32_t>(sb & ~int64_t{3}) | ((0x3210u + 0x1111u * static_cast<uint32_t>(sb & 3)) << 16);
+        uint32_t sel[4];
+        for (int k = 0; k < 4; ++k) {
+          sel[k] = 0;
+          for (int b = 0; b < 4; ++b) sel[k] |= static_cast<uint32_t>(4 * k + b < len1 ? b : 4 + b) << (4 * b);
+        }
+        dd[2] = sel[0] | (sel[1] << 16);
+        dd[3] = sel[2] | (sel[3] << 16);
+      }
+      L->n_gen = static_cast<int>(gen.size());
+      QK_CUDA(cudaMalloc(&L->gather, L->kpad * 2));
+      QK_CUDA(cudaMemcpy(L->gather, gather.data(), L->kpad * 2, cudaMemcpyHostToDevice));
+      QK_CUDA(cudaMalloc(&L->chunk_desc, nch * 16));
+      QK_CUDA(cudaMemcpy(L->chunk_desc, desc.data(), nch * 16, cudaMemcpyHostToDevice));
+      QK_CUDA(cudaMalloc(&L->gen_chunk, std::max<size_t>(gen.size(), 1) * 2));
+      if (!gen.empty()) QK_CUDA(cudaMemcpy(L->gen_chunk, gen.data(), gen.size() * 2, cudaMemcpyHostToDevice));
     }
     if (rows > 0) {
       QK_CUDA(cudaMalloc(&L->w_scale, rows * 4));
@@ -398,6 +473,8 @@ quik_status quik_layer_destroy(quik_layer_t L) {
   cudaFree(L->out_src);
   cudaFree(L->lane_mask);
   cudaFree(L->gather);
+  cudaFree(L->chunk_desc);
+  cudaFree(L->gen_chunk);
   delete L;
   return QUIK_OK;
 }
@@ -436,6 +513,42 @@ quik_status quik_quantize_activations_fused(quik_ctx_t ctx, quik_layer_t L, cons
     q.scale = scale ? scale : static_cast<float*>(ctx->scale.ensure(M * 4));
     q.zero = zero ? zero : static_cast<float*>(ctx->zero.ensure(M * 4));
     q.xo32 = x_outlier;
+    q.err = ctx->d_err;
+    check_launch(launch_quantize(q, as_stream(stream)), "quantize kernel");
+    return QUIK_OK;
+  });
+}
+
+quik_status quik_quantize_activations_gemm(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M,
+                                           int8_t* codes, float* scale, float* zero, void* x_outlier16, void* stream) {
+  if (!ctx || !L) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context or layer");
+  if (M < 0 || (M > 0 && (!x || !scale || !zero || (L->kpad && !codes) || (L->opad && !x_outlier16))))
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "quantize (GEMM layout): bad arguments");
+  if (L->in_features * (xdt == QUIK_F32 ? 4 : 2) > 128 * 1024)
+    return fail(QUIK_ERR_UNSUPPORTED, "quantize: row wider than 128 KiB (register-resident quantizer limit)");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    QuantArgs q{};
+    q.x = x;
+    q.x_is_f32 = xdt == QUIK_F32;
+    q.M = M;
+    q.K = L->in_features;
+    q.ldx = L->in_features;
+    q.lane_mask = L->lane_mask;
+    q.gather = L->gather;
+    q.chunk_desc = L->chunk_desc;
+    q.gen_chunk = L->gen_chunk;
+    q.n_gen = L->n_gen;
+    q.out_src = L->out_src;
+    q.kb = L->kb;
+    q.n_out = L->n_outlier;
+    q.bits = L->bits;
+    q.q8 = L->kpad ? codes : nullptr;
+    q.kpad = L->kpad;
+    q.scale = scale;
+    q.zero = zero;
+    q.xo16 = L->opad ? static_cast<__half*>(x_outlier16) : nullptr;
+    q.opad = L->opad;
     q.err = ctx->d_err;
     check_launch(launch_quantize(q, as_stream(stream)), "quantize kernel");
     return QUIK_OK;
@@ -523,6 +636,85 @@ quik_status quik_dequantize_epilogue(quik_ctx_t ctx, const int32_t* acc, int64_t
   });
 }
 
+}  // extern "C"
+
+namespace {
+// The forward on device buffers (argument checks done by the caller).
+quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M, void* y,
+                         quik_dtype ydt, int64_t ldy, quik_variant variant, cudaStream_t st, void* mid_event) {
+  if (M == 0 || L->out_features == 0) return QUIK_OK;
+  const int64_t N = L->out_features;
+  if (variant == QUIK_V3_FUSED_EPILOGUE) {
+    run_k1(ctx, L, x, xdt, M, st);
+    if (mid_event) QK_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(mid_event), st));
+    GemmArgs gm = gemm_args(ctx, L, M);
+    gm.out = y;
+    gm.ldo = ldy;
+    gm.mode = ydt == QUIK_F16 ? kModeF16 : kModeF32;
+    if (g_probe_mode) gm.mode = kModeProbe;
+    run_gemm(ctx, gm, st);
+    return QUIK_OK;
+  }
+  if (variant == QUIK_V1_UNFUSED) {
+    // split (runtime.cpp:169-186) then unfused quantisation of the base matrix (:188-197):
+    // the split is K1 in "copy" form writing f32 base/outlier columns, then K1 again
+    // over the base matrix with the identity permutation.
+    float* xb32 = static_cast<float*>(ctx->xbase.ensure(static_cast<size_t>(M * std::max<int64_t>(L->kb, 1) * 4)));
+    // split pass: gather base columns in permutation order as f32 (exact) and the
+    // outliers as f16 GEMM operands.
+    SplitArgs s{};
+    s.x = x;
+    s.x_is_f32 = xdt == QUIK_F32;
+    s.M = M;
+    s.K = L->in_features;
+    s.ldx = L->in_features;
+    s.base_src = L->base_src;
+    s.kb = L->kb;
+    s.out_src = L->out_src;
+    s.n_out = L->n_outlier;
+    s.xbase = xb32;
+    s.xo16 = L->opad ? static_cast<__half*>(ctx->xo16.ensure(static_cast<size_t>(M * L->opad * 2))) : nullptr;
+    s.opad = L->opad;
+    check_launch(launch_split(s, st), "split kernel");
+    QuantArgs q{};
+    q.x = xb32;
+    q.x_is_f32 = 1;
+    q.M = M;
+    q.K = L->kb;
+    q.ldx = L->kb;
+    q.kb = L->kb;
+    q.bits = L->bits;
+    q.q8 = L->kpad ? static_cast<int8_t*>(ctx->q8.ensure(static_cast<size_t>(M * L->kpad))) : nullptr;
+    q.kpad = L->kpad;
+    q.scale = static_cast<float*>(ctx->scale.ensure(M * 4));
+    q.zero = static_cast<float*>(ctx->zero.ensure(M * 4));
+    q.err = ctx->d_err;
+    check_launch(launch_quantize(q, st), "quantize kernel");
+  } else {
+    run_k1(ctx, L, x, xdt, M, st);
+  }
+  // V1/V2 tail: the int32 accumulator through global memory, then the same
+  // epilogue + outlier MMAs as V3 reading it back (bit-identical to V3).
+  int32_t* acc = static_cast<int32_t*>(ctx->acc.ensure(static_cast<size_t>(M * N * 4)));
+  GemmArgs gi = gemm_args(ctx, L, M);
+  gi.out = acc;
+  gi.ldo = N;
+  gi.mode = kModeInt32;
+  if (L->kpad) run_gemm(ctx, gi, st);
+  else QK_CUDA(cudaMemsetAsync(acc, 0, static_cast<size_t>(M * N * 4), st));
+  GemmArgs go = gemm_args(ctx, L, M);
+  go.acc_in = acc;
+  go.ld_acc = N;
+  go.out = y;
+  go.ldo = ldy;
+  go.mode = ydt == QUIK_F16 ? kModeAccInitF16 : kModeAccInitF32;
+  run_gemm(ctx, go, st);
+  return QUIK_OK;
+}
+}  // namespace
+
+extern "C" {
+
 quik_status quik_linear_forward_ex(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M,
                                    void* y, quik_dtype ydt, int64_t ldy, quik_variant variant, void* stream,
                                    void* mid_event) {
@@ -536,81 +728,66 @@ quik_status quik_linear_forward_ex(quik_ctx_t ctx, quik_layer_t L, const void* x
   if (ctx->device != L->device) return fail(QUIK_ERR_INVALID_ARGUMENT, "context and layer live on different devices");
   return guarded([&] {
     DeviceGuard g(ctx->device);
-    cudaStream_t st = as_stream(stream);
-    if (M == 0 || L->out_features == 0) return QUIK_OK;
-    const int64_t N = L->out_features;
-    if (variant == QUIK_V3_FUSED_EPILOGUE) {
-      run_k1(ctx, L, x, xdt, M, st);
-      if (mid_event) QK_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(mid_event), st));
-      GemmArgs gm = gemm_args(ctx, L, M);
-      gm.out = y;
-      gm.ldo = ldy;
-      gm.mode = ydt == QUIK_F16 ? kModeF16 : kModeF32;
-      if (g_probe_mode) gm.mode = kModeProbe;
-      run_gemm(ctx, gm, st);
-      return QUIK_OK;
-    }
-    if (variant == QUIK_V1_UNFUSED) {
-      // split (runtime.cpp:169-186) then unfused quantisation of the base matrix (:188-197):
-      // the split is K1 in "copy" form writing f32 base/outlier columns, then K1 again
-      // over the base matrix with the identity permutation.
-      float* xb32 = static_cast<float*>(ctx->xbase.ensure(static_cast<size_t>(M * std::max<int64_t>(L->kb, 1) * 4)));
-      // split pass: gather base columns in permutation order as f32 (exact) and the
-      // outliers as f16 GEMM operands.
-      SplitArgs s{};
-      s.x = x;
-      s.x_is_f32 = xdt == QUIK_F32;
-      s.M = M;
-      s.K = L->in_features;
-      s.ldx = L->in_features;
-      s.base_src = L->base_src;
-      s.kb = L->kb;
-      s.out_src = L->out_src;
-      s.n_out = L->n_outlier;
-      s.xbase = xb32;
-      s.xo16 = L->opad ? static_cast<__half*>(ctx->xo16.ensure(static_cast<size_t>(M * L->opad * 2))) : nullptr;
-      s.opad = L->opad;
-      check_launch(launch_split(s, st), "split kernel");
-      QuantArgs q{};
-      q.x = xb32;
-      q.x_is_f32 = 1;
-      q.M = M;
-      q.K = L->kb;
-      q.ldx = L->kb;
-      q.kb = L->kb;
-      q.bits = L->bits;
-      q.q8 = L->kpad ? static_cast<int8_t*>(ctx->q8.ensure(static_cast<size_t>(M * L->kpad))) : nullptr;
-      q.kpad = L->kpad;
-      q.scale = static_cast<float*>(ctx->scale.ensure(M * 4));
-      q.zero = static_cast<float*>(ctx->zero.ensure(M * 4));
-      q.err = ctx->d_err;
-      check_launch(launch_quantize(q, st), "quantize kernel");
-    } else {
-      run_k1(ctx, L, x, xdt, M, st);
-    }
-    // V1/V2 tail: the int32 accumulator through global memory, then the same
-    // epilogue + outlier MMAs as V3 reading it back (bit-identical to V3).
-    int32_t* acc = static_cast<int32_t*>(ctx->acc.ensure(static_cast<size_t>(M * N * 4)));
-    GemmArgs gi = gemm_args(ctx, L, M);
-    gi.out = acc;
-    gi.ldo = N;
-    gi.mode = kModeInt32;
-    if (L->kpad) run_gemm(ctx, gi, st);
-    else QK_CUDA(cudaMemsetAsync(acc, 0, static_cast<size_t>(M * N * 4), st));
-    GemmArgs go = gemm_args(ctx, L, M);
-    go.acc_in = acc;
-    go.ld_acc = N;
-    go.out = y;
-    go.ldo = ldy;
-    go.mode = ydt == QUIK_F16 ? kModeAccInitF16 : kModeAccInitF32;
-    run_gemm(ctx, go, st);
-    return QUIK_OK;
+    return forward_impl(ctx, L, x, xdt, M, y, ydt, ldy, variant, as_stream(stream), mid_event);
   });
 }
 
 quik_status quik_linear_forward_strided(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M,
                                         void* y, quik_dtype ydt, int64_t ldy, quik_variant variant, void* stream) {
   return quik_linear_forward_ex(ctx, L, x, xdt, M, y, ydt, ldy, variant, stream, nullptr);
+}
+
+quik_status quik_linear_forward_host(quik_ctx_t ctx, quik_layer_t L, const void* x_host, quik_dtype xdt, int64_t M,
+                                     void* y_host, quik_dtype ydt, int64_t chunk_tokens, void* stream) {
+  if (!ctx || !L) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context or layer");
+  if (M < 0) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_matmul: negative token count");
+  if (M > 0 && (!x_host || !y_host)) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_matmul: null input or output");
+  if (M > 0x7fffffffLL) return fail(QUIK_ERR_UNSUPPORTED, "quik_matmul: token count exceeds 2^31");
+  if (chunk_tokens < 0) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_matmul: negative chunk size");
+  if (L->in_features * (xdt == QUIK_F32 ? 4 : 2) > 128 * 1024)
+    return fail(QUIK_ERR_UNSUPPORTED, "quik_matmul: row wider than 128 KiB (register-resident quantizer limit)");
+  if (ctx->device != L->device) return fail(QUIK_ERR_INVALID_ARGUMENT, "context and layer live on different devices");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = as_stream(stream);
+    const int64_t K = L->in_features, N = L->out_features;
+    if (M == 0 || N == 0) return QUIK_OK;
+    ctx->ensure_pipeline();
+    const size_t xe = xdt == QUIK_F32 ? 4 : 2, ye = ydt == QUIK_F32 ? 4 : 2;
+    // Chunking: copy-in of chunk c+1, the two kernels of chunk c and copy-out of
+    // chunk c-1 run concurrently (PCIe is full duplex; the copies dominate). About
+    // 8 chunks, each a multiple of 256 tokens (whole CTA-pair tiles).
+    int64_t chunk = chunk_tokens;
+    if (chunk == 0) chunk = std::max<int64_t>(256, round_up((M + 7) / 8, 256));
+    if ((M + chunk - 1) / chunk > kMaxHostChunks) chunk = (M + kMaxHostChunks - 1) / kMaxHostChunks;
+    const int64_t nchunks = (M + chunk - 1) / chunk;
+    char* xd = static_cast<char*>(ctx->xdev.ensure(static_cast<size_t>(M * K) * xe));
+    char* yd = static_cast<char*>(ctx->ydev.ensure(static_cast<size_t>(M * N) * ye));
+    const char* xh = static_cast<const char*>(x_host);
+    char* yh = static_cast<char*>(y_host);
+    // everything already queued on `stream` (including an earlier call's use of the
+    // staging buffers) happens before this call's copies
+    QK_CUDA(cudaEventRecord(ctx->ev_start, st));
+    QK_CUDA(cudaStreamWaitEvent(ctx->s_in, ctx->ev_start, 0));
+    QK_CUDA(cudaStreamWaitEvent(ctx->s_out, ctx->ev_start, 0));
+    for (int64_t c = 0; c < nchunks; ++c) {
+      const int64_t m0 = c * chunk, mc = std::min(chunk, M - m0);
+      QK_CUDA(cudaMemcpyAsync(xd + m0 * K * xe, xh + m0 * K * xe, static_cast<size_t>(mc * K) * xe,
+                              cudaMemcpyHostToDevice, ctx->s_in));
+      QK_CUDA(cudaEventRecord(ctx->ev_in[c], ctx->s_in));
+      QK_CUDA(cudaStreamWaitEvent(st, ctx->ev_in[c], 0));
+      const quik_status s =
+          forward_impl(ctx, L, xd + m0 * K * xe, xdt, mc, yd + m0 * N * ye, ydt, N, QUIK_V3_FUSED_EPILOGUE, st, nullptr);
+      if (s != QUIK_OK) return s;
+      QK_CUDA(cudaEventRecord(ctx->ev_out[c], st));
+      QK_CUDA(cudaStreamWaitEvent(ctx->s_out, ctx->ev_out[c], 0));
+      QK_CUDA(cudaMemcpyAsync(yh + m0 * N * ye, yd + m0 * N * ye, static_cast<size_t>(mc * N) * ye,
+                              cudaMemcpyDeviceToHost, ctx->s_out));
+    }
+    QK_CUDA(cudaEventRecord(ctx->ev_done, ctx->s_out));
+    QK_CUDA(cudaStreamWaitEvent(st, ctx->ev_done, 0));
+    return QUIK_OK;
+  });
 }
 
 quik_status quik_rtn_quantize_weights(quik_ctx_t ctx, const float* w, int64_t N, int64_t K,

@@ -83,6 +83,17 @@ struct QuantArgs {
   const uint8_t* lane_mask;
   const uint16_t* gather;
   const int32_t* out_src;
+  //   chunk_desc [kpad / 16] x uint4, the hot kernel's compaction rule per 16-byte
+  //             output chunk (row independent): byte p = p < len1 ? A[p] : B[p] where
+  //             A / B are 16-byte windows of the uncompacted code row.
+  //               .x = A word offset (bytes, 4-aligned) | A funnel selector << 16
+  //               .y = B word offset | B funnel selector << 16
+  //               .z / .w = merge selectors of output words 0,1 / 2,3 (16 bits each)
+  //             .x == 0xFFFFFFFF: "general" chunk (more than one gap), listed in
+  //   gen_chunk [n_gen] u16 and gathered per byte through `gather`.
+  const uint32_t* chunk_desc;
+  const uint16_t* gen_chunk;
+  int n_gen;
   int64_t kb;               // base column count K_b
   int64_t n_out;
   int bits;                 // 4 or 8

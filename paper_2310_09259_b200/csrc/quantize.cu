@@ -9,7 +9,9 @@
 //   q = lround((v - vmin) / scale) (ties away from zero); stored = clamp(q - hr,
 //   -hr, hr - 1). Every FP op is an explicit _rn intrinsic, so the result is
 //   bit-identical to the reference compiled with -ffp-contract=off.
+#include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "sm100.cuh"
@@ -430,6 +432,317 @@ __global__ void __launch_bounds__(512) quantize_rows_kernel(const QuantArgs a) {
   }
 }
 
+// Hot-path K1 (f16 x, 16-byte aligned rows, K % 8 == 0, GEMM-layout outputs only).
+// Same numerics as quantize_rows_kernel, organised for HBM throughput and a short
+// instruction stream (the one-CTA-per-row kernel issues ~27 instructions per
+// element and is issue-bound at ~2 TB/s):
+//   * persistent CTAs walk rows blockIdx.x, +gridDim.x, ...; each row is fetched
+//     into a shared-memory ring by one TMA bulk copy issued `stages` rows ahead;
+//   * everything row-independent is hoisted out of the row loop: the per-vector
+//     outlier lane masks live in registers; the compaction descriptors are
+//     L1-resident per-layer tables;
+//   * min/max: packed HMNMX2; outlier lanes are replaced (one LOP3 per word) by the
+//     row's first base value, which cannot move the base min/max;
+//   * codes are written uncompacted to shared memory (one 8-byte store per vector);
+//   * compaction by 16-byte output chunk with a uniform two-window rule: byte p of
+//     the chunk is window A[p] (p < len1) or window B[p]; each window is 5 aligned
+//     32-bit shared loads + 4 byte permutes, the merge is 4 byte permutes. The few
+//     chunks with more than one outlier gap ("general") are gathered per byte by
+//     the first warps in a separate, warp-uniform loop.
+// Thread tid owns vectors v = tid + i * nt (i < VPT) and chunk slots tid + k * nt.
+__device__ __forceinline__ float redux_min(float v) {
+  float r;
+  asm volatile("redux.sync.min.NaN.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ float redux_max(float v) {
+  float r;
+  asm volatile("redux.sync.max.NaN.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+// f32 = f16 - f32 in one instruction (FHADD), exact conversion then IEEE rn subtraction
+__device__ __forceinline__ float sub_f16_f32(uint32_t h, float c) {
+  float d;
+  asm("sub.rn.f32.f16 %0, %1, %2;" : "=f"(d) : "h"(static_cast<unsigned short>(h)), "f"(c));
+  return d;
+}
+
+template <int BITS, int VPT>
+__global__ void __launch_bounds__(512) quantize_hot_kernel(const QuantArgs a, int stages, int row_stride) {
+  extern __shared__ __align__(128) uint8_t s_dyn[];
+  __shared__ float s_min[16], s_max[16];
+  __shared__ int s_nf[16];
+  __shared__ unsigned s_key[16];
+  __shared__ __align__(8) uint64_t s_full[8];
+  constexpr int kHr = 1 << (BITS - 1);
+  constexpr float kLevels = static_cast<float>((1 << BITS) - 1);
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int tid = threadIdx.x;
+  const int nt = blockDim.x;
+  const int nwarps = (nt + 31) >> 5;
+  const int K = static_cast<int>(a.K);
+  const int M = static_cast<int>(a.M);
+  const int nvec = K >> 3;
+  const int kb = static_cast<int>(a.kb);
+  const int kr16 = (K + 15) & ~15;
+  const uint32_t row_bytes = static_cast<uint32_t>(K) * 2u;
+  // two code rows (double-buffered so that one barrier per row can be dropped), then the ring
+  const int code_stride = (kr16 + 32 + 127) & ~127;
+  uint8_t* s_codes0 = s_dyn;                         // [2][code_stride]: codes by column, zero tail
+  uint8_t* s_ring = s_dyn + 2 * code_stride;         // [stages][row_stride]
+  const bool has_out = a.lane_mask != nullptr;
+  const int nchunk = static_cast<int>(a.kpad >> 4);
+  const __half* xg = reinterpret_cast<const __half*>(a.x);
+  const uint4* cdesc = reinterpret_cast<const uint4*>(a.chunk_desc);
+  const int first_base = has_out ? static_cast<int>(a.gather[0]) : 0;  // column of base position 0
+
+  // row-independent: outlier lane masks of this thread's vectors
+  uint2 lm[VPT];
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int v = tid + i * nt;
+    lm[i] = (has_out && v < nvec) ? __ldg(reinterpret_cast<const uint2*>(a.lane_mask) + v) : make_uint2(0u, 0u);
+  }
+
+  // row-independent: this thread's outlier slots (i = tid, tid + nt) -> source column, -1 = zero pad
+  int osrc[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int i = tid + j * nt;
+    osrc[j] = (has_out && i < a.n_out) ? __ldg(&a.out_src[i]) : -1;
+  }
+  const int opad = static_cast<int>(a.opad);
+  const bool xo_hoisted = opad <= 2 * nt;
+
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&s_full[s], 1);
+    fence_mbar_init();
+  }
+  if (tid < 16) reinterpret_cast<uint32_t*>(s_codes0 + (tid >> 3) * code_stride + kr16)[tid & 7] = 0u;  // zero tails
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) {
+      const int r = blockIdx.x + s * gridDim.x;
+      if (r >= M) break;
+      mbar_arrive_expect_tx(&s_full[s], row_bytes);
+      bulk_load_1d(s_ring + s * row_stride, xg + static_cast<int64_t>(r) * a.ldx, row_bytes, &s_full[s]);
+    }
+  }
+
+  int s = 0, s_prev = -1;
+  uint32_t ph = 0, cb = 0;
+  int t_prev = -1;
+#pragma unroll 1
+  for (int t = blockIdx.x; t < M; t += gridDim.x, cb ^= 1u) {
+    const uint4* srow = reinterpret_cast<const uint4*>(s_ring + s * row_stride);
+    uint8_t* s_codes = s_codes0 + cb * code_stride;
+    mbar_wait(&s_full[s], ph);
+
+    uint4 raw[VPT];
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int v = tid + i * nt;
+      raw[i] = v < nvec ? srow[v] : make_uint4(0, 0, 0, 0);
+    }
+    // ---- pass 1: packed min / max over the base columns
+    __half2 hmin = u2h2(0x7C007C00u), hmax = u2h2(0xFC00FC00u);
+    if (has_out) {
+      const uint32_t h0 = reinterpret_cast<const uint16_t*>(srow)[first_base];
+      const uint32_t fill = h0 | (h0 << 16);  // a base value of this row, in both halves
+#pragma unroll
+      for (int i = 0; i < VPT; ++i) {
+        if (tid + i * nt >= nvec) continue;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const uint32_t mk = __byte_perm(w < 2 ? lm[i].x : lm[i].y, 0u, (w & 1) ? 0x3322u : 0x1100u);
+          const __half2 x2 = u2h2(((&raw[i].x)[w] & ~mk) | (fill & mk));
+          hmin = __hmin2_nan(hmin, x2);
+          hmax = __hmax2_nan(hmax, x2);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < VPT; ++i) {
+        if (tid + i * nt >= nvec) continue;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const __half2 x2 = u2h2((&raw[i].x)[w]);
+          hmin = __hmin2_nan(hmin, x2);
+          hmax = __hmax2_nan(hmax, x2);
+        }
+      }
+    }
+    float vmin, vmax;
+    int nonfinite;
+    {
+      const float2 fmn = __half22float2(hmin);
+      const float2 fmx = __half22float2(hmax);
+      nonfinite = isnan(fmn.x) || isnan(fmn.y) || isnan(fmx.x) || isnan(fmx.y) || fmx.x == INFINITY ||
+                  fmx.y == INFINITY || fmn.x == -INFINITY || fmn.y == -INFINITY;
+      vmin = fminf(fmn.x, fmn.y);
+      vmax = fmaxf(fmx.x, fmx.y);
+    }
+    vmin = redux_min(vmin);
+    vmax = redux_max(vmax);
+    nonfinite = __reduce_or_sync(0xffffffffu, nonfinite);
+    if ((tid & 31) == 0) { s_min[tid >> 5] = vmin; s_max[tid >> 5] = vmax; s_nf[tid >> 5] = nonfinite; }
+    __syncthreads();  // (A): also, every thread is done with the previous row
+    if (tid == 0 && s_prev >= 0) {
+      // refill the previous row's ring slot (its last reader passed barrier A)
+      const int rn = t_prev + stages * gridDim.x;
+      if (rn < M) {
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&s_full[s_prev], row_bytes);
+        bulk_load_1d(s_ring + s_prev * row_stride, xg + static_cast<int64_t>(rn) * a.ldx, row_bytes, &s_full[s_prev]);
+      }
+    }
+    {
+      const int l = tid & 31;
+      vmin = redux_min(l < nwarps ? s_min[l] : INFINITY);
+      vmax = redux_max(l < nwarps ? s_max[l] : -INFINITY);
+      nonfinite = __reduce_or_sync(0xffffffffu, l < nwarps ? s_nf[l] : 0);
+    }
+    if (kb == 0) { vmin = 0.f; vmax = 0.f; }
+    if (vmin == 0.0f && kb > 0) {
+      // rare: the sign of a zero minimum is the first-seen zero's (block-uniform branch)
+      unsigned key = 0xFFFFFFFFu;
+#pragma unroll
+      for (int i = 0; i < VPT; ++i) {
+        const int v = tid + i * nt;
+        if (v >= nvec) continue;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float x = elem<__half>(raw[i], e);
+          const uint32_t mbyte = ((e < 4 ? lm[i].x : lm[i].y) >> (8 * (e & 3))) & 0xFFu;
+          if (mbyte == 0 && x == 0.0f) {
+            const unsigned k = (static_cast<unsigned>(v * 8 + e) << 1) | (__float_as_uint(x) >> 31);
+            key = k < key ? k : key;
+          }
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const unsigned o = __shfl_xor_sync(0xffffffffu, key, off);
+        key = o < key ? o : key;
+      }
+      if ((tid & 31) == 0) s_key[tid >> 5] = key;
+      __syncthreads();
+      key = s_key[0];
+      for (int w = 1; w < nwarps; ++w) key = s_key[w] < key ? s_key[w] : key;
+      vmin = (key & 1u) ? -0.0f : 0.0f;
+    }
+    const float range = __fsub_rn(vmax, vmin);
+    const float scale = range == 0.0f ? 1.0f : __fdiv_rn(range, kLevels);
+    const float rcp = __frcp_rn(scale);
+    if (tid == 0) {
+      if (nonfinite && a.err) atomicExch(a.err, 1);
+      a.scale[t] = scale;
+      a.zero[t] = vmin;
+    }
+    const unsigned long long rcp2 = f32x2_pack(rcp, rcp);
+    constexpr float kMagic = 12582912.0f - static_cast<float>(kHr);  // 1.5 * 2^23 - half_range
+    const unsigned long long magic2 = f32x2_pack(kMagic, kMagic);
+
+    // ---- pass 2: codes for every column (exactness argument: quantize_rows_kernel)
+    uint32_t near_vec = 0;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int v = tid + i * nt;
+      if (v >= nvec) continue;
+      uint32_t tb[8];
+      float rmax = 0.0f;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const uint32_t xw = (&raw[i].x)[w];
+        const unsigned long long d2 = f32x2_pack(sub_f16_f32(xw & 0xFFFFu, vmin), sub_f16_f32(xw >> 16, vmin));
+        unsigned long long qa2, t2, rq2, r2;
+        asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(qa2) : "l"(d2), "l"(rcp2));
+        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t2) : "l"(qa2), "l"(magic2));
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(rq2) : "l"(t2), "l"(magic2));
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r2) : "l"(qa2), "l"(rq2));
+        float r0, r1;
+        f32x2_unpack(r2, r0, r1);
+        rmax = fmaxf(rmax, fmaxf(fabsf(r0), fabsf(r1)));
+        tb[2 * w] = static_cast<uint32_t>(t2);
+        tb[2 * w + 1] = static_cast<uint32_t>(t2 >> 32);
+      }
+      near_vec |= (!(rmax < kNearTie) ? 1u : 0u) << i;
+      const uint32_t w0 = __byte_perm(__byte_perm(tb[0], tb[1], 0x0040), __byte_perm(tb[2], tb[3], 0x0040), 0x5410);
+      const uint32_t w1 = __byte_perm(__byte_perm(tb[4], tb[5], 0x0040), __byte_perm(tb[6], tb[7], 0x0040), 0x5410);
+      *reinterpret_cast<uint2*>(s_codes + v * 8) = make_uint2(w0, w1);
+    }
+    if (near_vec) {
+      // rare: elements within 2^-12 of a rounding boundary take the exact IEEE quotient
+      const __half* row = reinterpret_cast<const __half*>(srow);
+#pragma unroll 1
+      for (uint32_t nv = near_vec; nv; nv &= nv - 1) {
+        const int v = tid + (__ffs(nv) - 1) * nt;
+#pragma unroll 1
+        for (int e = 0; e < 8; ++e) {
+          const int c = v * 8 + e;
+          const float d = __fsub_rn(__half2float(row[c]), vmin);
+          const float qa = __fmul_rn(d, rcp);
+          const float r = __fsub_rn(qa, __fsub_rn(__fadd_rn(qa, kMagic), kMagic));
+          if (!(fabsf(r) < kNearTie))
+            s_codes[c] = static_cast<uint8_t>(static_cast<int>(quant_slow(d, scale)) - kHr);
+        }
+      }
+    }
+    __syncthreads();  // (B) codes complete
+
+    // ---- outliers (ascending index order, runtime.cpp:217) from the row in the ring
+    if (a.xo16) {
+      const uint16_t* row = reinterpret_cast<const uint16_t*>(srow);
+      uint16_t* xo = reinterpret_cast<uint16_t*>(a.xo16) + static_cast<int64_t>(t) * opad;
+      if (xo_hoisted) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int i = tid + j * nt;
+          if (i < opad) xo[i] = osrc[j] >= 0 ? row[osrc[j]] : static_cast<uint16_t>(0);
+        }
+      } else {
+        for (int i = tid; i < opad; i += nt) xo[i] = (has_out && i < a.n_out) ? row[__ldg(&a.out_src[i])] : 0;
+      }
+    }
+    // ---- compacted code row: two-window chunks, then the general chunks
+    uint4* dst = reinterpret_cast<uint4*>(a.q8 + static_cast<int64_t>(t) * a.kpad);
+#pragma unroll
+    for (int k = 0; k < (VPT > 1 ? VPT / 2 : 1); ++k) {
+      const int cidx = tid + k * nt;
+      if (cidx >= nchunk) break;
+      const uint4 d = __ldg(cdesc + cidx);
+      if (d.x == 0xFFFFFFFFu) continue;  // general chunk (second loop)
+      const uint32_t* wa = reinterpret_cast<const uint32_t*>(s_codes + (d.x & 0xFFFFu));
+      const uint32_t* wb = reinterpret_cast<const uint32_t*>(s_codes + (d.y & 0xFFFFu));
+      const uint32_t sa = d.x >> 16, sb = d.y >> 16;
+      const uint32_t a0 = wa[0], a1 = wa[1], a2 = wa[2], a3 = wa[3], a4 = wa[4];
+      const uint32_t b0 = wb[0], b1 = wb[1], b2 = wb[2], b3 = wb[3], b4 = wb[4];
+      const uint32_t o0 = __byte_perm(__byte_perm(a0, a1, sa), __byte_perm(b0, b1, sb), d.z & 0xFFFFu);
+      const uint32_t o1 = __byte_perm(__byte_perm(a1, a2, sa), __byte_perm(b1, b2, sb), d.z >> 16);
+      const uint32_t o2 = __byte_perm(__byte_perm(a2, a3, sa), __byte_perm(b2, b3, sb), d.w & 0xFFFFu);
+      const uint32_t o3 = __byte_perm(__byte_perm(a3, a4, sa), __byte_perm(b3, b4, sb), d.w >> 16);
+      dst[cidx] = make_uint4(o0, o1, o2, o3);
+    }
+    for (int gi = tid; gi < a.n_gen; gi += nt) {
+      const int cidx = a.gen_chunk[gi];
+      const uint4 g0 = __ldg(reinterpret_cast<const uint4*>(a.gather + cidx * 16));
+      const uint4 g1 = __ldg(reinterpret_cast<const uint4*>(a.gather + cidx * 16 + 8));
+      const uint32_t gw[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      uint32_t w[4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint32_t c0 = s_codes[gw[2 * kk] & 0xFFFFu], c1 = s_codes[gw[2 * kk] >> 16];
+        const uint32_t c2 = s_codes[gw[2 * kk + 1] & 0xFFFFu], c3 = s_codes[gw[2 * kk + 1] >> 16];
+        w[kk] = __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410);
+      }
+      dst[cidx] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    s_prev = s;
+    t_prev = t;
+    if (++s == stages) { s = 0; ph ^= 1u; }
+  }
+}
+
 __global__ void split_kernel(const SplitArgs a) {
   const int64_t t = blockIdx.y;
   for (int64_t j = blockIdx.x * blockDim.x + threadIdx.x; j < a.kb + a.opad; j += gridDim.x * blockDim.x) {
@@ -612,8 +925,58 @@ cudaError_t launch_quantize_t(const QuantArgs& a, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+template <int B>
+cudaError_t launch_quantize_hot(const QuantArgs& a, cudaStream_t stream) {
+  const int64_t nvec = a.K / 8;
+  int vpt = 1;
+  while (vpt < 8 && (nvec + vpt - 1) / vpt > 256) vpt *= 2;
+  const int threads = static_cast<int>(round_up((nvec + vpt - 1) / vpt, 32));
+  if (a.kpad / 16 > static_cast<int64_t>(vpt > 1 ? vpt / 2 : 1) * threads) return cudaErrorNotSupported;
+  const int row_stride = static_cast<int>(round_up(a.K * 2, 128));
+  const int codes = 2 * static_cast<int>(round_up(round_up(a.K, 16) + 32, 128));
+  // ring depth: about 32 KB of rows per CTA (at least 2 stages), <= 8 stages
+  static const int ring_kb = [] {  // tuning knob: QUIK_K1_RING_KB (ring bytes per CTA)
+    const char* e = getenv("QUIK_K1_RING_KB");
+    return e ? atoi(e) : 32;
+  }();
+  int stages = static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(8, (ring_kb * 1024) / row_stride)));
+  while (stages > 2 && codes + stages * row_stride > 200 * 1024) --stages;  // (2 stages: no prefetch overlap)
+  const int smem = codes + stages * row_stride;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+#define QUIK_QH_LAUNCH(V)                                                                                  \
+  do {                                                                                                     \
+    auto kern = quantize_hot_kernel<B, V>;                                                                 \
+    cudaError_t e = ensure_smem_attr(kern, smem);                                                          \
+    if (e != cudaSuccess) return e;                                                                        \
+    int per_sm = 0;                                                                                        \
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);                       \
+    if (e != cudaSuccess) return e;                                                                        \
+    const int64_t grid = std::min<int64_t>(a.M, static_cast<int64_t>(std::max(per_sm, 1)) * sms);          \
+    kern<<<static_cast<unsigned>(grid), threads, smem, stream>>>(a, stages, row_stride);                   \
+  } while (0)
+  if (vpt == 1) QUIK_QH_LAUNCH(1);
+  else if (vpt == 2) QUIK_QH_LAUNCH(2);
+  else if (vpt == 4) QUIK_QH_LAUNCH(4);
+  else QUIK_QH_LAUNCH(8);
+#undef QUIK_QH_LAUNCH
+  return cudaGetLastError();
+}
+
 cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t stream) {
   if (a.M == 0) return cudaSuccess;
+  // hot path: f16 rows, 16-byte aligned, GEMM-layout outputs only
+  const bool hot = !a.x_is_f32 && a.q8 && !a.packed && !a.xo32 && a.chunk_desc && a.gather && a.K % 8 == 0 &&
+                   a.K / 8 <= 512 * 8 && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && (a.ldx * 2) % 16 == 0;
+  static const int variant = [] {  // tuning: QUIK_K1_VARIANT=0 forces the general kernel
+    const char* e = getenv("QUIK_K1_VARIANT");
+    return e ? atoi(e) : 1;
+  }();
+  if (hot && variant != 0) {
+    const cudaError_t e = a.bits == 4 ? launch_quantize_hot<4>(a, stream) : launch_quantize_hot<8>(a, stream);
+    if (e != cudaErrorNotSupported) return e;  // else: shape outside the hot kernel's range
+  }
   if (a.x_is_f32) return a.bits == 4 ? launch_quantize_t<float, 4>(a, stream) : launch_quantize_t<float, 8>(a, stream);
   return a.bits == 4 ? launch_quantize_t<__half, 4>(a, stream) : launch_quantize_t<__half, 8>(a, stream);
 }

@@ -367,6 +367,47 @@ class QuikLinear:
 
     __call__ = forward
 
+    def quantize_gemm_layout(self, x):
+        """Diagnostics: K1 as the hot path runs it (C ABI quik_quantize_activations_gemm).
+        Returns (codes int8 [M][kpad], scale [M], zero [M], x_outlier f16 [M][opad])."""
+        torch = _torch()
+        M = x.shape[0]
+        kb = self.in_features - self.n_outlier
+        kpad = (kb + 127) // 128 * 128
+        opad = (self.n_outlier + 63) // 64 * 64
+        dev = x.device
+        codes = torch.empty((M, kpad), dtype=torch.int8, device=dev)
+        scale = torch.empty(M, dtype=torch.float32, device=dev)
+        zero = torch.empty(M, dtype=torch.float32, device=dev)
+        xo = torch.empty((M, opad), dtype=torch.float16, device=dev)
+        xdt = _lib.QUIK_F16 if x.dtype == torch.float16 else _lib.QUIK_F32
+        _lib.check(self._lib.quik_quantize_activations_gemm(
+            self.ctx.handle, self.handle, _ptr(x.contiguous()), xdt, M, _ptr(codes), _ptr(scale), _ptr(zero), _ptr(xo),
+            C.c_void_p(_stream_ptr(torch, dev))))
+        _lib.check(self._lib.quik_ctx_sync(self.ctx.handle, C.c_void_p(_stream_ptr(torch, dev))))
+        return codes, scale, zero, xo
+
+    def forward_host(self, x, out, chunk_tokens: int = 0):
+        """Host (CPU, ideally pinned) x [M][in_features] -> host out [M][out_features],
+        chunked so the H2D copy, the kernels and the D2H copy overlap
+        (C ABI quik_linear_forward_host). Asynchronous on the current stream."""
+        torch = _torch()
+        if x.dim() != 2 or x.shape[1] != self.in_features:
+            raise ValueError(f"quik_matmul: input has {x.shape[-1]} features, layer expects {self.in_features}")
+        if x.device.type != "cpu" or out.device.type != "cpu":
+            raise ValueError("forward_host: x and out must be host tensors")
+        if x.dtype not in (torch.float16, torch.float32) or out.dtype not in (torch.float16, torch.float32):
+            raise ValueError("forward_host: float16 or float32 tensors expected")
+        if not (x.is_contiguous() and out.is_contiguous()) or tuple(out.shape) != (x.shape[0], self.out_features):
+            raise ValueError("forward_host: contiguous x [M][in] and out [M][out] expected")
+        xdt = _lib.QUIK_F16 if x.dtype == torch.float16 else _lib.QUIK_F32
+        ydt = _lib.QUIK_F16 if out.dtype == torch.float16 else _lib.QUIK_F32
+        dev = torch.device("cuda", self.device)
+        _lib.check(self._lib.quik_linear_forward_host(
+            self.ctx.handle, self.handle, C.c_void_p(x.data_ptr()), xdt, x.shape[0], C.c_void_p(out.data_ptr()), ydt,
+            int(chunk_tokens), C.c_void_p(_stream_ptr(torch, dev))))
+        return out
+
 
 # --------------------------------------------------------------------------- reference-facing API
 

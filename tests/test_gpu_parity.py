@@ -495,3 +495,100 @@ def test_cpp_facade_parity_driver():
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failure(s)" in r.stdout
+
+
+@pytest.mark.parametrize("xdt,ydt", [("f16", "f16"), ("f32", "f32"), ("f32", "f16")])
+def test_forward_host_chunked_equals_device(xdt, ydt):
+    """quik_linear_forward_host (host buffers, chunked copy/compute overlap) is
+    bit-identical to the device-buffer forward for any chunking, pinned or not."""
+    m = q()
+    import torch
+
+    dt = {"f16": torch.float16, "f32": torch.float32}
+    rng = np.random.default_rng(41)
+    L, x, _ = make_layer(rng, 1000, 1024, 384, 4, 64, heavy_cols=4)
+    dev = m.QuikLinear(to_layer(L))
+    xh = torch.from_numpy(x).to(dt[xdt])
+    want = dev(xh.cuda(), out_dtype=dt[ydt]).cpu()
+    for chunk, pin in [(0, True), (256, True), (100, False), (1000, True), (7, True)]:
+        xin = xh.pin_memory() if pin else xh.clone()
+        yh = torch.empty((1000, 384), dtype=dt[ydt])
+        if pin:
+            yh = yh.pin_memory()
+        dev.forward_host(xin, yh, chunk_tokens=chunk)
+        torch.cuda.synchronize()
+        assert torch.equal(yh.view(torch.int16 if ydt == "f16" else torch.int32),
+                           want.view(torch.int16 if ydt == "f16" else torch.int32)), (chunk, pin)
+
+
+def _hot_k1_case(m, o, x16, idx, bits, N=8):
+    """Runs the hot-path quantizer (GEMM layout) and checks it bit-exactly against
+    the oracle's fused quantizer on the same (f16-representable) input."""
+    import torch
+
+    M, K = x16.shape
+    x = x16.astype(np.float32)
+    st, pk, sc, ze, xo = o.quantize_fused(x, idx, bits)
+    assert st == 0
+    kb = K - len(idx)
+    want = o.unpack(pk, M, kb, bits).reshape(M, kb) if kb else np.zeros((M, 0), np.int8)
+    rng = np.random.default_rng(5)
+    L = dict(in_features=K, out_features=N, bits=bits, idx=np.asarray(idx, np.int64),
+             base=np.zeros(N * row_bytes(kb, bits), np.uint8), scales=np.ones(N, np.float32),
+             wreduced=np.zeros(N, np.float32), outlier_weights=np.zeros((N, len(idx)), np.float32), bias=None)
+    dev = m.QuikLinear(to_layer(L))
+    codes, s, z, xo16 = dev.quantize_gemm_layout(torch.from_numpy(x16).cuda())
+    codes, s, z, xo16 = codes.cpu().numpy(), s.cpu().numpy(), z.cpu().numpy(), xo16.cpu().numpy()
+    np.testing.assert_array_equal(codes[:, :kb], want.astype(np.int8))
+    assert not codes[:, kb:].any()
+    np.testing.assert_array_equal(s.view(np.uint32), sc.view(np.uint32))
+    np.testing.assert_array_equal(z.view(np.uint32), ze.view(np.uint32))
+    if len(idx):
+        np.testing.assert_array_equal(xo16[:, :len(idx)].astype(np.float32), xo.reshape(M, -1))
+    assert not xo16[:, len(idx):].astype(np.float32).any()
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+def test_hot_quantizer_gemm_layout_bit_exact(bits):
+    """The hot-path K1 (f16 rows, descriptor compaction) against the oracle: codes,
+    scale, zero and outlier gather bit-exact, at random shapes and outlier sets
+    (clustered outliers exercise the per-byte chunks, sparse ones the fast chunks)."""
+    m = q()
+    o = oracle()
+    for seed in range(24):
+        rng = np.random.default_rng(7000 + seed)
+        K = int(rng.integers(1, 600)) * 8
+        M = int(rng.integers(1, 12))
+        x = rng.normal(0, 1.0, size=(M, K)).astype(np.float16)
+        k = int(rng.integers(0, min(K, 300)))
+        if seed % 3 == 0:
+            start = int(rng.integers(0, K - k + 1))
+            idx = np.arange(start, start + k, dtype=np.int64)  # one contiguous block
+        else:
+            idx = np.sort(rng.choice(K, size=k, replace=False)).astype(np.int64)
+        x[:, idx] *= 30
+        _hot_k1_case(m, o, x, idx, bits)
+
+
+def test_hot_quantizer_ties_zeros_and_shapes():
+    """Exact .5 ties (grid-aligned rows), signed zero minima, constant rows, and the
+    BASELINE shapes' row widths (8192 / 11008 / 28672) through the hot kernel."""
+    m = q()
+    o = oracle()
+    rng = np.random.default_rng(77)
+    for bits in (4, 8):
+        levels = (1 << bits) - 1
+        # grid-aligned: (v - vmin) / scale lands on k + 0.5 exactly for many elements
+        g = rng.integers(0, 2 * levels + 1, size=(6, 512)).astype(np.float32) * 0.5
+        g[:, 0] = 0.0
+        g[:, 1] = levels
+        x = g.astype(np.float16)
+        x[2, :] = 3.0                      # constant row -> scale 1
+        x[3, 5] = -0.0                     # zero min with a negative zero first
+        x[3, :5] = np.abs(x[3, :5]) + 1
+        _hot_k1_case(m, o, x, np.array([], np.int64), bits)
+        _hot_k1_case(m, o, x, np.array([3, 17, 100, 101, 102, 511], np.int64), bits)
+    for K, O in [(8192, 256), (11008, 688), (28672, 896)]:
+        x = rng.normal(0, 1, size=(3, K)).astype(np.float16)
+        idx = np.sort(rng.choice(K, size=O, replace=False)).astype(np.int64)
+        _hot_k1_case(m, o, x, idx, 4 if K == 8192 else 8)
