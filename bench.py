@@ -54,7 +54,31 @@ WORKLOADS = {
                       N=4096, O=688, bits=8),
     "cfg4-opt-fc1": dict(desc="OPT-66B fc1 9216->36864, 256 outliers, W4A4, 2048 tokens", M=2048, K=9216,
                          N=36864, O=256, bits=4),
+    # BASELINE.json configs[4]: W4A4 + 2:4 structured-sparse base weights, LLaMA-2-13B
+    # (hidden 5120, intermediate 13824; public model card), 2048 tokens
+    "cfg5-up": dict(desc="LLaMA-2-13B up/gate 5120->13824, 256 outliers, W4A4 + 2:4 sparse, 2048 tokens", M=2048,
+                    K=5120, N=13824, O=256, bits=4, sparse=True),
+    "cfg5-q": dict(desc="LLaMA-2-13B q/k/v/o 5120->5120, 256 outliers, W4A4 + 2:4 sparse, 2048 tokens", M=2048,
+                   K=5120, N=5120, O=256, bits=4, sparse=True),
 }
+
+
+def prune_24(W, base_cols):
+    """2:4 magnitude pruning over the permuted base columns (the two smallest |w| of
+    every aligned group of 4 -> 0): the structure sparsegpt_joint produces
+    (quantizer.cpp:299-337) with an identity Hessian. W: torch or numpy [N][K]."""
+    import torch
+
+    t = torch.as_tensor(W)
+    cols = torch.as_tensor(base_cols, device=t.device)
+    wb = t[:, cols]
+    g = wb.shape[1] // 4 * 4
+    grp = wb[:, :g].reshape(t.shape[0], -1, 4)
+    drop = grp.abs().argsort(dim=-1, stable=True)[..., :2]
+    grp.scatter_(-1, drop, 0.0)
+    wb[:, :g] = grp.reshape(t.shape[0], g)
+    t[:, cols] = wb
+    return W
 
 CPU_SAMPLE_TOKENS = 64  # bounded sample of the workload for the CPU reference
 
@@ -91,6 +115,8 @@ def synth_host(w, seed, tokens):
         x[:, heavy] *= 50.0
     x = x.astype(np.float16).astype(np.float32)
     idx = r.select_outliers(x, w["O"])
+    if w.get("sparse"):
+        prune_24(W, np.setdiff1d(np.arange(w["K"]), idx))  # the reference runs it densely over the zeros
     q = r.rtn_quantize_weights(W, idx, w["bits"])
     del W
     L = dict(in_features=w["K"], out_features=w["N"], bits=w["bits"], act_bits=w["bits"], base=q["base"],
@@ -225,9 +251,14 @@ def run_ours(args, w):
     del x, maxabs
     Wt = torch.randn((ns, K), generator=torch.Generator(device=dev).manual_seed(args.seed * 1000 + rank), device=dev,
                      dtype=torch.float32)
+    sparse = bool(w.get("sparse"))
+    if sparse:
+        prune_24(Wt, torch.as_tensor(outliers.permutation[: K - O], device=dev))
     base, sc, wr, ow = q.rtn_quantize_weights_device(Wt, outliers, bits)
     del Wt
-    layer = q.QuikLinear.from_device(outliers, base, sc, wr, ow, bits)
+    layer = q.QuikLinear.from_device(outliers, base, sc, wr, ow, bits, sparse=sparse)
+    if sparse and not layer.is_sparse:
+        raise SystemExit("2:4 workload: layer did not compress")
     del base, ow
     torch.cuda.synchronize()
 
@@ -311,6 +342,8 @@ def run_ours(args, w):
     kb = K - O
     p_f16 = pk["bf16"]
     p_i8 = 2.0 * p_f16  # B200 dense INT8 = 2x dense FP16/BF16 tensor rate
+    if sparse:
+        p_i8 *= 2.0  # 2:4 sparse INT8 (tcgen05.mma.sp) = 2x dense INT8
     ops_rank = 2.0 * M * ns * K
     t_ideal_s = 2.0 * M * ns * kb / (p_i8 * 1e12) + 2.0 * M * ns * O / (p_f16 * 1e12)
     mixed_peak = ops_rank / t_ideal_s / 1e12
@@ -325,10 +358,12 @@ def run_ours(args, w):
             traffic = None
     roofline = dict(bound="tensor", achieved=achieved, peak=mixed_peak, unit="TFLOP/s", frac=achieved / mixed_peak,
                     traffic=traffic,
-                    kernel="quik_gemm_kernel (fused int8 GEMM + f16 outlier GEMM + dequant epilogue)",
+                    kernel="quik_gemm_kernel (fused int8 GEMM%s + f16 outlier GEMM + dequant epilogue)"
+                           % (" on 2:4-compressed weights, tcgen05.mma.sp" if sparse else ""),
                     peak_basis=(f"{pk['source']} bf16 burst {p_f16:.1f} TF/s (MEASURED_PEAKS.json) for the "
-                                f"{O} f16 outlier columns; INT8 peak = 2x that = {p_i8:.1f} TOPS for the {kb} "
-                                "int columns; mixed peak = ops / (int_ops/P_i8 + f16_ops/P_f16)"),
+                                f"{O} f16 outlier columns; INT8 peak = {'4x (2:4 sparse)' if sparse else '2x'} that = "
+                                f"{p_i8:.1f} TOPS for the {kb} int columns (dense-equivalent ops); mixed peak = ops / "
+                                "(int_ops/P_i8 + f16_ops/P_f16)"),
                     int8_only_frac=achieved / p_i8, kernel_ms=gemm_avg)
     bytes_q = M * K * 2 + M * (kb + 127) // 128 * 128 + M * ((O + 63) // 64 * 64) * 2 + 8 * M
     quant = dict(kernel="quantize_hot_kernel (K1, persistent TMA ring)", ms=quant_avg, algorithmic_bytes=bytes_q,

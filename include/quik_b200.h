@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define QUIK_B200_ABI_VERSION 1
+#define QUIK_B200_ABI_VERSION 2
 
 typedef enum quik_status {
   QUIK_OK = 0,
@@ -88,6 +88,13 @@ typedef struct quik_weights_desc {
   const float* bias;
   int64_t row_begin;
   int64_t row_end;
+  /* 1: the base weights are 2:4 structured sparse (reference: sparsegpt_joint,
+   * quantizer.cpp:299-337 -- at most two non-zero codes per aligned group of 4
+   * permuted base columns). The layer is compressed to half the codes + 4-bit
+   * metadata and runs on tcgen05.mma.sp (exactly equal to the dense sum). If some
+   * group has more than two non-zero codes the layer stays dense; see
+   * quik_layer_is_sparse. 0: dense. (ABI version 2; absent in version 1.) */
+  int sparsity;
 } quik_weights_desc;
 
 /* Uploads and repacks the weights into the device GEMM layout.
@@ -97,6 +104,8 @@ quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* desc, qui
 quik_status quik_layer_destroy(quik_layer_t layer);
 quik_status quik_layer_info(quik_layer_t layer, int64_t* in_features, int64_t* out_features,
                             int64_t* n_outlier, int* bits);
+/* 1 if the layer runs the 2:4 sparse GEMM (sparsity requested and compressible). */
+int quik_layer_is_sparse(quik_layer_t layer);
 
 /*
  * K1 fused quantizer. reference: quantize_activations_fused (runtime.hpp:55-56,
@@ -174,8 +183,9 @@ quik_status quik_rtn_quantize_weights(quik_ctx_t ctx, const float* w, int64_t N,
                                       float* scales, float* wreduced, float* outlier_weights, void* stream);
 
 /* Tuning/debug knob (process-wide): force the GEMM tile, cta_group in {1, 2} and
- * token block_n in {32, 64, 128} (1-CTA) or {128, 256} (CTA pair); (0, 0) restores
- * the heuristic. */
+ * token block_n in {32, 64, 128} (1-CTA) or {128, 192, 256} (CTA pair; 2:4 sparse
+ * layers use 192 where 256 is asked, dense ones 256 for 192); (0, 0) restores the
+ * heuristic. */
 quik_status quik_set_gemm_tile(int cta_group, int block_n);
 
 /* Diagnostics (process-wide): when on, the V3 forward runs the fused GEMM

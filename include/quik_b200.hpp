@@ -189,11 +189,21 @@ struct OutlierSet {
 };
 
 // quantizer.hpp:48-58
+// quantizer.hpp:32-43: 2:4 structured mask over base weight positions
+struct SparsityMask {
+  int64_t rows = 0;
+  int64_t cols = 0;
+  std::vector<uint8_t> kept;
+  bool empty() const { return kept.empty(); }
+  bool kept_at(int64_t r, int64_t c) const { return kept[static_cast<size_t>(r * cols + c)] != 0; }
+};
+
 struct QuantizedWeights {
   PackedIntMatrix base;
   std::vector<float> scales;
   FpMatrix outlier_weights;
   std::vector<float> wreduced;
+  SparsityMask mask;  // empty unless produced by sparsegpt_joint (-> 2:4 sparse GEMM)
   int bits() const { return base.bits; }
   int64_t out_features() const { return base.rows; }
   int64_t base_features() const { return base.cols; }
@@ -261,6 +271,7 @@ class DeviceLayer {
     d.bias = L.bias.empty() ? nullptr : L.bias.data();
     d.row_begin = row_begin;
     d.row_end = row_end;
+    d.sparsity = L.weights.mask.empty() ? 0 : 1;
     detail::check(quik_layer_create(detail::ctx(), &d, &h_));
     int64_t in = 0, out = 0;
     quik_layer_info(h_, &in, &out, nullptr, nullptr);

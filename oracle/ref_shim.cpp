@@ -285,6 +285,33 @@ int qr_make_test_layer(uint32_t seed, int64_t tokens, int64_t in, int64_t out, i
   }
 }
 
+// sparsegpt_joint (quantizer.cpp:299-337): joint 2:4 pruning + quantization, the
+// producer of the sparse layers (cfg5). hsum: row-major K x K Hessian sum (FP64)
+// over `tokens` calibration rows, or NULL for Hessian::identity(K). Outputs as
+// qr_rtn_quantize_weights plus the mask [N][K - n_out] (1 = kept).
+int qr_sparsegpt_joint(const float* w, int64_t N, int64_t K, const int64_t* idx, int64_t n_out, int bits,
+                       const double* hsum, int64_t tokens, uint8_t* base, float* scales, float* wreduced,
+                       float* outlier_w, uint8_t* mask) {
+  try {
+    auto o = quik::OutlierSet::from_indices(K, std::vector<int64_t>(idx, idx + n_out));
+    quik::Hessian h = quik::Hessian::identity(K);
+    if (hsum) {
+      h.dim = K;
+      h.token_count = tokens;
+      h.sum.assign(hsum, hsum + K * K);
+    }
+    auto q = quik::sparsegpt_joint(to_fp(w, N, K), h, o, bits);
+    std::memcpy(base, q.base.data.data(), q.base.data.size());
+    std::memcpy(scales, q.scales.data(), N * 4);
+    std::memcpy(wreduced, q.wreduced.data(), N * 4);
+    if (n_out) std::memcpy(outlier_w, q.outlier_weights.data.data(), N * n_out * 4);
+    std::memcpy(mask, q.mask.kept.data(), q.mask.kept.size());
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
 // The reference tests' seeded Gaussian generator (tests/test_helpers.hpp:128-134):
 // std::mt19937(seed) + std::normal_distribution<float>(0, stddev), row-major.
 void qr_random_matrix(uint32_t seed, int64_t rows, int64_t cols, float stddev, float* out) {

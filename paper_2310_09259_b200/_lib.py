@@ -29,7 +29,7 @@ EXPORTED_SYMBOLS = (
     "quik_dequantize_epilogue", "quik_linear_forward", "quik_linear_forward_strided",
     "quik_linear_forward_launches", "quik_linear_forward_ex", "quik_rtn_quantize_weights",
     "quik_set_gemm_tile", "quik_set_probe_mode", "quik_linear_forward_host",
-    "quik_quantize_activations_gemm",
+    "quik_quantize_activations_gemm", "quik_layer_is_sparse",
 )
 
 
@@ -56,6 +56,7 @@ class WeightsDesc(C.Structure):
         ("bias", C.c_void_p),
         ("row_begin", C.c_int64),
         ("row_end", C.c_int64),
+        ("sparsity", C.c_int),
     ]
 
 
@@ -97,6 +98,7 @@ def load() -> C.CDLL:
             "quik_set_probe_mode": (i32, [i32]),
             "quik_linear_forward_host": (i32, [vp, vp, vp, i32, i64, vp, i32, i64, vp]),
             "quik_quantize_activations_gemm": (i32, [vp, vp, vp, i32, i64, vp, vp, vp, vp, vp]),
+            "quik_layer_is_sparse": (i32, [vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)

@@ -123,7 +123,10 @@ struct quik_layer_s {
   int device = 0;
   int64_t in_features = 0, out_features = 0, n_outlier = 0, kb = 0, kpad = 0, opad = 0;
   int bits = 4;
-  int8_t* w8 = nullptr;      // [out][kpad]
+  int8_t* w8 = nullptr;      // [out][kpad] (null when sparse)
+  int sparse = 0;            // 2:4 sparse GEMM operands below are in use
+  int8_t* w_sp = nullptr;    // [out][kpad / 2]
+  uint8_t* meta = nullptr;   // metadata planes (kernels.h GemmArgs)
   __half* wo16 = nullptr;    // [out][opad]
   float* w_scale = nullptr;  // [out]
   float* wreduced = nullptr; // [out]
@@ -206,6 +209,9 @@ GemmArgs gemm_args(quik_ctx_t ctx, const quik_layer_s* L, int64_t M) {
   g.a_scale = static_cast<const float*>(ctx->scale.p);
   g.a_zero = static_cast<const float*>(ctx->zero.p);
   g.half_range = static_cast<float>(1 << (L->bits - 1));
+  g.sparse = L->sparse;
+  g.w_sp = L->w_sp;
+  g.meta = L->meta;
   return g;
 }
 
@@ -247,7 +253,7 @@ quik_status quik_set_gemm_tile(int cta_group, int block_n) {
     return QUIK_OK;
   }
   const bool ok = (cta_group == 1 && (block_n == 32 || block_n == 64 || block_n == 128)) ||
-                  (cta_group == 2 && (block_n == 128 || block_n == 256));
+                  (cta_group == 2 && (block_n == 128 || block_n == 192 || block_n == 256));
   if (!ok) return fail(QUIK_ERR_INVALID_ARGUMENT, "unsupported GEMM tile configuration");
   quikb200::gemm_tile_override = (cta_group << 16) | block_n;
   return QUIK_OK;
@@ -358,7 +364,7 @@ quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* d, quik_l
     L->n_outlier = d->n_outlier;
     L->bits = d->bits;
     L->kb = kb;
-    L->kpad = round_up(kb, kKBlockBytes);
+    L->kpad = round_up(kb, d->sparsity ? 2 * kKBlockBytes : kKBlockBytes);
     L->opad = round_up(d->n_outlier, 64);
 
     // permutation tables (calibration.cpp:69-91): non-outliers ascending, outliers ascending
@@ -444,6 +450,30 @@ quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* d, quik_l
         QK_CUDA(cudaMemcpy(tmp, d->base + rb * rbytes, static_cast<size_t>(rows * rbytes), cudaMemcpyDefault));
         check_launch(launch_unpack_to_gemm(static_cast<const uint8_t*>(tmp), rows, kb, d->bits, L->w8, L->kpad, st),
                      "weight unpack");
+        if (d->sparsity) {
+          // 2:4 compression (tcgen05.mma.sp operands); stays dense if not compressible
+          const int64_t npad = round_up(rows, kBlockM);
+          QK_CUDA(cudaMalloc(&L->w_sp, static_cast<size_t>(rows * L->kpad / 2)));
+          QK_CUDA(cudaMalloc(&L->meta, static_cast<size_t>(2 * (L->kpad / 256) * npad * 16)));
+          int* d_bad = nullptr;
+          QK_CUDA(cudaMalloc(&d_bad, sizeof(int)));
+          QK_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
+          check_launch(launch_compress_24(L->w8, rows, L->kpad, L->w_sp, L->meta, d_bad, st), "2:4 compression");
+          int bad = 0;
+          QK_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+          QK_CUDA(cudaStreamSynchronize(st));
+          cudaFree(d_bad);
+          if (bad) {
+            cudaFree(L->w_sp);
+            cudaFree(L->meta);
+            L->w_sp = nullptr;
+            L->meta = nullptr;
+          } else {
+            L->sparse = 1;
+            QK_CUDA(cudaFree(L->w8));
+            L->w8 = nullptr;
+          }
+        }
       }
       if (d->n_outlier) {
         QK_CUDA(cudaMalloc(&L->wo16, static_cast<size_t>(rows * L->opad * 2)));
@@ -465,6 +495,8 @@ quik_status quik_layer_destroy(quik_layer_t L) {
   DeviceGuard g(L->device);
   cudaDeviceSynchronize();
   cudaFree(L->w8);
+  cudaFree(L->w_sp);
+  cudaFree(L->meta);
   cudaFree(L->wo16);
   cudaFree(L->w_scale);
   cudaFree(L->wreduced);
@@ -478,6 +510,8 @@ quik_status quik_layer_destroy(quik_layer_t L) {
   delete L;
   return QUIK_OK;
 }
+
+int quik_layer_is_sparse(quik_layer_t L) { return L ? L->sparse : 0; }
 
 quik_status quik_layer_info(quik_layer_t L, int64_t* in_f, int64_t* out_f, int64_t* n_out, int* bits) {
   if (!L) return fail(QUIK_ERR_INVALID_ARGUMENT, "null layer");

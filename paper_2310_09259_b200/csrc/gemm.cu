@@ -45,22 +45,38 @@ constexpr int kChunk = 32;                                     // tokens per epi
 constexpr int kStoreBufBytes = kChunk * 32 * 2;                // [32 tokens][32 features] f16
 constexpr int kStagingBytes = kEpiWarps * 2 * kStoreBufBytes;  // double-buffered per warp
 
-template <int CG, int BN>
+// SP (2:4 sparse base weights): one integer stage covers 256 logical K: the
+// compressed weight tile (128 rows x 128 B = 256 logical K), two 128-byte swizzle
+// atoms of activations and the 4 KB metadata tile [2 halves][128 rows][16 B],
+// which the MMA warp copies into a TMEM ring (tcgen05.cp) ahead of the 4
+// tcgen05.mma.sp (K = 64 each) that read it.
+constexpr int kMetaSlots = 4;     // TMEM metadata ring (8 columns per stage)
+constexpr int kMetaTileBytes = 4096;
+
+template <int CG, int BN, bool SP = false>
 struct Cfg {
   static constexpr int kBRows = BN / CG;                  // token rows staged per CTA
   static constexpr int kABytes = kBlockM * kKBlockBytes;  // 16 KB: 128 weight rows per CTA
-  static constexpr int kBBytes = kBRows * kKBlockBytes;
-  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kBAtomBytes = kBRows * kKBlockBytes;
+  static constexpr int kBBytes = kBAtomBytes * (SP ? 2 : 1);
+  static constexpr int kMetaBytes = SP ? kMetaTileBytes : 0;
+  static constexpr int kStageBytes = kABytes + kBBytes + kMetaBytes;
   static constexpr int kBudget = 227 * 1024 - 1024 - kStagingBytes - 512;
   static constexpr int kStages = (kBudget / kStageBytes) > 8 ? 8 : (kBudget / kStageBytes);
-  static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
+  static constexpr int kAccCols = 2 * BN;                 // two accumulator buffers
+  static constexpr int kMetaCol = kAccCols;               // SP: metadata ring after the accumulators
+  static constexpr int kTmemCols = SP ? 512 : (2 * BN < 32 ? 32 : 2 * BN);
+  static_assert(!SP || kAccCols + 8 * kMetaSlots <= 512, "TMEM: accumulators + metadata ring");
   static constexpr int kBarBytes = (2 * kStages + 8) * 8 + 16;
   static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kStagingBytes + kBarBytes;
   static constexpr int kTileRows = kBlockM * CG;          // weight rows per (cluster) tile
+  static constexpr int kIntStageBytes = kABytes + kBBytes + kMetaBytes;  // expect-tx per CTA
+  static constexpr int kOutStageBytes = kABytes + kBAtomBytes;
 };
 
 struct KParams {
-  CUtensorMap tm_w;   // int8 [N][kpad], box {128 B, 128 rows}
+  CUtensorMap tm_w;   // int8 [N][kpad] (SP: compressed [N][kpad / 2]), box {128 B, 128 rows}
+  CUtensorMap tm_e;   // SP: metadata [2 * n_kb * n_pad rows][16 B], box {16 B, 128 rows}
   CUtensorMap tm_x;   // int8 [M][kpad], box {128 B, BN/CG rows}
   CUtensorMap tm_wo;  // f16 [N][opad], box {64, 128}
   CUtensorMap tm_xo;  // f16 [M][opad], box {64, BN/CG}
@@ -79,6 +95,7 @@ struct KParams {
   long long ldo;
   const int32_t* acc_in;
   long long ld_acc;
+  int meta_rows;  // SP: n_pad = round_up(N, 128) rows per metadata (stage, half) plane
 };
 
 template <int CG, int MODE>
@@ -87,9 +104,9 @@ __device__ __forceinline__ void arrive_leader(uint64_t* bar) {
   else mbar_arrive(bar);
 }
 
-template <int CG, int BN, int MODE>
+template <int CG, int BN, int MODE, bool SP>
 __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_constant__ KParams p) {
-  using C = Cfg<CG, BN>;
+  using C = Cfg<CG, BN, SP>;
   constexpr bool kAccGlobal = MODE == kModeAccInitF32 || MODE == kModeAccInitF16;
   constexpr bool kF16Out = MODE == kModeF16 || MODE == kModeAccInitF16;
   constexpr bool kInt32Out = MODE == kModeInt32;
@@ -118,6 +135,7 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
 
   if (warp == 0 && lane == 0) {
     if (kb_int) { tma_prefetch(&p.tm_w); tma_prefetch(&p.tm_x); }
+    if (SP && kb_int) tma_prefetch(&p.tm_e);
     if (kb_out) { tma_prefetch(&p.tm_wo); tma_prefetch(&p.tm_xo); }
   }
   if (warp == 1 && lane == 0) {
@@ -154,19 +172,36 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
       const uint64_t pol_x = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
+      auto tma = [&](void* dst, const CUtensorMap* m, int c0, int c1, uint64_t pol) {
+        if constexpr (CG == 1) tma_load_2d(dst, m, c0, c1, &full[stage], pol);
+        else tma_load_2d_pair(dst, m, c0, c1, &full[stage], pol);
+      };
+      // outlier block (or dense integer block): A + one B atom at column kc
       auto load = [&](const CUtensorMap* ma, const CUtensorMap* mx, int kc, int wrow, int trow) {
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* sa = smem + stage * C::kStageBytes;
-        uint8_t* sb = sa + C::kABytes;
-        if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::kStageBytes);
-        if constexpr (CG == 1) {
-          tma_load_2d(sa, ma, kc, wrow, &full[stage], pol_w);
-          tma_load_2d(sb, mx, kc, trow, &full[stage], pol_x);
-        } else {
-          tma_load_2d_pair(sa, ma, kc, wrow, &full[stage], pol_w);
-          tma_load_2d_pair(sb, mx, kc, trow, &full[stage], pol_x);
-        }
+        if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::kOutStageBytes);
+        tma(sa, ma, kc, wrow, pol_w);
+        tma(sa + C::kABytes, mx, kc, trow, pol_x);
         if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+      };
+      // integer block kb: dense = load(); SP = compressed A + two B atoms + metadata tile
+      auto load_int = [&](int kb, int wrow, int trow) {
+        if constexpr (!SP) {
+          load(&p.tm_w, &p.tm_x, kb * kKBlockBytes, wrow, trow);
+        } else {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::kStageBytes;
+          uint8_t* sb = sa + C::kABytes;
+          uint8_t* se = sb + C::kBBytes;
+          if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::kIntStageBytes);
+          tma(sa, &p.tm_w, kb * kKBlockBytes, wrow, pol_w);
+          tma(sb, &p.tm_x, kb * 2 * kKBlockBytes, trow, pol_x);
+          tma(sb + C::kBAtomBytes, &p.tm_x, kb * 2 * kKBlockBytes + kKBlockBytes, trow, pol_x);
+          tma(se, &p.tm_e, 0, (2 * kb) * p.meta_rows + wrow, pol_w);
+          tma(se + kMetaTileBytes / 2, &p.tm_e, 0, (2 * kb + 1) * p.meta_rows + wrow, pol_w);
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
       };
       auto rows_of = [&](int tile, int& wrow, int& trow) {
         const int nb = tile / tiles_m, mb = tile % tiles_m;
@@ -177,13 +212,13 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         int wr, tr;
         rows_of(tile, wr, tr);
-        for (int kb = 0; kb < h_a; ++kb) load(&p.tm_w, &p.tm_x, kb * kKBlockBytes, wr, tr);
+        for (int kb = 0; kb < h_a; ++kb) load_int(kb, wr, tr);
         if (two_phase && prev >= 0) {
           int pw, pt;
           rows_of(prev, pw, pt);
           for (int ko = 0; ko < kb_out; ++ko) load(&p.tm_wo, &p.tm_xo, ko * 64, pw, pt);
         }
-        for (int kb = h_a; kb < kb_int; ++kb) load(&p.tm_w, &p.tm_x, kb * kKBlockBytes, wr, tr);
+        for (int kb = h_a; kb < kb_int; ++kb) load_int(kb, wr, tr);
         prev = tile;
       }
       if (two_phase && prev >= 0) {
@@ -196,6 +231,8 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
     if (lane == 0 && leader) {
       constexpr uint32_t id_i8 = idesc_make(2u, 1u, kBlockM * CG, BN);
       constexpr uint32_t id_f16 = idesc_make(1u, 0u, kBlockM * CG, BN);
+      constexpr uint32_t id_sp = idesc_make(2u, 1u, kBlockM * CG, BN) | (1u << 2);  // sparse flag
+      (void)id_sp;
       int stage = 0;
       uint32_t phase = 0;
       auto next_stage = [&](uint64_t& adesc, uint64_t& bdesc) {
@@ -209,13 +246,28 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
         mma_commit<CG>(&empty[stage]);
         if (++stage == C::kStages) { stage = 0; phase ^= 1; }
       };
+      uint32_t meta_slot = 0;
       auto int_blocks = [&](uint32_t d, int k0, int k1) {
         for (int kb = k0; kb < k1; ++kb) {
           uint64_t ad, bd;
           next_stage(ad, bd);
+          if constexpr (!SP) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)  // 4 x K=32 int8 = 128 bytes
-            mma_i8<CG>(d, ad + 2 * k, bd + 2 * k, id_i8, (kb | k) != 0);
+            for (int k = 0; k < 4; ++k)  // 4 x K=32 int8 = 128 bytes
+              mma_i8<CG>(d, ad + 2 * k, bd + 2 * k, id_i8, (kb | k) != 0);
+          } else {
+            // metadata tile -> TMEM ring slot (two 128 x 128-bit copies), then 4 sparse
+            // MMAs of 64 logical K: A advances 32 compressed bytes, B 64 bytes (two atoms)
+            const uint32_t te = tmem_base + C::kMetaCol + meta_slot * 8;
+            const uint32_t se = smem_u32(smem + stage * C::kStageBytes + C::kABytes + C::kBBytes);
+            tmem_cp_128x128b<CG>(te, smem_desc_rows16(se));
+            tmem_cp_128x128b<CG>(te + 4, smem_desc_rows16(se + kMetaTileBytes / 2));
+            const uint64_t bd1 = bd + ((C::kBAtomBytes >> 4) & 0x3FFF);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_sp_i8<CG>(d, ad + 2 * k, (k < 2 ? bd : bd1) + 4 * (k & 1), id_sp, te + 2 * k, (kb | k) != 0);
+            if (++meta_slot == kMetaSlots) meta_slot = 0;
+          }
           release_stage();
         }
       };
@@ -421,10 +473,10 @@ bool make_map(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int elem
   return r == CUDA_SUCCESS;
 }
 
-template <int CG, int BN, int MODE>
+template <int CG, int BN, int MODE, bool SP>
 cudaError_t launch_cfg(const KParams& kp, int num_sms, cudaStream_t stream) {
-  using C = Cfg<CG, BN>;
-  auto kern = quik_gemm_kernel<CG, BN, MODE>;
+  using C = Cfg<CG, BN, SP>;
+  auto kern = quik_gemm_kernel<CG, BN, MODE, SP>;
   cudaError_t e = ensure_smem_attr(kern, C::kSmemBytes);
   if (e != cudaSuccess) return e;
   const long long tiles = static_cast<long long>((kp.M + BN - 1) / BN) * ((kp.N + C::kTileRows - 1) / C::kTileRows);
@@ -451,12 +503,24 @@ cudaError_t launch_cfg(const KParams& kp, int num_sms, cudaStream_t stream) {
 template <int CG, int BN>
 cudaError_t launch_mode(const KParams& kp, int mode, int num_sms, cudaStream_t stream) {
   switch (mode) {
-    case kModeInt32: return launch_cfg<CG, BN, kModeInt32>(kp, num_sms, stream);
-    case kModeAccInitF32: return launch_cfg<CG, BN, kModeAccInitF32>(kp, num_sms, stream);
-    case kModeAccInitF16: return launch_cfg<CG, BN, kModeAccInitF16>(kp, num_sms, stream);
-    case kModeF32: return launch_cfg<CG, BN, kModeF32>(kp, num_sms, stream);
-    case kModeProbe: return launch_cfg<CG, BN, kModeProbe>(kp, num_sms, stream);
-    default: return launch_cfg<CG, BN, kModeF16>(kp, num_sms, stream);
+    case kModeInt32: return launch_cfg<CG, BN, kModeInt32, false>(kp, num_sms, stream);
+    case kModeAccInitF32: return launch_cfg<CG, BN, kModeAccInitF32, false>(kp, num_sms, stream);
+    case kModeAccInitF16: return launch_cfg<CG, BN, kModeAccInitF16, false>(kp, num_sms, stream);
+    case kModeF32: return launch_cfg<CG, BN, kModeF32, false>(kp, num_sms, stream);
+    case kModeProbe: return launch_cfg<CG, BN, kModeProbe, false>(kp, num_sms, stream);
+    default: return launch_cfg<CG, BN, kModeF16, false>(kp, num_sms, stream);
+  }
+}
+
+// 2:4 sparse base weights: the fused modes and the raw int32 accumulator (parity)
+template <int CG, int BN>
+cudaError_t launch_mode_sp(const KParams& kp, int mode, int num_sms, cudaStream_t stream) {
+  switch (mode) {
+    case kModeInt32: return launch_cfg<CG, BN, kModeInt32, true>(kp, num_sms, stream);
+    case kModeF32: return launch_cfg<CG, BN, kModeF32, true>(kp, num_sms, stream);
+    case kModeProbe: return launch_cfg<CG, BN, kModeProbe, true>(kp, num_sms, stream);
+    case kModeF16: return launch_cfg<CG, BN, kModeF16, true>(kp, num_sms, stream);
+    default: return cudaErrorInvalidValue;  // V1/V2 tails read int32 accumulators: dense kernel
   }
 }
 
@@ -470,12 +534,15 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
   if (!get_encoder()) { *err_msg = "cuTensorMapEncodeTiled unavailable"; return cudaErrorNotSupported; }
   // Token tile: narrow UMMA N for small M (memory-bound weight streaming, 1-CTA);
   // CTA-pair M = 256 tiles once the token count makes the GEMM compute-bound.
+  const bool sp = a.sparse && a.mode != kModeAccInitF32 && a.mode != kModeAccInitF16;
   int cg = 1, bn = 128;
   if (a.M <= 32) bn = 32;
   else if (a.M <= 64) bn = 64;
   else if (a.M <= 128) bn = 128;
-  else { cg = 2; bn = 256; }
+  else { cg = 2; bn = sp ? 192 : 256; }  // SP: 2 x 192 accumulator columns + metadata ring in TMEM
   if (gemm_tile_override) { cg = gemm_tile_override >> 16; bn = gemm_tile_override & 0xFFFF; }
+  if (sp && cg == 2 && bn == 256) bn = 192;  // 192 is the sparse CTA-pair tile, 256 the dense one
+  if (!sp && cg == 2 && bn == 192) bn = 256;
 
   KParams kp{};
   kp.M = static_cast<int>(a.M);
@@ -488,7 +555,25 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
   kp.acc_in = a.acc_in;
   kp.ld_acc = a.ld_acc;
   const uint32_t brows = static_cast<uint32_t>(bn / cg);
-  if (kp.kb_int) {
+  if (kp.kb_int && sp) {
+    // compressed weights [N][kpad / 2], activations [M][kpad] (two atoms per stage),
+    // metadata planes [(2 * kb + h) * n_pad + row][16 B]
+    if (a.kpad % (2 * kKBlockBytes) != 0) { *err_msg = "sparse layer: kpad must be a multiple of 256"; return cudaErrorInvalidValue; }
+    kp.kb_int = static_cast<int>(a.kpad / (2 * kKBlockBytes));
+    kp.meta_rows = static_cast<int>(round_up(a.N, kBlockM));
+    cuuint64_t edims[2] = {16, static_cast<cuuint64_t>(2) * kp.kb_int * kp.meta_rows};
+    cuuint64_t estr[1] = {16};
+    cuuint32_t ebox[2] = {16, static_cast<cuuint32_t>(kBlockM)};
+    cuuint32_t eel[2] = {1, 1};
+    if (!make_map(&kp.tm_w, a.w_sp, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, a.kpad / 2, a.N, a.kpad / 2, kBlockM) ||
+        !make_map(&kp.tm_x, a.x, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, a.kpad, a.M, a.kpad, brows) ||
+        g_encode(&kp.tm_e, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(a.meta), edims, estr, ebox, eel,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      *err_msg = "tensor map encode failed (sparse operands)";
+      return cudaErrorInvalidValue;
+    }
+  } else if (kp.kb_int) {
     if (!make_map(&kp.tm_w, a.w, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, a.kpad, a.N, a.kpad, kBlockM) ||
         !make_map(&kp.tm_x, a.x, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, a.kpad, a.M, a.kpad, brows)) {
       *err_msg = "tensor map encode failed (int8 operands)";
@@ -527,6 +612,16 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
   kp.out = a.out;
   kp.ldo = a.ldo;
   const int key = (cg << 16) | bn;
+  if (sp) {
+    switch (key) {
+      case (1 << 16) | 32: return launch_mode_sp<1, 32>(kp, a.mode, num_sms, stream);
+      case (1 << 16) | 64: return launch_mode_sp<1, 64>(kp, a.mode, num_sms, stream);
+      case (1 << 16) | 128: return launch_mode_sp<1, 128>(kp, a.mode, num_sms, stream);
+      case (2 << 16) | 128: return launch_mode_sp<2, 128>(kp, a.mode, num_sms, stream);
+      case (2 << 16) | 192: return launch_mode_sp<2, 192>(kp, a.mode, num_sms, stream);
+      default: *err_msg = "unsupported sparse tile configuration"; return cudaErrorInvalidValue;
+    }
+  }
   switch (key) {
     case (1 << 16) | 32: return launch_mode<1, 32>(kp, a.mode, num_sms, stream);
     case (1 << 16) | 64: return launch_mode<1, 64>(kp, a.mode, num_sms, stream);

@@ -59,7 +59,20 @@ struct GemmArgs {
   int mode;
   const int32_t* acc_in; // kModeAccInit*: int32 accumulators [M][ld_acc]
   int64_t ld_acc;
+  // 2:4 sparse base weights (sparse != 0; kpad multiple of 256): compressed values
+  // [N][kpad / 2] (two kept codes per group of 4, ascending position) and metadata
+  // planes [(2 * kb + h) * round_up(N, 128) + n][16 B] for stage kb (256 logical K),
+  // half h (128 logical K = 32 groups, nibble per group, low nibble first).
+  int sparse;
+  const int8_t* w_sp;
+  const uint8_t* meta;
 };
+
+// Compresses dense int8 GEMM-layout weights [N][kpad] (kpad % 256 == 0) into the
+// 2:4 sparse operands above. *bad is set to 1 if a group of 4 has more than two
+// non-zero codes (the layer then stays dense).
+cudaError_t launch_compress_24(const int8_t* w8, int64_t N, int64_t kpad, int8_t* w_sp, uint8_t* meta, int* bad,
+                               cudaStream_t stream);
 
 // Launches the fused persistent tcgen05 kernel (int8 GEMM + f16 outlier GEMM +
 // dequantisation epilogue). Returns a cudaError_t / CUresult-derived status in

@@ -872,6 +872,51 @@ __global__ void __launch_bounds__(256) rtn_rows_kernel(const float* __restrict__
   for (int64_t i = tid; i < n_out; i += blockDim.x) outlier_w[r * n_out + i] = row[out_src[i]];
 }
 
+// 2:4 compression of the GEMM-layout weights (layer create). Thread = one row x
+// 32 logical K (8 groups of 4): two kept codes per group (the non-zero ones, padded
+// with the lowest remaining positions), ascending, and the group's metadata nibble
+// (index of the first kept value in bits [1:0], second in [3:2]).
+__global__ void compress24_kernel(const int8_t* __restrict__ w8, int64_t N, int64_t kpad, int8_t* __restrict__ w_sp,
+                                  uint8_t* __restrict__ meta, int64_t npad, int* bad) {
+  const int64_t per_row = kpad / 32;
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= N * per_row) return;
+  const int64_t n = idx / per_row, o = idx % per_row;
+  const uint4* src = reinterpret_cast<const uint4*>(w8 + n * kpad + 32 * o);
+  const uint4 lo = src[0], hi = src[1];
+  const uint32_t words[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+  uint32_t vals[4] = {0, 0, 0, 0};
+  uint32_t nib = 0;
+  bool over = false;
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    const uint32_t w = words[g];
+    int i0 = -1, i1 = -1, cnt = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if ((w >> (8 * e)) & 0xFFu) {
+        ++cnt;
+        if (i0 < 0) i0 = e;
+        else if (i1 < 0) i1 = e;
+      }
+    over |= cnt > 2;
+    if (i0 < 0) {
+      i0 = 0;
+      i1 = 1;
+    } else if (i1 < 0) {
+      if (i0 == 3) i0 = 2, i1 = 3;
+      else i1 = i0 + 1;
+    }
+    const uint32_t v0 = (w >> (8 * i0)) & 0xFFu, v1 = (w >> (8 * i1)) & 0xFFu;
+    vals[g >> 1] |= (v0 | (v1 << 8)) << (16 * (g & 1));
+    nib |= static_cast<uint32_t>(i0 | (i1 << 2)) << (4 * g);
+  }
+  if (over) atomicExch(bad, 1);
+  *reinterpret_cast<uint4*>(w_sp + n * (kpad / 2) + 16 * o) = make_uint4(vals[0], vals[1], vals[2], vals[3]);
+  const int64_t g0 = 8 * o, kb = g0 / 64, gl = g0 % 64, h = gl / 32;
+  *reinterpret_cast<uint32_t*>(meta + ((2 * kb + h) * npad + n) * 16 + (gl % 32) / 2) = nib;
+}
+
 dim3 grid2(int64_t cols, int64_t rows) {
   int64_t gx = (cols + 255) / 256;
   if (gx > 64) gx = 64;
@@ -984,6 +1029,18 @@ cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t stream) {
 cudaError_t launch_split(const SplitArgs& a, cudaStream_t stream) {
   if (a.M == 0 || a.kb + a.opad == 0) return cudaSuccess;
   split_kernel<<<grid2(a.kb + a.opad, a.M), 256, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compress_24(const int8_t* w8, int64_t N, int64_t kpad, int8_t* w_sp, uint8_t* meta, int* bad,
+                               cudaStream_t stream) {
+  if (N == 0 || kpad == 0) return cudaSuccess;
+  if (kpad % 256) return cudaErrorInvalidValue;
+  const int64_t npad = round_up(N, kBlockM);
+  cudaError_t e = cudaMemsetAsync(meta, 0, static_cast<size_t>(2 * (kpad / 256) * npad * 16), stream);
+  if (e != cudaSuccess) return e;
+  const int64_t work = N * (kpad / 32);
+  compress24_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, stream>>>(w8, N, kpad, w_sp, meta, npad, bad);
   return cudaGetLastError();
 }
 

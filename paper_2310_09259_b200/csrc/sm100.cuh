@@ -216,6 +216,50 @@ __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a_desc, uint64
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// 2:4-sparse D[tmem] (+)= A_sparse[smem] * B[smem]^T, int8 -> int32, K = 64 logical
+// per instruction. The metadata (4 bits per group of 4 logical K: index of the
+// first kept value in bits [1:0], of the second in [3:2]; group g of the MMA at
+// bits 4g of the lane's 64-bit word) is read from TMEM at `e_tmem` (lane = A row).
+// Encoding pinned on the device by tools/sp_probe.cu / sp_probe2.cu.
+template <int CG>
+__device__ __forceinline__ void mma_sp_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t e_tmem, uint32_t accumulate) {
+  if constexpr (CG == 1)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.sp.cta_group::1.kind::i8 [%0], %1, %2, [%5], %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(e_tmem)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.sp.cta_group::2.kind::i8 [%0], %1, %2, [%5], %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(e_tmem)
+        : "memory");
+}
+// Shared-memory descriptor of a plain [rows][16 B] row-major tile (no swizzle):
+// core matrices of 8 rows x 16 B are contiguous 128-byte blocks, SBO = 128 B.
+__device__ __forceinline__ uint64_t smem_desc_rows16(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1u) << 16;
+  d |= static_cast<uint64_t>(128u >> 4) << 32;
+  d |= static_cast<uint64_t>(1u) << 46;
+  return d;
+}
+// Shared -> TMEM copy of 128 lanes x 128 bits (lane i <- row i of the tile). CG == 2:
+// issued by the leader; each CTA of the pair copies from its own shared memory
+// (same offset) into its own TMEM.
+template <int CG>
+__device__ __forceinline__ void tmem_cp_128x128b(uint32_t taddr, uint64_t sdesc) {
+  if constexpr (CG == 1)
+    asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+  else
+    asm volatile("tcgen05.cp.cta_group::2.128x128b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+
 // Arrive on an mbarrier once all previously issued tcgen05 async ops of this
 // thread complete (implies tcgen05.fence::before_thread_sync). CG == 2: the
 // arrival is multicast to the same barrier in both CTAs of the pair.

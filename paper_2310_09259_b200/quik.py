@@ -261,7 +261,10 @@ class QuikLinear:
     tcgen05 kernel on the current CUDA stream. `row_begin/row_end` select an
     output-row shard (multi-GPU column sharding)."""
 
-    def __init__(self, layer: QuikLinearLayer, device: Optional[int] = None, row_begin: int = 0, row_end: int = 0):
+    def __init__(self, layer: QuikLinearLayer, device: Optional[int] = None, row_begin: int = 0, row_end: int = 0,
+                 sparse: Optional[bool] = None):
+        """sparse: request the 2:4 sparse GEMM (default: when the weights carry a
+        SparsityMask, i.e. come from sparsegpt_joint, quantizer.cpp:299-337)."""
         torch = _torch()
         layer.validate()
         self._lib = _lib.load()
@@ -287,7 +290,8 @@ class QuikLinear:
             scales=k["scales"].ctypes.data, wreduced=k["wreduced"].ctypes.data,
             outlier_weights=k["ow"].ctypes.data, outlier_indices=k["idx"].ctypes.data if k["idx"].size else None,
             n_outlier=self.n_outlier, bias=None if k["bias"] is None else k["bias"].ctypes.data,
-            row_begin=row_begin, row_end=row_end)
+            row_begin=row_begin, row_end=row_end,
+            sparsity=int(bool(w.mask is not None if sparse is None else sparse)))
         h = C.c_void_p()
         with torch.cuda.device(self.device):
             _lib.check(self._lib.quik_layer_create(self.ctx.handle, C.byref(d), C.byref(h)))
@@ -299,7 +303,7 @@ class QuikLinear:
 
     @classmethod
     def from_device(cls, outliers: OutlierSet, base, scales, wreduced, outlier_weights, bits: int, bias=None,
-                    row_begin: int = 0, row_end: int = 0) -> "QuikLinear":
+                    row_begin: int = 0, row_end: int = 0, sparse: bool = False) -> "QuikLinear":
         """Builds the layer straight from device tensors in the reference formats
         (e.g. the output of rtn_quantize_weights_device) without a host round trip."""
         torch = _torch()
@@ -317,7 +321,8 @@ class QuikLinear:
             base=base.data_ptr(), scales=scales.data_ptr(), wreduced=wreduced.data_ptr(),
             outlier_weights=None if ow is None else ow.data_ptr(),
             outlier_indices=idx.ctypes.data if idx.size else None, n_outlier=self.n_outlier,
-            bias=None if bias is None else bias.data_ptr(), row_begin=row_begin, row_end=row_end)
+            bias=None if bias is None else bias.data_ptr(), row_begin=row_begin, row_end=row_end,
+            sparsity=int(sparse))
         h = C.c_void_p()
         with torch.cuda.device(self.device):
             torch.cuda.current_stream().synchronize()
@@ -335,6 +340,11 @@ class QuikLinear:
                 self.handle = None
         except Exception:
             pass
+
+    @property
+    def is_sparse(self) -> bool:
+        """True when the layer runs the 2:4 sparse tcgen05 GEMM."""
+        return bool(self._lib.quik_layer_is_sparse(self.handle))
 
     @staticmethod
     def launches(variant: PipelineVariant = PipelineVariant.V3FusedEpilogue) -> int:

@@ -12,6 +12,9 @@ Cases:
   ref_test_layer_8bit  same generator, 8-bit, 24 x 200 -> 72, 8 outliers
   f16_*                numpy-seeded layers with f16-representable x and outlier
                        weights (device f16 path), weights from the reference RTN
+  sp24_*               2:4 sparse layers from the reference's sparsegpt_joint (identity
+                       or random-PSD Hessian), mask stored; *_tail2 / *_tail3 have a
+                       trailing dense remainder group of 2 / 3 base columns
 For every case the npz stores the layer, x, and the reference outputs:
 quantize_activations_fused (packed / scale / zero / x_out), int_matmul of the
 packed activations with the packed weights, and quik_matmul V1 / V2 / V3.
@@ -49,6 +52,26 @@ def ref_layer(r, seed, tokens, in_f, out_f, bits, O, heavy):
     return L, x
 
 
+def sparse_layer(r, rng, M, K, N, O, bits, psd):
+    x = rng.normal(0.0, 1.0, size=(M, K)).astype(np.float32)
+    for c in rng.choice(K, size=3, replace=False):
+        x[:, c] *= 100.0
+    x = x.astype(np.float16).astype(np.float32)
+    idx = r.select_outliers(x, O)
+    w = rng.normal(0.0, 0.5, size=(N, K)).astype(np.float32)
+    hsum = None
+    if psd:
+        xc = rng.normal(0.0, 1.0, size=(4 * K, K))
+        hsum = xc.T @ xc
+    st, q = r.sparsegpt_joint(w, idx, bits, hsum=hsum, tokens=4 * K if psd else 0)
+    assert st == 0, st
+    bias = rng.normal(0.0, 0.1, size=N).astype(np.float32)
+    L = dict(in_features=K, out_features=N, bits=bits, act_bits=bits, base=q["base"], scales=q["scales"],
+             wreduced=q["wreduced"], outlier_weights=q["outlier_weights"].astype(np.float16).astype(np.float32),
+             idx=idx, bias=bias, mask=q["mask"])
+    return L, x
+
+
 def outputs(r, L, x):
     bits = L["bits"]
     st, pk, sc, ze, xo = r.quantize_fused(x, L["idx"], bits)
@@ -78,14 +101,27 @@ def main():
     }.items():
         L, x, _ = make_layer(rng, M, K, N, bits, O, heavy_cols=heavy, checker=r)
         cases[name] = (L, x)
+    # 2:4 sparse layers (cfg5 path) from the reference's sparsegpt_joint, f16-representable
+    # x and outlier weights; the mask is stored so the device builds the sparse GEMM
+    srng = np.random.default_rng(240)
+    for name, (M, K, N, O, bits, psd) in {
+        "sp24_w4_o16": (40, 256, 160, 16, 4, False),
+        "sp24_w4_o64_psd": (24, 512, 200, 64, 4, True),
+        "sp24_w8_o32_psd": (17, 384, 136, 32, 8, True),
+        "sp24_w4_o0": (64, 640, 256, 0, 4, True),
+        "sp24_w4_o0_tail2": (12, 262, 96, 0, 4, False),
+        "sp24_w4_o0_tail3": (12, 259, 96, 0, 4, False),
+    }.items():
+        cases[name] = sparse_layer(r, srng, M, K, N, O, bits, psd)
     blob, manifest = {}, {}
     for name, (L, x) in cases.items():
         out = outputs(r, L, x)
         manifest[name] = dict(M=int(x.shape[0]), K=int(L["in_features"]), N=int(L["out_features"]),
                               outliers=int(len(L["idx"])), bits=int(L["bits"]))
         blob[f"{name}.x"] = x
-        for k in ("base", "scales", "wreduced", "outlier_weights", "idx", "bias"):
-            blob[f"{name}.{k}"] = np.asarray(L[k])
+        for k in ("base", "scales", "wreduced", "outlier_weights", "idx", "bias", "mask"):
+            if k in L:
+                blob[f"{name}.{k}"] = np.asarray(L[k])
         for k, v in out.items():
             blob[f"{name}.{k}"] = v
     np.savez_compressed(HERE / "quik_golden.npz", **blob)

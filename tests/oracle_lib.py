@@ -222,6 +222,25 @@ class Ref(_Base):
         self.lib.qr_layer_destroy.restype = None
         self.lib.qr_layer_destroy(C.c_void_p(h))
 
+    def sparsegpt_joint(self, w, idx, bits, hsum=None, tokens=0):
+        """The reference's sparsegpt_joint (quantizer.cpp:299-337): 2:4 pruning +
+        quantization. hsum: K x K FP64 Hessian sum or None (identity)."""
+        w = np.ascontiguousarray(w, np.float32)
+        N, K = w.shape
+        idx = np.ascontiguousarray(idx, np.int64)
+        kb = K - idx.size
+        base = np.zeros(max(N * row_bytes(kb, bits), 1), np.uint8)
+        sc = np.zeros(max(N, 1), np.float32)
+        wr = np.zeros(max(N, 1), np.float32)
+        ow = np.zeros(max(N * idx.size, 1), np.float32)
+        mask = np.zeros(max(N * kb, 1), np.uint8)
+        h = None if hsum is None else np.ascontiguousarray(hsum, np.float64)
+        st = self.f("sparsegpt_joint")(_p(w), C.c_int64(N), C.c_int64(K), _p(idx), C.c_int64(idx.size), bits,
+                                       _p(h) if h is not None else None, C.c_int64(tokens), _p(base), _p(sc), _p(wr),
+                                       _p(ow), _p(mask))
+        return st, dict(base=base[: N * row_bytes(kb, bits)], scales=sc[:N], wreduced=wr[:N],
+                        outlier_weights=ow[: N * idx.size].reshape(N, idx.size), mask=mask[: N * kb].reshape(N, kb))
+
     def random_matrix(self, seed, rows, cols, stddev=1.0):
         out = np.zeros(max(rows * cols, 1), np.float32)
         fn = self.lib.qr_random_matrix

@@ -592,3 +592,105 @@ def test_hot_quantizer_ties_zeros_and_shapes():
         x = rng.normal(0, 1, size=(3, K)).astype(np.float16)
         idx = np.sort(rng.choice(K, size=O, replace=False)).astype(np.int64)
         _hot_k1_case(m, o, x, idx, 4 if K == 8192 else 8)
+
+
+# --------------------------------------------------------------------------- 2:4 sparse base weights (cfg5)
+
+
+def to_sparse_layer(L):
+    layer = to_layer(L)
+    layer.weights.mask = np.asarray(L["mask"], np.uint8)
+    return layer
+
+
+def make_sparse_layer(rng, M, K, N, bits, O, heavy_cols=2):
+    """RTN layer whose permuted base weights are pruned 2:4 by magnitude (the two
+    smallest |w| of every aligned group of 4 base columns -> 0) before quantization."""
+    o = oracle()
+    L, x, w = make_layer(rng, M, K, N, bits, O, heavy_cols=heavy_cols)
+    idx = np.asarray(L["idx"], np.int64)
+    base_cols = np.setdiff1d(np.arange(K), idx)
+    kb = base_cols.size
+    wb = w[:, base_cols].copy()
+    g = kb // 4 * 4
+    grp = np.abs(wb[:, :g]).reshape(N, -1, 4)
+    drop = np.argsort(grp, axis=-1, kind="stable")[..., :2]
+    mask = np.ones((N, kb), np.uint8)
+    mg = mask[:, :g].reshape(N, -1, 4)
+    np.put_along_axis(mg, drop, 0, axis=-1)
+    mask[:, :g] = mg.reshape(N, g)
+    w2 = w.copy()
+    w2[:, base_cols] = wb * mask
+    q = o.rtn_quantize_weights(w2, idx, bits)
+    L.update(base=q["base"], scales=q["scales"], wreduced=q["wreduced"], mask=mask)
+    return L, x
+
+
+@pytest.mark.parametrize("name", sorted(n for n in _CASES if n.startswith("sp24_")))
+def test_sparse_device_matches_reference_golden(name):
+    """2:4 sparse layers from the reference's sparsegpt_joint (tests/golden): the device
+    compresses them and runs tcgen05.mma.sp; outputs vs the reference quik_matmul."""
+    m = q()
+    import torch
+
+    meta = _CASES[name]
+    g = lambda k: _G[f"{name}.{k}"]  # noqa: E731
+    K, N, O, bits = meta["K"], meta["N"], meta["outliers"], meta["bits"]
+    L = dict(in_features=K, out_features=N, bits=bits, base=g("base"), scales=g("scales"), wreduced=g("wreduced"),
+             outlier_weights=g("outlier_weights"), idx=g("idx"), bias=g("bias"), mask=g("mask"))
+    dev = m.QuikLinear(to_sparse_layer(L))
+    # a trailing dense remainder group of 3 base columns is not 2:4 -> the layer stays dense
+    assert dev.is_sparse == (not name.endswith("tail3")), name
+    x = g("x")
+    xt = torch.from_numpy(x).cuda()
+    want = g("out_v3")
+    for v in m.PipelineVariant:
+        y = dev(xt, out_dtype=torch.float32, variant=v).cpu().numpy()
+        if O == 0:
+            np.testing.assert_array_equal(y.view(np.uint32), want.view(np.uint32))
+        else:
+            assert rel_frob(want, y) < 1e-5, (v, rel_frob(want, y))
+    y16 = dev(xt.half()).float().cpu().numpy()
+    assert rel_frob(want, y16) <= 5e-4
+
+
+@pytest.mark.parametrize("cg,bn", [(1, 32), (1, 64), (1, 128), (2, 128), (2, 192)])
+def test_sparse_every_tile_config_exact(tile, cg, bn):
+    """Each sparse GEMM tile: O = 0 layers bit-exact (f32 out, so the INT32
+    accumulators of the compressed MMAs are exact), outlier layers within tolerance,
+    V1 = V2 = V3, ragged M / N / K."""
+    m = q()
+    o = oracle()
+    import torch
+
+    assert tile(cg, bn) == 0
+    rng = np.random.default_rng(500 + 10 * cg + bn)
+    for (M, K, N, bits, O) in [(300, 1024, 500, 4, 0), (77, 600, 257, 8, 0), (200, 1100, 384, 4, 64)]:
+        L, x = make_sparse_layer(rng, M, K, N, bits, O)
+        st, want = o.quik_matmul(L, x, 2)
+        assert st == 0
+        dev = m.QuikLinear(to_sparse_layer(L))
+        assert dev.is_sparse
+        xt = torch.from_numpy(x).cuda()
+        outs = [dev(xt, out_dtype=torch.float32, variant=v).cpu().numpy() for v in m.PipelineVariant]
+        for y in outs:
+            np.testing.assert_array_equal(y.view(np.uint32), outs[2].view(np.uint32))
+        if O == 0:
+            np.testing.assert_array_equal(outs[2].view(np.uint32), want.view(np.uint32))
+        else:
+            assert rel_frob(want, outs[2]) < 1e-5
+
+
+def test_sparse_not_compressible_stays_dense():
+    """A layer flagged sparse whose groups hold 3+ non-zero codes stays on the dense
+    GEMM (no silent wrong answers)."""
+    m = q()
+    o = oracle()
+    rng = np.random.default_rng(9)
+    L, x, _ = make_layer(rng, 20, 256, 64, 4, 0)
+    L["mask"] = np.ones((64, 256), np.uint8)
+    dev = m.QuikLinear(to_sparse_layer(L))
+    assert not dev.is_sparse
+    st, want = o.quik_matmul(L, x, 2)
+    got = m.quik_matmul(to_layer(L), x)
+    np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))

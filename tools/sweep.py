@@ -22,6 +22,10 @@ SHAPES = [
     ("cfg3 70B up/gate", 4096, 8192, 28672, 256, 4),
     ("cfg3 70B down W8A8", 4096, 28672, 8192, 896, 8),
     ("cfg5-shape 13B up", 2048, 5120, 13824, 256, 4),
+    ("cfg5 13B up 2:4", 2048, 5120, 13824, 256, 4, True),
+    ("cfg5 13B q 2:4", 2048, 5120, 5120, 256, 4, True),
+    ("cfg3 70B up/gate 2:4", 4096, 8192, 28672, 256, 4, True),
+    ("cfg4 OPT fc1 M=16 2:4", 16, 9216, 36864, 256, 4, True),
 ]
 OPT_FC1 = [(m, 9216, 36864, 256, 4) for m in (1, 16, 64, 128, 256, 512, 1024, 2048, 4096, 8192)]
 
@@ -39,9 +43,9 @@ def timeit(fn, iters=20, warm=5):
     return a.elapsed_time(b) / iters
 
 
-def run(name, M, K, N, O, bits, layers):
+def run(name, M, K, N, O, bits, layers, sparse=False):
     dev = torch.device("cuda", 0)
-    key = (K, N, O, bits)
+    key = (K, N, O, bits, sparse)
     if key not in layers:
         layers.clear()
         torch.cuda.empty_cache()
@@ -49,9 +53,13 @@ def run(name, M, K, N, O, bits, layers):
         idx = torch.randperm(K, generator=g, device=dev)[:O].sort().values.cpu().numpy()
         outl = q.OutlierSet.from_indices(K, idx)
         W = torch.randn(N, K, device=dev, generator=g)
+        if sparse:
+            from bench import prune_24
+
+            prune_24(W, torch.as_tensor(outl.permutation[: K - O], device=dev))
         base, sc, wr, ow = q.rtn_quantize_weights_device(W, outl, bits)
         del W
-        layers[key] = (q.QuikLinear.from_device(outl, base, sc, wr, ow, bits),
+        layers[key] = (q.QuikLinear.from_device(outl, base, sc, wr, ow, bits, sparse=sparse),
                        torch.randn(N, K, device=dev, dtype=torch.float16))
     layer, W16 = layers[key]
     x = torch.randn(M, K, device=dev, dtype=torch.float16)
@@ -79,7 +87,7 @@ def run(name, M, K, N, O, bits, layers):
         torch.matmul(x, W16.t(), out=out16)
     t16 = timeit(g16.replay)
     ops = 2.0 * M * N * K
-    return dict(name=name, M=M, K=K, N=N, O=O, bits=bits, step_ms=t_step, step_eager_ms=t_step_eager,
+    return dict(name=name, M=M, K=K, N=N, O=O, bits=bits, sparse=layer.is_sparse, step_ms=t_step, step_eager_ms=t_step_eager,
                 k1_ms=t_k1, gemm_ms=t_gemm,
                 tops=ops / t_step / 1e9, cublas_f16_ms=t16, speedup_vs_f16=t16 / t_step)
 
@@ -87,12 +95,15 @@ def run(name, M, K, N, O, bits, layers):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--only", default="")
     args = ap.parse_args()
     layers = {}
     res = []
     for s in SHAPES:
-        res.append(run(*s, layers))
-    for m, K, N, O, bits in (OPT_FC1[::3] if args.quick else OPT_FC1):
+        if args.only and args.only not in s[0]:
+            continue
+        res.append(run(*s[:6], layers, *s[6:]))
+    for m, K, N, O, bits in ([] if args.only else OPT_FC1[::3] if args.quick else OPT_FC1):
         res.append(run(f"cfg4 OPT-66B fc1 M={m}", m, K, N, O, bits, layers))
     for r in res:
         print(json.dumps(r), flush=True)
