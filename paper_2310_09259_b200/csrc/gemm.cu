@@ -30,6 +30,8 @@
 
 #include <cstdlib>
 #include <mutex>
+#include <vector>
+#include <cstdio>
 
 #include "kernels.h"
 #include "sm100.cuh"
@@ -96,24 +98,49 @@ struct KParams {
   const int32_t* acc_in;
   long long ld_acc;
   int meta_rows;  // SP: n_pad = round_up(N, 128) rows per metadata (stage, half) plane
+  int split_num;  // h_a = kb_int * split_num / 8
+  // diagnostics (QUIK_GEMM_TRACE): per leader CTA and tile iteration (< kTraceTiles),
+  // kTraceSlots globaltimer stamps; null in normal runs
+  long long* trace;
 };
+constexpr int kTraceTiles = 64;
+constexpr int kTraceSlots = 12;
+__device__ __forceinline__ long long gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// slots: 0 MMA before tempty wait, 1 after it, 2 first-half int issued, 3 after tconv
+// wait, 4 all issued, 5 summed full-barrier wait (ns); 6 epi before tint wait, 7 after,
+// 8 pass 1 done, 9 after tfin wait, 10 pass 2 done
 
-template <int CG, int MODE>
-__device__ __forceinline__ void arrive_leader(uint64_t* bar) {
-  if constexpr (CG == 2) mbar_arrive_cluster(bar, 0);
+// Arrive on the barrier of this CTA pair's leader (cluster rank `leader_rank`).
+template <int CG>
+__device__ __forceinline__ void arrive_leader(uint64_t* bar, uint32_t leader_rank) {
+  if constexpr (CG == 2) mbar_arrive_cluster(bar, leader_rank);
   else mbar_arrive(bar);
 }
 
-template <int CG, int BN, int MODE, bool SP>
+// MC (CG == 2 only): clusters of 4 CTAs = 2 CTA pairs that compute the tiles of two
+// adjacent weight blocks on the same token block. The activation (B) tiles are
+// identical for both pairs, so each is fetched once: CTA (pair p, rank r) loads
+// half p of its B rows and TMA-multicasts it to (0, r) and (1, r). A stage is
+// refilled only after both pairs' MMAs released it (empty barriers count 2, the
+// MMA commits multicast to all 4 CTAs). Halves the L2->SM traffic of B.
+template <int CG, int BN, int MODE, bool SP, bool MC>
 __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_constant__ KParams p) {
   using C = Cfg<CG, BN, SP>;
+  static_assert(!MC || CG == 2, "multicast clusters pair CTA pairs");
+  constexpr int CL = MC ? 4 : CG;  // CTAs per cluster
   constexpr bool kAccGlobal = MODE == kModeAccInitF32 || MODE == kModeAccInitF16;
   constexpr bool kF16Out = MODE == kModeF16 || MODE == kModeAccInitF16;
   constexpr bool kInt32Out = MODE == kModeInt32;
   constexpr bool kProbe = MODE == kModeProbe;
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned, derived by pointer arithmetic so the compiler keeps the shared
+  // address space (STS / LDS instead of generic stores in the epilogue staging)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* staging = smem + C::kStages * C::kStageBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(staging + kStagingBytes);
   uint64_t* empty = full + C::kStages;
@@ -125,13 +152,19 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const uint32_t crank = CG == 2 ? cluster_ctarank() : 0u;
+  const uint32_t rank = crank & 1u;   // rank inside the CTA pair
+  const uint32_t pair = crank >> 1;   // pair inside the cluster (MC)
+  const uint32_t leader_rank = crank & ~1u;
   const bool leader = rank == 0;
+  const uint16_t pair_mask = static_cast<uint16_t>(3u << (2 * pair));
 
   const int kb_int = kAccGlobal ? 0 : p.kb_int;
   const int kb_out = kInt32Out ? 0 : p.kb_out;
   const bool two_phase = kb_out > 0;
-  const int h_a = kb_int / 2;
+  // int k-blocks of tile i issued before the outlier MMAs of tile i-1: the epilogue's
+  // in-place dequantisation of tile i-1 must finish within them (p.split_num / 8)
+  const int h_a = (kb_int * p.split_num) >> 3;
 
   if (warp == 0 && lane == 0) {
     if (kb_int) { tma_prefetch(&p.tm_w); tma_prefetch(&p.tm_x); }
@@ -139,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
     if (kb_out) { tma_prefetch(&p.tm_wo); tma_prefetch(&p.tm_xo); }
   }
   if (warp == 1 && lane == 0) {
-    for (int i = 0; i < C::kStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < C::kStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], MC ? 2 : 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tint[i], 1);
       mbar_init(&tconv[i], kEpiWarps * CG);
@@ -159,9 +192,14 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
 
   const int tiles_m = (p.M + BN - 1) / BN;
   const int tiles_n = (p.N + C::kTileRows - 1) / C::kTileRows;
-  const int num_tiles = tiles_m * tiles_n;
-  const int cluster_id = blockIdx.x / CG;
-  const int num_clusters = gridDim.x / CG;
+  // work units: tiles, or (MC) pairs of weight blocks on one token block
+  const int num_tiles = tiles_m * (MC ? (tiles_n + 1) / 2 : tiles_n);
+  const int cluster_id = blockIdx.x / CL;
+  const int num_clusters = gridDim.x / CL;
+  auto decode = [&](int tile, int& nb, int& mb) {
+    nb = MC ? 2 * (tile / tiles_m) + static_cast<int>(pair) : tile / tiles_m;
+    mb = tile % tiles_m;
+  };
   // Tile order: consecutive tile ids share the weight block (n) so the clusters
   // that run concurrently read the same weight rows through L2.
 
@@ -176,13 +214,24 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
         if constexpr (CG == 1) tma_load_2d(dst, m, c0, c1, &full[stage], pol);
         else tma_load_2d_pair(dst, m, c0, c1, &full[stage], pol);
       };
+      // B (token) tile of this CTA: MC -> half `pair`, multicast to both pairs
+      const uint16_t mc_mask = static_cast<uint16_t>((1u << rank) | (1u << (2 + rank)));
+      auto tma_b = [&](uint8_t* dst, const CUtensorMap* m, int c0, int trow, uint64_t pol) {
+        if constexpr (MC) {
+          constexpr int kHalfRows = C::kBRows / 2;
+          tma_load_2d_pair_mc(dst + pair * kHalfRows * kKBlockBytes, m, c0, trow + static_cast<int>(pair) * kHalfRows,
+                              &full[stage], mc_mask, pol);
+        } else {
+          tma(dst, m, c0, trow, pol);
+        }
+      };
       // outlier block (or dense integer block): A + one B atom at column kc
       auto load = [&](const CUtensorMap* ma, const CUtensorMap* mx, int kc, int wrow, int trow) {
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* sa = smem + stage * C::kStageBytes;
         if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::kOutStageBytes);
         tma(sa, ma, kc, wrow, pol_w);
-        tma(sa + C::kABytes, mx, kc, trow, pol_x);
+        tma_b(sa + C::kABytes, mx, kc, trow, pol_x);
         if (++stage == C::kStages) { stage = 0; phase ^= 1; }
       };
       // integer block kb: dense = load(); SP = compressed A + two B atoms + metadata tile
@@ -196,15 +245,16 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
           uint8_t* se = sb + C::kBBytes;
           if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::kIntStageBytes);
           tma(sa, &p.tm_w, kb * kKBlockBytes, wrow, pol_w);
-          tma(sb, &p.tm_x, kb * 2 * kKBlockBytes, trow, pol_x);
-          tma(sb + C::kBAtomBytes, &p.tm_x, kb * 2 * kKBlockBytes + kKBlockBytes, trow, pol_x);
+          tma_b(sb, &p.tm_x, kb * 2 * kKBlockBytes, trow, pol_x);
+          tma_b(sb + C::kBAtomBytes, &p.tm_x, kb * 2 * kKBlockBytes + kKBlockBytes, trow, pol_x);
           tma(se, &p.tm_e, 0, (2 * kb) * p.meta_rows + wrow, pol_w);
           tma(se + kMetaTileBytes / 2, &p.tm_e, 0, (2 * kb + 1) * p.meta_rows + wrow, pol_w);
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
       };
       auto rows_of = [&](int tile, int& wrow, int& trow) {
-        const int nb = tile / tiles_m, mb = tile % tiles_m;
+        int nb, mb;
+        decode(tile, nb, mb);
         wrow = nb * C::kTileRows + static_cast<int>(rank) * kBlockM;
         trow = mb * BN + static_cast<int>(rank) * C::kBRows;
       };
@@ -235,15 +285,22 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
       (void)id_sp;
       int stage = 0;
       uint32_t phase = 0;
+      long long full_wait = 0;
       auto next_stage = [&](uint64_t& adesc, uint64_t& bdesc) {
-        mbar_wait(&full[stage], phase);
+        if (p.trace) {
+          const long long t0 = gtime();
+          mbar_wait(&full[stage], phase);
+          full_wait += gtime() - t0;
+        } else {
+          mbar_wait(&full[stage], phase);
+        }
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
         adesc = umma_desc_sw128(sa);
         bdesc = umma_desc_sw128(sa + C::kABytes);
       };
       auto release_stage = [&]() {
-        mma_commit<CG>(&empty[stage]);
+        mma_commit<CG>(&empty[stage], MC ? static_cast<uint16_t>(0xF) : static_cast<uint16_t>(3));
         if (++stage == C::kStages) { stage = 0; phase ^= 1; }
       };
       uint32_t meta_slot = 0;
@@ -284,18 +341,24 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
             mma_f16<CG>(d, ad + 2 * k, bd + 2 * k, id_f16, 1u);
           release_stage();
         }
-        mma_commit<CG>(&tfin[bp]);
+        mma_commit<CG>(&tfin[bp], pair_mask);
       };
       int it = 0;
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
         const int b = it & 1;
+        long long* tr = (p.trace && it < kTraceTiles) ? p.trace + (cluster_id * kTraceTiles + it) * kTraceSlots : nullptr;
+        if (tr) { tr[0] = gtime(); full_wait = 0; }
         mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
+        if (tr) tr[1] = gtime();
         const uint32_t d = tmem_base + b * BN;
         int_blocks(d, 0, h_a);
+        if (tr) tr[2] = gtime();
         if (two_phase && it > 0) out_blocks(it - 1);
+        if (tr) tr[3] = gtime();
         int_blocks(d, h_a, kb_int);
-        mma_commit<CG>(&tint[b]);
+        mma_commit<CG>(&tint[b], pair_mask);
+        if (tr) { tr[4] = gtime(); tr[5] = full_wait; }
       }
       if (two_phase && it > 0) out_blocks(it - 1);
     }
@@ -314,7 +377,8 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
       const int b = it & 1;
       const uint32_t par = (it >> 1) & 1;
-      const int nb = tile / tiles_m, mb = tile % tiles_m;
+      int nb, mb;
+      decode(tile, nb, mb);
       const int n0 = nb * C::kTileRows + static_cast<int>(rank) * kBlockM + q * 32;  // warp's first feature
       const int n = n0 + lane;
       const bool n_ok = n < p.N;
@@ -325,10 +389,35 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
         if (p.bias) bs = __ldg(&p.bias[n]);
       }
       const uint32_t tacc = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + b * BN;
+      // per-token activation scale / shifted zero of this warp's chunks, loaded before
+      // waiting for the accumulators so their latency is off the critical path
+      // (the outlier MMAs of this tile wait for the dequantisation below)
+      constexpr int kMaxChunks = (kHalf + kChunk - 1) / kChunk;
+      float sa_pre[kMaxChunks], zs_pre[kMaxChunks];
+#pragma unroll
+      for (int ci = 0; ci < kMaxChunks; ++ci) {
+        const int t_l = mb * BN + c_begin + ci * kChunk + lane;
+        const bool ok = !kInt32Out && t_l < p.M && c_begin + ci * kChunk < c_end;
+        const float sa_l = ok ? __ldg(&p.a_scale[t_l]) : 0.f;
+        const float za_l = ok ? __ldg(&p.a_zero[t_l]) : 0.f;
+        sa_pre[ci] = sa_l;
+        zs_pre[ci] = __fadd_rn(za_l, __fmul_rn(p.half_range, sa_l));  // runtime.cpp:74
+      }
+      auto pick = [&](const float (&a)[kMaxChunks], int ci) {
+        float r = a[0];
+#pragma unroll
+        for (int k = 1; k < kMaxChunks; ++k) r = ci == k ? a[k] : r;
+        return r;
+      };
+      long long* tr = (p.trace && leader && warp == kEpiWarp0 && lane == 0 && it < kTraceTiles)
+                          ? p.trace + (cluster_id * kTraceTiles + it) * kTraceSlots
+                          : nullptr;
+      if (tr) tr[6] = gtime();
       if (!kAccGlobal) {
         mbar_wait(&tint[b], par);
         tc_fence_after();
       }
+      if (tr) tr[7] = gtime();
 
       // init = bias + dequant_element(acc, ...) for 32 tokens of this warp's 32 rows
       auto dequant_chunk = [&](int c, uint32_t (&v)[32]) {
@@ -345,10 +434,9 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = 0u;
         }
-        const int t_l = mb * BN + c + lane;
-        const float sa_l = t_l < p.M ? __ldg(&p.a_scale[t_l]) : 0.f;
-        const float za_l = t_l < p.M ? __ldg(&p.a_zero[t_l]) : 0.f;
-        const float zs_l = __fadd_rn(za_l, __fmul_rn(p.half_range, sa_l));  // runtime.cpp:74
+        const int ci = (c - c_begin) / kChunk;
+        const float sa_l = pick(sa_pre, ci);
+        const float zs_l = pick(zs_pre, ci);
         if (!kAccGlobal && kb_int > 0) tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -415,10 +503,12 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) arrive_leader<CG, MODE>(&tconv[b]);
+        if (lane == 0) arrive_leader<CG>(&tconv[b], leader_rank);
+        if (tr) tr[8] = gtime();
         // pass 2: outlier MMAs have accumulated onto init
         mbar_wait(&tfin[b], par);
         tc_fence_after();
+        if (tr) tr[9] = gtime();
 #pragma unroll 1
         for (int c = c_begin; c < c_end; c += kChunk) {
           uint32_t v[32];
@@ -429,7 +519,8 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) arrive_leader<CG, MODE>(&tempty[b]);
+      if (lane == 0) arrive_leader<CG>(&tempty[b], leader_rank);
+      if (tr) tr[10] = gtime();
     }
     if (lane == 0) bulk_wait_all();
   }
@@ -473,54 +564,106 @@ bool make_map(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int elem
   return r == CUDA_SUCCESS;
 }
 
-template <int CG, int BN, int MODE, bool SP>
+template <int CG, int BN, int MODE, bool SP, bool MC>
 cudaError_t launch_cfg(const KParams& kp, int num_sms, cudaStream_t stream) {
   using C = Cfg<CG, BN, SP>;
-  auto kern = quik_gemm_kernel<CG, BN, MODE, SP>;
+  constexpr int CL = MC ? 4 : CG;
+  auto kern = quik_gemm_kernel<CG, BN, MODE, SP, MC>;
   cudaError_t e = ensure_smem_attr(kern, C::kSmemBytes);
   if (e != cudaSuccess) return e;
-  const long long tiles = static_cast<long long>((kp.M + BN - 1) / BN) * ((kp.N + C::kTileRows - 1) / C::kTileRows);
-  const int max_clusters = num_sms / CG;
-  const int clusters = static_cast<int>(tiles < max_clusters ? tiles : max_clusters);
-  if (clusters <= 0) return cudaSuccess;
+  const long long tn = (kp.N + C::kTileRows - 1) / C::kTileRows;
+  const long long tiles = static_cast<long long>((kp.M + BN - 1) / BN) * (MC ? (tn + 1) / 2 : tn);
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(clusters * CG);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = C::kSmemBytes;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (kernel waits via griddepcontrol)
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
+  // persistent grid: as many clusters as can be co-resident (clusters must fit inside
+  // a GPC, so num_sms / CL over-counts; a second partial wave would double the time)
+  static int resident[2][2] = {{0, 0}, {0, 0}};
+  int& max_clusters = resident[CL == 4][CG == 2];
+  if (max_clusters == 0) {
+    cfg.gridDim = dim3(static_cast<unsigned>(num_sms / CL * CL));
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+      (void)cudaGetLastError();
+      n = num_sms / CL;
+    }
+    max_clusters = n;
+  }
+  const int clusters = static_cast<int>(tiles < max_clusters ? tiles : max_clusters);
+  if (clusters <= 0) return cudaSuccess;
+  cfg.gridDim = dim3(clusters * CL);
   return cudaLaunchKernelEx(&cfg, kern, kp);
 }
 
-template <int CG, int BN>
+template <int CG, int BN, bool MC = false>
 cudaError_t launch_mode(const KParams& kp, int mode, int num_sms, cudaStream_t stream) {
   switch (mode) {
-    case kModeInt32: return launch_cfg<CG, BN, kModeInt32, false>(kp, num_sms, stream);
-    case kModeAccInitF32: return launch_cfg<CG, BN, kModeAccInitF32, false>(kp, num_sms, stream);
-    case kModeAccInitF16: return launch_cfg<CG, BN, kModeAccInitF16, false>(kp, num_sms, stream);
-    case kModeF32: return launch_cfg<CG, BN, kModeF32, false>(kp, num_sms, stream);
-    case kModeProbe: return launch_cfg<CG, BN, kModeProbe, false>(kp, num_sms, stream);
-    default: return launch_cfg<CG, BN, kModeF16, false>(kp, num_sms, stream);
+    case kModeInt32: return launch_cfg<CG, BN, kModeInt32, false, MC>(kp, num_sms, stream);
+    case kModeAccInitF32: return launch_cfg<CG, BN, kModeAccInitF32, false, MC>(kp, num_sms, stream);
+    case kModeAccInitF16: return launch_cfg<CG, BN, kModeAccInitF16, false, MC>(kp, num_sms, stream);
+    case kModeF32: return launch_cfg<CG, BN, kModeF32, false, MC>(kp, num_sms, stream);
+    case kModeProbe: return launch_cfg<CG, BN, kModeProbe, false, MC>(kp, num_sms, stream);
+    default: return launch_cfg<CG, BN, kModeF16, false, MC>(kp, num_sms, stream);
   }
 }
 
 // 2:4 sparse base weights: the fused modes and the raw int32 accumulator (parity)
-template <int CG, int BN>
+template <int CG, int BN, bool MC = false>
 cudaError_t launch_mode_sp(const KParams& kp, int mode, int num_sms, cudaStream_t stream) {
   switch (mode) {
-    case kModeInt32: return launch_cfg<CG, BN, kModeInt32, true>(kp, num_sms, stream);
-    case kModeF32: return launch_cfg<CG, BN, kModeF32, true>(kp, num_sms, stream);
-    case kModeProbe: return launch_cfg<CG, BN, kModeProbe, true>(kp, num_sms, stream);
-    case kModeF16: return launch_cfg<CG, BN, kModeF16, true>(kp, num_sms, stream);
+    case kModeInt32: return launch_cfg<CG, BN, kModeInt32, true, MC>(kp, num_sms, stream);
+    case kModeF32: return launch_cfg<CG, BN, kModeF32, true, MC>(kp, num_sms, stream);
+    case kModeProbe: return launch_cfg<CG, BN, kModeProbe, true, MC>(kp, num_sms, stream);
+    case kModeF16: return launch_cfg<CG, BN, kModeF16, true, MC>(kp, num_sms, stream);
     default: return cudaErrorInvalidValue;  // V1/V2 tails read int32 accumulators: dense kernel
+  }
+}
+
+constexpr int kKeyMC = 1 << 30;  // dispatch key flag: 4-CTA multicast clusters
+
+cudaError_t launch_sp_key(int key, const KParams& kp, int mode, int num_sms, cudaStream_t stream) {
+  if (key & kKeyMC) {
+    switch (key & ~kKeyMC) {
+      case (2 << 16) | 128: return launch_mode_sp<2, 128, true>(kp, mode, num_sms, stream);
+      case (2 << 16) | 192: return launch_mode_sp<2, 192, true>(kp, mode, num_sms, stream);
+      default: return cudaErrorInvalidConfiguration;
+    }
+  }
+  switch (key) {
+    case (1 << 16) | 32: return launch_mode_sp<1, 32>(kp, mode, num_sms, stream);
+    case (1 << 16) | 64: return launch_mode_sp<1, 64>(kp, mode, num_sms, stream);
+    case (1 << 16) | 128: return launch_mode_sp<1, 128>(kp, mode, num_sms, stream);
+    case (2 << 16) | 128: return launch_mode_sp<2, 128>(kp, mode, num_sms, stream);
+    case (2 << 16) | 192: return launch_mode_sp<2, 192>(kp, mode, num_sms, stream);
+    default: return cudaErrorInvalidConfiguration;
+  }
+}
+
+cudaError_t launch_dense_key(int key, const KParams& kp, int mode, int num_sms, cudaStream_t stream) {
+  if (key & kKeyMC) {
+    switch (key & ~kKeyMC) {
+      case (2 << 16) | 128: return launch_mode<2, 128, true>(kp, mode, num_sms, stream);
+      case (2 << 16) | 256: return launch_mode<2, 256, true>(kp, mode, num_sms, stream);
+      default: return cudaErrorInvalidConfiguration;
+    }
+  }
+  switch (key) {
+    case (1 << 16) | 32: return launch_mode<1, 32>(kp, mode, num_sms, stream);
+    case (1 << 16) | 64: return launch_mode<1, 64>(kp, mode, num_sms, stream);
+    case (1 << 16) | 128: return launch_mode<1, 128>(kp, mode, num_sms, stream);
+    case (2 << 16) | 128: return launch_mode<2, 128>(kp, mode, num_sms, stream);
+    case (2 << 16) | 256: return launch_mode<2, 256>(kp, mode, num_sms, stream);
+    default: return cudaErrorInvalidConfiguration;
   }
 }
 
@@ -554,7 +697,15 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
   if (acc_global) kp.kb_int = 0;
   kp.acc_in = a.acc_in;
   kp.ld_acc = a.ld_acc;
-  const uint32_t brows = static_cast<uint32_t>(bn / cg);
+  // QUIK_GEMM_MC=1 enables the 4-CTA multicast clusters. Off by default: measured on
+  // B200 the k-loop is bound by TMA latency x shared-memory ring capacity, not by
+  // L2->SM bandwidth, and fewer 4-CTA clusters fit per GPC (tools/trace_view.py).
+  static const int mc_env = [] {
+    const char* e = getenv("QUIK_GEMM_MC");
+    return e ? atoi(e) : 0;
+  }();
+  const bool mc = cg == 2 && mc_env != 0 && a.mode != kModeAccInitF32 && a.mode != kModeAccInitF16;
+  const uint32_t brows = static_cast<uint32_t>(bn / cg / (mc ? 2 : 1));
   if (kp.kb_int && sp) {
     // compressed weights [N][kpad / 2], activations [M][kpad] (two atoms per stage),
     // metadata planes [(2 * kb + h) * n_pad + row][16 B]
@@ -592,6 +743,19 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
     return e ? atoi(e) : 0;
   }();
   kp.w_policy = w_policy;
+  static const int split_env = [] {  // tuning: QUIK_SPLIT_NUM in 1..7 (eighths of the int k-blocks)
+    const char* e = getenv("QUIK_SPLIT_NUM");
+    return e ? atoi(e) : 0;
+  }();
+  kp.split_num = (split_env >= 1 && split_env <= 7) ? split_env : (sp ? 6 : 4);
+  static const char* trace_path = getenv("QUIK_GEMM_TRACE");  // diagnostics: timeline dump
+  static long long* trace_buf = nullptr;
+  const size_t trace_bytes = static_cast<size_t>(num_sms) * kTraceTiles * kTraceSlots * 8;
+  if (trace_path && (a.mode == kModeF16 || a.mode == kModeF32)) {
+    if (!trace_buf && cudaMalloc(&trace_buf, trace_bytes) != cudaSuccess) trace_buf = nullptr;
+    if (trace_buf) cudaMemsetAsync(trace_buf, 0, trace_bytes, stream);
+    kp.trace = trace_buf;
+  }
   kp.tma_store = 0;
   if ((a.mode == kModeF16 || a.mode == kModeAccInitF16) && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 &&
       (a.ldo * 2) % 16 == 0) {
@@ -611,25 +775,28 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
   kp.half_range = a.half_range;
   kp.out = a.out;
   kp.ldo = a.ldo;
-  const int key = (cg << 16) | bn;
-  if (sp) {
-    switch (key) {
-      case (1 << 16) | 32: return launch_mode_sp<1, 32>(kp, a.mode, num_sms, stream);
-      case (1 << 16) | 64: return launch_mode_sp<1, 64>(kp, a.mode, num_sms, stream);
-      case (1 << 16) | 128: return launch_mode_sp<1, 128>(kp, a.mode, num_sms, stream);
-      case (2 << 16) | 128: return launch_mode_sp<2, 128>(kp, a.mode, num_sms, stream);
-      case (2 << 16) | 192: return launch_mode_sp<2, 192>(kp, a.mode, num_sms, stream);
-      default: *err_msg = "unsupported sparse tile configuration"; return cudaErrorInvalidValue;
+  const int key = ((cg << 16) | bn) | (mc ? kKeyMC : 0);
+  if (kp.trace) {
+    // launch, then dump the timeline of this call (overwrites the file each call)
+    cudaError_t e = sp ? launch_sp_key(key, kp, a.mode, num_sms, stream) : launch_dense_key(key, kp, a.mode, num_sms, stream);
+    if (e != cudaSuccess) return e;
+    std::vector<long long> h(trace_bytes / 8);
+    cudaStreamSynchronize(stream);
+    cudaMemcpy(h.data(), kp.trace, trace_bytes, cudaMemcpyDeviceToHost);
+    if (FILE* f = fopen(trace_path, "wb")) {
+      fwrite(h.data(), 8, h.size(), f);
+      fclose(f);
     }
+    return cudaSuccess;
   }
-  switch (key) {
-    case (1 << 16) | 32: return launch_mode<1, 32>(kp, a.mode, num_sms, stream);
-    case (1 << 16) | 64: return launch_mode<1, 64>(kp, a.mode, num_sms, stream);
-    case (1 << 16) | 128: return launch_mode<1, 128>(kp, a.mode, num_sms, stream);
-    case (2 << 16) | 128: return launch_mode<2, 128>(kp, a.mode, num_sms, stream);
-    case (2 << 16) | 256: return launch_mode<2, 256>(kp, a.mode, num_sms, stream);
-    default: *err_msg = "unsupported tile configuration"; return cudaErrorInvalidValue;
+  if (sp) {
+    const cudaError_t e = launch_sp_key(key, kp, a.mode, num_sms, stream);
+    if (e == cudaErrorInvalidConfiguration) *err_msg = "unsupported sparse tile configuration";
+    return e;
   }
+  const cudaError_t e = launch_dense_key(key, kp, a.mode, num_sms, stream);
+  if (e == cudaErrorInvalidConfiguration) *err_msg = "unsupported tile configuration";
+  return e;
 }
 
 }  // namespace quikb200
