@@ -188,6 +188,15 @@ quik_status quik_rtn_quantize_weights(quik_ctx_t ctx, const float* w, int64_t N,
  * heuristic. */
 quik_status quik_set_gemm_tile(int cta_group, int block_n);
 
+/* Tuning knob (process-wide): 1 runs CTA-pair GEMM tiles in 4-CTA clusters whose two
+ * pairs share (TMA-multicast) the activation tiles; 0 (default) plain CTA pairs. */
+quik_status quik_set_gemm_multicast(int on);
+
+/* Tuning knob (process-wide): 1 streams INT4 weights from HBM and widens them to INT8
+ * in shared memory for the 1-CTA (M <= 128) GEMM tiles of 4-bit layers; 0 (default)
+ * uses the INT8 copy. */
+quik_status quik_set_gemm_w4(int on);
+
 /* Diagnostics (process-wide): when on, the V3 forward runs the fused GEMM
  * without writing the output (mainloop + TMEM drain only). Never for results. */
 quik_status quik_set_probe_mode(int on);

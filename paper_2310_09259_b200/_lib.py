@@ -29,7 +29,8 @@ EXPORTED_SYMBOLS = (
     "quik_dequantize_epilogue", "quik_linear_forward", "quik_linear_forward_strided",
     "quik_linear_forward_launches", "quik_linear_forward_ex", "quik_rtn_quantize_weights",
     "quik_set_gemm_tile", "quik_set_probe_mode", "quik_linear_forward_host",
-    "quik_quantize_activations_gemm", "quik_layer_is_sparse",
+    "quik_quantize_activations_gemm", "quik_layer_is_sparse", "quik_set_gemm_multicast",
+    "quik_set_gemm_w4",
 )
 
 
@@ -99,6 +100,8 @@ def load() -> C.CDLL:
             "quik_linear_forward_host": (i32, [vp, vp, vp, i32, i64, vp, i32, i64, vp]),
             "quik_quantize_activations_gemm": (i32, [vp, vp, vp, i32, i64, vp, vp, vp, vp, vp]),
             "quik_layer_is_sparse": (i32, [vp]),
+            "quik_set_gemm_multicast": (i32, [i32]),
+            "quik_set_gemm_w4": (i32, [i32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)

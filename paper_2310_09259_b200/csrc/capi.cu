@@ -126,6 +126,7 @@ struct quik_layer_s {
   int8_t* w8 = nullptr;      // [out][kpad] (null when sparse)
   int sparse = 0;            // 2:4 sparse GEMM operands below are in use
   int8_t* w_sp = nullptr;    // [out][kpad / 2]
+  uint8_t* w4 = nullptr;     // [out][kpad / 2] INT4 weights (4-bit layers), device nibble layout
   uint8_t* meta = nullptr;   // metadata planes (kernels.h GemmArgs)
   __half* wo16 = nullptr;    // [out][opad]
   float* w_scale = nullptr;  // [out]
@@ -210,6 +211,7 @@ GemmArgs gemm_args(quik_ctx_t ctx, const quik_layer_s* L, int64_t M) {
   g.a_zero = static_cast<const float*>(ctx->zero.p);
   g.half_range = static_cast<float>(1 << (L->bits - 1));
   g.sparse = L->sparse;
+  g.w4 = L->w4;
   g.w_sp = L->w_sp;
   g.meta = L->meta;
   return g;
@@ -256,6 +258,16 @@ quik_status quik_set_gemm_tile(int cta_group, int block_n) {
                   (cta_group == 2 && (block_n == 128 || block_n == 192 || block_n == 256));
   if (!ok) return fail(QUIK_ERR_INVALID_ARGUMENT, "unsupported GEMM tile configuration");
   quikb200::gemm_tile_override = (cta_group << 16) | block_n;
+  return QUIK_OK;
+}
+
+quik_status quik_set_gemm_w4(int on) {
+  quikb200::gemm_w4 = on ? 1 : 0;
+  return QUIK_OK;
+}
+
+quik_status quik_set_gemm_multicast(int on) {
+  quikb200::gemm_multicast = on ? 1 : 0;
   return QUIK_OK;
 }
 
@@ -450,6 +462,11 @@ quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* d, quik_l
         QK_CUDA(cudaMemcpy(tmp, d->base + rb * rbytes, static_cast<size_t>(rows * rbytes), cudaMemcpyDefault));
         check_launch(launch_unpack_to_gemm(static_cast<const uint8_t*>(tmp), rows, kb, d->bits, L->w8, L->kpad, st),
                      "weight unpack");
+        if (d->bits == 4) {
+          // INT4 copy for the weight-streaming (small-M) GEMM tiles
+          QK_CUDA(cudaMalloc(&L->w4, static_cast<size_t>(rows * L->kpad / 2)));
+          check_launch(launch_pack_w4(L->w8, rows, L->kpad, L->w4, st), "int4 weight pack");
+        }
         if (d->sparsity) {
           // 2:4 compression (tcgen05.mma.sp operands); stays dense if not compressible
           const int64_t npad = round_up(rows, kBlockM);
@@ -497,6 +514,7 @@ quik_status quik_layer_destroy(quik_layer_t L) {
   cudaFree(L->w8);
   cudaFree(L->w_sp);
   cudaFree(L->meta);
+  cudaFree(L->w4);
   cudaFree(L->wo16);
   cudaFree(L->w_scale);
   cudaFree(L->wreduced);

@@ -55,30 +55,38 @@ constexpr int kStagingBytes = kEpiWarps * 2 * kStoreBufBytes;  // double-buffere
 constexpr int kMetaSlots = 4;     // TMEM metadata ring (8 columns per stage)
 constexpr int kMetaTileBytes = 4096;
 
-template <int CG, int BN, bool SP = false>
+// W4 (INT4 weights in HBM): the producer TMA-loads the packed 4-bit weight tile
+// (128 rows x 64 B = 128 K, device nibble layout, see capi.cu) into a staging slot of
+// the stage; two transform warps widen it to the int8 128-byte-swizzled A tile in
+// shared memory and signal `ready` to the MMA warp. Halves the weight bytes from HBM.
+constexpr int kA4Bytes = kBlockM * kKBlockBytes / 2;  // 8 KB
+
+template <int CG, int BN, bool SP = false, bool W4 = false>
 struct Cfg {
   static constexpr int kBRows = BN / CG;                  // token rows staged per CTA
   static constexpr int kABytes = kBlockM * kKBlockBytes;  // 16 KB: 128 weight rows per CTA
   static constexpr int kBAtomBytes = kBRows * kKBlockBytes;
   static constexpr int kBBytes = kBAtomBytes * (SP ? 2 : 1);
   static constexpr int kMetaBytes = SP ? kMetaTileBytes : 0;
-  static constexpr int kStageBytes = kABytes + kBBytes + kMetaBytes;
+  static constexpr int kA4Off = kABytes + kBBytes + kMetaBytes;  // W4 staging slot
+  static constexpr int kStageBytes = kABytes + kBBytes + kMetaBytes + (W4 ? kA4Bytes : 0);
   static constexpr int kBudget = 227 * 1024 - 1024 - kStagingBytes - 512;
   static constexpr int kStages = (kBudget / kStageBytes) > 8 ? 8 : (kBudget / kStageBytes);
   static constexpr int kAccCols = 2 * BN;                 // two accumulator buffers
   static constexpr int kMetaCol = kAccCols;               // SP: metadata ring after the accumulators
   static constexpr int kTmemCols = SP ? 512 : (2 * BN < 32 ? 32 : 2 * BN);
   static_assert(!SP || kAccCols + 8 * kMetaSlots <= 512, "TMEM: accumulators + metadata ring");
-  static constexpr int kBarBytes = (2 * kStages + 8) * 8 + 16;
+  static constexpr int kBarBytes = (3 * kStages + 8) * 8 + 16;
   static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kStagingBytes + kBarBytes;
   static constexpr int kTileRows = kBlockM * CG;          // weight rows per (cluster) tile
-  static constexpr int kIntStageBytes = kABytes + kBBytes + kMetaBytes;  // expect-tx per CTA
+  static constexpr int kIntStageBytes = (W4 ? kA4Bytes : kABytes) + kBBytes + kMetaBytes;  // expect-tx per CTA
   static constexpr int kOutStageBytes = kABytes + kBAtomBytes;
 };
 
 struct KParams {
   CUtensorMap tm_w;   // int8 [N][kpad] (SP: compressed [N][kpad / 2]), box {128 B, 128 rows}
   CUtensorMap tm_e;   // SP: metadata [2 * n_kb * n_pad rows][16 B], box {16 B, 128 rows}
+  CUtensorMap tm_w4;  // W4: packed int4 weights [N][kpad / 2], box {64 B, 128 rows}, no swizzle
   CUtensorMap tm_x;   // int8 [M][kpad], box {128 B, BN/CG rows}
   CUtensorMap tm_wo;  // f16 [N][opad], box {64, 128}
   CUtensorMap tm_xo;  // f16 [M][opad], box {64, BN/CG}
@@ -127,10 +135,11 @@ __device__ __forceinline__ void arrive_leader(uint64_t* bar, uint32_t leader_ran
 // half p of its B rows and TMA-multicasts it to (0, r) and (1, r). A stage is
 // refilled only after both pairs' MMAs released it (empty barriers count 2, the
 // MMA commits multicast to all 4 CTAs). Halves the L2->SM traffic of B.
-template <int CG, int BN, int MODE, bool SP, bool MC>
+template <int CG, int BN, int MODE, bool SP, bool MC, bool W4>
 __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_constant__ KParams p) {
-  using C = Cfg<CG, BN, SP>;
+  using C = Cfg<CG, BN, SP, W4>;
   static_assert(!MC || CG == 2, "multicast clusters pair CTA pairs");
+  static_assert(!(W4 && (SP || MC)), "W4 is a dense-weight variant");
   constexpr int CL = MC ? 4 : CG;  // CTAs per cluster
   constexpr bool kAccGlobal = MODE == kModeAccInitF32 || MODE == kModeAccInitF16;
   constexpr bool kF16Out = MODE == kModeF16 || MODE == kModeAccInitF16;
@@ -148,7 +157,8 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
   uint64_t* tconv = tint + 2;           // [2] init written into TMEM          (epilogue -> MMA)
   uint64_t* tfin = tconv + 2;           // [2] outlier MMAs done, tile final   (MMA -> epilogue)
   uint64_t* tempty = tfin + 2;          // [2] accumulator buffer drained      (epilogue -> MMA)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* ready = tempty + 2;         // [kStages] W4: int8 A tile widened     (transform -> MMA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ready + C::kStages);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -169,6 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
   if (warp == 0 && lane == 0) {
     if (kb_int) { tma_prefetch(&p.tm_w); tma_prefetch(&p.tm_x); }
     if (SP && kb_int) tma_prefetch(&p.tm_e);
+    if (W4 && kb_int) tma_prefetch(&p.tm_w4);
     if (kb_out) { tma_prefetch(&p.tm_wo); tma_prefetch(&p.tm_xo); }
   }
   if (warp == 1 && lane == 0) {
@@ -179,6 +190,8 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
       mbar_init(&tfin[i], 1);
       mbar_init(&tempty[i], kEpiWarps * CG);
     }
+    if (W4)
+      for (int i = 0; i < C::kStages; ++i) mbar_init(&ready[i], 2);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<CG>(tmem_slot, C::kTmemCols);
@@ -236,7 +249,14 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
       };
       // integer block kb: dense = load(); SP = compressed A + two B atoms + metadata tile
       auto load_int = [&](int kb, int wrow, int trow) {
-        if constexpr (!SP) {
+        if constexpr (W4) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::kStageBytes;
+          if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::kIntStageBytes);
+          tma(sa + C::kA4Off, &p.tm_w4, kb * (kKBlockBytes / 2), wrow, pol_w);
+          tma_b(sa + C::kABytes, &p.tm_x, kb * kKBlockBytes, trow, pol_x);
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        } else if constexpr (!SP) {
           load(&p.tm_w, &p.tm_x, kb * kKBlockBytes, wrow, trow);
         } else {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -286,13 +306,14 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
       int stage = 0;
       uint32_t phase = 0;
       long long full_wait = 0;
-      auto next_stage = [&](uint64_t& adesc, uint64_t& bdesc) {
+      auto next_stage = [&](uint64_t& adesc, uint64_t& bdesc, bool widened = false) {
+        uint64_t* bar = widened ? &ready[stage] : &full[stage];
         if (p.trace) {
           const long long t0 = gtime();
-          mbar_wait(&full[stage], phase);
+          mbar_wait(bar, phase);
           full_wait += gtime() - t0;
         } else {
-          mbar_wait(&full[stage], phase);
+          mbar_wait(bar, phase);
         }
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
@@ -307,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
       auto int_blocks = [&](uint32_t d, int k0, int k1) {
         for (int kb = k0; kb < k1; ++kb) {
           uint64_t ad, bd;
-          next_stage(ad, bd);
+          next_stage(ad, bd, W4);
           if constexpr (!SP) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)  // 4 x K=32 int8 = 128 bytes
@@ -361,6 +382,67 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
         if (tr) { tr[4] = gtime(); tr[5] = full_wait; }
       }
       if (two_phase && it > 0) out_blocks(it - 1);
+    }
+  } else if (W4 && (warp == 2 || warp == 3)) {
+    // INT4 -> INT8 widening of the weight tiles, stage by stage in the producer's order
+    // (int blocks [0, h_a) | outlier blocks of the previous tile | [h_a, kb_int)).
+    // Input slot: [128 rows][64 B]; byte i of 16-byte chunk c holds k = 32c + i in its
+    // low nibble and k = 32c + 16 + i in its high nibble (signed 4-bit). Output: the
+    // int8 A tile, row r, 16-byte chunk j at physical chunk j ^ (r & 7) (SWIZZLE_128B).
+    const int t64 = (warp - 2) * 32 + lane;
+    int stage = 0;
+    uint32_t phase = 0;
+    // outlier stages are not widened, but `ready` must still complete one phase per
+    // use of the stage so its parity stays in step with the ring (the MMA warp waits on
+    // it with the ring phase). Waiting for the stage's data first keeps the transform
+    // behind the producer, i.e. at most one ring wrap ahead of the MMA warp.
+    auto skip = [&](int n) {
+      for (int i = 0; i < n; ++i) {
+        mbar_wait(&full[stage], phase);
+        if (lane == 0) mbar_arrive(&ready[stage]);
+        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+      }
+    };
+    auto widen = [&](int n) {
+      for (int i = 0; i < n; ++i) {
+        mbar_wait(&full[stage], phase);
+        uint8_t* sa = smem + stage * C::kStageBytes;
+        const uint8_t* s4 = sa + C::kA4Off;
+        // all 8 input chunks first (independent loads in flight), then widen + store
+        uint4 win[8];
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int item = t64 + it * 64;  // 512 = 128 rows x 4 input chunks
+          win[it] = *reinterpret_cast<const uint4*>(s4 + (item >> 2) * 64 + (item & 3) * 16);
+        }
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int item = t64 + it * 64;
+          const int r = item >> 2, c = item & 3;
+          const uint4 w = win[it];
+          uint32_t lo[4], hi[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t v = (&w.x)[k];
+            const uint32_t l = v & 0x0F0F0F0Fu, h = (v >> 4) & 0x0F0F0F0Fu;
+            lo[k] = l + (l & 0x08080808u) * 0x1Eu;  // sign-extend each 4-bit value to 8 bits
+            hi[k] = h + (h & 0x08080808u) * 0x1Eu;
+          }
+          uint8_t* row = sa + r * kKBlockBytes;
+          *reinterpret_cast<uint4*>(row + (((2 * c) ^ (r & 7)) << 4)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+          *reinterpret_cast<uint4*>(row + (((2 * c + 1) ^ (r & 7)) << 4)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        }
+        fence_proxy_async_smem();  // generic writes -> tensor-core (async proxy) reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ready[stage]);
+        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+      }
+    };
+    int it = 0;
+    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
+      widen(h_a);
+      if (two_phase && it > 0) skip(kb_out);
+      widen(kb_int - h_a);
     }
   } else if (warp >= kEpiWarp0) {
     const int e = warp - kEpiWarp0;
@@ -564,11 +646,11 @@ bool make_map(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int elem
   return r == CUDA_SUCCESS;
 }
 
-template <int CG, int BN, int MODE, bool SP, bool MC>
+template <int CG, int BN, int MODE, bool SP, bool MC, bool W4 = false>
 cudaError_t launch_cfg(const KParams& kp, int num_sms, cudaStream_t stream) {
-  using C = Cfg<CG, BN, SP>;
+  using C = Cfg<CG, BN, SP, W4>;
   constexpr int CL = MC ? 4 : CG;
-  auto kern = quik_gemm_kernel<CG, BN, MODE, SP, MC>;
+  auto kern = quik_gemm_kernel<CG, BN, MODE, SP, MC, W4>;
   cudaError_t e = ensure_smem_attr(kern, C::kSmemBytes);
   if (e != cudaSuccess) return e;
   const long long tn = (kp.N + C::kTileRows - 1) / C::kTileRows;
@@ -617,6 +699,18 @@ cudaError_t launch_mode(const KParams& kp, int mode, int num_sms, cudaStream_t s
   }
 }
 
+// INT4 weights widened in shared memory (1-CTA tiles: the memory-bound small-M regime)
+template <int BN>
+cudaError_t launch_mode_w4(const KParams& kp, int mode, int num_sms, cudaStream_t stream) {
+  switch (mode) {
+    case kModeInt32: return launch_cfg<1, BN, kModeInt32, false, false, true>(kp, num_sms, stream);
+    case kModeF32: return launch_cfg<1, BN, kModeF32, false, false, true>(kp, num_sms, stream);
+    case kModeProbe: return launch_cfg<1, BN, kModeProbe, false, false, true>(kp, num_sms, stream);
+    case kModeF16: return launch_cfg<1, BN, kModeF16, false, false, true>(kp, num_sms, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 // 2:4 sparse base weights: the fused modes and the raw int32 accumulator (parity)
 template <int CG, int BN, bool MC = false>
 cudaError_t launch_mode_sp(const KParams& kp, int mode, int num_sms, cudaStream_t stream) {
@@ -630,6 +724,7 @@ cudaError_t launch_mode_sp(const KParams& kp, int mode, int num_sms, cudaStream_
 }
 
 constexpr int kKeyMC = 1 << 30;  // dispatch key flag: 4-CTA multicast clusters
+constexpr int kKeyW4 = 1 << 29;  // dispatch key flag: INT4 weights widened in shared memory
 
 cudaError_t launch_sp_key(int key, const KParams& kp, int mode, int num_sms, cudaStream_t stream) {
   if (key & kKeyMC) {
@@ -650,6 +745,14 @@ cudaError_t launch_sp_key(int key, const KParams& kp, int mode, int num_sms, cud
 }
 
 cudaError_t launch_dense_key(int key, const KParams& kp, int mode, int num_sms, cudaStream_t stream) {
+  if (key & kKeyW4) {
+    switch (key & ~kKeyW4) {
+      case (1 << 16) | 32: return launch_mode_w4<32>(kp, mode, num_sms, stream);
+      case (1 << 16) | 64: return launch_mode_w4<64>(kp, mode, num_sms, stream);
+      case (1 << 16) | 128: return launch_mode_w4<128>(kp, mode, num_sms, stream);
+      default: return cudaErrorInvalidConfiguration;
+    }
+  }
   if (key & kKeyMC) {
     switch (key & ~kKeyMC) {
       case (2 << 16) | 128: return launch_mode<2, 128, true>(kp, mode, num_sms, stream);
@@ -669,7 +772,12 @@ cudaError_t launch_dense_key(int key, const KParams& kp, int mode, int num_sms, 
 
 }  // namespace
 
-int gemm_tile_override = 0;  // debug/tuning: 0 = heuristic, else (CG << 16) | BN
+int gemm_tile_override = 0;
+int gemm_multicast = 0;  // 1: 4-CTA multicast clusters for CTA-pair tiles (quik_set_gemm_multicast)
+// 1: INT4-weight 1-CTA tiles when the layer has INT4 weights (quik_set_gemm_w4). Off by
+// default: with the widened tile inside each ring stage the ring holds 6 instead of 8
+// stages and the weight stream is latency-bound (92 vs 60 us at OPT-66B fc1, M = 16).
+int gemm_w4 = 0;  // debug/tuning: 0 = heuristic, else (CG << 16) | BN
 
 cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream, const char** err_msg) {
   *err_msg = nullptr;
@@ -704,7 +812,10 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
     const char* e = getenv("QUIK_GEMM_MC");
     return e ? atoi(e) : 0;
   }();
-  const bool mc = cg == 2 && mc_env != 0 && a.mode != kModeAccInitF32 && a.mode != kModeAccInitF16;
+  // INT4 weights from HBM for the 1-CTA (weight-streaming, M <= 128) tiles
+  const bool w4 = cg == 1 && a.w4 != nullptr && !sp && a.mode != kModeAccInitF32 && a.mode != kModeAccInitF16 &&
+                  gemm_w4 != 0;
+  const bool mc = cg == 2 && (mc_env != 0 || gemm_multicast != 0) && a.mode != kModeAccInitF32 && a.mode != kModeAccInitF16;
   const uint32_t brows = static_cast<uint32_t>(bn / cg / (mc ? 2 : 1));
   if (kp.kb_int && sp) {
     // compressed weights [N][kpad / 2], activations [M][kpad] (two atoms per stage),
@@ -722,6 +833,18 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
       *err_msg = "tensor map encode failed (sparse operands)";
+      return cudaErrorInvalidValue;
+    }
+  } else if (kp.kb_int && w4) {
+    cuuint64_t wdims[2] = {static_cast<cuuint64_t>(a.kpad / 2), static_cast<cuuint64_t>(a.N)};
+    cuuint64_t wstr[1] = {static_cast<cuuint64_t>(a.kpad / 2)};
+    cuuint32_t wbox[2] = {static_cast<cuuint32_t>(kKBlockBytes / 2), static_cast<cuuint32_t>(kBlockM)};
+    cuuint32_t wel[2] = {1, 1};
+    if (g_encode(&kp.tm_w4, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(a.w4), wdims, wstr, wbox, wel,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+        !make_map(&kp.tm_x, a.x, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, a.kpad, a.M, a.kpad, brows)) {
+      *err_msg = "tensor map encode failed (int4 operands)";
       return cudaErrorInvalidValue;
     }
   } else if (kp.kb_int) {
@@ -775,7 +898,7 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
   kp.half_range = a.half_range;
   kp.out = a.out;
   kp.ldo = a.ldo;
-  const int key = ((cg << 16) | bn) | (mc ? kKeyMC : 0);
+  const int key = ((cg << 16) | bn) | (mc ? kKeyMC : 0) | (w4 ? kKeyW4 : 0);
   if (kp.trace) {
     // launch, then dump the timeline of this call (overwrites the file each call)
     cudaError_t e = sp ? launch_sp_key(key, kp, a.mode, num_sms, stream) : launch_dense_key(key, kp, a.mode, num_sms, stream);

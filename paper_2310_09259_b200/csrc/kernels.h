@@ -66,7 +66,13 @@ struct GemmArgs {
   int sparse;
   const int8_t* w_sp;
   const uint8_t* meta;
+  // INT4 weights in the device nibble layout [N][kpad / 2] (or null): per 16-byte chunk
+  // c of a row, byte i = (k = 32c + i) | (k = 32c + 16 + i) << 4, signed 4-bit values.
+  const uint8_t* w4;
 };
+
+// GEMM-layout int8 weights [N][kpad] (values in [-8, 7]) -> device INT4 layout above.
+cudaError_t launch_pack_w4(const int8_t* w8, int64_t N, int64_t kpad, uint8_t* w4, cudaStream_t stream);
 
 // Compresses dense int8 GEMM-layout weights [N][kpad] (kpad % 256 == 0) into the
 // 2:4 sparse operands above. *bad is set to 1 if a group of 4 has more than two
@@ -78,6 +84,8 @@ cudaError_t launch_compress_24(const int8_t* w8, int64_t N, int64_t kpad, int8_t
 // dequantisation epilogue). Returns a cudaError_t / CUresult-derived status in
 // *err_msg on failure.
 extern int gemm_tile_override;  // (cta_group << 16) | block_n, 0 = heuristic
+extern int gemm_multicast;      // 1: 4-CTA TMA-multicast clusters for CTA-pair tiles
+extern int gemm_w4;             // 1: INT4-weight (widened in smem) 1-CTA tiles when available
 cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream, const char** err_msg);
 
 // K1: fused split + per-token asymmetric quantisation (runtime.cpp:36-66,

@@ -917,6 +917,23 @@ __global__ void compress24_kernel(const int8_t* __restrict__ w8, int64_t N, int6
   *reinterpret_cast<uint32_t*>(meta + ((2 * kb + h) * npad + n) * 16 + (gl % 32) / 2) = nib;
 }
 
+// INT4 weight repack for the W4 GEMM tiles: thread = one 16-byte output chunk.
+__global__ void pack_w4_kernel(const int8_t* __restrict__ w8, int64_t N, int64_t kpad, uint8_t* __restrict__ w4) {
+  const int64_t per_row = kpad / 32;
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= N * per_row) return;
+  const int64_t n = idx / per_row, c = idx % per_row;
+  const uint4* src = reinterpret_cast<const uint4*>(w8 + n * kpad + 32 * c);
+  const uint4 lo = src[0], hi = src[1];
+  uint32_t out[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t a = (&lo.x)[k] & 0x0F0F0F0Fu, b = (&hi.x)[k] & 0x0F0F0F0Fu;
+    out[k] = a | (b << 4);
+  }
+  *reinterpret_cast<uint4*>(w4 + n * (kpad / 2) + 16 * c) = make_uint4(out[0], out[1], out[2], out[3]);
+}
+
 dim3 grid2(int64_t cols, int64_t rows) {
   int64_t gx = (cols + 255) / 256;
   if (gx > 64) gx = 64;
@@ -1041,6 +1058,13 @@ cudaError_t launch_compress_24(const int8_t* w8, int64_t N, int64_t kpad, int8_t
   if (e != cudaSuccess) return e;
   const int64_t work = N * (kpad / 32);
   compress24_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, stream>>>(w8, N, kpad, w_sp, meta, npad, bad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_w4(const int8_t* w8, int64_t N, int64_t kpad, uint8_t* w4, cudaStream_t stream) {
+  if (N == 0 || kpad == 0) return cudaSuccess;
+  const int64_t work = N * (kpad / 32);
+  pack_w4_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, stream>>>(w8, N, kpad, w4);
   return cudaGetLastError();
 }
 

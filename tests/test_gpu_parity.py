@@ -372,13 +372,23 @@ def test_non_finite_input_flags_numerical_error():
 # --------------------------------------------------------------------------- every tile configuration
 
 
-@pytest.fixture
-def tile():
+@pytest.fixture(params=[0, 1], ids=["default", "alt"])
+def tile(request):
+    """Forces a GEMM tile. "alt": CTA-pair tiles run as 4-CTA TMA-multicast clusters,
+    1-CTA tiles stream INT4 weights and widen them in shared memory (W4)."""
     import paper_2310_09259_b200 as m
 
     lib = m.load_library()
-    yield lambda cg, bn: lib.quik_set_gemm_tile(cg, bn)
+
+    def force(cg, bn):
+        lib.quik_set_gemm_multicast(1 if (request.param and cg == 2) else 0)
+        lib.quik_set_gemm_w4(1 if (request.param and cg == 1) else 0)
+        return lib.quik_set_gemm_tile(cg, bn)
+
+    yield force
     lib.quik_set_gemm_tile(0, 0)
+    lib.quik_set_gemm_multicast(0)
+    lib.quik_set_gemm_w4(0)
 
 
 @pytest.mark.parametrize("cg,bn", [(1, 32), (1, 64), (1, 128), (2, 128), (2, 256)])
