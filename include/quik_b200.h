@@ -197,6 +197,12 @@ quik_status quik_set_gemm_multicast(int on);
  * uses the INT8 copy. */
 quik_status quik_set_gemm_w4(int on);
 
+/* Tuning knob (process-wide): on (default off) V3 forwards with M <= 64 tokens run the
+ * split-K weight-streaming GEMM (int32 workspace) + the fused dequant/outlier
+ * epilogue (bit-identical results); int4 (default 1) streams the INT4 weights of
+ * 4-bit layers. */
+quik_status quik_set_stream_gemm(int on, int int4);
+
 /* Diagnostics (process-wide): when on, the V3 forward runs the fused GEMM
  * without writing the output (mainloop + TMEM drain only). Never for results. */
 quik_status quik_set_probe_mode(int on);

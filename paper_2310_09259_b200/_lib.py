@@ -30,7 +30,7 @@ EXPORTED_SYMBOLS = (
     "quik_linear_forward_launches", "quik_linear_forward_ex", "quik_rtn_quantize_weights",
     "quik_set_gemm_tile", "quik_set_probe_mode", "quik_linear_forward_host",
     "quik_quantize_activations_gemm", "quik_layer_is_sparse", "quik_set_gemm_multicast",
-    "quik_set_gemm_w4",
+    "quik_set_gemm_w4", "quik_set_stream_gemm",
 )
 
 
@@ -102,6 +102,7 @@ def load() -> C.CDLL:
             "quik_layer_is_sparse": (i32, [vp]),
             "quik_set_gemm_multicast": (i32, [i32]),
             "quik_set_gemm_w4": (i32, [i32]),
+            "quik_set_stream_gemm": (i32, [i32, i32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)

@@ -106,6 +106,15 @@ struct quik_ctx_s {
   cudaEvent_t ev_start = nullptr, ev_done = nullptr;
   cudaEvent_t ev_in[kMaxHostChunks] = {}, ev_out[kMaxHostChunks] = {};
   DevBuf xdev, ydev;
+  // split-K workspace of the weight-streaming path: int32 [M][N], kept all-zero
+  // between calls (the AccInit epilogue clears what it reads)
+  DevBuf ws;
+  int32_t* ensure_ws(size_t bytes, cudaStream_t st) {
+    const size_t before = ws.cap;
+    void* p = ws.ensure(bytes);
+    if (ws.cap != before) QK_CUDA(cudaMemsetAsync(p, 0, ws.cap, st));
+    return static_cast<int32_t*>(p);
+  }
   void ensure_pipeline() {
     if (s_in) return;
     QK_CUDA(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
@@ -266,6 +275,12 @@ quik_status quik_set_gemm_w4(int on) {
   return QUIK_OK;
 }
 
+quik_status quik_set_stream_gemm(int on, int int4) {
+  quikb200::gemm_stream = on ? 1 : 0;
+  quikb200::gemm_w4_stream = int4 ? 1 : 0;
+  return QUIK_OK;
+}
+
 quik_status quik_set_gemm_multicast(int on) {
   quikb200::gemm_multicast = on ? 1 : 0;
   return QUIK_OK;
@@ -307,7 +322,7 @@ quik_status quik_ctx_destroy(quik_ctx_t ctx) {
   DeviceGuard g(ctx->device);
   cudaDeviceSynchronize();
   for (DevBuf* b : {&ctx->q8, &ctx->scale, &ctx->zero, &ctx->xo16, &ctx->acc, &ctx->fp, &ctx->xbase, &ctx->xo32,
-                    &ctx->wtmp, &ctx->xdev, &ctx->ydev})
+                    &ctx->wtmp, &ctx->xdev, &ctx->ydev, &ctx->ws})
     b->release();
   if (ctx->s_in) {
     cudaStreamDestroy(ctx->s_in);
@@ -696,6 +711,33 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
                          quik_dtype ydt, int64_t ldy, quik_variant variant, cudaStream_t st, void* mid_event) {
   if (M == 0 || L->out_features == 0) return QUIK_OK;
   const int64_t N = L->out_features;
+  if (variant == QUIK_V3_FUSED_EPILOGUE && M <= 64 && L->kpad && !L->sparse && quikb200::gemm_stream && !g_probe_mode) {
+    // weight-streaming regime: K1 -> split-K stream GEMM into the zeroed int32
+    // workspace -> the fused kernel's AccInit mode (dequant + outlier MMAs + store,
+    // clears the workspace); same arithmetic as the fused V3 kernel
+    run_k1(ctx, L, x, xdt, M, st);
+    if (mid_event) QK_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(mid_event), st));
+    int32_t* ws = ctx->ensure_ws(static_cast<size_t>(M * N * 4), st);
+    StreamArgs sa{};
+    sa.w8 = L->w8;
+    sa.w4 = quikb200::gemm_w4_stream ? L->w4 : nullptr;
+    sa.x = static_cast<const int8_t*>(ctx->q8.p);
+    sa.kpad = L->kpad;
+    sa.M = M;
+    sa.N = N;
+    sa.acc = ws;
+    const char* msg = nullptr;
+    check_launch(launch_stream_gemm(sa, ctx->num_sms, st, &msg), "stream gemm kernel", msg);
+    GemmArgs go = gemm_args(ctx, L, M);
+    go.acc_in = ws;
+    go.acc_clear = ws;
+    go.ld_acc = N;
+    go.out = y;
+    go.ldo = ldy;
+    go.mode = ydt == QUIK_F16 ? kModeAccInitF16 : kModeAccInitF32;
+    run_gemm(ctx, go, st);
+    return QUIK_OK;
+  }
   if (variant == QUIK_V3_FUSED_EPILOGUE) {
     run_k1(ctx, L, x, xdt, M, st);
     if (mid_event) QK_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(mid_event), st));

@@ -105,6 +105,7 @@ struct KParams {
   long long ldo;
   const int32_t* acc_in;
   long long ld_acc;
+  int32_t* acc_clear;
   int meta_rows;  // SP: n_pad = round_up(N, 128) rows per metadata (stage, half) plane
   int split_num;  // h_a = kb_int * split_num / 8
   // diagnostics (QUIK_GEMM_TRACE): per leader CTA and tile iteration (< kTraceTiles),
@@ -504,11 +505,19 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
       // init = bias + dequant_element(acc, ...) for 32 tokens of this warp's 32 rows
       auto dequant_chunk = [&](int c, uint32_t (&v)[32]) {
         if (kAccGlobal) {
+          // all 32 loads in flight first, then the clears (acc_clear aliases acc_in)
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int t = mb * BN + c + j;
-            v[j] = (t < p.M && n_ok) ? static_cast<uint32_t>(__ldg(&p.acc_in[static_cast<long long>(t) * p.ld_acc + n]))
+            v[j] = (t < p.M && n_ok) ? static_cast<uint32_t>(__ldcg(&p.acc_in[static_cast<long long>(t) * p.ld_acc + n]))
                                      : 0u;
+          }
+          if (p.acc_clear) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int t = mb * BN + c + j;
+              if (t < p.M && n_ok) p.acc_clear[static_cast<long long>(t) * p.ld_acc + n] = 0;  // workspace -> zeros
+            }
           }
         } else if (kb_int > 0) {
           tmem_ld32(tacc + c, v);
@@ -631,6 +640,22 @@ bool get_encoder() {
   });
   return g_encode != nullptr;
 }
+
+}  // namespace
+
+CUresult encode_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t pitch,
+                       uint32_t box_inner, uint32_t box_rows, bool swizzle128) {
+  if (!get_encoder()) return CUDA_ERROR_NOT_SUPPORTED;
+  cuuint64_t dims[2] = {inner, rows};
+  cuuint64_t strides[1] = {pitch};
+  cuuint32_t box[2] = {box_inner, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
+namespace {
 
 // 2D K-major tile map with 128-byte swizzle. inner = elements per row (logical
 // extent), pitch in bytes, box = {box_inner elements (128 B), box_rows}.
@@ -805,6 +830,7 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
   if (acc_global) kp.kb_int = 0;
   kp.acc_in = a.acc_in;
   kp.ld_acc = a.ld_acc;
+  kp.acc_clear = a.acc_clear;
   // QUIK_GEMM_MC=1 enables the 4-CTA multicast clusters. Off by default: measured on
   // B200 the k-loop is bound by TMA latency x shared-memory ring capacity, not by
   // L2->SM bandwidth, and fewer 4-CTA clusters fit per GPC (tools/trace_view.py).
@@ -874,7 +900,7 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
   static const char* trace_path = getenv("QUIK_GEMM_TRACE");  // diagnostics: timeline dump
   static long long* trace_buf = nullptr;
   const size_t trace_bytes = static_cast<size_t>(num_sms) * kTraceTiles * kTraceSlots * 8;
-  if (trace_path && (a.mode == kModeF16 || a.mode == kModeF32)) {
+  if (trace_path && a.mode != kModeInt32 && a.mode != kModeProbe) {
     if (!trace_buf && cudaMalloc(&trace_buf, trace_bytes) != cudaSuccess) trace_buf = nullptr;
     if (trace_buf) cudaMemsetAsync(trace_buf, 0, trace_bytes, stream);
     kp.trace = trace_buf;

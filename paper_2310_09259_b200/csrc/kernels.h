@@ -59,6 +59,7 @@ struct GemmArgs {
   int mode;
   const int32_t* acc_in; // kModeAccInit*: int32 accumulators [M][ld_acc]
   int64_t ld_acc;
+  int32_t* acc_clear;    // kModeAccInit*: if non-null (== acc_in), zeroed after reading
   // 2:4 sparse base weights (sparse != 0; kpad multiple of 256): compressed values
   // [N][kpad / 2] (two kept codes per group of 4, ascending position) and metadata
   // planes [(2 * kb + h) * round_up(N, 128) + n][16 B] for stage kb (256 logical K),
@@ -70,6 +71,23 @@ struct GemmArgs {
   // c of a row, byte i = (k = 32c + i) | (k = 32c + 16 + i) << 4, signed 4-bit values.
   const uint8_t* w4;
 };
+
+// Weight-streaming split-K integer GEMM for M <= 64 (stream.cu): adds
+// sum_k W[n][k] * X8[t][k] into the int32 workspace acc[t][n] (which must hold
+// zeros or a partial sum). W from w4 (device INT4 layout) if non-null, else w8.
+struct StreamArgs {
+  const int8_t* w8;   // [N][kpad]
+  const uint8_t* w4;  // [N][kpad / 2] or null
+  const int8_t* x;    // [M][kpad]
+  int64_t kpad, M, N;
+  int32_t* acc;       // [M][N]
+  int splits;         // 0 = automatic
+};
+cudaError_t launch_stream_gemm(const StreamArgs& a, int num_sms, cudaStream_t stream, const char** err_msg);
+
+// 2D K-major tensor map (uint8), box {box_inner bytes, box_rows}, 128-byte swizzle or none.
+CUresult encode_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t pitch,
+                       uint32_t box_inner, uint32_t box_rows, bool swizzle128);
 
 // GEMM-layout int8 weights [N][kpad] (values in [-8, 7]) -> device INT4 layout above.
 cudaError_t launch_pack_w4(const int8_t* w8, int64_t N, int64_t kpad, uint8_t* w4, cudaStream_t stream);
@@ -86,6 +104,8 @@ cudaError_t launch_compress_24(const int8_t* w8, int64_t N, int64_t kpad, int8_t
 extern int gemm_tile_override;  // (cta_group << 16) | block_n, 0 = heuristic
 extern int gemm_multicast;      // 1: 4-CTA TMA-multicast clusters for CTA-pair tiles
 extern int gemm_w4;             // 1: INT4-weight (widened in smem) 1-CTA tiles when available
+extern int gemm_stream;         // 1: M <= 64 forwards use the split-K weight-streaming GEMM
+extern int gemm_w4_stream;      // 1: ... streaming the INT4 weights (4-bit layers)
 cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream, const char** err_msg);
 
 // K1: fused split + per-token asymmetric quantisation (runtime.cpp:36-66,
