@@ -639,40 +639,47 @@ __global__ void __launch_bounds__(512) quantize_hot_kernel(const QuantArgs a, in
       a.scale[t] = scale;
       a.zero[t] = vmin;
     }
-    const unsigned long long rcp2 = f32x2_pack(rcp, rcp);
+    // Bracketed rounding (exact): with rcp = fl(1/scale), the reference quotient
+    // fl(d / scale) lies strictly inside (d * rcp_lo, d * rcp_hi) for d > 0, since
+    // |fl(d/scale) - d*rcp| <= 2 * 2^-24 * d*rcp < 2^-20 * d*rcp. One FMA each
+    // rounds d*rcp_x + (1.5 * 2^23 - hr) to an integer (ties-to-even); if both land on
+    // the same integer R, no half-integer lies strictly between the brackets, so
+    // lround(fl(d/scale)) - hr = R - 1.5 * 2^23 exactly and the low byte of the FMA
+    // result is the stored code. Otherwise (within ~2^-20 * q of a tie, incl. exact
+    // ties) the element takes the IEEE quotient. 2 FFMA2 + 1 LOP3 per pair.
+    const float rcp_lo = __fmul_rd(rcp, 1.0f - 0x1p-20f), rcp_hi = __fmul_ru(rcp, 1.0f + 0x1p-20f);
+    const unsigned long long rlo2 = f32x2_pack(rcp_lo, rcp_lo), rhi2 = f32x2_pack(rcp_hi, rcp_hi);
     constexpr float kMagic = 12582912.0f - static_cast<float>(kHr);  // 1.5 * 2^23 - half_range
     const unsigned long long magic2 = f32x2_pack(kMagic, kMagic);
 
-    // ---- pass 2: codes for every column (exactness argument: quantize_rows_kernel)
+    // ---- pass 2: codes for every column
     uint32_t near_vec = 0;
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       const int v = tid + i * nt;
       if (v >= nvec) continue;
       uint32_t tb[8];
-      float rmax = 0.0f;
+      uint32_t diff = 0;
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
         const uint32_t xw = (&raw[i].x)[w];
         const unsigned long long d2 = f32x2_pack(sub_f16_f32(xw & 0xFFFFu, vmin), sub_f16_f32(xw >> 16, vmin));
-        unsigned long long qa2, t2, rq2, r2;
-        asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(qa2) : "l"(d2), "l"(rcp2));
-        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t2) : "l"(qa2), "l"(magic2));
-        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(rq2) : "l"(t2), "l"(magic2));
-        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r2) : "l"(qa2), "l"(rq2));
-        float r0, r1;
-        f32x2_unpack(r2, r0, r1);
-        rmax = fmaxf(rmax, fmaxf(fabsf(r0), fabsf(r1)));
-        tb[2 * w] = static_cast<uint32_t>(t2);
-        tb[2 * w + 1] = static_cast<uint32_t>(t2 >> 32);
+        unsigned long long tl2, th2;
+        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(tl2) : "l"(d2), "l"(rlo2), "l"(magic2));
+        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(th2) : "l"(d2), "l"(rhi2), "l"(magic2));
+        const uint32_t l0 = static_cast<uint32_t>(tl2), l1 = static_cast<uint32_t>(tl2 >> 32);
+        diff |= (l0 ^ static_cast<uint32_t>(th2)) | (l1 ^ static_cast<uint32_t>(th2 >> 32));
+        tb[2 * w] = l0;
+        tb[2 * w + 1] = l1;
       }
-      near_vec |= (!(rmax < kNearTie) ? 1u : 0u) << i;
+      near_vec |= (diff != 0u ? 1u : 0u) << i;
       const uint32_t w0 = __byte_perm(__byte_perm(tb[0], tb[1], 0x0040), __byte_perm(tb[2], tb[3], 0x0040), 0x5410);
       const uint32_t w1 = __byte_perm(__byte_perm(tb[4], tb[5], 0x0040), __byte_perm(tb[6], tb[7], 0x0040), 0x5410);
       *reinterpret_cast<uint2*>(s_codes + v * 8) = make_uint2(w0, w1);
     }
     if (near_vec) {
-      // rare: elements within 2^-12 of a rounding boundary take the exact IEEE quotient
+      // rare: elements whose brackets straddle a rounding boundary take the exact
+      // IEEE quotient, rounded half away from zero (runtime.cpp:58)
       const __half* row = reinterpret_cast<const __half*>(srow);
 #pragma unroll 1
       for (uint32_t nv = near_vec; nv; nv &= nv - 1) {
@@ -681,9 +688,7 @@ __global__ void __launch_bounds__(512) quantize_hot_kernel(const QuantArgs a, in
         for (int e = 0; e < 8; ++e) {
           const int c = v * 8 + e;
           const float d = __fsub_rn(__half2float(row[c]), vmin);
-          const float qa = __fmul_rn(d, rcp);
-          const float r = __fsub_rn(qa, __fsub_rn(__fadd_rn(qa, kMagic), kMagic));
-          if (!(fabsf(r) < kNearTie))
+          if (__float_as_uint(__fmaf_rn(d, rcp_lo, kMagic)) != __float_as_uint(__fmaf_rn(d, rcp_hi, kMagic)))
             s_codes[c] = static_cast<uint8_t>(static_cast<int>(quant_slow(d, scale)) - kHr);
         }
       }
