@@ -37,7 +37,8 @@ typedef enum quik_status {
   QUIK_ERR_NUMERICAL = 3,        /* reference: quik::NumericalError (non-finite activations) */
   QUIK_ERR_CUDA = 4,             /* CUDA runtime / driver failure, or no sm_100 device */
   QUIK_ERR_NCCL = 5,             /* reserved: collective failure */
-  QUIK_ERR_UNSUPPORTED = 6
+  QUIK_ERR_UNSUPPORTED = 6,
+  QUIK_ERR_FORMAT = 7            /* reference: quik::FormatError (layer bundle I/O) */
 } quik_status;
 
 /* Element types of activation / output buffers. */
@@ -106,6 +107,27 @@ quik_status quik_layer_info(quik_layer_t layer, int64_t* in_features, int64_t* o
                             int64_t* n_outlier, int* bits);
 /* 1 if the layer runs the 2:4 sparse GEMM (sparsity requested and compressible). */
 int quik_layer_is_sparse(quik_layer_t layer);
+
+/*
+ * Layer bundles: the reference's on-disk layer format
+ * (<dir>/manifest.json + blob files; container.cpp, layer_io.cpp), read on the host
+ * with every check of TensorContainer::read (container.cpp:167-226) and load_layer
+ * (layer_io.cpp:32-74); failures return QUIK_ERR_FORMAT (quik::FormatError).
+ * quik_bundle_weights fills a descriptor with host pointers into the bundle
+ * (valid until quik_bundle_close; sparsity = 1 when a sparsity_mask is present),
+ * ready for quik_layer_create (set row_begin / row_end for a shard).
+ * quik_bundle_tensor exposes any tensor: dtype 0 = f32, 1 = i8, 2 = i4p; shape[<= 4].
+ */
+typedef struct quik_bundle_s* quik_bundle_t;
+quik_status quik_bundle_open(const char* dir, quik_bundle_t* out);
+quik_status quik_bundle_weights(quik_bundle_t bundle, quik_weights_desc* desc);
+quik_status quik_bundle_tensor(quik_bundle_t bundle, const char* name, const void** data, int* dtype,
+                               int64_t* shape, int* ndim);
+quik_status quik_bundle_close(quik_bundle_t bundle);
+/* open + quik_layer_create (shard [row_begin, row_end), 0/0 = all rows) + close:
+ * bundle -> device GEMM layout in one call. */
+quik_status quik_layer_load_bundle(quik_ctx_t ctx, const char* dir, int64_t row_begin, int64_t row_end,
+                                   quik_layer_t* out);
 
 /*
  * K1 fused quantizer. reference: quantize_activations_fused (runtime.hpp:55-56,

@@ -50,6 +50,7 @@ inline void check(quik_status s) {
     case QUIK_ERR_INVALID_ARGUMENT: throw std::invalid_argument(m);
     case QUIK_ERR_OUT_OF_RANGE: throw std::out_of_range(m);
     case QUIK_ERR_NUMERICAL: throw NumericalError(m);
+    case QUIK_ERR_FORMAT: throw FormatError(m);
     default: throw CudaError(m);
   }
 }
@@ -329,6 +330,45 @@ class DeviceLayer {
 };
 
 // ---------------------------------------------------------------- reference functions
+
+// layer_io.hpp / layer_io.cpp:32-74: reference layer bundle -> host layer (FormatError
+// on every reference failure mode; parsed by the C ABI bundle reader)
+inline QuikLinearLayer load_layer(const std::string& dir) {
+  quik_bundle_t b = nullptr;
+  detail::check(quik_bundle_open(dir.c_str(), &b));
+  struct Close {
+    quik_bundle_t b;
+    ~Close() { quik_bundle_close(b); }
+  } close{b};
+  quik_weights_desc d{};
+  detail::check(quik_bundle_weights(b, &d));
+  QuikLinearLayer L;
+  L.act_bits = d.act_bits;
+  L.outliers = OutlierSet::from_indices(d.in_features,
+                                        std::vector<int64_t>(d.outlier_indices, d.outlier_indices + d.n_outlier));
+  const int64_t kb = d.in_features - d.n_outlier;
+  L.weights.base.rows = d.out_features;
+  L.weights.base.cols = kb;
+  L.weights.base.bits = d.bits;
+  L.weights.base.data.assign(d.base, d.base + d.out_features * L.weights.base.row_bytes());
+  L.weights.scales.assign(d.scales, d.scales + d.out_features);
+  L.weights.wreduced.assign(d.wreduced, d.wreduced + d.out_features);
+  L.weights.outlier_weights = FpMatrix(d.out_features, d.n_outlier);
+  if (d.n_outlier)
+    std::memcpy(L.weights.outlier_weights.data.data(), d.outlier_weights, d.out_features * d.n_outlier * 4);
+  if (d.bias) L.bias.assign(d.bias, d.bias + d.out_features);
+  if (d.sparsity) {
+    const void* m = nullptr;
+    int dt = 0, nd = 0;
+    int64_t shape[4] = {0, 0, 0, 0};
+    detail::check(quik_bundle_tensor(b, "sparsity_mask", &m, &dt, shape, &nd));
+    L.weights.mask.rows = shape[0];
+    L.weights.mask.cols = shape[1];
+    L.weights.mask.kept.assign(static_cast<const uint8_t*>(m),
+                               static_cast<const uint8_t*>(m) + shape[0] * shape[1]);
+  }
+  return L;
+}
 
 // runtime.hpp:85-87 (uploads the layer per call, like the reference re-reads its weights)
 inline FpMatrix quik_matmul(const QuikLinearLayer& layer, const FpMatrix& x,

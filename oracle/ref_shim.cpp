@@ -17,6 +17,7 @@
 #include "quik/packed.hpp"
 #include "quik/quantizer.hpp"
 #include "quik/runtime.hpp"
+#include "quik/layer_io.hpp"
 
 namespace {
 
@@ -25,6 +26,8 @@ int status_of(const std::exception_ptr& e) {
     std::rethrow_exception(e);
   } catch (const quik::NumericalError&) {
     return 3;
+  } catch (const quik::FormatError&) {
+    return 7;
   } catch (const std::out_of_range&) {
     return 2;
   } catch (const std::invalid_argument&) {
@@ -306,6 +309,42 @@ int qr_sparsegpt_joint(const float* w, int64_t N, int64_t K, const int64_t* idx,
     std::memcpy(wreduced, q.wreduced.data(), N * 4);
     if (n_out) std::memcpy(outlier_w, q.outlier_weights.data.data(), N * n_out * 4);
     std::memcpy(mask, q.mask.kept.data(), q.mask.kept.size());
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
+// save_layer (layer_io.cpp:7-30): writes a layer bundle exactly as the reference does
+// (the fixtures of the bundle-loader tests). mask: [N][K - n_out] or NULL; wfp32:
+// reference weights [N][K] or NULL.
+int qr_save_layer(const char* dir, int64_t in, int64_t out_f, int bits, int act_bits, const uint8_t* base,
+                  const float* scales, const float* wreduced, const float* outlier_w, const int64_t* idx,
+                  int64_t n_out, const float* bias, const uint8_t* mask, const float* wfp32) {
+  try {
+    quik::QuikLinearLayer L;
+    L.outliers = quik::OutlierSet::from_indices(in, std::vector<int64_t>(idx, idx + n_out));
+    const int64_t kb = in - n_out;
+    L.weights.base.rows = out_f;
+    L.weights.base.cols = kb;
+    L.weights.base.bits = bits;
+    L.weights.base.data.assign(base, base + out_f * (bits == 4 ? (kb + 1) / 2 : kb));
+    L.weights.scales.assign(scales, scales + out_f);
+    L.weights.wreduced.assign(wreduced, wreduced + out_f);
+    L.weights.outlier_weights = quik::FpMatrix(out_f, n_out);
+    if (n_out) std::memcpy(L.weights.outlier_weights.data.data(), outlier_w, out_f * n_out * 4);
+    if (bias) L.bias.assign(bias, bias + out_f);
+    if (mask) {
+      L.weights.mask.rows = out_f;
+      L.weights.mask.cols = kb;
+      L.weights.mask.kept.assign(mask, mask + out_f * kb);
+    }
+    if (wfp32) {
+      L.reference_weights = quik::FpMatrix(out_f, in);
+      std::memcpy(L.reference_weights.data.data(), wfp32, out_f * in * 4);
+    }
+    L.act_bits = act_bits;
+    quik::save_layer(L, dir);
     return 0;
   } catch (...) {
     return status_of(std::current_exception());

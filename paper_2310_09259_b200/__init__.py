@@ -7,7 +7,9 @@ kernels behind the C ABI in include/quik_b200.h.
 from .quik import (  # noqa: F401
     ActQuantResult,
     Context,
+    FormatError,
     NumericalError,
+    load_layer,
     OutlierSet,
     PackedIntMatrix,
     PipelineVariant,

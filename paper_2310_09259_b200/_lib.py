@@ -18,6 +18,7 @@ QUIK_ERR_NUMERICAL = 3
 QUIK_ERR_CUDA = 4
 QUIK_ERR_NCCL = 5
 QUIK_ERR_UNSUPPORTED = 6
+QUIK_ERR_FORMAT = 7
 
 QUIK_F16 = 0
 QUIK_F32 = 1
@@ -30,12 +31,17 @@ EXPORTED_SYMBOLS = (
     "quik_linear_forward_launches", "quik_linear_forward_ex", "quik_rtn_quantize_weights",
     "quik_set_gemm_tile", "quik_set_probe_mode", "quik_linear_forward_host",
     "quik_quantize_activations_gemm", "quik_layer_is_sparse", "quik_set_gemm_multicast",
-    "quik_set_gemm_w4", "quik_set_stream_gemm",
+    "quik_set_gemm_w4", "quik_set_stream_gemm", "quik_bundle_open", "quik_bundle_weights",
+    "quik_bundle_tensor", "quik_bundle_close", "quik_layer_load_bundle",
 )
 
 
 class NumericalError(RuntimeError):
     """reference: quik::NumericalError (matrix.hpp:18-21) — non-finite activations."""
+
+
+class FormatError(RuntimeError):
+    """reference: quik::FormatError (matrix.hpp:12-15) — malformed layer bundle / container."""
 
 
 class QuikCudaError(RuntimeError):
@@ -103,6 +109,12 @@ def load() -> C.CDLL:
             "quik_set_gemm_multicast": (i32, [i32]),
             "quik_set_gemm_w4": (i32, [i32]),
             "quik_set_stream_gemm": (i32, [i32, i32]),
+            "quik_bundle_open": (i32, [C.c_char_p, C.POINTER(vp)]),
+            "quik_bundle_weights": (i32, [vp, C.POINTER(WeightsDesc)]),
+            "quik_bundle_tensor": (i32, [vp, C.c_char_p, C.POINTER(vp), C.POINTER(i32), C.POINTER(i64),
+                                         C.POINTER(i32)]),
+            "quik_bundle_close": (i32, [vp]),
+            "quik_layer_load_bundle": (i32, [vp, C.c_char_p, i64, i64, C.POINTER(vp)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)
@@ -125,4 +137,6 @@ def check(status: int) -> None:
         raise NumericalError(msg)
     if status == QUIK_ERR_UNSUPPORTED:
         raise NotImplementedError(msg)
+    if status == QUIK_ERR_FORMAT:
+        raise FormatError(msg)
     raise QuikCudaError(msg)

@@ -26,7 +26,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
                      "-I" + str(ROOT / "include")]
-SOURCES = ["gemm.cu", "stream.cu", "quantize.cu", "capi.cu"]
+SOURCES = ["gemm.cu", "stream.cu", "quantize.cu", "capi.cu", "bundle.cpp"]
 
 
 def _run(cmd: list[str], cwd: Path | None = None) -> None:
@@ -88,11 +88,16 @@ def build_reference(force: bool = False) -> Path | None:
     if not REF_SRC.exists():
         return out if out.exists() else None
     out.parent.mkdir(exist_ok=True)
-    srcs = [REF_SRC / "src" / f for f in ("packed.cpp", "calibration.cpp", "quantizer.cpp", "runtime.cpp")]
+    srcs = [REF_SRC / "src" / f for f in ("packed.cpp", "calibration.cpp", "quantizer.cpp", "runtime.cpp",
+                                            "container.cpp", "layer_io.cpp")]
     shim = odir / "ref_shim.cpp"
+    # the container / layer-bundle sources include <json.hpp> (nlohmann 3.x, vendored in
+    # the reference's absent vendor dir; the same header ships with cudnn_frontend here)
+    json_dir = Path(sys.prefix) / "lib" / f"python{sys.version_info.major}.{sys.version_info.minor}" / \
+        "site-packages" / "include" / "cudnn_frontend" / "thirdparty" / "nlohmann"
     if force or _stale(out, srcs + [shim]):
         _run(["g++", "-std=c++20", "-O3", "-DNDEBUG", "-fopenmp", "-ffp-contract=off", "-fPIC", "-shared",
-              "-I" + str(REF_SRC / "include"), *map(str, srcs), str(shim), "-o", str(out)])
+              "-I" + str(REF_SRC / "include"), "-I" + str(json_dir), *map(str, srcs), str(shim), "-o", str(out)])
     return out
 
 

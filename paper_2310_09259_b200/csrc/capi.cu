@@ -38,8 +38,15 @@ cudaError_t ensure_smem_attr_impl(const void* kernel, int bytes) {
 }  // namespace quikb200
 
 namespace {
-
 thread_local std::string g_err;
+}  // namespace
+
+namespace quikb200 {
+void set_last_error(const std::string& msg) { g_err = msg; }
+}  // namespace quikb200
+
+namespace {
+
 int g_probe_mode = 0;  // diagnostics: V3 GEMM without output stores (quik_set_probe_mode)
 
 quik_status fail(quik_status s, const std::string& msg) {
@@ -247,6 +254,7 @@ const char* quik_status_string(quik_status s) {
     case QUIK_ERR_CUDA: return "cuda error";
     case QUIK_ERR_NCCL: return "nccl error";
     case QUIK_ERR_UNSUPPORTED: return "unsupported";
+    case QUIK_ERR_FORMAT: return "format error";
   }
   return "unknown";
 }

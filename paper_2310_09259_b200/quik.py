@@ -20,7 +20,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from ._lib import NumericalError  # noqa: F401  (re-export)
+from ._lib import FormatError, NumericalError  # noqa: F401  (re-export)
 
 
 # --------------------------------------------------------------------------- types
@@ -217,6 +217,26 @@ class Context:
     def sync(self, stream) -> None:
         _lib.check(self._lib.quik_ctx_sync(self.handle, C.c_void_p(stream)))
 
+    @classmethod
+    def from_bundle(cls, path, device: Optional[int] = None, row_begin: int = 0, row_end: int = 0) -> "QuikLinear":
+        """Bundle -> device GEMM layout in one call (C ABI quik_layer_load_bundle, SURVEY.md
+        §8f.1); `row_begin/row_end` load only an output-row shard. A bundle with a
+        sparsity mask (sparsegpt_joint) gets the 2:4 sparse GEMM."""
+        torch = _torch()
+        self = cls.__new__(cls)
+        self._lib = _lib.load()
+        self.ctx = context(device)
+        self.device = self.ctx.device
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(self._lib.quik_layer_load_bundle(self.ctx.handle, str(path).encode(), row_begin, row_end,
+                                                        C.byref(h)))
+        self.handle = h
+        inf, of, no, bits = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int()
+        self._lib.quik_layer_info(h, C.byref(inf), C.byref(of), C.byref(no), C.byref(bits))
+        self.in_features, self.out_features, self.n_outlier, self.bits = inf.value, of.value, no.value, bits.value
+        return self
+
     def __del__(self):
         try:
             if getattr(self, "handle", None):
@@ -331,6 +351,26 @@ class QuikLinear:
         of = C.c_int64()
         self._lib.quik_layer_info(h, None, C.byref(of), None, None)
         self.out_features = of.value
+        return self
+
+    @classmethod
+    def from_bundle(cls, path, device: Optional[int] = None, row_begin: int = 0, row_end: int = 0) -> "QuikLinear":
+        """Bundle -> device GEMM layout in one call (C ABI quik_layer_load_bundle, SURVEY.md
+        §8f.1); `row_begin/row_end` load only an output-row shard. A bundle with a
+        sparsity mask (sparsegpt_joint) gets the 2:4 sparse GEMM."""
+        torch = _torch()
+        self = cls.__new__(cls)
+        self._lib = _lib.load()
+        self.ctx = context(device)
+        self.device = self.ctx.device
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(self._lib.quik_layer_load_bundle(self.ctx.handle, str(path).encode(), row_begin, row_end,
+                                                        C.byref(h)))
+        self.handle = h
+        inf, of, no, bits = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int()
+        self._lib.quik_layer_info(h, C.byref(inf), C.byref(of), C.byref(no), C.byref(bits))
+        self.in_features, self.out_features, self.n_outlier, self.bits = inf.value, of.value, no.value, bits.value
         return self
 
     def __del__(self):
@@ -513,6 +553,54 @@ def dequantize_epilogue(acc: np.ndarray, a: ActQuantResult, weight_scales, wredu
                                                     _ptr(sw), _ptr(wr), _ptr(out), C.c_void_p(s)))
     ctx.sync(s)
     return out.cpu().numpy()
+
+
+def _bundle_tensor(lib, h, name):
+    """-> numpy copy of one bundle tensor (f32 -> float32, i8 / i4p -> raw uint8 bytes), or None."""
+    data, dt, nd = C.c_void_p(), C.c_int(), C.c_int()
+    shape = (C.c_int64 * 4)()
+    if lib.quik_bundle_tensor(h, name.encode(), C.byref(data), C.byref(dt), shape, C.byref(nd)) != _lib.QUIK_OK:
+        return None, None, None
+    shp = tuple(int(shape[i]) for i in range(nd.value))
+    if not data.value or (shp and int(np.prod(shp)) == 0):
+        return (np.zeros(shp, np.float32) if dt.value == 0 else np.zeros(0, np.uint8)), dt.value, shp
+    if dt.value == 0:
+        n = int(np.prod(shp)) if shp else 0
+        arr = np.ctypeslib.as_array((C.c_float * max(n, 1)).from_address(data.value))[:n].copy().reshape(shp)
+    else:
+        rows = shp[0] if len(shp) == 2 else 1
+        nbytes = rows * ((shp[-1] + 1) // 2 if dt.value == 2 else shp[-1]) if shp else 0
+        arr = np.ctypeslib.as_array((C.c_uint8 * max(nbytes, 1)).from_address(data.value))[:nbytes].copy()
+    return arr, dt.value, shp
+
+
+def load_layer(path) -> QuikLinearLayer:
+    """reference: load_layer (layer_io.hpp, layer_io.cpp:32-74): a layer bundle
+    (manifest.json + blobs) -> QuikLinearLayer, host arrays. Malformed bundles raise
+    FormatError (C ABI quik_bundle_open, which repeats every reference check)."""
+    lib = _lib.load()
+    h = C.c_void_p()
+    _lib.check(lib.quik_bundle_open(str(path).encode(), C.byref(h)))
+    try:
+        d = _lib.WeightsDesc()
+        _lib.check(lib.quik_bundle_weights(h, C.byref(d)))
+        base, bdt, bshape = _bundle_tensor(lib, h, "weight_base")
+        scales, _, _ = _bundle_tensor(lib, h, "weight_scales")
+        wred, _, _ = _bundle_tensor(lib, h, "wreduced")
+        ow, _, _ = _bundle_tensor(lib, h, "outlier_weights")
+        bias, _, _ = _bundle_tensor(lib, h, "bias")
+        mask, mdt, mshape = _bundle_tensor(lib, h, "sparsity_mask")
+        idx = np.ctypeslib.as_array((C.c_int64 * max(d.n_outlier, 1)).from_address(d.outlier_indices or 0)) \
+            if d.n_outlier else np.zeros(0, np.int64)
+        idx = np.array(idx[: d.n_outlier], dtype=np.int64)
+        bits = 4 if bdt == 2 else 8
+        weights = QuantizedWeights(PackedIntMatrix(bshape[0], bshape[1], bits, base), scales.reshape(-1),
+                                   ow.reshape(bshape[0], -1), wred.reshape(-1),
+                                   None if mask is None else mask.reshape(mshape))
+        return QuikLinearLayer(weights, OutlierSet.from_indices(int(d.in_features), idx),
+                               None if bias is None else bias.reshape(-1), int(d.act_bits))
+    finally:
+        lib.quik_bundle_close(h)
 
 
 def rtn_quantize_weights_device(w, outliers: OutlierSet, bits: int):

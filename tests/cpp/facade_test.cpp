@@ -47,7 +47,7 @@ static Q::FpMatrix rows(std::initializer_list<std::initializer_list<float>> init
   return m;
 }
 
-int main() {
+int main(int argc, char** argv) {
   // test_packed.cpp:78-92 — int_matmul hand-computed 2x2, INT8 and INT4
   {
     const std::vector<int8_t> xv = {1, -2, 3, 4}, wv = {5, 6, -7, 8}, w4 = {5, 6, -7, 7};
@@ -183,6 +183,22 @@ int main() {
     CHECK(throws<std::invalid_argument>([&] { Q::quik_matmul(L, Q::FpMatrix(1, 8)); }));
     L.act_bits = 4;
     CHECK(throws<std::invalid_argument>([&] { Q::quik_matmul(L, Q::FpMatrix(1, 9)); }));
+  }
+  // layer_io.cpp:32-74 through the bundle reader: reference bundles load with the same
+  // fields, the sparse one keeps its mask; a missing bundle is a FormatError
+  // (test_runtime.cpp:452-482). Bundles: tests/golden/bundle_* (reference save_layer).
+  if (argc > 1) {
+    const std::string root = argv[1];
+    const Q::QuikLinearLayer d = Q::load_layer(root + "/bundle_f16_w4_o64");
+    CHECK(d.in_features() == 512 && d.out_features() == 256 && d.outliers.outlier_count() == 64);
+    CHECK(d.weights.bits() == 4 && d.act_bits == 4 && d.bias.size() == 256 && d.weights.mask.empty());
+    const Q::QuikLinearLayer s = Q::load_layer(root + "/bundle_sp24_w4_o16");
+    CHECK(!s.weights.mask.empty() && s.weights.mask.rows == 160 && s.weights.mask.cols == 240);
+    Q::FpMatrix x(3, 256);
+    for (int64_t i = 0; i < x.size(); ++i) x.data[static_cast<size_t>(i)] = static_cast<float>((i * 37) % 11) - 5.0f;
+    const Q::FpMatrix y = Q::quik_matmul(s, x);  // sparse layer -> 2:4 GEMM
+    CHECK(y.rows == 3 && y.cols == 160);
+    CHECK(throws<Q::FormatError>([&] { Q::load_layer(root + "/missing"); }));
   }
   std::printf("facade_test: %d failure(s)\n", g_fail);
   return g_fail;

@@ -12,6 +12,7 @@ Cases:
   ref_test_layer_8bit  same generator, 8-bit, 24 x 200 -> 72, 8 outliers
   f16_*                numpy-seeded layers with f16-representable x and outlier
                        weights (device f16 path), weights from the reference RTN
+  bundle_<case>/       the f16_w4_o64 and sp24_w4_o16 layers as reference layer bundles
   sp24_*               2:4 sparse layers from the reference's sparsegpt_joint (identity
                        or random-PSD Hessian), mask stored; *_tail2 / *_tail3 have a
                        trailing dense remainder group of 2 / 3 base columns
@@ -124,6 +125,14 @@ def main():
                 blob[f"{name}.{k}"] = np.asarray(L[k])
         for k, v in out.items():
             blob[f"{name}.{k}"] = v
+    # layer bundles written by the reference's own save_layer (layer_io.cpp:7-30) for the
+    # bundle-loader GPU tests
+    import shutil
+    for name in ("f16_w4_o64", "sp24_w4_o16"):
+        L, _ = cases[name]
+        d = HERE / f"bundle_{name}"
+        shutil.rmtree(d, ignore_errors=True)
+        assert r.save_layer(d, L, mask=L.get("mask")) == 0
     np.savez_compressed(HERE / "quik_golden.npz", **blob)
     (HERE / "quik_golden.json").write_text(json.dumps(
         dict(generator="tests/golden/make_golden.py", source="oracle/_ref/libquik_ref.so (reference proj/src compiled "

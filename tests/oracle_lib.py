@@ -241,6 +241,16 @@ class Ref(_Base):
         return st, dict(base=base[: N * row_bytes(kb, bits)], scales=sc[:N], wreduced=wr[:N],
                         outlier_weights=ow[: N * idx.size].reshape(N, idx.size), mask=mask[: N * kb].reshape(N, kb))
 
+    def save_layer(self, path, L, mask=None, wfp32=None):
+        """The reference's save_layer (layer_io.cpp:7-30) -> bundle directory."""
+        keep, args = self._layer_args(L)
+        m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+        w = None if wfp32 is None else np.ascontiguousarray(wfp32, np.float32)
+        return self.f("save_layer")(str(path).encode(), C.c_int64(L["in_features"]), C.c_int64(L["out_features"]),
+                                    L["bits"], L.get("act_bits", L["bits"]), _p(keep["base"]), _p(keep["scales"]),
+                                    _p(keep["wreduced"]), _p(keep["outlier_weights"]), _p(keep["idx"]),
+                                    C.c_int64(np.asarray(L["idx"]).size), _p(keep["bias"]), _p(m), _p(w))
+
     def random_matrix(self, seed, rows, cols, stddev=1.0):
         out = np.zeros(max(rows * cols, 1), np.float32)
         fn = self.lib.qr_random_matrix

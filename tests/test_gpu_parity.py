@@ -502,7 +502,8 @@ def test_cpp_facade_parity_driver():
 
     exe = Path(__file__).resolve().parent.parent / "build" / "tests" / "facade_test"
     assert exe.exists(), "build/tests/facade_test not built (__graft_entry__.build())"
-    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    golden = Path(__file__).resolve().parent / "golden"
+    r = subprocess.run([str(exe), str(golden)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failure(s)" in r.stdout
 
@@ -738,3 +739,32 @@ def test_stream_gemm_bit_identical_to_fused(bits):
                 np.testing.assert_array_equal(outs[1].view(np.uint32), want.view(np.uint32))
     finally:
         lib.quik_set_stream_gemm(0, 1)
+
+
+# --------------------------------------------------------------------------- layer bundles (§8f.1)
+
+
+@pytest.mark.parametrize("name", ["f16_w4_o64", "sp24_w4_o16"])
+def test_bundle_to_device_matches_reference(name):
+    """Reference layer bundles (tests/golden/bundle_*, written by the reference's
+    save_layer) loaded straight into the device layout (quik_layer_load_bundle): the
+    forward matches the reference quik_matmul outputs of the same layer, the sparse
+    bundle runs the 2:4 GEMM, and a row-shard load equals the slice of the full layer."""
+    m = q()
+    import torch
+    from pathlib import Path
+
+    d = Path(__file__).resolve().parent / "golden" / f"bundle_{name}"
+    g = lambda k: _G[f"{name}.{k}"]  # noqa: E731
+    dev = m.QuikLinear.from_bundle(d)
+    assert dev.is_sparse == name.startswith("sp24")
+    xt = torch.from_numpy(g("x")).cuda()
+    y = dev(xt, out_dtype=torch.float32).cpu().numpy()
+    assert rel_frob(g("out_v3"), y) < 1e-5
+    N = dev.out_features
+    r0, r1 = N // 3, N // 3 + 64
+    shard = m.QuikLinear.from_bundle(d, row_begin=r0, row_end=r1)
+    ys = shard(xt, out_dtype=torch.float32).cpu().numpy()
+    np.testing.assert_array_equal(ys.view(np.uint32), y[:, r0:r1].view(np.uint32))
+    host = m.load_layer(d)  # reference semantics: host arrays
+    np.testing.assert_array_equal(m.quik_matmul(host, g("x")).view(np.uint32), y.view(np.uint32))
