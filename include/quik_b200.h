@@ -103,6 +103,17 @@ typedef struct quik_weights_desc {
  * of the weights (packed.cpp:110-111), which the device path does once here. */
 quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* desc, quik_layer_t* out);
 quik_status quik_layer_destroy(quik_layer_t layer);
+
+/* Gated MLP projection (reference forward_model with gated_mlp_ops,
+ * runtime.cpp:320-392): one layer computing h = silu(gate(x)) * up(x) [M][F] in a
+ * single K1 + GEMM launch pair -- the up and gate rows are interleaved in blocks of 32
+ * so every GEMM tile holds both projections of the same 32-feature blocks, and the
+ * epilogue forms silu(gate) * up in f32 (silu(e) = e / (1 + exp(-e))) before the
+ * f16/f32 store. up / gate: same shapes, bits and outlier set (the shared input x is
+ * quantized once); F (and a row shard) a multiple of 32. The down projection is a
+ * plain layer applied to h. quik_layer_info reports out_features = F. */
+quik_status quik_layer_create_gated(quik_ctx_t ctx, const quik_weights_desc* up, const quik_weights_desc* gate,
+                                   quik_layer_t* out);
 quik_status quik_layer_info(quik_layer_t layer, int64_t* in_features, int64_t* out_features,
                             int64_t* n_outlier, int* bits);
 /* 1 if the layer runs the 2:4 sparse GEMM (sparsity requested and compressible). */

@@ -228,6 +228,23 @@ int qr_layer_forward(void* h, const float* x, int64_t M, int variant, float* out
   }
 }
 
+// forward_model_trace over gated_mlp_ops (runtime.cpp:325-388) with layer handles
+// {up, gate, down}: out = down(silu(gate(x)) * up(x)) [M][down out]; h (optional) =
+// the Hadamard product value v4 [M][up out].
+int qr_gated_mlp(void* up, void* gate, void* down, const float* x, int64_t M, float* out, float* h) {
+  try {
+    std::vector<quik::QuikLinearLayer> layers = {static_cast<Layer*>(up)->layer, static_cast<Layer*>(gate)->layer,
+                                                 static_cast<Layer*>(down)->layer};
+    const auto ops = quik::gated_mlp_ops();
+    auto vals = quik::forward_model_trace(layers, ops, to_fp(x, M, layers[0].in_features()));
+    std::memcpy(out, vals.back().data.data(), vals.back().data.size() * 4);
+    if (h) std::memcpy(h, vals[4].data.data(), vals[4].data.size() * 4);
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
 int qr_rtn_quantize_weights(const float* w, int64_t N, int64_t K, const int64_t* idx, int64_t n_out, int bits,
                             uint8_t* base, float* scales, float* wreduced, float* outlier_w) {
   try {

@@ -14,6 +14,7 @@ from .quik import (  # noqa: F401
     PackedIntMatrix,
     PipelineVariant,
     QuantizedWeights,
+    QuikGatedMLP,
     QuikLinear,
     QuikLinearLayer,
     StageTimes,

@@ -32,7 +32,7 @@ EXPORTED_SYMBOLS = (
     "quik_set_gemm_tile", "quik_set_probe_mode", "quik_linear_forward_host",
     "quik_quantize_activations_gemm", "quik_layer_is_sparse", "quik_set_gemm_multicast",
     "quik_set_gemm_w4", "quik_set_stream_gemm", "quik_bundle_open", "quik_bundle_weights",
-    "quik_bundle_tensor", "quik_bundle_close", "quik_layer_load_bundle",
+    "quik_bundle_tensor", "quik_bundle_close", "quik_layer_load_bundle", "quik_layer_create_gated",
 )
 
 
@@ -115,6 +115,7 @@ def load() -> C.CDLL:
                                          C.POINTER(i32)]),
             "quik_bundle_close": (i32, [vp]),
             "quik_layer_load_bundle": (i32, [vp, C.c_char_p, i64, i64, C.POINTER(vp)]),
+            "quik_layer_create_gated": (i32, [vp, C.POINTER(WeightsDesc), C.POINTER(WeightsDesc), C.POINTER(vp)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)

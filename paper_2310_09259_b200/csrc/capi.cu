@@ -141,6 +141,7 @@ struct quik_layer_s {
   int bits = 4;
   int8_t* w8 = nullptr;      // [out][kpad] (null when sparse)
   int sparse = 0;            // 2:4 sparse GEMM operands below are in use
+  int gated = 0;             // gated MLP layer: rows interleave up / gate (32-row blocks), output width N / 2
   int8_t* w_sp = nullptr;    // [out][kpad / 2]
   uint8_t* w4 = nullptr;     // [out][kpad / 2] INT4 weights (4-bit layers), device nibble layout
   uint8_t* meta = nullptr;   // metadata planes (kernels.h GemmArgs)
@@ -220,6 +221,7 @@ GemmArgs gemm_args(quik_ctx_t ctx, const quik_layer_s* L, int64_t M) {
   g.opad = L->opad;
   g.M = M;
   g.N = L->out_features;
+  g.gated = L->gated;
   g.w_scale = L->w_scale;
   g.wreduced = L->wreduced;
   g.bias = L->bias;
@@ -530,6 +532,58 @@ quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* d, quik_l
   });
 }
 
+quik_status quik_layer_create_gated(quik_ctx_t ctx, const quik_weights_desc* up, const quik_weights_desc* gate,
+                                   quik_layer_t* out) {
+  if (!ctx || !up || !gate || !out) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_layer_create_gated: null argument");
+  if (up->in_features != gate->in_features || up->out_features != gate->out_features || up->bits != gate->bits ||
+      up->act_bits != gate->act_bits || up->n_outlier != gate->n_outlier)
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "gated MLP: up and gate layers differ in shape, bits or outlier count");
+  for (int64_t i = 0; i < up->n_outlier; ++i)
+    if (!up->outlier_indices || !gate->outlier_indices || up->outlier_indices[i] != gate->outlier_indices[i])
+      return fail(QUIK_ERR_INVALID_ARGUMENT, "gated MLP: up and gate layers need the same outlier set (shared quantizer)");
+  if ((up->bias == nullptr) != (gate->bias == nullptr))
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "gated MLP: bias on one projection only");
+  const int64_t F = up->out_features;
+  const int64_t rb = up->row_begin, re = (up->row_begin == 0 && up->row_end == 0) ? F : up->row_end;
+  if (rb < 0 || re < rb || re > F || rb % 32 || (re - rb) % 32)
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "gated MLP: feature count / shard must be a multiple of 32");
+  if (up->sparsity != gate->sparsity) return fail(QUIK_ERR_INVALID_ARGUMENT, "gated MLP: mixed 2:4 sparsity");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    // interleave the two row sets in blocks of 32 (host copies; arrays may live on the device)
+    const int64_t rows = re - rb, kb = up->in_features - up->n_outlier, O = up->n_outlier;
+    const int64_t rbytes = packed_row_bytes(kb, up->bits);
+    std::vector<uint8_t> base(static_cast<size_t>(2 * rows * rbytes));
+    std::vector<float> sc(static_cast<size_t>(2 * rows)), wr(static_cast<size_t>(2 * rows)),
+        ow(static_cast<size_t>(2 * rows * O)), bias(up->bias ? static_cast<size_t>(2 * rows) : 0);
+    auto fetch = [&](void* dst, const void* src, size_t bytes) {
+      if (bytes) QK_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDefault));
+    };
+    for (int64_t blk = 0; blk < rows / 32; ++blk)
+      for (int which = 0; which < 2; ++which) {
+        const quik_weights_desc* d = which ? gate : up;
+        const int64_t src_row = rb + 32 * blk, dst_row = 64 * blk + 32 * which;
+        fetch(base.data() + dst_row * rbytes, d->base + src_row * rbytes, static_cast<size_t>(32 * rbytes));
+        fetch(sc.data() + dst_row, d->scales + src_row, 32 * 4);
+        fetch(wr.data() + dst_row, d->wreduced + src_row, 32 * 4);
+        if (O) fetch(ow.data() + dst_row * O, d->outlier_weights + src_row * O, static_cast<size_t>(32 * O * 4));
+        if (d->bias) fetch(bias.data() + dst_row, d->bias + src_row, 32 * 4);
+      }
+    quik_weights_desc c = *up;
+    c.out_features = 2 * rows;
+    c.base = base.data();
+    c.scales = sc.data();
+    c.wreduced = wr.data();
+    c.outlier_weights = O ? ow.data() : nullptr;
+    c.bias = up->bias ? bias.data() : nullptr;
+    c.row_begin = 0;
+    c.row_end = 0;
+    const quik_status st = quik_layer_create(ctx, &c, out);
+    if (st == QUIK_OK) (*out)->gated = 1;
+    return st;
+  });
+}
+
 quik_status quik_layer_destroy(quik_layer_t L) {
   if (!L) return QUIK_OK;
   DeviceGuard g(L->device);
@@ -557,7 +611,7 @@ int quik_layer_is_sparse(quik_layer_t L) { return L ? L->sparse : 0; }
 quik_status quik_layer_info(quik_layer_t L, int64_t* in_f, int64_t* out_f, int64_t* n_out, int* bits) {
   if (!L) return fail(QUIK_ERR_INVALID_ARGUMENT, "null layer");
   if (in_f) *in_f = L->in_features;
-  if (out_f) *out_f = L->out_features;
+  if (out_f) *out_f = L->gated ? L->out_features / 2 : L->out_features;
   if (n_out) *n_out = L->n_outlier;
   if (bits) *bits = L->bits;
   return QUIK_OK;
@@ -824,7 +878,8 @@ quik_status quik_linear_forward_ex(quik_ctx_t ctx, quik_layer_t L, const void* x
   if (M < 0) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_matmul: negative token count");
   if (M > 0 && (!x || !y)) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_matmul: null input or output");
   if (M > 0x7fffffffLL) return fail(QUIK_ERR_UNSUPPORTED, "quik_matmul: token count exceeds 2^31");
-  if (ldy < L->out_features) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_matmul: output pitch < out_features");
+  if (ldy < (L->gated ? L->out_features / 2 : L->out_features))
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_matmul: output pitch < out_features");
   if (L->in_features * (xdt == QUIK_F32 ? 4 : 2) > 128 * 1024)
     return fail(QUIK_ERR_UNSUPPORTED, "quik_matmul: row wider than 128 KiB (register-resident quantizer limit)");
   if (ctx->device != L->device) return fail(QUIK_ERR_INVALID_ARGUMENT, "context and layer live on different devices");
@@ -852,7 +907,7 @@ quik_status quik_linear_forward_host(quik_ctx_t ctx, quik_layer_t L, const void*
   return guarded([&] {
     DeviceGuard g(ctx->device);
     cudaStream_t st = as_stream(stream);
-    const int64_t K = L->in_features, N = L->out_features;
+    const int64_t K = L->in_features, N = L->gated ? L->out_features / 2 : L->out_features;  // output width
     if (M == 0 || N == 0) return QUIK_OK;
     ctx->ensure_pipeline();
     const size_t xe = xdt == QUIK_F32 ? 4 : 2, ye = ydt == QUIK_F32 ? 4 : 2;
@@ -931,7 +986,8 @@ quik_status quik_rtn_quantize_weights(quik_ctx_t ctx, const float* w, int64_t N,
 quik_status quik_linear_forward(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M, void* y,
                                 quik_dtype ydt, quik_variant variant, void* stream) {
   if (!L) return fail(QUIK_ERR_INVALID_ARGUMENT, "null layer");
-  return quik_linear_forward_strided(ctx, L, x, xdt, M, y, ydt, L->out_features, variant, stream);
+  return quik_linear_forward_strided(ctx, L, x, xdt, M, y, ydt, L->gated ? L->out_features / 2 : L->out_features,
+                                     variant, stream);
 }
 
 }  // extern "C"

@@ -108,6 +108,10 @@ struct KParams {
   int32_t* acc_clear;
   int meta_rows;  // SP: n_pad = round_up(N, 128) rows per metadata (stage, half) plane
   int split_num;  // h_a = kb_int * split_num / 8
+  // gated MLP: weight rows interleave up / gate in blocks of 32
+  // (combined row 64b + w: w < 32 -> up feature 32b + w, else gate feature 32b + w - 32);
+  // the epilogue emits h[t][f] = silu(gate) * up into an [M][N / 2] output
+  int gated;
   // diagnostics (QUIK_GEMM_TRACE): per leader CTA and tile iteration (< kTraceTiles),
   // kTraceSlots globaltimer stamps; null in normal runs
   long long* trace;
@@ -539,9 +543,36 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
           v[j] = __float_as_uint(__fadd_rn(bs, x));
         }
       };
+      // gated: the gate warp (odd quadrant) hands its 32 x 32 f32 values to the up warp
+      // (even quadrant, same column half) through the gate warp's staging buffer; the up
+      // warp forms silu(gate) * up (reference forward_model: e / (1 + exp(-e)), then the
+      // Hadamard product, f32) and stores it at feature f = n / 2
+      const bool gate_warp = p.gated && (q & 1);
+      const int pair_bar = 1 + (e >> 1);  // named barriers 1..4, 64 threads each
+      float* xch = reinterpret_cast<float*>(staging + (e | 1) * 2 * kStoreBufBytes);
+      const int n0_out = p.gated ? n0 / 2 : n0;
       // writes 32 tokens x 32 features of final values
-      auto emit_chunk = [&](int c, const uint32_t (&v)[32]) {
+      auto emit_chunk = [&](int c, uint32_t (&v)[32]) {
         if constexpr (kProbe) return;
+        if (p.gated) {
+          if (gate_warp) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) xch[j * 32 + lane] = __uint_as_float(v[j]);
+            named_barrier_sync(pair_bar, 64);
+            named_barrier_sync(pair_bar, 64);  // the up warp has read the exchange buffer
+            return;
+          }
+          named_barrier_sync(pair_bar, 64);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float g = xch[j * 32 + lane];
+            // fast exp / divide (a few ulp; the reference's own std::exp differs from any
+            // device exp by ulps, so the gated output is compared within tolerance)
+            const float silu = __fdividef(g, 1.0f + __expf(-g));
+            v[j] = __float_as_uint(__fmul_rn(silu, __uint_as_float(v[j])));
+          }
+          named_barrier_sync(pair_bar, 64);
+        }
         if (tma_out) {
           __half* buf = reinterpret_cast<__half*>(my_stage + sbuf * kStoreBufBytes);
           if (lane == 0) bulk_wait_read<1>();  // the store issued from this buffer 2 chunks ago has read it
@@ -551,7 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&p.tm_y, buf, n0, mb * BN + c, pol_y);
+            tma_store_2d(&p.tm_y, buf, n0_out, mb * BN + c, pol_y);
             bulk_commit();
           }
           sbuf ^= 1;
@@ -561,7 +592,7 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
         for (int j = 0; j < 32; ++j) {
           const int t = mb * BN + c + j;
           if (t >= p.M || !n_ok) continue;
-          const long long off = static_cast<long long>(t) * p.ldo + n;
+          const long long off = static_cast<long long>(t) * p.ldo + (p.gated ? n0_out + lane : n);
           if (kInt32Out) reinterpret_cast<int32_t*>(p.out)[off] = static_cast<int32_t>(v[j]);
           else if (kF16Out) reinterpret_cast<__half*>(p.out)[off] = __float2half_rn(__uint_as_float(v[j]));
           else reinterpret_cast<float*>(p.out)[off] = __uint_as_float(v[j]);
@@ -897,6 +928,7 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
     return e ? atoi(e) : 0;
   }();
   kp.split_num = (split_env >= 1 && split_env <= 7) ? split_env : (sp ? 6 : 4);
+  kp.gated = a.gated && a.mode != kModeInt32 && a.mode != kModeProbe;  // raw accumulators stay per row
   static const char* trace_path = getenv("QUIK_GEMM_TRACE");  // diagnostics: timeline dump
   static long long* trace_buf = nullptr;
   const size_t trace_bytes = static_cast<size_t>(num_sms) * kTraceTiles * kTraceSlots * 8;
@@ -908,7 +940,7 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
   kp.tma_store = 0;
   if ((a.mode == kModeF16 || a.mode == kModeAccInitF16) && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 &&
       (a.ldo * 2) % 16 == 0) {
-    cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.N), static_cast<cuuint64_t>(a.M)};
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.gated ? a.N / 2 : a.N), static_cast<cuuint64_t>(a.M)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.ldo * 2)};
     cuuint32_t box[2] = {32, static_cast<cuuint32_t>(kChunk)};
     cuuint32_t estr[2] = {1, 1};

@@ -70,6 +70,9 @@ struct GemmArgs {
   // INT4 weights in the device nibble layout [N][kpad / 2] (or null): per 16-byte chunk
   // c of a row, byte i = (k = 32c + i) | (k = 32c + 16 + i) << 4, signed 4-bit values.
   const uint8_t* w4;
+  // gated MLP layer (rows interleave up / gate in blocks of 32): out is [M][N / 2],
+  // h = silu(gate) * up (modes kModeF16 / kModeF32, no tile splitting of the pairs)
+  int gated;
 };
 
 // Weight-streaming split-K integer GEMM for M <= 64 (stream.cu): adds

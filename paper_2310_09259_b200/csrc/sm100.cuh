@@ -186,6 +186,11 @@ __device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const CUtensorMap
       : "memory");
 }
 
+// Named barrier among `count` threads (multiple of 32) of the CTA.
+__device__ __forceinline__ void named_barrier_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 // ------------------------------------------------------------------ clusters
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;

@@ -218,6 +218,30 @@ class Context:
         _lib.check(self._lib.quik_ctx_sync(self.handle, C.c_void_p(stream)))
 
     @classmethod
+    def gated(cls, up: QuikLinearLayer, gate: QuikLinearLayer, device: Optional[int] = None, row_begin: int = 0,
+              row_end: int = 0) -> "QuikLinear":
+        """Gated MLP projection h = silu(gate(x)) * up(x) (reference forward_model with
+        gated_mlp_ops, runtime.cpp:320-392) as ONE layer: shared quantizer, one GEMM
+        whose epilogue forms silu(gate) * up (C ABI quik_layer_create_gated)."""
+        torch = _torch()
+        up.validate()
+        gate.validate()
+        self = cls.__new__(cls)
+        self._lib = _lib.load()
+        self.ctx = context(device)
+        self.device = self.ctx.device
+        du, ku = _host_desc(up, row_begin=row_begin, row_end=row_end)
+        dg, kg = _host_desc(gate, row_begin=row_begin, row_end=row_end)
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(self._lib.quik_layer_create_gated(self.ctx.handle, C.byref(du), C.byref(dg), C.byref(h)))
+        self.handle = h
+        inf, of, no, bits = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int()
+        self._lib.quik_layer_info(h, C.byref(inf), C.byref(of), C.byref(no), C.byref(bits))
+        self.in_features, self.out_features, self.n_outlier, self.bits = inf.value, of.value, no.value, bits.value
+        return self
+
+    @classmethod
     def from_bundle(cls, path, device: Optional[int] = None, row_begin: int = 0, row_end: int = 0) -> "QuikLinear":
         """Bundle -> device GEMM layout in one call (C ABI quik_layer_load_bundle, SURVEY.md
         §8f.1); `row_begin/row_end` load only an output-row shard. A bundle with a
@@ -271,6 +295,30 @@ def _ptr(t) -> C.c_void_p:
 
 def _dev(torch, a: np.ndarray, device: int):
     return torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{device}")
+
+
+def _host_desc(layer: QuikLinearLayer, sparse: Optional[bool] = None, row_begin: int = 0, row_end: int = 0):
+    """-> (WeightsDesc over host copies, the copies to keep alive)."""
+    w = layer.weights
+    n_out = layer.outliers.outlier_count()
+    keep = dict(
+        base=np.ascontiguousarray(w.base.data, dtype=np.uint8),
+        scales=np.ascontiguousarray(w.scales, dtype=np.float32),
+        wreduced=np.ascontiguousarray(w.wreduced, dtype=np.float32),
+        ow=np.ascontiguousarray(np.asarray(w.outlier_weights, dtype=np.float32).reshape(-1)
+                                if n_out and w.out_features() else np.zeros(1, np.float32)),
+        idx=np.ascontiguousarray(layer.outliers.indices, dtype=np.int64),
+        bias=None if layer.bias is None else np.ascontiguousarray(layer.bias, dtype=np.float32),
+    )
+    d = _lib.WeightsDesc(
+        in_features=layer.in_features(), out_features=w.out_features(), bits=w.bits(), act_bits=layer.act_bits,
+        base=keep["base"].ctypes.data if keep["base"].size else None,
+        scales=keep["scales"].ctypes.data, wreduced=keep["wreduced"].ctypes.data,
+        outlier_weights=keep["ow"].ctypes.data, outlier_indices=keep["idx"].ctypes.data if keep["idx"].size else None,
+        n_outlier=n_out, bias=None if keep["bias"] is None else keep["bias"].ctypes.data,
+        row_begin=row_begin, row_end=row_end,
+        sparsity=int(bool(w.mask is not None if sparse is None else sparse)))
+    return d, keep
 
 
 class QuikLinear:
@@ -351,6 +399,30 @@ class QuikLinear:
         of = C.c_int64()
         self._lib.quik_layer_info(h, None, C.byref(of), None, None)
         self.out_features = of.value
+        return self
+
+    @classmethod
+    def gated(cls, up: QuikLinearLayer, gate: QuikLinearLayer, device: Optional[int] = None, row_begin: int = 0,
+              row_end: int = 0) -> "QuikLinear":
+        """Gated MLP projection h = silu(gate(x)) * up(x) (reference forward_model with
+        gated_mlp_ops, runtime.cpp:320-392) as ONE layer: shared quantizer, one GEMM
+        whose epilogue forms silu(gate) * up (C ABI quik_layer_create_gated)."""
+        torch = _torch()
+        up.validate()
+        gate.validate()
+        self = cls.__new__(cls)
+        self._lib = _lib.load()
+        self.ctx = context(device)
+        self.device = self.ctx.device
+        du, ku = _host_desc(up, row_begin=row_begin, row_end=row_end)
+        dg, kg = _host_desc(gate, row_begin=row_begin, row_end=row_end)
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(self._lib.quik_layer_create_gated(self.ctx.handle, C.byref(du), C.byref(dg), C.byref(h)))
+        self.handle = h
+        inf, of, no, bits = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int()
+        self._lib.quik_layer_info(h, C.byref(inf), C.byref(of), C.byref(no), C.byref(bits))
+        self.in_features, self.out_features, self.n_outlier, self.bits = inf.value, of.value, no.value, bits.value
         return self
 
     @classmethod
@@ -572,6 +644,26 @@ def _bundle_tensor(lib, h, name):
         nbytes = rows * ((shp[-1] + 1) // 2 if dt.value == 2 else shp[-1]) if shp else 0
         arr = np.ctypeslib.as_array((C.c_uint8 * max(nbytes, 1)).from_address(data.value))[:nbytes].copy()
     return arr, dt.value, shp
+
+
+class QuikGatedMLP:
+    """The reference's gated MLP block (gated_mlp_ops, runtime.cpp:380-388:
+    down(silu(gate(x)) * up(x))) on the device: the fused gated projection (one K1 +
+    one GEMM) followed by the down projection (its own K1 + GEMM)."""
+
+    def __init__(self, up: QuikLinearLayer, gate: QuikLinearLayer, down: QuikLinearLayer,
+                 device: Optional[int] = None):
+        self.proj = QuikLinear.gated(up, gate, device)
+        self.down = QuikLinear(down, device)
+        if self.down.in_features != self.proj.out_features:
+            raise ValueError("gated MLP: down projection input != up/gate output features")
+
+    def forward(self, x, out=None, out_dtype=None, hidden_dtype=None):
+        """hidden_dtype: dtype of h between the projections (default: x's dtype)."""
+        h = self.proj(x, out_dtype=hidden_dtype or x.dtype)
+        return self.down(h, out=out, out_dtype=out_dtype)
+
+    __call__ = forward
 
 
 def load_layer(path) -> QuikLinearLayer:

@@ -241,6 +241,18 @@ class Ref(_Base):
         return st, dict(base=base[: N * row_bytes(kb, bits)], scales=sc[:N], wreduced=wr[:N],
                         outlier_weights=ow[: N * idx.size].reshape(N, idx.size), mask=mask[: N * kb].reshape(N, kb))
 
+    def gated_mlp(self, up, gate, down, x):
+        """The reference's forward_model(gated_mlp_ops): -> (st, out, h = silu(gate) * up)."""
+        hs = [self.layer_create(L) for L in (up, gate, down)]
+        x = np.ascontiguousarray(x, np.float32)
+        out = np.zeros((x.shape[0], down["out_features"]), np.float32)
+        h = np.zeros((x.shape[0], up["out_features"]), np.float32)
+        st = self.f("gated_mlp")(C.c_void_p(hs[0][0]), C.c_void_p(hs[1][0]), C.c_void_p(hs[2][0]), _p(x),
+                                 C.c_int64(x.shape[0]), _p(out), _p(h))
+        for hh, _ in hs:
+            self.layer_destroy(hh)
+        return st, out, h
+
     def save_layer(self, path, L, mask=None, wfp32=None):
         """The reference's save_layer (layer_io.cpp:7-30) -> bundle directory."""
         keep, args = self._layer_args(L)

@@ -768,3 +768,79 @@ def test_bundle_to_device_matches_reference(name):
     np.testing.assert_array_equal(ys.view(np.uint32), y[:, r0:r1].view(np.uint32))
     host = m.load_layer(d)  # reference semantics: host arrays
     np.testing.assert_array_equal(m.quik_matmul(host, g("x")).view(np.uint32), y.view(np.uint32))
+
+
+# --------------------------------------------------------------------------- gated MLP (§8f.2)
+
+
+def _mlp_layers(rng, M, K, F, bits_ud, bits_down, O, O_down):
+    """up / gate sharing the outlier set selected from x (the same input), and a down
+    projection with its own outliers; RTN weights through the oracle. Weights are scaled
+    so the hidden state h stays inside the f16 range of the outlier operands (the device
+    path rounds outlier activations to f16, |x| <= 65504)."""
+    o = oracle()
+    up, x, w = make_layer(rng, M, K, F, bits_ud, O, heavy_cols=3)
+    qu = o.rtn_quantize_weights(w * 0.02, up["idx"], bits_ud)
+    up.update(base=qu["base"], scales=qu["scales"], wreduced=qu["wreduced"],
+              outlier_weights=qu["outlier_weights"].astype(np.float16).astype(np.float32))
+    wg = rng.normal(0.0, 0.01, size=(F, K)).astype(np.float32)
+    qg = o.rtn_quantize_weights(wg, up["idx"], bits_ud)
+    gate = dict(up, base=qg["base"], scales=qg["scales"], wreduced=qg["wreduced"],
+                outlier_weights=qg["outlier_weights"].astype(np.float16).astype(np.float32),
+                bias=rng.normal(0.0, 0.1, size=F).astype(np.float32))
+    wd = rng.normal(0.0, 0.5, size=(K, F)).astype(np.float32)
+    idx_d = np.sort(rng.choice(F, size=O_down, replace=False)).astype(np.int64)
+    qd = o.rtn_quantize_weights(wd, idx_d, bits_down)
+    down = dict(in_features=F, out_features=K, bits=bits_down, act_bits=bits_down, base=qd["base"],
+                scales=qd["scales"], wreduced=qd["wreduced"],
+                outlier_weights=qd["outlier_weights"].astype(np.float16).astype(np.float32), idx=idx_d,
+                bias=rng.normal(0.0, 0.1, size=K).astype(np.float32))
+    return up, gate, down, x
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+def test_gated_projection_and_mlp_match_reference(bits):
+    """h = silu(gate(x)) * up(x) from ONE fused layer (shared K1, interleaved up/gate
+    rows, silu * up in the epilogue) and the whole block down(h) against the reference's
+    forward_model(gated_mlp_ops) (runtime.cpp:325-388)."""
+    m = q()
+    r = ref()
+    import torch
+
+    rng = np.random.default_rng(600 + bits)
+    for (M, K, F, O, Od) in [(40, 256, 160, 32, 16), (300, 512, 384, 64, 32), (7, 384, 96, 0, 0)]:
+        up, gate, down, x = _mlp_layers(rng, M, K, F, bits, 8, O, Od)
+        st, want, want_h = r.gated_mlp(up, gate, down, x)
+        assert st == 0
+        proj = m.QuikLinear.gated(to_layer(up), to_layer(gate))
+        assert proj.out_features == F
+        xt = torch.from_numpy(x).cuda()
+        h32 = proj(xt, out_dtype=torch.float32).cpu().numpy()
+        assert rel_frob(want_h, h32) < 1e-5, rel_frob(want_h, h32)  # exp ulps + f16 outlier order
+        for v in m.PipelineVariant:  # V1 / V2 / V3 identical on the device
+            hv = proj(xt, out_dtype=torch.float32, variant=v).cpu().numpy()
+            np.testing.assert_array_equal(hv.view(np.uint32), h32.view(np.uint32))
+        mlp = m.QuikGatedMLP(to_layer(up), to_layer(gate), to_layer(down))
+        y32 = mlp(xt, out_dtype=torch.float32, hidden_dtype=torch.float32).cpu().numpy()
+        assert rel_frob(want, y32) < 1e-3, rel_frob(want, y32)
+        y16 = mlp(xt.half()).float().cpu().numpy()
+        assert rel_frob(want, y16) < 2e-2, rel_frob(want, y16)  # h rounded to f16 before down's quantizer
+        if F % 64 == 0:  # 32-feature-aligned row shard == slice of the full projection
+            sh = m.QuikLinear.gated(to_layer(up), to_layer(gate), row_begin=32, row_end=96)
+            hs = sh(xt, out_dtype=torch.float32).cpu().numpy()
+            np.testing.assert_array_equal(hs.view(np.uint32), h32[:, 32:96].view(np.uint32))
+
+
+@pytest.mark.parametrize("cg,bn", [(1, 32), (1, 128), (2, 128), (2, 256)])
+def test_gated_projection_every_tile(tile, cg, bn):
+    m = q()
+    import torch
+
+    rng = np.random.default_rng(700 + bn)
+    up, gate, down, x = _mlp_layers(rng, 260, 640, 320, 4, 8, 64, 16)
+    proj = m.QuikLinear.gated(to_layer(up), to_layer(gate))
+    xt = torch.from_numpy(x).cuda()
+    want = proj(xt, out_dtype=torch.float32).cpu().numpy()
+    assert tile(cg, bn) == 0
+    got = proj(xt, out_dtype=torch.float32).cpu().numpy()
+    np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
