@@ -487,11 +487,6 @@ quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* d, quik_l
         QK_CUDA(cudaMemcpy(tmp, d->base + rb * rbytes, static_cast<size_t>(rows * rbytes), cudaMemcpyDefault));
         check_launch(launch_unpack_to_gemm(static_cast<const uint8_t*>(tmp), rows, kb, d->bits, L->w8, L->kpad, st),
                      "weight unpack");
-        if (d->bits == 4) {
-          // INT4 copy for the weight-streaming (small-M) GEMM tiles
-          QK_CUDA(cudaMalloc(&L->w4, static_cast<size_t>(rows * L->kpad / 2)));
-          check_launch(launch_pack_w4(L->w8, rows, L->kpad, L->w4, st), "int4 weight pack");
-        }
         if (d->sparsity) {
           // 2:4 compression (tcgen05.mma.sp operands); stays dense if not compressible
           const int64_t npad = round_up(rows, kBlockM);
@@ -768,11 +763,26 @@ quik_status quik_dequantize_epilogue(quik_ctx_t ctx, const int32_t* acc, int64_t
 }  // extern "C"
 
 namespace {
+// INT4 weight copy for the opt-in W4 / INT4-stream GEMM variants, made on first use
+// (not at layer create: it would cost 50 % of the int8 weights' HBM for every 4-bit
+// layer). Not during stream capture (cudaMalloc): those forwards read int8 weights.
+void ensure_w4(quik_layer_s* L, cudaStream_t st) {
+  if (L->w4 || L->bits != 4 || !L->w8 || L->sparse) return;
+  if (!quikb200::gemm_w4 && !(quikb200::gemm_stream && quikb200::gemm_w4_stream)) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  QK_CUDA(cudaStreamIsCapturing(st, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return;
+  const int64_t rows = L->out_features;  // all rows (gated: up + gate)
+  QK_CUDA(cudaMalloc(&L->w4, static_cast<size_t>(rows * L->kpad / 2)));
+  check_launch(launch_pack_w4(L->w8, rows, L->kpad, L->w4, st), "int4 weight pack");
+}
+
 // The forward on device buffers (argument checks done by the caller).
 quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M, void* y,
                          quik_dtype ydt, int64_t ldy, quik_variant variant, cudaStream_t st, void* mid_event) {
   if (M == 0 || L->out_features == 0) return QUIK_OK;
   const int64_t N = L->out_features;
+  ensure_w4(L, st);
   if (variant == QUIK_V3_FUSED_EPILOGUE && M <= 64 && L->kpad && !L->sparse && quikb200::gemm_stream && !g_probe_mode) {
     // weight-streaming regime: K1 -> split-K stream GEMM into the zeroed int32
     // workspace -> the fused kernel's AccInit mode (dequant + outlier MMAs + store,
