@@ -194,6 +194,17 @@ quik_status quik_linear_forward_ex(quik_ctx_t ctx, quik_layer_t layer, const voi
                                    void* y, quik_dtype y_dtype, int64_t ldy, quik_variant variant, void* stream,
                                    void* mid_event);
 
+/* WeightOnly mode (reference LayerMode::WeightOnly, weight_only_forward,
+ * runtime.cpp:115-136): activations stay floating point,
+ *   y = (bias + x_o W_o^T) + x_b (q * scale)^T
+ * on device buffers, asynchronous on `stream`. 4-bit layers stream INT4 weights (an
+ * INT4 copy is made on the first call). Every product is exact; f32 accumulation in
+ * a different order than the reference. f32 inputs are carried as two f16 planes
+ * (hi + lo), f16 inputs exactly; inputs must be inside the f16 range. Not for gated
+ * or 2:4-compressed layers (QUIK_ERR_UNSUPPORTED). */
+quik_status quik_linear_forward_weight_only(quik_ctx_t ctx, quik_layer_t layer, const void* x, quik_dtype x_dtype,
+                                            int64_t M, void* y, quik_dtype y_dtype, int64_t ldy, void* stream);
+
 /* The hot path with HOST activations and outputs: what the reference's
  * quik_matmul(layer, FpMatrix) call (runtime.hpp:85-87) does with host data.
  * x_host [M][in_features] and y_host [M][out_features] are host memory (page-locked

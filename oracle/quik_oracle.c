@@ -373,3 +373,40 @@ void qo_compute_wreduced(const uint8_t* base, int64_t N, int64_t kb, int bits, c
   }
   free(v);
 }
+
+/* runtime.cpp:115-136 (LayerMode::WeightOnly). quik_matmul validates the layer first
+ * (runtime.cpp:247, :150-167; act_bits need not match in this mode) and dispatches
+ * here at :255: split_activations (:169-186), unpack_values of the base codes,
+ * fp_linear (:96-113) for bias + outliers, then per output the sequential FP32 sum
+ * acc += x_b[j] * (float(q[j]) * scale) added onto it. */
+int qo_weight_only_forward(const qo_layer* L, const float* x, int64_t M, float* out) {
+  if (L->bits != 4 && L->bits != 8) return QO_INVALID_ARGUMENT;
+  const int64_t K = L->in_features, N = L->out_features, O = L->n_outlier, kb = K - O;
+  if (kb < 0) return QO_INVALID_ARGUMENT;
+  int64_t* perm = (int64_t*)malloc(sizeof(int64_t) * ((size_t)K + 1));
+  if (qo_outlier_permutation(K, L->outlier_idx, O, perm)) {
+    free(perm);
+    return QO_INVALID_ARGUMENT;
+  }
+  float* xb = (float*)malloc(sizeof(float) * ((size_t)(M * kb) + 1));
+  float* xo = (float*)malloc(sizeof(float) * ((size_t)(M * O) + 1));
+  int8_t* q = (int8_t*)malloc((size_t)(N * kb) + 1);
+  qo_split_activations(x, M, K, perm, kb, L->outlier_idx, O, xb, xo);
+  qo_unpack(L->base, N, kb, L->bits, q);
+  qo_fp_linear(xo, M, O, L->outlier_weights, L->bias, N, out);
+  for (int64_t t = 0; t < M; ++t) {
+    const float* xr = xb + t * kb;
+    for (int64_t r = 0; r < N; ++r) {
+      const int8_t* qr = q + r * kb;
+      const float scale = L->scales[r];
+      float acc = 0.0f;
+      for (int64_t j = 0; j < kb; ++j) acc += xr[j] * ((float)qr[j] * scale);
+      out[t * N + r] += acc;
+    }
+  }
+  free(q);
+  free(xo);
+  free(xb);
+  free(perm);
+  return QO_OK;
+}

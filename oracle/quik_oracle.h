@@ -77,6 +77,9 @@ typedef struct qo_layer {
 
 /* runtime.cpp:246-318, LayerMode::Quik; variant 0=V1, 1=V2, 2=V3. */
 int qo_quik_matmul(const qo_layer* layer, const float* x, int64_t M, int variant, float* out);
+/* runtime.cpp:115-136, LayerMode::WeightOnly: fp_linear(x_o, W_o, bias) then
+ * out[t][r] += sum_j x_b[t][j] * ((float)q[r][j] * scale[r]), sequential FP32. */
+int qo_weight_only_forward(const qo_layer* layer, const float* x, int64_t M, float* out);
 
 /* quantizer.cpp:339-371 (+ :251-264, :17-22): RTN symmetric per-row, FP64 internals. */
 int qo_rtn_quantize_weights(const float* w, int64_t N, int64_t K, const int64_t* idx, int64_t n_out, int bits,

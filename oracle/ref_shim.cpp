@@ -196,6 +196,21 @@ int qr_quik_matmul(int64_t in, int64_t out_f, int bits, int act_bits, const uint
   }
 }
 
+// LayerMode::WeightOnly through the reference's own quik_matmul (runtime.cpp:255).
+int qr_weight_only(int64_t in, int64_t out_f, int bits, int act_bits, const uint8_t* base, const float* scales,
+                   const float* wreduced, const float* ow, const int64_t* idx, int64_t n_out, const float* bias,
+                   const float* x, int64_t M, float* out) {
+  try {
+    auto L = make_layer(in, out_f, bits, act_bits, base, scales, wreduced, ow, idx, n_out, bias);
+    L.mode = quik::LayerMode::WeightOnly;
+    auto r = quik::quik_matmul(L, to_fp(x, M, in));
+    std::memcpy(out, r.data.data(), r.data.size() * 4);
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
 // Persistent layer handle so timing loops exclude layer assembly.
 void* qr_layer_create(int64_t in, int64_t out_f, int bits, int act_bits, const uint8_t* base, const float* scales,
                       const float* wreduced, const float* ow, const int64_t* idx, int64_t n_out, const float* bias) {

@@ -106,7 +106,7 @@ struct quik_ctx_s {
   int device = 0;
   int num_sms = 148;
   int* d_err = nullptr;
-  DevBuf q8, scale, zero, xo16, acc, fp, xbase, xo32, wtmp;
+  DevBuf q8, scale, zero, xo16, acc, fp, xbase, xo32, wtmp, wo_ws;
   // host-buffer forward (quik_linear_forward_host): copy-in / copy-out streams and
   // per-chunk events, created on first use; device staging for x and y.
   cudaStream_t s_in = nullptr, s_out = nullptr;
@@ -146,6 +146,7 @@ struct quik_layer_s {
   uint8_t* w4 = nullptr;     // [out][kpad / 2] INT4 weights (4-bit layers), device nibble layout
   uint8_t* meta = nullptr;   // metadata planes (kernels.h GemmArgs)
   __half* wo16 = nullptr;    // [out][opad]
+  __half* wo16_lo = nullptr; // [out][opad] f16(w_o - f16(w_o)): weight-only forward (f32-accurate outliers)
   float* w_scale = nullptr;  // [out]
   float* wreduced = nullptr; // [out]
   float* bias = nullptr;     // [out] or null
@@ -332,7 +333,7 @@ quik_status quik_ctx_destroy(quik_ctx_t ctx) {
   DeviceGuard g(ctx->device);
   cudaDeviceSynchronize();
   for (DevBuf* b : {&ctx->q8, &ctx->scale, &ctx->zero, &ctx->xo16, &ctx->acc, &ctx->fp, &ctx->xbase, &ctx->xo32,
-                    &ctx->wtmp, &ctx->xdev, &ctx->ydev, &ctx->ws})
+                    &ctx->wtmp, &ctx->xdev, &ctx->ydev, &ctx->ws, &ctx->wo_ws})
     b->release();
   if (ctx->s_in) {
     cudaStreamDestroy(ctx->s_in);
@@ -519,6 +520,9 @@ quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* d, quik_l
                            cudaMemcpyDefault));
         check_launch(launch_f32_to_f16_padded(static_cast<const float*>(tmp), rows, d->n_outlier, L->wo16, L->opad, st),
                      "outlier weight convert");
+        QK_CUDA(cudaMalloc(&L->wo16_lo, static_cast<size_t>(rows * L->opad * 2)));
+        check_launch(launch_f16_lo_padded(static_cast<const float*>(tmp), rows, d->n_outlier, L->wo16_lo, L->opad, st),
+                     "outlier weight convert (lo)");
       }
     }
     QK_CUDA(cudaStreamSynchronize(st));
@@ -588,6 +592,7 @@ quik_status quik_layer_destroy(quik_layer_t L) {
   cudaFree(L->meta);
   cudaFree(L->w4);
   cudaFree(L->wo16);
+  cudaFree(L->wo16_lo);
   cudaFree(L->w_scale);
   cudaFree(L->wreduced);
   cudaFree(L->bias);
@@ -766,9 +771,9 @@ namespace {
 // INT4 weight copy for the opt-in W4 / INT4-stream GEMM variants, made on first use
 // (not at layer create: it would cost 50 % of the int8 weights' HBM for every 4-bit
 // layer). Not during stream capture (cudaMalloc): those forwards read int8 weights.
-void ensure_w4(quik_layer_s* L, cudaStream_t st) {
+void ensure_w4(quik_layer_s* L, cudaStream_t st, bool needed = false) {
   if (L->w4 || L->bits != 4 || !L->w8 || L->sparse) return;
-  if (!quikb200::gemm_w4 && !(quikb200::gemm_stream && quikb200::gemm_w4_stream)) return;
+  if (!needed && !quikb200::gemm_w4 && !(quikb200::gemm_stream && quikb200::gemm_w4_stream)) return;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   QK_CUDA(cudaStreamIsCapturing(st, &cs));
   if (cs != cudaStreamCaptureStatusNone) return;
@@ -902,6 +907,53 @@ quik_status quik_linear_forward_ex(quik_ctx_t ctx, quik_layer_t L, const void* x
 quik_status quik_linear_forward_strided(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M,
                                         void* y, quik_dtype ydt, int64_t ldy, quik_variant variant, void* stream) {
   return quik_linear_forward_ex(ctx, L, x, xdt, M, y, ydt, ldy, variant, stream, nullptr);
+}
+
+quik_status quik_linear_forward_weight_only(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt,
+                                            int64_t M, void* y, quik_dtype ydt, int64_t ldy, void* stream) {
+  if (!ctx || !L) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context or layer");
+  if (M < 0) return fail(QUIK_ERR_INVALID_ARGUMENT, "weight_only_forward: negative token count");
+  if (M > 0 && (!x || !y)) return fail(QUIK_ERR_INVALID_ARGUMENT, "weight_only_forward: null input or output");
+  if (M > 0x7fffffffLL) return fail(QUIK_ERR_UNSUPPORTED, "weight_only_forward: token count exceeds 2^31");
+  if (L->gated) return fail(QUIK_ERR_UNSUPPORTED, "weight_only_forward: gated MLP layers run in quik mode only");
+  if (ldy < L->out_features) return fail(QUIK_ERR_INVALID_ARGUMENT, "weight_only_forward: output pitch < out_features");
+  if (L->sparse) return fail(QUIK_ERR_UNSUPPORTED, "weight_only_forward: 2:4-compressed layers run in quik mode only");
+  if (ctx->device != L->device) return fail(QUIK_ERR_INVALID_ARGUMENT, "context and layer live on different devices");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = as_stream(stream);
+    if (M == 0 || L->out_features == 0) return QUIK_OK;
+    ensure_w4(L, st, true);  // INT4 weights are what the decode regime streams
+    WoArgs a{};
+    a.x = x;
+    a.x_is_f32 = xdt == QUIK_F32;
+    a.M = M;
+    a.ldx = L->in_features;
+    a.base_src = L->base_src;
+    a.kb = L->kb;
+    a.kpad = L->kpad;
+    a.out_src = L->out_src;
+    a.n_out = L->n_outlier;
+    a.opad = L->opad;
+    a.w4 = L->bits == 4 ? L->w4 : nullptr;
+    a.w8 = L->w8;
+    a.wo = L->wo16;
+    a.wo_lo = L->wo16_lo;
+    a.scale = L->w_scale;
+    a.bias = L->bias;
+    a.N = L->out_features;
+    a.y = y;
+    a.y_is_f16 = ydt == QUIK_F16;
+    a.ldy = ldy;
+    size_t pb = 0, po = 0;
+    const size_t wsb = wo_workspace_bytes(a, ctx->num_sms, &pb, &po);
+    a.xb = static_cast<__half*>(ctx->xbase.ensure(std::max<size_t>(pb, 16)));
+    a.xo = static_cast<__half*>(ctx->xo16.ensure(std::max<size_t>(po, 16)));
+    a.ws = wsb ? static_cast<float*>(ctx->wo_ws.ensure(wsb)) : nullptr;
+    const char* msg = nullptr;
+    check_launch(launch_weight_only(a, ctx->num_sms, st, &msg), "weight-only kernel", msg);
+    return QUIK_OK;
+  });
 }
 
 quik_status quik_linear_forward_host(quik_ctx_t ctx, quik_layer_t L, const void* x_host, quik_dtype xdt, int64_t M,

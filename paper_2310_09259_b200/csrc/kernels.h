@@ -88,6 +88,36 @@ struct StreamArgs {
 };
 cudaError_t launch_stream_gemm(const StreamArgs& a, int num_sms, cudaStream_t stream, const char** err_msg);
 
+// WeightOnly forward (wo.cu, reference weight_only_forward runtime.cpp:115-136).
+struct WoArgs {
+  const void* x;        // [M][ldx] f16 or f32
+  int x_is_f32;
+  int64_t M, ldx;
+  const int32_t* base_src;  // [kb] permuted base column -> source column
+  int64_t kb, kpad;
+  const int32_t* out_src;   // [n_out]
+  int64_t n_out, opad;
+  const uint8_t* w4;        // INT4 device layout [N][kpad / 2] (4-bit layers) or null
+  const int8_t* w8;         // [N][kpad] (used when w4 is null)
+  const __half* wo;         // [N][opad] f16(w_o)
+  const __half* wo_lo;      // [N][opad] f16(w_o - f16(w_o))
+  const float* scale;       // [N]
+  const float* bias;        // [N] or null
+  int64_t N;
+  __half* xb;               // workspace [P*M][kpad] (P = 2 for f32 input)
+  __half* xo;               // workspace [P*M][opad]
+  float* ws;                // workspace (wo_workspace_bytes)
+  void* y;
+  int y_is_f16;
+  int64_t ldy;
+};
+// Workspace bytes for ws (0 when the GEMM writes y directly) and the token planes.
+size_t wo_workspace_bytes(const WoArgs& a, int num_sms, size_t* plane_bytes_b, size_t* plane_bytes_o);
+cudaError_t launch_weight_only(const WoArgs& a, int num_sms, cudaStream_t stream, const char** err_msg);
+// dst[r][c] = f16(src[r][c] - f16(src[r][c])) (zero padded to pitch)
+cudaError_t launch_f16_lo_padded(const float* src, int64_t rows, int64_t cols, __half* dst, int64_t pitch,
+                                 cudaStream_t stream);
+
 // 2D K-major tensor map (uint8), box {box_inner bytes, box_rows}, 128-byte swizzle or none.
 CUresult encode_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t pitch,
                        uint32_t box_inner, uint32_t box_rows, bool swizzle128);

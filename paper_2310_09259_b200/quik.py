@@ -217,50 +217,6 @@ class Context:
     def sync(self, stream) -> None:
         _lib.check(self._lib.quik_ctx_sync(self.handle, C.c_void_p(stream)))
 
-    @classmethod
-    def gated(cls, up: QuikLinearLayer, gate: QuikLinearLayer, device: Optional[int] = None, row_begin: int = 0,
-              row_end: int = 0) -> "QuikLinear":
-        """Gated MLP projection h = silu(gate(x)) * up(x) (reference forward_model with
-        gated_mlp_ops, runtime.cpp:320-392) as ONE layer: shared quantizer, one GEMM
-        whose epilogue forms silu(gate) * up (C ABI quik_layer_create_gated)."""
-        torch = _torch()
-        up.validate()
-        gate.validate()
-        self = cls.__new__(cls)
-        self._lib = _lib.load()
-        self.ctx = context(device)
-        self.device = self.ctx.device
-        du, ku = _host_desc(up, row_begin=row_begin, row_end=row_end)
-        dg, kg = _host_desc(gate, row_begin=row_begin, row_end=row_end)
-        h = C.c_void_p()
-        with torch.cuda.device(self.device):
-            _lib.check(self._lib.quik_layer_create_gated(self.ctx.handle, C.byref(du), C.byref(dg), C.byref(h)))
-        self.handle = h
-        inf, of, no, bits = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int()
-        self._lib.quik_layer_info(h, C.byref(inf), C.byref(of), C.byref(no), C.byref(bits))
-        self.in_features, self.out_features, self.n_outlier, self.bits = inf.value, of.value, no.value, bits.value
-        return self
-
-    @classmethod
-    def from_bundle(cls, path, device: Optional[int] = None, row_begin: int = 0, row_end: int = 0) -> "QuikLinear":
-        """Bundle -> device GEMM layout in one call (C ABI quik_layer_load_bundle, SURVEY.md
-        §8f.1); `row_begin/row_end` load only an output-row shard. A bundle with a
-        sparsity mask (sparsegpt_joint) gets the 2:4 sparse GEMM."""
-        torch = _torch()
-        self = cls.__new__(cls)
-        self._lib = _lib.load()
-        self.ctx = context(device)
-        self.device = self.ctx.device
-        h = C.c_void_p()
-        with torch.cuda.device(self.device):
-            _lib.check(self._lib.quik_layer_load_bundle(self.ctx.handle, str(path).encode(), row_begin, row_end,
-                                                        C.byref(h)))
-        self.handle = h
-        inf, of, no, bits = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int()
-        self._lib.quik_layer_info(h, C.byref(inf), C.byref(of), C.byref(no), C.byref(bits))
-        self.in_features, self.out_features, self.n_outlier, self.bits = inf.value, of.value, no.value, bits.value
-        return self
-
     def __del__(self):
         try:
             if getattr(self, "handle", None):
@@ -488,6 +444,29 @@ class QuikLinear:
         return out
 
     __call__ = forward
+
+    def weight_only(self, x, out=None, out_dtype=None):
+        """LayerMode::WeightOnly (reference weight_only_forward, runtime.cpp:115-136):
+        activations stay floating point, y = (bias + x_o W_o^T) + x_b (q * scale)^T.
+        x: CUDA tensor [M][in_features] f16/f32 -> [M][out_features] (f16 default).
+        Asynchronous on the current stream (C ABI quik_linear_forward_weight_only)."""
+        torch = _torch()
+        if x.dim() != 2 or x.shape[1] != self.in_features:
+            raise ValueError(f"weight_only_forward: input has {x.shape[-1]} features, layer expects {self.in_features}")
+        if x.dtype not in (torch.float16, torch.float32):
+            raise ValueError("weight_only_forward: input must be float16 or float32")
+        x = x.contiguous()
+        M = x.shape[0]
+        if out is None:
+            out = torch.empty((M, self.out_features), dtype=out_dtype or torch.float16, device=x.device)
+        if out.stride(1) != 1 or out.stride(0) < self.out_features:
+            raise ValueError("output must be row-major with pitch >= out_features")
+        ydt = _lib.QUIK_F16 if out.dtype == torch.float16 else _lib.QUIK_F32
+        xdt = _lib.QUIK_F16 if x.dtype == torch.float16 else _lib.QUIK_F32
+        _lib.check(self._lib.quik_linear_forward_weight_only(
+            self.ctx.handle, self.handle, _ptr(x), xdt, M, _ptr(out), ydt, out.stride(0),
+            C.c_void_p(_stream_ptr(torch, x.device))))
+        return out
 
     def quantize_gemm_layout(self, x):
         """Diagnostics: K1 as the hot path runs it (C ABI quik_quantize_activations_gemm).

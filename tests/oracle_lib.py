@@ -148,8 +148,16 @@ class Oracle(_Base):
                       None if bias is None else bias.ctypes.data)
         x = np.ascontiguousarray(x, np.float32)
         out = np.zeros((x.shape[0], L["out_features"]), np.float32)
-        st = self.lib.qo_quik_matmul(C.byref(lay), _p(x), C.c_int64(x.shape[0]), variant, _p(out))
+        fn = self.lib.qo_weight_only_forward if variant == "weight_only" else None
+        if fn is not None:
+            st = fn(C.byref(lay), _p(x), C.c_int64(x.shape[0]), _p(out))
+        else:
+            st = self.lib.qo_quik_matmul(C.byref(lay), _p(x), C.c_int64(x.shape[0]), variant, _p(out))
         return st, out
+
+    def weight_only(self, L, x):
+        """runtime.cpp:115-136 (LayerMode::WeightOnly) restated in C."""
+        return self.quik_matmul(L, x, variant="weight_only")
 
 
 class Ref(_Base):
@@ -199,6 +207,14 @@ class Ref(_Base):
         st = self.f("quik_matmul")(*args, _p(x), C.c_int64(x.shape[0]), variant, _p(out), _p(t))
         if times is not None:
             times[:] = t
+        return st, out
+
+    def weight_only(self, L, x):
+        """The reference's quik_matmul with layer.mode = LayerMode::WeightOnly."""
+        keep, args = self._layer_args(L)
+        x = np.ascontiguousarray(x, np.float32)
+        out = np.zeros((x.shape[0], L["out_features"]), np.float32)
+        st = self.f("weight_only")(*args, _p(x), C.c_int64(x.shape[0]), _p(out))
         return st, out
 
     def layer_create(self, L):
@@ -312,3 +328,29 @@ def make_layer(rng: np.random.Generator, tokens, in_f, out_f, bits, n_outliers, 
     L = dict(in_features=in_f, out_features=out_f, bits=bits, act_bits=bits, base=q["base"], scales=q["scales"],
              wreduced=q["wreduced"], outlier_weights=ow, idx=idx, bias=bias)
     return L, x, w
+
+
+def weight_only_f64(L, x, checker=None):
+    """The reference test's FP64 oracle for LayerMode::WeightOnly (test_runtime.cpp:
+    284-300): x times the de-permuted dequantized weights (q * scale in the base
+    columns, the outlier weights in theirs) plus bias, in float64."""
+    chk = checker or oracle()
+    K, N = L["in_features"], L["out_features"]
+    idx = np.asarray(L["idx"], np.int64)
+    kb = K - idx.size
+    st, perm = chk.permutation(K, idx)
+    assert st == 0, st
+    q = chk.unpack(L["base"], N, kb, L["bits"]).astype(np.float64)
+    w = np.zeros((N, K), np.float64)
+    w[:, perm[:kb]] = q * np.asarray(L["scales"], np.float64)[:, None]
+    if idx.size:
+        w[:, idx] = np.asarray(L["outlier_weights"], np.float64)
+    y = np.asarray(x, np.float64) @ w.T
+    if L.get("bias") is not None:
+        y += np.asarray(L["bias"], np.float64)[None, :]
+    return y
+
+
+def rel_frobenius(ref_, out):
+    ref_ = np.asarray(ref_, np.float64)
+    return float(np.linalg.norm(np.asarray(out, np.float64) - ref_) / max(np.linalg.norm(ref_), 1e-300))

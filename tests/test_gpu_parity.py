@@ -844,3 +844,93 @@ def test_gated_projection_every_tile(tile, cg, bn):
     assert tile(cg, bn) == 0
     got = proj(xt, out_dtype=torch.float32).cpu().numpy()
     np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+# --------------------------------------------------------------------------- weight-only (§8f.3)
+
+
+def _wo_bound(L, x, K_eff):
+    """Per-element error bound of the weight-only kernel vs FP64: exact products, the
+    f32 hi/lo split residuals (2^-22 relative) and an f32 summation over K terms
+    (gamma_K = K 2^-24), all relative to S = sum_k |x_k| |w_k| (+ |bias|)."""
+    from oracle_lib import oracle as _o
+
+    chk = _o()
+    K, N = L["in_features"], L["out_features"]
+    idx = np.asarray(L["idx"], np.int64)
+    kb = K - idx.size
+    st, perm = chk.permutation(K, idx)
+    qv = np.abs(chk.unpack(L["base"], N, kb, L["bits"]).astype(np.float64))
+    w = np.zeros((N, K), np.float64)
+    w[:, perm[:kb]] = qv * np.abs(np.asarray(L["scales"], np.float64))[:, None]
+    if idx.size:
+        w[:, idx] = np.abs(np.asarray(L["outlier_weights"], np.float64))
+    S = np.abs(np.asarray(x, np.float64)) @ w.T
+    if L.get("bias") is not None:
+        S += np.abs(np.asarray(L["bias"], np.float64))[None, :]
+    return (K_eff * 2.0 ** -24 + 2.0 ** -20) * S
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+def test_weight_only_matches_reference(bits):
+    """LayerMode::WeightOnly (runtime.cpp:115-136) on the device: f32 activations (two
+    f16 planes) -> f32 out meets the reference test's bar (rel Frobenius < 1e-6 vs FP64,
+    test_runtime.cpp:284-300) and a per-element bound; f16 activations -> f16 out within
+    half an f16 ulp + the same bound. Shapes cover the direct-store path (one split),
+    split-K + finalize, ragged N / K, O = 0, no bias, and M up to 300."""
+    from oracle_lib import rel_frobenius, weight_only_f64
+
+    m = q()
+    import torch
+
+    rng = np.random.default_rng(4100 + bits)
+    cases = [(1, 4096, 4096, 64), (7, 64, 24, 8), (16, 3000, 1000, 128), (33, 640, 2048, 0), (5, 1024, 300, 16),
+             (300, 2048, 512, 32), (1024, 512, 4096, 64), (2, 200, 129, 4)]
+    for (M, K, N, O) in cases:
+        L, x, _ = make_layer(rng, M, K, N, bits, O, heavy_cols=2, with_bias=(M % 2 == 1), fp16_inputs=False)
+        dev = m.QuikLinear(to_layer(L))
+        # f32 in -> f32 out
+        y = dev.weight_only(torch.from_numpy(x).cuda(), out_dtype=torch.float32).cpu().numpy()
+        want = weight_only_f64(L, x)
+        assert rel_frobenius(want, y) < 1e-6, (M, K, N, O)
+        assert np.all(np.abs(y - want) <= _wo_bound(L, x, K) + 1e-30), (M, K, N, O)
+        # f16 in -> f16 out (the decode hot path)
+        x16 = x.astype(np.float16)
+        y16 = dev.weight_only(torch.from_numpy(x16).cuda()).cpu().numpy().astype(np.float64)
+        want16 = weight_only_f64(L, x16.astype(np.float32))
+        tol = F16_REL * np.abs(want16) + _wo_bound(L, x16.astype(np.float32), K) * 2 + 6.0e-8
+        assert np.all(np.abs(y16 - want16) <= tol), (M, K, N, O)
+        # deterministic (fixed-order split reduction)
+        y2 = dev.weight_only(torch.from_numpy(x).cuda(), out_dtype=torch.float32).cpu().numpy()
+        np.testing.assert_array_equal(y.view(np.uint32), y2.view(np.uint32))
+
+
+def test_weight_only_keeps_activations_in_fp():
+    """test_runtime.cpp:284-300 on the device: weight-only vs FP64 of the dequantized
+    weights < 1e-6, and its error vs the FP product is no larger than quik mode's."""
+    from oracle_lib import rel_frobenius, weight_only_f64
+
+    m = q()
+    import torch
+
+    rng = np.random.default_rng(137)
+    L, x, w = make_layer(rng, 7, 64, 24, 4, 8, heavy_cols=2, fp16_inputs=False)
+    dev = m.QuikLinear(to_layer(L))
+    xt = torch.from_numpy(x).cuda()
+    out = dev.weight_only(xt, out_dtype=torch.float32).cpu().numpy()
+    assert rel_frobenius(weight_only_f64(L, x), out) < 1e-6
+    fp_ref = x.astype(np.float64) @ w.astype(np.float64).T + L["bias"].astype(np.float64)[None, :]
+    quik_out = dev(xt, out_dtype=torch.float32).cpu().numpy()
+    assert rel_frobenius(fp_ref, out) <= rel_frobenius(fp_ref, quik_out)
+
+
+def test_weight_only_rejects_gated_and_compressed_layers():
+    m = q()
+    import torch
+
+    rng = np.random.default_rng(9)
+    up, x, _ = make_layer(rng, 4, 256, 64, 4, 16)
+    gate = dict(up)
+    g = m.QuikLinear.gated(to_layer(up), to_layer(gate))
+    with pytest.raises(NotImplementedError):
+        g.weight_only(torch.from_numpy(x).cuda())
