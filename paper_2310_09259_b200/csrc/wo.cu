@@ -47,7 +47,6 @@ namespace quikb200 {
 
 namespace {
 
-constexpr int kWThreads = 512;
 constexpr int kWABytes = kBlockM * kKBlockBytes;  // 16 KB: packed weight tile or one f16 outlier tile
 constexpr int kWTmemA = 128;                        // columns per TMEM A buffer (256 K as f16x2)
 
@@ -60,18 +59,27 @@ struct WCfg {
   // even stage count gives every stage a single group) and outlier stages (warp 1).
   static constexpr int kSlotB = kWABytes + 4 * kBAtom;
   static constexpr int kSlotO = kWABytes + kBAtom;
-  static constexpr int kStagesB = BN == 16 ? 6 : 4;
+  static constexpr int kStagesB = BN == 16 ? 6 : 4;  // multiple of the group count
   static constexpr int kStagesO = 4;
   static_assert(kStagesB % 2 == 0, "base stages alternate between the two widening groups");
   static constexpr int kRingBytes = kStagesB * kSlotB + kStagesO * kSlotO;
-  static constexpr int kBarBytes = (2 * kStagesB + 2 * kStagesO + 8) * 8 + 16;
+  static constexpr int kBarBytes = (2 * kStagesB + 2 * kStagesO + 10) * 8 + 16;
   static constexpr int kSmemBytes = 1024 + kRingBytes + kBarBytes;
   static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
   static constexpr int kAccCol = 2 * kWTmemA;  // accumulators after the two A buffers
   // per unit buffer: base (widening group 0), base (group 1), outliers: 3 x BN columns,
   // double-buffered
-  static constexpr int kAccBuf = 3 * BN;
-  static_assert(kAccCol + 2 * kAccBuf <= 512, "TMEM budget");
+  // G widening groups (each 4 warps, one TMEM A buffer of 128 columns, one issuing warp
+  // and one base accumulator): 3 when the TMEM budget allows it (BN = 16)
+  static constexpr int G = BN == 16 ? 3 : 2;
+  static constexpr int kAccColG = G * kWTmemA;
+  static constexpr int kAccBufG = (G + 1) * BN;  // G base accumulators + outliers
+  static_assert(kAccColG + 2 * kAccBufG <= 512, "TMEM budget");
+  static_assert(kStagesB % G == 0, "every base stage belongs to one widening group");
+  // warps: 0 producer, 1 outlier issuer + TMEM allocator, 2 .. 4G+1 widening, then 4
+  // epilogue warps, then G base issuers
+  static constexpr int kWidenEnd = 2 + 4 * G, kEpiEnd = kWidenEnd + 4;
+  static constexpr int kThreads = (kEpiEnd + G) * 32;
 };
 
 struct WParams {
@@ -133,8 +141,9 @@ __device__ __forceinline__ void commit_e(uint64_t* bar) {
 }
 
 template <int BN>
-__global__ void __launch_bounds__(kWThreads, 1) wo_gemm_kernel(const __grid_constant__ WParams p) {
+__global__ void __launch_bounds__(WCfg<BN>::kThreads, 1) wo_gemm_kernel(const __grid_constant__ WParams p) {
   using C = WCfg<BN>;
+  constexpr int G = C::G;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* ring_b = smem;
@@ -143,9 +152,9 @@ __global__ void __launch_bounds__(kWThreads, 1) wo_gemm_kernel(const __grid_cons
   uint64_t* empty_b = full_b + C::kStagesB;
   uint64_t* full_o = empty_b + C::kStagesB;
   uint64_t* empty_o = full_o + C::kStagesO;
-  uint64_t* a_full = empty_o + C::kStagesO;  // [2] widening group g -> base issuer g
-  uint64_t* a_empty = a_full + 2;         // [2] base issuer g -> widening group g
-  uint64_t* acc_full = a_empty + 2;       // [2] the three issuers -> epilogue
+  uint64_t* a_full = empty_o + C::kStagesO;  // [G] widening group g -> base issuer g
+  uint64_t* a_empty = a_full + 3;         // [G] base issuer g -> widening group g
+  uint64_t* acc_full = a_empty + 3;       // [2] the G + 1 issuers -> epilogue
   uint64_t* acc_empty = acc_full + 2;     // [2] epilogue -> issuers
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
@@ -166,10 +175,12 @@ __global__ void __launch_bounds__(kWThreads, 1) wo_gemm_kernel(const __grid_cons
     if (lane == 0) {
       for (int i = 0; i < C::kStagesB; ++i) { mbar_init(&full_b[i], 1); mbar_init(&empty_b[i], 1); }
       for (int i = 0; i < C::kStagesO; ++i) { mbar_init(&full_o[i], 1); mbar_init(&empty_o[i], 1); }
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < G; ++i) {
         mbar_init(&a_full[i], 4);
         mbar_init(&a_empty[i], 1);
-        mbar_init(&acc_full[i], 3);
+      }
+      for (int i = 0; i < 2; ++i) {
+        mbar_init(&acc_full[i], G + 1);
         mbar_init(&acc_empty[i], 4);
       }
       fence_mbar_init();
@@ -182,6 +193,7 @@ __global__ void __launch_bounds__(kWThreads, 1) wo_gemm_kernel(const __grid_cons
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the token planes are complete
+  asm volatile("griddepcontrol.launch_dependents;");   // let the finalize kernel launch early
 
   const int tiles_n = (p.N + kBlockM - 1) / kBlockM;
   const int num_units = tiles_n * p.tiles_t * p.splits;
@@ -233,7 +245,7 @@ __global__ void __launch_bounds__(kWThreads, 1) wo_gemm_kernel(const __grid_cons
         }
       }
     }
-  } else if (warp == 1 || warp >= 14) {
+  } else if (warp == 1 || warp >= C::kEpiEnd) {
     // MMA issuers. A single thread issues at most one small-N tcgen05.mma per ~45
     // cycles (tools/ts_rate.cu: 44.5 cycles at N = 16, 13.4 with four issuing warps),
     // and a 256-K INT4 stage is 16 K = 16 steps, so the base stages are issued by two
@@ -242,7 +254,7 @@ __global__ void __launch_bounds__(kWThreads, 1) wo_gemm_kernel(const __grid_cons
     // acc_full once per unit (count 3).
     {  // the whole warp runs the loop (converged); elected lanes issue
       constexpr uint32_t idesc = idesc_make(1u, 0u, kBlockM, BN);
-      const int role = warp == 1 ? 2 : warp - 14;  // 0/1: base group, 2: outliers
+      const int role = warp == 1 ? G : warp - C::kEpiEnd;  // < G: base group, G: outliers
       int bc = 0, oc = 0, it = 0, gi = 0;
       for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
         int nb, tb, s, i0, i1;
@@ -250,15 +262,15 @@ __global__ void __launch_bounds__(kWThreads, 1) wo_gemm_kernel(const __grid_cons
         const int b = it & 1;
         mbar_wait_sleep(&acc_empty[b], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem_base + C::kAccCol + b * C::kAccBuf + role * BN;
+        const uint32_t d = tmem_base + C::kAccColG + b * C::kAccBufG + role * BN;
         bool first = true;
         for (int i = i0; i < i1; ++i, ++gi) {
           if (i < p.nbase) {
             const int st = bc % C::kStagesB;
             uint8_t* slot = ring_b + st * C::kSlotB;
-            const int g = bc & 1;
+            const int g = bc % G, use = bc / G;
             if (role == g) {
-              mbar_wait_spin(&a_full[g], (bc >> 1) & 1);  // widened (the widening warps saw `full`)
+              mbar_wait_spin(&a_full[g], use & 1);  // widened (the widening warps saw `full`)
               tc_fence_after();
               if (p.trace && lane == 0 && blockIdx.x == 0 && gi < 256) p.trace[gi * 8 + 6] = wo_gtime();
               const uint32_t a_tm = tmem_base + g * kWTmemA;
@@ -274,7 +286,7 @@ __global__ void __launch_bounds__(kWThreads, 1) wo_gemm_kernel(const __grid_cons
             }
             ++bc;
           } else {
-            if (role == 2) {
+            if (role == G) {
               const int st = oc % C::kStagesO;
               uint8_t* slot = ring_o + st * C::kSlotO;
               mbar_wait(&full_o[st], (oc / C::kStagesO) & 1);
@@ -292,9 +304,9 @@ __global__ void __launch_bounds__(kWThreads, 1) wo_gemm_kernel(const __grid_cons
         commit_e(&acc_full[b]);
       }
     }
-  } else if (warp <= 9) {
+  } else if (warp < C::kWidenEnd) {
     // widening: thread = weight row r of the 128-row tile (TMEM lane r)
-    const int quad = warp & 3, g = (warp - 2) >> 2;
+    const int quad = warp & 3, g = (warp - 2) >> 2;  // TMEM lane quadrant = warp % 4
     const int r = quad * 32 + lane;
     const uint32_t a_tm = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + g * kWTmemA;
     int bc = 0, gi = 0;
@@ -304,10 +316,10 @@ __global__ void __launch_bounds__(kWThreads, 1) wo_gemm_kernel(const __grid_cons
       decode(u, nb, tb, s, i0, i1);
       for (int i = i0; i < i1; ++i, ++gi) {
         if (i < p.nbase) {
-          if ((bc & 1) == g) {
+          if (bc % G == g) {
             const int st = bc % C::kStagesB;
             mbar_wait_sleep(&full_b[st], (bc / C::kStagesB) & 1);
-            mbar_wait_spin(&a_empty[g], ((bc >> 1) & 1) ^ 1);
+            mbar_wait_spin(&a_empty[g], ((bc / G) & 1) ^ 1);
             tc_fence_after();
             if (tr && quad == 0 && gi < 256) p.trace[gi * 8 + 1] = wo_gtime();
             const uint8_t* wrow = ring_b + st * C::kSlotB + r * kKBlockBytes;
@@ -373,8 +385,8 @@ __global__ void __launch_bounds__(kWThreads, 1) wo_gemm_kernel(const __grid_cons
       decode(u, nb, tb, s, i0, i1);
       // accumulators written in this unit: base issuer g iff one of its stages is here
       const int nbi = nbase_in(i0, i1);
-      const bool used0 = nbi >= 2 || (nbi == 1 && (bc0 & 1) == 0);
-      const bool used1 = nbi >= 2 || (nbi == 1 && (bc0 & 1) == 1);
+      uint32_t used = 0;  // bit g: base issuer g has a stage in this unit
+      for (int k = 0; k < nbi && k < G; ++k) used |= 1u << ((bc0 + k) % G);
       const bool has_out = i1 > p.nbase;
       bc0 += nbi;
       const int b = it & 1;
@@ -384,21 +396,39 @@ __global__ void __launch_bounds__(kWThreads, 1) wo_gemm_kernel(const __grid_cons
       const float bi = (nok && s == 0 && p.bias) ? __ldg(p.bias + n) : 0.0f;
       mbar_wait_sleep(&acc_full[b], (it >> 1) & 1);
       tc_fence_after();
-      const uint32_t tacc = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + C::kAccCol + b * C::kAccBuf;
+      const uint32_t tacc = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + C::kAccColG + b * C::kAccBufG;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
-        uint32_t v0[32], v1[32], vo[32];
+        float vb[32], vo[32];
         if constexpr (BN == 16) {
-          tmem_ld32(tacc, v0);  // base 0 in columns 0-15, base 1 in 16-31
-          tmem_ld32(tacc + 32, vo);  // outliers in 32-47
+          // G = 3: base 0-2 in columns 0-47, outliers in 48-63
+          uint32_t x0[32], x1[32];
+          tmem_ld32(tacc, x0);
+          tmem_ld32(tacc + 32, x1);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) v1[j] = v0[16 + j];
+          for (int j = 0; j < 16; ++j) {
+            float a = 0.0f;
+            if (used & 1u) a = __uint_as_float(x0[j]);
+            if (used & 2u) a = __fadd_rn(a, __uint_as_float(x0[16 + j]));
+            if (used & 4u) a = __fadd_rn(a, __uint_as_float(x1[j]));
+            vb[j] = a;
+            vo[j] = __uint_as_float(x1[16 + j]);
+          }
         } else {
-          tmem_ld32(tacc + c, v0);
-          tmem_ld32(tacc + BN + c, v1);
-          tmem_ld32(tacc + 2 * BN + c, vo);
+          uint32_t x0[32], x1[32], xo[32];
+          tmem_ld32(tacc + c, x0);
+          tmem_ld32(tacc + BN + c, x1);
+          tmem_ld32(tacc + 2 * BN + c, xo);
           tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float a = 0.0f;
+            if (used & 1u) a = __uint_as_float(x0[j]);
+            if (used & 2u) a = __fadd_rn(a, __uint_as_float(x1[j]));
+            vb[j] = a;
+            vo[j] = __uint_as_float(xo[j]);
+          }
         }
         if (nok) {
 #pragma unroll
@@ -406,11 +436,8 @@ __global__ void __launch_bounds__(kWThreads, 1) wo_gemm_kernel(const __grid_cons
             const int t = tb * BN + c + j;
             if (t < p.R) {
               float v = t < p.M ? bi : 0.0f;  // bias once: hi plane, first split
-              if (has_out) v = __fadd_rn(v, __uint_as_float(vo[j]));
-              const float base = used0 ? (used1 ? __fadd_rn(__uint_as_float(v0[j]), __uint_as_float(v1[j]))
-                                                : __uint_as_float(v0[j]))
-                                       : (used1 ? __uint_as_float(v1[j]) : 0.0f);
-              if (used0 || used1) v = __fmaf_rn(sc, base, v);
+              if (has_out) v = __fadd_rn(v, vo[j]);
+              if (used) v = __fmaf_rn(sc, vb[j], v);
               if (p.mode == 0)
                 static_cast<float*>(p.out)[(static_cast<long long>(s) * p.R + t) * p.N + n] = v;
               else if (p.mode == 1)
@@ -438,6 +465,9 @@ __global__ void __launch_bounds__(kWThreads, 1) wo_gemm_kernel(const __grid_cons
 // token planes: x -> xb f16 [P*M][kpad] (base columns in permutation order, zero
 // padded) and xo f16 [P*M][opad]; P = 2 for f32 input (hi, lo planes)
 __global__ void wo_planes_kernel(const WoArgs a, __half* __restrict__ xb, __half* __restrict__ xo, int planes) {
+  // the GEMM (launched with programmatic serialisation) may start its prologue now; it
+  // waits for this grid's completion before reading the planes
+  asm volatile("griddepcontrol.launch_dependents;");
   const int64_t width = a.kpad + a.opad;
   for (int64_t t = blockIdx.y; t < a.M; t += gridDim.y)
   for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < width;
@@ -462,6 +492,7 @@ __global__ void wo_planes_kernel(const WoArgs a, __half* __restrict__ xb, __half
 
 __global__ void wo_finalize_kernel(const float* __restrict__ ws, int64_t M, int64_t N, int splits, int planes,
                                    void* y, int y_f16, int64_t ldy) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the GEMM's partials are complete
   const int64_t total = M * N;
   const int64_t R = M * planes;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
@@ -508,8 +539,16 @@ WoPlan plan(const WoArgs& a, int num_sms) {
   pl.nout = static_cast<int>(2 * (a.opad / 64));
   const int items = pl.nbase + pl.nout;
   const long long tiles = ((a.N + kBlockM - 1) / kBlockM) * static_cast<long long>(pl.tiles_t);
+  // K splits: minimise the busiest CTA's stage count, ceil(units / SMs) x (stages per
+  // unit + 1 for the unit's pipeline fill / epilogue); e.g. LLaMA-2-70B up (224 tiles x
+  // 39 stages): 3 splits -> 5 x 14 instead of 2 splits -> 4 x 21
   int splits = 1;
-  while (tiles * splits < 2LL * num_sms && items / (splits * 2) >= 2) splits *= 2;
+  long long best = -1;
+  for (int sp = 1; sp <= 16 && sp <= items; ++sp) {
+    const long long waves = (tiles * sp + num_sms - 1) / num_sms;
+    const long long cost = waves * ((items + sp - 1) / sp + 1);
+    if (best < 0 || cost < best) { best = cost; splits = sp; }
+  }
   pl.splits = splits;
   return pl;
 }
@@ -522,7 +561,7 @@ cudaError_t launch_wo_t(const WParams& wp, int units, int num_sms, cudaStream_t 
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(units < num_sms ? units : num_sms));
-  cfg.blockDim = dim3(kWThreads);
+  cfg.blockDim = dim3(C::kThreads);
   cfg.dynamicSmemBytes = C::kSmemBytes;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -614,8 +653,17 @@ cudaError_t launch_weight_only(const WoArgs& a, int num_sms, cudaStream_t stream
   if (e != cudaSuccess || direct) return e;
   const int64_t total = a.M * a.N;
   const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 4 * num_sms));
-  wo_finalize_kernel<<<blocks, 256, 0, stream>>>(a.ws, a.M, a.N, pl.splits, pl.planes, a.y, a.y_is_f16, a.ldy);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(256);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, wo_finalize_kernel, static_cast<const float*>(a.ws), a.M, a.N, pl.splits,
+                            pl.planes, a.y, a.y_is_f16, a.ldy);
 }
 
 cudaError_t launch_f16_lo_padded(const float* src, int64_t rows, int64_t cols, __half* dst, int64_t pitch,

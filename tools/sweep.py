@@ -96,14 +96,21 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--only", default="")
+    ap.add_argument("--stream", default="", help="'int8' / 'int4': split-K weight-streaming GEMM for M <= 64")
+    ap.add_argument("--opt-m", default="", help="comma list of OPT fc1 token counts (default: all)")
     args = ap.parse_args()
+    if args.stream:
+        q._lib.check(q.load_library().quik_set_stream_gemm(1, 1 if args.stream == "int4" else 0))
     layers = {}
     res = []
     for s in SHAPES:
         if args.only and args.only not in s[0]:
             continue
         res.append(run(*s[:6], layers, *s[6:]))
-    for m, K, N, O, bits in ([] if args.only else OPT_FC1[::3] if args.quick else OPT_FC1):
+    opt = OPT_FC1[::3] if args.quick else OPT_FC1
+    if args.opt_m:
+        opt = [o for o in OPT_FC1 if str(o[0]) in args.opt_m.split(",")]
+    for m, K, N, O, bits in ([] if args.only and not args.opt_m else opt):
         res.append(run(f"cfg4 OPT-66B fc1 M={m}", m, K, N, O, bits, layers))
     for r in res:
         print(json.dumps(r), flush=True)
