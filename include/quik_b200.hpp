@@ -212,12 +212,18 @@ struct QuantizedWeights {
 
 enum class PipelineVariant { V1Unfused, V2FusedQuant, V3FusedEpilogue };  // runtime.hpp:31
 
-// runtime.hpp:33-44 (LayerMode::Quik)
+// runtime.hpp:25. Quik: the W4A4/W8A8 hot path; WeightOnly: activations stay FP
+// (quik_linear_forward_weight_only); FpReference needs the original FP weights, which
+// the device layer does not hold (std::invalid_argument, as the reference without them).
+enum class LayerMode { Quik, WeightOnly, FpReference };
+
+// runtime.hpp:33-44
 struct QuikLinearLayer {
   QuantizedWeights weights;
   OutlierSet outliers;
   std::vector<float> bias;
   int act_bits = 4;
+  LayerMode mode = LayerMode::Quik;
   int64_t in_features() const { return outliers.feature_count; }
   int64_t out_features() const { return weights.out_features(); }
   void validate() const {  // runtime.cpp:150-167
@@ -228,7 +234,7 @@ struct QuikLinearLayer {
       throw std::invalid_argument("layer: base column count mismatch");
     if (!bias.empty() && static_cast<int64_t>(bias.size()) != out_features())
       throw std::invalid_argument("layer: bias length != out_features");
-    if (act_bits != weights.bits())
+    if (mode == LayerMode::Quik && act_bits != weights.bits())
       throw std::invalid_argument("layer: activation bits must match weight bits in quik mode");
     if (act_bits != 4 && act_bits != 8) throw std::invalid_argument("activation bits must be 4 or 8");
   }
@@ -258,11 +264,14 @@ class DeviceLayer {
  public:
   explicit DeviceLayer(const QuikLinearLayer& L, int64_t row_begin = 0, int64_t row_end = 0) {
     L.validate();
+    if (L.mode == LayerMode::FpReference)
+      throw std::invalid_argument("FpReference mode requires the original FP weights");
+    mode_ = L.mode;
     quik_weights_desc d{};
     d.in_features = L.in_features();
     d.out_features = L.out_features();
     d.bits = L.weights.bits();
-    d.act_bits = L.act_bits;
+    d.act_bits = L.mode == LayerMode::WeightOnly ? L.weights.bits() : L.act_bits;  // unused in weight-only mode
     d.base = L.weights.base.data.data();
     d.scales = L.weights.scales.data();
     d.wreduced = L.weights.wreduced.data();
@@ -294,6 +303,14 @@ class DeviceLayer {
                                   std::to_string(in_));
     FpMatrix y(x.rows, out_);
     if (x.rows == 0 || out_ == 0) return y;
+    if (mode_ == LayerMode::WeightOnly) {  // runtime.cpp:255 -> weight_only_forward
+      detail::Buf dx(x.data.data(), x.data.size() * 4), dy(y.data.size() * 4);
+      detail::check(quik_linear_forward_weight_only(detail::ctx(), h_, dx.p, QUIK_F32, x.rows, dy.p, QUIK_F32, out_,
+                                                    nullptr));
+      detail::check(quik_ctx_sync(detail::ctx(), nullptr));
+      dy.get(y.data.data(), y.data.size() * 4);
+      return y;
+    }
     if (v == PipelineVariant::V3FusedEpilogue && !times) {
       // host buffers straight through the chunked copy/compute pipeline
       detail::check(quik_linear_forward_host(detail::ctx(), h_, x.data.data(), QUIK_F32, x.rows, y.data.data(),
@@ -327,6 +344,7 @@ class DeviceLayer {
  private:
   quik_layer_t h_ = nullptr;
   int64_t in_ = 0, out_ = 0;
+  LayerMode mode_ = LayerMode::Quik;
 };
 
 // ---------------------------------------------------------------- reference functions

@@ -171,6 +171,46 @@ int main(int argc, char** argv) {
       }
     }
   }
+  // LayerMode::WeightOnly (test_runtime.cpp:284-300): FP32 activations, device result
+  // vs the C restatement of weight_only_forward (itself pinned to the reference)
+  {
+    std::mt19937 rng(137);
+    std::normal_distribution<float> nd(0.f, 1.f);
+    for (int trial = 0; trial < 4; ++trial) {
+      const int bits = trial % 2 == 0 ? 4 : 8;
+      const int64_t M = 7 + 9 * trial, K = 64 + 96 * trial, N = 24 + 40 * trial, O = (trial % 2) * 8;
+      Q::FpMatrix x(M, K), w(N, K);
+      for (float& v : x.data) v = nd(rng);
+      for (float& v : w.data) v = 0.5f * nd(rng);
+      std::vector<int64_t> idx(O);
+      qo_select_outliers(x.data.data(), M, K, O, idx.data());
+      Q::QuikLinearLayer L;
+      L.outliers = Q::OutlierSet::from_indices(K, idx);
+      L.weights = Q::rtn_quantize_weights(w, L.outliers, bits);
+      L.act_bits = bits == 4 ? 8 : 4;  // need not match the weights in this mode (runtime.cpp:163)
+      L.bias.assign(N, -0.5f);
+      L.mode = Q::LayerMode::WeightOnly;
+      const auto y = Q::quik_matmul(L, x);
+      qo_layer ql{K, N, O, bits, bits, L.weights.base.data.data(), L.weights.scales.data(), L.weights.wreduced.data(),
+                  L.weights.outlier_weights.data.data(), L.outliers.indices.data(), L.bias.data()};
+      std::vector<float> want(M * N);
+      CHECK(qo_weight_only_forward(&ql, x.data.data(), M, want.data()) == QO_OK);
+      double d2 = 0, r2 = 0;
+      for (size_t i = 0; i < want.size(); ++i) {
+        d2 += (double(y.data[i]) - want[i]) * (double(y.data[i]) - want[i]);
+        r2 += double(want[i]) * want[i];
+      }
+      CHECK(std::sqrt(d2 / r2) < 1e-6);
+    }
+    Q::QuikLinearLayer R;
+    R.outliers = Q::OutlierSet::from_indices(8, {});
+    R.weights.base = Q::pack_int4(std::vector<int8_t>(16, 0), 2, 8);
+    R.weights.scales = {1.f, 1.f};
+    R.weights.wreduced = {0.f, 0.f};
+    R.weights.outlier_weights = Q::FpMatrix(2, 0);
+    R.mode = Q::LayerMode::FpReference;
+    CHECK(throws<std::invalid_argument>([&] { Q::quik_matmul(R, Q::FpMatrix(1, 8)); }));
+  }
   // validation (runtime.cpp:150-167)
   {
     Q::QuikLinearLayer L;
