@@ -53,33 +53,35 @@ constexpr int kWTmemA = 128;                        // columns per TMEM A buffer
 template <int BN>
 struct WCfg {
   static constexpr int kBAtom = BN * kKBlockBytes;  // BN plane rows x 64 f16
-  // Two rings, each with exactly one consumer sequence per stage (a consumer that skips
-  // other consumers' items could otherwise run a whole ring cycle ahead and alias an
-  // mbarrier phase): base stages (consumed alternately by widening groups 0 / 1, so an
-  // even stage count gives every stage a single group) and outlier stages (warp 1).
-  static constexpr int kSlotB = kWABytes + 4 * kBAtom;
-  static constexpr int kSlotO = kWABytes + kBAtom;
-  static constexpr int kStagesB = BN == 16 ? 6 : 4;  // multiple of the group count
-  static constexpr int kStagesO = 4;
-  static_assert(kStagesB % 2 == 0, "base stages alternate between the two widening groups");
-  static constexpr int kRingBytes = kStagesB * kSlotB + kStagesO * kSlotO;
-  static constexpr int kBarBytes = (2 * kStagesB + 2 * kStagesO + 10) * 8 + 16;
-  static constexpr int kSmemBytes = 1024 + kRingBytes + kBarBytes;
-  static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
-  static constexpr int kAccCol = 2 * kWTmemA;  // accumulators after the two A buffers
-  // per unit buffer: base (widening group 0), base (group 1), outliers: 3 x BN columns,
-  // double-buffered
   // G widening groups (each 4 warps, one TMEM A buffer of 128 columns, one issuing warp
   // and one base accumulator): 3 when the TMEM budget allows it (BN = 16)
   static constexpr int G = BN == 16 ? 3 : 2;
+  // Three rings, each stage with exactly one consumer sequence (a consumer that skips
+  // other consumers' items could otherwise run a whole ring cycle ahead and alias an
+  // mbarrier phase):
+  //  * weight tiles (16 KB, consumed by widening group bc % G, released as soon as the
+  //    group has widened them: the MMAs read A from TMEM) - deep, it covers HBM latency;
+  //  * token tiles of the base stages (L2-resident, consumed by base issuer bc % G);
+  //  * outlier stages (f16 weight tile + token tile, consumed by warp 1).
+  static constexpr int kSlotW = kWABytes;
+  static constexpr int kSlotT = 4 * kBAtom;
+  static constexpr int kSlotO = kWABytes + kBAtom;
+  static constexpr int kStagesW = BN == 16 ? 9 : 6;
+  static constexpr int kStagesT = BN == 16 ? 3 : 4;
+  static constexpr int kStagesO = BN == 16 ? 3 : 2;
+  static_assert(kStagesW % G == 0 && kStagesT % G == 0, "every base stage belongs to one group / issuer");
+  static constexpr int kOffT = kStagesW * kSlotW, kOffO = kOffT + kStagesT * kSlotT;
+  static constexpr int kRingBytes = kOffO + kStagesO * kSlotO;
+  static constexpr int kBarBytes = (2 * (kStagesW + kStagesT + kStagesO) + 2 * G + 4) * 8 + 16;
+  static constexpr int kSmemBytes = 1024 + kRingBytes + kBarBytes;
+  static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
   static constexpr int kAccColG = G * kWTmemA;
-  static constexpr int kAccBufG = (G + 1) * BN;  // G base accumulators + outliers
+  static constexpr int kAccBufG = (G + 1) * BN;  // G base accumulators + outliers, double-buffered
   static_assert(kAccColG + 2 * kAccBufG <= 512, "TMEM budget");
-  static_assert(kStagesB % G == 0, "every base stage belongs to one widening group");
-  // warps: 0 producer, 1 outlier issuer + TMEM allocator, 2 .. 4G+1 widening, then 4
-  // epilogue warps, then G base issuers
-  static constexpr int kWidenEnd = 2 + 4 * G, kEpiEnd = kWidenEnd + 4;
-  static constexpr int kThreads = (kEpiEnd + G) * 32;
+  // warps: 0 weight producer, 1 outlier issuer + TMEM allocator, 2 .. 4G+1 widening, 4
+  // epilogue warps, G base issuers, 1 token / outlier producer
+  static constexpr int kWidenEnd = 2 + 4 * G, kEpiEnd = kWidenEnd + 4, kIssEnd = kEpiEnd + G;
+  static constexpr int kThreads = (kIssEnd + 1) * 32;
 };
 
 struct WParams {
@@ -146,11 +148,14 @@ __global__ void __launch_bounds__(WCfg<BN>::kThreads, 1) wo_gemm_kernel(const __
   constexpr int G = C::G;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* ring_b = smem;
-  uint8_t* ring_o = smem + C::kStagesB * C::kSlotB;
-  uint64_t* full_b = reinterpret_cast<uint64_t*>(smem + C::kRingBytes);
-  uint64_t* empty_b = full_b + C::kStagesB;
-  uint64_t* full_o = empty_b + C::kStagesB;
+  uint8_t* ring_w = smem;
+  uint8_t* ring_t = smem + C::kOffT;
+  uint8_t* ring_o = smem + C::kOffO;
+  uint64_t* full_w = reinterpret_cast<uint64_t*>(smem + C::kRingBytes);
+  uint64_t* empty_w = full_w + C::kStagesW;
+  uint64_t* full_t = empty_w + C::kStagesW;
+  uint64_t* empty_t = full_t + C::kStagesT;
+  uint64_t* full_o = empty_t + C::kStagesT;
   uint64_t* empty_o = full_o + C::kStagesO;
   uint64_t* a_full = empty_o + C::kStagesO;  // [G] widening group g -> base issuer g
   uint64_t* a_empty = a_full + 3;         // [G] base issuer g -> widening group g
@@ -173,7 +178,8 @@ __global__ void __launch_bounds__(WCfg<BN>::kThreads, 1) wo_gemm_kernel(const __
   }
   if (warp == 1) {
     if (lane == 0) {
-      for (int i = 0; i < C::kStagesB; ++i) { mbar_init(&full_b[i], 1); mbar_init(&empty_b[i], 1); }
+      for (int i = 0; i < C::kStagesW; ++i) { mbar_init(&full_w[i], 1); mbar_init(&empty_w[i], 4); }
+      for (int i = 0; i < C::kStagesT; ++i) { mbar_init(&full_t[i], 1); mbar_init(&empty_t[i], 1); }
       for (int i = 0; i < C::kStagesO; ++i) { mbar_init(&full_o[i], 1); mbar_init(&empty_o[i], 1); }
       for (int i = 0; i < G; ++i) {
         mbar_init(&a_full[i], 4);
@@ -211,41 +217,51 @@ __global__ void __launch_bounds__(WCfg<BN>::kThreads, 1) wo_gemm_kernel(const __
   };
   auto nbase_in = [&](int i0, int i1) { return max(0, min(i1, p.nbase) - i0); };
 
-  if (warp == 0) {
+  if (warp == 0 || warp == C::kIssEnd) {
     if (lane == 0) {
-      // weights stream once per token tile (decode: once)
+      // weights stream once per token tile (decode: once); token planes are re-read by
+      // every weight block
       const uint64_t pol_w = p.tiles_t == 1 ? policy_evict_first() : policy_evict_normal();
-      const uint64_t pol_x = policy_evict_last();   // token planes are re-read by every block
+      const uint64_t pol_x = policy_evict_last();
+      const bool wprod = warp == 0;  // warp 0: weight ring; last warp: token + outlier rings
       int bc = 0, oc = 0, gi = 0;
       for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
         int nb, tb, s, i0, i1;
         decode(u, nb, tb, s, i0, i1);
         for (int i = i0; i < i1; ++i, ++gi) {
           if (i < p.nbase) {
-            const int st = bc % C::kStagesB;
-            mbar_wait_sleep(&empty_b[st], ((bc / C::kStagesB) & 1) ^ 1);
-            if (p.trace && blockIdx.x == 0 && gi < 256) p.trace[gi * 8 + 0] = wo_gtime();
-            uint8_t* slot = ring_b + st * C::kSlotB;
-            mbar_arrive_expect_tx(&full_b[st], kWABytes + natoms * C::kBAtom);
-            tma_load_2d(slot, &p.tm_w, i * kKBlockBytes, nb * kBlockM, &full_b[st], pol_w);
-            for (int a = 0; a < natoms; ++a)
-              tma_load_2d(slot + kWABytes + a * C::kBAtom, &p.tm_xb, (i * natoms + a) * kKBlockBytes, tb * BN,
-                          &full_b[st], pol_x);
+            if (wprod) {
+              const int st = bc % C::kStagesW;
+              mbar_wait_sleep(&empty_w[st], ((bc / C::kStagesW) & 1) ^ 1);
+              if (p.trace && blockIdx.x == 0 && gi < 256) p.trace[gi * 8 + 0] = wo_gtime();
+              mbar_arrive_expect_tx(&full_w[st], kWABytes);
+              tma_load_2d(ring_w + st * C::kSlotW, &p.tm_w, i * kKBlockBytes, nb * kBlockM, &full_w[st], pol_w);
+            } else {
+              const int st = bc % C::kStagesT;
+              mbar_wait_sleep(&empty_t[st], ((bc / C::kStagesT) & 1) ^ 1);
+              uint8_t* slot = ring_t + st * C::kSlotT;
+              mbar_arrive_expect_tx(&full_t[st], natoms * C::kBAtom);
+              for (int a = 0; a < natoms; ++a)
+                tma_load_2d(slot + a * C::kBAtom, &p.tm_xb, (i * natoms + a) * kKBlockBytes, tb * BN, &full_t[st],
+                            pol_x);
+            }
             ++bc;
           } else {
-            const int j = i - p.nbase, st = oc % C::kStagesO;
-            mbar_wait_sleep(&empty_o[st], ((oc / C::kStagesO) & 1) ^ 1);
-            uint8_t* slot = ring_o + st * C::kSlotO;
-            mbar_arrive_expect_tx(&full_o[st], kWABytes + C::kBAtom);
-            tma_load_2d(slot, (j & 1) ? &p.tm_wolo : &p.tm_wo, (j >> 1) * kKBlockBytes, nb * kBlockM, &full_o[st],
-                        pol_w);
-            tma_load_2d(slot + kWABytes, &p.tm_xo, (j >> 1) * kKBlockBytes, tb * BN, &full_o[st], pol_x);
+            if (!wprod) {
+              const int j = i - p.nbase, st = oc % C::kStagesO;
+              mbar_wait_sleep(&empty_o[st], ((oc / C::kStagesO) & 1) ^ 1);
+              uint8_t* slot = ring_o + st * C::kSlotO;
+              mbar_arrive_expect_tx(&full_o[st], kWABytes + C::kBAtom);
+              tma_load_2d(slot, (j & 1) ? &p.tm_wolo : &p.tm_wo, (j >> 1) * kKBlockBytes, nb * kBlockM, &full_o[st],
+                          pol_w);
+              tma_load_2d(slot + kWABytes, &p.tm_xo, (j >> 1) * kKBlockBytes, tb * BN, &full_o[st], pol_x);
+            }
             ++oc;
           }
         }
       }
     }
-  } else if (warp == 1 || warp >= C::kEpiEnd) {
+  } else if (warp == 1 || warp >= C::kEpiEnd) {  // (warp C::kIssEnd is handled above)
     // MMA issuers. A single thread issues at most one small-N tcgen05.mma per ~45
     // cycles (tools/ts_rate.cu: 44.5 cycles at N = 16, 13.4 with four issuing warps),
     // and a 256-K INT4 stage is 16 K = 16 steps, so the base stages are issued by two
@@ -266,22 +282,23 @@ __global__ void __launch_bounds__(WCfg<BN>::kThreads, 1) wo_gemm_kernel(const __
         bool first = true;
         for (int i = i0; i < i1; ++i, ++gi) {
           if (i < p.nbase) {
-            const int st = bc % C::kStagesB;
-            uint8_t* slot = ring_b + st * C::kSlotB;
+            const int st = bc % C::kStagesT;
+            uint8_t* slot = ring_t + st * C::kSlotT;
             const int g = bc % G, use = bc / G;
             if (role == g) {
-              mbar_wait_spin(&a_full[g], use & 1);  // widened (the widening warps saw `full`)
+              mbar_wait_spin(&a_full[g], use & 1);                     // A widened into TMEM
+              mbar_wait(&full_t[st], (bc / C::kStagesT) & 1);          // token tile landed
               tc_fence_after();
               if (p.trace && lane == 0 && blockIdx.x == 0 && gi < 256) p.trace[gi * 8 + 6] = wo_gtime();
               const uint32_t a_tm = tmem_base + g * kWTmemA;
               const int ksteps = natoms * 4;
-              const uint64_t bd0 = umma_desc_sw128(smem_u32(slot + kWABytes));
+              const uint64_t bd0 = umma_desc_sw128(smem_u32(slot));
               for (int j = 0; j < ksteps; ++j)
                 mma_f16_ts_e(d, a_tm + 8 * j, bd0 + (j >> 2) * (C::kBAtom >> 4) + 2 * (j & 3), idesc,
                              (first && j == 0) ? 0u : 1u);
               first = false;
               commit_e(&a_empty[g]);
-              commit_e(&empty_b[st]);
+              commit_e(&empty_t[st]);
               if (p.trace && lane == 0 && blockIdx.x == 0 && gi < 256) p.trace[gi * 8 + 7] = wo_gtime();
             }
             ++bc;
@@ -317,12 +334,12 @@ __global__ void __launch_bounds__(WCfg<BN>::kThreads, 1) wo_gemm_kernel(const __
       for (int i = i0; i < i1; ++i, ++gi) {
         if (i < p.nbase) {
           if (bc % G == g) {
-            const int st = bc % C::kStagesB;
-            mbar_wait_sleep(&full_b[st], (bc / C::kStagesB) & 1);
+            const int st = bc % C::kStagesW;
+            mbar_wait_sleep(&full_w[st], (bc / C::kStagesW) & 1);
             mbar_wait_spin(&a_empty[g], ((bc / G) & 1) ^ 1);
             tc_fence_after();
             if (tr && quad == 0 && gi < 256) p.trace[gi * 8 + 1] = wo_gtime();
-            const uint8_t* wrow = ring_b + st * C::kSlotB + r * kKBlockBytes;
+            const uint8_t* wrow = ring_w + st * C::kSlotW + r * kKBlockBytes;
             if (p.w4) {
               // chunk c (16 B) holds k = 32c + i (low nibble of byte i) and 32c + 16 + i
               // (high nibble); column = k / 2
@@ -369,7 +386,10 @@ __global__ void __launch_bounds__(WCfg<BN>::kThreads, 1) wo_gemm_kernel(const __
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&a_full[g]);
+            if (lane == 0) {
+              mbar_arrive(&empty_w[st]);  // weight tile consumed (the MMAs read TMEM)
+              mbar_arrive(&a_full[g]);
+            }
             if (tr && gi < 256) p.trace[gi * 8 + 2 + quad] = wo_gtime();
           }
           ++bc;
@@ -399,36 +419,36 @@ __global__ void __launch_bounds__(WCfg<BN>::kThreads, 1) wo_gemm_kernel(const __
       const uint32_t tacc = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + C::kAccColG + b * C::kAccBufG;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
-        float vb[32], vo[32];
+        float vb[32];
+        uint32_t vo[32];  // outlier accumulator columns (raw f32 bits)
         if constexpr (BN == 16) {
           // G = 3: base 0-2 in columns 0-47, outliers in 48-63
-          uint32_t x0[32], x1[32];
+          uint32_t x0[32];
           tmem_ld32(tacc, x0);
-          tmem_ld32(tacc + 32, x1);
+          tmem_ld32(tacc + 32, vo);
           tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             float a = 0.0f;
             if (used & 1u) a = __uint_as_float(x0[j]);
             if (used & 2u) a = __fadd_rn(a, __uint_as_float(x0[16 + j]));
-            if (used & 4u) a = __fadd_rn(a, __uint_as_float(x1[j]));
+            if (used & 4u) a = __fadd_rn(a, __uint_as_float(vo[j]));
             vb[j] = a;
-            vo[j] = __uint_as_float(x1[16 + j]);
+            vo[j] = vo[16 + j];
           }
         } else {
-          uint32_t x0[32], x1[32], xo[32];
-          tmem_ld32(tacc + c, x0);
-          tmem_ld32(tacc + BN + c, x1);
-          tmem_ld32(tacc + 2 * BN + c, xo);
+          // G = 2: one 32-column load per accumulator, summed in place
+          tmem_ld32(tacc + c, vo);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            float a = 0.0f;
-            if (used & 1u) a = __uint_as_float(x0[j]);
-            if (used & 2u) a = __fadd_rn(a, __uint_as_float(x1[j]));
-            vb[j] = a;
-            vo[j] = __uint_as_float(xo[j]);
-          }
+          for (int j = 0; j < 32; ++j) vb[j] = (used & 1u) ? __uint_as_float(vo[j]) : 0.0f;
+          tmem_ld32(tacc + BN + c, vo);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (used & 2u) vb[j] = __fadd_rn(vb[j], __uint_as_float(vo[j]));
+          tmem_ld32(tacc + 2 * BN + c, vo);
+          tmem_ld_wait();
         }
         if (nok) {
 #pragma unroll
@@ -436,7 +456,7 @@ __global__ void __launch_bounds__(WCfg<BN>::kThreads, 1) wo_gemm_kernel(const __
             const int t = tb * BN + c + j;
             if (t < p.R) {
               float v = t < p.M ? bi : 0.0f;  // bias once: hi plane, first split
-              if (has_out) v = __fadd_rn(v, vo[j]);
+              if (has_out) v = __fadd_rn(v, __uint_as_float(vo[j]));
               if (used) v = __fmaf_rn(sc, vb[j], v);
               if (p.mode == 0)
                 static_cast<float*>(p.out)[(static_cast<long long>(s) * p.R + t) * p.N + n] = v;

@@ -26,9 +26,11 @@ __device__ __forceinline__ void mma_ts_elect(uint32_t d, uint32_t a_tmem, uint64
       : "memory");
 }
 
-// whole warp converged, elect.sync per MMA (operands warp-uniform)
-template <int N>
-__global__ void __launch_bounds__(128, 1) rate_warp(int iters, unsigned long long* cycles) {
+// whole warp converged, elect.sync per MMA (operands warp-uniform). STORERS > 0: four
+// more warps keep writing TMEM (tcgen05.st, other columns) meanwhile, as the
+// weight-only kernel's widening warps do.
+template <int N, int STORERS = 0>
+__global__ void __launch_bounds__(256, 1) rate_warp(int iters, unsigned long long* cycles) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t bar;
@@ -62,6 +64,15 @@ __global__ void __launch_bounds__(128, 1) rate_warp(int iters, unsigned long lon
       if (blockIdx.x == 0) *cycles = t1 - t0;
     }
     __syncwarp();
+  } else if (STORERS && warp >= 4 && warp < 8) {
+    uint32_t r[32];
+    for (int j = 0; j < 32; ++j) r[j] = 0x3c003c00u;
+    const uint32_t ta = t + (static_cast<uint32_t>((warp & 3) * 32) << 16) + 384;
+    for (int it = 0; it < iters / 2; ++it) {
+#pragma unroll
+      for (int h = 0; h < 4; ++h) tmem_st32(ta + 32 * h, r);
+      tmem_st_wait();
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -71,19 +82,20 @@ __global__ void __launch_bounds__(128, 1) rate_warp(int iters, unsigned long lon
   }
 }
 
-template <int N>
+template <int N, int STORERS = 0>
 void run_warp(int sms) {
-  auto k = rate_warp<N>;
+  auto k = rate_warp<N, STORERS>;
   const int smem = 64 * 1024 + 1024;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   unsigned long long* dc;
   cudaMalloc(&dc, 8);
   const int iters = 2048;
-  k<<<sms, 128, smem>>>(iters, dc);
+  k<<<sms, STORERS ? 256 : 128, smem>>>(iters, dc);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long cyc = 0;
   cudaMemcpy(&cyc, dc, 8, cudaMemcpyDeviceToHost);
-  printf("kind::f16 M=128 N=%3d TS, converged warp + elect.sync: %s  %.1f cycles/MMA\n", N,
+  printf("kind::f16 M=128 N=%3d TS, converged warp + elect.sync%s: %s  %.1f cycles/MMA\n", N,
+         STORERS ? ", 4 warps storing TMEM meanwhile" : "",
          e == cudaSuccess ? "ok" : cudaGetErrorString(e), double(cyc) / (iters * 16.0));
   cudaFree(dc);
 }
@@ -170,5 +182,6 @@ int main() {
   run<16, false, 1, 2>(sms);
   run_warp<16>(sms);
   run_warp<32>(sms);
+  run_warp<16, 1>(sms);
   return 0;
 }
