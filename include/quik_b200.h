@@ -194,6 +194,18 @@ quik_status quik_linear_forward_ex(quik_ctx_t ctx, quik_layer_t layer, const voi
                                    void* y, quik_dtype y_dtype, int64_t ldy, quik_variant variant, void* stream,
                                    void* mid_event);
 
+/* Output-feature shard forward with the all-gather fused into the epilogue (SURVEY.md
+ * §8e; replaces quik_matmul + ncclAllGather for one shard): the shard layer's f16
+ * output tiles [M][shard columns] are TMA-stored at column `col_offset` of EVERY
+ * destination y_dst[0..n_dst) (row pitch ldy elements): y_dst[0] is this GPU's output,
+ * the others peer GPUs' outputs mapped into this process (cudaDeviceEnablePeerAccess
+ * or cudaIpcOpenMemHandle), so the exchange rides NVLink tile by tile while the GEMM
+ * runs. n_dst <= 8; col_offset and ldy multiples of 8. The caller orders readers
+ * after every rank's call (stream events / a barrier), as after an all-gather. */
+quik_status quik_linear_forward_sharded(quik_ctx_t ctx, quik_layer_t shard, const void* x, quik_dtype x_dtype,
+                                        int64_t M, void* const* y_dst, int n_dst, int64_t ldy, int64_t col_offset,
+                                        void* stream);
+
 /* WeightOnly mode (reference LayerMode::WeightOnly, weight_only_forward,
  * runtime.cpp:115-136): activations stay floating point,
  *   y = (bias + x_o W_o^T) + x_b (q * scale)^T

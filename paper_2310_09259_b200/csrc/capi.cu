@@ -784,7 +784,8 @@ void ensure_w4(quik_layer_s* L, cudaStream_t st, bool needed = false) {
 
 // The forward on device buffers (argument checks done by the caller).
 quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M, void* y,
-                         quik_dtype ydt, int64_t ldy, quik_variant variant, cudaStream_t st, void* mid_event) {
+                         quik_dtype ydt, int64_t ldy, quik_variant variant, cudaStream_t st, void* mid_event,
+                         void* const* peers = nullptr, int n_peer = 0) {
   if (M == 0 || L->out_features == 0) return QUIK_OK;
   const int64_t N = L->out_features;
   ensure_w4(L, st);
@@ -812,6 +813,8 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
     go.out = y;
     go.ldo = ldy;
     go.mode = ydt == QUIK_F16 ? kModeAccInitF16 : kModeAccInitF32;
+    go.peer_out = peers;
+    go.n_peer = n_peer;
     run_gemm(ctx, go, st);
     return QUIK_OK;
   }
@@ -823,6 +826,8 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
     gm.ldo = ldy;
     gm.mode = ydt == QUIK_F16 ? kModeF16 : kModeF32;
     if (g_probe_mode) gm.mode = kModeProbe;
+    gm.peer_out = peers;
+    gm.n_peer = n_peer;
     run_gemm(ctx, gm, st);
     return QUIK_OK;
   }
@@ -907,6 +912,32 @@ quik_status quik_linear_forward_ex(quik_ctx_t ctx, quik_layer_t L, const void* x
 quik_status quik_linear_forward_strided(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M,
                                         void* y, quik_dtype ydt, int64_t ldy, quik_variant variant, void* stream) {
   return quik_linear_forward_ex(ctx, L, x, xdt, M, y, ydt, ldy, variant, stream, nullptr);
+}
+
+quik_status quik_linear_forward_sharded(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M,
+                                        void* const* y_dst, int n_dst, int64_t ldy, int64_t col_offset, void* stream) {
+  if (!ctx || !L) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context or layer");
+  if (M < 0) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_matmul: negative token count");
+  if (n_dst < 1 || n_dst > 1 + kMaxPeerOut) return fail(QUIK_ERR_INVALID_ARGUMENT, "sharded forward: 1..8 destinations");
+  if (M > 0 && !x) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_matmul: null input");
+  for (int i = 0; i < n_dst; ++i)
+    if (M > 0 && !y_dst[i]) return fail(QUIK_ERR_INVALID_ARGUMENT, "sharded forward: null destination");
+  const int64_t w = L->gated ? L->out_features / 2 : L->out_features;
+  if (col_offset < 0 || col_offset + w > ldy)
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "sharded forward: shard columns exceed the output pitch");
+  if (((col_offset * 2) % 16) != 0 || ((ldy * 2) % 16) != 0)
+    return fail(QUIK_ERR_UNSUPPORTED, "sharded forward: column offset and pitch must be multiples of 8 (f16 TMA store)");
+  if (M > 0x7fffffffLL) return fail(QUIK_ERR_UNSUPPORTED, "quik_matmul: token count exceeds 2^31");
+  if (L->in_features * (xdt == QUIK_F32 ? 4 : 2) > 128 * 1024)
+    return fail(QUIK_ERR_UNSUPPORTED, "quik_matmul: row wider than 128 KiB (register-resident quantizer limit)");
+  if (ctx->device != L->device) return fail(QUIK_ERR_INVALID_ARGUMENT, "context and layer live on different devices");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    void* peers[kMaxPeerOut] = {};
+    for (int i = 1; i < n_dst; ++i) peers[i - 1] = static_cast<__half*>(y_dst[i]) + col_offset;
+    return forward_impl(ctx, L, x, xdt, M, static_cast<__half*>(y_dst[0]) + col_offset, QUIK_F16, ldy,
+                        QUIK_V3_FUSED_EPILOGUE, as_stream(stream), nullptr, peers, n_dst - 1);
+  });
 }
 
 quik_status quik_linear_forward_weight_only(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt,

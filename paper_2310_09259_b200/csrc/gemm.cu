@@ -115,6 +115,9 @@ struct KParams {
   // diagnostics (QUIK_GEMM_TRACE): per leader CTA and tile iteration (< kTraceTiles),
   // kTraceSlots globaltimer stamps; null in normal runs
   long long* trace;
+  // fused all-gather: each output tile is also stored through these maps (peer outputs)
+  int n_peer;
+  CUtensorMap tm_peer[kMaxPeerOut];
 };
 constexpr int kTraceTiles = 64;
 constexpr int kTraceSlots = 12;
@@ -583,6 +586,9 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
           __syncwarp();
           if (lane == 0) {
             tma_store_2d(&p.tm_y, buf, n0_out, mb * BN + c, pol_y);
+            // fused all-gather: the same staged tile to every peer output (NVLink P2P
+            // stores overlap the next tiles' MMAs); one bulk group covers them all
+            for (int i = 0; i < p.n_peer; ++i) tma_store_2d(&p.tm_peer[i], buf, n0_out, mb * BN + c, pol_y);
             bulk_commit();
           }
           sbuf ^= 1;
@@ -947,6 +953,20 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
     kp.tma_store = g_encode(&kp.tm_y, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.out, dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    for (int i = 0; kp.tma_store && i < a.n_peer; ++i) {
+      if (!a.peer_out[i] || (reinterpret_cast<uintptr_t>(a.peer_out[i]) & 15) != 0 ||
+          g_encode(&kp.tm_peer[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.peer_out[i], dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+        *err_msg = "peer output: null, misaligned or not encodable";
+        return cudaErrorInvalidValue;
+      }
+    }
+  }
+  kp.n_peer = a.n_peer;
+  if (a.n_peer > kMaxPeerOut || (a.n_peer > 0 && !kp.tma_store)) {
+    *err_msg = "peer outputs need an f16, 16-byte aligned output (TMA store) and at most 7 peers";
+    return cudaErrorInvalidValue;
   }
   kp.w_scale = a.w_scale;
   kp.wreduced = a.wreduced;

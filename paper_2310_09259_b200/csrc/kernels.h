@@ -73,7 +73,13 @@ struct GemmArgs {
   // gated MLP layer (rows interleave up / gate in blocks of 32): out is [M][N / 2],
   // h = silu(gate) * up (modes kModeF16 / kModeF32, no tile splitting of the pairs)
   int gated;
+  // fused all-gather: every output tile is also TMA-stored to these
+  // destinations (same [M][ldo] layout, typically peer GPUs' outputs mapped into this
+  // process), f16 TMA-store outputs only
+  void* const* peer_out;
+  int n_peer;
 };
+constexpr int kMaxPeerOut = 7;
 
 // Weight-streaming split-K integer GEMM for M <= 64 (stream.cu): adds
 // sum_k W[n][k] * X8[t][k] into the int32 workspace acc[t][n] (which must hold

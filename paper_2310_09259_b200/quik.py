@@ -445,6 +445,25 @@ class QuikLinear:
 
     __call__ = forward
 
+    def forward_sharded(self, x, outs, col_offset: int):
+        """Shard forward with the all-gather fused into the epilogue (C ABI
+        quik_linear_forward_sharded): this layer's f16 output columns land at
+        `col_offset` of every tensor in `outs` ([M][N_total] f16; outs[0] local, the
+        others e.g. peer-GPU tensors with peer access enabled)."""
+        torch = _torch()
+        x = x.contiguous()
+        M = x.shape[0]
+        ldy = outs[0].stride(0)
+        for o in outs:
+            if o.dtype != torch.float16 or o.stride(1) != 1 or o.stride(0) != ldy or o.shape[0] != M:
+                raise ValueError("sharded outputs must be row-major f16 [M][N] with one pitch")
+        arr = (C.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+        xdt = _lib.QUIK_F16 if x.dtype == torch.float16 else _lib.QUIK_F32
+        _lib.check(self._lib.quik_linear_forward_sharded(
+            self.ctx.handle, self.handle, _ptr(x), xdt, M, arr, len(outs), ldy, col_offset,
+            C.c_void_p(_stream_ptr(torch, x.device))))
+        return outs
+
     def weight_only(self, x, out=None, out_dtype=None):
         """LayerMode::WeightOnly (reference weight_only_forward, runtime.cpp:115-136):
         activations stay floating point, y = (bias + x_o W_o^T) + x_b (q * scale)^T.

@@ -934,3 +934,38 @@ def test_weight_only_rejects_gated_and_compressed_layers():
     g = m.QuikLinear.gated(to_layer(up), to_layer(gate))
     with pytest.raises(NotImplementedError):
         g.weight_only(torch.from_numpy(x).cuda())
+
+
+# --------------------------------------------------------------------------- fused all-gather (§8e)
+
+
+@pytest.mark.parametrize("M,stream", [(300, 0), (16, 0), (16, 1)])
+def test_sharded_forward_fused_all_gather(M, stream):
+    """quik_linear_forward_sharded: each output-row shard TMA-stores its tiles into
+    EVERY destination (here two buffers on one GPU standing in for the local and a
+    peer output). After both shards ran, each destination equals the unsharded forward
+    bit for bit (the per-element arithmetic does not depend on the sharding)."""
+    m = q()
+    import torch
+
+    lib = m.load_library()
+    rng = np.random.default_rng(77 + M)
+    L, x, _ = make_layer(rng, M, 1024, 768, 4, 32, heavy_cols=2)
+    layer = to_layer(L)
+    full = m.QuikLinear(layer)
+    xt = torch.from_numpy(x).cuda().half()
+    try:
+        lib.quik_set_stream_gemm(stream, 1)
+        want = full(xt)
+        ns = 768 // 3
+        shards = [m.QuikLinear(layer, row_begin=r * ns, row_end=(r + 1) * ns) for r in range(3)]
+        outs = [torch.full((M, 768), float("nan"), dtype=torch.float16, device="cuda") for _ in range(2)]
+        for r, sh in enumerate(shards):
+            sh.forward_sharded(xt, outs, r * ns)
+        torch.cuda.synchronize()
+        for o in outs:
+            assert torch.equal(o.view(torch.int16), want.view(torch.int16))
+    finally:
+        lib.quik_set_stream_gemm(0, 1)
+    with pytest.raises(NotImplementedError):  # pitch / offset not TMA-aligned
+        shards[0].forward_sharded(xt, [torch.empty((M, 770), dtype=torch.float16, device="cuda")], 3)
