@@ -788,8 +788,14 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
                          void* const* peers = nullptr, int n_peer = 0) {
   if (M == 0 || L->out_features == 0) return QUIK_OK;
   const int64_t N = L->out_features;
-  ensure_w4(L, st);
-  if (variant == QUIK_V3_FUSED_EPILOGUE && M <= 64 && L->kpad && !L->sparse && quikb200::gemm_stream && !g_probe_mode) {
+  // Decode regime (M <= 32, 4-bit layers): the INT4 split-K stream kernel (stream4.cu)
+  // reads half the weight bytes of the fused kernel's INT8 tiles and spreads small
+  // layers over every SM; default on (QUIK_STREAM4=0 disables). Needs the INT4 weight
+  // copy, made on the first such forward outside stream capture.
+  const bool small = variant == QUIK_V3_FUSED_EPILOGUE && M <= 64 && L->kpad && !L->sparse && !g_probe_mode;
+  const bool auto4 = small && quikb200::gemm_stream4_auto && L->bits == 4 && M <= 32 && !L->gated;
+  ensure_w4(L, st, auto4);
+  if ((auto4 && L->w4) || (small && quikb200::gemm_stream)) {
     // weight-streaming regime: K1 -> split-K stream GEMM into the zeroed int32
     // workspace -> the fused kernel's AccInit mode (dequant + outlier MMAs + store,
     // clears the workspace); same arithmetic as the fused V3 kernel
@@ -798,7 +804,7 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
     int32_t* ws = ctx->ensure_ws(static_cast<size_t>(M * N * 4), st);
     StreamArgs sa{};
     sa.w8 = L->w8;
-    sa.w4 = quikb200::gemm_w4_stream ? L->w4 : nullptr;
+    sa.w4 = (auto4 || quikb200::gemm_w4_stream) ? L->w4 : nullptr;
     sa.x = static_cast<const int8_t*>(ctx->q8.p);
     sa.kpad = L->kpad;
     sa.M = M;

@@ -93,6 +93,8 @@ struct StreamArgs {
   int splits;         // 0 = automatic
 };
 cudaError_t launch_stream_gemm(const StreamArgs& a, int num_sms, cudaStream_t stream, const char** err_msg);
+// INT4 weights (w4 required): TMEM-widened A operand, kind::i8 MMAs (stream4.cu)
+cudaError_t launch_stream4_gemm(const StreamArgs& a, int num_sms, cudaStream_t stream, const char** err_msg);
 
 // WeightOnly forward (wo.cu, reference weight_only_forward runtime.cpp:115-136).
 struct WoArgs {
@@ -145,6 +147,7 @@ extern int gemm_multicast;      // 1: 4-CTA TMA-multicast clusters for CTA-pair 
 extern int gemm_w4;             // 1: INT4-weight (widened in smem) 1-CTA tiles when available
 extern int gemm_stream;         // 1: M <= 64 forwards use the split-K weight-streaming GEMM
 extern int gemm_w4_stream;      // 1: ... streaming the INT4 weights (4-bit layers)
+extern int gemm_stream4_auto;   // 1: 4-bit layers at M <= 32 use the INT4 stream kernel (default)
 cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream, const char** err_msg);
 
 // K1: fused split + per-token asymmetric quantisation (runtime.cpp:36-66,

@@ -341,6 +341,28 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar, uint16_t mask = 3) {
         : "memory");
 }
 
+// Converged-warp variants (the whole warp executes, one elected lane issues): with
+// warp-uniform operands ptxas emits back-to-back UTC*MMA instead of the per-instruction
+// ELECT / R2UR / branch loop of a single-lane region (13 vs 44 cycles per small-N MMA,
+// tools/ts_rate.cu).
+__device__ __forceinline__ void commit_e(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+// D[tmem] (+)= A[tmem] * B[smem]^T, int8 -> int32 (A: lane = row, column j = 4 int8
+// {k = 4j .. 4j+3}, K = 32 per instruction = 8 columns; tools/ts_probe.cu)
+__device__ __forceinline__ void mma_i8_ts_e(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
 // 32 lanes x 32 consecutive 32-bit columns: lane i of the warp receives TMEM
 // lane (base_lane + i), columns [col, col+32).
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {

@@ -134,13 +134,6 @@ __device__ __forceinline__ void mma_f16_ss_e(uint32_t d, uint64_t adesc, uint64_
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
-__device__ __forceinline__ void commit_e(uint64_t* bar) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
-          smem_u32(bar))
-      : "memory");
-}
 
 template <int BN>
 __global__ void __launch_bounds__(WCfg<BN>::kThreads, 1) wo_gemm_kernel(const __grid_constant__ WParams p) {
