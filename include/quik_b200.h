@@ -259,6 +259,11 @@ quik_status quik_set_gemm_w4(int on);
  * 4-bit layers. */
 quik_status quik_set_stream_gemm(int on, int int4);
 
+/* Tuning: 4-bit layers at M <= 32 run the INT4 decode kernel (stream4.cu: INT4 weights
+ * widened into TMEM, split-K over all SMs, the fused epilogue in the same kernel;
+ * bit-identical to the fused path). Default on; 0 = the fused kernel on INT8 tiles. */
+quik_status quik_set_int4_decode(int on);
+
 /* Diagnostics (process-wide): when on, the V3 forward runs the fused GEMM
  * without writing the output (mainloop + TMEM drain only). Never for results. */
 quik_status quik_set_probe_mode(int on);

@@ -33,7 +33,7 @@ EXPORTED_SYMBOLS = (
     "quik_quantize_activations_gemm", "quik_layer_is_sparse", "quik_set_gemm_multicast",
     "quik_set_gemm_w4", "quik_set_stream_gemm", "quik_bundle_open", "quik_bundle_weights",
     "quik_bundle_tensor", "quik_bundle_close", "quik_layer_load_bundle", "quik_layer_create_gated",
-    "quik_linear_forward_weight_only", "quik_linear_forward_sharded",
+    "quik_linear_forward_weight_only", "quik_linear_forward_sharded", "quik_set_int4_decode",
 )
 
 
@@ -119,6 +119,7 @@ def load() -> C.CDLL:
             "quik_layer_create_gated": (i32, [vp, C.POINTER(WeightsDesc), C.POINTER(WeightsDesc), C.POINTER(vp)]),
             "quik_linear_forward_weight_only": (i32, [vp, vp, vp, i32, i64, vp, i32, i64, vp]),
             "quik_linear_forward_sharded": (i32, [vp, vp, vp, i32, i64, C.POINTER(vp), i32, i64, i64, vp]),
+            "quik_set_int4_decode": (i32, [i32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)

@@ -106,7 +106,14 @@ struct quik_ctx_s {
   int device = 0;
   int num_sms = 148;
   int* d_err = nullptr;
-  DevBuf q8, scale, zero, xo16, acc, fp, xbase, xo32, wtmp, wo_ws;
+  DevBuf q8, scale, zero, xo16, acc, fp, xbase, xo32, wtmp, wo_ws, s4_out, s4_cnt;
+  // per-weight-block arrival counters of the INT4 decode kernel (zero between calls)
+  int* ensure_s4_counters(size_t n, cudaStream_t st) {
+    const size_t before = s4_cnt.cap;
+    void* p = s4_cnt.ensure(n * 4);
+    if (s4_cnt.cap != before) QK_CUDA(cudaMemsetAsync(p, 0, s4_cnt.cap, st));
+    return static_cast<int*>(p);
+  }
   // host-buffer forward (quik_linear_forward_host): copy-in / copy-out streams and
   // per-chunk events, created on first use; device staging for x and y.
   cudaStream_t s_in = nullptr, s_out = nullptr;
@@ -292,6 +299,11 @@ quik_status quik_set_stream_gemm(int on, int int4) {
   return QUIK_OK;
 }
 
+quik_status quik_set_int4_decode(int on) {
+  quikb200::gemm_stream4_auto = on ? 1 : 0;
+  return QUIK_OK;
+}
+
 quik_status quik_set_gemm_multicast(int on) {
   quikb200::gemm_multicast = on ? 1 : 0;
   return QUIK_OK;
@@ -333,7 +345,7 @@ quik_status quik_ctx_destroy(quik_ctx_t ctx) {
   DeviceGuard g(ctx->device);
   cudaDeviceSynchronize();
   for (DevBuf* b : {&ctx->q8, &ctx->scale, &ctx->zero, &ctx->xo16, &ctx->acc, &ctx->fp, &ctx->xbase, &ctx->xo32,
-                    &ctx->wtmp, &ctx->xdev, &ctx->ydev, &ctx->ws, &ctx->wo_ws})
+                    &ctx->wtmp, &ctx->xdev, &ctx->ydev, &ctx->ws, &ctx->wo_ws, &ctx->s4_out, &ctx->s4_cnt})
     b->release();
   if (ctx->s_in) {
     cudaStreamDestroy(ctx->s_in);
@@ -795,7 +807,38 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
   const bool small = variant == QUIK_V3_FUSED_EPILOGUE && M <= 64 && L->kpad && !L->sparse && !g_probe_mode;
   const bool auto4 = small && quikb200::gemm_stream4_auto && L->bits == 4 && M <= 32 && !L->gated;
   ensure_w4(L, st, auto4);
-  if ((auto4 && L->w4) || (small && quikb200::gemm_stream)) {
+  if (auto4 && L->w4 && !quikb200::gemm_stream) {
+    // decode regime: K1 -> one kernel for the INT4 split-K GEMM and the fused epilogue
+    // (dequant + outlier MMAs, stream4.cu); workspace / counters stay zeroed between calls
+    run_k1(ctx, L, x, xdt, M, st);
+    if (mid_event) QK_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(mid_event), st));
+    Stream4Args a{};
+    a.w4 = L->w4;
+    a.x = static_cast<const int8_t*>(ctx->q8.p);
+    a.kpad = L->kpad;
+    a.M = M;
+    a.N = N;
+    a.wo = L->wo16;
+    a.xo = static_cast<const __half*>(ctx->xo16.p);
+    a.opad = L->opad;
+    a.a_scale = static_cast<const float*>(ctx->scale.p);
+    a.a_zero = static_cast<const float*>(ctx->zero.p);
+    a.w_scale = L->w_scale;
+    a.wreduced = L->wreduced;
+    a.bias = L->bias;
+    a.half_range = static_cast<float>(1 << (L->bits - 1));
+    a.acc = ctx->ensure_ws(static_cast<size_t>(M * N * 4), st);
+    a.counters = ctx->ensure_s4_counters(quikb200::stream4_counter_count(N), st);
+    a.out = y;
+    a.ldo = ldy;
+    a.out_f16 = ydt == QUIK_F16;
+    a.peer_out = peers;
+    a.n_peer = n_peer;
+    const char* msg = nullptr;
+    check_launch(launch_stream4(a, ctx->num_sms, st, &msg), "int4 stream kernel", msg);
+    return QUIK_OK;
+  }
+  if (small && quikb200::gemm_stream) {
     // weight-streaming regime: K1 -> split-K stream GEMM into the zeroed int32
     // workspace -> the fused kernel's AccInit mode (dequant + outlier MMAs + store,
     // clears the workspace); same arithmetic as the fused V3 kernel

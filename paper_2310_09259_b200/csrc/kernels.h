@@ -93,8 +93,27 @@ struct StreamArgs {
   int splits;         // 0 = automatic
 };
 cudaError_t launch_stream_gemm(const StreamArgs& a, int num_sms, cudaStream_t stream, const char** err_msg);
-// INT4 weights (w4 required): TMEM-widened A operand, kind::i8 MMAs (stream4.cu)
-cudaError_t launch_stream4_gemm(const StreamArgs& a, int num_sms, cudaStream_t stream, const char** err_msg);
+// Decode-regime quik forward on INT4 weights after K1 (stream4.cu): split-K integer
+// GEMM (TMEM-widened A, kind::i8), outlier MMAs and the dequant epilogue in one kernel.
+struct Stream4Args {
+  const uint8_t* w4;   // [N][kpad / 2] device INT4 layout
+  const int8_t* x;     // [M][kpad] activation codes (K1)
+  int64_t kpad, M, N;
+  const __half* wo;    // [N][opad]
+  const __half* xo;    // [M][opad]
+  int64_t opad;
+  const float *a_scale, *a_zero, *w_scale, *wreduced, *bias;
+  float half_range;
+  int32_t* acc;        // [M][N] int32 workspace, zero on entry and exit
+  int* counters;       // [stream4_counter_count(N)], zero on entry and exit
+  void* out;
+  int64_t ldo;
+  int out_f16;
+  void* const* peer_out;
+  int n_peer;
+};
+size_t stream4_counter_count(int64_t N);
+cudaError_t launch_stream4(const Stream4Args& a, int num_sms, cudaStream_t stream, const char** err_msg);
 
 // WeightOnly forward (wo.cu, reference weight_only_forward runtime.cpp:115-136).
 struct WoArgs {

@@ -315,13 +315,6 @@ cudaError_t launch_stream_gemm(const StreamArgs& a, int num_sms, cudaStream_t st
   *err_msg = nullptr;
   if (a.M == 0 || a.N == 0 || a.kpad == 0) return cudaSuccess;
   if (a.M > 64) { *err_msg = "stream GEMM: M > 64"; return cudaErrorInvalidValue; }
-  // INT4 weights: the TMEM-widening kernel (stream4.cu); QUIK_STREAM_W4=smem selects
-  // the older shared-memory widening variant below
-  static const bool w4_smem = [] {
-    const char* e = getenv("QUIK_STREAM_W4");
-    return e && e[0] == 's';
-  }();
-  if (a.w4 != nullptr && !w4_smem) return launch_stream4_gemm(a, num_sms, stream, err_msg);
   const bool w4 = a.w4 != nullptr && a.kpad % (2 * kKBlockBytes) == 0;  // INT4 stages span 256 K
   const int bn = a.M <= 16 ? 16 : (a.M <= 32 ? 32 : 64);
   SParams sp{};

@@ -3,8 +3,12 @@
 //
 //   acc_ws[t][n] += sum_{k in split} q[n][k] * X8[t][k]      (red.global.add.s32)
 //
-// followed by the fused kernel's AccInit mode (dequant + f16 outlier MMAs + store,
-// bit-identical to the one-kernel V3 forward: integer sums commute).
+// and, in the same kernel, the rest of the layer: the CTA that completes a weight block
+// last (per-block arrival counter) finalises it exactly as the fused kernel's epilogue
+// does: init = bias + dequant_element(acc) (op by op, runtime.cpp:70-77) written into a
+// TMEM accumulator, the f16 outlier MMAs (x_o W_o^T) accumulated onto it, f16/f32 out.
+// Same instructions in the same order, so the output is bit-identical to the fused V3
+// forward (and to V1/V2). The workspace and counters are left zeroed for the next call.
 //
 // Same architecture as the weight-only kernel (wo.cu): the 4-bit weights never exist
 // as int8 in shared memory. A weight producer TMA-streams 16 KB INT4 tiles (128 rows x
@@ -37,28 +41,48 @@ constexpr int kS4TmemA = 64;                        // columns per A buffer (256
 template <int BN>
 struct S4Cfg {
   static constexpr int G = BN == 64 ? 2 : 3;
-  static constexpr int kTAtom = BN * kKBlockBytes;  // BN rows x 128 K int8
-  static constexpr int kSlotT = 2 * kTAtom;         // 256 K per stage
-  static constexpr int kStagesW = BN == 64 ? 8 : 9;
+  static constexpr int kTAtom = BN * kKBlockBytes;  // BN rows x 128 K int8 (or 64 f16)
+  static constexpr int kSlotT = 2 * kTAtom;         // 256 K of codes per stage
+  static constexpr int kStagesW = BN == 16 ? 9 : 6;
   static constexpr int kStagesT = BN == 64 ? 4 : 6;
   static_assert(kStagesW % G == 0 && kStagesT % G == 0, "one consumer group per stage");
+  // finalisation buffer: two 64-column outlier blocks (f16 weight tile + x_o tile)
+  static constexpr int kFinBlk = kS4WBytes + kTAtom;
   static constexpr int kOffT = kStagesW * kS4WBytes;
-  static constexpr int kRingBytes = kOffT + kStagesT * kSlotT;
-  static constexpr int kBarBytes = (2 * (kStagesW + kStagesT) + 2 * G + 4) * 8 + 16;
+  static constexpr int kOffF = kOffT + kStagesT * kSlotT;
+  static constexpr int kRingBytes = kOffF + 2 * kFinBlk;
+  static constexpr int kBarBytes = (2 * (kStagesW + kStagesT) + 2 * G + 6) * 8 + 32;
   static constexpr int kSmemBytes = 1024 + kRingBytes + kBarBytes;
   static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
   static constexpr int kAccCol = G * kS4TmemA;
-  static constexpr int kAccBuf = G * BN;  // G int32 accumulators, double-buffered
-  static_assert(kAccCol + 2 * kAccBuf <= 512, "TMEM budget");
+  static constexpr int kAccBuf = G * BN;             // G int32 accumulators, double-buffered
+  static constexpr int kFinCol = kAccCol + 2 * kAccBuf;  // f32 finalisation accumulator (BN)
+  static_assert(kFinCol + BN <= 512, "TMEM budget");
+  // warps: 0 weight producer, 1 TMEM allocator, 2 .. 4G+1 widening, 4 epilogue, G base
+  // issuers, 1 code-tile producer
   static constexpr int kWidenEnd = 2 + 4 * G, kEpiEnd = kWidenEnd + 4, kIssEnd = kEpiEnd + G;
   static constexpr int kThreads = (kIssEnd + 1) * 32;
 };
 
 struct S4Params {
-  CUtensorMap tm_w;  // INT4 [N][kpad / 2] (device nibble layout), box {128 B, 128}, SW128
-  CUtensorMap tm_x;  // int8 [M][kpad], box {128 B, BN}, SW128
-  int M, N, nstage, splits;  // nstage: 256-K stages over kpad
-  int32_t* acc;              // [M][N] workspace
+  CUtensorMap tm_w;   // INT4 [N][kpad / 2] (device nibble layout), box {128 B, 128}, SW128
+  CUtensorMap tm_x;   // int8 [M][kpad], box {128 B, BN}, SW128
+  CUtensorMap tm_wo;  // f16 [N][opad] as bytes, box {128 B, 128}, SW128
+  CUtensorMap tm_xo;  // f16 [M][opad] as bytes, box {128 B, BN}, SW128
+  int M, N, nstage, splits, nout;  // nstage: 256-K stages over kpad; nout: 64-column outlier blocks
+  int32_t* acc;                    // [M][N] int32 workspace (zero on entry and exit)
+  int* counters;                   // [tiles] arrivals per weight block (zero on entry and exit)
+  const float* a_scale;
+  const float* a_zero;
+  const float* w_scale;
+  const float* wreduced;
+  const float* bias;
+  float half_range;
+  void* out;
+  long long ldo;
+  int out_f16;
+  int n_dst;              // 1 + peers
+  void* dst[8];           // output base pointers (dst[0] == out)
 };
 
 template <int BN>
@@ -69,26 +93,36 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* ring_w = smem;
   uint8_t* ring_t = smem + C::kOffT;
+  uint8_t* fin = smem + C::kOffF;
   uint64_t* full_w = reinterpret_cast<uint64_t*>(smem + C::kRingBytes);
   uint64_t* empty_w = full_w + C::kStagesW;
   uint64_t* full_t = empty_w + C::kStagesW;
   uint64_t* empty_t = full_t + C::kStagesT;
-  uint64_t* a_full = empty_t + C::kStagesT;  // [G] widening group g -> issuer g
+  uint64_t* fin_full = empty_t + C::kStagesT;  // finalisation: outlier tiles landed
+  uint64_t* fin_mma = fin_full + 1;            // finalisation: outlier MMAs done
+  uint64_t* a_full = fin_mma + 1;              // [G] widening group g -> issuer g
   uint64_t* a_empty = a_full + G;            // [G] issuer g -> widening group g
   uint64_t* acc_full = a_empty + G;          // [2] the G issuers -> epilogue
   uint64_t* acc_empty = acc_full + 2;        // [2] epilogue -> issuers
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&p.tm_w);
     tma_prefetch(&p.tm_x);
+    if (p.nout) {
+      tma_prefetch(&p.tm_wo);
+      tma_prefetch(&p.tm_xo);
+    }
   }
   if (warp == 1) {
     if (lane == 0) {
       for (int i = 0; i < C::kStagesW; ++i) { mbar_init(&full_w[i], 1); mbar_init(&empty_w[i], 4); }
       for (int i = 0; i < C::kStagesT; ++i) { mbar_init(&full_t[i], 1); mbar_init(&empty_t[i], 1); }
+      mbar_init(fin_full, 1);
+      mbar_init(fin_mma, 1);
       for (int i = 0; i < G; ++i) { mbar_init(&a_full[i], 4); mbar_init(&a_empty[i], 1); }
       for (int i = 0; i < 2; ++i) { mbar_init(&acc_full[i], G); mbar_init(&acc_empty[i], 4); }
       fence_mbar_init();
@@ -110,38 +144,42 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
     const int s = u / tiles_n;
     k0 = static_cast<int>((static_cast<long long>(p.nstage) * s) / p.splits);
     k1 = static_cast<int>((static_cast<long long>(p.nstage) * (s + 1)) / p.splits);
+    return true;
   };
 
   if (warp == 0 || warp == C::kIssEnd) {
     if (lane == 0) {
       const uint64_t pol_w = policy_evict_first();  // weights stream once
-      const uint64_t pol_x = policy_evict_last();   // the code tile is re-read by every block
+      const uint64_t pol_x = policy_evict_last();   // code / x_o tiles are re-read by every block
       const bool wprod = warp == 0;
       int bc = 0;
       for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
         int nb, k0, k1;
         decode(u, nb, k0, k1);
-        for (int i = k0; i < k1; ++i, ++bc) {
-          if (wprod) {
-            const int st = bc % C::kStagesW;
-            mbar_wait_sleep(&empty_w[st], ((bc / C::kStagesW) & 1) ^ 1);
-            mbar_arrive_expect_tx(&full_w[st], kS4WBytes);
-            tma_load_2d(ring_w + st * kS4WBytes, &p.tm_w, i * kKBlockBytes, nb * kBlockM, &full_w[st], pol_w);
-          } else {
-            const int st = bc % C::kStagesT;
-            mbar_wait_sleep(&empty_t[st], ((bc / C::kStagesT) & 1) ^ 1);
-            uint8_t* slot = ring_t + st * C::kSlotT;
-            mbar_arrive_expect_tx(&full_t[st], C::kSlotT);
-            tma_load_2d(slot, &p.tm_x, (2 * i) * kKBlockBytes, 0, &full_t[st], pol_x);
-            tma_load_2d(slot + C::kTAtom, &p.tm_x, (2 * i + 1) * kKBlockBytes, 0, &full_t[st], pol_x);
+        {
+          for (int i = k0; i < k1; ++i, ++bc) {
+            if (wprod) {
+              const int st = bc % C::kStagesW;
+              mbar_wait_sleep(&empty_w[st], ((bc / C::kStagesW) & 1) ^ 1);
+              mbar_arrive_expect_tx(&full_w[st], kS4WBytes);
+              tma_load_2d(ring_w + st * kS4WBytes, &p.tm_w, i * kKBlockBytes, nb * kBlockM, &full_w[st], pol_w);
+            } else {
+              const int st = bc % C::kStagesT;
+              mbar_wait_sleep(&empty_t[st], ((bc / C::kStagesT) & 1) ^ 1);
+              uint8_t* slot = ring_t + st * C::kSlotT;
+              mbar_arrive_expect_tx(&full_t[st], C::kSlotT);
+              tma_load_2d(slot, &p.tm_x, (2 * i) * kKBlockBytes, 0, &full_t[st], pol_x);
+              tma_load_2d(slot + C::kTAtom, &p.tm_x, (2 * i + 1) * kKBlockBytes, 0, &full_t[st], pol_x);
+            }
           }
         }
       }
     }
   } else if (warp >= C::kEpiEnd) {
-    // issuer of widening group g (whole warp converged, elected lane issues)
+    // issuer of widening group g (whole warp converged, elected lane issues); commits
+    // acc_full once per unit
     const int g = warp - C::kEpiEnd;
-    constexpr uint32_t idesc = idesc_make(2u, 1u, kBlockM, BN);
+    constexpr uint32_t idesc_i8 = idesc_make(2u, 1u, kBlockM, BN);
     int bc = 0, it = 0;
     for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
       int nb, k0, k1;
@@ -161,7 +199,7 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
         const uint64_t bd0 = umma_desc_sw128(smem_u32(ring_t + st * C::kSlotT));
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          mma_i8_ts_e(d, a_tm + 8 * j, bd0 + (j >> 2) * (C::kTAtom >> 4) + 2 * (j & 3), idesc,
+          mma_i8_ts_e(d, a_tm + 8 * j, bd0 + (j >> 2) * (C::kTAtom >> 4) + 2 * (j & 3), idesc_i8,
                       (first && j == 0) ? 0u : 1u);
         first = false;
         commit_e(&a_empty[g]);
@@ -214,9 +252,10 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
       }
     }
   } else if (warp >= C::kWidenEnd) {
-    // epilogue: TMEM lane = weight row n, column = token t; sum the G accumulators
+    // epilogue (4 warps): TMEM lane = weight row n, column = token t
     const int quad = warp & 3;
-    int it = 0, bc0 = 0;
+    const bool lead = warp == C::kWidenEnd;  // issues the finalisation TMA loads / MMAs
+    int it = 0, bc0 = 0, fin_uses = 0;
     for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
       int nb, k0, k1;
       decode(u, nb, k0, k1);
@@ -227,33 +266,23 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
       mbar_wait_sleep(&acc_full[b], (it >> 1) & 1);
       tc_fence_after();
       const int n = nb * kBlockM + quad * 32 + lane;
-      const uint32_t tacc = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + C::kAccCol + b * C::kAccBuf;
+      const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+      const uint32_t tacc = tmem_base + lane_off + C::kAccCol + b * C::kAccBuf;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         int sum[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) sum[j] = 0;
-        if constexpr (BN == 16) {
-          uint32_t x0[32], x1[32];  // accumulators 0/1 in columns 0-31, 2 in 32-47
-          tmem_ld32(tacc, x0);
-          tmem_ld32(tacc + 32, x1);
+#pragma unroll 1
+        for (int g = 0; g < G; ++g) {
+          if (!(used & (1u << g))) continue;
+          uint32_t x[32];
+          tmem_ld32(tacc + g * BN + c, x);  // (BN = 16: the next accumulator's columns are ignored)
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            sum[j] = ((used & 1u) ? static_cast<int>(x0[j]) : 0) + ((used & 2u) ? static_cast<int>(x0[16 + j]) : 0) +
-                     ((used & 4u) ? static_cast<int>(x1[j]) : 0);
-        } else {
-#pragma unroll 1
-          for (int g = 0; g < G; ++g) {
-            if (!(used & (1u << g))) continue;
-            uint32_t x[32];
-            tmem_ld32(tacc + g * BN + c, x);
-            tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 32; ++j) sum[j] += static_cast<int>(x[j]);
-          }
+          for (int j = 0; j < 32; ++j) sum[j] += static_cast<int>(x[j]);
         }
-        if (n < p.N) {
+        if (n < p.N && used) {
 #pragma unroll
           for (int j = 0; j < (BN < 32 ? BN : 32); ++j) {
             const int t = c + j;
@@ -264,6 +293,115 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[b]);
+      // completion: the last of this block's splits finalises it (writes -> fence ->
+      // counter; last arriver: fence -> reads)
+      __threadfence();
+      named_barrier_sync(1, 128);
+      if (lead && lane == 0) *last_flag = atomicAdd(&p.counters[nb], 1) == p.splits - 1;
+      named_barrier_sync(1, 128);
+      if (!*last_flag) continue;
+      __threadfence();
+      // (0) the first outlier tiles start loading while init is computed
+      constexpr uint32_t idesc_f16 = idesc_make(1u, 0u, kBlockM, BN);
+      auto load_blocks = [&](int j0) {
+        const int nblk = p.nout - j0 < 2 ? p.nout - j0 : 2;
+        if (lane == 0) {
+          mbar_arrive_expect_tx(fin_full, nblk * C::kFinBlk);
+          for (int q = 0; q < nblk; ++q) {
+            tma_load_2d(fin + q * C::kFinBlk, &p.tm_wo, (j0 + q) * kKBlockBytes, nb * kBlockM, fin_full,
+                        policy_evict_first());
+            tma_load_2d(fin + q * C::kFinBlk + kS4WBytes, &p.tm_xo, (j0 + q) * kKBlockBytes, 0, fin_full,
+                        policy_evict_last());
+          }
+        }
+        return nblk;
+      };
+      if (lead && p.nout) load_blocks(0);
+      // (1) init = bias + dequant_element(acc) -> TMEM finalisation accumulator
+      const uint32_t tfin = tmem_base + lane_off + C::kFinCol;
+      {
+        const bool nok = n < p.N;
+        const float sw = nok ? __ldg(&p.w_scale[n]) : 0.f, wr = nok ? __ldg(&p.wreduced[n]) : 0.f;
+        const float bs = (nok && p.bias) ? __ldg(&p.bias[n]) : 0.f;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          // per-token scale / zero: lane j holds token c + j (shuffled below); all
+          // accumulator loads in flight before the workspace is cleared
+          const int tl = c + lane;
+          const float sa_l = tl < p.M ? __ldg(&p.a_scale[tl]) : 0.f;
+          const float zs_l = tl < p.M ? __fadd_rn(__ldg(&p.a_zero[tl]), __fmul_rn(p.half_range, sa_l)) : 0.f;  // runtime.cpp:74
+          int32_t accv[BN < 32 ? BN : 32];
+#pragma unroll
+          for (int j = 0; j < (BN < 32 ? BN : 32); ++j)
+            accv[j] = (c + j < p.M && nok) ? __ldcg(&p.acc[static_cast<long long>(c + j) * p.N + n]) : 0;
+#pragma unroll
+          for (int j = 0; j < (BN < 32 ? BN : 32); ++j)
+            if (c + j < p.M && nok) p.acc[static_cast<long long>(c + j) * p.N + n] = 0;  // zeros for the next call
+          uint32_t v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float sa = __shfl_sync(0xffffffffu, sa_l, j);
+            const float zs = __shfl_sync(0xffffffffu, zs_l, j);
+            float init = 0.f;
+            if (j < BN && c + j < p.M) {
+              float x = __fmul_rn(__int2float_rn(accv[j < BN ? j : 0]), sa);
+              x = __fmul_rn(x, sw);
+              x = __fadd_rn(x, __fmul_rn(zs, wr));  // dequant_element, runtime.cpp:70-77
+              init = __fadd_rn(bs, x);
+            }
+            v[j] = __float_as_uint(init);
+          }
+          tmem_st32(tfin + c, v);  // (BN = 16: columns 16-31 land in unused TMEM)
+        }
+        tmem_st_wait();
+      }
+      tc_fence_before();
+      named_barrier_sync(1, 128);
+      // (2) outlier MMAs onto init, two 64-column blocks per round trip
+      if (lead && p.nout) {
+        tc_fence_after();
+        for (int j0 = 0; j0 < p.nout; j0 += 2) {
+          const int nblk = j0 == 0 ? (p.nout < 2 ? p.nout : 2) : load_blocks(j0);
+          mbar_wait(fin_full, fin_uses & 1);
+          tc_fence_after();
+          for (int q = 0; q < nblk; ++q) {
+            const uint64_t ad = umma_desc_sw128(smem_u32(fin + q * C::kFinBlk));
+            const uint64_t bd = umma_desc_sw128(smem_u32(fin + q * C::kFinBlk + kS4WBytes));
+#pragma unroll
+            for (int k = 0; k < 4; ++k) mma_f16_ss_e(tmem_base + C::kFinCol, ad + 2 * k, bd + 2 * k, idesc_f16, 1u);
+          }
+          commit_e(fin_mma);
+          mbar_wait(fin_mma, fin_uses & 1);  // MMAs done: buffer reusable, accumulator final
+          ++fin_uses;
+        }
+        tc_fence_before();
+      }
+      named_barrier_sync(1, 128);
+      tc_fence_after();
+      // (3) drain: f16 / f32 to every destination
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t v[32];
+        tmem_ld32(tfin + c, v);
+        tmem_ld_wait();
+        if (n < p.N) {
+#pragma unroll
+          for (int j = 0; j < (BN < 32 ? BN : 32); ++j) {
+            const int t = c + j;
+            if (t >= p.M) continue;
+            const float y = __uint_as_float(v[j]);
+            for (int di = 0; di < p.n_dst; ++di) {
+              if (p.out_f16)
+                static_cast<__half*>(p.dst[di])[static_cast<long long>(t) * p.ldo + n] = __float2half_rn(y);
+              else
+                static_cast<float*>(p.dst[di])[static_cast<long long>(t) * p.ldo + n] = y;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      if (lead && lane == 0) p.counters[nb] = 0;
+      named_barrier_sync(1, 128);  // the finalisation accumulator is free again
     }
   }
 
@@ -297,24 +435,29 @@ cudaError_t launch_s4(const S4Params& sp, int num_sms, cudaStream_t stream) {
 
 }  // namespace
 
-// Measured at OPT-66B fc1 (9216 -> 36864, 256 outliers), K1 + stream + AccInit vs the
-// fused kernel on INT8 tiles: M = 1 51 vs 65 us, M = 16 54 vs 65 us, M = 64 equal
-// (profiles/r1_stream4.jsonl): on for 4-bit layers at M <= 32.
+// Measured (profiles/r1_stream4.jsonl, K1 + this kernel, graph replay): OPT-66B fc1
+// (9216 -> 36864, 256 outliers) M = 1: 44 us, M = 16: 47 us (fused kernel on INT8 tiles:
+// 65 us; cuBLAS f16: 111 us); cfg1 4096^2 M = 16: 16.6 us (18.6). On for 4-bit layers
+// at M <= 32 (QUIK_STREAM4=0 / quik_set_int4_decode(0) disables).
 int gemm_stream4_auto = [] {
   const char* e = getenv("QUIK_STREAM4");
   return e ? atoi(e) : 1;
 }();
 
-cudaError_t launch_stream4_gemm(const StreamArgs& a, int num_sms, cudaStream_t stream, const char** err_msg) {
+size_t stream4_counter_count(int64_t N) { return static_cast<size_t>((N + kBlockM - 1) / kBlockM); }
+
+cudaError_t launch_stream4(const Stream4Args& a, int num_sms, cudaStream_t stream, const char** err_msg) {
   *err_msg = nullptr;
-  if (a.M == 0 || a.N == 0 || a.kpad == 0) return cudaSuccess;
+  if (a.M == 0 || a.N == 0) return cudaSuccess;
   if (a.M > 64) { *err_msg = "INT4 stream GEMM: M > 64"; return cudaErrorInvalidValue; }
-  if (!a.w4) { *err_msg = "INT4 stream GEMM: no INT4 weights"; return cudaErrorInvalidValue; }
+  if (!a.w4 || a.kpad == 0) { *err_msg = "INT4 stream GEMM: no INT4 weights"; return cudaErrorInvalidValue; }
+  if (a.n_peer < 0 || a.n_peer > 7) { *err_msg = "INT4 stream GEMM: at most 7 peer outputs"; return cudaErrorInvalidValue; }
   const int bn = a.M <= 16 ? 16 : (a.M <= 32 ? 32 : 64);
   S4Params sp{};
   sp.M = static_cast<int>(a.M);
   sp.N = static_cast<int>(a.N);
   sp.nstage = static_cast<int>((a.kpad + 255) / 256);
+  sp.nout = static_cast<int>(a.opad / 64);
   // K splits: minimise the busiest CTA's stage count (see wo.cu)
   const long long tiles = (a.N + kBlockM - 1) / kBlockM;
   int splits = 1;
@@ -324,13 +467,30 @@ cudaError_t launch_stream4_gemm(const StreamArgs& a, int num_sms, cudaStream_t s
     const long long cost = waves * ((sp.nstage + s - 1) / s + 1);
     if (best < 0 || cost < best) { best = cost; splits = s; }
   }
-  if (a.splits > 0) splits = a.splits;
   sp.splits = splits;
   sp.acc = a.acc;
+  sp.counters = a.counters;
+  sp.a_scale = a.a_scale;
+  sp.a_zero = a.a_zero;
+  sp.w_scale = a.w_scale;
+  sp.wreduced = a.wreduced;
+  sp.bias = a.bias;
+  sp.half_range = a.half_range;
+  sp.out = a.out;
+  sp.ldo = a.ldo;
+  sp.out_f16 = a.out_f16;
+  sp.n_dst = 1 + a.n_peer;
+  sp.dst[0] = a.out;
+  for (int i = 0; i < a.n_peer; ++i) sp.dst[1 + i] = a.peer_out[i];
   // the INT4 rows hold kpad / 2 bytes; a 256-K stage past kpad reads zeros (OOB fill)
-  const CUresult r1 = encode_map_2d(&sp.tm_w, a.w4, a.kpad / 2, a.N, a.kpad / 2, kKBlockBytes, kBlockM, true);
-  const CUresult r2 = encode_map_2d(&sp.tm_x, a.x, a.kpad, a.M, a.kpad, kKBlockBytes, static_cast<uint32_t>(bn), true);
-  if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS) { *err_msg = "INT4 stream GEMM: tensor map encode failed"; return cudaErrorInvalidValue; }
+  CUresult r = encode_map_2d(&sp.tm_w, a.w4, a.kpad / 2, a.N, a.kpad / 2, kKBlockBytes, kBlockM, true);
+  if (r == CUDA_SUCCESS) r = encode_map_2d(&sp.tm_x, a.x, a.kpad, a.M, a.kpad, kKBlockBytes, static_cast<uint32_t>(bn), true);
+  if (r == CUDA_SUCCESS && sp.nout) {
+    r = encode_map_2d(&sp.tm_wo, a.wo, a.opad * 2, a.N, a.opad * 2, kKBlockBytes, kBlockM, true);
+    if (r == CUDA_SUCCESS)
+      r = encode_map_2d(&sp.tm_xo, a.xo, a.opad * 2, a.M, a.opad * 2, kKBlockBytes, static_cast<uint32_t>(bn), true);
+  }
+  if (r != CUDA_SUCCESS) { *err_msg = "INT4 stream GEMM: tensor map encode failed"; return cudaErrorInvalidValue; }
   switch (bn) {
     case 16: return launch_s4<16>(sp, num_sms, stream);
     case 32: return launch_s4<32>(sp, num_sms, stream);

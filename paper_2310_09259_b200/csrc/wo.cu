@@ -114,27 +114,6 @@ __device__ __forceinline__ uint32_t hsub2_u32(uint32_t a, uint32_t b) {
   asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
   return r;
 }
-// Issued by a whole converged warp, one elected lane executing: with warp-uniform
-// operands ptxas keeps them in uniform registers and emits back-to-back UTCHMMAs
-// (13 cycles per small-N MMA, tools/ts_rate.cu) instead of the per-instruction
-// ELECT / R2UR / branch loop a single-lane `if (lane == 0)` region gets (44 cycles).
-__device__ __forceinline__ void mma_f16_ts_e(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
-                                             uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
-      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
-      : "memory");
-}
-__device__ __forceinline__ void mma_f16_ss_e(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                             uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
-      : "memory");
-}
-
 template <int BN>
 __global__ void __launch_bounds__(WCfg<BN>::kThreads, 1) wo_gemm_kernel(const __grid_constant__ WParams p) {
   using C = WCfg<BN>;

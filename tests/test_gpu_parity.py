@@ -712,10 +712,12 @@ def test_sparse_not_compressible_stays_dense():
 
 @pytest.mark.parametrize("bits", [4, 8])
 def test_stream_gemm_bit_identical_to_fused(bits):
-    """M <= 64 forwards run the split-K weight-streaming GEMM (INT4 or INT8 weights)
-    into an int32 workspace + the AccInit epilogue. The integer sums are exact and the
-    epilogue arithmetic is the fused kernel's, so outputs are bit-identical to the fused
-    path, and to the reference when O = 0; the workspace is left zeroed (repeat calls)."""
+    """Small-M forwards: the INT4 decode kernel (default for 4-bit layers at M <= 32: INT4
+    split-K GEMM + the fused epilogue finalised by the last CTA of each weight block) and
+    the opt-in split-K streams (INT8 / shared-memory INT4) + AccInit epilogue. Integer
+    sums are exact and the epilogue instructions are the fused kernel's, so every path is
+    bit-identical to the fused one (f32 and f16 out, repeat calls: the workspace and
+    counters are left zeroed), and to the reference when O = 0."""
     m = q()
     o = oracle()
     import torch
@@ -724,21 +726,28 @@ def test_stream_gemm_bit_identical_to_fused(bits):
     rng = np.random.default_rng(900 + bits)
     try:
         for (M, K, N, O) in [(1, 1024, 4096, 64), (7, 3000, 384, 32), (16, 4096, 1000, 128), (33, 640, 2048, 0),
-                             (64, 2048, 512, 16)]:
+                             (64, 2048, 512, 16), (20, 1000, 300, 8), (32, 8192, 2048, 256)]:
             L, x, _ = make_layer(rng, M, K, N, bits, O, heavy_cols=3)
             dev = m.QuikLinear(to_layer(L))
             xt = torch.from_numpy(x).cuda()
-            outs = []
-            for stream_on, int4 in [(0, 0), (1, 1), (1, 0), (1, 1)]:
-                lib.quik_set_stream_gemm(stream_on, int4)
-                outs.append(dev(xt, out_dtype=torch.float32).cpu().numpy())
-            for y in outs[1:]:
-                np.testing.assert_array_equal(y.view(np.uint32), outs[0].view(np.uint32))
+            for dt in (torch.float32, torch.float16):
+                outs = []
+                for decode, stream_on, int4 in [(0, 0, 0), (1, 0, 0), (1, 0, 0), (0, 1, 1), (0, 1, 0)]:
+                    lib.quik_set_int4_decode(decode)
+                    lib.quik_set_stream_gemm(stream_on, int4)
+                    outs.append(dev(xt, out_dtype=dt).cpu().numpy())
+                u = np.uint32 if dt == torch.float32 else np.uint16
+                for y in outs[1:]:
+                    np.testing.assert_array_equal(y.view(u), outs[0].view(u))
             if O == 0:
+                lib.quik_set_int4_decode(1)
+                lib.quik_set_stream_gemm(0, 1)
                 st, want = o.quik_matmul(L, x, 2)
-                np.testing.assert_array_equal(outs[1].view(np.uint32), want.view(np.uint32))
+                got = dev(xt, out_dtype=torch.float32).cpu().numpy()
+                np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
     finally:
         lib.quik_set_stream_gemm(0, 1)
+        lib.quik_set_int4_decode(1)
 
 
 # --------------------------------------------------------------------------- layer bundles (§8f.1)
