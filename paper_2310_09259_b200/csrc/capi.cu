@@ -807,7 +807,17 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
   const bool small = variant == QUIK_V3_FUSED_EPILOGUE && M <= 64 && L->kpad && !L->sparse && !g_probe_mode;
   const bool auto4 = small && quikb200::gemm_stream4_auto && L->bits == 4 && M <= 32 && !L->gated;
   ensure_w4(L, st, auto4);
-  if (auto4 && L->w4 && !quikb200::gemm_stream) {
+  bool decode = auto4 && L->w4 && !quikb200::gemm_stream;
+  if (decode) {
+    // under stream capture no workspace may be (re)allocated: use the fused path when
+    // the decode workspace / counters are not sized yet (a warm-up call sizes them)
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    QK_CUDA(cudaStreamIsCapturing(st, &cs));
+    if (cs != cudaStreamCaptureStatusNone &&
+        (ctx->ws.cap < static_cast<size_t>(M * N * 4) || ctx->s4_cnt.cap < quikb200::stream4_counter_count(N) * 4))
+      decode = false;
+  }
+  if (decode) {
     // decode regime: K1 -> one kernel for the INT4 split-K GEMM and the fused epilogue
     // (dequant + outlier MMAs, stream4.cu); workspace / counters stay zeroed between calls
     run_k1(ctx, L, x, xdt, M, st);

@@ -978,3 +978,37 @@ def test_sharded_forward_fused_all_gather(M, stream):
         lib.quik_set_stream_gemm(0, 1)
     with pytest.raises(NotImplementedError):  # pitch / offset not TMA-aligned
         shards[0].forward_sharded(xt, [torch.empty((M, 770), dtype=torch.float16, device="cuda")], 3)
+
+
+def test_decode_path_under_graph_capture():
+    """A small-M forward captured into a CUDA graph before the decode workspace exists
+    (the warm-up ran the fused path) takes the fused path instead of allocating inside
+    the capture; after a decode warm-up the captured forward runs the INT4 decode
+    kernel. Both replay bit-identically to the eager fused forward."""
+    m = q()
+    import torch
+
+    rng = np.random.default_rng(5)
+    L, x, _ = make_layer(rng, 8, 2048, 4096, 4, 32, heavy_cols=2)
+    lib = m.load_library()
+    m.quik._ctxs.clear()  # a fresh context: no decode workspace yet
+    dev = m.QuikLinear(to_layer(L))
+    xt = torch.from_numpy(x).cuda().half()
+    try:
+        for warm_decode in (0, 1):
+            lib.quik_set_int4_decode(warm_decode)
+            want = dev(xt)  # warm-up (sizes K1 buffers; the decode workspace only when warm_decode)
+            torch.cuda.synchronize()
+            lib.quik_set_int4_decode(1)
+            y = torch.empty_like(want)
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                dev(xt, out=y)
+            y.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(y.view(torch.int16), want.view(torch.int16))
+    finally:
+        lib.quik_set_int4_decode(1)
