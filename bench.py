@@ -227,10 +227,19 @@ def run_ours(args, w):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # QUIK_BENCH_DIST_BACKEND=gloo + fewer GPUs than ranks: a functional check of the
+    # N > 1 code path on a one-GPU box (ranks share the device); never a bench number
+    backend = os.environ.get("QUIK_BENCH_DIST_BACKEND", "nccl")
+    ndev = torch.cuda.device_count()
+    if backend != "nccl" and ndev < world:
+        local = local % ndev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     M, K, N, O, bits = w["M"], w["K"], w["N"], w["O"], w["bits"]
     if N % world:
         raise SystemExit(f"out_features {N} not divisible by {world} GPUs")
@@ -262,6 +271,14 @@ def run_ours(args, w):
     del base, ow
     torch.cuda.synchronize()
 
+    def all_gather(out, inp):
+        if backend == "nccl":
+            dist.all_gather_into_tensor(out, inp)
+        else:  # gloo check mode: through host memory
+            parts = [torch.empty_like(inp, device="cpu") for _ in range(world)]
+            dist.all_gather(parts, inp.cpu())
+            out.copy_(torch.stack(parts))
+
     y_local = torch.empty((M, ns), dtype=torch.float16, device=dev)
     if world > 1:
         gathered = torch.empty((world, M, ns), dtype=torch.float16, device=dev)
@@ -278,7 +295,7 @@ def run_ours(args, w):
         if e:
             e[2].record()
         if world > 1:
-            dist.all_gather_into_tensor(gathered, y_local)
+            all_gather(gathered, y_local)
             y.view(M, world, ns).copy_(gathered.permute(1, 0, 2))
 
     for e3 in ev:  # materialise the raw cudaEvent handles
@@ -409,7 +426,7 @@ def run_ours(args, w):
             xd.copy_(xh, non_blocking=True)
             layer.forward(xd, out=y_local)
             if world > 1:
-                dist.all_gather_into_tensor(gathered, y_local)
+                all_gather(gathered, y_local)
                 y.view(M, world, ns).copy_(gathered.permute(1, 0, 2))
                 if rank == 0:
                     yh.copy_(y, non_blocking=True)
