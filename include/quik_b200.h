@@ -194,6 +194,24 @@ quik_status quik_linear_forward_ex(quik_ctx_t ctx, quik_layer_t layer, const voi
                                    void* y, quik_dtype y_dtype, int64_t ldy, quik_variant variant, void* stream,
                                    void* mid_event);
 
+/* GPTQ / SparseGPT weight quantisation on the device: the reference's
+ * gptq_quantize (quantizer.cpp:292-297, sparse = 0) or sparsegpt_joint (:299-337,
+ * sparse = 1) with Hessian hessian_sum [K][K] f64 (sum x x^T before damping, host or
+ * device) and damping_frac; FP64 throughout (cuSOLVER Cholesky, blocked column
+ * recursion with DGEMM trailing updates). w [N][K] f32 and the outputs may be host or
+ * device memory (UVA); outputs in the reference's layout: base i4p/i8 [N][row bytes of
+ * K - n_outlier], scales/wreduced [N], outlier_weights [N][n_outlier], mask [N][K - n]
+ * (sparse). Synchronous. QUIK_ERR_NUMERICAL when the damped Hessian is not positive
+ * definite (the reference's NumericalError). */
+quik_status quik_gptq_quantize(quik_ctx_t ctx, const float* w, int64_t N, int64_t K, const double* hessian_sum,
+                               double damping_frac, const int64_t* outlier_indices, int64_t n_outlier, int bits,
+                               int use_clipping, int sparse, uint8_t* base, float* scales, float* wreduced,
+                               float* outlier_weights, uint8_t* mask);
+
+/* Hessian::accumulate (quantizer.cpp:193-213): h_sum [K][K] f64 (DEVICE memory) += x^T x
+ * for the calibration batch x [T][K] f32 (host or device). Synchronous. */
+quik_status quik_hessian_accumulate(quik_ctx_t ctx, const float* x, int64_t T, int64_t K, double* h_sum);
+
 /* Output-feature shard forward with the all-gather fused into the epilogue (SURVEY.md
  * §8e; replaces quik_matmul + ncclAllGather for one shard): the shard layer's f16
  * output tiles [M][shard columns] are TMA-stored at column `col_offset` of EVERY

@@ -347,6 +347,43 @@ int qr_sparsegpt_joint(const float* w, int64_t N, int64_t K, const int64_t* idx,
   }
 }
 
+// gptq_quantize (quantizer.cpp:292-297) / sparsegpt_joint (:299-337) with an explicit
+// Hessian sum (identity when hsum is NULL), damping fraction and clipping flag.
+int qr_gptq(const float* w, int64_t N, int64_t K, const int64_t* idx, int64_t n_out, int bits, const double* hsum,
+            int64_t tokens, double damping, int use_clipping, int sparse, uint8_t* base, float* scales,
+            float* wreduced, float* outlier_w, uint8_t* mask) {
+  try {
+    auto o = quik::OutlierSet::from_indices(K, std::vector<int64_t>(idx, idx + n_out));
+    quik::Hessian h = quik::Hessian::identity(K, damping);
+    if (hsum) {
+      h.token_count = tokens;
+      h.sum.assign(hsum, hsum + K * K);
+    }
+    auto q = sparse ? quik::sparsegpt_joint(to_fp(w, N, K), h, o, bits, use_clipping != 0)
+                    : quik::gptq_quantize(to_fp(w, N, K), h, o, bits, use_clipping != 0);
+    std::memcpy(base, q.base.data.data(), q.base.data.size());
+    std::memcpy(scales, q.scales.data(), N * 4);
+    std::memcpy(wreduced, q.wreduced.data(), N * 4);
+    if (n_out) std::memcpy(outlier_w, q.outlier_weights.data.data(), N * n_out * 4);
+    if (sparse && mask) std::memcpy(mask, q.mask.kept.data(), q.mask.kept.size());
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
+// build_hessian (quantizer.cpp:225-240) over one batch x [T][K]: the FP64 sum.
+int qr_build_hessian(const float* x, int64_t T, int64_t K, double* hsum) {
+  try {
+    std::vector<quik::FpMatrix> b{to_fp(x, T, K)};
+    quik::Hessian h = quik::build_hessian(b);
+    std::memcpy(hsum, h.sum.data(), K * K * 8);
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
 // save_layer (layer_io.cpp:7-30): writes a layer bundle exactly as the reference does
 // (the fixtures of the bundle-loader tests). mask: [N][K - n_out] or NULL; wfp32:
 // reference weights [N][K] or NULL.

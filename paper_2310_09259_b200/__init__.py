@@ -19,6 +19,8 @@ from .quik import (  # noqa: F401
     QuikLinearLayer,
     StageTimes,
     dequantize_epilogue,
+    gptq_quantize_device,
+    hessian_device,
     int_matmul,
     pack_values,
     quantize_activations,

@@ -34,6 +34,7 @@ EXPORTED_SYMBOLS = (
     "quik_set_gemm_w4", "quik_set_stream_gemm", "quik_bundle_open", "quik_bundle_weights",
     "quik_bundle_tensor", "quik_bundle_close", "quik_layer_load_bundle", "quik_layer_create_gated",
     "quik_linear_forward_weight_only", "quik_linear_forward_sharded", "quik_set_int4_decode",
+    "quik_gptq_quantize", "quik_hessian_accumulate",
 )
 
 
@@ -120,6 +121,8 @@ def load() -> C.CDLL:
             "quik_linear_forward_weight_only": (i32, [vp, vp, vp, i32, i64, vp, i32, i64, vp]),
             "quik_linear_forward_sharded": (i32, [vp, vp, vp, i32, i64, C.POINTER(vp), i32, i64, i64, vp]),
             "quik_set_int4_decode": (i32, [i32]),
+            "quik_gptq_quantize": (i32, [vp, vp, i64, i64, vp, C.c_double, vp, i64, i32, i32, i32, vp, vp, vp, vp, vp]),
+            "quik_hessian_accumulate": (i32, [vp, vp, i64, i64, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)

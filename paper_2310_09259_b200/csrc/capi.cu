@@ -973,6 +973,52 @@ quik_status quik_linear_forward_strided(quik_ctx_t ctx, quik_layer_t L, const vo
   return quik_linear_forward_ex(ctx, L, x, xdt, M, y, ydt, ldy, variant, stream, nullptr);
 }
 
+quik_status quik_gptq_quantize(quik_ctx_t ctx, const float* w, int64_t N, int64_t K, const double* hessian_sum,
+                               double damping_frac, const int64_t* outlier_indices, int64_t n_outlier, int bits,
+                               int use_clipping, int sparse, uint8_t* base, float* scales, float* wreduced,
+                               float* outlier_weights, uint8_t* mask) {
+  if (!ctx) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context");
+  if (N > 0 && (!w || !hessian_sum || !base || !scales || !wreduced || (n_outlier && !outlier_weights) ||
+                (n_outlier && !outlier_indices) || (sparse && !mask)))
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "gptq: null argument");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    GptqArgs a{};
+    a.w = w;
+    a.N = N;
+    a.K = K;
+    a.hessian_sum = hessian_sum;
+    a.damping = damping_frac;
+    a.outlier_idx = outlier_indices;
+    a.n_out = n_outlier;
+    a.bits = bits;
+    a.use_clipping = use_clipping;
+    a.sparse = sparse;
+    a.base = base;
+    a.scales = scales;
+    a.wreduced = wreduced;
+    a.outlier_weights = outlier_weights;
+    a.mask = mask;
+    std::string msg;
+    const int st = quikb200::gptq_quantize_device(a, &msg);
+    if (st == 1) return fail(QUIK_ERR_INVALID_ARGUMENT, msg);
+    if (st == 3) return fail(QUIK_ERR_NUMERICAL, msg);
+    if (st != 0) return fail(QUIK_ERR_CUDA, msg);
+    return QUIK_OK;
+  });
+}
+
+quik_status quik_hessian_accumulate(quik_ctx_t ctx, const float* x, int64_t T, int64_t K, double* h_sum) {
+  if (!ctx) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context");
+  if (T < 0 || K < 0 || (T > 0 && K > 0 && (!x || !h_sum))) return fail(QUIK_ERR_INVALID_ARGUMENT, "hessian: bad argument");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    std::string msg;
+    if (quikb200::hessian_accumulate_device(x, T, K, h_sum, &msg) != 0) return fail(QUIK_ERR_CUDA, msg);
+    return QUIK_OK;
+  });
+}
+
 quik_status quik_linear_forward_sharded(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M,
                                         void* const* y_dst, int n_dst, int64_t ldy, int64_t col_offset, void* stream) {
   if (!ctx || !L) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context or layer");

@@ -2,6 +2,8 @@
 // kernel translation units. Not part of the public ABI.
 #pragma once
 
+#include <string>
+
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -144,6 +146,25 @@ cudaError_t launch_weight_only(const WoArgs& a, int num_sms, cudaStream_t stream
 // dst[r][c] = f16(src[r][c] - f16(src[r][c])) (zero padded to pitch)
 cudaError_t launch_f16_lo_padded(const float* src, int64_t rows, int64_t cols, __half* dst, int64_t pitch,
                                  cudaStream_t stream);
+
+// GPTQ / SparseGPT on the device (gptq.cu); returns 0 ok, 1 invalid argument,
+// 3 numerical (Hessian not positive definite), 4 CUDA / library failure.
+struct GptqArgs {
+  const float* w;            // [N][K] (host or device)
+  int64_t N, K;
+  const double* hessian_sum; // [K][K] sum x x^T before damping (host or device)
+  double damping;
+  const int64_t* outlier_idx;  // host, sorted
+  int64_t n_out;
+  int bits, use_clipping, sparse;
+  uint8_t* base;             // [N][row_bytes(K - n_out)] i4p / i8
+  float* scales;             // [N]
+  float* wreduced;           // [N]
+  float* outlier_weights;    // [N][n_out]
+  uint8_t* mask;             // [N][K - n_out] when sparse (else unused)
+};
+int gptq_quantize_device(const GptqArgs& a, std::string* msg);
+int hessian_accumulate_device(const float* x, int64_t T, int64_t K, double* h_dev, std::string* msg);
 
 // 2D K-major tensor map (uint8), box {box_inner bytes, box_rows}, 128-byte swizzle or none.
 CUresult encode_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t pitch,

@@ -720,6 +720,76 @@ def rtn_quantize_weights_device(w, outliers: OutlierSet, bits: int):
     return base[: N * row_bytes(kb, bits)], scales[:N], wred[:N], ow[: N * O].view(N, O)
 
 
+def hessian_device(batches, device: Optional[int] = None):
+    """reference: build_hessian / Hessian::accumulate (quantizer.cpp:193-240) on the device:
+    the FP64 sum of x x^T over the calibration batches (host or CUDA f32 [T][K]).
+    Returns a CUDA float64 tensor [K][K] (before damping)."""
+    torch = _torch()
+    h = None
+    for x in batches:
+        xt = torch.as_tensor(x)
+        if xt.dtype != torch.float32:
+            xt = xt.float()
+        xt = xt.contiguous()
+        T, K = xt.shape
+        ctx = context(device if xt.device.type != "cuda" else xt.device.index)
+        if h is None:
+            h = torch.zeros((K, K), dtype=torch.float64, device=f"cuda:{ctx.device}")
+        if h.shape[0] != K:
+            raise ValueError(f"Hessian: batch has {K} features, expected {h.shape[0]}")
+        _lib.check(_lib.load().quik_hessian_accumulate(ctx.handle, C.c_void_p(xt.data_ptr()), T, K, _ptr(h)))
+    if h is None:
+        raise ValueError("build_hessian: no calibration tokens")
+    return h
+
+
+def gptq_quantize_device(w, outliers: OutlierSet, bits: int, hessian_sum, damping_frac: float = 0.01,
+                         use_clipping: bool = False, sparse: bool = False,
+                         device: Optional[int] = None) -> QuantizedWeights:
+    """reference: gptq_quantize (quantizer.cpp:292-297) or, sparse=True,
+    sparsegpt_joint (:299-337), computed on the device in FP64. w: f32 [out][in] (numpy
+    or torch); hessian_sum: [in][in] f64 sum of x x^T (numpy or torch, e.g.
+    hessian_device). Returns host QuantizedWeights (mask set when sparse)."""
+    torch = _torch()
+    if bits not in (4, 8):
+        raise ValueError("weight bits must be 4 or 8")
+    wt = torch.as_tensor(w).float().contiguous()
+    N, K = wt.shape
+    if K != outliers.feature_count:
+        raise ValueError(f"outlier set covers {outliers.feature_count} features, weights have {K}")
+    ht = torch.as_tensor(hessian_sum, dtype=torch.float64).contiguous()
+    if tuple(ht.shape) != (K, K):
+        raise ValueError(f"Hessian dim {ht.shape[0]} does not match weight columns {K}")
+    ctx = context(device)
+    kb = outliers.base_count()
+    O = outliers.outlier_count()
+    base = np.zeros(max(N * row_bytes(kb, bits), 1), np.uint8)
+    scales = np.zeros(max(N, 1), np.float32)
+    wred = np.zeros(max(N, 1), np.float32)
+    ow = np.zeros(max(N * O, 1), np.float32)
+    mask = np.zeros(max(N * kb, 1), np.uint8) if sparse else None
+    idx = np.ascontiguousarray(outliers.indices, dtype=np.int64)
+    if wt.device.type == "cpu":
+        wt = wt.numpy()
+        wptr = C.c_void_p(wt.ctypes.data)
+    else:
+        wptr = C.c_void_p(wt.data_ptr())
+    if ht.device.type == "cpu":
+        ht = ht.numpy()
+        hptr = C.c_void_p(ht.ctypes.data)
+    else:
+        hptr = C.c_void_p(ht.data_ptr())
+    _lib.check(_lib.load().quik_gptq_quantize(
+        ctx.handle, wptr, N, K, hptr, C.c_double(damping_frac), C.c_void_p(idx.ctypes.data if idx.size else None), O,
+        bits, int(use_clipping), int(sparse), C.c_void_p(base.ctypes.data), C.c_void_p(scales.ctypes.data),
+        C.c_void_p(wred.ctypes.data), C.c_void_p(ow.ctypes.data), C.c_void_p(mask.ctypes.data) if sparse else None))
+    qw = QuantizedWeights(PackedIntMatrix(N, kb, bits, base[: N * row_bytes(kb, bits)]), scales[:N],
+                          ow[: N * O].reshape(N, O), wred[:N])
+    if sparse:
+        qw.mask = mask[: N * kb].reshape(N, kb)
+    return qw
+
+
 def rtn_quantize_weights(w: np.ndarray, outliers: OutlierSet, bits: int) -> QuantizedWeights:
     """reference: rtn_quantize_weights (quantizer.hpp:87-88), use_clipping = false.
     Host f32 [out][in] in, QuantizedWeights (host arrays) out; computed on the GPU."""

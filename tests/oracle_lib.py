@@ -257,6 +257,35 @@ class Ref(_Base):
         return st, dict(base=base[: N * row_bytes(kb, bits)], scales=sc[:N], wreduced=wr[:N],
                         outlier_weights=ow[: N * idx.size].reshape(N, idx.size), mask=mask[: N * kb].reshape(N, kb))
 
+    def gptq(self, w, idx, bits, hsum=None, tokens=1, damping=0.01, use_clipping=False, sparse=False):
+        """The reference's gptq_quantize / sparsegpt_joint with an explicit Hessian sum."""
+        w = np.ascontiguousarray(w, np.float32)
+        N, K = w.shape
+        idx = np.ascontiguousarray(idx, np.int64)
+        kb = K - idx.size
+        base = np.zeros(max(N * row_bytes(kb, bits), 1), np.uint8)
+        sc = np.zeros(max(N, 1), np.float32)
+        wr = np.zeros(max(N, 1), np.float32)
+        ow = np.zeros(max(N * idx.size, 1), np.float32)
+        mask = np.zeros(max(N * kb, 1), np.uint8)
+        h = None if hsum is None else np.ascontiguousarray(hsum, np.float64)
+        fn = self.f("gptq")
+        fn.argtypes = None
+        st = fn(_p(w), C.c_int64(N), C.c_int64(K), _p(idx), C.c_int64(idx.size), C.c_int(bits),
+                _p(h) if h is not None else None, C.c_int64(tokens), C.c_double(damping), C.c_int(int(use_clipping)),
+                C.c_int(int(sparse)), _p(base), _p(sc), _p(wr), _p(ow), _p(mask))
+        return st, dict(base=base[: N * row_bytes(kb, bits)], scales=sc[:N], wreduced=wr[:N],
+                        outlier_weights=ow[: N * idx.size].reshape(N, idx.size),
+                        mask=mask[: N * kb].reshape(N, kb) if sparse else None)
+
+    def build_hessian(self, x):
+        x = np.ascontiguousarray(x, np.float32)
+        T, K = x.shape
+        h = np.zeros((K, K), np.float64)
+        st = self.f("build_hessian")(_p(x), C.c_int64(T), C.c_int64(K), _p(h))
+        assert st == 0, st
+        return h
+
     def gated_mlp(self, up, gate, down, x):
         """The reference's forward_model(gated_mlp_ops): -> (st, out, h = silu(gate) * up)."""
         hs = [self.layer_create(L) for L in (up, gate, down)]

@@ -1012,3 +1012,84 @@ def test_decode_path_under_graph_capture():
             assert torch.equal(y.view(torch.int16), want.view(torch.int16))
     finally:
         lib.quik_set_int4_decode(1)
+
+
+# --------------------------------------------------------------------------- GPU GPTQ / SparseGPT (§8f.4)
+
+
+def _gptq_case(rng, N, K, O, T, heavy=2):
+    w = (rng.normal(0.0, 0.5, size=(N, K))).astype(np.float32)
+    x = rng.normal(0.0, 1.0, size=(T, K)).astype(np.float32)
+    for _ in range(heavy):
+        x[:, int(rng.integers(0, K))] *= 20.0
+    idx = np.sort(rng.choice(K, size=O, replace=False)).astype(np.int64)
+    return w, x, idx
+
+
+@pytest.mark.parametrize("sparse", [0, 1])
+def test_gptq_identity_hessian_bit_exact(sparse):
+    """H = I: no error compensation, so the device GPTQ / SparseGPT equal the
+    reference's bit for bit (codes, scales, wreduced, outlier weights, 2:4 mask), with
+    and without the clip search, 4 and 8 bits."""
+    m = q()
+    r = ref()
+    rng = np.random.default_rng(31 + sparse)
+    for bits in (4, 8):
+        for clip in (False, True):
+            N, K, O = 48, 200, 8
+            w, _, idx = _gptq_case(rng, N, K, O, 1)
+            st, want = r.gptq(w, idx, bits, None, 1, 0.01, clip, bool(sparse))
+            assert st == 0
+            got = m.gptq_quantize_device(w, m.OutlierSet.from_indices(K, idx), bits, np.eye(K), 0.01, clip, bool(sparse))
+            np.testing.assert_array_equal(got.base.data, want["base"])
+            np.testing.assert_array_equal(got.scales.view(np.uint32), want["scales"].view(np.uint32))
+            np.testing.assert_array_equal(got.wreduced.view(np.uint32), want["wreduced"].view(np.uint32))
+            np.testing.assert_array_equal(got.outlier_weights, want["outlier_weights"])
+            if sparse:
+                np.testing.assert_array_equal(got.mask, want["mask"])
+
+
+@pytest.mark.parametrize("sparse", [0, 1])
+def test_gptq_matches_reference(sparse):
+    """Calibrated Hessians (heavy activation columns): the device GPTQ / SparseGPT vs
+    the reference's gptq_quantize / sparsegpt_joint on the same Hessian. The Cholesky
+    factor (cuSOLVER) and the blocked trailing updates (DGEMM) differ from the
+    reference's loops only by FP64 rounding, so codes, masks and scales agree exactly
+    and the outlier weights to float rounding; crossing a block boundary (K > 64) and
+    a trailing partial block are covered."""
+    m = q()
+    r = ref()
+    rng = np.random.default_rng(41 + sparse)
+    for (N, K, O, T, bits, clip) in [(64, 96, 4, 256, 4, False), (40, 333, 16, 512, 4, True),
+                                     (96, 256, 0, 300, 8, False), (33, 150, 10, 128, 8, True)]:
+        w, x, idx = _gptq_case(rng, N, K, O, T)
+        h = r.build_hessian(x)
+        st, want = r.gptq(w, idx, bits, h, T, 0.01, clip, bool(sparse))
+        assert st == 0
+        got = m.gptq_quantize_device(w, m.OutlierSet.from_indices(K, idx), bits, h, 0.01, clip, bool(sparse))
+        codes_got = m.unpack_values(got.base)
+        codes_want = m.unpack_values(m.PackedIntMatrix(N, K - O, bits, want["base"]))
+        agree = float((codes_got == codes_want).mean())
+        assert agree == 1.0, (N, K, O, agree)
+        np.testing.assert_array_equal(got.scales.view(np.uint32), want["scales"].view(np.uint32))
+        np.testing.assert_array_equal(got.wreduced.view(np.uint32), want["wreduced"].view(np.uint32))
+        np.testing.assert_allclose(got.outlier_weights, want["outlier_weights"], rtol=1e-6, atol=1e-6)
+        if sparse:
+            np.testing.assert_array_equal(got.mask, want["mask"])
+
+
+def test_hessian_device_and_not_positive_definite():
+    """The FP64 Hessian sum on the device equals the reference's to FP64 rounding; a
+    Hessian that stays singular after damping (zero trace) raises NumericalError like
+    the reference (quantizer.cpp:84-91)."""
+    m = q()
+    r = ref()
+    rng = np.random.default_rng(5)
+    x = rng.normal(size=(300, 72)).astype(np.float32)
+    h = m.hessian_device([x[:100], x[100:]]).cpu().numpy()
+    np.testing.assert_allclose(h, r.build_hessian(x), rtol=1e-12, atol=1e-9)
+    w = rng.normal(size=(8, 72)).astype(np.float32)
+    st, _ = r.gptq(w, np.array([], np.int64), 4, np.zeros((72, 72)), 1, 0.01)
+    assert st == 3  # reference: NumericalError
+    with pytest.raises(m.NumericalError):
+        m.gptq_quantize_device(w, m.OutlierSet.from_indices(72, []), 4, np.zeros((72, 72)))
