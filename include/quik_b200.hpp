@@ -520,4 +520,90 @@ inline QuantizedWeights rtn_quantize_weights(const FpMatrix& w, const OutlierSet
   return q;
 }
 
+// quantizer.hpp:18-31: the calibration statistic H = sum x x^T (FP64), accumulated on
+// the device (quik_hessian_accumulate), kept on the host like the reference's.
+struct Hessian {
+  int64_t dim = 0;
+  int64_t token_count = 0;
+  std::vector<double> sum;  // row-major dim x dim, before damping
+  double damping_frac = 0.01;
+
+  void accumulate(const FpMatrix& batch) {
+    if (dim == 0 && token_count == 0) {
+      dim = batch.cols;
+      sum.assign(static_cast<size_t>(dim * dim), 0.0);
+    }
+    if (batch.cols != dim)
+      throw std::invalid_argument("Hessian: batch has " + std::to_string(batch.cols) + " features, expected " +
+                                  std::to_string(dim));
+    if (batch.rows > 0) {
+      detail::Buf dh(sum.data(), sum.size() * 8);
+      detail::check(quik_hessian_accumulate(detail::ctx(), batch.data.data(), batch.rows, batch.cols,
+                                            static_cast<double*>(dh.p)));
+      dh.get(sum.data(), sum.size() * 8);
+    }
+    token_count += batch.rows;
+  }
+  double at(int64_t i, int64_t j) const { return sum[static_cast<size_t>(i * dim + j)]; }
+  static Hessian identity(int64_t dim, double damping_frac = 0.01) {
+    Hessian h;
+    h.dim = dim;
+    h.token_count = 1;
+    h.damping_frac = damping_frac;
+    h.sum.assign(static_cast<size_t>(dim * dim), 0.0);
+    for (int64_t i = 0; i < dim; ++i) h.sum[static_cast<size_t>(i * dim + i)] = 1.0;
+    return h;
+  }
+};
+
+// quantizer.cpp:225-240
+inline Hessian build_hessian(const std::vector<FpMatrix>& batches, double damping_frac = 0.01) {
+  Hessian h;
+  h.damping_frac = damping_frac;
+  for (const FpMatrix& b : batches) h.accumulate(b);
+  if (h.token_count == 0) throw std::invalid_argument("build_hessian: no calibration tokens");
+  return h;
+}
+
+namespace detail {
+inline QuantizedWeights gptq_device(const FpMatrix& w, const Hessian& h, const OutlierSet& o, int bits,
+                                    bool use_clipping, bool sparse) {
+  if (h.dim != w.cols)
+    throw std::invalid_argument("Hessian dim " + std::to_string(h.dim) + " does not match weight columns " +
+                                std::to_string(w.cols));
+  if (o.feature_count != w.cols)
+    throw std::invalid_argument("outlier set covers " + std::to_string(o.feature_count) + " features, weights have " +
+                                std::to_string(w.cols));
+  QuantizedWeights q;
+  q.base.rows = w.rows;
+  q.base.cols = o.base_count();
+  q.base.bits = bits;
+  q.base.data.resize(static_cast<size_t>(w.rows * q.base.row_bytes()));
+  q.scales.resize(static_cast<size_t>(w.rows));
+  q.wreduced.resize(static_cast<size_t>(w.rows));
+  q.outlier_weights = FpMatrix(w.rows, o.outlier_count());
+  if (sparse) {
+    q.mask.rows = w.rows;
+    q.mask.cols = o.base_count();
+    q.mask.kept.resize(static_cast<size_t>(w.rows * o.base_count()));
+  }
+  if (w.rows == 0) return q;
+  check(quik_gptq_quantize(ctx(), w.data.data(), w.rows, w.cols, h.sum.data(), h.damping_frac, o.indices.data(),
+                           o.outlier_count(), bits, use_clipping ? 1 : 0, sparse ? 1 : 0, q.base.data.data(),
+                           q.scales.data(), q.wreduced.data(), q.outlier_weights.data.data(),
+                           sparse ? q.mask.kept.data() : nullptr));
+  return q;
+}
+}  // namespace detail
+
+// quantizer.cpp:292-297 / :299-337 on the device (FP64; quik_gptq_quantize)
+inline QuantizedWeights gptq_quantize(const FpMatrix& w, const Hessian& h, const OutlierSet& o, int bits,
+                                      bool use_clipping = false) {
+  return detail::gptq_device(w, h, o, bits, use_clipping, false);
+}
+inline QuantizedWeights sparsegpt_joint(const FpMatrix& w, const Hessian& h, const OutlierSet& o, int bits,
+                                        bool use_clipping = false) {
+  return detail::gptq_device(w, h, o, bits, use_clipping, true);
+}
+
 }  // namespace quik::b200

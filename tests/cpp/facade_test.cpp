@@ -211,6 +211,44 @@ int main(int argc, char** argv) {
     R.mode = Q::LayerMode::FpReference;
     CHECK(throws<std::invalid_argument>([&] { Q::quik_matmul(R, Q::FpMatrix(1, 8)); }));
   }
+  // GPTQ / SparseGPT on the device through the reference signatures (quantizer.hpp:18-90):
+  // H = I means no compensation, so gptq_quantize equals RTN bit for bit; a calibrated
+  // Hessian from build_hessian matches the host FP64 sum; sparsegpt_joint's mask keeps
+  // exactly two of every full group of four (quantizer.cpp:299-337)
+  {
+    std::mt19937 rng(211);
+    std::normal_distribution<float> nd(0.f, 1.f);
+    const int64_t N = 24, K = 136, O = 8;
+    Q::FpMatrix w(N, K), x(64, K);
+    for (float& v : w.data) v = 0.5f * nd(rng);
+    for (float& v : x.data) v = nd(rng);
+    std::vector<int64_t> idx(O);
+    qo_select_outliers(x.data.data(), 64, K, O, idx.data());
+    const auto o = Q::OutlierSet::from_indices(K, idx);
+    const auto g = Q::gptq_quantize(w, Q::Hessian::identity(K), o, 4);
+    const auto rt = Q::rtn_quantize_weights(w, o, 4);
+    CHECK(g.base.data == rt.base.data);
+    CHECK(std::memcmp(g.scales.data(), rt.scales.data(), N * 4) == 0);
+    const Q::Hessian h = Q::build_hessian({x});
+    double maxrel = 0;
+    for (int64_t i = 0; i < K; ++i)
+      for (int64_t j = 0; j < K; ++j) {
+        double ref = 0;
+        for (int64_t t = 0; t < 64; ++t) ref += double(x.data[t * K + i]) * double(x.data[t * K + j]);
+        maxrel = std::max(maxrel, std::fabs(h.at(i, j) - ref) / (std::fabs(ref) + 1e-9));
+      }
+    CHECK(h.token_count == 64 && maxrel < 1e-12);
+    const auto sp = Q::sparsegpt_joint(w, h, o, 4);
+    bool groups_ok = sp.mask.rows == N && sp.mask.cols == K - O;
+    for (int64_t r = 0; r < N && groups_ok; ++r)
+      for (int64_t gi = 0; gi < (K - O) / 4; ++gi) {
+        int kept = 0;
+        for (int e = 0; e < 4; ++e) kept += sp.mask.kept_at(r, 4 * gi + e);
+        groups_ok = groups_ok && kept == 2;
+      }
+    CHECK(groups_ok);
+    CHECK(throws<std::invalid_argument>([&] { Q::gptq_quantize(w, Q::Hessian::identity(K + 1), o, 4); }));
+  }
   // validation (runtime.cpp:150-167)
   {
     Q::QuikLinearLayer L;
