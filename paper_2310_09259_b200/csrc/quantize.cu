@@ -694,6 +694,15 @@ __global__ void __launch_bounds__(512) quantize_hot_kernel(const QuantArgs a, in
       }
     }
     __syncthreads();  // (B) codes complete
+    // this row's compaction descriptors (row-independent, L1-resident): all loads in
+    // flight before the outlier gather instead of one at a time in the copy-out loop
+    constexpr int kCk = VPT > 1 ? VPT / 2 : 1;
+    uint4 dpre[kCk];
+#pragma unroll
+    for (int k = 0; k < kCk; ++k) {
+      const int cidx = tid + k * nt;
+      dpre[k] = cidx < nchunk ? __ldg(cdesc + cidx) : make_uint4(0xFFFFFFFFu, 0u, 0u, 0u);
+    }
 
     // ---- outliers (ascending index order, runtime.cpp:217) from the row in the ring
     if (a.xo16) {
@@ -712,11 +721,10 @@ __global__ void __launch_bounds__(512) quantize_hot_kernel(const QuantArgs a, in
     // ---- compacted code row: two-window chunks, then the general chunks
     uint4* dst = reinterpret_cast<uint4*>(a.q8 + static_cast<int64_t>(t) * a.kpad);
 #pragma unroll
-    for (int k = 0; k < (VPT > 1 ? VPT / 2 : 1); ++k) {
+    for (int k = 0; k < kCk; ++k) {
       const int cidx = tid + k * nt;
-      if (cidx >= nchunk) break;
-      const uint4 d = __ldg(cdesc + cidx);
-      if (d.x == 0xFFFFFFFFu) continue;  // general chunk (second loop)
+      const uint4 d = dpre[k];
+      if (d.x == 0xFFFFFFFFu) continue;  // general chunk (second loop) or past the row
       const uint32_t* wa = reinterpret_cast<const uint32_t*>(s_codes + (d.x & 0xFFFFu));
       const uint32_t* wb = reinterpret_cast<const uint32_t*>(s_codes + (d.y & 0xFFFFu));
       const uint32_t sa = d.x >> 16, sb = d.y >> 16;
