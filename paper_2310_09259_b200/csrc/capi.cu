@@ -1111,9 +1111,9 @@ quik_status quik_linear_forward_host(quik_ctx_t ctx, quik_layer_t L, const void*
     const size_t xe = xdt == QUIK_F32 ? 4 : 2, ye = ydt == QUIK_F32 ? 4 : 2;
     // Chunking: copy-in of chunk c+1, the two kernels of chunk c and copy-out of
     // chunk c-1 run concurrently (PCIe is full duplex; the copies dominate). About
-    // 8 chunks, each a multiple of 256 tokens (whole CTA-pair tiles).
+    // 16 chunks (pipeline fill / drain ~1/16 of the copies), each a multiple of 256 tokens.
     int64_t chunk = chunk_tokens;
-    if (chunk == 0) chunk = std::max<int64_t>(256, round_up((M + 7) / 8, 256));
+    if (chunk == 0) chunk = std::max<int64_t>(256, round_up((M + 15) / 16, 256));
     if ((M + chunk - 1) / chunk > kMaxHostChunks) chunk = (M + kMaxHostChunks - 1) / kMaxHostChunks;
     const int64_t nchunks = (M + chunk - 1) / chunk;
     char* xd = static_cast<char*>(ctx->xdev.ensure(static_cast<size_t>(M * K) * xe));
