@@ -239,7 +239,7 @@ quik_status quik_linear_forward_weight_only(quik_ctx_t ctx, quik_layer_t layer, 
  * quik_matmul(layer, FpMatrix) call (runtime.hpp:85-87) does with host data.
  * x_host [M][in_features] and y_host [M][out_features] are host memory (page-locked
  * for full overlap). The token rows are processed in chunks of `chunk_tokens`
- * (0 = automatic, about 8 chunks of multiples of 256): the host->device copy of
+ * (0 = automatic, about 16 chunks of multiples of 256): the host->device copy of
  * chunk c+1, the V3 kernels of chunk c and the device->host copy of chunk c-1 run
  * concurrently on context-owned copy streams. Asynchronous on `stream`: y_host is
  * complete once `stream` reaches this point (synchronise or use quik_ctx_sync). */
