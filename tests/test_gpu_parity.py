@@ -1093,3 +1093,34 @@ def test_hessian_device_and_not_positive_definite():
     assert st == 3  # reference: NumericalError
     with pytest.raises(m.NumericalError):
         m.gptq_quantize_device(w, m.OutlierSet.from_indices(72, []), 4, np.zeros((72, 72)))
+
+
+def test_sharded_quik_linear_nccl_world1():
+    """The torch.distributed path of ShardedQuikLinear over NCCL on the device (world
+    size 1 here: one GPU): shard upload, forward and all-gather equal the unsharded
+    layer bit for bit."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    m = q()
+    from paper_2310_09259_b200.sharded import ShardedQuikLinear
+
+    rng = np.random.default_rng(12)
+    L, x, _ = make_layer(rng, 96, 512, 384, 4, 16, heavy_cols=2)
+    layer = to_layer(L)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29543")
+    created = not dist.is_initialized()
+    if created:
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        xt = torch.from_numpy(x).cuda().half()
+        got = ShardedQuikLinear(layer, device=0).forward(xt)
+        want = m.QuikLinear(layer)(xt)
+        torch.cuda.synchronize()
+        assert torch.equal(got.view(torch.int16), want.view(torch.int16))
+    finally:
+        if created:
+            dist.destroy_process_group()
