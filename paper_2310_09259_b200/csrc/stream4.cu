@@ -25,6 +25,7 @@
 // issuers, 1 activation-tile producer.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -134,7 +135,9 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // K1's codes are complete
+  // PDL: only the roles that read K1's outputs (the code-tile producer; the epilogue,
+  // which finalises with the per-token scales and outlier columns) wait for K1; the
+  // weight stream and its widening start while K1 is still running.
 
   const int tiles_n = (p.N + kBlockM - 1) / kBlockM;
   const int num_units = tiles_n * p.splits;
@@ -152,6 +155,7 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
       const uint64_t pol_w = policy_evict_first();  // weights stream once
       const uint64_t pol_x = policy_evict_last();   // code / x_o tiles are re-read by every block
       const bool wprod = warp == 0;
+      if (!wprod) asm volatile("griddepcontrol.wait;" ::: "memory");  // K1's codes are complete
       int bc = 0;
       for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
         int nb, k0, k1;
@@ -255,6 +259,7 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
     // epilogue (4 warps): TMEM lane = weight row n, column = token t
     const int quad = warp & 3;
     const bool lead = warp == C::kWidenEnd;  // issues the finalisation TMA loads / MMAs
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // K1's scales / outlier columns
     int it = 0, bc0 = 0, fin_uses = 0;
     for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
       int nb, k0, k1;
@@ -467,6 +472,11 @@ cudaError_t launch_stream4(const Stream4Args& a, int num_sms, cudaStream_t strea
     const long long cost = waves * ((sp.nstage + s - 1) / s + 1);
     if (best < 0 || cost < best) { best = cost; splits = s; }
   }
+  static const int splits_env = [] {  // tuning: QUIK_S4_SPLITS forces the K split count
+    const char* e = getenv("QUIK_S4_SPLITS");
+    return e ? atoi(e) : 0;
+  }();
+  if (splits_env > 0) splits = std::min(splits_env, sp.nstage);
   sp.splits = splits;
   sp.acc = a.acc;
   sp.counters = a.counters;
