@@ -441,8 +441,8 @@ cudaError_t launch_s4(const S4Params& sp, int num_sms, cudaStream_t stream) {
 }  // namespace
 
 // Measured (profiles/r1_stream4.jsonl, K1 + this kernel, graph replay): OPT-66B fc1
-// (9216 -> 36864, 256 outliers) M = 1: 44 us, M = 16: 47 us (fused kernel on INT8 tiles:
-// 65 us; cuBLAS f16: 111 us); cfg1 4096^2 M = 16: 16.6 us (18.6). On for 4-bit layers
+// (9216 -> 36864, 256 outliers) M = 1: 43 us, M = 16: 45.5 us (fused kernel on INT8
+// tiles: 65 us; cuBLAS f16: 110 us); cfg1 4096^2 M = 16: 14.6 us (18.6). On for 4-bit layers
 // at M <= 32 (QUIK_STREAM4=0 / quik_set_int4_decode(0) disables).
 int gemm_stream4_auto = [] {
   const char* e = getenv("QUIK_STREAM4");

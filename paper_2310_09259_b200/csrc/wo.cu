@@ -170,7 +170,8 @@ __global__ void __launch_bounds__(WCfg<BN>::kThreads, 1) wo_gemm_kernel(const __
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // the token planes are complete
+  // PDL: only the token / outlier-tile producer reads the planes kernel's output and
+  // waits for it; the weight stream and its widening start right away
   asm volatile("griddepcontrol.launch_dependents;");   // let the finalize kernel launch early
 
   const int tiles_n = (p.N + kBlockM - 1) / kBlockM;
@@ -196,6 +197,7 @@ __global__ void __launch_bounds__(WCfg<BN>::kThreads, 1) wo_gemm_kernel(const __
       const uint64_t pol_w = p.tiles_t == 1 ? policy_evict_first() : policy_evict_normal();
       const uint64_t pol_x = policy_evict_last();
       const bool wprod = warp == 0;  // warp 0: weight ring; last warp: token + outlier rings
+      if (!wprod) asm volatile("griddepcontrol.wait;" ::: "memory");  // the token planes are complete
       int bc = 0, oc = 0, gi = 0;
       for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
         int nb, tb, s, i0, i1;
