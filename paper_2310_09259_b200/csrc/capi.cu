@@ -805,7 +805,7 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
   // layers over every SM; default on (QUIK_STREAM4=0 disables). Needs the INT4 weight
   // copy, made on the first such forward outside stream capture.
   const bool small = variant == QUIK_V3_FUSED_EPILOGUE && M <= 64 && L->kpad && !L->sparse && !g_probe_mode;
-  const bool auto4 = small && quikb200::gemm_stream4_auto && L->bits == 4 && M <= 32 && !L->gated;
+  const bool auto4 = small && quikb200::gemm_stream4_auto && L->bits == 4 && M <= 32;
   ensure_w4(L, st, auto4);
   bool decode = auto4 && L->w4 && !quikb200::gemm_stream;
   if (decode) {
@@ -842,6 +842,7 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
     a.out = y;
     a.ldo = ldy;
     a.out_f16 = ydt == QUIK_F16;
+    a.gated = L->gated;
     a.peer_out = peers;
     a.n_peer = n_peer;
     const char* msg = nullptr;

@@ -111,6 +111,7 @@ struct Stream4Args {
   void* out;
   int64_t ldo;
   int out_f16;
+  int gated;           // gated MLP layer (rows interleave up / gate): out is [M][N / 2]
   void* const* peer_out;
   int n_peer;
 };

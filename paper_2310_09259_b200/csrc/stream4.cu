@@ -82,6 +82,7 @@ struct S4Params {
   void* out;
   long long ldo;
   int out_f16;
+  int gated;              // rows interleave up / gate (32-row blocks): out is [M][N / 2]
   int n_dst;              // 1 + peers
   void* dst[8];           // output base pointers (dst[0] == out)
 };
@@ -383,12 +384,48 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
       }
       named_barrier_sync(1, 128);
       tc_fence_after();
-      // (3) drain: f16 / f32 to every destination
+      // (3) drain: f16 / f32 to every destination. Gated MLP layers (rows interleave up /
+      // gate in blocks of 32: quadrants 0, 2 up, 1, 3 gate) emit h = silu(gate) * up at
+      // output feature nb * 64 + (quad / 2) * 32 + lane, like the fused epilogue: the gate
+      // warp hands silu(g) to its up warp through shared memory (the free finalisation
+      // buffer) between two 64-thread named barriers.
+      float* xch = reinterpret_cast<float*>(fin) + (quad >> 1) * 1024;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t v[32];
         tmem_ld32(tfin + c, v);
         tmem_ld_wait();
+        if (p.gated) {
+          const int pair_bar = 2 + (quad >> 1);
+          if (quad & 1) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float g = __uint_as_float(v[j]);
+              xch[j * 32 + lane] = __fdividef(g, 1.0f + __expf(-g));
+            }
+            named_barrier_sync(pair_bar, 64);
+            named_barrier_sync(pair_bar, 64);  // the up warp has read the exchange buffer
+            continue;
+          }
+          named_barrier_sync(pair_bar, 64);
+          const int f = nb * (kBlockM / 2) + (quad >> 1) * 32 + lane;
+          if (n < p.N) {
+#pragma unroll
+            for (int j = 0; j < (BN < 32 ? BN : 32); ++j) {
+              const int t = c + j;
+              if (t >= p.M) continue;
+              const float h = __fmul_rn(xch[j * 32 + lane], __uint_as_float(v[j]));
+              for (int di = 0; di < p.n_dst; ++di) {
+                if (p.out_f16)
+                  static_cast<__half*>(p.dst[di])[static_cast<long long>(t) * p.ldo + f] = __float2half_rn(h);
+                else
+                  static_cast<float*>(p.dst[di])[static_cast<long long>(t) * p.ldo + f] = h;
+              }
+            }
+          }
+          named_barrier_sync(pair_bar, 64);
+          continue;
+        }
         if (n < p.N) {
 #pragma unroll
           for (int j = 0; j < (BN < 32 ? BN : 32); ++j) {
@@ -489,6 +526,7 @@ cudaError_t launch_stream4(const Stream4Args& a, int num_sms, cudaStream_t strea
   sp.out = a.out;
   sp.ldo = a.ldo;
   sp.out_f16 = a.out_f16;
+  sp.gated = a.gated;
   sp.n_dst = 1 + a.n_peer;
   sp.dst[0] = a.out;
   for (int i = 0; i < a.n_peer; ++i) sp.dst[1 + i] = a.peer_out[i];

@@ -1124,3 +1124,29 @@ def test_sharded_quik_linear_nccl_world1():
     finally:
         if created:
             dist.destroy_process_group()
+
+
+def test_gated_projection_decode_kernel_bit_identical():
+    """4-bit gated projections at M <= 32 run the INT4 decode kernel, whose finalisation
+    pairs the gate / up quadrants like the fused epilogue: identical bits to the fused
+    path (decode off), f32 and f16 out, full layer and a 64-feature row shard."""
+    m = q()
+    import torch
+
+    lib = m.load_library()
+    rng = np.random.default_rng(4242)
+    try:
+        for (M, K, F, O) in [(1, 512, 256, 32), (16, 1024, 640, 0), (29, 768, 384, 64)]:
+            up, gate, down, x = _mlp_layers(rng, M, K, F, 4, 8, O, 0)
+            xt = torch.from_numpy(x).cuda().half()
+            for rb, re_ in [(0, 0), (64, 192)]:
+                proj = m.QuikLinear.gated(to_layer(up), to_layer(gate), row_begin=rb, row_end=re_)
+                for dt in (torch.float32, torch.float16):
+                    lib.quik_set_int4_decode(0)
+                    want = proj(xt, out_dtype=dt)
+                    lib.quik_set_int4_decode(1)
+                    got = proj(xt, out_dtype=dt)
+                    u = torch.int32 if dt == torch.float32 else torch.int16
+                    assert torch.equal(got.view(u), want.view(u)), (M, F, rb, dt)
+    finally:
+        lib.quik_set_int4_decode(1)
