@@ -277,9 +277,10 @@ quik_status quik_set_gemm_w4(int on);
  * 4-bit layers. */
 quik_status quik_set_stream_gemm(int on, int int4);
 
-/* Tuning: 4-bit layers at M <= 32 run the INT4 decode kernel (stream4.cu: INT4 weights
- * widened into TMEM, split-K over all SMs, the fused epilogue in the same kernel;
- * bit-identical to the fused path). Default on; 0 = the fused kernel on INT8 tiles. */
+/* Tuning: dense layers at M <= 32 run the decode kernel (stream4.cu: split-K over all
+ * SMs on INT4 weights widened into TMEM (4-bit) or INT8 tiles (8-bit), the fused
+ * epilogue in the same kernel; bit-identical to the fused path). Default on; 0 = the
+ * fused kernel. */
 quik_status quik_set_int4_decode(int on);
 
 /* Diagnostics (process-wide): when on, the V3 forward runs the fused GEMM

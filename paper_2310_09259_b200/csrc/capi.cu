@@ -805,9 +805,9 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
   // layers over every SM; default on (QUIK_STREAM4=0 disables). Needs the INT4 weight
   // copy, made on the first such forward outside stream capture.
   const bool small = variant == QUIK_V3_FUSED_EPILOGUE && M <= 64 && L->kpad && !L->sparse && !g_probe_mode;
-  const bool auto4 = small && quikb200::gemm_stream4_auto && L->bits == 4 && M <= 32;
-  ensure_w4(L, st, auto4);
-  bool decode = auto4 && L->w4 && !quikb200::gemm_stream;
+  const bool auto4 = small && quikb200::gemm_stream4_auto && M <= 32;
+  ensure_w4(L, st, auto4 && L->bits == 4);
+  bool decode = auto4 && (L->bits == 4 ? L->w4 != nullptr : L->w8 != nullptr) && !quikb200::gemm_stream;
   if (decode) {
     // under stream capture no workspace may be (re)allocated: use the fused path when
     // the decode workspace / counters are not sized yet (a warm-up call sizes them)
@@ -823,7 +823,8 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
     run_k1(ctx, L, x, xdt, M, st);
     if (mid_event) QK_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(mid_event), st));
     Stream4Args a{};
-    a.w4 = L->w4;
+    a.w4 = L->bits == 4 ? L->w4 : nullptr;
+    a.w8 = L->w8;
     a.x = static_cast<const int8_t*>(ctx->q8.p);
     a.kpad = L->kpad;
     a.M = M;

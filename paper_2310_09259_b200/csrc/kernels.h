@@ -98,7 +98,8 @@ cudaError_t launch_stream_gemm(const StreamArgs& a, int num_sms, cudaStream_t st
 // Decode-regime quik forward on INT4 weights after K1 (stream4.cu): split-K integer
 // GEMM (TMEM-widened A, kind::i8), outlier MMAs and the dequant epilogue in one kernel.
 struct Stream4Args {
-  const uint8_t* w4;   // [N][kpad / 2] device INT4 layout
+  const uint8_t* w4;   // [N][kpad / 2] device INT4 layout (4-bit layers)
+  const int8_t* w8;    // [N][kpad] (8-bit layers, when w4 is null)
   const int8_t* x;     // [M][kpad] activation codes (K1)
   int64_t kpad, M, N;
   const __half* wo;    // [N][opad]

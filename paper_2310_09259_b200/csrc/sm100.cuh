@@ -370,6 +370,14 @@ __device__ __forceinline__ void mma_f16_ss_e(uint32_t d, uint64_t adesc, uint64_
       : "memory");
 }
 
+__device__ __forceinline__ void mma_i8_ss_e(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
 // D[tmem] (+)= A[tmem] * B[smem]^T, int8 -> int32 (A: lane = row, column j = 4 int8
 // {k = 4j .. 4j+3}, K = 32 per instruction = 8 columns; tools/ts_probe.cu)
 __device__ __forceinline__ void mma_i8_ts_e(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,

@@ -70,7 +70,8 @@ struct S4Params {
   CUtensorMap tm_x;   // int8 [M][kpad], box {128 B, BN}, SW128
   CUtensorMap tm_wo;  // f16 [N][opad] as bytes, box {128 B, 128}, SW128
   CUtensorMap tm_xo;  // f16 [M][opad] as bytes, box {128 B, BN}, SW128
-  int M, N, nstage, splits, nout;  // nstage: 256-K stages over kpad; nout: 64-column outlier blocks
+  int M, N, nstage, splits, nout;  // nstage: K stages (INT4 256 K, INT8 128 K); nout: 64-column outlier blocks
+  int w8;                          // INT8 weights (A from the weight ring, no widening)
   int32_t* acc;                    // [M][N] int32 workspace (zero on entry and exit)
   int* counters;                   // [tiles] arrivals per weight block (zero on entry and exit)
   const float* a_scale;
@@ -121,7 +122,8 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
   }
   if (warp == 1) {
     if (lane == 0) {
-      for (int i = 0; i < C::kStagesW; ++i) { mbar_init(&full_w[i], 1); mbar_init(&empty_w[i], 4); }
+      // INT4: a weight slot is released by its 4 widening warps; INT8: by its issuer's commit
+      for (int i = 0; i < C::kStagesW; ++i) { mbar_init(&full_w[i], 1); mbar_init(&empty_w[i], p.w8 ? 1 : 4); }
       for (int i = 0; i < C::kStagesT; ++i) { mbar_init(&full_t[i], 1); mbar_init(&empty_t[i], 1); }
       mbar_init(fin_full, 1);
       mbar_init(fin_mma, 1);
@@ -172,9 +174,14 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
               const int st = bc % C::kStagesT;
               mbar_wait_sleep(&empty_t[st], ((bc / C::kStagesT) & 1) ^ 1);
               uint8_t* slot = ring_t + st * C::kSlotT;
-              mbar_arrive_expect_tx(&full_t[st], C::kSlotT);
-              tma_load_2d(slot, &p.tm_x, (2 * i) * kKBlockBytes, 0, &full_t[st], pol_x);
-              tma_load_2d(slot + C::kTAtom, &p.tm_x, (2 * i + 1) * kKBlockBytes, 0, &full_t[st], pol_x);
+              if (p.w8) {  // 128-K stages: one code atom
+                mbar_arrive_expect_tx(&full_t[st], C::kTAtom);
+                tma_load_2d(slot, &p.tm_x, i * kKBlockBytes, 0, &full_t[st], pol_x);
+              } else {
+                mbar_arrive_expect_tx(&full_t[st], C::kSlotT);
+                tma_load_2d(slot, &p.tm_x, (2 * i) * kKBlockBytes, 0, &full_t[st], pol_x);
+                tma_load_2d(slot + C::kTAtom, &p.tm_x, (2 * i + 1) * kKBlockBytes, 0, &full_t[st], pol_x);
+              }
             }
           }
         }
@@ -197,11 +204,26 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
       for (int i = k0; i < k1; ++i, ++bc) {
         if (bc % G != g) continue;
         const int st = bc % C::kStagesT;
+        const uint64_t bd0 = umma_desc_sw128(smem_u32(ring_t + st * C::kSlotT));
+        if (p.w8) {
+          // INT8 weights: A straight from the weight ring (SS MMAs), 128 K per stage
+          const int sw = bc % C::kStagesW;
+          mbar_wait(&full_w[sw], (bc / C::kStagesW) & 1);
+          mbar_wait(&full_t[st], (bc / C::kStagesT) & 1);
+          tc_fence_after();
+          const uint64_t ad = umma_desc_sw128(smem_u32(ring_w + sw * kS4WBytes));
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            mma_i8_ss_e(d, ad + 2 * j, bd0 + 2 * j, idesc_i8, (first && j == 0) ? 0u : 1u);
+          first = false;
+          commit_e(&empty_w[sw]);
+          commit_e(&empty_t[st]);
+          continue;
+        }
         mbar_wait_spin(&a_full[g], (bc / G) & 1);          // A widened into TMEM
         mbar_wait(&full_t[st], (bc / C::kStagesT) & 1);    // code tile landed
         tc_fence_after();
         const uint32_t a_tm = tmem_base + g * kS4TmemA;
-        const uint64_t bd0 = umma_desc_sw128(smem_u32(ring_t + st * C::kSlotT));
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           mma_i8_ts_e(d, a_tm + 8 * j, bd0 + (j >> 2) * (C::kTAtom >> 4) + 2 * (j & 3), idesc_i8,
@@ -220,7 +242,7 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
     const int r = quad * 32 + lane;
     const uint32_t a_tm = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + g * kS4TmemA;
     int bc = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+    for (int u = blockIdx.x; u < num_units && !p.w8; u += gridDim.x) {  // (INT8: nothing to widen)
       int nb, k0, k1;
       decode(u, nb, k0, k1);
       for (int i = k0; i < k1; ++i, ++bc) {
@@ -492,13 +514,14 @@ cudaError_t launch_stream4(const Stream4Args& a, int num_sms, cudaStream_t strea
   *err_msg = nullptr;
   if (a.M == 0 || a.N == 0) return cudaSuccess;
   if (a.M > 64) { *err_msg = "INT4 stream GEMM: M > 64"; return cudaErrorInvalidValue; }
-  if (!a.w4 || a.kpad == 0) { *err_msg = "INT4 stream GEMM: no INT4 weights"; return cudaErrorInvalidValue; }
+  if ((!a.w4 && !a.w8) || a.kpad == 0) { *err_msg = "decode GEMM: no weights"; return cudaErrorInvalidValue; }
   if (a.n_peer < 0 || a.n_peer > 7) { *err_msg = "INT4 stream GEMM: at most 7 peer outputs"; return cudaErrorInvalidValue; }
   const int bn = a.M <= 16 ? 16 : (a.M <= 32 ? 32 : 64);
   S4Params sp{};
   sp.M = static_cast<int>(a.M);
   sp.N = static_cast<int>(a.N);
-  sp.nstage = static_cast<int>((a.kpad + 255) / 256);
+  sp.w8 = a.w4 ? 0 : 1;
+  sp.nstage = static_cast<int>(sp.w8 ? a.kpad / 128 : (a.kpad + 255) / 256);
   sp.nout = static_cast<int>(a.opad / 64);
   // K splits: minimise the busiest CTA's stage count (see wo.cu)
   const long long tiles = (a.N + kBlockM - 1) / kBlockM;
@@ -531,7 +554,8 @@ cudaError_t launch_stream4(const Stream4Args& a, int num_sms, cudaStream_t strea
   sp.dst[0] = a.out;
   for (int i = 0; i < a.n_peer; ++i) sp.dst[1 + i] = a.peer_out[i];
   // the INT4 rows hold kpad / 2 bytes; a 256-K stage past kpad reads zeros (OOB fill)
-  CUresult r = encode_map_2d(&sp.tm_w, a.w4, a.kpad / 2, a.N, a.kpad / 2, kKBlockBytes, kBlockM, true);
+  CUresult r = sp.w8 ? encode_map_2d(&sp.tm_w, a.w8, a.kpad, a.N, a.kpad, kKBlockBytes, kBlockM, true)
+                     : encode_map_2d(&sp.tm_w, a.w4, a.kpad / 2, a.N, a.kpad / 2, kKBlockBytes, kBlockM, true);
   if (r == CUDA_SUCCESS) r = encode_map_2d(&sp.tm_x, a.x, a.kpad, a.M, a.kpad, kKBlockBytes, static_cast<uint32_t>(bn), true);
   if (r == CUDA_SUCCESS && sp.nout) {
     r = encode_map_2d(&sp.tm_wo, a.wo, a.opad * 2, a.N, a.opad * 2, kKBlockBytes, kBlockM, true);

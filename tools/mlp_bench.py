@@ -58,11 +58,14 @@ def timeit(fn, iters=20):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
+    ap.add_argument("--tokens", type=int, default=0, help="override M (e.g. 1 / 16 for decode)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     for name, M, H, F, O, Od, b_ud, b_d in SHAPES:
         if args.only and args.only not in name:
             continue
+        if args.tokens:
+            M = args.tokens
         g = torch.Generator(device=dev).manual_seed(5)
         outl, tu = device_layer(dev, H, F, O, b_ud, g)
         _, tg = device_layer(dev, H, F, O, b_ud, g, idx=outl.indices)
