@@ -1150,3 +1150,35 @@ def test_gated_projection_decode_kernel_bit_identical():
                     assert torch.equal(got.view(u), want.view(u)), (M, F, rb, dt)
     finally:
         lib.quik_set_int4_decode(1)
+
+
+def test_decode_kernel_fuzz_bit_identical():
+    """60 random small-M layers (M 1-32, ragged K / N, 0-256 outliers, 4 and 8 bits,
+    with and without bias, f16 / f32 out): the decode kernel equals the fused kernel
+    bit for bit, and repeated calls stay identical (workspace / counters reset)."""
+    m = q()
+    import torch
+
+    lib = m.load_library()
+    rng = np.random.default_rng(2024)
+    try:
+        for trial in range(60):
+            bits = 4 if trial % 2 == 0 else 8
+            M = int(rng.integers(1, 33))
+            K = int(rng.integers(64, 3000))
+            N = int(rng.integers(1, 1500))
+            O = int(min(rng.choice([0, 8, 64, 256]), K // 4))
+            L, x, _ = make_layer(rng, M, K, N, bits, O, heavy_cols=2, with_bias=bool(trial % 3))
+            dev = m.QuikLinear(to_layer(L))
+            xt = torch.from_numpy(x).cuda()
+            dt = torch.float16 if trial % 4 < 2 else torch.float32
+            lib.quik_set_int4_decode(0)
+            want = dev(xt, out_dtype=dt)
+            lib.quik_set_int4_decode(1)
+            got1 = dev(xt, out_dtype=dt)
+            got2 = dev(xt, out_dtype=dt)
+            u = torch.int16 if dt == torch.float16 else torch.int32
+            assert torch.equal(got1.view(u), want.view(u)), (trial, M, K, N, O, bits)
+            assert torch.equal(got2.view(u), want.view(u)), (trial, "repeat")
+    finally:
+        lib.quik_set_int4_decode(1)
