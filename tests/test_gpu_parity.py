@@ -1182,3 +1182,28 @@ def test_decode_kernel_fuzz_bit_identical():
             assert torch.equal(got2.view(u), want.view(u)), (trial, "repeat")
     finally:
         lib.quik_set_int4_decode(1)
+
+
+def test_weight_only_fuzz():
+    """30 random layers through the weight-only kernel (M 1-40, ragged K / N, 0-128
+    outliers, 4 / 8 bits, f32 in): rel Frobenius < 1e-6 vs FP64 (the reference test's
+    bar) and repeat calls bit-identical."""
+    from oracle_lib import rel_frobenius, weight_only_f64
+
+    m = q()
+    import torch
+
+    rng = np.random.default_rng(77)
+    for trial in range(30):
+        bits = 4 if trial % 2 == 0 else 8
+        M = int(rng.integers(1, 41))
+        K = int(rng.integers(32, 2500))
+        N = int(rng.integers(1, 1200))
+        O = int(min(rng.choice([0, 4, 32, 128]), K // 4))
+        L, x, _ = make_layer(rng, M, K, N, bits, O, heavy_cols=2, with_bias=bool(trial % 3), fp16_inputs=False)
+        dev = m.QuikLinear(to_layer(L))
+        xt = torch.from_numpy(x).cuda()
+        y1 = dev.weight_only(xt, out_dtype=torch.float32).cpu().numpy()
+        y2 = dev.weight_only(xt, out_dtype=torch.float32).cpu().numpy()
+        assert rel_frobenius(weight_only_f64(L, x), y1) < 1e-6, (trial, M, K, N, O, bits)
+        np.testing.assert_array_equal(y1.view(np.uint32), y2.view(np.uint32))
