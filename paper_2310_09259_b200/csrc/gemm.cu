@@ -207,9 +207,13 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  // Programmatic dependent launch: everything above overlapped the previous
-  // kernel (the quantizer); wait for its results before touching them.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // Programmatic dependent launch: everything above overlapped the previous kernel
+  // (the quantizer); wait for its results before touching them. Dense tiles: the
+  // producer first issues the weight loads of its first ring stages (weights do not
+  // depend on K1) and waits before the token tiles; the epilogue waits before reading
+  // the per-token scales; the MMA warp only reads what the producer staged.
+  constexpr bool kEarlyW = !SP && !W4 && !MC;
+  if constexpr (!kEarlyW) asm volatile("griddepcontrol.wait;" ::: "memory");
 
   const int tiles_m = (p.M + BN - 1) / BN;
   const int tiles_n = (p.N + C::kTileRows - 1) / C::kTileRows;
@@ -286,11 +290,31 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
         wrow = nb * C::kTileRows + static_cast<int>(rank) * kBlockM;
         trow = mb * BN + static_cast<int>(rank) * C::kBRows;
       };
+      int pre = 0;  // integer blocks of the first tile whose weight tiles went out early
+      if constexpr (kEarlyW) {
+        int wr0 = 0, tr0 = 0;
+        if (cluster_id < num_tiles) {
+          rows_of(cluster_id, wr0, tr0);
+          pre = h_a < C::kStages ? h_a : C::kStages;
+          for (int kb = 0; kb < pre; ++kb) {  // fresh ring stages 0 .. pre-1
+            stage = kb;
+            if (leader) mbar_arrive_expect_tx(&full[kb], CG * C::kOutStageBytes);
+            tma(smem + kb * C::kStageBytes, &p.tm_w, kb * kKBlockBytes, wr0, pol_w);
+          }
+        }
+        asm volatile("griddepcontrol.wait;" ::: "memory");  // K1's codes are complete
+        for (int kb = 0; kb < pre; ++kb) {
+          stage = kb;
+          tma_b(smem + kb * C::kStageBytes + C::kABytes, &p.tm_x, kb * kKBlockBytes, tr0, pol_x);
+        }
+        stage = pre == C::kStages ? 0 : pre;
+        phase = pre == C::kStages ? 1u : 0u;
+      }
       int prev = -1;
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         int wr, tr;
         rows_of(tile, wr, tr);
-        for (int kb = 0; kb < h_a; ++kb) load_int(kb, wr, tr);
+        for (int kb = (tile == cluster_id ? pre : 0); kb < h_a; ++kb) load_int(kb, wr, tr);
         if (two_phase && prev >= 0) {
           int pw, pt;
           rows_of(prev, pw, pt);
@@ -453,6 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
       widen(kb_int - h_a);
     }
   } else if (warp >= kEpiWarp0) {
+    if constexpr (kEarlyW) asm volatile("griddepcontrol.wait;" ::: "memory");  // per-token scales, acc_in
     const int e = warp - kEpiWarp0;
     const int q = warp & 3;  // TMEM lane quadrant (hardware: lanes 32*(warp%4) .. +31)
     const int h = e >> 2;
