@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
   // producer first issues the weight loads of its first ring stages (weights do not
   // depend on K1) and waits before the token tiles; the epilogue waits before reading
   // the per-token scales; the MMA warp only reads what the producer staged.
-  constexpr bool kEarlyW = !SP && !W4 && !MC;
+  constexpr bool kEarlyW = !W4 && !MC;
   if constexpr (!kEarlyW) asm volatile("griddepcontrol.wait;" ::: "memory");
 
   const int tiles_m = (p.M + BN - 1) / BN;
@@ -298,14 +298,26 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
           pre = h_a < C::kStages ? h_a : C::kStages;
           for (int kb = 0; kb < pre; ++kb) {  // fresh ring stages 0 .. pre-1
             stage = kb;
-            if (leader) mbar_arrive_expect_tx(&full[kb], CG * C::kOutStageBytes);
-            tma(smem + kb * C::kStageBytes, &p.tm_w, kb * kKBlockBytes, wr0, pol_w);
+            uint8_t* sa = smem + kb * C::kStageBytes;
+            if (leader) mbar_arrive_expect_tx(&full[kb], CG * (SP ? C::kIntStageBytes : C::kOutStageBytes));
+            tma(sa, &p.tm_w, kb * kKBlockBytes, wr0, pol_w);
+            if constexpr (SP) {  // 2:4 metadata of the stage (a weight-side tensor too)
+              uint8_t* se = sa + C::kABytes + C::kBBytes;
+              tma(se, &p.tm_e, 0, (2 * kb) * p.meta_rows + wr0, pol_w);
+              tma(se + kMetaTileBytes / 2, &p.tm_e, 0, (2 * kb + 1) * p.meta_rows + wr0, pol_w);
+            }
           }
         }
         asm volatile("griddepcontrol.wait;" ::: "memory");  // K1's codes are complete
         for (int kb = 0; kb < pre; ++kb) {
           stage = kb;
-          tma_b(smem + kb * C::kStageBytes + C::kABytes, &p.tm_x, kb * kKBlockBytes, tr0, pol_x);
+          uint8_t* sb = smem + kb * C::kStageBytes + C::kABytes;
+          if constexpr (SP) {
+            tma_b(sb, &p.tm_x, kb * 2 * kKBlockBytes, tr0, pol_x);
+            tma_b(sb + C::kBAtomBytes, &p.tm_x, kb * 2 * kKBlockBytes + kKBlockBytes, tr0, pol_x);
+          } else {
+            tma_b(sb, &p.tm_x, kb * kKBlockBytes, tr0, pol_x);
+          }
         }
         stage = pre == C::kStages ? 0 : pre;
         phase = pre == C::kStages ? 1u : 0u;
