@@ -326,6 +326,9 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         int wr, tr;
         rows_of(tile, wr, tr);
+        // last tile of this CTA: the next kernel (the next layer's quantizer) may start
+        // its prologue on SMs this grid has left
+        if (tile + num_clusters >= num_tiles) asm volatile("griddepcontrol.launch_dependents;");
         for (int kb = (tile == cluster_id ? pre : 0); kb < h_a; ++kb) load_int(kb, wr, tr);
         if (two_phase && prev >= 0) {
           int pw, pt;

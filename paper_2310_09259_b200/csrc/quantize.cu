@@ -521,6 +521,10 @@ __global__ void __launch_bounds__(512) quantize_hot_kernel(const QuantArgs a, in
   if (tid < 16) reinterpret_cast<uint32_t*>(s_codes0 + (tid >> 3) * code_stride + kr16)[tid & 7] = 0u;  // zero tails
   __syncthreads();
   if (tid == 0) {
+    // PDL: everything above (tables, barriers) overlapped the previous kernel; its
+    // outputs may be this layer's input and it may still read this kernel's output
+    // buffers, so the first row loads (and hence every write) come after the wait
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     for (int s = 0; s < stages; ++s) {
       const int r = blockIdx.x + s * gridDim.x;
       if (r >= M) break;
@@ -1029,7 +1033,18 @@ cudaError_t launch_quantize_hot(const QuantArgs& a, cudaStream_t stream) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);                       \
     if (e != cudaSuccess) return e;                                                                        \
     const int64_t grid = std::min<int64_t>(a.M, static_cast<int64_t>(std::max(per_sm, 1)) * sms);          \
-    kern<<<static_cast<unsigned>(grid), threads, smem, stream>>>(a, stages, row_stride);                   \
+    cudaLaunchConfig_t cfg{};                                                                              \
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));                                                       \
+    cfg.blockDim = dim3(threads);                                                                          \
+    cfg.dynamicSmemBytes = smem;                                                                           \
+    cfg.stream = stream;                                                                                   \
+    cudaLaunchAttribute attr[1];                                                                           \
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                                       \
+    attr[0].val.programmaticStreamSerializationAllowed = 1;                                                \
+    cfg.attrs = attr;                                                                                      \
+    cfg.numAttrs = 1;                                                                                      \
+    e = cudaLaunchKernelEx(&cfg, kern, a, stages, row_stride);                                             \
+    if (e != cudaSuccess) return e;                                                                        \
   } while (0)
   if (vpt == 1) QUIK_QH_LAUNCH(1);
   else if (vpt == 2) QUIK_QH_LAUNCH(2);

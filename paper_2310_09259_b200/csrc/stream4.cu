@@ -163,6 +163,8 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
       for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
         int nb, k0, k1;
         decode(u, nb, k0, k1);
+        if (wprod && u + static_cast<int>(gridDim.x) >= num_units)
+          asm volatile("griddepcontrol.launch_dependents;");  // last unit: the next kernel may start its prologue
         {
           for (int i = k0; i < k1; ++i, ++bc) {
             if (wprod) {
