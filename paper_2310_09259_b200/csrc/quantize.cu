@@ -467,8 +467,8 @@ __device__ __forceinline__ float sub_f16_f32(uint32_t h, float c) {
   return d;
 }
 
-template <int BITS, int VPT>
-__global__ void __launch_bounds__(512) quantize_hot_kernel(const QuantArgs a, int stages, int row_stride) {
+template <int BITS, int VPT, bool FULL>
+__global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(const QuantArgs a, int stages, int row_stride) {
   extern __shared__ __align__(128) uint8_t s_dyn[];
   __shared__ float s_min[16], s_max[16];
   __shared__ int s_nf[16];
@@ -483,6 +483,8 @@ __global__ void __launch_bounds__(512) quantize_hot_kernel(const QuantArgs a, in
   const int K = static_cast<int>(a.K);
   const int M = static_cast<int>(a.M);
   const int nvec = K >> 3;
+  // FULL: nvec == blockDim * VPT (host checked), every vector slot is in the row
+  auto in_row = [&](int v) { return FULL || v < nvec; };
   const int kb = static_cast<int>(a.kb);
   const int kr16 = (K + 15) & ~15;
   const uint32_t row_bytes = static_cast<uint32_t>(K) * 2u;
@@ -501,7 +503,7 @@ __global__ void __launch_bounds__(512) quantize_hot_kernel(const QuantArgs a, in
 #pragma unroll
   for (int i = 0; i < VPT; ++i) {
     const int v = tid + i * nt;
-    lm[i] = (has_out && v < nvec) ? __ldg(reinterpret_cast<const uint2*>(a.lane_mask) + v) : make_uint2(0u, 0u);
+    lm[i] = (has_out && in_row(v)) ? __ldg(reinterpret_cast<const uint2*>(a.lane_mask) + v) : make_uint2(0u, 0u);
   }
 
   // row-independent: this thread's outlier slots (i = tid, tid + nt) -> source column, -1 = zero pad
@@ -546,7 +548,7 @@ __global__ void __launch_bounds__(512) quantize_hot_kernel(const QuantArgs a, in
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       const int v = tid + i * nt;
-      raw[i] = v < nvec ? srow[v] : make_uint4(0, 0, 0, 0);
+      raw[i] = in_row(v) ? srow[v] : make_uint4(0, 0, 0, 0);
     }
     // ---- pass 1: packed min / max over the base columns
     __half2 hmin = u2h2(0x7C007C00u), hmax = u2h2(0xFC00FC00u);
@@ -555,7 +557,7 @@ __global__ void __launch_bounds__(512) quantize_hot_kernel(const QuantArgs a, in
       const uint32_t fill = h0 | (h0 << 16);  // a base value of this row, in both halves
 #pragma unroll
       for (int i = 0; i < VPT; ++i) {
-        if (tid + i * nt >= nvec) continue;
+        if (!in_row(tid + i * nt)) continue;
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
           const uint32_t mk = __byte_perm(w < 2 ? lm[i].x : lm[i].y, 0u, (w & 1) ? 0x3322u : 0x1100u);
@@ -567,7 +569,7 @@ __global__ void __launch_bounds__(512) quantize_hot_kernel(const QuantArgs a, in
     } else {
 #pragma unroll
       for (int i = 0; i < VPT; ++i) {
-        if (tid + i * nt >= nvec) continue;
+        if (!in_row(tid + i * nt)) continue;
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
           const __half2 x2 = u2h2((&raw[i].x)[w]);
@@ -613,7 +615,7 @@ __global__ void __launch_bounds__(512) quantize_hot_kernel(const QuantArgs a, in
 #pragma unroll
       for (int i = 0; i < VPT; ++i) {
         const int v = tid + i * nt;
-        if (v >= nvec) continue;
+        if (!in_row(v)) continue;
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const float x = elem<__half>(raw[i], e);
@@ -661,7 +663,7 @@ __global__ void __launch_bounds__(512) quantize_hot_kernel(const QuantArgs a, in
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       const int v = tid + i * nt;
-      if (v >= nvec) continue;
+      if (!in_row(v)) continue;
       uint32_t tb[8];
       uint32_t diff = 0;
 #pragma unroll
@@ -1021,12 +1023,13 @@ cudaError_t launch_quantize_hot(const QuantArgs& a, cudaStream_t stream) {
   int stages = static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(8, (ring_kb * 1024) / row_stride)));
   while (stages > 2 && codes + stages * row_stride > 200 * 1024) --stages;  // (2 stages: no prefetch overlap)
   const int smem = codes + stages * row_stride;
+  const bool full = static_cast<int64_t>(threads) * vpt == nvec;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
 #define QUIK_QH_LAUNCH(V)                                                                                  \
   do {                                                                                                     \
-    auto kern = quantize_hot_kernel<B, V>;                                                                 \
+    auto kern = full ? quantize_hot_kernel<B, V, true> : quantize_hot_kernel<B, V, false>;                  \
     cudaError_t e = ensure_smem_attr(kern, smem);                                                          \
     if (e != cudaSuccess) return e;                                                                        \
     int per_sm = 0;                                                                                        \
