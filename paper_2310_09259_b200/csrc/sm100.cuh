@@ -186,9 +186,12 @@ __device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const CUtensorMap
       : "memory");
 }
 
-// Named barrier among `count` threads (multiple of 32) of the CTA.
+// Named barrier among `count` threads (multiple of 32) of the CTA, called by whole
+// warps. The non-.aligned form: lanes of a warp need not arrive converged (after
+// lane-0-only branches the compiler may not have reconverged them; bar.sync, the
+// .aligned form, is then undefined and compute-sanitizer synccheck flags it).
 __device__ __forceinline__ void named_barrier_sync(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
 // ------------------------------------------------------------------ clusters
