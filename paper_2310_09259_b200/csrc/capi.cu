@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <cstdio>
 #include <cstring>
@@ -33,6 +34,19 @@ cudaError_t ensure_smem_attr_impl(const void* kernel, int bytes) {
   if (it != done.end() && it->second >= bytes) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess) done[{kernel, dev}] = bytes;
+  return e;
+}
+// Resident CTAs per SM, queried once per (kernel, device, block size, smem bytes).
+cudaError_t occupancy_cached_impl(const void* kernel, int threads, int smem, int* per_sm) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int, int>, int> seen;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = seen.find({kernel, dev, threads, smem});
+  if (it != seen.end()) { *per_sm = it->second; return cudaSuccess; }
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kernel, threads, smem);
+  if (e == cudaSuccess) seen[{kernel, dev, threads, smem}] = *per_sm;
   return e;
 }
 }  // namespace quikb200

@@ -25,6 +25,11 @@ template <typename K>
 cudaError_t ensure_smem_attr(K kernel, int bytes) {
   return ensure_smem_attr_impl(reinterpret_cast<const void*>(kernel), bytes);
 }
+cudaError_t occupancy_cached_impl(const void* kernel, int threads, int smem, int* per_sm);  // capi.cu
+template <typename K>
+cudaError_t occupancy_cached(K kernel, int threads, int smem, int* per_sm) {
+  return occupancy_cached_impl(reinterpret_cast<const void*>(kernel), threads, smem, per_sm);
+}
 
 // Output of the fused layer: y = f16/f32( (bias + dequant(acc)) + x_out . W_out^T ),
 // where the outlier product is accumulated by the tensor cores onto the f32

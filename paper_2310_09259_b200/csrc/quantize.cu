@@ -488,10 +488,11 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(cons
   const int kb = static_cast<int>(a.kb);
   const int kr16 = (K + 15) & ~15;
   const uint32_t row_bytes = static_cast<uint32_t>(K) * 2u;
-  // two code rows (double-buffered so that one barrier per row can be dropped), then the ring
+  // one code row (written after barrier A of row t+1, read before it for row t), then
+  // the ring
   const int code_stride = (kr16 + 32 + 127) & ~127;
-  uint8_t* s_codes0 = s_dyn;                         // [2][code_stride]: codes by column, zero tail
-  uint8_t* s_ring = s_dyn + 2 * code_stride;         // [stages][row_stride]
+  uint8_t* s_codes = s_dyn;                          // [code_stride]: codes by column, zero tail
+  uint8_t* s_ring = s_dyn + code_stride;             // [stages][row_stride]
   const bool has_out = a.lane_mask != nullptr;
   const int nchunk = static_cast<int>(a.kpad >> 4);
   const __half* xg = reinterpret_cast<const __half*>(a.x);
@@ -520,7 +521,7 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(cons
     for (int s = 0; s < stages; ++s) mbar_init(&s_full[s], 1);
     fence_mbar_init();
   }
-  if (tid < 16) reinterpret_cast<uint32_t*>(s_codes0 + (tid >> 3) * code_stride + kr16)[tid & 7] = 0u;  // zero tails
+  if (tid < 8) reinterpret_cast<uint32_t*>(s_codes + kr16)[tid] = 0u;  // zero tail
   __syncthreads();
   if (tid == 0) {
     // PDL: everything above (tables, barriers) overlapped the previous kernel; its
@@ -535,13 +536,11 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(cons
     }
   }
 
-  int s = 0, s_prev = -1;
-  uint32_t ph = 0, cb = 0;
-  int t_prev = -1;
+  int s = 0;
+  uint32_t ph = 0;
 #pragma unroll 1
-  for (int t = blockIdx.x; t < M; t += gridDim.x, cb ^= 1u) {
+  for (int t = blockIdx.x; t < M; t += gridDim.x) {
     const uint4* srow = reinterpret_cast<const uint4*>(s_ring + s * row_stride);
-    uint8_t* s_codes = s_codes0 + cb * code_stride;
     mbar_wait(&s_full[s], ph);
 
     uint4 raw[VPT];
@@ -549,6 +548,13 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(cons
     for (int i = 0; i < VPT; ++i) {
       const int v = tid + i * nt;
       raw[i] = in_row(v) ? srow[v] : make_uint4(0, 0, 0, 0);
+    }
+    // this row's outlier values (the ring slot is refilled at barrier A)
+    uint16_t xov[2] = {0, 0};
+    if (a.xo16 && xo_hoisted) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (osrc[j] >= 0) xov[j] = reinterpret_cast<const uint16_t*>(srow)[osrc[j]];
     }
     // ---- pass 1: packed min / max over the base columns
     __half2 hmin = u2h2(0x7C007C00u), hmax = u2h2(0xFC00FC00u);
@@ -592,14 +598,15 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(cons
     vmax = redux_max(vmax);
     nonfinite = __reduce_or_sync(0xffffffffu, nonfinite);
     if ((tid & 31) == 0) { s_min[tid >> 5] = vmin; s_max[tid >> 5] = vmax; s_nf[tid >> 5] = nonfinite; }
-    __syncthreads();  // (A): also, every thread is done with the previous row
-    if (tid == 0 && s_prev >= 0) {
-      // refill the previous row's ring slot (its last reader passed barrier A)
-      const int rn = t_prev + stages * gridDim.x;
+    __syncthreads();  // (A): every thread is done with the previous row and holds this one in registers
+    if (tid == 0) {
+      // refill this row's ring slot: after A nothing reads it (row in registers,
+      // outlier values read above, the rare exact-division path selects from registers)
+      const int rn = t + stages * gridDim.x;
       if (rn < M) {
         fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&s_full[s_prev], row_bytes);
-        bulk_load_1d(s_ring + s_prev * row_stride, xg + static_cast<int64_t>(rn) * a.ldx, row_bytes, &s_full[s_prev]);
+        mbar_arrive_expect_tx(&s_full[s], row_bytes);
+        bulk_load_1d(s_ring + s * row_stride, xg + static_cast<int64_t>(rn) * a.ldx, row_bytes, &s_full[s]);
       }
     }
     {
@@ -686,14 +693,19 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(cons
     if (near_vec) {
       // rare: elements whose brackets straddle a rounding boundary take the exact
       // IEEE quotient, rounded half away from zero (runtime.cpp:58)
-      const __half* row = reinterpret_cast<const __half*>(srow);
 #pragma unroll 1
       for (uint32_t nv = near_vec; nv; nv &= nv - 1) {
-        const int v = tid + (__ffs(nv) - 1) * nt;
-#pragma unroll 1
+        const int iv = __ffs(nv) - 1;
+        const int v = tid + iv * nt;
+        uint4 rv = raw[0];
+#pragma unroll
+        for (int i = 1; i < VPT; ++i)
+          if (i == iv) rv = raw[i];
+#pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int c = v * 8 + e;
-          const float d = __fsub_rn(__half2float(row[c]), vmin);
+          const uint32_t hw = (&rv.x)[e >> 1];
+          const float d = __fsub_rn(__half2float(__ushort_as_half(static_cast<unsigned short>((e & 1) ? hw >> 16 : hw & 0xFFFFu))), vmin);
           if (__float_as_uint(__fmaf_rn(d, rcp_lo, kMagic)) != __float_as_uint(__fmaf_rn(d, rcp_hi, kMagic)))
             s_codes[c] = static_cast<uint8_t>(static_cast<int>(quant_slow(d, scale)) - kHr);
         }
@@ -712,16 +724,16 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(cons
 
     // ---- outliers (ascending index order, runtime.cpp:217) from the row in the ring
     if (a.xo16) {
-      const uint16_t* row = reinterpret_cast<const uint16_t*>(srow);
       uint16_t* xo = reinterpret_cast<uint16_t*>(a.xo16) + static_cast<int64_t>(t) * opad;
       if (xo_hoisted) {
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int i = tid + j * nt;
-          if (i < opad) xo[i] = osrc[j] >= 0 ? row[osrc[j]] : static_cast<uint16_t>(0);
+          if (i < opad) xo[i] = xov[j];
         }
-      } else {
-        for (int i = tid; i < opad; i += nt) xo[i] = (has_out && i < a.n_out) ? row[__ldg(&a.out_src[i])] : 0;
+      } else {  // more outliers than 2 per thread: from global memory (L2: the row was just read)
+        const uint16_t* xrow = reinterpret_cast<const uint16_t*>(xg + static_cast<int64_t>(t) * a.ldx);
+        for (int i = tid; i < opad; i += nt) xo[i] = (has_out && i < a.n_out) ? xrow[__ldg(&a.out_src[i])] : 0;
       }
     }
     // ---- compacted code row: two-window chunks, then the general chunks
@@ -756,8 +768,6 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(cons
       }
       dst[cidx] = make_uint4(w[0], w[1], w[2], w[3]);
     }
-    s_prev = s;
-    t_prev = t;
     if (++s == stages) { s = 0; ph ^= 1u; }
   }
 }
@@ -1014,14 +1024,15 @@ cudaError_t launch_quantize_hot(const QuantArgs& a, cudaStream_t stream) {
   const int threads = static_cast<int>(round_up((nvec + vpt - 1) / vpt, 32));
   if (a.kpad / 16 > static_cast<int64_t>(vpt > 1 ? vpt / 2 : 1) * threads) return cudaErrorNotSupported;
   const int row_stride = static_cast<int>(round_up(a.K * 2, 128));
-  const int codes = 2 * static_cast<int>(round_up(round_up(a.K, 16) + 32, 128));
-  // ring depth: about 32 KB of rows per CTA (at least 2 stages), <= 8 stages
+  const int codes = static_cast<int>(round_up(round_up(a.K, 16) + 32, 128));
+  // ring depth: about 32 KB of rows per CTA (a slot is refilled as soon as its row is in
+  // registers, so one stage still overlaps the next row's load), <= 8 stages
   static const int ring_kb = [] {  // tuning knob: QUIK_K1_RING_KB (ring bytes per CTA)
     const char* e = getenv("QUIK_K1_RING_KB");
     return e ? atoi(e) : 32;
   }();
   int stages = static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(8, (ring_kb * 1024) / row_stride)));
-  while (stages > 2 && codes + stages * row_stride > 200 * 1024) --stages;  // (2 stages: no prefetch overlap)
+  while (stages > 1 && codes + stages * row_stride > 200 * 1024) --stages;
   const int smem = codes + stages * row_stride;
   const bool full = static_cast<int64_t>(threads) * vpt == nvec;
   int dev = 0, sms = 148;
@@ -1033,7 +1044,7 @@ cudaError_t launch_quantize_hot(const QuantArgs& a, cudaStream_t stream) {
     cudaError_t e = ensure_smem_attr(kern, smem);                                                          \
     if (e != cudaSuccess) return e;                                                                        \
     int per_sm = 0;                                                                                        \
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);                       \
+    e = occupancy_cached(kern, threads, smem, &per_sm);                                                    \
     if (e != cudaSuccess) return e;                                                                        \
     const int64_t grid = std::min<int64_t>(a.M, static_cast<int64_t>(std::max(per_sm, 1)) * sms);          \
     cudaLaunchConfig_t cfg{};                                                                              \
