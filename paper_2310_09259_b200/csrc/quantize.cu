@@ -1019,8 +1019,17 @@ cudaError_t launch_quantize_t(const QuantArgs& a, cudaStream_t stream) {
 template <int B>
 cudaError_t launch_quantize_hot(const QuantArgs& a, cudaStream_t stream) {
   const int64_t nvec = a.K / 8;
+  // about 4 warps per row (measured: 128-thread rows beat 256-thread ones at cfg2 q/k/v/o
+  // 12.1 -> 10.7 us and cfg3 28.8 -> 28.2 us; fewer threads per block barrier)
   int vpt = 1;
-  while (vpt < 8 && (nvec + vpt - 1) / vpt > 256) vpt *= 2;
+  while (vpt < 8 && (nvec + vpt - 1) / vpt > 128) vpt *= 2;
+  static const int vpt_env = [] {  // tuning knob: QUIK_K1_VPT forces 16-byte vectors per thread
+    const char* e = getenv("QUIK_K1_VPT");
+    return e ? atoi(e) : 0;
+  }();
+  if ((vpt_env == 1 || vpt_env == 2 || vpt_env == 4 || vpt_env == 8) &&
+      (nvec + vpt_env - 1) / vpt_env <= (vpt_env >= 8 ? 512 : 256))  // the kernel's launch bounds
+    vpt = vpt_env;
   const int threads = static_cast<int>(round_up((nvec + vpt - 1) / vpt, 32));
   if (a.kpad / 16 > static_cast<int64_t>(vpt > 1 ? vpt / 2 : 1) * threads) return cudaErrorNotSupported;
   const int row_stride = static_cast<int>(round_up(a.K * 2, 128));
