@@ -614,6 +614,20 @@ def to_sparse_layer(L):
     return layer
 
 
+def test_hot_quantizer_ring_wrap_and_many_outliers():
+    """The hot K1 with more rows than CTAs x ring stages (every ring slot refilled at
+    barrier A of its row, several times per CTA) at the BASELINE row widths, and with
+    more outlier columns than two per thread (the outlier gather from global memory)."""
+    m = q()
+    o = oracle()
+    rng = np.random.default_rng(7100)
+    for K, M, O, bits in [(1024, 20000, 600, 4), (2048, 3000, 700, 8), (8192, 2500, 256, 4), (28672, 700, 896, 8)]:
+        x = rng.normal(0, 1, size=(M, K)).astype(np.float16)
+        idx = np.sort(rng.choice(K, size=O, replace=False)).astype(np.int64)
+        x[:, idx[::3]] *= 30
+        _hot_k1_case(m, o, x, idx, bits)
+
+
 def make_sparse_layer(rng, M, K, N, bits, O, heavy_cols=2):
     """RTN layer whose permuted base weights are pruned 2:4 by magnitude (the two
     smallest |w| of every aligned group of 4 base columns -> 0) before quantization."""
