@@ -326,30 +326,38 @@ def test_cfg1_oracle_shape():
     assert rel_frob(want, y16) < 5e-4
 
 
-def test_large_layer_token_subset_exact():
+@pytest.mark.parametrize("M,K,N,bits,O", [(1024, 8192, 4096, 4, 0), (4096, 1024, 8192, 4, 0), (3000, 2048, 6000, 8, 0),
+                                         (4096, 1024, 8192, 4, 128), (2500, 2048, 5000, 8, 256)])
+def test_large_layer_token_subset_exact(M, K, N, bits, O):
     """Full-size property: tokens and output rows are independent, so the oracle on a
-    subset of tokens and rows checks the full-size device run exactly (O = 0, f32)."""
+    subset of tokens and rows checks the full-size device run (O = 0: exactly, f32).
+    The 4096 x 8192 / 3000 x 6000 outputs are several tiles per persistent CTA (pair):
+    TMEM accumulator double buffering and the tile scheduler's phases across tiles."""
     m = q()
     o = oracle()
     import torch
 
-    rng = np.random.default_rng(43)
-    M, K, N = 1024, 8192, 4096
-    L, x, _ = make_layer(rng, M, K, N, 4, 0, heavy_cols=0)
+    rng = np.random.default_rng(43 + M + O)
+    L, x, _ = make_layer(rng, M, K, N, bits, O, heavy_cols=min(O, 4))
     dev = m.QuikLinear(to_layer(L))
     y = dev(torch.from_numpy(x).cuda(), out_dtype=torch.float32).cpu().numpy()
-    toks = np.sort(rng.choice(M, 6, replace=False))
-    rows = np.sort(rng.choice(N, 300, replace=False))
-    rb = row_bytes(K, 4)
+    toks = np.unique(np.concatenate([rng.choice(M, 6, replace=False), [0, M - 1]]))
+    rows = np.unique(np.concatenate([rng.choice(N, 300, replace=False), [0, N - 1]]))
+    rb = row_bytes(K - O, bits)
     sub = dict(L)
     sub["out_features"] = rows.size
     sub["base"] = np.asarray(L["base"]).reshape(N, rb)[rows].reshape(-1)
     sub["scales"] = L["scales"][rows]
     sub["wreduced"] = L["wreduced"][rows]
-    sub["outlier_weights"] = np.zeros((rows.size, 0), np.float32)
+    sub["outlier_weights"] = np.asarray(L["outlier_weights"]).reshape(N, O)[rows]
     sub["bias"] = L["bias"][rows]
     st, want = o.quik_matmul(sub, x[toks], 2)
-    np.testing.assert_array_equal(y[np.ix_(toks, rows)].view(np.uint32), want.view(np.uint32))
+    assert st == 0
+    got = y[np.ix_(toks, rows)]
+    if O == 0:
+        np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+    else:
+        assert rel_frob(want, got) < 1e-5
 
 
 def test_non_finite_input_flags_numerical_error():
@@ -405,6 +413,12 @@ def test_every_tile_config_exact(tile, cg, bn):
         wv = rng.integers(-lim - 1, lim + 1, size=(n, k))
         got = m.int_matmul(m.pack_values(xv, t, k, bits), m.pack_values(wv, n, k, bits))
         np.testing.assert_array_equal(got, xv @ wv.T)
+    # many tiles per persistent CTA in every configuration (f64 BLAS is exact here)
+    t, k, n = 2048, 512, 3000
+    xv = rng.integers(-8, 8, size=(t, k))
+    wv = rng.integers(-8, 8, size=(n, k))
+    got = m.int_matmul(m.pack_values(xv, t, k, 4), m.pack_values(wv, n, k, 4))
+    np.testing.assert_array_equal(got, (xv.astype(np.float64) @ wv.T.astype(np.float64)).astype(np.int64))
     L, x, _ = make_layer(rng, 300, 700, 300, 4, 0, heavy_cols=2)
     st, want = o.quik_matmul(L, x, 2)
     got = m.quik_matmul(to_layer(L), x)
@@ -704,6 +718,25 @@ def test_sparse_every_tile_config_exact(tile, cg, bn):
             np.testing.assert_array_equal(outs[2].view(np.uint32), want.view(np.uint32))
         else:
             assert rel_frob(want, outs[2]) < 1e-5
+    # many tiles per persistent CTA: the oracle on a token / row subset (rows independent)
+    M, K, N = 2048, 1024, 3000
+    L, x = make_sparse_layer(rng, M, K, N, 4, 0)
+    dev = m.QuikLinear(to_sparse_layer(L))
+    assert dev.is_sparse
+    y = dev(torch.from_numpy(x).cuda(), out_dtype=torch.float32).cpu().numpy()
+    toks = np.unique(np.concatenate([rng.choice(M, 5, replace=False), [0, M - 1]]))
+    rows = np.unique(np.concatenate([rng.choice(N, 200, replace=False), [0, N - 1]]))
+    sub = dict(L)
+    sub["out_features"] = rows.size
+    sub["base"] = np.asarray(L["base"]).reshape(N, row_bytes(K, 4))[rows].reshape(-1)
+    for key in ("scales", "wreduced", "bias"):
+        sub[key] = np.asarray(L[key])[rows]
+    sub["outlier_weights"] = np.zeros((rows.size, 0), np.float32)
+    if "mask" in L:
+        sub["mask"] = np.asarray(L["mask"]).reshape(N, -1)[rows]
+    st, want = o.quik_matmul(sub, x[toks], 2)
+    assert st == 0
+    np.testing.assert_array_equal(y[np.ix_(toks, rows)].view(np.uint32), want.view(np.uint32))
 
 
 def test_sparse_not_compressible_stays_dense():
