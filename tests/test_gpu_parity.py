@@ -1227,6 +1227,16 @@ def test_decode_kernel_fuzz_bit_identical():
             u = torch.int16 if dt == torch.float16 else torch.int32
             assert torch.equal(got1.view(u), want.view(u)), (trial, M, K, N, O, bits)
             assert torch.equal(got2.view(u), want.view(u)), (trial, "repeat")
+        # more (weight block, K split) units than CTAs: several units per persistent CTA
+        for (M, K, N, O, bits) in [(1, 4096, 8192, 128, 4), (16, 4096, 8192, 256, 8), (32, 2048, 12288, 64, 4)]:
+            L, x, _ = make_layer(rng, M, K, N, bits, O, heavy_cols=2, with_bias=True)
+            dev = m.QuikLinear(to_layer(L))
+            xt = torch.from_numpy(x).cuda()
+            lib.quik_set_int4_decode(0)
+            want = dev(xt, out_dtype=torch.float32)
+            lib.quik_set_int4_decode(1)
+            got = dev(xt, out_dtype=torch.float32)
+            assert torch.equal(got.view(torch.int32), want.view(torch.int32)), (M, K, N, O, bits)
     finally:
         lib.quik_set_int4_decode(1)
 
@@ -1254,3 +1264,9 @@ def test_weight_only_fuzz():
         y2 = dev.weight_only(xt, out_dtype=torch.float32).cpu().numpy()
         assert rel_frobenius(weight_only_f64(L, x), y1) < 1e-6, (trial, M, K, N, O, bits)
         np.testing.assert_array_equal(y1.view(np.uint32), y2.view(np.uint32))
+    # more (weight block, K split) units than CTAs
+    for (M, K, N, O, bits) in [(1, 4096, 8192, 128, 4), (40, 2048, 12288, 32, 8)]:
+        L, x, _ = make_layer(rng, M, K, N, bits, O, heavy_cols=2, with_bias=True, fp16_inputs=False)
+        dev = m.QuikLinear(to_layer(L))
+        y = dev.weight_only(torch.from_numpy(x).cuda(), out_dtype=torch.float32).cpu().numpy()
+        assert rel_frobenius(weight_only_f64(L, x), y) < 1e-6, (M, K, N, O, bits)
