@@ -437,7 +437,8 @@ __global__ void __launch_bounds__(512) quantize_rows_kernel(const QuantArgs a) {
 // instruction stream (the one-CTA-per-row kernel issues ~27 instructions per
 // element and is issue-bound at ~2 TB/s):
 //   * persistent CTAs walk rows blockIdx.x, +gridDim.x, ...; each row is fetched
-//     into a shared-memory ring by one TMA bulk copy issued `stages` rows ahead;
+//     into a shared-memory ring by one TMA bulk copy issued `stages` rows ahead
+//     (a slot is refilled at barrier A of its own row, once the row is in registers);
 //   * everything row-independent is hoisted out of the row loop: the per-vector
 //     outlier lane masks live in registers; the compaction descriptors are
 //     L1-resident per-layer tables;
