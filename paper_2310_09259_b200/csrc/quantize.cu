@@ -1024,6 +1024,20 @@ cudaError_t launch_quantize_hot(const QuantArgs& a, cudaStream_t stream) {
   // 12.1 -> 10.7 us and cfg3 28.8 -> 28.2 us; fewer threads per block barrier)
   int vpt = 1;
   while (vpt < 8 && (nvec + vpt - 1) / vpt > 128) vpt *= 2;
+  // an exact fit (FULL: no bounds checks, fewer registers) wins over the 4-warp target:
+  // the exact fit with the fewest threads >= 128, else the one with the most threads
+  int best = 0;
+  int64_t best_thr = 0;
+  for (int v = 1; v <= 8; v *= 2) {
+    const int64_t thr = nvec / v;
+    if (thr * v != nvec || thr % 32 || thr > (v >= 8 ? 512 : 256)) continue;
+    const bool wide = thr >= 128, best_wide = best_thr >= 128;
+    if (!best || (wide && (!best_wide || thr < best_thr)) || (!wide && !best_wide && thr > best_thr)) {
+      best = v;
+      best_thr = thr;
+    }
+  }
+  if (best) vpt = best;
   static const int vpt_env = [] {  // tuning knob: QUIK_K1_VPT forces 16-byte vectors per thread
     const char* e = getenv("QUIK_K1_VPT");
     return e ? atoi(e) : 0;

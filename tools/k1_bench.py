@@ -21,6 +21,7 @@ SHAPES = [  # name, M, K, O, bits
     ("cfg2 7B qkvo", 2048, 4096, 256, 4),
     ("cfg2 7B down W8A8", 2048, 11008, 688, 8),
     ("cfg1", 16, 4096, 128, 4),
+    ("cfg5 13B up", 2048, 5120, 256, 4),
 ]
 
 
