@@ -80,7 +80,7 @@ def prune_24(W, base_cols):
     t[:, cols] = wb
     return W
 
-CPU_SAMPLE_TOKENS = 64  # bounded sample of the workload for the CPU reference
+CPU_SAMPLE_TOKENS = 256  # bounded sample of the workload for the CPU reference (~1 s per call at cfg3)
 
 
 def peaks():
@@ -127,34 +127,53 @@ def synth_host(w, seed, tokens):
 def run_reference(args, w):
     """The reference's own CPU implementation (oracle/_ref = proj/src compiled unchanged,
     OpenMP on all host threads), each step one quik_matmul V3 call on a bounded token
-    sample of the workload."""
+    sample of the workload. With --layer-npz (bench.py's own cpu_baseline leg) the layer
+    and the sampled tokens come from the GPU arm's run and the output is saved to
+    --ref-out as the parity checker."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     cores = os.cpu_count() or 1
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
-    M_s = args.cpu_tokens
-    r, L, x = synth_host(w, args.seed, M_s)
+    if args.layer_npz:
+        sys.path.insert(0, str(ROOT / "tests"))
+        from oracle_lib import ref  # the reference's compiled sources (the cpu_baseline leg)
+
+        r = ref()
+        z = np.load(args.layer_npz)
+        x = z["x"]
+        L = dict(in_features=int(z["in_features"]), out_features=int(z["out_features"]), bits=int(z["bits"]),
+                 act_bits=int(z["bits"]), base=z["base"], scales=z["scales"], wreduced=z["wreduced"],
+                 outlier_weights=z["outlier_weights"], idx=z["idx"], bias=z["bias"] if "bias" in z else None)
+        n_out = L["out_features"]
+    else:
+        r, L, x = synth_host(w, args.seed, args.cpu_tokens)
+        n_out = w["N"]
+    M_s = x.shape[0]
     h, keep = r.layer_create(L)
     times = np.zeros(6)
     for _ in range(args.warmup):
-        st, _ = r.layer_forward(h, x, w["N"], 2)
+        st, _ = r.layer_forward(h, x, n_out, 2)
         assert st == 0, st
     per = []
     stage = np.zeros(6)
+    y = None
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        st, _ = r.layer_forward(h, x, w["N"], 2, times)
+        st, y = r.layer_forward(h, x, n_out, 2, times)
         per.append(time.perf_counter() - t0)
+        assert st == 0, st
         stage += times
     r.layer_destroy(h)
-    total = sum(per)
-    ops = 2.0 * M_s * w["N"] * w["K"]
-    value = ops * args.steps / total / 1e12
-    sample = (f"{M_s} of {w['M']} tokens of {args.workload} ({w['desc']}); quik_matmul V3 per step, "
-              f"OpenMP threads={os.environ.get('OMP_NUM_THREADS')}")
+    if args.ref_out:
+        np.save(args.ref_out, y)
+    med = statistics.median(per)
+    ops = 2.0 * M_s * n_out * w["K"]
+    value = ops / med / 1e12
+    sample = (f"{M_s} of {w['M']} tokens of {args.workload} ({w['desc']}); quik_matmul V3 per step (median of "
+              f"{args.steps}), OpenMP threads={os.environ.get('OMP_NUM_THREADS')}")
     out = dict(metric=METRIC, value=value, unit="TOPS", n_gpus=args.gpus, steps=args.steps, warmup=args.warmup,
-               ms_per_step=1e3 * total / args.steps, higher_is_better=True, scaling="strong", vs_baseline=None,
+               ms_per_step=1e3 * med, higher_is_better=True, scaling="strong", vs_baseline=None,
                dtype="int8", data="synthetic", impl="reference",
                config=dict(workload=args.workload, M=w["M"], K=w["K"], N=w["N"], outliers=w["O"], bits=w["bits"],
                            sample_tokens=M_s),
@@ -218,6 +237,90 @@ class ClockSampler:
                     power_w_max=max(r["power"] for r in rows))
 
 
+L2_BYTES = 126 * 1024 * 1024  # B200 L2
+
+
+def cublaslt_int8_peak(dev):
+    """Live dense INT8 tensor-core throughput of this GPU: cuBLASLt (torch._int_mm)
+    int8 x int8 -> int32 at 8192^3, best of 5 (tools/int8_peak.py is the standalone
+    version whose output is committed under profiles/)."""
+    import torch
+
+    n = 8192
+    a = torch.randint(-128, 127, (n, n), dtype=torch.int8, device=dev)
+    b = torch.randint(-128, 127, (n, n), dtype=torch.int8, device=dev).t()
+    for _ in range(2):
+        torch._int_mm(a, b)
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(5):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        torch._int_mm(a, b)
+        e.record()
+        torch.cuda.synchronize()
+        best = min(best, s.elapsed_time(e))
+    del a, b
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+
+
+def f16_output_bound(want, xs_o, ow, bias):
+    """Per-element bound on |y_f16 - reference| (the same formula as
+    tests/oracle_lib.f16_output_bound): 2^-11|r| + 2^-25 + (1 + 2^-11)(1.125 O + 3) 2^-24 T,
+    T = |r| + 2|bias| + 2 sum|x_o w_o|."""
+    O = xs_o.shape[1]
+    r = np.abs(want.astype(np.float64))
+    T = r.copy()
+    if O:
+        T += 2.0 * (np.abs(xs_o.astype(np.float64)) @ np.abs(ow.astype(np.float64)).T)
+    if bias is not None:
+        T += 2.0 * np.abs(bias.astype(np.float64))[None, :]
+    return 2.0 ** -11 * r + 2.0 ** -25 + (1.0 + 2.0 ** -11) * (1.125 * O + 3.0) * 2.0 ** -24 * T
+
+
+def cpu_leg(args, w, host, xs16, y_sample):
+    """cpu_baseline + parity: the reference's own quik_matmul (oracle/_ref, the unmodified
+    sources, OpenMP on every host core; a subprocess so OMP_NUM_THREADS applies) on the
+    SAME layer and the sampled tokens of this run's input. Returns (cpu_baseline, parity):
+    the reference's output on those tokens is the checker for this run's y."""
+    tmp = tempfile.mkdtemp(prefix="quik_bench_")
+    lp, op = os.path.join(tmp, "layer.npz"), os.path.join(tmp, "ref_out.npy")
+    xs = xs16.astype(np.float32)
+    np.savez(lp, x=xs, **host)
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--workload", args.workload,
+           "--steps", "3", "--warmup", "1", "--layer-npz", lp, "--ref-out", op]
+    env = dict(os.environ)
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE"):
+        env.pop(k, None)
+    env["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+        line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
+        cpu = json.loads(line)["cpu_baseline"]
+        want = np.load(op)
+    except Exception as exc:  # reported, never silently replaced
+        return (dict(value=None, unit="TOPS", cores=os.cpu_count(), kind="reference",
+                     sample=f"failed: {type(exc).__name__}: {exc}"[:300]),
+                dict(status="not run", reason=f"reference leg failed: {type(exc).__name__}"))
+    finally:
+        for f in (lp, op):
+            if os.path.exists(f):
+                os.unlink(f)
+        os.rmdir(tmp)
+    idx = host["idx"]
+    bound = f16_output_bound(want, xs[:, idx], host["outlier_weights"], host.get("bias"))
+    err = np.abs(y_sample.astype(np.float64) - want)
+    ratio = float((err / bound).max())
+    rel = float(np.linalg.norm(y_sample.astype(np.float64) - want) / max(np.linalg.norm(want), 1e-300))
+    ok = ratio <= 1.0 and rel <= 5e-4 and bool(np.all(np.isfinite(y_sample)))
+    parity = dict(status="ok" if ok else "fail", tokens=int(xs.shape[0]), rows=int(want.shape[1]),
+                  max_err_over_bound=ratio, rel_frobenius=rel,
+                  checker="reference quik_matmul V3 (oracle/_ref: proj/src compiled unchanged) on the same layer and "
+                          "the sampled tokens of this run's x; f16 y vs the f32 reference within the derived per-element "
+                          "bound (DESIGN.md §4) and rel_frobenius <= 5e-4")
+    return cpu, parity
+
+
 def run_ours(args, w):
     import torch
     import torch.distributed as dist
@@ -231,6 +334,8 @@ def run_ours(args, w):
     # N > 1 code path on a one-GPU box (ranks share the device); never a bench number
     backend = os.environ.get("QUIK_BENCH_DIST_BACKEND", "nccl")
     ndev = torch.cuda.device_count()
+    if backend == "nccl" and world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
     if backend != "nccl" and ndev < world:
         local = local % ndev
     torch.cuda.set_device(local)
@@ -244,7 +349,7 @@ def run_ours(args, w):
     if N % world:
         raise SystemExit(f"out_features {N} not divisible by {world} GPUs")
     ns = N // world
-    rb, re_ = rank * ns, (rank + 1) * ns
+    kb = K - O
 
     # ---- synthetic layer, generated on the device (same seed on every rank)
     g = torch.Generator(device=dev)
@@ -262,14 +367,29 @@ def run_ours(args, w):
                      dtype=torch.float32)
     sparse = bool(w.get("sparse"))
     if sparse:
-        prune_24(Wt, torch.as_tensor(outliers.permutation[: K - O], device=dev))
+        prune_24(Wt, torch.as_tensor(outliers.permutation[:kb], device=dev))
     base, sc, wr, ow = q.rtn_quantize_weights_device(Wt, outliers, bits)
     del Wt
     layer = q.QuikLinear.from_device(outliers, base, sc, wr, ow, bits, sparse=sparse)
     if sparse and not layer.is_sparse:
         raise SystemExit("2:4 workload: layer did not compress")
+    check_cpu = rank == 0 and world == 1 and not args.no_cpu
+    host = None
+    if check_cpu:  # reference-format copy of the layer for the CPU reference leg (cpu_baseline + parity)
+        host = dict(base=base.cpu().numpy(), scales=sc.cpu().numpy(), wreduced=wr.cpu().numpy(),
+                    outlier_weights=ow.half().float().cpu().numpy().reshape(ns, O), idx=outliers.indices,
+                    in_features=np.int64(K), out_features=np.int64(ns), bits=np.int64(bits))
     del base, ow
     torch.cuda.synchronize()
+
+    # inputs rotated over enough copies of x that the set exceeds L2 (x is only read by
+    # K1; the weights and y are each larger than L2 at the headline shape)
+    nbuf = max(1, -(-3 * L2_BYTES // 2 // (M * K * 2)))
+    nbuf = min(nbuf, 8)
+    xs_dev = [x16] + [x16.clone() for _ in range(nbuf - 1)]
+    footprint = nbuf * M * K * 2 + ns * ((kb + 127) // 128 * 128) + M * ns * 2
+    flush = footprint < 2 * L2_BYTES
+    flush_buf = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev) if flush else None
 
     def all_gather(out, inp):
         if backend == "nccl":
@@ -284,52 +404,78 @@ def run_ours(args, w):
         gathered = torch.empty((world, M, ns), dtype=torch.float16, device=dev)
         y = torch.empty((M, N), dtype=torch.float16, device=dev)
 
-    steps, warm = args.steps, args.warmup
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
-
-    def step(i=None):
-        e = ev[i] if i is not None else None
-        if e:
-            e[0].record()
-        layer.forward(x16, out=y_local, mid_event=e[1] if e else None)
-        if e:
-            e[2].record()
+    def step(i, mid_event=None):
+        layer.forward(xs_dev[i % nbuf], out=y_local, mid_event=mid_event)
         if world > 1:
             all_gather(gathered, y_local)
             y.view(M, world, ns).copy_(gathered.permute(1, 0, 2))
 
-    for e3 in ev:  # materialise the raw cudaEvent handles
-        for e in e3:
-            e.record()
-    for _ in range(warm):
-        step()
+    steps, warm = args.steps, args.warmup
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    ev_step = [(ev(), ev()) for _ in range(steps)]
+    ev_mid = [(ev(), ev(), ev()) for _ in range(steps)]
+    for e in [e for t in ev_step + ev_mid for e in t]:  # materialise the raw cudaEvent handles
+        e.record()
+    for i in range(warm):
+        step(i)
     torch.cuda.synchronize()
 
-    # clocks are sampled from just before the timed region through a sustained
-    # continuation of the same workload right after it (the timed region of K
-    # steps is far shorter than nvidia-smi's sampling interval)
+    # ---- timed region: K steps, max over ranks. Large workloads: back to back with no
+    # event inside (the PDL chain K1 -> GEMM -> next K1 runs as in production);
+    # L2-resident workloads: each step bracketed by events with an L2 flush in between
     sampler = ClockSampler(local) if not args.no_clocks else None
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    start.record()
-    for i in range(steps):
-        step(i)
-    end.record()
-    torch.cuda.synchronize()
+    start, end = ev(), ev()
+    if not flush:
+        start.record()
+        for i in range(steps):
+            step(i)
+        end.record()
+        torch.cuda.synchronize()
+        total_ms = start.elapsed_time(end)
+    else:
+        for i in range(steps):
+            flush_buf.fill_(float(i))
+            ev_step[i][0].record()
+            step(i)
+            ev_step[i][1].record()
+        torch.cuda.synchronize()
+        total_ms = sum(a.elapsed_time(b) for a, b in ev_step)
     if world > 1:
         dist.barrier()
+
+    # ---- per-step and per-kernel passes (outside the headline region): the median step
+    # and the K1 / GEMM split (an event between the two kernels)
+    for i in range(steps):
+        if flush:
+            flush_buf.fill_(float(i))
+        ev_step[i][0].record()
+        step(i)
+        ev_step[i][1].record()
+    torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in ev_step]
+    for i in range(steps):
+        if flush:
+            flush_buf.fill_(float(i))
+        ev_mid[i][0].record()
+        layer.forward(xs_dev[i % nbuf], out=y_local, mid_event=ev_mid[i][1])
+        ev_mid[i][2].record()
+    torch.cuda.synchronize()
+    quant_ms = [a.elapsed_time(b) for a, b, _ in ev_mid]
+    gemm_ms = [b.elapsed_time(c) for _, b, c in ev_mid]
+
     sustained = None
     if args.soak_s > 0:
         # sustained continuation (power-cap steady state), reported next to the value
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0, s1 = ev(), ev()
         n_sus = 0
         t_end = time.perf_counter() + args.soak_s
         s0.record()
         while time.perf_counter() < t_end:
-            for _ in range(20):
-                step()
+            for j in range(20):
+                step(j)
             n_sus += 20
             torch.cuda.synchronize()
         s1.record()
@@ -342,51 +488,60 @@ def run_ours(args, w):
                          note="same step repeated back to back for --soak-s seconds after the timed region")
     clocks = sampler.stop() if sampler else None
 
-    total_ms = start.elapsed_time(end)
-    gemm_ms = [e[1].elapsed_time(e[2]) for e in ev]
-    quant_ms = [e[0].elapsed_time(e[1]) for e in ev]
-    stats = torch.tensor([total_ms, statistics.mean(gemm_ms), statistics.mean(quant_ms)], device=dev,
-                         dtype=torch.float64)
+    stats = torch.tensor([total_ms, statistics.median(step_ms), statistics.median(gemm_ms),
+                          statistics.median(quant_ms), statistics.mean(gemm_ms), statistics.mean(quant_ms)],
+                         device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(stats, op=dist.ReduceOp.MAX)
-    total_ms, gemm_avg, quant_avg = stats.tolist()
+    total_ms, step_med, gemm_med, quant_med, gemm_mean, quant_mean = stats.tolist()
     ms_per_step = total_ms / steps
     ops = 2.0 * M * N * K
     value = ops / (ms_per_step * 1e-3) / 1e12
 
     # ---- roofline of the dominant kernel (fused GEMM), per launch on this rank
     pk = peaks()
-    kb = K - O
     p_f16 = pk["bf16"]
-    p_i8 = 2.0 * p_f16  # B200 dense INT8 = 2x dense FP16/BF16 tensor rate
+    i8_live = cublaslt_int8_peak(dev) if not args.no_cublas else None
+    # INT8 peak: the larger of 2x the measured bf16 rate (B200 dense INT8 = 2x FP16) and
+    # the live cuBLASLt INT8 rate (conservative: the larger peak gives the lower frac)
+    p_i8 = max(2.0 * p_f16, i8_live or 0.0)
     if sparse:
         p_i8 *= 2.0  # 2:4 sparse INT8 (tcgen05.mma.sp) = 2x dense INT8
     ops_rank = 2.0 * M * ns * K
     t_ideal_s = 2.0 * M * ns * kb / (p_i8 * 1e12) + 2.0 * M * ns * O / (p_f16 * 1e12)
     mixed_peak = ops_rank / t_ideal_s / 1e12
-    achieved = ops_rank / (gemm_avg * 1e-3) / 1e12
+    achieved = ops_rank / (gemm_med * 1e-3) / 1e12
+    a_bytes = (lambda n: (n + 1) // 2) if bits == 4 else (lambda n: n)
+    w_bytes = ns * a_bytes(kb) if not sparse else ns * a_bytes(kb) // 2 + ns * kb // 8
+    gemm_bytes = M * a_bytes(kb) + w_bytes + ns * O * 2 + M * O * 2 + 12 * ns + 8 * M + M * ns * 2
     traffic = None
     tp = ROOT / "profiles" / "ncu_gemm_traffic.json"
     if tp.exists():
         try:
-            tj = json.loads(tp.read_text())
-            traffic = tj.get(args.workload)
+            traffic = json.loads(tp.read_text()).get(args.workload)
         except Exception:
             traffic = None
     roofline = dict(bound="tensor", achieved=achieved, peak=mixed_peak, unit="TFLOP/s", frac=achieved / mixed_peak,
-                    traffic=traffic,
+                    traffic=traffic, algorithmic_bytes=gemm_bytes,
+                    traffic_ratio=(traffic / gemm_bytes) if traffic else None,
                     kernel="quik_gemm_kernel (fused int8 GEMM%s + f16 outlier GEMM + dequant epilogue)"
                            % (" on 2:4-compressed weights, tcgen05.mma.sp" if sparse else ""),
-                    peak_basis=(f"{pk['source']} bf16 burst {p_f16:.1f} TF/s (MEASURED_PEAKS.json) for the "
-                                f"{O} f16 outlier columns; INT8 peak = {'4x (2:4 sparse)' if sparse else '2x'} that = "
-                                f"{p_i8:.1f} TOPS for the {kb} int columns (dense-equivalent ops); mixed peak = ops / "
-                                "(int_ops/P_i8 + f16_ops/P_f16)"),
-                    int8_only_frac=achieved / p_i8, kernel_ms=gemm_avg)
-    bytes_q = M * K * 2 + M * (kb + 127) // 128 * 128 + M * ((O + 63) // 64 * 64) * 2 + 8 * M
-    quant = dict(kernel="quantize_hot_kernel (K1, persistent TMA ring)", ms=quant_avg, algorithmic_bytes=bytes_q,
-                 achieved_gbs=bytes_q / (quant_avg * 1e-3) / 1e9 if quant_avg > 0 else None,
-                 peak_gbs=pk["hbm_gbs"],
-                 frac=(bytes_q / (quant_avg * 1e-3) / 1e9) / pk["hbm_gbs"] if quant_avg > 0 else None)
+                    kernel_ms_median=gemm_med, kernel_ms_mean=gemm_mean,
+                    peak_basis=(f"{pk['source']} bf16 burst {p_f16:.1f} TF/s (MEASURED_PEAKS.json) for the {O} f16 "
+                                f"outlier columns; INT8 peak = max(2 x bf16, live cuBLASLt int8 "
+                                f"{(i8_live or 0):.1f} TOPS) = {p_i8 / (2 if sparse else 1):.1f} TOPS"
+                                f"{' x2 for 2:4 sparse' if sparse else ''} for the {kb} int columns (dense-equivalent "
+                                "ops); mixed peak = ops / (int_ops/P_i8 + f16_ops/P_f16); achieved from the median "
+                                "GEMM launch (CUDA events on the launch stream)"),
+                    int8_peak_cublaslt_tops=i8_live, int8_only_frac=achieved / p_i8)
+    # K1 algorithmic bytes per SURVEY.md §8(d): x f16 in, the codes at the reference's
+    # width (INT4: ceil(K_b/2) per token), x_outlier f16, scale + zero
+    bytes_q = M * K * 2 + M * a_bytes(kb) + M * O * 2 + 8 * M
+    quant = dict(kernel="quantize_hot_kernel (K1, persistent TMA ring)", ms_median=quant_med, ms_mean=quant_mean,
+                 algorithmic_bytes=bytes_q, achieved_gbs=bytes_q / (quant_med * 1e-3) / 1e9,
+                 peak_gbs=pk["hbm_gbs"], frac=(bytes_q / (quant_med * 1e-3) / 1e9) / pk["hbm_gbs"],
+                 device_layout_bytes=M * K * 2 + M * ((kb + 127) // 128 * 128) + M * ((O + 63) // 64 * 64) * 2 + 8 * M,
+                 note="§8(d) bytes (codes at the INT%d width); the kernel writes int8 GEMM-layout codes" % bits)
 
     # ---- FP16 cuBLAS GEMM of the same (sharded) shape, same x
     fp16 = None
@@ -396,18 +551,22 @@ def run_ours(args, w):
         for _ in range(3):
             torch.matmul(x16, Wf.t(), out=out16)
         torch.cuda.synchronize()
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s0.record()
-        for _ in range(steps):
-            torch.matmul(x16, Wf.t(), out=out16)
-        s1.record()
+        t16s = []
+        for i in range(steps):
+            if flush:
+                flush_buf.fill_(float(i))
+            ev_step[i][0].record()
+            torch.matmul(xs_dev[i % nbuf], Wf.t(), out=out16)
+            ev_step[i][1].record()
         torch.cuda.synchronize()
-        t16 = torch.tensor([s0.elapsed_time(s1) / steps], device=dev, dtype=torch.float64)
+        t16s = [a.elapsed_time(b) for a, b in ev_step]
+        t16 = torch.tensor([statistics.median(t16s)], device=dev, dtype=torch.float64)
         if world > 1:
             dist.all_reduce(t16, op=dist.ReduceOp.MAX)
         t16 = float(t16.item())
-        fp16 = dict(ms=t16, tflops=2.0 * M * ns * K / (t16 * 1e-3) / 1e12, speedup_step=t16 / (ms_per_step),
-                    speedup_gemm=t16 / gemm_avg, note="torch.matmul f16 (cuBLAS) of the per-rank shape, same x")
+        fp16 = dict(ms_median=t16, tflops=2.0 * M * ns * K / (t16 * 1e-3) / 1e12, speedup_step=t16 / step_med,
+                    speedup_gemm=t16 / gemm_med,
+                    note="torch.matmul f16 (cuBLAS) of the per-rank shape, same x; medians of per-step events")
         del Wf, out16
 
     # ---- e2e: host (pinned) buffers through the public API, copies inside the timed region
@@ -425,19 +584,16 @@ def run_ours(args, w):
                 return
             xd.copy_(xh, non_blocking=True)
             layer.forward(xd, out=y_local)
-            if world > 1:
-                all_gather(gathered, y_local)
-                y.view(M, world, ns).copy_(gathered.permute(1, 0, 2))
-                if rank == 0:
-                    yh.copy_(y, non_blocking=True)
-            else:
-                yh.copy_(y_local, non_blocking=True)
+            all_gather(gathered, y_local)
+            y.view(M, world, ns).copy_(gathered.permute(1, 0, 2))
+            if rank == 0:
+                yh.copy_(y, non_blocking=True)
 
         e2e_step()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a, b = ev(), ev()
         a.record()
         for _ in range(e2e_steps):
             e2e_step()
@@ -453,32 +609,32 @@ def run_ours(args, w):
                          if world == 1 else "QuikLinear.forward (C ABI quik_linear_forward_ex) + NCCL all-gather")
                    + " with pinned host f16 x -> y")
 
-    # ---- CPU baseline: the reference's own code on this host, rank 0, N = 1 only
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cmd = [sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--workload", args.workload,
-               "--steps", "3", "--warmup", "1", "--cpu-tokens", str(args.cpu_tokens)]
-        env = dict(os.environ)
-        for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK"):
-            env.pop(k, None)
-        env["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
-        try:
-            r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
-            line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
-            cpu = json.loads(line)["cpu_baseline"]
-        except Exception as exc:  # reported, never silently replaced
-            cpu = dict(value=None, unit="TOPS", cores=os.cpu_count(), kind="reference",
-                       sample=f"failed: {type(exc).__name__}")
+    # ---- CPU reference leg (rank 0, N = 1): cpu_baseline timing and the parity check of
+    # this run's y, both from the reference's own code on the same layer and tokens
+    cpu, parity = None, dict(status="not run", reason="N > 1 or --no-cpu")
+    if check_cpu:
+        rs = np.random.default_rng(args.seed)
+        toks = np.sort(rs.choice(M, min(M, args.cpu_tokens), replace=False))
+        ti = torch.as_tensor(toks, device=dev)
+        layer.forward(xs_dev[0], out=y_local)  # y of the first input buffer
+        y_sample = y_local[ti].float().cpu().numpy()
+        xs16 = xs_dev[0][ti].cpu().numpy()
+        cpu, parity = cpu_leg(args, w, host, xs16, y_sample)
+        if cpu.get("sample"):
+            cpu["sample"] += f"; tokens = {toks.size} sampled rows of this run's x (the same layer)"
 
     if rank == 0:
         out = dict(metric=METRIC, value=value, unit="TOPS", n_gpus=world, steps=steps, warmup=warm,
-                   ms_per_step=ms_per_step, higher_is_better=True, scaling="strong", vs_baseline=None,
-                   dtype="int8", data="synthetic",
+                   ms_per_step=ms_per_step, ms_per_step_median=step_med, higher_is_better=True, scaling="strong",
+                   vs_baseline=None, dtype="int8", data="synthetic",
                    config=dict(workload=args.workload, desc=w["desc"], M=M, K=K, N=N, outliers=O, bits=bits,
                                parallelism=f"output-feature shards x{world}" + (" + NCCL all-gather" if world > 1 else ""),
-                               l2="inputs larger than L2 (int8 weights %.0f MB, x f16 %.0f MB); no flush" %
-                                  (N * ((kb + 127) // 128 * 128) / 1e6, M * K * 2 / 1e6)),
-                   roofline=roofline, cpu_baseline=cpu, e2e=e2e, fp16_cublas=fp16, quantizer=quant,
+                               l2=(f"L2 flushed between steps (workload {footprint / 1e6:.0f} MB < 2 x L2); value = "
+                                   "sum of per-step event times" if flush else
+                                   f"inputs larger than L2: x rotated over {nbuf} buffers ({nbuf * M * K * 2 / 1e6:.0f} "
+                                   f"MB), int8 weights {ns * ((kb + 127) // 128 * 128) / 1e6:.0f} MB, y "
+                                   f"{M * ns * 2 / 1e6:.0f} MB; no flush")),
+                   parity=parity, roofline=roofline, cpu_baseline=cpu, e2e=e2e, fp16_cublas=fp16, quantizer=quant,
                    sustained=sustained,
                    clocks=clocks, gpu_launches=steps * q.QuikLinear.launches(),
                    precision="W%dA%d integer codes on tcgen05 kind::i8 (s32 accumulate) + f16 outliers (f32 accumulate), f16 out"
@@ -486,6 +642,19 @@ def run_ours(args, w):
         emit(out)
     if world > 1:
         dist.destroy_process_group()
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N > 1 without a torchrun environment: launch N ranks of this script (one
+    process per GPU, rendezvous on 127.0.0.1) and return their exit status."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
 
 
 def main():
@@ -502,8 +671,12 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cublas", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--layer-npz", default="", help=argparse.SUPPRESS)  # internal: the cpu_baseline leg
+    ap.add_argument("--ref-out", default="", help=argparse.SUPPRESS)
     ap.add_argument("--tile", default="", help="force the GEMM tile 'cta_group,block_n' (tuning)")
     args = ap.parse_args()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     if args.tile and args.impl == "ours":
         import paper_2310_09259_b200 as q
 

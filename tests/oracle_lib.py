@@ -383,3 +383,31 @@ def weight_only_f64(L, x, checker=None):
 def rel_frobenius(ref_, out):
     ref_ = np.asarray(ref_, np.float64)
     return float(np.linalg.norm(np.asarray(out, np.float64) - ref_) / max(np.linalg.norm(ref_), 1e-300))
+
+
+def f16_output_bound(L, x, want, y_is_f16=True):
+    """Per-element bound on |y_device - want| for the Quik-mode forward.
+
+    want = the reference's f32 output on the same f16-representable x and outlier weights,
+    computed as r = fl(fl(bias + sum_seq x_o*w_o) + D) (runtime.cpp:96-113, :288-301);
+    the device computes v = TC-accumulate(fl(bias + D); x_o*w_o) in f32 and rounds it to
+    f16 (D, the dequant term, is bit-identical on both sides; every x_o*w_o product of
+    two f16 values is exact in f32). With u = 2^-24 and
+    T = |bias| + |D| + sum|x_o*w_o|  (<= |want| + 2|bias| + 2 sum|x_o*w_o|):
+      |r - exact| <= (O + 1) u T          sequential f32 sum of bias + O products, + D
+      |v - exact| <= (O/8 + 2) u T        init rounding + <= 2u of the running magnitude
+                                          per 16-deep tcgen05 kind::f16 MMA step
+      |f16(v) - v| <= 2^-11 |v| + 2^-25   round to nearest (normal / subnormal f16)
+    so |y - r| <= 2^-11 |r| + 2^-25 + (1 + 2^-11) (1.125 O + 3) u T."""
+    idx = np.asarray(L["idx"])
+    O = idx.size
+    xo = np.asarray(x, np.float64)[:, idx]
+    ow = np.asarray(L["outlier_weights"], np.float64).reshape(-1, O) if O else None
+    P = np.abs(xo) @ np.abs(ow).T if O else 0.0
+    B = np.abs(np.asarray(L["bias"], np.float64))[None, :] if L.get("bias") is not None else 0.0
+    r = np.abs(np.asarray(want, np.float64))
+    T = r + 2.0 * B + 2.0 * P
+    delta = (1.0 + 2.0 ** -11) * (1.125 * O + 3.0) * 2.0 ** -24 * T
+    if not y_is_f16:
+        return delta
+    return 2.0 ** -11 * r + 2.0 ** -25 + delta
