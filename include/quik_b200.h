@@ -17,7 +17,15 @@
  * Threading: a layer handle is immutable after creation; forwards on the same
  * layer may run concurrently from different contexts (SPEC.md "forward passes
  * are pure and may run concurrently"). A context owns scratch memory and must
- * not be used from two host threads at once.
+ * not be used from two host threads at once. Calls through one context on
+ * different streams are ordered: each call waits (cudaStreamWaitEvent) for the
+ * previous call's work when the stream changes, so they cannot race on the
+ * scratch; a CUDA graph captured through a context must be replayed on one stream.
+ *
+ * Numerical errors: a non-finite activation sets the context's device flag; the
+ * next quik_ctx_sync() reports QUIK_ERR_NUMERICAL and clears it. Asynchronous
+ * forwards do not check it themselves; quik_ctx_clear_error() resets it before a
+ * call whose errors should be reported on their own.
  */
 #ifndef QUIK_B200_H_
 #define QUIK_B200_H_
@@ -28,7 +36,7 @@
 extern "C" {
 #endif
 
-#define QUIK_B200_ABI_VERSION 2
+#define QUIK_B200_ABI_VERSION 3
 
 typedef enum quik_status {
   QUIK_OK = 0,
@@ -59,6 +67,13 @@ quik_status quik_ctx_create(int device, quik_ctx_t* out);
 quik_status quik_ctx_destroy(quik_ctx_t ctx);
 /* Synchronises `stream`, then reports (and clears) the non-finite-input flag. */
 quik_status quik_ctx_sync(quik_ctx_t ctx, void* stream);
+/* Clears the non-finite-input flag (asynchronously, on `stream`). */
+quik_status quik_ctx_clear_error(quik_ctx_t ctx, void* stream);
+/* Sizes the context's scratch for forwards of `layer` with up to M tokens (codes,
+ * scales, outlier operands, the decode workspace and the INT4 weight copy at M <= 32),
+ * so that later forwards can be captured into a CUDA graph: scratch cannot grow during
+ * capture (those calls return QUIK_ERR_INVALID_ARGUMENT). Synchronous. */
+quik_status quik_ctx_reserve(quik_ctx_t ctx, quik_layer_t layer, int64_t M);
 
 /*
  * Layer weights, HOST memory, in the reference's formats.
@@ -118,6 +133,9 @@ quik_status quik_layer_info(quik_layer_t layer, int64_t* in_features, int64_t* o
                             int64_t* n_outlier, int* bits);
 /* 1 if the layer runs the 2:4 sparse GEMM (sparsity requested and compressible). */
 int quik_layer_is_sparse(quik_layer_t layer);
+/* Device GEMM layout of the layer's activation operands (what quik_quantize_activations_gemm
+ * writes): codes int8 [M][kpad], x_outlier16 f16 [M][opad]. */
+quik_status quik_layer_layout(quik_layer_t layer, int64_t* kpad, int64_t* opad);
 
 /*
  * Layer bundles: the reference's on-disk layer format
@@ -247,14 +265,57 @@ quik_status quik_linear_forward_host(quik_ctx_t ctx, quik_layer_t layer, const v
                                      int64_t M, void* y_host, quik_dtype y_dtype, int64_t chunk_tokens, void* stream);
 
 /* Round-to-nearest weight quantization on the device.
- * reference: rtn_quantize_weights (quantizer.hpp:87-88, quantizer.cpp:339-371) with
- * use_clipping = false; bit-exact (FP64 scale, ties away from zero, wreduced in FP64).
+ * reference: rtn_quantize_weights (quantizer.hpp:89-90, quantizer.cpp:339-371); with
+ * use_clipping the per-row clip factor of clip_search (quantizer.cpp:266-290: 51
+ * factors 0.50..1.00, sequential FP64 error sums, ties to the larger factor); bit-exact
+ * (FP64 scale, ties away from zero, wreduced in FP64).
  * w: DEVICE f32 [N][K]. outlier_indices: HOST, sorted unique. Outputs (DEVICE):
  * base packed [N][row_bytes(K - n_outlier)] (i4p / i8), scales [N], wreduced [N],
  * outlier_weights [N][n_outlier] f32 (original values, permuted-tail order). */
 quik_status quik_rtn_quantize_weights(quik_ctx_t ctx, const float* w, int64_t N, int64_t K,
-                                      const int64_t* outlier_indices, int64_t n_outlier, int bits, uint8_t* base,
-                                      float* scales, float* wreduced, float* outlier_weights, void* stream);
+                                      const int64_t* outlier_indices, int64_t n_outlier, int bits, int use_clipping,
+                                      uint8_t* base, float* scales, float* wreduced, float* outlier_weights,
+                                      void* stream);
+
+/* quik_matmul with StageTimes (runtime.hpp:72-80, runtime.cpp:265-315): the forward of
+ * quik_linear_forward_strided timed with CUDA events at the kernel boundaries; waits for
+ * completion. stage_ms[6] = {split, quantize, int_matmul, fp_matmul, dequantize, add}
+ * (ms), fused_flags[2] = {quantize_fused, dequantize_fused}. A fused stage reports under
+ * the first field it covers, as in the reference: V3 -> quantize_ms (K1: split +
+ * quantize) and int_matmul_ms (the fused GEMM: int + outlier matmul + dequantize + add);
+ * V1 -> split_ms, quantize_ms, int_matmul_ms (int32 GEMM) and fp_matmul_ms (one kernel:
+ * outlier matmul + dequantize + add); V2 as V1 with split folded into quantize_ms. */
+quik_status quik_linear_forward_timed(quik_ctx_t ctx, quik_layer_t layer, const void* x, quik_dtype x_dtype,
+                                      int64_t M, void* y, quik_dtype y_dtype, int64_t ldy, quik_variant variant,
+                                      void* stream, double* stage_ms, int* fused_flags);
+
+/* split_activations (runtime.hpp:48, runtime.cpp:169-186): x [M][in_features] ->
+ * x_base f32 [M][K_b] (permuted base columns) and x_outlier f32 [M][n_outlier]. */
+quik_status quik_split_activations(quik_ctx_t ctx, quik_layer_t layer, const void* x, quik_dtype x_dtype, int64_t M,
+                                   float* x_base, float* x_outlier, void* stream);
+
+/* unpack_values / unpack_int4 (packed.hpp:48-51, packed.cpp:68-91): packed
+ * [rows][row_bytes] -> int8 [rows][cols]. */
+quik_status quik_unpack_values(quik_ctx_t ctx, const uint8_t* packed, int64_t rows, int64_t cols, int bits,
+                               int8_t* out, void* stream);
+
+/* compute_wreduced (quantizer.hpp:94, quantizer.cpp:373-382): wreduced[r] =
+ * float(double(scales[r]) * sum_j q[r][j]), bit-exact. base packed [rows][row_bytes(cols)]. */
+quik_status quik_compute_wreduced(quik_ctx_t ctx, const uint8_t* base, int64_t rows, int64_t cols, int bits,
+                                  const float* scales, float* wreduced, void* stream);
+
+/* dequantize_weights (quantizer.hpp:98, quantizer.cpp:384-403): the de-permuted f32
+ * reconstruction out [rows][in_features]: q * scale in the base columns, the outlier
+ * weights in theirs. base / scales / outlier_weights / out DEVICE; outlier_indices HOST
+ * (sorted, unique); rows <= 65535 per call. Synchronous. */
+quik_status quik_dequantize_weights(quik_ctx_t ctx, const uint8_t* base, int64_t rows, int64_t in_features, int bits,
+                                    const float* scales, const float* outlier_weights, const int64_t* outlier_indices,
+                                    int64_t n_outlier, float* out, void* stream);
+
+/* forward_model's elementwise block ops (runtime.cpp:339-360) on f32 device buffers:
+ * op 0 = Silu out = a / (1 + exp(-a)), 1 = Multiply out = a * b, 2 = Add out = a + b. */
+quik_status quik_elementwise(quik_ctx_t ctx, int op, const float* a, const float* b, float* out, int64_t n,
+                             void* stream);
 
 /* Tuning/debug knob (process-wide): force the GEMM tile, cta_group in {1, 2} and
  * token block_n in {32, 64, 128} (1-CTA) or {128, 192, 256} (CTA pair; 2:4 sparse

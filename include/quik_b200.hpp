@@ -154,11 +154,28 @@ inline PackedIntMatrix pack_values(std::span<const int8_t> v, int64_t rows, int6
 inline PackedIntMatrix pack_int4(std::span<const int8_t> v, int64_t r, int64_t c) { return pack_values(v, r, c, 4); }
 inline PackedIntMatrix pack_int8(std::span<const int8_t> v, int64_t r, int64_t c) { return pack_values(v, r, c, 8); }
 
+// packed.cpp:86-91 (unpack_values) / :68-84 (unpack_int4), on the device
 inline std::vector<int8_t> unpack_values(const PackedIntMatrix& m) {
   std::vector<int8_t> out(static_cast<size_t>(m.rows * m.cols));
-  for (int64_t r = 0; r < m.rows; ++r)
-    for (int64_t c = 0; c < m.cols; ++c) out[static_cast<size_t>(r * m.cols + c)] = static_cast<int8_t>(m.get(r, c));
+  if (out.empty()) return out;
+  detail::Buf dp(m.data.data(), m.data.size()), dout(out.size());
+  detail::check(quik_unpack_values(detail::ctx(), static_cast<const uint8_t*>(dp.p), m.rows, m.cols, m.bits,
+                                   static_cast<int8_t*>(dout.p), nullptr));
+  detail::check(quik_ctx_sync(detail::ctx(), nullptr));
+  dout.get(out.data(), out.size());
   return out;
+}
+inline std::vector<int8_t> unpack_int4(const PackedIntMatrix& m) {
+  if (m.bits != 4) throw std::invalid_argument("unpack_int4: matrix is not 4-bit");
+  return unpack_values(m);
+}
+
+// matrix.hpp:67-73
+inline void check_same_shape(const FpMatrix& a, const FpMatrix& b, const char* what) {
+  if (a.rows != b.rows || a.cols != b.cols)
+    throw std::invalid_argument(std::string(what) + ": shape mismatch (" + std::to_string(a.rows) + "x" +
+                                std::to_string(a.cols) + " vs " + std::to_string(b.rows) + "x" +
+                                std::to_string(b.cols) + ")");
 }
 
 // calibration.hpp:37-48; from_indices calibration.cpp:69-91
@@ -319,26 +336,33 @@ class DeviceLayer {
       return y;
     }
     detail::Buf dx(x.data.data(), x.data.size() * 4), dy(y.data.size() * 4);
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    cudaEventRecord(e0, nullptr);
-    const quik_status s = quik_linear_forward(detail::ctx(), h_, dx.p, QUIK_F32, x.rows, dy.p, QUIK_F32,
-                                              static_cast<quik_variant>(v), nullptr);
-    cudaEventRecord(e1, nullptr);
-    detail::check(s);
-    detail::check(quik_ctx_sync(detail::ctx(), nullptr));
     if (times) {
-      float ms = 0;
-      cudaEventElapsedTime(&ms, e0, e1);
-      times->quantize_fused = v != PipelineVariant::V1Unfused;
-      times->dequantize_fused = v == PipelineVariant::V3FusedEpilogue;
-      times->int_matmul_ms = ms;
+      // per-stage CUDA-event times (runtime.cpp:265-315 convention; see quik_linear_forward_timed)
+      double ms[6] = {0, 0, 0, 0, 0, 0};
+      int fused[2] = {0, 0};
+      detail::check(quik_linear_forward_timed(detail::ctx(), h_, dx.p, QUIK_F32, x.rows, dy.p, QUIK_F32, out_,
+                                              static_cast<quik_variant>(v), nullptr, ms, fused));
+      times->split_ms = ms[0];
+      times->quantize_ms = ms[1];
+      times->int_matmul_ms = ms[2];
+      times->fp_matmul_ms = ms[3];
+      times->dequantize_ms = ms[4];
+      times->add_ms = ms[5];
+      times->quantize_fused = fused[0] != 0;
+      times->dequantize_fused = fused[1] != 0;
+    } else {
+      detail::check(quik_linear_forward(detail::ctx(), h_, dx.p, QUIK_F32, x.rows, dy.p, QUIK_F32,
+                                        static_cast<quik_variant>(v), nullptr));
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    detail::check(quik_ctx_sync(detail::ctx(), nullptr));
     dy.get(y.data.data(), y.data.size() * 4);
     return y;
+  }
+
+  // Device-resident forward: x / y device pointers, asynchronous on `stream`.
+  void forward_device(const void* x, quik_dtype xdt, int64_t M, void* y, quik_dtype ydt, void* stream = nullptr,
+                      PipelineVariant v = PipelineVariant::V3FusedEpilogue) const {
+    detail::check(quik_linear_forward(detail::ctx(), h_, x, xdt, M, y, ydt, static_cast<quik_variant>(v), stream));
   }
 
  private:
@@ -492,8 +516,9 @@ inline FpMatrix dequantize_epilogue(const Int32Matrix& acc, const ActQuantResult
   return out;
 }
 
-// quantizer.hpp:87-88 (use_clipping = false), on the device, bit-exact
-inline QuantizedWeights rtn_quantize_weights(const FpMatrix& w, const OutlierSet& o, int bits) {
+// quantizer.hpp:89-90, on the device, bit-exact (incl. clip_search with use_clipping)
+inline QuantizedWeights rtn_quantize_weights(const FpMatrix& w, const OutlierSet& o, int bits,
+                                             bool use_clipping = false) {
   if (o.feature_count != w.cols)
     throw std::invalid_argument("outlier set covers " + std::to_string(o.feature_count) + " features, weights have " +
                                 std::to_string(w.cols));
@@ -509,7 +534,8 @@ inline QuantizedWeights rtn_quantize_weights(const FpMatrix& w, const OutlierSet
   detail::Buf dw(w.data.data(), w.data.size() * 4), db(q.base.data.size()), ds(w.rows * 4), dr(w.rows * 4),
       dow(q.outlier_weights.data.size() * 4);
   detail::check(quik_rtn_quantize_weights(detail::ctx(), static_cast<const float*>(dw.p), w.rows, w.cols,
-                                          o.indices.data(), o.outlier_count(), bits, static_cast<uint8_t*>(db.p),
+                                          o.indices.data(), o.outlier_count(), bits, use_clipping ? 1 : 0,
+                                          static_cast<uint8_t*>(db.p),
                                           static_cast<float*>(ds.p), static_cast<float*>(dr.p),
                                           static_cast<float*>(dow.p), nullptr));
   detail::check(quik_ctx_sync(detail::ctx(), nullptr));
@@ -545,6 +571,12 @@ struct Hessian {
     token_count += batch.rows;
   }
   double at(int64_t i, int64_t j) const { return sum[static_cast<size_t>(i * dim + j)]; }
+  // quantizer.cpp:225-229: damping_frac * mean diagonal (trace summed in index order)
+  double lambda() const {
+    double trace = 0.0;
+    for (int64_t i = 0; i < dim; ++i) trace += at(i, i);
+    return damping_frac * trace / static_cast<double>(dim);
+  }
   static Hessian identity(int64_t dim, double damping_frac = 0.01) {
     Hessian h;
     h.dim = dim;
@@ -557,7 +589,7 @@ struct Hessian {
 };
 
 // quantizer.cpp:225-240
-inline Hessian build_hessian(const std::vector<FpMatrix>& batches, double damping_frac = 0.01) {
+inline Hessian build_hessian(std::span<const FpMatrix> batches, double damping_frac = 0.01) {
   Hessian h;
   h.damping_frac = damping_frac;
   for (const FpMatrix& b : batches) h.accumulate(b);
@@ -604,6 +636,162 @@ inline QuantizedWeights gptq_quantize(const FpMatrix& w, const Hessian& h, const
 inline QuantizedWeights sparsegpt_joint(const FpMatrix& w, const Hessian& h, const OutlierSet& o, int bits,
                                         bool use_clipping = false) {
   return detail::gptq_device(w, h, o, bits, use_clipping, true);
+}
+
+// quantizer.hpp:94 / quantizer.cpp:373-382, on the device (bit-exact)
+inline std::vector<float> compute_wreduced(const QuantizedWeights& q) {
+  std::vector<float> out(static_cast<size_t>(q.base.rows));
+  if (out.empty()) return out;
+  detail::Buf db(q.base.data.data(), q.base.data.size()), ds(q.scales.data(), q.scales.size() * 4),
+      dout(out.size() * 4);
+  detail::check(quik_compute_wreduced(detail::ctx(), static_cast<const uint8_t*>(db.p), q.base.rows, q.base.cols,
+                                      q.base.bits, static_cast<const float*>(ds.p), static_cast<float*>(dout.p),
+                                      nullptr));
+  detail::check(quik_ctx_sync(detail::ctx(), nullptr));
+  dout.get(out.data(), out.size() * 4);
+  return out;
+}
+
+// quantizer.hpp:98 / quantizer.cpp:384-403, on the device
+inline FpMatrix dequantize_weights(const QuantizedWeights& q, const OutlierSet& o) {
+  if (o.base_count() != q.base_features() || o.outlier_count() != q.outlier_weights.cols)
+    throw std::invalid_argument("dequantize_weights: outlier set does not match weights");
+  FpMatrix out(q.out_features(), o.feature_count);
+  if (out.data.empty()) return out;
+  detail::Buf db(q.base.data.data(), q.base.data.size()), ds(q.scales.data(), q.scales.size() * 4),
+      dow(q.outlier_weights.data.data(), q.outlier_weights.data.size() * 4), dout(out.data.size() * 4);
+  for (int64_t r0 = 0; r0 < out.rows; r0 += 65535) {
+    const int64_t nr = std::min<int64_t>(65535, out.rows - r0);
+    detail::check(quik_dequantize_weights(
+        detail::ctx(), static_cast<const uint8_t*>(db.p) + r0 * q.base.row_bytes(), nr, o.feature_count, q.bits(),
+        static_cast<const float*>(ds.p) + r0, static_cast<const float*>(dow.p) + r0 * o.outlier_count(),
+        o.indices.data(), o.outlier_count(), static_cast<float*>(dout.p) + r0 * o.feature_count, nullptr));
+  }
+  detail::check(quik_ctx_sync(detail::ctx(), nullptr));
+  dout.get(out.data.data(), out.data.size() * 4);
+  return out;
+}
+
+// runtime.hpp:48 / runtime.cpp:169-186, on the device
+inline std::pair<FpMatrix, FpMatrix> split_activations(const FpMatrix& x, const OutlierSet& o) {
+  if (x.cols != o.feature_count)
+    throw std::invalid_argument("split_activations: input has " + std::to_string(x.cols) +
+                                " features, outlier set covers " + std::to_string(o.feature_count));
+  FpMatrix base(x.rows, o.base_count()), outl(x.rows, o.outlier_count());
+  if (x.rows == 0) return {std::move(base), std::move(outl)};
+  QuikLinearLayer carrier;  // permutation tables only (no weight rows)
+  carrier.outliers = o;
+  carrier.weights.base.cols = o.base_count();
+  carrier.weights.outlier_weights = FpMatrix(0, o.outlier_count());
+  DeviceLayer L(carrier);
+  detail::Buf dx(x.data.data(), x.data.size() * 4), db(base.data.size() * 4), dout(outl.data.size() * 4);
+  detail::check(quik_split_activations(detail::ctx(), L.handle(), dx.p, QUIK_F32, x.rows, static_cast<float*>(db.p),
+                                       static_cast<float*>(dout.p), nullptr));
+  detail::check(quik_ctx_sync(detail::ctx(), nullptr));
+  db.get(base.data.data(), base.data.size() * 4);
+  dout.get(outl.data.data(), outl.data.size() * 4);
+  return {std::move(base), std::move(outl)};
+}
+
+// ---------------------------------------------------------------- model graphs (runtime.hpp:91-111)
+struct BlockOp {
+  enum class Kind { Linear, Silu, Multiply, Add };
+  Kind kind = Kind::Linear;
+  int a = 0;
+  int b = -1;
+  int layer = -1;
+};
+
+// runtime.cpp:373-382: up/gate/SiLU/Hadamard/down over layers {0: up, 1: gate, 2: down}
+inline std::vector<BlockOp> gated_mlp_ops() {
+  using K = BlockOp::Kind;
+  return {
+      {K::Linear, 0, -1, 0},
+      {K::Linear, 0, -1, 1},
+      {K::Silu, 2, -1, -1},
+      {K::Multiply, 3, 1, -1},
+      {K::Linear, 4, -1, 2},
+  };
+}
+
+// runtime.cpp:325-371 on the device: every value stays in device memory (f32); Linear ops
+// run the QUIK forward of a DeviceLayer (uploaded once per call), Silu / Multiply / Add
+// run quik_elementwise. Same op semantics and errors as the reference.
+inline std::vector<FpMatrix> forward_model_trace(std::span<const QuikLinearLayer> layers,
+                                                 std::span<const BlockOp> ops, const FpMatrix& x) {
+  std::vector<std::unique_ptr<DeviceLayer>> dev(layers.size());
+  std::vector<FpMatrix> values;
+  std::vector<std::unique_ptr<detail::Buf>> dvals;
+  values.reserve(ops.size() + 1);
+  values.push_back(x);
+  dvals.push_back(std::make_unique<detail::Buf>(x.data.data(), x.data.size() * 4));
+  auto check_value = [&](int i) {
+    if (i < 0 || i >= static_cast<int>(values.size()))
+      throw std::invalid_argument("forward_model: op references undefined value " + std::to_string(i));
+  };
+  for (const BlockOp& op : ops) {
+    switch (op.kind) {
+      case BlockOp::Kind::Linear: {
+        if (op.layer < 0 || op.layer >= static_cast<int>(layers.size()))
+          throw std::invalid_argument("forward_model: op references undefined layer " + std::to_string(op.layer));
+        check_value(op.a);
+        const FpMatrix& in = values[static_cast<size_t>(op.a)];
+        const QuikLinearLayer& L = layers[static_cast<size_t>(op.layer)];
+        L.validate();
+        if (in.cols != L.in_features())
+          throw std::invalid_argument("quik_matmul: input has " + std::to_string(in.cols) +
+                                      " features, layer expects " + std::to_string(L.in_features()));
+        if (!dev[static_cast<size_t>(op.layer)]) dev[static_cast<size_t>(op.layer)] = std::make_unique<DeviceLayer>(L);
+        FpMatrix v(in.rows, L.out_features());
+        auto dv = std::make_unique<detail::Buf>(v.data.size() * 4);
+        if (in.rows && v.cols) {
+          const DeviceLayer& D = *dev[static_cast<size_t>(op.layer)];
+          if (L.mode == LayerMode::WeightOnly)
+            detail::check(quik_linear_forward_weight_only(detail::ctx(), D.handle(), dvals[op.a]->p, QUIK_F32, in.rows,
+                                                          dv->p, QUIK_F32, v.cols, nullptr));
+          else
+            D.forward_device(dvals[op.a]->p, QUIK_F32, in.rows, dv->p, QUIK_F32);
+        }
+        values.push_back(std::move(v));
+        dvals.push_back(std::move(dv));
+        break;
+      }
+      case BlockOp::Kind::Silu: {
+        check_value(op.a);
+        FpMatrix v(values[op.a].rows, values[op.a].cols);
+        auto dv = std::make_unique<detail::Buf>(v.data.size() * 4);
+        detail::check(quik_elementwise(detail::ctx(), 0, static_cast<const float*>(dvals[op.a]->p), nullptr,
+                                       static_cast<float*>(dv->p), v.size(), nullptr));
+        values.push_back(std::move(v));
+        dvals.push_back(std::move(dv));
+        break;
+      }
+      case BlockOp::Kind::Multiply:
+      case BlockOp::Kind::Add: {
+        check_value(op.a);
+        check_value(op.b);
+        check_same_shape(values[op.a], values[op.b], "forward_model elementwise op");
+        FpMatrix v(values[op.a].rows, values[op.a].cols);
+        auto dv = std::make_unique<detail::Buf>(v.data.size() * 4);
+        detail::check(quik_elementwise(detail::ctx(), op.kind == BlockOp::Kind::Multiply ? 1 : 2,
+                                       static_cast<const float*>(dvals[op.a]->p),
+                                       static_cast<const float*>(dvals[op.b]->p), static_cast<float*>(dv->p),
+                                       v.size(), nullptr));
+        values.push_back(std::move(v));
+        dvals.push_back(std::move(dv));
+        break;
+      }
+    }
+  }
+  if (values.size() == 1) throw std::invalid_argument("forward_model: empty op list");
+  detail::check(quik_ctx_sync(detail::ctx(), nullptr));
+  for (size_t i = 1; i < values.size(); ++i) dvals[i]->get(values[i].data.data(), values[i].data.size() * 4);
+  return values;
+}
+
+inline FpMatrix forward_model(std::span<const QuikLinearLayer> layers, std::span<const BlockOp> ops,
+                              const FpMatrix& x) {
+  return std::move(forward_model_trace(layers, ops, x).back());
 }
 
 }  // namespace quik::b200

@@ -321,8 +321,39 @@ static int8_t quantize_to_grid(double value, double inv_scale, int maxq) {
 }
 
 /* quantizer.cpp:339-371 with rtn_quantize_row (:251-264), clip factor 1. */
-int qo_rtn_quantize_weights(const float* w, int64_t N, int64_t K, const int64_t* idx, int64_t n_out, int bits,
-                            uint8_t* base, float* scales, float* wreduced, float* outlier_w) {
+/* clip_search (quantizer.cpp:266-290): c in {0.50, 0.51, ..., 1.00} minimising the
+ * sequential FP64 sum of squared round-trip errors; ties toward the larger c. */
+static float clip_search(const float* w, const int64_t* perm, int64_t kb, int bits) {
+  const int maxq = (1 << (bits - 1)) - 1;
+  double amax = 0.0;
+  for (int64_t j = 0; j < kb; ++j) {
+    const double a = (double)fabsf(w[perm[j]]);
+    if (a > amax) amax = a;
+  }
+  if (amax == 0.0) return 1.0f;
+  double best_err = INFINITY;
+  float best_c = 1.0f;
+  for (int step = 0; step <= 50; ++step) {
+    const float c = (float)(0.50 + 0.01 * step);
+    const double scale = (double)c * amax / maxq;
+    const double inv_scale = 1.0 / scale;
+    double err = 0.0;
+    for (int64_t j = 0; j < kb; ++j) {
+      const float v = w[perm[j]];
+      const double dq = (double)quantize_to_grid(v, inv_scale, maxq) * scale;
+      const double d = (double)v - dq;
+      err += d * d;
+    }
+    if (err <= best_err) {
+      best_err = err;
+      best_c = c;
+    }
+  }
+  return best_c;
+}
+
+int qo_rtn_quantize_weights_clip(const float* w, int64_t N, int64_t K, const int64_t* idx, int64_t n_out, int bits,
+                                 int use_clipping, uint8_t* base, float* scales, float* wreduced, float* outlier_w) {
   if (bits != 4 && bits != 8) return QO_INVALID_ARGUMENT;
   int64_t* perm = (int64_t*)malloc(sizeof(int64_t) * ((size_t)K + 1));
   if (qo_outlier_permutation(K, idx, n_out, perm)) {
@@ -338,13 +369,15 @@ int qo_rtn_quantize_weights(const float* w, int64_t N, int64_t K, const int64_t*
       const double a = (double)fabsf(w[r * K + perm[j]]);
       if (a > amax) amax = a;
     }
+    /* rtn_quantize_weights :355: clip = use_clipping && n_base > 0 ? clip_search : 1 */
+    const float clip = use_clipping && kb > 0 ? clip_search(w + r * K, perm, kb, bits) : 1.0f;
     float scale_f;
     int64_t qsum = 0;
     if (amax == 0.0) {
       for (int64_t j = 0; j < kb; ++j) q[r * kb + j] = 0;
       scale_f = 1.0f;
     } else {
-      const double scale = 1.0 * amax / maxq; /* (double)clip_factor(=1.0f) * amax / maxq */
+      const double scale = (double)clip * amax / maxq; /* rtn_quantize_row, quantizer.cpp:258 */
       const double inv_scale = 1.0 / scale;
       for (int64_t j = 0; j < kb; ++j) {
         q[r * kb + j] = quantize_to_grid(w[r * K + perm[j]], inv_scale, maxq);
@@ -360,6 +393,32 @@ int qo_rtn_quantize_weights(const float* w, int64_t N, int64_t K, const int64_t*
   free(q);
   free(perm);
   return st;
+}
+
+int qo_rtn_quantize_weights(const float* w, int64_t N, int64_t K, const int64_t* idx, int64_t n_out, int bits,
+                            uint8_t* base, float* scales, float* wreduced, float* outlier_w) {
+  return qo_rtn_quantize_weights_clip(w, N, K, idx, n_out, bits, 0, base, scales, wreduced, outlier_w);
+}
+
+/* dequantize_weights (quantizer.cpp:384-403): out[r][perm[j]] = (float)q * scale[r]
+ * for base columns, the outlier weights in theirs. */
+int qo_dequantize_weights(const uint8_t* base, int64_t N, int64_t K, const int64_t* idx, int64_t n_out, int bits,
+                          const float* scales, const float* outlier_w, float* out) {
+  int64_t* perm = (int64_t*)malloc(sizeof(int64_t) * ((size_t)K + 1));
+  if (qo_outlier_permutation(K, idx, n_out, perm)) {
+    free(perm);
+    return QO_INVALID_ARGUMENT;
+  }
+  const int64_t kb = K - n_out;
+  int8_t* q = (int8_t*)malloc((size_t)(N * kb) + 1);
+  qo_unpack(base, N, kb, bits, q);
+  for (int64_t r = 0; r < N; ++r) {
+    for (int64_t j = 0; j < kb; ++j) out[r * K + perm[j]] = (float)q[r * kb + j] * scales[r];
+    for (int64_t j = 0; j < n_out; ++j) out[r * K + perm[kb + j]] = outlier_w[r * n_out + j];
+  }
+  free(q);
+  free(perm);
+  return 0;
 }
 
 /* quantizer.cpp:373-382 */

@@ -84,6 +84,12 @@ int qo_weight_only_forward(const qo_layer* layer, const float* x, int64_t M, flo
 /* quantizer.cpp:339-371 (+ :251-264, :17-22): RTN symmetric per-row, FP64 internals. */
 int qo_rtn_quantize_weights(const float* w, int64_t N, int64_t K, const int64_t* idx, int64_t n_out, int bits,
                             uint8_t* base, float* scales, float* wreduced, float* outlier_w);
+/* the same with use_clipping (clip_search, quantizer.cpp:266-290, :355) */
+int qo_rtn_quantize_weights_clip(const float* w, int64_t N, int64_t K, const int64_t* idx, int64_t n_out, int bits,
+                                 int use_clipping, uint8_t* base, float* scales, float* wreduced, float* outlier_w);
+/* quantizer.cpp:384-403 */
+int qo_dequantize_weights(const uint8_t* base, int64_t N, int64_t K, const int64_t* idx, int64_t n_out, int bits,
+                          const float* scales, const float* outlier_w, float* out);
 /* quantizer.cpp:373-382 */
 void qo_compute_wreduced(const uint8_t* base, int64_t N, int64_t kb, int bits, const float* scales, float* out);
 

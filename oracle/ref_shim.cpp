@@ -275,6 +275,57 @@ int qr_rtn_quantize_weights(const float* w, int64_t N, int64_t K, const int64_t*
   }
 }
 
+int qr_rtn_quantize_weights_clip(const float* w, int64_t N, int64_t K, const int64_t* idx, int64_t n_out, int bits,
+                                 int use_clipping, uint8_t* base, float* scales, float* wreduced, float* outlier_w) {
+  try {
+    auto o = quik::OutlierSet::from_indices(K, std::vector<int64_t>(idx, idx + n_out));
+    auto q = quik::rtn_quantize_weights(to_fp(w, N, K), o, bits, use_clipping != 0);
+    std::memcpy(base, q.base.data.data(), q.base.data.size());
+    std::memcpy(scales, q.scales.data(), N * 4);
+    std::memcpy(wreduced, q.wreduced.data(), N * 4);
+    if (n_out) std::memcpy(outlier_w, q.outlier_weights.data.data(), N * n_out * 4);
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
+// compute_wreduced / dequantize_weights of a layer in the reference's formats
+int qr_compute_wreduced(const uint8_t* base, int64_t N, int64_t kb, int bits, const float* scales, float* out) {
+  try {
+    quik::QuantizedWeights q;
+    q.base.rows = N;
+    q.base.cols = kb;
+    q.base.bits = bits;
+    q.base.data.assign(base, base + N * q.base.row_bytes());
+    q.scales.assign(scales, scales + N);
+    const auto r = quik::compute_wreduced(q);
+    std::memcpy(out, r.data(), N * 4);
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
+int qr_dequantize_weights(const uint8_t* base, int64_t N, int64_t K, const int64_t* idx, int64_t n_out, int bits,
+                          const float* scales, const float* outlier_w, float* out) {
+  try {
+    auto o = quik::OutlierSet::from_indices(K, std::vector<int64_t>(idx, idx + n_out));
+    quik::QuantizedWeights q;
+    q.base.rows = N;
+    q.base.cols = K - n_out;
+    q.base.bits = bits;
+    q.base.data.assign(base, base + N * q.base.row_bytes());
+    q.scales.assign(scales, scales + N);
+    q.outlier_weights = to_fp(outlier_w, N, n_out);
+    const auto r = quik::dequantize_weights(q, o);
+    std::memcpy(out, r.data.data(), r.data.size() * 4);
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
 // The reference tests' layer fixture, exactly (tests/test_runtime.cpp:27-45
 // make_layer): W ~ N(0, .5), x ~ N(0, 1) from mt19937(seed), `heavy` random
 // columns x100, outliers = select_outliers(x), RTN weights, bias ~ N(0, .1).

@@ -6,6 +6,7 @@ kernels behind the C ABI in include/quik_b200.h.
 """
 from .quik import (  # noqa: F401
     ActQuantResult,
+    BlockOp,
     Context,
     FormatError,
     NumericalError,
@@ -18,7 +19,12 @@ from .quik import (  # noqa: F401
     QuikLinear,
     QuikLinearLayer,
     StageTimes,
+    compute_wreduced,
     dequantize_epilogue,
+    dequantize_weights,
+    forward_model,
+    forward_model_trace,
+    gated_mlp_ops,
     gptq_quantize_device,
     hessian_device,
     int_matmul,
@@ -29,6 +35,8 @@ from .quik import (  # noqa: F401
     row_bytes,
     rtn_quantize_weights,
     rtn_quantize_weights_device,
+    split_activations,
+    unpack_int4,
     unpack_values,
 )
 from ._lib import LIB_PATH, load as load_library  # noqa: F401

@@ -34,7 +34,9 @@ EXPORTED_SYMBOLS = (
     "quik_set_gemm_w4", "quik_set_stream_gemm", "quik_bundle_open", "quik_bundle_weights",
     "quik_bundle_tensor", "quik_bundle_close", "quik_layer_load_bundle", "quik_layer_create_gated",
     "quik_linear_forward_weight_only", "quik_linear_forward_sharded", "quik_set_int4_decode",
-    "quik_gptq_quantize", "quik_hessian_accumulate",
+    "quik_gptq_quantize", "quik_hessian_accumulate", "quik_ctx_clear_error", "quik_ctx_reserve", "quik_layer_layout",
+    "quik_linear_forward_timed", "quik_split_activations", "quik_unpack_values", "quik_compute_wreduced",
+    "quik_dequantize_weights", "quik_elementwise",
 )
 
 
@@ -102,7 +104,16 @@ def load() -> C.CDLL:
             "quik_linear_forward_strided": (i32, [vp, vp, vp, i32, i64, vp, i32, i64, i32, vp]),
             "quik_linear_forward_launches": (i32, [i32]),
             "quik_linear_forward_ex": (i32, [vp, vp, vp, i32, i64, vp, i32, i64, i32, vp, vp]),
-            "quik_rtn_quantize_weights": (i32, [vp, vp, i64, i64, vp, i64, i32, vp, vp, vp, vp, vp]),
+            "quik_rtn_quantize_weights": (i32, [vp, vp, i64, i64, vp, i64, i32, i32, vp, vp, vp, vp, vp]),
+            "quik_ctx_clear_error": (i32, [vp, vp]),
+            "quik_ctx_reserve": (i32, [vp, vp, i64]),
+            "quik_layer_layout": (i32, [vp, C.POINTER(i64), C.POINTER(i64)]),
+            "quik_linear_forward_timed": (i32, [vp, vp, vp, i32, i64, vp, i32, i64, i32, vp, vp, vp]),
+            "quik_split_activations": (i32, [vp, vp, vp, i32, i64, vp, vp, vp]),
+            "quik_unpack_values": (i32, [vp, vp, i64, i64, i32, vp, vp]),
+            "quik_compute_wreduced": (i32, [vp, vp, i64, i64, i32, vp, vp, vp]),
+            "quik_dequantize_weights": (i32, [vp, vp, i64, i64, i32, vp, vp, vp, i64, vp, vp]),
+            "quik_elementwise": (i32, [vp, i32, vp, vp, vp, i64, vp]),
             "quik_set_gemm_tile": (i32, [i32, i32]),
             "quik_set_probe_mode": (i32, [i32]),
             "quik_linear_forward_host": (i32, [vp, vp, vp, i32, i64, vp, i32, i64, vp]),

@@ -79,11 +79,20 @@ struct CudaFail {
     if (_e != cudaSuccess) throw CudaFail{_e, #expr};               \
   } while (0)
 
+// The stream of the API call in progress on this thread: scratch growth (cudaFree /
+// cudaMalloc) is not allowed while it is being captured into a CUDA graph.
+thread_local cudaStream_t t_call_stream = nullptr;
+
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
   void* ensure(size_t bytes) {
     if (bytes <= cap) return p;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(t_call_stream, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+      throw std::invalid_argument(
+          "scratch memory would grow during CUDA graph capture: run one forward (or quik_ctx_reserve) at the "
+          "largest token count before capturing");
     if (p) { QK_CUDA(cudaDeviceSynchronize()); QK_CUDA(cudaFree(p)); p = nullptr; cap = 0; }
     const size_t want = std::max<size_t>(bytes, 1 << 16);
     QK_CUDA(cudaMalloc(&p, want));
@@ -120,7 +129,7 @@ struct quik_ctx_s {
   int device = 0;
   int num_sms = 148;
   int* d_err = nullptr;
-  DevBuf q8, scale, zero, xo16, acc, fp, xbase, xo32, wtmp, wo_ws, s4_out, s4_cnt;
+  DevBuf q8, scale, zero, xo16, acc, fp, xbase, xo32, wtmp, wo_ws, s4_out, s4_cnt, aux;
   // per-weight-block arrival counters of the INT4 decode kernel (zero between calls)
   int* ensure_s4_counters(size_t n, cudaStream_t st) {
     const size_t before = s4_cnt.cap;
@@ -142,6 +151,29 @@ struct quik_ctx_s {
     void* p = ws.ensure(bytes);
     if (ws.cap != before) QK_CUDA(cudaMemsetAsync(p, 0, ws.cap, st));
     return static_cast<int32_t*>(p);
+  }
+  // Scratch is shared by every call on this context: a call on a different stream than
+  // the previous one waits for the previous call's last kernel (event), so forwards
+  // issued on several streams through one context serialise instead of racing on the
+  // codes / scales / decode workspace. Skipped while the stream is being captured
+  // (a captured graph must be replayed on one stream per context).
+  cudaEvent_t ev_last = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool have_last = false;
+  bool begin_call(cudaStream_t st) {
+    t_call_stream = st;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    QK_CUDA(cudaStreamIsCapturing(st, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return false;
+    if (!ev_last) QK_CUDA(cudaEventCreateWithFlags(&ev_last, cudaEventDisableTiming));
+    if (have_last && last_stream != st) QK_CUDA(cudaStreamWaitEvent(st, ev_last, 0));
+    return true;
+  }
+  void end_call(cudaStream_t st, bool ordered) {
+    if (!ordered) return;
+    QK_CUDA(cudaEventRecord(ev_last, st));
+    last_stream = st;
+    have_last = true;
   }
   void ensure_pipeline() {
     if (s_in) return;
@@ -203,6 +235,16 @@ void check_launch(cudaError_t e, const char* what, const char* extra = nullptr) 
 }
 
 int64_t packed_row_bytes(int64_t cols, int bits) { return bits == 4 ? (cols + 1) / 2 : cols; }
+
+// Runs one API call's device work on `st` ordered after the context's previous call
+// (quik_ctx_s::begin_call / end_call).
+template <typename F>
+quik_status on_stream(quik_ctx_t ctx, cudaStream_t st, F&& f) {
+  const bool ordered = ctx->begin_call(st);
+  const quik_status r = f();
+  if (r == QUIK_OK) ctx->end_call(st, ordered);
+  return r;
+}
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
@@ -359,7 +401,7 @@ quik_status quik_ctx_destroy(quik_ctx_t ctx) {
   DeviceGuard g(ctx->device);
   cudaDeviceSynchronize();
   for (DevBuf* b : {&ctx->q8, &ctx->scale, &ctx->zero, &ctx->xo16, &ctx->acc, &ctx->fp, &ctx->xbase, &ctx->xo32,
-                    &ctx->wtmp, &ctx->xdev, &ctx->ydev, &ctx->ws, &ctx->wo_ws, &ctx->s4_out, &ctx->s4_cnt})
+                    &ctx->wtmp, &ctx->xdev, &ctx->ydev, &ctx->ws, &ctx->wo_ws, &ctx->s4_out, &ctx->s4_cnt, &ctx->aux})
     b->release();
   if (ctx->s_in) {
     cudaStreamDestroy(ctx->s_in);
@@ -371,6 +413,7 @@ quik_status quik_ctx_destroy(quik_ctx_t ctx) {
       cudaEventDestroy(ctx->ev_out[i]);
     }
   }
+  if (ctx->ev_last) cudaEventDestroy(ctx->ev_last);
   cudaFree(ctx->d_err);
   delete ctx;
   return QUIK_OK;
@@ -652,25 +695,27 @@ quik_status quik_quantize_activations_fused(quik_ctx_t ctx, quik_layer_t L, cons
     return fail(QUIK_ERR_UNSUPPORTED, "fused quantization: row wider than 128 KiB (register-resident quantizer limit)");
   return guarded([&] {
     DeviceGuard g(ctx->device);
-    QuantArgs q{};
-    q.x = x;
-    q.x_is_f32 = xdt == QUIK_F32;
-    q.M = M;
-    q.K = L->in_features;
-    q.ldx = L->in_features;
-    q.lane_mask = L->lane_mask;
-    q.gather = L->gather;
-    q.out_src = L->out_src;
-    q.kb = L->kb;
-    q.n_out = L->n_outlier;
-    q.bits = L->bits;
-    q.packed = packed;
-    q.scale = scale ? scale : static_cast<float*>(ctx->scale.ensure(M * 4));
-    q.zero = zero ? zero : static_cast<float*>(ctx->zero.ensure(M * 4));
-    q.xo32 = x_outlier;
-    q.err = ctx->d_err;
-    check_launch(launch_quantize(q, as_stream(stream)), "quantize kernel");
-    return QUIK_OK;
+    return on_stream(ctx, as_stream(stream), [&]() -> quik_status {
+      QuantArgs q{};
+      q.x = x;
+      q.x_is_f32 = xdt == QUIK_F32;
+      q.M = M;
+      q.K = L->in_features;
+      q.ldx = L->in_features;
+      q.lane_mask = L->lane_mask;
+      q.gather = L->gather;
+      q.out_src = L->out_src;
+      q.kb = L->kb;
+      q.n_out = L->n_outlier;
+      q.bits = L->bits;
+      q.packed = packed;
+      q.scale = scale ? scale : static_cast<float*>(ctx->scale.ensure(M * 4));
+      q.zero = zero ? zero : static_cast<float*>(ctx->zero.ensure(M * 4));
+      q.xo32 = x_outlier;
+      q.err = ctx->d_err;
+      check_launch(launch_quantize(q, as_stream(stream)), "quantize kernel");
+      return QUIK_OK;
+    });
   });
 }
 
@@ -683,30 +728,32 @@ quik_status quik_quantize_activations_gemm(quik_ctx_t ctx, quik_layer_t L, const
     return fail(QUIK_ERR_UNSUPPORTED, "quantize: row wider than 128 KiB (register-resident quantizer limit)");
   return guarded([&] {
     DeviceGuard g(ctx->device);
-    QuantArgs q{};
-    q.x = x;
-    q.x_is_f32 = xdt == QUIK_F32;
-    q.M = M;
-    q.K = L->in_features;
-    q.ldx = L->in_features;
-    q.lane_mask = L->lane_mask;
-    q.gather = L->gather;
-    q.chunk_desc = L->chunk_desc;
-    q.gen_chunk = L->gen_chunk;
-    q.n_gen = L->n_gen;
-    q.out_src = L->out_src;
-    q.kb = L->kb;
-    q.n_out = L->n_outlier;
-    q.bits = L->bits;
-    q.q8 = L->kpad ? codes : nullptr;
-    q.kpad = L->kpad;
-    q.scale = scale;
-    q.zero = zero;
-    q.xo16 = L->opad ? static_cast<__half*>(x_outlier16) : nullptr;
-    q.opad = L->opad;
-    q.err = ctx->d_err;
-    check_launch(launch_quantize(q, as_stream(stream)), "quantize kernel");
-    return QUIK_OK;
+    return on_stream(ctx, as_stream(stream), [&]() -> quik_status {
+      QuantArgs q{};
+      q.x = x;
+      q.x_is_f32 = xdt == QUIK_F32;
+      q.M = M;
+      q.K = L->in_features;
+      q.ldx = L->in_features;
+      q.lane_mask = L->lane_mask;
+      q.gather = L->gather;
+      q.chunk_desc = L->chunk_desc;
+      q.gen_chunk = L->gen_chunk;
+      q.n_gen = L->n_gen;
+      q.out_src = L->out_src;
+      q.kb = L->kb;
+      q.n_out = L->n_outlier;
+      q.bits = L->bits;
+      q.q8 = L->kpad ? codes : nullptr;
+      q.kpad = L->kpad;
+      q.scale = scale;
+      q.zero = zero;
+      q.xo16 = L->opad ? static_cast<__half*>(x_outlier16) : nullptr;
+      q.opad = L->opad;
+      q.err = ctx->d_err;
+      check_launch(launch_quantize(q, as_stream(stream)), "quantize kernel");
+      return QUIK_OK;
+    });
   });
 }
 
@@ -719,20 +766,22 @@ quik_status quik_quantize_activations(quik_ctx_t ctx, const void* x, quik_dtype 
     return fail(QUIK_ERR_UNSUPPORTED, "quantize: row wider than 128 KiB (register-resident quantizer limit)");
   return guarded([&] {
     DeviceGuard g(ctx->device);
-    QuantArgs q{};
-    q.x = x;
-    q.x_is_f32 = xdt == QUIK_F32;
-    q.M = M;
-    q.K = K;
-    q.ldx = K;
-    q.kb = K;
-    q.bits = bits;
-    q.packed = packed;
-    q.scale = scale ? scale : static_cast<float*>(ctx->scale.ensure(M * 4));
-    q.zero = zero ? zero : static_cast<float*>(ctx->zero.ensure(M * 4));
-    q.err = ctx->d_err;
-    check_launch(launch_quantize(q, as_stream(stream)), "quantize kernel");
-    return QUIK_OK;
+    return on_stream(ctx, as_stream(stream), [&]() -> quik_status {
+      QuantArgs q{};
+      q.x = x;
+      q.x_is_f32 = xdt == QUIK_F32;
+      q.M = M;
+      q.K = K;
+      q.ldx = K;
+      q.kb = K;
+      q.bits = bits;
+      q.packed = packed;
+      q.scale = scale ? scale : static_cast<float*>(ctx->scale.ensure(M * 4));
+      q.zero = zero ? zero : static_cast<float*>(ctx->zero.ensure(M * 4));
+      q.err = ctx->d_err;
+      check_launch(launch_quantize(q, as_stream(stream)), "quantize kernel");
+      return QUIK_OK;
+    });
   });
 }
 
@@ -753,28 +802,30 @@ quik_status quik_int_matmul(quik_ctx_t ctx, const uint8_t* xp, int64_t xr, int64
   if (xr > 0x7fffffffLL || wr > 0x7fffffffLL) return fail(QUIK_ERR_UNSUPPORTED, "int_matmul: dimension exceeds 2^31");
   return guarded([&] {
     DeviceGuard g(ctx->device);
-    cudaStream_t st = as_stream(stream);
-    if (xr == 0 || wr == 0) return QUIK_OK;
-    if (xc == 0) {
-      QK_CUDA(cudaMemsetAsync(out, 0, static_cast<size_t>(xr * wr * 4), st));
+    return on_stream(ctx, as_stream(stream), [&]() -> quik_status {
+      cudaStream_t st = as_stream(stream);
+      if (xr == 0 || wr == 0) return QUIK_OK;
+      if (xc == 0) {
+        QK_CUDA(cudaMemsetAsync(out, 0, static_cast<size_t>(xr * wr * 4), st));
+        return QUIK_OK;
+      }
+      const int64_t kpad = round_up(xc, kKBlockBytes);
+      int8_t* x8 = static_cast<int8_t*>(ctx->q8.ensure(static_cast<size_t>(xr * kpad)));
+      int8_t* w8 = static_cast<int8_t*>(ctx->wtmp.ensure(static_cast<size_t>(wr * kpad)));
+      check_launch(launch_unpack_to_gemm(xp, xr, xc, xb, x8, kpad, st), "unpack x");
+      check_launch(launch_unpack_to_gemm(wp, wr, wc, wb, w8, kpad, st), "unpack w");
+      GemmArgs gm{};
+      gm.w = w8;
+      gm.x = x8;
+      gm.kpad = kpad;
+      gm.M = xr;
+      gm.N = wr;
+      gm.out = out;
+      gm.ldo = wr;
+      gm.mode = kModeInt32;
+      run_gemm(ctx, gm, st);
       return QUIK_OK;
-    }
-    const int64_t kpad = round_up(xc, kKBlockBytes);
-    int8_t* x8 = static_cast<int8_t*>(ctx->q8.ensure(static_cast<size_t>(xr * kpad)));
-    int8_t* w8 = static_cast<int8_t*>(ctx->wtmp.ensure(static_cast<size_t>(wr * kpad)));
-    check_launch(launch_unpack_to_gemm(xp, xr, xc, xb, x8, kpad, st), "unpack x");
-    check_launch(launch_unpack_to_gemm(wp, wr, wc, wb, w8, kpad, st), "unpack w");
-    GemmArgs gm{};
-    gm.w = w8;
-    gm.x = x8;
-    gm.kpad = kpad;
-    gm.M = xr;
-    gm.N = wr;
-    gm.out = out;
-    gm.ldo = wr;
-    gm.mode = kModeInt32;
-    run_gemm(ctx, gm, st);
-    return QUIK_OK;
+    });
   });
 }
 
@@ -809,8 +860,17 @@ void ensure_w4(quik_layer_s* L, cudaStream_t st, bool needed = false) {
 }
 
 // The forward on device buffers (argument checks done by the caller).
+// Events recorded at the stage boundaries of one forward (StageTimes, runtime.hpp:72-80);
+// any may be null.
+struct StageMarks {
+  cudaEvent_t after_split = nullptr, after_quant = nullptr, after_int = nullptr;
+};
+void mark(cudaEvent_t e, cudaStream_t st) {
+  if (e) QK_CUDA(cudaEventRecord(e, st));
+}
+
 quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M, void* y,
-                         quik_dtype ydt, int64_t ldy, quik_variant variant, cudaStream_t st, void* mid_event,
+                         quik_dtype ydt, int64_t ldy, quik_variant variant, cudaStream_t st, const StageMarks& sm,
                          void* const* peers = nullptr, int n_peer = 0) {
   if (M == 0 || L->out_features == 0) return QUIK_OK;
   const int64_t N = L->out_features;
@@ -835,7 +895,7 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
     // decode regime: K1 -> one kernel for the INT4 split-K GEMM and the fused epilogue
     // (dequant + outlier MMAs, stream4.cu); workspace / counters stay zeroed between calls
     run_k1(ctx, L, x, xdt, M, st);
-    if (mid_event) QK_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(mid_event), st));
+    mark(sm.after_quant, st);
     Stream4Args a{};
     a.w4 = L->bits == 4 ? L->w4 : nullptr;
     a.w8 = L->w8;
@@ -869,7 +929,7 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
     // workspace -> the fused kernel's AccInit mode (dequant + outlier MMAs + store,
     // clears the workspace); same arithmetic as the fused V3 kernel
     run_k1(ctx, L, x, xdt, M, st);
-    if (mid_event) QK_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(mid_event), st));
+    mark(sm.after_quant, st);
     int32_t* ws = ctx->ensure_ws(static_cast<size_t>(M * N * 4), st);
     StreamArgs sa{};
     sa.w8 = L->w8;
@@ -895,7 +955,7 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
   }
   if (variant == QUIK_V3_FUSED_EPILOGUE) {
     run_k1(ctx, L, x, xdt, M, st);
-    if (mid_event) QK_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(mid_event), st));
+    mark(sm.after_quant, st);
     GemmArgs gm = gemm_args(ctx, L, M);
     gm.out = y;
     gm.ldo = ldy;
@@ -927,6 +987,7 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
     s.xo16 = L->opad ? static_cast<__half*>(ctx->xo16.ensure(static_cast<size_t>(M * L->opad * 2))) : nullptr;
     s.opad = L->opad;
     check_launch(launch_split(s, st), "split kernel");
+    mark(sm.after_split, st);
     QuantArgs q{};
     q.x = xb32;
     q.x_is_f32 = 1;
@@ -944,6 +1005,7 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
   } else {
     run_k1(ctx, L, x, xdt, M, st);
   }
+  mark(sm.after_quant, st);
   // V1/V2 tail: the int32 accumulator through global memory, then the same
   // epilogue + outlier MMAs as V3 reading it back (bit-identical to V3).
   int32_t* acc = static_cast<int32_t*>(ctx->acc.ensure(static_cast<size_t>(M * N * 4)));
@@ -953,6 +1015,7 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
   gi.mode = kModeInt32;
   if (L->kpad) run_gemm(ctx, gi, st);
   else QK_CUDA(cudaMemsetAsync(acc, 0, static_cast<size_t>(M * N * 4), st));
+  mark(sm.after_int, st);
   GemmArgs go = gemm_args(ctx, L, M);
   go.acc_in = acc;
   go.ld_acc = N;
@@ -980,7 +1043,10 @@ quik_status quik_linear_forward_ex(quik_ctx_t ctx, quik_layer_t L, const void* x
   if (ctx->device != L->device) return fail(QUIK_ERR_INVALID_ARGUMENT, "context and layer live on different devices");
   return guarded([&] {
     DeviceGuard g(ctx->device);
-    return forward_impl(ctx, L, x, xdt, M, y, ydt, ldy, variant, as_stream(stream), mid_event);
+    StageMarks sm;
+    sm.after_quant = reinterpret_cast<cudaEvent_t>(mid_event);
+    return on_stream(ctx, as_stream(stream),
+                     [&] { return forward_impl(ctx, L, x, xdt, M, y, ydt, ldy, variant, as_stream(stream), sm); });
   });
 }
 
@@ -1056,8 +1122,10 @@ quik_status quik_linear_forward_sharded(quik_ctx_t ctx, quik_layer_t L, const vo
     DeviceGuard g(ctx->device);
     void* peers[kMaxPeerOut] = {};
     for (int i = 1; i < n_dst; ++i) peers[i - 1] = static_cast<__half*>(y_dst[i]) + col_offset;
-    return forward_impl(ctx, L, x, xdt, M, static_cast<__half*>(y_dst[0]) + col_offset, QUIK_F16, ldy,
-                        QUIK_V3_FUSED_EPILOGUE, as_stream(stream), nullptr, peers, n_dst - 1);
+    return on_stream(ctx, as_stream(stream), [&] {
+      return forward_impl(ctx, L, x, xdt, M, static_cast<__half*>(y_dst[0]) + col_offset, QUIK_F16, ldy,
+                          QUIK_V3_FUSED_EPILOGUE, as_stream(stream), StageMarks{}, peers, n_dst - 1);
+    });
   });
 }
 
@@ -1073,38 +1141,40 @@ quik_status quik_linear_forward_weight_only(quik_ctx_t ctx, quik_layer_t L, cons
   if (ctx->device != L->device) return fail(QUIK_ERR_INVALID_ARGUMENT, "context and layer live on different devices");
   return guarded([&] {
     DeviceGuard g(ctx->device);
-    cudaStream_t st = as_stream(stream);
-    if (M == 0 || L->out_features == 0) return QUIK_OK;
-    ensure_w4(L, st, true);  // INT4 weights are what the decode regime streams
-    WoArgs a{};
-    a.x = x;
-    a.x_is_f32 = xdt == QUIK_F32;
-    a.M = M;
-    a.ldx = L->in_features;
-    a.base_src = L->base_src;
-    a.kb = L->kb;
-    a.kpad = L->kpad;
-    a.out_src = L->out_src;
-    a.n_out = L->n_outlier;
-    a.opad = L->opad;
-    a.w4 = L->bits == 4 ? L->w4 : nullptr;
-    a.w8 = L->w8;
-    a.wo = L->wo16;
-    a.wo_lo = L->wo16_lo;
-    a.scale = L->w_scale;
-    a.bias = L->bias;
-    a.N = L->out_features;
-    a.y = y;
-    a.y_is_f16 = ydt == QUIK_F16;
-    a.ldy = ldy;
-    size_t pb = 0, po = 0;
-    const size_t wsb = wo_workspace_bytes(a, ctx->num_sms, &pb, &po);
-    a.xb = static_cast<__half*>(ctx->xbase.ensure(std::max<size_t>(pb, 16)));
-    a.xo = static_cast<__half*>(ctx->xo16.ensure(std::max<size_t>(po, 16)));
-    a.ws = wsb ? static_cast<float*>(ctx->wo_ws.ensure(wsb)) : nullptr;
-    const char* msg = nullptr;
-    check_launch(launch_weight_only(a, ctx->num_sms, st, &msg), "weight-only kernel", msg);
-    return QUIK_OK;
+    return on_stream(ctx, as_stream(stream), [&]() -> quik_status {
+      cudaStream_t st = as_stream(stream);
+      if (M == 0 || L->out_features == 0) return QUIK_OK;
+      ensure_w4(L, st, true);  // INT4 weights are what the decode regime streams
+      WoArgs a{};
+      a.x = x;
+      a.x_is_f32 = xdt == QUIK_F32;
+      a.M = M;
+      a.ldx = L->in_features;
+      a.base_src = L->base_src;
+      a.kb = L->kb;
+      a.kpad = L->kpad;
+      a.out_src = L->out_src;
+      a.n_out = L->n_outlier;
+      a.opad = L->opad;
+      a.w4 = L->bits == 4 ? L->w4 : nullptr;
+      a.w8 = L->w8;
+      a.wo = L->wo16;
+      a.wo_lo = L->wo16_lo;
+      a.scale = L->w_scale;
+      a.bias = L->bias;
+      a.N = L->out_features;
+      a.y = y;
+      a.y_is_f16 = ydt == QUIK_F16;
+      a.ldy = ldy;
+      size_t pb = 0, po = 0;
+      const size_t wsb = wo_workspace_bytes(a, ctx->num_sms, &pb, &po);
+      a.xb = static_cast<__half*>(ctx->xbase.ensure(std::max<size_t>(pb, 16)));
+      a.xo = static_cast<__half*>(ctx->xo16.ensure(std::max<size_t>(po, 16)));
+      a.ws = wsb ? static_cast<float*>(ctx->wo_ws.ensure(wsb)) : nullptr;
+      const char* msg = nullptr;
+      check_launch(launch_weight_only(a, ctx->num_sms, st, &msg), "weight-only kernel", msg);
+      return QUIK_OK;
+    });
   });
 }
 
@@ -1120,50 +1190,54 @@ quik_status quik_linear_forward_host(quik_ctx_t ctx, quik_layer_t L, const void*
   if (ctx->device != L->device) return fail(QUIK_ERR_INVALID_ARGUMENT, "context and layer live on different devices");
   return guarded([&] {
     DeviceGuard g(ctx->device);
-    cudaStream_t st = as_stream(stream);
-    const int64_t K = L->in_features, N = L->gated ? L->out_features / 2 : L->out_features;  // output width
-    if (M == 0 || N == 0) return QUIK_OK;
-    ctx->ensure_pipeline();
-    const size_t xe = xdt == QUIK_F32 ? 4 : 2, ye = ydt == QUIK_F32 ? 4 : 2;
-    // Chunking: copy-in of chunk c+1, the two kernels of chunk c and copy-out of
-    // chunk c-1 run concurrently (PCIe is full duplex; the copies dominate). About
-    // 16 chunks (pipeline fill / drain ~1/16 of the copies), each a multiple of 256 tokens.
-    int64_t chunk = chunk_tokens;
-    if (chunk == 0) chunk = std::max<int64_t>(256, round_up((M + 15) / 16, 256));
-    if ((M + chunk - 1) / chunk > kMaxHostChunks) chunk = (M + kMaxHostChunks - 1) / kMaxHostChunks;
-    const int64_t nchunks = (M + chunk - 1) / chunk;
-    char* xd = static_cast<char*>(ctx->xdev.ensure(static_cast<size_t>(M * K) * xe));
-    char* yd = static_cast<char*>(ctx->ydev.ensure(static_cast<size_t>(M * N) * ye));
-    const char* xh = static_cast<const char*>(x_host);
-    char* yh = static_cast<char*>(y_host);
-    // everything already queued on `stream` (including an earlier call's use of the
-    // staging buffers) happens before this call's copies
-    QK_CUDA(cudaEventRecord(ctx->ev_start, st));
-    QK_CUDA(cudaStreamWaitEvent(ctx->s_in, ctx->ev_start, 0));
-    QK_CUDA(cudaStreamWaitEvent(ctx->s_out, ctx->ev_start, 0));
-    for (int64_t c = 0; c < nchunks; ++c) {
-      const int64_t m0 = c * chunk, mc = std::min(chunk, M - m0);
-      QK_CUDA(cudaMemcpyAsync(xd + m0 * K * xe, xh + m0 * K * xe, static_cast<size_t>(mc * K) * xe,
-                              cudaMemcpyHostToDevice, ctx->s_in));
-      QK_CUDA(cudaEventRecord(ctx->ev_in[c], ctx->s_in));
-      QK_CUDA(cudaStreamWaitEvent(st, ctx->ev_in[c], 0));
-      const quik_status s =
-          forward_impl(ctx, L, xd + m0 * K * xe, xdt, mc, yd + m0 * N * ye, ydt, N, QUIK_V3_FUSED_EPILOGUE, st, nullptr);
-      if (s != QUIK_OK) return s;
-      QK_CUDA(cudaEventRecord(ctx->ev_out[c], st));
-      QK_CUDA(cudaStreamWaitEvent(ctx->s_out, ctx->ev_out[c], 0));
-      QK_CUDA(cudaMemcpyAsync(yh + m0 * N * ye, yd + m0 * N * ye, static_cast<size_t>(mc * N) * ye,
-                              cudaMemcpyDeviceToHost, ctx->s_out));
-    }
-    QK_CUDA(cudaEventRecord(ctx->ev_done, ctx->s_out));
-    QK_CUDA(cudaStreamWaitEvent(st, ctx->ev_done, 0));
-    return QUIK_OK;
+    return on_stream(ctx, as_stream(stream), [&]() -> quik_status {
+      cudaStream_t st = as_stream(stream);
+      const int64_t K = L->in_features, N = L->gated ? L->out_features / 2 : L->out_features;  // output width
+      if (M == 0 || N == 0) return QUIK_OK;
+      ctx->ensure_pipeline();
+      const size_t xe = xdt == QUIK_F32 ? 4 : 2, ye = ydt == QUIK_F32 ? 4 : 2;
+      // Chunking: copy-in of chunk c+1, the two kernels of chunk c and copy-out of
+      // chunk c-1 run concurrently (PCIe is full duplex; the copies dominate). About
+      // 16 chunks (pipeline fill / drain ~1/16 of the copies), each a multiple of 256 tokens.
+      int64_t chunk = chunk_tokens;
+      if (chunk == 0) chunk = std::max<int64_t>(256, round_up((M + 15) / 16, 256));
+      if ((M + chunk - 1) / chunk > kMaxHostChunks) chunk = (M + kMaxHostChunks - 1) / kMaxHostChunks;
+      const int64_t nchunks = (M + chunk - 1) / chunk;
+      char* xd = static_cast<char*>(ctx->xdev.ensure(static_cast<size_t>(M * K) * xe));
+      char* yd = static_cast<char*>(ctx->ydev.ensure(static_cast<size_t>(M * N) * ye));
+      const char* xh = static_cast<const char*>(x_host);
+      char* yh = static_cast<char*>(y_host);
+      // everything already queued on `stream` (including an earlier call's use of the
+      // staging buffers) happens before this call's copies
+      QK_CUDA(cudaEventRecord(ctx->ev_start, st));
+      QK_CUDA(cudaStreamWaitEvent(ctx->s_in, ctx->ev_start, 0));
+      QK_CUDA(cudaStreamWaitEvent(ctx->s_out, ctx->ev_start, 0));
+      for (int64_t c = 0; c < nchunks; ++c) {
+        const int64_t m0 = c * chunk, mc = std::min(chunk, M - m0);
+        QK_CUDA(cudaMemcpyAsync(xd + m0 * K * xe, xh + m0 * K * xe, static_cast<size_t>(mc * K) * xe,
+                                cudaMemcpyHostToDevice, ctx->s_in));
+        QK_CUDA(cudaEventRecord(ctx->ev_in[c], ctx->s_in));
+        QK_CUDA(cudaStreamWaitEvent(st, ctx->ev_in[c], 0));
+        const quik_status s =
+            forward_impl(ctx, L, xd + m0 * K * xe, xdt, mc, yd + m0 * N * ye, ydt, N, QUIK_V3_FUSED_EPILOGUE, st,
+                         StageMarks{});
+        if (s != QUIK_OK) return s;
+        QK_CUDA(cudaEventRecord(ctx->ev_out[c], st));
+        QK_CUDA(cudaStreamWaitEvent(ctx->s_out, ctx->ev_out[c], 0));
+        QK_CUDA(cudaMemcpyAsync(yh + m0 * N * ye, yd + m0 * N * ye, static_cast<size_t>(mc * N) * ye,
+                                cudaMemcpyDeviceToHost, ctx->s_out));
+      }
+      QK_CUDA(cudaEventRecord(ctx->ev_done, ctx->s_out));
+      QK_CUDA(cudaStreamWaitEvent(st, ctx->ev_done, 0));
+      return QUIK_OK;
+    });
   });
 }
 
 quik_status quik_rtn_quantize_weights(quik_ctx_t ctx, const float* w, int64_t N, int64_t K,
-                                      const int64_t* outlier_indices, int64_t n_outlier, int bits, uint8_t* base,
-                                      float* scales, float* wreduced, float* outlier_weights, void* stream) {
+                                      const int64_t* outlier_indices, int64_t n_outlier, int bits, int use_clipping,
+                                      uint8_t* base, float* scales, float* wreduced, float* outlier_weights,
+                                      void* stream) {
   if (!ctx) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context");
   if (bits != 4 && bits != 8) return fail(QUIK_ERR_INVALID_ARGUMENT, "weight bits must be 4 or 8");
   if (N < 0 || K < 0 || n_outlier < 0 || n_outlier > K)
@@ -1178,21 +1252,238 @@ quik_status quik_rtn_quantize_weights(quik_ctx_t ctx, const float* w, int64_t N,
   }
   return guarded([&] {
     DeviceGuard g(ctx->device);
+    return on_stream(ctx, as_stream(stream), [&]() -> quik_status {
+      cudaStream_t st = as_stream(stream);
+      const int64_t kb = K - n_outlier;
+      std::vector<int32_t> tab(static_cast<size_t>(K));
+      std::vector<char> is_out(static_cast<size_t>(K), 0);
+      for (int64_t i = 0; i < n_outlier; ++i) is_out[outlier_indices[i]] = 1;
+      int64_t p = 0;
+      for (int64_t f = 0; f < K; ++f)
+        if (!is_out[f]) tab[p++] = static_cast<int32_t>(f);
+      for (int64_t i = 0; i < n_outlier; ++i) tab[p++] = static_cast<int32_t>(outlier_indices[i]);
+      int32_t* dtab = static_cast<int32_t*>(ctx->xbase.ensure(static_cast<size_t>(std::max<int64_t>(K, 1) * 4)));
+      if (K) QK_CUDA(cudaMemcpyAsync(dtab, tab.data(), K * 4, cudaMemcpyHostToDevice, st));
+      float* clip = nullptr;
+      if (use_clipping && kb > 0) {  // clip_search per row (quantizer.cpp:266-290, :355)
+        clip = static_cast<float*>(ctx->aux.ensure(static_cast<size_t>(std::max<int64_t>(N, 1) * 4)));
+        check_launch(launch_clip_search(w, N, K, dtab, kb, bits, clip, st), "clip search kernel");
+      }
+      check_launch(launch_rtn_weights(w, N, K, dtab, kb, dtab + kb, n_outlier, bits, base, scales, wreduced,
+                                      outlier_weights, clip, st),
+                   "rtn weight kernel");
+      QK_CUDA(cudaStreamSynchronize(st));  // tab must outlive the copy
+      return QUIK_OK;
+    });
+  });
+}
+
+quik_status quik_layer_layout(quik_layer_t L, int64_t* kpad, int64_t* opad) {
+  if (!L) return fail(QUIK_ERR_INVALID_ARGUMENT, "null layer");
+  if (kpad) *kpad = L->kpad;
+  if (opad) *opad = L->opad;
+  return QUIK_OK;
+}
+
+quik_status quik_ctx_clear_error(quik_ctx_t ctx, void* stream) {
+  if (!ctx) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    QK_CUDA(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), as_stream(stream)));
+    return QUIK_OK;
+  });
+}
+
+quik_status quik_ctx_reserve(quik_ctx_t ctx, quik_layer_t L, int64_t M) {
+  if (!ctx || !L) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context or layer");
+  if (M < 0 || M > 0x7fffffffLL) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_ctx_reserve: bad token count");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    t_call_stream = nullptr;
+    if (M == 0) return QUIK_OK;
+    const int64_t N = L->out_features;
+    if (L->kpad) ctx->q8.ensure(static_cast<size_t>(M * L->kpad));
+    ctx->scale.ensure(M * 4);
+    ctx->zero.ensure(M * 4);
+    if (L->opad) ctx->xo16.ensure(static_cast<size_t>(M * L->opad * 2));
+    if (M <= 32 && L->kpad && !L->sparse) {  // decode kernel workspace + counters (zeroed)
+      ctx->ensure_ws(static_cast<size_t>(M * N * 4), nullptr);
+      ctx->ensure_s4_counters(quikb200::stream4_counter_count(N), nullptr);
+      ensure_w4(L, nullptr, L->bits == 4);
+    }
+    QK_CUDA(cudaDeviceSynchronize());
+    return QUIK_OK;
+  });
+}
+
+quik_status quik_linear_forward_timed(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M,
+                                      void* y, quik_dtype ydt, int64_t ldy, quik_variant variant, void* stream,
+                                      double* stage_ms, int* fused_flags) {
+  if (!ctx || !L) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context or layer");
+  if (M < 0) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_matmul: negative token count");
+  if (M > 0 && (!x || !y)) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_matmul: null input or output");
+  if (M > 0x7fffffffLL) return fail(QUIK_ERR_UNSUPPORTED, "quik_matmul: token count exceeds 2^31");
+  if (ldy < (L->gated ? L->out_features / 2 : L->out_features))
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_matmul: output pitch < out_features");
+  if (L->in_features * (xdt == QUIK_F32 ? 4 : 2) > 128 * 1024)
+    return fail(QUIK_ERR_UNSUPPORTED, "quik_matmul: row wider than 128 KiB (register-resident quantizer limit)");
+  if (ctx->device != L->device) return fail(QUIK_ERR_INVALID_ARGUMENT, "context and layer live on different devices");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
     cudaStream_t st = as_stream(stream);
-    const int64_t kb = K - n_outlier;
-    std::vector<int32_t> tab(static_cast<size_t>(K));
-    std::vector<char> is_out(static_cast<size_t>(K), 0);
-    for (int64_t i = 0; i < n_outlier; ++i) is_out[outlier_indices[i]] = 1;
-    int64_t p = 0;
-    for (int64_t f = 0; f < K; ++f)
-      if (!is_out[f]) tab[p++] = static_cast<int32_t>(f);
-    for (int64_t i = 0; i < n_outlier; ++i) tab[p++] = static_cast<int32_t>(outlier_indices[i]);
-    int32_t* dtab = static_cast<int32_t*>(ctx->xbase.ensure(static_cast<size_t>(std::max<int64_t>(K, 1) * 4)));
-    if (K) QK_CUDA(cudaMemcpyAsync(dtab, tab.data(), K * 4, cudaMemcpyHostToDevice, st));
-    check_launch(launch_rtn_weights(w, N, K, dtab, kb, dtab + kb, n_outlier, bits, base, scales, wreduced,
-                                    outlier_weights, st),
-                 "rtn weight kernel");
-    QK_CUDA(cudaStreamSynchronize(st));  // tab must outlive the copy
+    cudaEvent_t ev[5] = {};
+    for (auto& e : ev) QK_CUDA(cudaEventCreate(&e));
+    struct Free {
+      cudaEvent_t* e;
+      ~Free() {
+        for (int i = 0; i < 5; ++i) cudaEventDestroy(e[i]);
+      }
+    } free_ev{ev};
+    StageMarks sm;
+    const bool v1 = variant == QUIK_V1_UNFUSED, v3 = variant == QUIK_V3_FUSED_EPILOGUE;
+    sm.after_split = v1 ? ev[1] : nullptr;
+    sm.after_quant = ev[2];
+    sm.after_int = v3 ? nullptr : ev[3];
+    QK_CUDA(cudaEventRecord(ev[0], st));
+    const quik_status r = on_stream(ctx, st, [&] { return forward_impl(ctx, L, x, xdt, M, y, ydt, ldy, variant, st, sm); });
+    if (r != QUIK_OK) return r;
+    QK_CUDA(cudaEventRecord(ev[4], st));
+    QK_CUDA(cudaEventSynchronize(ev[4]));
+    // StageTimes (runtime.hpp:72-80): a fused stage reports under the first field it covers
+    // and flags itself fused. V3: K1 = split + quantize (quantize_ms, quantize_fused); the
+    // fused GEMM = int matmul + outlier matmul + dequantize + add (int_matmul_ms,
+    // dequantize_fused). V1 / V2: the int32 GEMM alone (int_matmul_ms), then one epilogue
+    // kernel = outlier matmul + dequantize + add (fp_matmul_ms, dequantize_fused).
+    double t[6] = {0, 0, 0, 0, 0, 0};
+    float ms = 0.0f;
+    if (M > 0 && L->out_features > 0) {
+      cudaEvent_t prev = ev[0];
+      if (v1) {
+        QK_CUDA(cudaEventElapsedTime(&ms, prev, ev[1]));
+        t[0] = ms;
+        prev = ev[1];
+      }
+      QK_CUDA(cudaEventElapsedTime(&ms, prev, ev[2]));
+      t[1] = ms;
+      if (v3) {
+        QK_CUDA(cudaEventElapsedTime(&ms, ev[2], ev[4]));
+        t[2] = ms;
+      } else {
+        QK_CUDA(cudaEventElapsedTime(&ms, ev[2], ev[3]));
+        t[2] = ms;
+        QK_CUDA(cudaEventElapsedTime(&ms, ev[3], ev[4]));
+        t[3] = ms;
+      }
+    }
+    if (stage_ms)
+      for (int i = 0; i < 6; ++i) stage_ms[i] = t[i];
+    if (fused_flags) {
+      fused_flags[0] = v1 ? 0 : 1;  // quantize_fused
+      fused_flags[1] = 1;           // dequantize_fused
+    }
+    return QUIK_OK;
+  });
+}
+
+quik_status quik_split_activations(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M,
+                                   float* x_base, float* x_outlier, void* stream) {
+  if (!ctx || !L) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context or layer");
+  if (M < 0 || (M > 0 && (!x || (L->kb && !x_base) || (L->n_outlier && !x_outlier))))
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "split_activations: bad arguments");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    return on_stream(ctx, as_stream(stream), [&]() -> quik_status {
+      SplitArgs s{};
+      s.x = x;
+      s.x_is_f32 = xdt == QUIK_F32;
+      s.M = M;
+      s.K = L->in_features;
+      s.ldx = L->in_features;
+      s.base_src = L->base_src;
+      s.kb = L->kb;
+      s.out_src = L->out_src;
+      s.n_out = L->n_outlier;
+      s.xbase = x_base;
+      s.xo32 = x_outlier;
+      s.opad = L->n_outlier;
+      check_launch(launch_split(s, as_stream(stream)), "split kernel");
+      return QUIK_OK;
+    });
+  });
+}
+
+quik_status quik_unpack_values(quik_ctx_t ctx, const uint8_t* packed, int64_t rows, int64_t cols, int bits,
+                               int8_t* out, void* stream) {
+  if (!ctx) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context");
+  if (bits != 4 && bits != 8) return fail(QUIK_ERR_INVALID_ARGUMENT, "unpack: bits must be 4 or 8");
+  if (rows < 0 || cols < 0 || (rows > 0 && cols > 0 && (!packed || !out)))
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "unpack: bad arguments");
+  if (rows > 0xffffLL * 0xffffLL) return fail(QUIK_ERR_UNSUPPORTED, "unpack: too many rows");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    check_launch(launch_unpack_to_gemm(packed, rows, cols, bits, out, cols, as_stream(stream)), "unpack kernel");
+    return QUIK_OK;
+  });
+}
+
+quik_status quik_compute_wreduced(quik_ctx_t ctx, const uint8_t* base, int64_t rows, int64_t cols, int bits,
+                                  const float* scales, float* wreduced, void* stream) {
+  if (!ctx) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context");
+  if (bits != 4 && bits != 8) return fail(QUIK_ERR_INVALID_ARGUMENT, "weight bits must be 4 or 8");
+  if (rows < 0 || cols < 0 || (rows > 0 && (!scales || !wreduced || (cols > 0 && !base))))
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "compute_wreduced: bad arguments");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    check_launch(launch_compute_wreduced(base, rows, cols, bits, scales, wreduced, as_stream(stream)),
+                 "wreduced kernel");
+    return QUIK_OK;
+  });
+}
+
+quik_status quik_dequantize_weights(quik_ctx_t ctx, const uint8_t* base, int64_t rows, int64_t in_features, int bits,
+                                    const float* scales, const float* outlier_weights, const int64_t* outlier_indices,
+                                    int64_t n_outlier, float* out, void* stream) {
+  if (!ctx) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context");
+  if (bits != 4 && bits != 8) return fail(QUIK_ERR_INVALID_ARGUMENT, "weight bits must be 4 or 8");
+  if (rows < 0 || in_features < 0 || n_outlier < 0 || n_outlier > in_features)
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "dequantize_weights: outlier set does not match weights");
+  if (n_outlier > 0 && !outlier_indices) return fail(QUIK_ERR_INVALID_ARGUMENT, "outlier indices missing");
+  for (int64_t i = 0; i < n_outlier; ++i) {
+    const int64_t v = outlier_indices[i];
+    if (v < 0 || v >= in_features || (i > 0 && v <= outlier_indices[i - 1]))
+      return fail(QUIK_ERR_INVALID_ARGUMENT, "OutlierSet: indices must be sorted, unique and inside the feature range");
+  }
+  if (rows > 0xffffLL) return fail(QUIK_ERR_UNSUPPORTED, "dequantize_weights: more than 65535 rows per call");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    return on_stream(ctx, as_stream(stream), [&]() -> quik_status {
+      cudaStream_t st = as_stream(stream);
+      std::vector<int32_t> perm(static_cast<size_t>(in_features));
+      std::vector<char> is_out(static_cast<size_t>(in_features), 0);
+      for (int64_t i = 0; i < n_outlier; ++i) is_out[outlier_indices[i]] = 1;
+      int64_t p = 0;
+      for (int64_t f = 0; f < in_features; ++f)
+        if (!is_out[f]) perm[p++] = static_cast<int32_t>(f);
+      for (int64_t i = 0; i < n_outlier; ++i) perm[p++] = static_cast<int32_t>(outlier_indices[i]);
+      int32_t* dperm = static_cast<int32_t*>(ctx->aux.ensure(static_cast<size_t>(std::max<int64_t>(in_features, 1) * 4)));
+      if (in_features) QK_CUDA(cudaMemcpyAsync(dperm, perm.data(), in_features * 4, cudaMemcpyHostToDevice, st));
+      check_launch(launch_dequantize_weights(base, rows, in_features, in_features - n_outlier, bits, scales, dperm,
+                                             outlier_weights, out, st),
+                   "dequantize weights kernel");
+      QK_CUDA(cudaStreamSynchronize(st));  // perm must outlive the copy
+      return QUIK_OK;
+    });
+  });
+}
+
+quik_status quik_elementwise(quik_ctx_t ctx, int op, const float* a, const float* b, float* out, int64_t n,
+                             void* stream) {
+  if (!ctx) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context");
+  if (op < 0 || op > 2) return fail(QUIK_ERR_INVALID_ARGUMENT, "elementwise: op must be silu (0), multiply (1), add (2)");
+  if (n < 0 || (n > 0 && (!a || !out || (op > 0 && !b)))) return fail(QUIK_ERR_INVALID_ARGUMENT, "elementwise: bad arguments");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    check_launch(launch_elementwise(op, a, b, out, n, as_stream(stream)), "elementwise kernel");
     return QUIK_OK;
   });
 }

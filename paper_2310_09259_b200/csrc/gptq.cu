@@ -82,7 +82,7 @@ __global__ void scales_kernel(const double* __restrict__ wd, int64_t N, int64_t 
     if (use_clipping && kb > 0) {
       double best_err = INFINITY;
       for (int step = 0; step <= 50; ++step) {
-        const float c = static_cast<float>(0.50 + 0.01 * step);
+        const float c = static_cast<float>(__dadd_rn(0.50, __dmul_rn(0.01, static_cast<double>(step))));
         const double scale = __ddiv_rn(__dmul_rn(static_cast<double>(c), amax), static_cast<double>(maxq));
         const double inv = __ddiv_rn(1.0, scale);
         double err = 0.0;

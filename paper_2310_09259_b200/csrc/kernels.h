@@ -252,6 +252,7 @@ struct SplitArgs {
   float* xbase;
   __half* xo16;
   int64_t opad;
+  float* xo32;  // split_activations: f32 outlier columns [M][n_out] (instead of xo16)
 };
 cudaError_t launch_split(const SplitArgs& a, cudaStream_t stream);
 
@@ -267,7 +268,18 @@ cudaError_t launch_f32_to_f16_padded(const float* src, int64_t rows, int64_t col
 // packed base [N][row_bytes(kb)], scales, wreduced, outlier weights [N][n_out].
 cudaError_t launch_rtn_weights(const float* w, int64_t N, int64_t K, const int32_t* base_src, int64_t kb,
                                const int32_t* out_src, int64_t n_out, int bits, uint8_t* base, float* scales,
-                               float* wreduced, float* outlier_w, cudaStream_t stream);
+                               float* wreduced, float* outlier_w, const float* clip, cudaStream_t stream);
+
+// weights.cu: clip_search per row (clip may then feed launch_rtn_weights), compute_wreduced,
+// dequantize_weights, forward_model's elementwise ops (0 silu, 1 multiply, 2 add).
+cudaError_t launch_clip_search(const float* w, int64_t N, int64_t K, const int32_t* base_src, int64_t kb, int bits,
+                               float* clip, cudaStream_t stream);
+cudaError_t launch_compute_wreduced(const uint8_t* base, int64_t N, int64_t kb, int bits, const float* scales,
+                                    float* out, cudaStream_t stream);
+cudaError_t launch_dequantize_weights(const uint8_t* base, int64_t N, int64_t K, int64_t kb, int bits,
+                                      const float* scales, const int32_t* perm, const float* ow, float* out,
+                                      cudaStream_t stream);
+cudaError_t launch_elementwise(int op, const float* a, const float* b, float* out, int64_t n, cudaStream_t stream);
 
 // dequantize_epilogue (runtime.cpp:222-244): out[t][r] = dequant_element(...).
 cudaError_t launch_dequant(const int32_t* acc, int64_t M, int64_t N, const float* a_scale,

@@ -780,6 +780,13 @@ __global__ void split_kernel(const SplitArgs a) {
       const int64_t c = a.base_src[j];
       a.xbase[t * a.kb + j] = a.x_is_f32 ? reinterpret_cast<const float*>(a.x)[t * a.ldx + c]
                                          : __half2float(reinterpret_cast<const __half*>(a.x)[t * a.ldx + c]);
+    } else if (a.xo32) {
+      const int64_t i = j - a.kb;
+      if (i < a.n_out) {
+        const int64_t c = a.out_src[i];
+        a.xo32[t * a.n_out + i] = a.x_is_f32 ? reinterpret_cast<const float*>(a.x)[t * a.ldx + c]
+                                             : __half2float(reinterpret_cast<const __half*>(a.x)[t * a.ldx + c]);
+      }
     } else if (a.xo16) {
       const int64_t i = j - a.kb;
       float v = 0.0f;
@@ -851,7 +858,8 @@ __global__ void __launch_bounds__(256) rtn_rows_kernel(const float* __restrict__
                                                        const int32_t* __restrict__ base_src, int64_t kb,
                                                        const int32_t* __restrict__ out_src, int64_t n_out, int bits,
                                                        uint8_t* __restrict__ base, float* __restrict__ scales,
-                                                       float* __restrict__ wreduced, float* __restrict__ outlier_w) {
+                                                       float* __restrict__ wreduced, float* __restrict__ outlier_w,
+                                                       const float* __restrict__ clip) {
   __shared__ float s_amax[8];
   __shared__ long long s_sum[8];
   const int64_t r = blockIdx.x;
@@ -866,7 +874,10 @@ __global__ void __launch_bounds__(256) rtn_rows_kernel(const float* __restrict__
   for (int i = 1; i < 8; ++i) amax = fmaxf(amax, s_amax[i]);
   const int maxq = (1 << (bits - 1)) - 1;
   const bool zero_row = amax == 0.0f;
-  const double scale = zero_row ? 1.0 : __ddiv_rn(static_cast<double>(amax), static_cast<double>(maxq));
+  // rtn_quantize_row: scale = double(clip_factor) * amax / maxq (clip_factor 1 without clipping)
+  const double camax = clip ? __dmul_rn(static_cast<double>(clip[r]), static_cast<double>(amax))
+                            : static_cast<double>(amax);
+  const double scale = zero_row ? 1.0 : __ddiv_rn(camax, static_cast<double>(maxq));
   const double inv_scale = __ddiv_rn(1.0, scale);
   const int64_t rb = bits == 4 ? (kb + 1) / 2 : kb;
   long long qsum = 0;
@@ -1150,10 +1161,10 @@ cudaError_t launch_f32_to_f16_padded(const float* src, int64_t rows, int64_t col
 
 cudaError_t launch_rtn_weights(const float* w, int64_t N, int64_t K, const int32_t* base_src, int64_t kb,
                                const int32_t* out_src, int64_t n_out, int bits, uint8_t* base, float* scales,
-                               float* wreduced, float* outlier_w, cudaStream_t stream) {
+                               float* wreduced, float* outlier_w, const float* clip, cudaStream_t stream) {
   if (N == 0) return cudaSuccess;
   rtn_rows_kernel<<<static_cast<unsigned>(N), 256, 0, stream>>>(w, K, base_src, kb, out_src, n_out, bits, base,
-                                                                scales, wreduced, outlier_w);
+                                                                scales, wreduced, outlier_w, clip);
   return cudaGetLastError();
 }
 

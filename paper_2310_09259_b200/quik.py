@@ -430,18 +430,49 @@ class QuikLinear:
             raise ValueError("quik_matmul: input must be float16 or float32")
         x = x.contiguous()
         M = x.shape[0]
-        if out is None:
-            dt = out_dtype or torch.float16
-            out = torch.empty((M, self.out_features), dtype=dt, device=x.device)
+        out = self._check_out(torch, x, out, out_dtype, "quik_matmul")
         ydt = _lib.QUIK_F16 if out.dtype == torch.float16 else _lib.QUIK_F32
         xdt = _lib.QUIK_F16 if x.dtype == torch.float16 else _lib.QUIK_F32
-        ldy = out.stride(0)
-        if out.stride(1) != 1 or ldy < self.out_features:
-            raise ValueError("output must be row-major with pitch >= out_features")
         _lib.check(self._lib.quik_linear_forward_ex(
-            self.ctx.handle, self.handle, _ptr(x), xdt, M, _ptr(out), ydt, ldy, int(variant),
+            self._ctx_handle(), self.handle, _ptr(x), xdt, M, _ptr(out), ydt, out.stride(0), int(variant),
             C.c_void_p(_stream_ptr(torch, x.device)), C.c_void_p(mid_event.cuda_event if mid_event else None)))
         return out
+
+    def _ctx_handle(self):
+        """The calling thread's context on this layer's device (scratch is per context)."""
+        return context(self.device).handle
+
+    def _check_out(self, torch, x, out, out_dtype, what):
+        """Allocates or validates the output: f16 / f32, row-major, >= M rows and
+        out_features columns, on the layer's device (as x)."""
+        M = x.shape[0]
+        if x.device.type != "cuda" or x.device.index != self.device:
+            raise ValueError(f"{what}: input must live on cuda:{self.device}")
+        if out is None:
+            dt = out_dtype or torch.float16
+            if dt not in (torch.float16, torch.float32):
+                raise ValueError(f"{what}: output dtype must be float16 or float32")
+            return torch.empty((M, self.out_features), dtype=dt, device=x.device)
+        if out.dtype not in (torch.float16, torch.float32):
+            raise ValueError(f"{what}: output dtype must be float16 or float32, got {out.dtype}")
+        if out.device != x.device:
+            raise ValueError(f"{what}: output on {out.device}, input on {x.device}")
+        if out.dim() != 2 or out.shape[0] < M or out.shape[1] < self.out_features:
+            raise ValueError(f"{what}: output must be at least [{M}][{self.out_features}], got {tuple(out.shape)}")
+        if out.stride(1) != 1 or out.stride(0) < self.out_features:
+            raise ValueError(f"{what}: output must be row-major with pitch >= out_features")
+        return out
+
+    def reserve(self, max_tokens: int) -> None:
+        """Sizes this thread's context scratch for forwards of up to max_tokens (C ABI
+        quik_ctx_reserve) so that forwards can be captured into a CUDA graph."""
+        _lib.check(self._lib.quik_ctx_reserve(self._ctx_handle(), self.handle, int(max_tokens)))
+
+    def check_numerics(self) -> None:
+        """Waits for the current stream and raises NumericalError if a forward since the
+        last check saw a non-finite activation (reference runtime.cpp:52)."""
+        torch = _torch()
+        _lib.check(self._lib.quik_ctx_sync(self._ctx_handle(), C.c_void_p(_stream_ptr(torch, self.device))))
 
     __call__ = forward
 
@@ -460,7 +491,7 @@ class QuikLinear:
         arr = (C.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
         xdt = _lib.QUIK_F16 if x.dtype == torch.float16 else _lib.QUIK_F32
         _lib.check(self._lib.quik_linear_forward_sharded(
-            self.ctx.handle, self.handle, _ptr(x), xdt, M, arr, len(outs), ldy, col_offset,
+            self._ctx_handle(), self.handle, _ptr(x), xdt, M, arr, len(outs), ldy, col_offset,
             C.c_void_p(_stream_ptr(torch, x.device))))
         return outs
 
@@ -476,14 +507,11 @@ class QuikLinear:
             raise ValueError("weight_only_forward: input must be float16 or float32")
         x = x.contiguous()
         M = x.shape[0]
-        if out is None:
-            out = torch.empty((M, self.out_features), dtype=out_dtype or torch.float16, device=x.device)
-        if out.stride(1) != 1 or out.stride(0) < self.out_features:
-            raise ValueError("output must be row-major with pitch >= out_features")
+        out = self._check_out(torch, x, out, out_dtype, "weight_only_forward")
         ydt = _lib.QUIK_F16 if out.dtype == torch.float16 else _lib.QUIK_F32
         xdt = _lib.QUIK_F16 if x.dtype == torch.float16 else _lib.QUIK_F32
         _lib.check(self._lib.quik_linear_forward_weight_only(
-            self.ctx.handle, self.handle, _ptr(x), xdt, M, _ptr(out), ydt, out.stride(0),
+            self._ctx_handle(), self.handle, _ptr(x), xdt, M, _ptr(out), ydt, out.stride(0),
             C.c_void_p(_stream_ptr(torch, x.device))))
         return out
 
@@ -492,9 +520,9 @@ class QuikLinear:
         Returns (codes int8 [M][kpad], scale [M], zero [M], x_outlier f16 [M][opad])."""
         torch = _torch()
         M = x.shape[0]
-        kb = self.in_features - self.n_outlier
-        kpad = (kb + 127) // 128 * 128
-        opad = (self.n_outlier + 63) // 64 * 64
+        kp, op = C.c_int64(), C.c_int64()
+        _lib.check(self._lib.quik_layer_layout(self.handle, C.byref(kp), C.byref(op)))
+        kpad, opad = kp.value, op.value
         dev = x.device
         codes = torch.empty((M, kpad), dtype=torch.int8, device=dev)
         scale = torch.empty(M, dtype=torch.float32, device=dev)
@@ -502,9 +530,9 @@ class QuikLinear:
         xo = torch.empty((M, opad), dtype=torch.float16, device=dev)
         xdt = _lib.QUIK_F16 if x.dtype == torch.float16 else _lib.QUIK_F32
         _lib.check(self._lib.quik_quantize_activations_gemm(
-            self.ctx.handle, self.handle, _ptr(x.contiguous()), xdt, M, _ptr(codes), _ptr(scale), _ptr(zero), _ptr(xo),
+            self._ctx_handle(), self.handle, _ptr(x.contiguous()), xdt, M, _ptr(codes), _ptr(scale), _ptr(zero), _ptr(xo),
             C.c_void_p(_stream_ptr(torch, dev))))
-        _lib.check(self._lib.quik_ctx_sync(self.ctx.handle, C.c_void_p(_stream_ptr(torch, dev))))
+        _lib.check(self._lib.quik_ctx_sync(self._ctx_handle(), C.c_void_p(_stream_ptr(torch, dev))))
         return codes, scale, zero, xo
 
     def forward_host(self, x, out, chunk_tokens: int = 0):
@@ -524,7 +552,7 @@ class QuikLinear:
         ydt = _lib.QUIK_F16 if out.dtype == torch.float16 else _lib.QUIK_F32
         dev = torch.device("cuda", self.device)
         _lib.check(self._lib.quik_linear_forward_host(
-            self.ctx.handle, self.handle, C.c_void_p(x.data_ptr()), xdt, x.shape[0], C.c_void_p(out.data_ptr()), ydt,
+            self._ctx_handle(), self.handle, C.c_void_p(x.data_ptr()), xdt, x.shape[0], C.c_void_p(out.data_ptr()), ydt,
             int(chunk_tokens), C.c_void_p(_stream_ptr(torch, dev))))
         return out
 
@@ -559,6 +587,7 @@ def quantize_activations_fused(x: np.ndarray, outliers: OutlierSet, bits: int):
     zero = torch.empty(max(M, 1), dtype=torch.float32, device=dx.device)
     xo = torch.empty(max(M * outliers.outlier_count(), 1), dtype=torch.float32, device=dx.device)
     s = _stream_ptr(torch, dx.device)
+    _lib.check(L._lib.quik_ctx_clear_error(ctx.handle, C.c_void_p(s)))  # report this call's errors only
     _lib.check(L._lib.quik_quantize_activations_fused(ctx.handle, L.handle, _ptr(dx), _lib.QUIK_F32, M,
                                                       _ptr(packed), _ptr(scale), _ptr(zero), _ptr(xo), C.c_void_p(s)))
     ctx.sync(s)
@@ -583,6 +612,7 @@ def quantize_activations(x_base: np.ndarray, bits: int) -> ActQuantResult:
     scale = torch.empty(max(M, 1), dtype=torch.float32, device=dx.device)
     zero = torch.empty(max(M, 1), dtype=torch.float32, device=dx.device)
     s = _stream_ptr(torch, dx.device)
+    _lib.check(_lib.load().quik_ctx_clear_error(ctx.handle, C.c_void_p(s)))
     _lib.check(_lib.load().quik_quantize_activations(ctx.handle, _ptr(dx), _lib.QUIK_F32, M, K, bits, _ptr(packed),
                                                      _ptr(scale), _ptr(zero), C.c_void_p(s)))
     ctx.sync(s)
@@ -693,8 +723,9 @@ def load_layer(path) -> QuikLinearLayer:
         lib.quik_bundle_close(h)
 
 
-def rtn_quantize_weights_device(w, outliers: OutlierSet, bits: int):
-    """reference: rtn_quantize_weights (quantizer.cpp:339-371), on the device.
+def rtn_quantize_weights_device(w, outliers: OutlierSet, bits: int, use_clipping: bool = False):
+    """reference: rtn_quantize_weights (quantizer.cpp:339-371; use_clipping -> per-row
+    clip_search, :266-290), on the device.
 
     w: CUDA f32 tensor [out][in]. Returns device tensors (base_packed u8
     [out*row_bytes], scales, wreduced, outlier_weights [out][n_outlier])."""
@@ -715,7 +746,8 @@ def rtn_quantize_weights_device(w, outliers: OutlierSet, bits: int):
     idx = np.ascontiguousarray(outliers.indices, dtype=np.int64)
     s = _stream_ptr(torch, w.device)
     _lib.check(_lib.load().quik_rtn_quantize_weights(
-        ctx.handle, _ptr(w), N, K, C.c_void_p(idx.ctypes.data if idx.size else None), O, bits, _ptr(base),
+        ctx.handle, _ptr(w), N, K, C.c_void_p(idx.ctypes.data if idx.size else None), O, bits, int(use_clipping),
+        _ptr(base),
         _ptr(scales), _ptr(wred), _ptr(ow), C.c_void_p(s)))
     return base[: N * row_bytes(kb, bits)], scales[:N], wred[:N], ow[: N * O].view(N, O)
 
@@ -790,8 +822,8 @@ def gptq_quantize_device(w, outliers: OutlierSet, bits: int, hessian_sum, dampin
     return qw
 
 
-def rtn_quantize_weights(w: np.ndarray, outliers: OutlierSet, bits: int) -> QuantizedWeights:
-    """reference: rtn_quantize_weights (quantizer.hpp:87-88), use_clipping = false.
+def rtn_quantize_weights(w: np.ndarray, outliers: OutlierSet, bits: int, use_clipping: bool = False) -> QuantizedWeights:
+    """reference: rtn_quantize_weights (quantizer.hpp:89-90), bit-exact incl. use_clipping.
     Host f32 [out][in] in, QuantizedWeights (host arrays) out; computed on the GPU."""
     torch = _torch()
     w = np.ascontiguousarray(w, dtype=np.float32)
@@ -799,7 +831,7 @@ def rtn_quantize_weights(w: np.ndarray, outliers: OutlierSet, bits: int) -> Quan
         raise ValueError(f"outlier set covers {outliers.feature_count} features, weights have {w.shape[-1]}")
     ctx = context()
     dw = _dev(torch, w, ctx.device)
-    base, sc, wr, ow = rtn_quantize_weights_device(dw, outliers, bits)
+    base, sc, wr, ow = rtn_quantize_weights_device(dw, outliers, bits, use_clipping)
     ctx.sync(_stream_ptr(torch, dw.device))
     N = w.shape[0]
     return QuantizedWeights(PackedIntMatrix(N, outliers.base_count(), bits, base.cpu().numpy()), sc.cpu().numpy(),
@@ -821,17 +853,187 @@ def quik_matmul(layer: QuikLinearLayer, x: np.ndarray,
     dev = QuikLinear(layer)
     dx = _dev(torch, x, dev.device)
     dt = torch.float32 if out_dtype == "float32" else torch.float16
-    ev = None
+    y = torch.empty((x.shape[0], dev.out_features), dtype=dt, device=dx.device)
+    s = C.c_void_p(_stream_ptr(torch, dx.device))
+    h = dev._ctx_handle()
+    _lib.check(dev._lib.quik_ctx_clear_error(h, s))  # report this call's errors only
+    ydt = _lib.QUIK_F16 if dt == torch.float16 else _lib.QUIK_F32
     if times is not None:
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-        ev[0].record()
-    y = dev.forward(dx, out_dtype=dt, variant=variant)
-    if ev is not None:
-        ev[1].record()
-    dev.ctx.sync(_stream_ptr(torch, dx.device))
-    if times is not None:
-        ms = ev[0].elapsed_time(ev[1])
-        times.quantize_fused = variant != PipelineVariant.V1Unfused
-        times.dequantize_fused = variant == PipelineVariant.V3FusedEpilogue
-        times.int_matmul_ms = ms  # one fused kernel pair; split timing lives in bench.py
+        # per-stage CUDA-event times, the reference's fused-stage convention (C ABI
+        # quik_linear_forward_timed; runtime.cpp:265-315)
+        ms = (C.c_double * 6)()
+        fl = (C.c_int * 2)()
+        _lib.check(dev._lib.quik_linear_forward_timed(h, dev.handle, _ptr(dx), _lib.QUIK_F32, x.shape[0], _ptr(y), ydt,
+                                                      dev.out_features, int(variant), s, ms, fl))
+        (times.split_ms, times.quantize_ms, times.int_matmul_ms, times.fp_matmul_ms, times.dequantize_ms,
+         times.add_ms) = list(ms)
+        times.quantize_fused, times.dequantize_fused = bool(fl[0]), bool(fl[1])
+    else:
+        dev.forward(dx, out=y, variant=variant)
+    _lib.check(dev._lib.quik_ctx_sync(h, s))
     return y.float().cpu().numpy()
+
+
+def split_activations(x: np.ndarray, outliers: OutlierSet):
+    """reference: split_activations (runtime.hpp:48, runtime.cpp:169-186) on the device:
+    x [M][K] -> (base [M][K_b] in permuted order, outlier columns [M][n_outlier]), f32."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    if x.ndim != 2 or x.shape[1] != outliers.feature_count:
+        raise ValueError(f"split_activations: input has {x.shape[-1]} features, outlier set covers "
+                         f"{outliers.feature_count}")
+    torch = _torch()
+    ctx = context()
+    M = x.shape[0]
+    kb, O = outliers.base_count(), outliers.outlier_count()
+    L = _outlier_handle(torch, outliers, 4, ctx.device)
+    dx = _dev(torch, x, ctx.device)
+    base = torch.empty(max(M * kb, 1), dtype=torch.float32, device=dx.device)
+    outl = torch.empty(max(M * O, 1), dtype=torch.float32, device=dx.device)
+    s = _stream_ptr(torch, dx.device)
+    _lib.check(L._lib.quik_split_activations(ctx.handle, L.handle, _ptr(dx), _lib.QUIK_F32, M, _ptr(base), _ptr(outl),
+                                             C.c_void_p(s)))
+    ctx.sync(s)
+    return base.cpu().numpy()[: M * kb].reshape(M, kb), outl.cpu().numpy()[: M * O].reshape(M, O)
+
+
+def _unpack_device(m: PackedIntMatrix) -> np.ndarray:
+    torch = _torch()
+    ctx = context()
+    n = m.rows * m.cols
+    if n == 0:
+        return np.zeros((m.rows, m.cols), np.int8)
+    dp = _dev(torch, m.data, ctx.device)
+    out = torch.empty(n, dtype=torch.int8, device=dp.device)
+    s = _stream_ptr(torch, dp.device)
+    _lib.check(_lib.load().quik_unpack_values(ctx.handle, _ptr(dp), m.rows, m.cols, m.bits, _ptr(out), C.c_void_p(s)))
+    ctx.sync(s)
+    return out.cpu().numpy().reshape(m.rows, m.cols)
+
+
+def unpack_int4(m: PackedIntMatrix) -> np.ndarray:
+    """reference: unpack_int4 (packed.hpp:48, packed.cpp:68-84) on the device; ValueError
+    (std::invalid_argument) unless m.bits == 4."""
+    if m.bits != 4:
+        raise ValueError("unpack_int4: matrix is not 4-bit")
+    return _unpack_device(m)
+
+
+def compute_wreduced(q: QuantizedWeights) -> np.ndarray:
+    """reference: compute_wreduced (quantizer.hpp:94, quantizer.cpp:373-382) on the device."""
+    torch = _torch()
+    ctx = context()
+    N = q.base.rows
+    if N == 0:
+        return np.zeros(0, np.float32)
+    db = _dev(torch, q.base.data if q.base.data.size else np.zeros(1, np.uint8), ctx.device)
+    ds = _dev(torch, np.ascontiguousarray(q.scales, np.float32), ctx.device)
+    out = torch.empty(N, dtype=torch.float32, device=db.device)
+    s = _stream_ptr(torch, db.device)
+    _lib.check(_lib.load().quik_compute_wreduced(ctx.handle, _ptr(db), N, q.base.cols, q.base.bits, _ptr(ds),
+                                                 _ptr(out), C.c_void_p(s)))
+    ctx.sync(s)
+    return out.cpu().numpy()
+
+
+def dequantize_weights(q: QuantizedWeights, outliers: OutlierSet) -> np.ndarray:
+    """reference: dequantize_weights (quantizer.hpp:98, quantizer.cpp:384-403) on the
+    device: the de-permuted f32 [out][in] reconstruction."""
+    ow = np.asarray(q.outlier_weights, np.float32).reshape(q.base.rows, -1) if q.base.rows else \
+        np.zeros((0, outliers.outlier_count()), np.float32)
+    if outliers.base_count() != q.base.cols or outliers.outlier_count() != ow.shape[1]:
+        raise ValueError("dequantize_weights: outlier set does not match weights")
+    torch = _torch()
+    ctx = context()
+    N, K = q.base.rows, outliers.feature_count
+    if N * K == 0:
+        return np.zeros((N, K), np.float32)
+    db = _dev(torch, q.base.data if q.base.data.size else np.zeros(1, np.uint8), ctx.device)
+    ds = _dev(torch, np.ascontiguousarray(q.scales, np.float32), ctx.device)
+    dow = _dev(torch, ow if ow.size else np.zeros(1, np.float32), ctx.device)
+    out = torch.empty((N, K), dtype=torch.float32, device=db.device)
+    idx = np.ascontiguousarray(outliers.indices, np.int64)
+    s = _stream_ptr(torch, db.device)
+    rb = q.base.row_bytes()
+    O = outliers.outlier_count()
+    for r0 in range(0, N, 65535):
+        nr = min(65535, N - r0)
+        _lib.check(_lib.load().quik_dequantize_weights(
+            ctx.handle, C.c_void_p(db.data_ptr() + r0 * rb), nr, K, q.base.bits, C.c_void_p(ds.data_ptr() + 4 * r0),
+            C.c_void_p(dow.data_ptr() + 4 * r0 * O), C.c_void_p(idx.ctypes.data if idx.size else None), O,
+            C.c_void_p(out.data_ptr() + 4 * r0 * K), C.c_void_p(s)))
+    ctx.sync(s)
+    return out.cpu().numpy()
+
+
+@dataclass
+class BlockOp:
+    """reference: BlockOp (runtime.hpp:91-101): value 0 is the model input, op i produces
+    value i + 1."""
+
+    class Kind(enum.IntEnum):
+        Linear = 0
+        Silu = 1
+        Multiply = 2
+        Add = 3
+
+    kind: "BlockOp.Kind" = 0
+    a: int = 0
+    b: int = -1
+    layer: int = -1
+
+
+def gated_mlp_ops():
+    """reference: gated_mlp_ops (runtime.cpp:373-382), layers {0: up, 1: gate, 2: down}."""
+    K = BlockOp.Kind
+    return [BlockOp(K.Linear, 0, -1, 0), BlockOp(K.Linear, 0, -1, 1), BlockOp(K.Silu, 2, -1, -1),
+            BlockOp(K.Multiply, 3, 1, -1), BlockOp(K.Linear, 4, -1, 2)]
+
+
+def forward_model_trace(layers, ops, x: np.ndarray):
+    """reference: forward_model_trace (runtime.hpp:105-107, runtime.cpp:325-371) with every
+    value on the device: Linear -> the QUIK forward of the layer (f32 in/out), Silu /
+    Multiply / Add -> quik_elementwise. Returns all values (host f32)."""
+    torch = _torch()
+    ctx = context()
+    x = np.ascontiguousarray(x, np.float32)
+    dev_layers = {}
+    vals = [_dev(torch, x, ctx.device)]
+    s = _stream_ptr(torch, vals[0].device)
+    lib = _lib.load()
+
+    def value(i):
+        if i < 0 or i >= len(vals):
+            raise ValueError(f"forward_model: op references undefined value {i}")
+        return vals[i]
+
+    for op in ops:
+        k = BlockOp.Kind(op.kind)
+        if k == BlockOp.Kind.Linear:
+            if op.layer < 0 or op.layer >= len(layers):
+                raise ValueError(f"forward_model: op references undefined layer {op.layer}")
+            if op.layer not in dev_layers:
+                dev_layers[op.layer] = QuikLinear(layers[op.layer], ctx.device)
+            vals.append(dev_layers[op.layer](value(op.a), out_dtype=torch.float32))
+        elif k == BlockOp.Kind.Silu:
+            a = value(op.a)
+            out = torch.empty_like(a)
+            _lib.check(lib.quik_elementwise(ctx.handle, 0, _ptr(a), None, _ptr(out), a.numel(), C.c_void_p(s)))
+            vals.append(out)
+        else:
+            a, b = value(op.a), value(op.b)
+            if a.shape != b.shape:
+                raise ValueError(f"forward_model elementwise op: shape mismatch ({a.shape[0]}x{a.shape[1]} vs "
+                                 f"{b.shape[0]}x{b.shape[1]})")
+            out = torch.empty_like(a)
+            _lib.check(lib.quik_elementwise(ctx.handle, 1 if k == BlockOp.Kind.Multiply else 2, _ptr(a), _ptr(b),
+                                            _ptr(out), a.numel(), C.c_void_p(s)))
+            vals.append(out)
+    if len(vals) == 1:
+        raise ValueError("forward_model: empty op list")
+    ctx.sync(s)
+    return [x] + [v.cpu().numpy() for v in vals[1:]]
+
+
+def forward_model(layers, ops, x: np.ndarray) -> np.ndarray:
+    """reference: forward_model (runtime.hpp:103-104)."""
+    return forward_model_trace(layers, ops, x)[-1]

@@ -229,7 +229,8 @@ int main(int argc, char** argv) {
     const auto rt = Q::rtn_quantize_weights(w, o, 4);
     CHECK(g.base.data == rt.base.data);
     CHECK(std::memcmp(g.scales.data(), rt.scales.data(), N * 4) == 0);
-    const Q::Hessian h = Q::build_hessian({x});
+    const std::vector<Q::FpMatrix> batches = {x};
+    const Q::Hessian h = Q::build_hessian(batches);
     double maxrel = 0;
     for (int64_t i = 0; i < K; ++i)
       for (int64_t j = 0; j < K; ++j) {
@@ -238,6 +239,9 @@ int main(int argc, char** argv) {
         maxrel = std::max(maxrel, std::fabs(h.at(i, j) - ref) / (std::fabs(ref) + 1e-9));
       }
     CHECK(h.token_count == 64 && maxrel < 1e-12);
+    double tr = 0;  // Hessian::lambda (quantizer.cpp:225-229)
+    for (int64_t i = 0; i < K; ++i) tr += h.at(i, i);
+    CHECK(h.lambda() == 0.01 * tr / static_cast<double>(K));
     const auto sp = Q::sparsegpt_joint(w, h, o, 4);
     bool groups_ok = sp.mask.rows == N && sp.mask.cols == K - O;
     for (int64_t r = 0; r < N && groups_ok; ++r)
@@ -248,6 +252,105 @@ int main(int argc, char** argv) {
       }
     CHECK(groups_ok);
     CHECK(throws<std::invalid_argument>([&] { Q::gptq_quantize(w, Q::Hessian::identity(K + 1), o, 4); }));
+  }
+  // The rest of the reference surface on the device, against the oracle (quantizer.cpp /
+  // runtime.cpp / packed.cpp): rtn_quantize_weights with use_clipping (clip_search),
+  // compute_wreduced, dequantize_weights, split_activations, unpack_int4 / unpack_values,
+  // per-stage StageTimes, forward_model(gated_mlp_ops)
+  {
+    std::mt19937 rng(99);
+    std::normal_distribution<float> nd(0.f, 1.f);
+    const int64_t N = 40, K = 300, O = 12, M = 7;
+    Q::FpMatrix w(N, K), x(M, K);
+    for (float& v : w.data) v = 0.5f * nd(rng);
+    for (float& v : x.data) v = nd(rng);
+    std::vector<int64_t> idx(O);
+    qo_select_outliers(x.data.data(), M, K, O, idx.data());
+    const auto o = Q::OutlierSet::from_indices(K, idx);
+    for (int bits : {4, 8}) {
+      const auto q = Q::rtn_quantize_weights(w, o, bits, true);
+      std::vector<uint8_t> base(N * q.base.row_bytes());
+      std::vector<float> sc(N), wr(N), ow(N * O);
+      qo_rtn_quantize_weights_clip(w.data.data(), N, K, idx.data(), O, bits, 1, base.data(), sc.data(), wr.data(),
+                                   ow.data());
+      CHECK(q.base.data == base);
+      CHECK(std::memcmp(q.scales.data(), sc.data(), N * 4) == 0 && std::memcmp(q.wreduced.data(), wr.data(), N * 4) == 0);
+      const auto q0 = Q::rtn_quantize_weights(w, o, bits);
+      CHECK(q0.scales != q.scales);  // clipping changes the scales
+      const auto wred = Q::compute_wreduced(q);
+      CHECK(std::memcmp(wred.data(), q.wreduced.data(), N * 4) == 0);
+      const auto dq = Q::dequantize_weights(q, o);
+      std::vector<float> want(N * K);
+      qo_dequantize_weights(q.base.data.data(), N, K, idx.data(), O, bits, q.scales.data(),
+                            q.outlier_weights.data.data(), want.data());
+      CHECK(std::memcmp(dq.data.data(), want.data(), want.size() * 4) == 0);
+      const auto vals = Q::unpack_values(q.base);
+      std::vector<int8_t> wv(N * (K - O));
+      qo_unpack(q.base.data.data(), N, K - O, bits, wv.data());
+      CHECK(vals == wv);
+      if (bits == 4) CHECK(Q::unpack_int4(q.base) == wv);
+      else CHECK(throws<std::invalid_argument>([&] { Q::unpack_int4(q.base); }));
+    }
+    {
+      const auto [xb, xo] = Q::split_activations(x, o);
+      std::vector<float> wb(M * (K - O)), wo(M * O);
+      qo_split_activations(x.data.data(), M, K, o.permutation.data(), K - O, idx.data(), O, wb.data(), wo.data());
+      CHECK(xb.rows == M && xb.cols == K - O && xo.cols == O);
+      CHECK(std::memcmp(xb.data.data(), wb.data(), wb.size() * 4) == 0 && std::memcmp(xo.data.data(), wo.data(), wo.size() * 4) == 0);
+      CHECK(throws<std::invalid_argument>([&] { Q::split_activations(Q::FpMatrix(1, K + 1), o); }));
+    }
+    // StageTimes per stage: V3 reports K1 under quantize_ms and the fused GEMM under
+    // int_matmul_ms; V1 fills split / quantize / int_matmul / fp_matmul
+    {
+      Q::QuikLinearLayer L;
+      L.outliers = o;
+      L.weights = Q::rtn_quantize_weights(w, o, 4);
+      L.act_bits = 4;
+      Q::StageTimes t3, t1;
+      const auto y3 = Q::quik_matmul(L, x, Q::PipelineVariant::V3FusedEpilogue, &t3);
+      const auto y1 = Q::quik_matmul(L, x, Q::PipelineVariant::V1Unfused, &t1);
+      CHECK(t3.quantize_fused && t3.dequantize_fused && t3.quantize_ms > 0 && t3.int_matmul_ms > 0 &&
+            t3.split_ms == 0 && t3.fp_matmul_ms == 0);
+      CHECK(!t1.quantize_fused && t1.split_ms > 0 && t1.quantize_ms > 0 && t1.int_matmul_ms > 0 && t1.fp_matmul_ms > 0);
+      CHECK(std::memcmp(y3.data.data(), y1.data.data(), y3.data.size() * 4) == 0);  // V1 == V3 bit for bit
+    }
+    // forward_model(gated_mlp_ops) on the device vs the oracle's layers + the
+    // reference's elementwise ops (runtime.cpp:325-382)
+    {
+      const int64_t F = 64;
+      Q::FpMatrix wu(F, K), wg(F, K), wd(K, F);
+      for (float& v : wu.data) v = 0.05f * nd(rng);
+      for (float& v : wg.data) v = 0.05f * nd(rng);
+      for (float& v : wd.data) v = 0.5f * nd(rng);
+      std::vector<Q::QuikLinearLayer> layers(3);
+      layers[0].outliers = o;
+      layers[0].weights = Q::rtn_quantize_weights(wu, o, 4);
+      layers[1].outliers = o;
+      layers[1].weights = Q::rtn_quantize_weights(wg, o, 4);
+      const auto od = Q::OutlierSet::from_indices(F, {3, 17});
+      layers[2].outliers = od;
+      layers[2].weights = Q::rtn_quantize_weights(wd, od, 8);
+      layers[2].act_bits = 8;
+      const auto ops = Q::gated_mlp_ops();
+      const auto tr = Q::forward_model_trace(layers, ops, x);
+      CHECK(tr.size() == 6 && tr[5].rows == M && tr[5].cols == K);
+      // values 1 / 2 exactly the single-layer forwards; 3 / 4 the reference's silu / multiply
+      const auto u = Q::quik_matmul(layers[0], x), g = Q::quik_matmul(layers[1], x);
+      CHECK(std::memcmp(tr[1].data.data(), u.data.data(), u.data.size() * 4) == 0);
+      CHECK(std::memcmp(tr[2].data.data(), g.data.data(), g.data.size() * 4) == 0);
+      double e3 = 0, e4 = 0;
+      for (size_t i = 0; i < g.data.size(); ++i) {
+        const float e = g.data[i];
+        const float sil = e / (1.0f + std::exp(-e));
+        e3 = std::max(e3, std::fabs(double(tr[3].data[i]) - sil) / (std::fabs(sil) + 1e-30));
+        e4 = std::max(e4, std::fabs(double(tr[4].data[i]) - double(tr[3].data[i] * u.data[i])));
+      }
+      CHECK(e3 < 1e-6 && e4 == 0.0);
+      const auto y = Q::forward_model(layers, ops, x);
+      CHECK(std::memcmp(y.data.data(), tr[5].data.data(), y.data.size() * 4) == 0);
+      const std::vector<Q::BlockOp> bad = {{Q::BlockOp::Kind::Silu, 7, -1, -1}};
+      CHECK(throws<std::invalid_argument>([&] { Q::forward_model(layers, bad, x); }));
+    }
   }
   // validation (runtime.cpp:150-167)
   {

@@ -91,7 +91,7 @@ class _Base:
                                       _p(a[3]), _p(out))
         return out
 
-    def rtn_quantize_weights(self, w, idx, bits):
+    def rtn_quantize_weights(self, w, idx, bits, use_clipping=False):
         w = np.ascontiguousarray(w, np.float32)
         N, K = w.shape
         idx = np.ascontiguousarray(idx, np.int64)
@@ -100,11 +100,28 @@ class _Base:
         scales = np.zeros(max(N, 1), np.float32)
         wred = np.zeros(max(N, 1), np.float32)
         ow = np.zeros(max(N * idx.size, 1), np.float32)
-        st = self.f("rtn_quantize_weights")(_p(w), C.c_int64(N), C.c_int64(K), _p(idx), C.c_int64(idx.size), bits,
-                                            _p(base), _p(scales), _p(wred), _p(ow))
+        st = self.f("rtn_quantize_weights_clip")(_p(w), C.c_int64(N), C.c_int64(K), _p(idx), C.c_int64(idx.size), bits,
+                                                 int(use_clipping), _p(base), _p(scales), _p(wred), _p(ow))
         assert st == 0, st
         return dict(base=base[: N * row_bytes(kb, bits)], scales=scales[:N], wreduced=wred[:N],
                     outlier_weights=ow[: N * idx.size].reshape(N, idx.size))
+
+
+    def compute_wreduced(self, base, N, kb, bits, scales):
+        out = np.zeros(max(N, 1), np.float32)
+        self.f("compute_wreduced")(_p(np.ascontiguousarray(base, np.uint8)), C.c_int64(N), C.c_int64(kb), bits,
+                                   _p(np.ascontiguousarray(scales, np.float32)), _p(out))
+        return out[:N]
+
+    def dequantize_weights(self, base, N, K, idx, bits, scales, ow):
+        idx = np.ascontiguousarray(idx, np.int64)
+        out = np.zeros(max(N * K, 1), np.float32)
+        st = self.f("dequantize_weights")(_p(np.ascontiguousarray(base, np.uint8)), C.c_int64(N), C.c_int64(K), _p(idx),
+                                          C.c_int64(idx.size), bits, _p(np.ascontiguousarray(scales, np.float32)),
+                                          _p(np.ascontiguousarray(ow, np.float32).reshape(-1)
+                                             if np.asarray(ow).size else np.zeros(1, np.float32)), _p(out))
+        assert st == 0, st
+        return out[: N * K].reshape(N, K)
 
 
 class Oracle(_Base):

@@ -38,7 +38,7 @@ def test_abi_version_and_status_strings():
     from paper_2310_09259_b200 import _lib
 
     lib = _lib.load()
-    assert lib.quik_abi_version() == 2
+    assert lib.quik_abi_version() == 3
     assert lib.quik_status_string(3) == b"numerical error"
     assert lib.quik_linear_forward_launches(2) == 2
 

@@ -81,7 +81,10 @@ def device_layer(M, K, N, O, bits, sparse, seed, bias=True):
 
 
 def subset_layer(host, rows, K, O, bits, idx):
-    t = lambda v: v[rows].cpu().numpy()  # noqa: E731
+    import torch
+
+    ri = torch.as_tensor(rows, device=host["scales"].device)
+    t = lambda v: v[ri].cpu().numpy()  # noqa: E731
     return dict(in_features=K, out_features=rows.size, bits=bits, act_bits=bits,
                 base=t(host["base"]).reshape(-1), scales=t(host["scales"]), wreduced=t(host["wreduced"]),
                 outlier_weights=t(host["ow"]).reshape(rows.size, O) if O else np.zeros((rows.size, 0), np.float32),
@@ -101,7 +104,7 @@ def test_baseline_config_full_shape(name, M, K, N, O, bits, sparse):
     rng = np.random.default_rng(7)
     toks = np.unique(np.concatenate([rng.choice(M, min(M, 6), replace=False), [0, M - 1]]))
     rows = np.unique(np.concatenate([rng.choice(N, 256, replace=False), [0, N - 1], np.arange(N - 128, N)]))
-    L = subset_layer(host, torch.as_tensor(rows, device=x16.device), K, O, bits, idx)
+    L = subset_layer(host, rows, K, O, bits, idx)
     xs = x16[torch.as_tensor(toks, device=x16.device)].float().cpu().numpy()
     st, want = o.quik_matmul(L, xs, 2)
     assert st == 0

@@ -1284,3 +1284,180 @@ def test_weight_only_fuzz():
         dev = m.QuikLinear(to_layer(L))
         y = dev.weight_only(torch.from_numpy(x).cuda(), out_dtype=torch.float32).cpu().numpy()
         assert rel_frobenius(weight_only_f64(L, x), y) < 1e-6, (M, K, N, O, bits)
+
+
+# --------------------------------------------------------------------------- rest of the reference surface
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+def test_rtn_clipping_compute_wreduced_dequantize_weights_vs_reference(bits):
+    """rtn_quantize_weights(use_clipping) (clip_search, quantizer.cpp:266-290),
+    compute_wreduced (:373-382) and dequantize_weights (:384-403) on the device against
+    the reference's own sources, bit-exact."""
+    m = q()
+    r = ref()
+    rng = np.random.default_rng(900 + bits)
+    for (N, K, O) in [(33, 257, 7), (300, 4096, 128), (5, 40, 0)]:
+        w = rng.normal(0, 0.5, size=(N, K)).astype(np.float32)
+        w[0] = 0.0
+        w[1, ::5] *= 30.0
+        idx = np.sort(rng.choice(K, O, replace=False)).astype(np.int64)
+        os_ = m.OutlierSet.from_indices(K, idx)
+        want = r.rtn_quantize_weights(w, idx, bits, use_clipping=True)
+        got = m.rtn_quantize_weights(w, os_, bits, use_clipping=True)
+        np.testing.assert_array_equal(got.base.data, want["base"])
+        np.testing.assert_array_equal(got.scales.view(np.uint32), want["scales"].view(np.uint32))
+        np.testing.assert_array_equal(got.wreduced.view(np.uint32), want["wreduced"].view(np.uint32))
+        np.testing.assert_array_equal(m.compute_wreduced(got).view(np.uint32), want["wreduced"].view(np.uint32))
+        dq = m.dequantize_weights(got, os_)
+        np.testing.assert_array_equal(dq.view(np.uint32), r.dequantize_weights(
+            want["base"], N, K, idx, bits, want["scales"], want["outlier_weights"]).view(np.uint32))
+
+
+def test_split_and_unpack_match_reference():
+    """split_activations (runtime.cpp:169-186) and unpack_int4 / unpack_values
+    (packed.cpp:68-91) through the device kernels."""
+    m = q()
+    o = oracle()
+    rng = np.random.default_rng(905)
+    x = rng.normal(size=(9, 300)).astype(np.float32)
+    idx = np.sort(rng.choice(300, 20, replace=False))
+    os_ = m.OutlierSet.from_indices(300, idx)
+    xb, xo = m.split_activations(x, os_)
+    np.testing.assert_array_equal(xb, x[:, os_.permutation[:280]])
+    np.testing.assert_array_equal(xo, x[:, idx])
+    with pytest.raises(ValueError):
+        m.split_activations(x[:, :299], os_)
+    for bits, cols in [(4, 7), (4, 64), (8, 33)]:
+        v = rng.integers(-8 if bits == 4 else -128, 8 if bits == 4 else 128, size=(5, cols))
+        pk = m.pack_values(v, 5, cols, bits)
+        np.testing.assert_array_equal(m._unpack_device(pk), v.astype(np.int8))
+        np.testing.assert_array_equal(m._unpack_device(pk), o.unpack(pk.data, 5, cols, bits))
+        if bits == 4:
+            np.testing.assert_array_equal(m.unpack_int4(pk), v.astype(np.int8))
+        else:
+            with pytest.raises(ValueError):
+                m.unpack_int4(pk)
+
+
+def test_stage_times_per_stage():
+    """StageTimes (runtime.hpp:72-80): per-stage CUDA-event times with the reference's
+    fused-stage convention; the timed forward equals the untimed one."""
+    m = q()
+    rng = np.random.default_rng(907)
+    L, x, _ = make_layer(rng, 64, 1024, 768, 4, 32, heavy_cols=2)
+    layer = to_layer(L)
+    t3, t2, t1 = m.StageTimes(), m.StageTimes(), m.StageTimes()
+    y3 = m.quik_matmul(layer, x, m.PipelineVariant.V3FusedEpilogue, t3)
+    y2 = m.quik_matmul(layer, x, m.PipelineVariant.V2FusedQuant, t2)
+    y1 = m.quik_matmul(layer, x, m.PipelineVariant.V1Unfused, t1)
+    assert t3.quantize_fused and t3.dequantize_fused and t3.quantize_ms > 0 and t3.int_matmul_ms > 0
+    assert t3.split_ms == 0 and t3.fp_matmul_ms == 0 and t3.dequantize_ms == 0
+    assert t2.quantize_fused and t2.quantize_ms > 0 and t2.int_matmul_ms > 0 and t2.fp_matmul_ms > 0
+    assert not t1.quantize_fused and t1.split_ms > 0 and t1.quantize_ms > 0 and t1.int_matmul_ms > 0
+    for y in (y2, y1):
+        np.testing.assert_array_equal(y.view(np.uint32), y3.view(np.uint32))
+    np.testing.assert_array_equal(m.quik_matmul(layer, x).view(np.uint32), y3.view(np.uint32))
+
+
+def test_forward_model_gated_mlp_ops_vs_reference():
+    """forward_model(gated_mlp_ops) (runtime.cpp:325-382) with every value on the device
+    against the reference's forward_model: the up / gate values bit-exact at O = 0, the
+    block within the down layer's quantizer sensitivity."""
+    m = q()
+    r = ref()
+    rng = np.random.default_rng(909)
+    up, gate, down, x = _mlp_layers(rng, 24, 256, 128, 4, 8, 0, 8)
+    layers = [to_layer(up), to_layer(gate), to_layer(down)]
+    tr = m.forward_model_trace(layers, m.gated_mlp_ops(), x)
+    assert len(tr) == 6
+    st, want, want_h = r.gated_mlp(up, gate, down, x)
+    assert st == 0
+    for i, L in ((1, up), (2, gate)):
+        s2, w2 = r.quik_matmul(L, x, 2)
+        np.testing.assert_array_equal(tr[i].view(np.uint32), w2.view(np.uint32))
+    assert rel_frob(want_h, tr[4]) < 1e-6
+    assert rel_frob(want, tr[5]) < 1e-3
+    np.testing.assert_array_equal(m.forward_model(layers, m.gated_mlp_ops(), x), tr[5])
+    with pytest.raises(ValueError):
+        m.forward_model(layers, [m.BlockOp(m.BlockOp.Kind.Linear, 0, -1, 5)], x)
+    with pytest.raises(ValueError):
+        m.forward_model(layers, [], x)
+
+
+def test_forward_output_validation():
+    """outputs of a wrong dtype, shape or device are rejected before the C ABI."""
+    m = q()
+    import torch
+
+    rng = np.random.default_rng(911)
+    L, x, _ = make_layer(rng, 8, 256, 128, 4, 16, heavy_cols=1)
+    dev = m.QuikLinear(to_layer(L))
+    xt = torch.from_numpy(x).cuda().half()
+    for bad in (torch.empty((8, 128), dtype=torch.bfloat16, device="cuda"),
+                torch.empty((8, 128), dtype=torch.int32, device="cuda"),
+                torch.empty((7, 128), dtype=torch.float16, device="cuda"),
+                torch.empty((8, 127), dtype=torch.float16, device="cuda"),
+                torch.empty((8, 128), dtype=torch.float16)):
+        with pytest.raises(ValueError):
+            dev(xt, out=bad)
+        with pytest.raises(ValueError):
+            dev.weight_only(xt, out=bad)
+    with pytest.raises(ValueError):
+        dev(xt, out_dtype=torch.bfloat16)
+    codes, scale, zero, xo = dev.quantize_gemm_layout(xt)
+    kp, op = codes.shape[1], xo.shape[1]
+    assert kp % 128 == 0 and kp >= 240 and op == 64
+
+
+def test_streams_share_context_scratch_safely():
+    """forwards through one context on two streams are ordered (the scratch is
+    shared); every result equals the single-stream forward."""
+    m = q()
+    import torch
+
+    rng = np.random.default_rng(913)
+    L, x, _ = make_layer(rng, 512, 2048, 4096, 4, 64, heavy_cols=2)
+    dev = m.QuikLinear(to_layer(L))
+    xs = [torch.from_numpy(x).cuda().half(), torch.from_numpy(x[::-1].copy()).cuda().half()]
+    want = [dev(v).clone() for v in xs]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    outs = []
+    for i in range(8):
+        s = s1 if i % 2 == 0 else s2
+        with torch.cuda.stream(s):
+            outs.append(dev(xs[i % 2]))
+    torch.cuda.synchronize()
+    for i, o_ in enumerate(outs):
+        assert torch.equal(o_, want[i % 2]), i
+
+
+def test_reserve_then_capture_and_numerics_flag():
+    """quik_ctx_reserve sizes the scratch so a larger-M forward can be captured into a
+    CUDA graph (scratch cannot grow under capture: clear error otherwise); the
+    non-finite flag is reported by check_numerics and cleared."""
+    m = q()
+    import torch
+
+    rng = np.random.default_rng(915)
+    L, x, _ = make_layer(rng, 300, 512, 256, 4, 16, heavy_cols=1)
+    dev = m.QuikLinear(to_layer(L))
+    xt = torch.from_numpy(x).cuda().half()
+    dev.reserve(300)
+    want = dev(xt).clone()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    out = torch.empty_like(want)
+    with torch.cuda.graph(g):
+        dev(xt, out=out)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, want)
+    bad = xt.clone()
+    bad[3, 7] = float("nan")
+    dev(bad)
+    with pytest.raises(m.NumericalError):
+        dev.check_numerics()
+    dev(xt)
+    dev.check_numerics()  # cleared by the previous check
