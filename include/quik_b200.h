@@ -318,25 +318,15 @@ quik_status quik_elementwise(quik_ctx_t ctx, int op, const float* a, const float
                              void* stream);
 
 /* Tuning/debug knob (process-wide): force the GEMM tile, cta_group in {1, 2} and
- * token block_n in {32, 64, 128} (1-CTA) or {128, 192, 256} (CTA pair; 2:4 sparse
- * layers use 192 where 256 is asked, dense ones 256 for 192); (0, 0) restores the
- * heuristic. */
+ * token block_n in {32, 64, 128} (1-CTA) or {128, 192, 256} (CTA pair; 2:4 sparse and
+ * 4-bit (INT4-weight) layers use 192 where 256 is asked, 8-bit dense ones 256 for 192);
+ * (0, 0) restores the heuristic. */
 quik_status quik_set_gemm_tile(int cta_group, int block_n);
 
-/* Tuning knob (process-wide): 1 runs CTA-pair GEMM tiles in 4-CTA clusters whose two
- * pairs share (TMA-multicast) the activation tiles; 0 (default) plain CTA pairs. */
+/* Tuning knob (process-wide): 1 runs the CTA-pair GEMM tiles of 8-bit dense layers in
+ * 4-CTA clusters whose two pairs share (TMA-multicast) the activation tiles; 0 (default)
+ * plain CTA pairs. */
 quik_status quik_set_gemm_multicast(int on);
-
-/* Tuning knob (process-wide): 1 streams INT4 weights from HBM and widens them to INT8
- * in shared memory for the 1-CTA (M <= 128) GEMM tiles of 4-bit layers; 0 (default)
- * uses the INT8 copy. */
-quik_status quik_set_gemm_w4(int on);
-
-/* Tuning knob (process-wide): on (default off) V3 forwards with M <= 64 tokens run the
- * split-K weight-streaming GEMM (int32 workspace) + the fused dequant/outlier
- * epilogue (bit-identical results); int4 (default 1) streams the INT4 weights of
- * 4-bit layers. */
-quik_status quik_set_stream_gemm(int on, int int4);
 
 /* Tuning: dense layers at M <= 32 run the decode kernel (stream4.cu: split-K over all
  * SMs on INT4 weights widened into TMEM (4-bit) or INT8 tiles (8-bit), the fused

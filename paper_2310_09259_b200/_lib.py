@@ -31,7 +31,7 @@ EXPORTED_SYMBOLS = (
     "quik_linear_forward_launches", "quik_linear_forward_ex", "quik_rtn_quantize_weights",
     "quik_set_gemm_tile", "quik_set_probe_mode", "quik_linear_forward_host",
     "quik_quantize_activations_gemm", "quik_layer_is_sparse", "quik_set_gemm_multicast",
-    "quik_set_gemm_w4", "quik_set_stream_gemm", "quik_bundle_open", "quik_bundle_weights",
+    "quik_bundle_open", "quik_bundle_weights",
     "quik_bundle_tensor", "quik_bundle_close", "quik_layer_load_bundle", "quik_layer_create_gated",
     "quik_linear_forward_weight_only", "quik_linear_forward_sharded", "quik_set_int4_decode",
     "quik_gptq_quantize", "quik_hessian_accumulate", "quik_ctx_clear_error", "quik_ctx_reserve", "quik_layer_layout",
@@ -120,8 +120,6 @@ def load() -> C.CDLL:
             "quik_quantize_activations_gemm": (i32, [vp, vp, vp, i32, i64, vp, vp, vp, vp, vp]),
             "quik_layer_is_sparse": (i32, [vp]),
             "quik_set_gemm_multicast": (i32, [i32]),
-            "quik_set_gemm_w4": (i32, [i32]),
-            "quik_set_stream_gemm": (i32, [i32, i32]),
             "quik_bundle_open": (i32, [C.c_char_p, C.POINTER(vp)]),
             "quik_bundle_weights": (i32, [vp, C.POINTER(WeightsDesc)]),
             "quik_bundle_tensor": (i32, [vp, C.c_char_p, C.POINTER(vp), C.POINTER(i32), C.POINTER(i64),

@@ -26,7 +26,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
                      "-I" + str(ROOT / "include")]
-SOURCES = ["gemm.cu", "stream.cu", "stream4.cu", "wo.cu", "gptq.cu", "quantize.cu", "weights.cu", "capi.cu", "bundle.cpp"]
+SOURCES = ["gemm.cu", "stream4.cu", "wo.cu", "gptq.cu", "quantize.cu", "weights.cu", "capi.cu", "bundle.cpp"]
 
 
 def _run(cmd: list[str], cwd: Path | None = None) -> None:

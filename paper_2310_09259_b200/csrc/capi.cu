@@ -192,14 +192,15 @@ struct quik_layer_s {
   int device = 0;
   int64_t in_features = 0, out_features = 0, n_outlier = 0, kb = 0, kpad = 0, opad = 0;
   int bits = 4;
-  int8_t* w8 = nullptr;      // [out][kpad] (null when sparse)
+  int8_t* w8 = nullptr;      // [out][kpad] INT8 weights of 8-bit dense layers (null otherwise)
   int sparse = 0;            // 2:4 sparse GEMM operands below are in use
   int gated = 0;             // gated MLP layer: rows interleave up / gate (32-row blocks), output width N / 2
   int8_t* w_sp = nullptr;    // [out][kpad / 2]
-  uint8_t* w4 = nullptr;     // [out][kpad / 2] INT4 weights (4-bit layers), device nibble layout
+  uint8_t* w4 = nullptr;     // [out][kpad / 2] INT4 weights of 4-bit dense layers, device nibble layout
   uint8_t* meta = nullptr;   // metadata planes (kernels.h GemmArgs)
   __half* wo16 = nullptr;    // [out][opad]
-  __half* wo16_lo = nullptr; // [out][opad] f16(w_o - f16(w_o)): weight-only forward (f32-accurate outliers)
+  __half* wo16_lo = nullptr; // [out][opad] f16(w_o - f16(w_o)): weight-only forward only, uploaded on its first call
+  std::vector<__half> wo16_lo_host;  // host copy of wo16_lo until then (keeps it out of HBM for quik-mode layers)
   float* w_scale = nullptr;  // [out]
   float* wreduced = nullptr; // [out]
   float* bias = nullptr;     // [out] or null
@@ -341,17 +342,6 @@ quik_status quik_set_gemm_tile(int cta_group, int block_n) {
                   (cta_group == 2 && (block_n == 128 || block_n == 192 || block_n == 256));
   if (!ok) return fail(QUIK_ERR_INVALID_ARGUMENT, "unsupported GEMM tile configuration");
   quikb200::gemm_tile_override = (cta_group << 16) | block_n;
-  return QUIK_OK;
-}
-
-quik_status quik_set_gemm_w4(int on) {
-  quikb200::gemm_w4 = on ? 1 : 0;
-  return QUIK_OK;
-}
-
-quik_status quik_set_stream_gemm(int on, int int4) {
-  quikb200::gemm_stream = on ? 1 : 0;
-  quikb200::gemm_w4_stream = int4 ? 1 : 0;
   return QUIK_OK;
 }
 
@@ -551,12 +541,21 @@ quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* d, quik_l
         QK_CUDA(cudaMemcpy(L->bias, d->bias + rb, rows * 4, cudaMemcpyDefault));
       }
       if (kb) {
+        // One device copy of the base weights: INT4 (device nibble layout, half the bytes
+        // of INT8) for 4-bit layers, INT8 for 8-bit layers, the 2:4-compressed codes for
+        // sparse layers. Staging buffers are released at the end of the call.
         const int64_t rbytes = packed_row_bytes(kb, d->bits);
-        QK_CUDA(cudaMalloc(&L->w8, static_cast<size_t>(rows * L->kpad)));
         void* tmp = ctx->wtmp.ensure(static_cast<size_t>(rows * rbytes));
         QK_CUDA(cudaMemcpy(tmp, d->base + rb * rbytes, static_cast<size_t>(rows * rbytes), cudaMemcpyDefault));
-        check_launch(launch_unpack_to_gemm(static_cast<const uint8_t*>(tmp), rows, kb, d->bits, L->w8, L->kpad, st),
-                     "weight unpack");
+        if (d->bits == 4 && !d->sparsity) {
+          QK_CUDA(cudaMalloc(&L->w4, static_cast<size_t>(rows * L->kpad / 2)));
+          check_launch(launch_pack_w4_abi(static_cast<const uint8_t*>(tmp), rows, kb, L->w4, L->kpad, st),
+                       "int4 weight pack");
+        } else {
+          QK_CUDA(cudaMalloc(&L->w8, static_cast<size_t>(rows * L->kpad)));
+          check_launch(launch_unpack_to_gemm(static_cast<const uint8_t*>(tmp), rows, kb, d->bits, L->w8, L->kpad, st),
+                       "weight unpack");
+        }
         if (d->sparsity) {
           // 2:4 compression (tcgen05.mma.sp operands); stays dense if not compressible
           const int64_t npad = round_up(rows, kBlockM);
@@ -575,6 +574,13 @@ quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* d, quik_l
             cudaFree(L->meta);
             L->w_sp = nullptr;
             L->meta = nullptr;
+            if (d->bits == 4) {  // not 2:4: a dense 4-bit layer after all -> INT4 weights
+              QK_CUDA(cudaMalloc(&L->w4, static_cast<size_t>(rows * L->kpad / 2)));
+              check_launch(launch_pack_w4(L->w8, rows, L->kpad, L->w4, st), "int4 weight pack");
+              QK_CUDA(cudaStreamSynchronize(st));
+              QK_CUDA(cudaFree(L->w8));
+              L->w8 = nullptr;
+            }
           } else {
             L->sparse = 1;
             QK_CUDA(cudaFree(L->w8));
@@ -589,12 +595,22 @@ quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* d, quik_l
                            cudaMemcpyDefault));
         check_launch(launch_f32_to_f16_padded(static_cast<const float*>(tmp), rows, d->n_outlier, L->wo16, L->opad, st),
                      "outlier weight convert");
-        QK_CUDA(cudaMalloc(&L->wo16_lo, static_cast<size_t>(rows * L->opad * 2)));
-        check_launch(launch_f16_lo_padded(static_cast<const float*>(tmp), rows, d->n_outlier, L->wo16_lo, L->opad, st),
+        // the weight-only forward's low f16 plane, computed here from the f32 weights and
+        // parked in host memory (the quik-mode hot path never reads it)
+        __half* lo = static_cast<__half*>(ctx->aux.ensure(static_cast<size_t>(rows * L->opad * 2)));
+        check_launch(launch_f16_lo_padded(static_cast<const float*>(tmp), rows, d->n_outlier, lo, L->opad, st),
                      "outlier weight convert (lo)");
+        L->wo16_lo_host.resize(static_cast<size_t>(rows * L->opad));
+        QK_CUDA(cudaMemcpyAsync(L->wo16_lo_host.data(), lo, static_cast<size_t>(rows * L->opad * 2),
+                                cudaMemcpyDeviceToHost, st));
       }
     }
     QK_CUDA(cudaStreamSynchronize(st));
+    // the layer's device copy is complete: give the staging memory back (a cfg3 layer
+    // would otherwise keep its 114 MB ABI copy + 29 MB f32 outliers in the context)
+    ctx->wtmp.release();
+    ctx->fp.release();
+    ctx->aux.release();
     *out = hold.release();
     return QUIK_OK;
   });
@@ -845,21 +861,6 @@ quik_status quik_dequantize_epilogue(quik_ctx_t ctx, const int32_t* acc, int64_t
 }  // extern "C"
 
 namespace {
-// INT4 weight copy for the opt-in W4 / INT4-stream GEMM variants, made on first use
-// (not at layer create: it would cost 50 % of the int8 weights' HBM for every 4-bit
-// layer). Not during stream capture (cudaMalloc): those forwards read int8 weights.
-void ensure_w4(quik_layer_s* L, cudaStream_t st, bool needed = false) {
-  if (L->w4 || L->bits != 4 || !L->w8 || L->sparse) return;
-  if (!needed && !quikb200::gemm_w4 && !(quikb200::gemm_stream && quikb200::gemm_w4_stream)) return;
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  QK_CUDA(cudaStreamIsCapturing(st, &cs));
-  if (cs != cudaStreamCaptureStatusNone) return;
-  const int64_t rows = L->out_features;  // all rows (gated: up + gate)
-  QK_CUDA(cudaMalloc(&L->w4, static_cast<size_t>(rows * L->kpad / 2)));
-  check_launch(launch_pack_w4(L->w8, rows, L->kpad, L->w4, st), "int4 weight pack");
-}
-
-// The forward on device buffers (argument checks done by the caller).
 // Events recorded at the stage boundaries of one forward (StageTimes, runtime.hpp:72-80);
 // any may be null.
 struct StageMarks {
@@ -874,14 +875,11 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
                          void* const* peers = nullptr, int n_peer = 0) {
   if (M == 0 || L->out_features == 0) return QUIK_OK;
   const int64_t N = L->out_features;
-  // Decode regime (M <= 32, 4-bit layers): the INT4 split-K stream kernel (stream4.cu)
-  // reads half the weight bytes of the fused kernel's INT8 tiles and spreads small
-  // layers over every SM; default on (QUIK_STREAM4=0 disables). Needs the INT4 weight
-  // copy, made on the first such forward outside stream capture.
-  const bool small = variant == QUIK_V3_FUSED_EPILOGUE && M <= 64 && L->kpad && !L->sparse && !g_probe_mode;
-  const bool auto4 = small && quikb200::gemm_stream4_auto && M <= 32;
-  ensure_w4(L, st, auto4 && L->bits == 4);
-  bool decode = auto4 && (L->bits == 4 ? L->w4 != nullptr : L->w8 != nullptr) && !quikb200::gemm_stream;
+  // Decode regime (M <= 32, dense layers): the split-K stream kernel (stream4.cu)
+  // spreads small layers over every SM (4-bit: INT4 weights widened into TMEM; 8-bit:
+  // INT8 tiles); default on (QUIK_STREAM4=0 disables).
+  bool decode = variant == QUIK_V3_FUSED_EPILOGUE && M <= 32 && L->kpad && !L->sparse && !g_probe_mode &&
+                quikb200::gemm_stream4_auto;
   if (decode) {
     // under stream capture no workspace may be (re)allocated: use the fused path when
     // the decode workspace / counters are not sized yet (a warm-up call sizes them)
@@ -922,35 +920,6 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
     a.n_peer = n_peer;
     const char* msg = nullptr;
     check_launch(launch_stream4(a, ctx->num_sms, st, &msg), "int4 stream kernel", msg);
-    return QUIK_OK;
-  }
-  if (small && quikb200::gemm_stream) {
-    // weight-streaming regime: K1 -> split-K stream GEMM into the zeroed int32
-    // workspace -> the fused kernel's AccInit mode (dequant + outlier MMAs + store,
-    // clears the workspace); same arithmetic as the fused V3 kernel
-    run_k1(ctx, L, x, xdt, M, st);
-    mark(sm.after_quant, st);
-    int32_t* ws = ctx->ensure_ws(static_cast<size_t>(M * N * 4), st);
-    StreamArgs sa{};
-    sa.w8 = L->w8;
-    sa.w4 = (auto4 || quikb200::gemm_w4_stream) ? L->w4 : nullptr;
-    sa.x = static_cast<const int8_t*>(ctx->q8.p);
-    sa.kpad = L->kpad;
-    sa.M = M;
-    sa.N = N;
-    sa.acc = ws;
-    const char* msg = nullptr;
-    check_launch(launch_stream_gemm(sa, ctx->num_sms, st, &msg), "stream gemm kernel", msg);
-    GemmArgs go = gemm_args(ctx, L, M);
-    go.acc_in = ws;
-    go.acc_clear = ws;
-    go.ld_acc = N;
-    go.out = y;
-    go.ldo = ldy;
-    go.mode = ydt == QUIK_F16 ? kModeAccInitF16 : kModeAccInitF32;
-    go.peer_out = peers;
-    go.n_peer = n_peer;
-    run_gemm(ctx, go, st);
     return QUIK_OK;
   }
   if (variant == QUIK_V3_FUSED_EPILOGUE) {
@@ -1144,7 +1113,14 @@ quik_status quik_linear_forward_weight_only(quik_ctx_t ctx, quik_layer_t L, cons
     return on_stream(ctx, as_stream(stream), [&]() -> quik_status {
       cudaStream_t st = as_stream(stream);
       if (M == 0 || L->out_features == 0) return QUIK_OK;
-      ensure_w4(L, st, true);  // INT4 weights are what the decode regime streams
+      if (L->n_outlier && !L->wo16_lo) {  // first weight-only call: upload the low outlier plane
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        QK_CUDA(cudaStreamIsCapturing(st, &cs));
+        if (cs != cudaStreamCaptureStatusNone)
+          return fail(QUIK_ERR_INVALID_ARGUMENT, "weight_only_forward: run one call before capturing it in a graph");
+        QK_CUDA(cudaMalloc(&L->wo16_lo, L->wo16_lo_host.size() * 2));
+        QK_CUDA(cudaMemcpy(L->wo16_lo, L->wo16_lo_host.data(), L->wo16_lo_host.size() * 2, cudaMemcpyHostToDevice));
+      }
       WoArgs a{};
       a.x = x;
       a.x_is_f32 = xdt == QUIK_F32;
@@ -1309,7 +1285,6 @@ quik_status quik_ctx_reserve(quik_ctx_t ctx, quik_layer_t L, int64_t M) {
     if (M <= 32 && L->kpad && !L->sparse) {  // decode kernel workspace + counters (zeroed)
       ctx->ensure_ws(static_cast<size_t>(M * N * 4), nullptr);
       ctx->ensure_s4_counters(quikb200::stream4_counter_count(N), nullptr);
-      ensure_w4(L, nullptr, L->bits == 4);
     }
     QK_CUDA(cudaDeviceSynchronize());
     return QUIK_OK;

@@ -21,11 +21,22 @@
 // so that the epilogue's two passes over tile i-1 (convert int32 -> f32 init in
 // place, then drain the finished f32 tile) overlap the integer MMAs of tile i.
 //
-// Warp roles (384 threads, 1 CTA per SM, persistent over tiles):
+// Warp roles (384 threads, 1 CTA per SM, persistent over tiles; 512 with W4):
 //   warp 0      TMA producer (one lane)
 //   warp 1      MMA issuer  (one lane, leader CTA only)
 //   warp 2      TMEM allocator
 //   warps 4..11 epilogue (TMEM lane quadrant = warp % 4, column half = (warp - 4) / 4)
+//   warps 12..15 W4 only: INT4 -> INT8 widening of the weight tiles into TMEM
+//
+// W4 (4-bit layers; the default for them): the weights stay INT4 in HBM (half the
+// bytes of an INT8 copy; packed.hpp:11-16 widened once per use instead of once per
+// call, packed.cpp:110-111). Each CTA TMA-loads its 128 x 64-byte INT4 tile (64-byte
+// swizzle) into the stage with its own barrier; four widening warps (one per TMEM lane
+// quadrant, thread = weight row) sign-extend the nibbles and tcgen05.st the int8 row
+// into a TMEM A-operand ring (lane = row, column j = k 4j..4j+3); the MMA warp issues
+// tcgen05.mma kind::i8 with A from TMEM and the activation codes from shared memory.
+// The widened operand never touches shared memory, so per stage the SM's shared
+// memory moves 8 KB of INT4 weights (TMA in + one read) instead of 16 KB twice.
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
@@ -43,6 +54,9 @@ namespace {
 constexpr int kEpiWarp0 = 4;
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
+constexpr int kWidenWarp0 = kEpiWarp0 + kEpiWarps;  // W4: warps 12..15 widen INT4 -> TMEM
+constexpr int kThreadsW4 = kThreads + 4 * 32;
+constexpr int kAStages = 4;                         // W4: TMEM A-operand ring (32 columns each)
 constexpr int kChunk = 32;                                     // tokens per epilogue step
 constexpr int kStoreBufBytes = kChunk * 32 * 2;                // [32 tokens][32 features] f16
 constexpr int kStagingBytes = kEpiWarps * 2 * kStoreBufBytes;  // double-buffered per warp
@@ -55,10 +69,9 @@ constexpr int kStagingBytes = kEpiWarps * 2 * kStoreBufBytes;  // double-buffere
 constexpr int kMetaSlots = 4;     // TMEM metadata ring (8 columns per stage)
 constexpr int kMetaTileBytes = 4096;
 
-// W4 (INT4 weights in HBM): the producer TMA-loads the packed 4-bit weight tile
-// (128 rows x 64 B = 128 K, device nibble layout, see capi.cu) into a staging slot of
-// the stage; two transform warps widen it to the int8 128-byte-swizzled A tile in
-// shared memory and signal `ready` to the MMA warp. Halves the weight bytes from HBM.
+// W4: the packed 4-bit weight tile of one k-block (128 rows x 64 B = 128 K, device
+// nibble layout: byte i of 16-byte chunk c holds k = 32c + i (low nibble) and
+// k = 32c + 16 + i (high nibble), two's complement), in the A region of the stage.
 constexpr int kA4Bytes = kBlockM * kKBlockBytes / 2;  // 8 KB
 
 template <int CG, int BN, bool SP = false, bool W4 = false>
@@ -68,25 +81,27 @@ struct Cfg {
   static constexpr int kBAtomBytes = kBRows * kKBlockBytes;
   static constexpr int kBBytes = kBAtomBytes * (SP ? 2 : 1);
   static constexpr int kMetaBytes = SP ? kMetaTileBytes : 0;
-  static constexpr int kA4Off = kABytes + kBBytes + kMetaBytes;  // W4 staging slot
-  static constexpr int kStageBytes = kABytes + kBBytes + kMetaBytes + (W4 ? kA4Bytes : 0);
+  static constexpr int kStageBytes = kABytes + kBBytes + kMetaBytes;  // W4: INT4 tile in the A region
   static constexpr int kBudget = 227 * 1024 - 1024 - kStagingBytes - 512;
   static constexpr int kStages = (kBudget / kStageBytes) > 8 ? 8 : (kBudget / kStageBytes);
   static constexpr int kAccCols = 2 * BN;                 // two accumulator buffers
   static constexpr int kMetaCol = kAccCols;               // SP: metadata ring after the accumulators
-  static constexpr int kTmemCols = SP ? 512 : (2 * BN < 32 ? 32 : 2 * BN);
-  static_assert(!SP || kAccCols + 8 * kMetaSlots <= 512, "TMEM: accumulators + metadata ring");
-  static constexpr int kBarBytes = (3 * kStages + 8) * 8 + 16;
+  static constexpr int kACol = kAccCols;                  // W4: A-operand ring after the accumulators
+  static constexpr int kTmemNeed = kAccCols + (SP ? 8 * kMetaSlots : 0) + (W4 ? 32 * kAStages : 0);
+  static constexpr int kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128
+                                 : kTmemNeed <= 256 ? 256 : 512;
+  static_assert(kTmemNeed <= 512, "TMEM: accumulators + metadata / A-operand ring");
+  static constexpr int kBarBytes = (4 * kStages + 8 + 2 * kAStages) * 8 + 16;
   static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kStagingBytes + kBarBytes;
   static constexpr int kTileRows = kBlockM * CG;          // weight rows per (cluster) tile
-  static constexpr int kIntStageBytes = (W4 ? kA4Bytes : kABytes) + kBBytes + kMetaBytes;  // expect-tx per CTA
+  static constexpr int kIntStageBytes = kABytes + kBBytes + kMetaBytes;  // expect-tx per CTA (not W4)
   static constexpr int kOutStageBytes = kABytes + kBAtomBytes;
 };
 
 struct KParams {
   CUtensorMap tm_w;   // int8 [N][kpad] (SP: compressed [N][kpad / 2]), box {128 B, 128 rows}
   CUtensorMap tm_e;   // SP: metadata [2 * n_kb * n_pad rows][16 B], box {16 B, 128 rows}
-  CUtensorMap tm_w4;  // W4: packed int4 weights [N][kpad / 2], box {64 B, 128 rows}, no swizzle
+  CUtensorMap tm_w4;  // W4: packed int4 weights [N][kpad / 2], box {64 B, 128 rows}, 64-byte swizzle
   CUtensorMap tm_x;   // int8 [M][kpad], box {128 B, BN/CG rows}
   CUtensorMap tm_wo;  // f16 [N][opad], box {64, 128}
   CUtensorMap tm_xo;  // f16 [M][opad], box {64, BN/CG}
@@ -144,7 +159,7 @@ __device__ __forceinline__ void arrive_leader(uint64_t* bar, uint32_t leader_ran
 // refilled only after both pairs' MMAs released it (empty barriers count 2, the
 // MMA commits multicast to all 4 CTAs). Halves the L2->SM traffic of B.
 template <int CG, int BN, int MODE, bool SP, bool MC, bool W4>
-__global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_constant__ KParams p) {
+__global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kernel(const __grid_constant__ KParams p) {
   using C = Cfg<CG, BN, SP, W4>;
   static_assert(!MC || CG == 2, "multicast clusters pair CTA pairs");
   static_assert(!(W4 && (SP || MC)), "W4 is a dense-weight variant");
@@ -165,8 +180,10 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
   uint64_t* tconv = tint + 2;           // [2] init written into TMEM          (epilogue -> MMA)
   uint64_t* tfin = tconv + 2;           // [2] outlier MMAs done, tile final   (MMA -> epilogue)
   uint64_t* tempty = tfin + 2;          // [2] accumulator buffer drained      (epilogue -> MMA)
-  uint64_t* ready = tempty + 2;         // [kStages] W4: int8 A tile widened     (transform -> MMA)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ready + C::kStages);
+  uint64_t* full4 = tempty + 2;         // [kStages] W4: this CTA's INT4 tile landed (TMA -> widen)
+  uint64_t* ready = full4 + C::kStages; // [kAStages] W4: TMEM A slot widened, both CTAs (widen -> MMA)
+  uint64_t* aempty = ready + kAStages;  // [kAStages] W4: TMEM A slot consumed (MMA -> widen)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + kAStages);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -198,8 +215,10 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
       mbar_init(&tfin[i], 1);
       mbar_init(&tempty[i], kEpiWarps * CG);
     }
-    if (W4)
-      for (int i = 0; i < C::kStages; ++i) mbar_init(&ready[i], 2);
+    if (W4) {
+      for (int i = 0; i < C::kStages; ++i) mbar_init(&full4[i], 1);
+      for (int i = 0; i < kAStages; ++i) { mbar_init(&ready[i], 4 * CG); mbar_init(&aempty[i], 1); }
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<CG>(tmem_slot, C::kTmemCols);
@@ -212,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
   // producer first issues the weight loads of its first ring stages (weights do not
   // depend on K1) and waits before the token tiles; the epilogue waits before reading
   // the per-token scales; the MMA warp only reads what the producer staged.
-  constexpr bool kEarlyW = !W4 && !MC;
+  constexpr bool kEarlyW = !MC;
   if constexpr (!kEarlyW) asm volatile("griddepcontrol.wait;" ::: "memory");
 
   const int tiles_m = (p.M + BN - 1) / BN;
@@ -262,10 +281,13 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
       // integer block kb: dense = load(); SP = compressed A + two B atoms + metadata tile
       auto load_int = [&](int kb, int wrow, int trow) {
         if constexpr (W4) {
+          // INT4 tile -> this CTA's stage, on this CTA's full4 barrier (the widening warps
+          // of each CTA wait for their own tile); activation tile -> the pair's full barrier
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::kStageBytes;
-          if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::kIntStageBytes);
-          tma(sa + C::kA4Off, &p.tm_w4, kb * (kKBlockBytes / 2), wrow, pol_w);
+          if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::kBBytes);
+          mbar_arrive_expect_tx(&full4[stage], kA4Bytes);
+          tma_load_2d(sa, &p.tm_w4, kb * (kKBlockBytes / 2), wrow, &full4[stage], pol_w);
           tma_b(sa + C::kABytes, &p.tm_x, kb * kKBlockBytes, trow, pol_x);
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         } else if constexpr (!SP) {
@@ -299,6 +321,12 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
           for (int kb = 0; kb < pre; ++kb) {  // fresh ring stages 0 .. pre-1
             stage = kb;
             uint8_t* sa = smem + kb * C::kStageBytes;
+            if constexpr (W4) {
+              if (leader) mbar_arrive_expect_tx(&full[kb], CG * C::kBBytes);
+              mbar_arrive_expect_tx(&full4[kb], kA4Bytes);
+              tma_load_2d(sa, &p.tm_w4, kb * (kKBlockBytes / 2), wr0, &full4[kb], pol_w);
+              continue;
+            }
             if (leader) mbar_arrive_expect_tx(&full[kb], CG * (SP ? C::kIntStageBytes : C::kOutStageBytes));
             tma(sa, &p.tm_w, kb * kKBlockBytes, wr0, pol_w);
             if constexpr (SP) {  // 2:4 metadata of the stage (a weight-side tensor too)
@@ -353,14 +381,17 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
       int stage = 0;
       uint32_t phase = 0;
       long long full_wait = 0;
+      int aslot = 0;  // W4: TMEM A-operand ring position
+      uint32_t aphase = 0;
       auto next_stage = [&](uint64_t& adesc, uint64_t& bdesc, bool widened = false) {
-        uint64_t* bar = widened ? &ready[stage] : &full[stage];
         if (p.trace) {
           const long long t0 = gtime();
-          mbar_wait(bar, phase);
+          mbar_wait(&full[stage], phase);
+          if (widened) mbar_wait(&ready[aslot], aphase);
           full_wait += gtime() - t0;
         } else {
-          mbar_wait(bar, phase);
+          mbar_wait(&full[stage], phase);
+          if (widened) mbar_wait(&ready[aslot], aphase);
         }
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
@@ -376,7 +407,15 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
         for (int kb = k0; kb < k1; ++kb) {
           uint64_t ad, bd;
           next_stage(ad, bd, W4);
-          if constexpr (!SP) {
+          if constexpr (W4) {
+            // A from the TMEM ring slot (both CTAs widened their rows into it)
+            const uint32_t a_tm = tmem_base + C::kACol + aslot * 32;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)  // 4 x K=32 int8 = 32 TMEM columns
+              mma_i8_ts<CG>(d, a_tm + 8 * k, bd + 2 * k, id_i8, (kb | k) != 0);
+            mma_commit<CG>(&aempty[aslot], static_cast<uint16_t>(3));  // slot free in both CTAs
+            if (++aslot == kAStages) { aslot = 0; aphase ^= 1; }
+          } else if constexpr (!SP) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)  // 4 x K=32 int8 = 128 bytes
               mma_i8<CG>(d, ad + 2 * k, bd + 2 * k, id_i8, (kb | k) != 0);
@@ -430,68 +469,59 @@ __global__ void __launch_bounds__(kThreads, 1) quik_gemm_kernel(const __grid_con
       }
       if (two_phase && it > 0) out_blocks(it - 1);
     }
-  } else if (W4 && (warp == 2 || warp == 3)) {
-    // INT4 -> INT8 widening of the weight tiles, stage by stage in the producer's order
-    // (int blocks [0, h_a) | outlier blocks of the previous tile | [h_a, kb_int)).
-    // Input slot: [128 rows][64 B]; byte i of 16-byte chunk c holds k = 32c + i in its
-    // low nibble and k = 32c + 16 + i in its high nibble (signed 4-bit). Output: the
-    // int8 A tile, row r, 16-byte chunk j at physical chunk j ^ (r & 7) (SWIZZLE_128B).
-    const int t64 = (warp - 2) * 32 + lane;
+  } else if (W4 && warp >= kWidenWarp0) {
+    // INT4 -> INT8 widening into the TMEM A ring, k-block by k-block in the producer's
+    // order (int blocks [0, h_a) | outlier blocks of the previous tile | [h_a, kb_int)).
+    // Thread = weight row r of this CTA (TMEM lane quadrant q = warp % 4). The INT4 tile
+    // lands 64-byte swizzled: 16-byte chunk c of row r sits at chunk c ^ ((r >> 1) & 3),
+    // so the 8 rows of a quarter warp read 8 distinct bank groups. Byte i of chunk c
+    // holds k = 32c + i (low nibble) and 32c + 16 + i (high nibble): word w of the chunk
+    // widens to TMEM columns 8c + w (low) and 8c + 4 + w (high).
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
     int stage = 0;
-    uint32_t phase = 0;
-    // outlier stages are not widened, but `ready` must still complete one phase per
-    // use of the stage so its parity stays in step with the ring (the MMA warp waits on
-    // it with the ring phase). Waiting for the stage's data first keeps the transform
-    // behind the producer, i.e. at most one ring wrap ahead of the MMA warp.
-    auto skip = [&](int n) {
-      for (int i = 0; i < n; ++i) {
-        mbar_wait(&full[stage], phase);
-        if (lane == 0) mbar_arrive(&ready[stage]);
-        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
-      }
-    };
+    uint32_t ph4 = 0;  // per-stage parity of full4 (outlier stages do not use it)
+    int aslot = 0;
+    uint32_t aphase = 0;
+    const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + C::kACol;
     auto widen = [&](int n) {
       for (int i = 0; i < n; ++i) {
-        mbar_wait(&full[stage], phase);
-        uint8_t* sa = smem + stage * C::kStageBytes;
-        const uint8_t* s4 = sa + C::kA4Off;
-        // all 8 input chunks first (independent loads in flight), then widen + store
-        uint4 win[8];
+        mbar_wait(&full4[stage], (ph4 >> stage) & 1u);
+        ph4 ^= 1u << stage;
+        const uint8_t* row = smem + stage * C::kStageBytes + r * (kKBlockBytes / 2);
+        uint4 win[4];
 #pragma unroll
-        for (int it = 0; it < 8; ++it) {
-          const int item = t64 + it * 64;  // 512 = 128 rows x 4 input chunks
-          win[it] = *reinterpret_cast<const uint4*>(s4 + (item >> 2) * 64 + (item & 3) * 16);
-        }
+        for (int c = 0; c < 4; ++c) win[c] = *reinterpret_cast<const uint4*>(row + ((c ^ ((r >> 1) & 3)) << 4));
+        uint32_t v[32];
 #pragma unroll
-        for (int it = 0; it < 8; ++it) {
-          const int item = t64 + it * 64;
-          const int r = item >> 2, c = item & 3;
-          const uint4 w = win[it];
-          uint32_t lo[4], hi[4];
+        for (int c = 0; c < 4; ++c) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint32_t v = (&w.x)[k];
-            const uint32_t l = v & 0x0F0F0F0Fu, h = (v >> 4) & 0x0F0F0F0Fu;
-            lo[k] = l + (l & 0x08080808u) * 0x1Eu;  // sign-extend each 4-bit value to 8 bits
-            hi[k] = h + (h & 0x08080808u) * 0x1Eu;
+          for (int w = 0; w < 4; ++w) {
+            const uint32_t x = (&win[c].x)[w];
+            const uint32_t l = x & 0x0F0F0F0Fu, h = (x >> 4) & 0x0F0F0F0Fu;
+            v[8 * c + w] = l + (l & 0x08080808u) * 0x1Eu;  // sign-extend each nibble to a byte
+            v[8 * c + 4 + w] = h + (h & 0x08080808u) * 0x1Eu;
           }
-          uint8_t* row = sa + r * kKBlockBytes;
-          *reinterpret_cast<uint4*>(row + (((2 * c) ^ (r & 7)) << 4)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-          *reinterpret_cast<uint4*>(row + (((2 * c + 1) ^ (r & 7)) << 4)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
         }
-        fence_proxy_async_smem();  // generic writes -> tensor-core (async proxy) reads
+        mbar_wait(&aempty[aslot], aphase ^ 1);  // the MMAs that read this slot are done
+        tc_fence_after();
+        tmem_st32(trow + aslot * 32, v);
+        tmem_st_wait();
+        tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&ready[stage]);
-        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        if (lane == 0) arrive_leader<CG>(&ready[aslot], leader_rank);
+        if (++aslot == kAStages) { aslot = 0; aphase ^= 1; }
+        if (++stage == C::kStages) stage = 0;
       }
     };
+    auto skip = [&](int n) { stage = (stage + n) % C::kStages; };
     int it = 0;
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
       widen(h_a);
       if (two_phase && it > 0) skip(kb_out);
       widen(kb_int - h_a);
     }
-  } else if (warp >= kEpiWarp0) {
+  } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
     if constexpr (kEarlyW) asm volatile("griddepcontrol.wait;" ::: "memory");  // per-token scales, acc_in
     const int e = warp - kEpiWarp0;
     const int q = warp & 3;  // TMEM lane quadrant (hardware: lanes 32*(warp%4) .. +31)
@@ -758,7 +788,7 @@ cudaError_t launch_cfg(const KParams& kp, int num_sms, cudaStream_t stream) {
   const long long tn = (kp.N + C::kTileRows - 1) / C::kTileRows;
   const long long tiles = static_cast<long long>((kp.M + BN - 1) / BN) * (MC ? (tn + 1) / 2 : tn);
   cudaLaunchConfig_t cfg{};
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(W4 ? kThreadsW4 : kThreads);
   cfg.dynamicSmemBytes = C::kSmemBytes;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
@@ -772,8 +802,8 @@ cudaError_t launch_cfg(const KParams& kp, int num_sms, cudaStream_t stream) {
   cfg.numAttrs = 2;
   // persistent grid: as many clusters as can be co-resident (clusters must fit inside
   // a GPC, so num_sms / CL over-counts; a second partial wave would double the time)
-  static int resident[2][2] = {{0, 0}, {0, 0}};
-  int& max_clusters = resident[CL == 4][CG == 2];
+  static int resident[2][2][2] = {};
+  int& max_clusters = resident[CL == 4][CG == 2][W4];
   if (max_clusters == 0) {
     cfg.gridDim = dim3(static_cast<unsigned>(num_sms / CL * CL));
     int n = 0;
@@ -801,15 +831,15 @@ cudaError_t launch_mode(const KParams& kp, int mode, int num_sms, cudaStream_t s
   }
 }
 
-// INT4 weights widened in shared memory (1-CTA tiles: the memory-bound small-M regime)
-template <int BN>
+// INT4 weights from HBM widened into TMEM (4-bit dense layers, every tile)
+template <int CG, int BN>
 cudaError_t launch_mode_w4(const KParams& kp, int mode, int num_sms, cudaStream_t stream) {
   switch (mode) {
-    case kModeInt32: return launch_cfg<1, BN, kModeInt32, false, false, true>(kp, num_sms, stream);
-    case kModeF32: return launch_cfg<1, BN, kModeF32, false, false, true>(kp, num_sms, stream);
-    case kModeProbe: return launch_cfg<1, BN, kModeProbe, false, false, true>(kp, num_sms, stream);
-    case kModeF16: return launch_cfg<1, BN, kModeF16, false, false, true>(kp, num_sms, stream);
-    default: return cudaErrorInvalidValue;
+    case kModeInt32: return launch_cfg<CG, BN, kModeInt32, false, false, true>(kp, num_sms, stream);
+    case kModeF32: return launch_cfg<CG, BN, kModeF32, false, false, true>(kp, num_sms, stream);
+    case kModeProbe: return launch_cfg<CG, BN, kModeProbe, false, false, true>(kp, num_sms, stream);
+    case kModeF16: return launch_cfg<CG, BN, kModeF16, false, false, true>(kp, num_sms, stream);
+    default: return cudaErrorInvalidValue;  // AccInit tails read int32 accumulators, no weights
   }
 }
 
@@ -826,7 +856,7 @@ cudaError_t launch_mode_sp(const KParams& kp, int mode, int num_sms, cudaStream_
 }
 
 constexpr int kKeyMC = 1 << 30;  // dispatch key flag: 4-CTA multicast clusters
-constexpr int kKeyW4 = 1 << 29;  // dispatch key flag: INT4 weights widened in shared memory
+constexpr int kKeyW4 = 1 << 29;  // dispatch key flag: INT4 weights widened into TMEM
 
 cudaError_t launch_sp_key(int key, const KParams& kp, int mode, int num_sms, cudaStream_t stream) {
   if (key & kKeyMC) {
@@ -849,9 +879,11 @@ cudaError_t launch_sp_key(int key, const KParams& kp, int mode, int num_sms, cud
 cudaError_t launch_dense_key(int key, const KParams& kp, int mode, int num_sms, cudaStream_t stream) {
   if (key & kKeyW4) {
     switch (key & ~kKeyW4) {
-      case (1 << 16) | 32: return launch_mode_w4<32>(kp, mode, num_sms, stream);
-      case (1 << 16) | 64: return launch_mode_w4<64>(kp, mode, num_sms, stream);
-      case (1 << 16) | 128: return launch_mode_w4<128>(kp, mode, num_sms, stream);
+      case (1 << 16) | 32: return launch_mode_w4<1, 32>(kp, mode, num_sms, stream);
+      case (1 << 16) | 64: return launch_mode_w4<1, 64>(kp, mode, num_sms, stream);
+      case (1 << 16) | 128: return launch_mode_w4<1, 128>(kp, mode, num_sms, stream);
+      case (2 << 16) | 128: return launch_mode_w4<2, 128>(kp, mode, num_sms, stream);
+      case (2 << 16) | 192: return launch_mode_w4<2, 192>(kp, mode, num_sms, stream);
       default: return cudaErrorInvalidConfiguration;
     }
   }
@@ -876,10 +908,6 @@ cudaError_t launch_dense_key(int key, const KParams& kp, int mode, int num_sms, 
 
 int gemm_tile_override = 0;
 int gemm_multicast = 0;  // 1: 4-CTA multicast clusters for CTA-pair tiles (quik_set_gemm_multicast)
-// 1: INT4-weight 1-CTA tiles when the layer has INT4 weights (quik_set_gemm_w4). Off by
-// default: with the widened tile inside each ring stage the ring holds 6 instead of 8
-// stages and the weight stream is latency-bound (92 vs 60 us at OPT-66B fc1, M = 16).
-int gemm_w4 = 0;  // debug/tuning: 0 = heuristic, else (CG << 16) | BN
 
 cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream, const char** err_msg) {
   *err_msg = nullptr;
@@ -894,8 +922,13 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
   else if (a.M <= 128) bn = 128;
   else { cg = 2; bn = sp ? 192 : 256; }  // SP: 2 x 192 accumulator columns + metadata ring in TMEM
   if (gemm_tile_override) { cg = gemm_tile_override >> 16; bn = gemm_tile_override & 0xFFFF; }
-  if (sp && cg == 2 && bn == 256) bn = 192;  // 192 is the sparse CTA-pair tile, 256 the dense one
-  if (!sp && cg == 2 && bn == 192) bn = 256;
+  // INT4 weights (4-bit dense layers): every tile streams them and widens into TMEM
+  const bool acc_tail = a.mode == kModeAccInitF32 || a.mode == kModeAccInitF16;
+  const bool w4 = a.w4 != nullptr && !sp && !acc_tail;
+  // 192 is the sparse and INT4 CTA-pair tile (2 x 192 accumulator columns + the
+  // metadata / A-operand ring in TMEM), 256 the INT8 one
+  if ((sp || w4) && cg == 2 && bn == 256) bn = 192;
+  if (!(sp || w4) && cg == 2 && bn == 192) bn = 256;
 
   KParams kp{};
   kp.M = static_cast<int>(a.M);
@@ -915,10 +948,7 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
     const char* e = getenv("QUIK_GEMM_MC");
     return e ? atoi(e) : 0;
   }();
-  // INT4 weights from HBM for the 1-CTA (weight-streaming, M <= 128) tiles
-  const bool w4 = cg == 1 && a.w4 != nullptr && !sp && a.mode != kModeAccInitF32 && a.mode != kModeAccInitF16 &&
-                  gemm_w4 != 0;
-  const bool mc = cg == 2 && (mc_env != 0 || gemm_multicast != 0) && a.mode != kModeAccInitF32 && a.mode != kModeAccInitF16;
+  const bool mc = cg == 2 && !w4 && (mc_env != 0 || gemm_multicast != 0) && !acc_tail;
   const uint32_t brows = static_cast<uint32_t>(bn / cg / (mc ? 2 : 1));
   if (kp.kb_int && sp) {
     // compressed weights [N][kpad / 2], activations [M][kpad] (two atoms per stage),
@@ -944,7 +974,7 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
     cuuint32_t wbox[2] = {static_cast<cuuint32_t>(kKBlockBytes / 2), static_cast<cuuint32_t>(kBlockM)};
     cuuint32_t wel[2] = {1, 1};
     if (g_encode(&kp.tm_w4, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(a.w4), wdims, wstr, wbox, wel,
-                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
         !make_map(&kp.tm_x, a.x, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, a.kpad, a.M, a.kpad, brows)) {
       *err_msg = "tensor map encode failed (int4 operands)";

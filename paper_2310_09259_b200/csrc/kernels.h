@@ -88,18 +88,6 @@ struct GemmArgs {
 };
 constexpr int kMaxPeerOut = 7;
 
-// Weight-streaming split-K integer GEMM for M <= 64 (stream.cu): adds
-// sum_k W[n][k] * X8[t][k] into the int32 workspace acc[t][n] (which must hold
-// zeros or a partial sum). W from w4 (device INT4 layout) if non-null, else w8.
-struct StreamArgs {
-  const int8_t* w8;   // [N][kpad]
-  const uint8_t* w4;  // [N][kpad / 2] or null
-  const int8_t* x;    // [M][kpad]
-  int64_t kpad, M, N;
-  int32_t* acc;       // [M][N]
-  int splits;         // 0 = automatic
-};
-cudaError_t launch_stream_gemm(const StreamArgs& a, int num_sms, cudaStream_t stream, const char** err_msg);
 // Decode-regime quik forward on INT4 weights after K1 (stream4.cu): split-K integer
 // GEMM (TMEM-widened A, kind::i8), outlier MMAs and the dequant epilogue in one kernel.
 struct Stream4Args {
@@ -179,6 +167,10 @@ CUresult encode_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_
 
 // GEMM-layout int8 weights [N][kpad] (values in [-8, 7]) -> device INT4 layout above.
 cudaError_t launch_pack_w4(const int8_t* w8, int64_t N, int64_t kpad, uint8_t* w4, cudaStream_t stream);
+// ABI i4p rows [N][ceil(kb/2)] (packed.hpp:11-16: low nibble = even column, stored = v + 8)
+// -> the device INT4 layout [N][kpad / 2] (zero beyond kb)
+cudaError_t launch_pack_w4_abi(const uint8_t* i4p, int64_t N, int64_t kb, uint8_t* w4, int64_t kpad,
+                               cudaStream_t stream);
 
 // Compresses dense int8 GEMM-layout weights [N][kpad] (kpad % 256 == 0) into the
 // 2:4 sparse operands above. *bad is set to 1 if a group of 4 has more than two
@@ -191,9 +183,6 @@ cudaError_t launch_compress_24(const int8_t* w8, int64_t N, int64_t kpad, int8_t
 // *err_msg on failure.
 extern int gemm_tile_override;  // (cta_group << 16) | block_n, 0 = heuristic
 extern int gemm_multicast;      // 1: 4-CTA TMA-multicast clusters for CTA-pair tiles
-extern int gemm_w4;             // 1: INT4-weight (widened in smem) 1-CTA tiles when available
-extern int gemm_stream;         // 1: M <= 64 forwards use the split-K weight-streaming GEMM
-extern int gemm_w4_stream;      // 1: ... streaming the INT4 weights (4-bit layers)
 extern int gemm_stream4_auto;   // 1: 4-bit layers at M <= 32 use the INT4 stream kernel (default)
 cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream, const char** err_msg);
 

@@ -975,6 +975,35 @@ __global__ void pack_w4_kernel(const int8_t* __restrict__ w8, int64_t N, int64_t
   *reinterpret_cast<uint4*>(w4 + n * (kpad / 2) + 16 * c) = make_uint4(out[0], out[1], out[2], out[3]);
 }
 
+// ABI i4p (stored = v + 8, low nibble = even column) -> device INT4 chunk layout:
+// byte i of 16-byte chunk c = nibble(k = 32c + i) | nibble(k = 32c + 16 + i) << 4, with
+// nibble = two's complement 4-bit v = stored ^ 8, zero past kb.
+__global__ void pack_w4_abi_kernel(const uint8_t* __restrict__ src, int64_t N, int64_t kb, uint8_t* __restrict__ w4,
+                                   int64_t kpad) {
+  const int64_t per_row = kpad / 32;
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= N * per_row) return;
+  const int64_t n = idx / per_row, c = idx % per_row;
+  const uint8_t* row = src + n * ((kb + 1) / 2);
+  auto nib = [&](int64_t k) -> uint32_t {
+    if (k >= kb) return 0u;
+    const uint32_t b = row[k >> 1];
+    return (((k & 1) ? (b >> 4) : b) & 0xFu) ^ 8u;
+  };
+  uint32_t out[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = 4 * w + b;
+      v |= (nib(32 * c + i) | (nib(32 * c + 16 + i) << 4)) << (8 * b);
+    }
+    out[w] = v;
+  }
+  *reinterpret_cast<uint4*>(w4 + n * (kpad / 2) + 16 * c) = make_uint4(out[0], out[1], out[2], out[3]);
+}
+
 dim3 grid2(int64_t cols, int64_t rows) {
   int64_t gx = (cols + 255) / 256;
   if (gx > 64) gx = 64;
@@ -1142,6 +1171,14 @@ cudaError_t launch_pack_w4(const int8_t* w8, int64_t N, int64_t kpad, uint8_t* w
   if (N == 0 || kpad == 0) return cudaSuccess;
   const int64_t work = N * (kpad / 32);
   pack_w4_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, stream>>>(w8, N, kpad, w4);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_w4_abi(const uint8_t* i4p, int64_t N, int64_t kb, uint8_t* w4, int64_t kpad,
+                               cudaStream_t stream) {
+  if (N == 0 || kpad == 0) return cudaSuccess;
+  const int64_t work = N * (kpad / 32);
+  pack_w4_abi_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, stream>>>(i4p, N, kb, w4, kpad);
   return cudaGetLastError();
 }
 

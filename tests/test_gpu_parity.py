@@ -383,24 +383,23 @@ def test_non_finite_input_flags_numerical_error():
 
 @pytest.fixture(params=[0, 1], ids=["default", "alt"])
 def tile(request):
-    """Forces a GEMM tile. "alt": CTA-pair tiles run as 4-CTA TMA-multicast clusters,
-    1-CTA tiles stream INT4 weights and widen them in shared memory (W4)."""
+    """Forces a GEMM tile. "alt": CTA-pair tiles of 8-bit dense layers run as 4-CTA
+    TMA-multicast clusters. (4-bit dense layers always stream INT4 weights widened into
+    TMEM; the raw int_matmul ABI runs the INT8-operand kernel.)"""
     import paper_2310_09259_b200 as m
 
     lib = m.load_library()
 
     def force(cg, bn):
         lib.quik_set_gemm_multicast(1 if (request.param and cg == 2) else 0)
-        lib.quik_set_gemm_w4(1 if (request.param and cg == 1) else 0)
         return lib.quik_set_gemm_tile(cg, bn)
 
     yield force
     lib.quik_set_gemm_tile(0, 0)
     lib.quik_set_gemm_multicast(0)
-    lib.quik_set_gemm_w4(0)
 
 
-@pytest.mark.parametrize("cg,bn", [(1, 32), (1, 64), (1, 128), (2, 128), (2, 256)])
+@pytest.mark.parametrize("cg,bn", [(1, 32), (1, 64), (1, 128), (2, 128), (2, 192), (2, 256)])
 def test_every_tile_config_exact(tile, cg, bn):
     """Forces each GEMM tile (1-CTA and CTA-pair) and checks the INT32 path and the
     O=0 f32 layer bit-exactly, with ragged M/N/K tails."""
@@ -760,12 +759,12 @@ def test_sparse_not_compressible_stays_dense():
 
 @pytest.mark.parametrize("bits", [4, 8])
 def test_stream_gemm_bit_identical_to_fused(bits):
-    """Small-M forwards: the INT4 decode kernel (default for 4-bit layers at M <= 32: INT4
-    split-K GEMM + the fused epilogue finalised by the last CTA of each weight block) and
-    the opt-in split-K streams (INT8 / shared-memory INT4) + AccInit epilogue. Integer
-    sums are exact and the epilogue instructions are the fused kernel's, so every path is
-    bit-identical to the fused one (f32 and f16 out, repeat calls: the workspace and
-    counters are left zeroed), and to the reference when O = 0."""
+    """Small-M forwards: the decode kernel (default for dense layers at M <= 32: split-K
+    GEMM on INT4 weights widened into TMEM (4-bit) or INT8 tiles (8-bit) + the fused
+    epilogue finalised by the last CTA of each weight block) against the fused kernel.
+    Integer sums are exact and the epilogue instructions are the fused kernel's, so both
+    are bit-identical (f32 and f16 out, repeat calls: the workspace and counters are left
+    zeroed), and equal to the reference when O = 0."""
     m = q()
     o = oracle()
     import torch
@@ -780,25 +779,19 @@ def test_stream_gemm_bit_identical_to_fused(bits):
             xt = torch.from_numpy(x).cuda()
             for dt in (torch.float32, torch.float16):
                 outs = []
-                for decode, stream_on, int4 in [(0, 0, 0), (1, 0, 0), (1, 0, 0), (0, 1, 1), (0, 1, 0)]:
+                for decode in (0, 1, 1):
                     lib.quik_set_int4_decode(decode)
-                    lib.quik_set_stream_gemm(stream_on, int4)
                     outs.append(dev(xt, out_dtype=dt).cpu().numpy())
                 u = np.uint32 if dt == torch.float32 else np.uint16
                 for y in outs[1:]:
                     np.testing.assert_array_equal(y.view(u), outs[0].view(u))
             if O == 0:
                 lib.quik_set_int4_decode(1)
-                lib.quik_set_stream_gemm(0, 1)
                 st, want = o.quik_matmul(L, x, 2)
                 got = dev(xt, out_dtype=torch.float32).cpu().numpy()
                 np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
     finally:
-        lib.quik_set_stream_gemm(0, 1)
         lib.quik_set_int4_decode(1)
-
-
-# --------------------------------------------------------------------------- layer bundles (§8f.1)
 
 
 @pytest.mark.parametrize("name", ["f16_w4_o64", "sp24_w4_o16"])
@@ -1025,7 +1018,7 @@ def test_sharded_forward_fused_all_gather(M, stream):
     full = m.QuikLinear(layer)
     xt = torch.from_numpy(x).cuda().half()
     try:
-        lib.quik_set_stream_gemm(stream, 1)
+        lib.quik_set_int4_decode(1 - stream)
         want = full(xt)
         ns = 768 // 3
         shards = [m.QuikLinear(layer, row_begin=r * ns, row_end=(r + 1) * ns) for r in range(3)]
@@ -1036,7 +1029,7 @@ def test_sharded_forward_fused_all_gather(M, stream):
         for o in outs:
             assert torch.equal(o.view(torch.int16), want.view(torch.int16))
     finally:
-        lib.quik_set_stream_gemm(0, 1)
+        lib.quik_set_int4_decode(1)
     with pytest.raises(NotImplementedError):  # pitch / offset not TMA-aligned
         shards[0].forward_sharded(xt, [torch.empty((M, 770), dtype=torch.float16, device="cuda")], 3)
 
@@ -1331,8 +1324,10 @@ def test_split_and_unpack_match_reference():
     for bits, cols in [(4, 7), (4, 64), (8, 33)]:
         v = rng.integers(-8 if bits == 4 else -128, 8 if bits == 4 else 128, size=(5, cols))
         pk = m.pack_values(v, 5, cols, bits)
-        np.testing.assert_array_equal(m._unpack_device(pk), v.astype(np.int8))
-        np.testing.assert_array_equal(m._unpack_device(pk), o.unpack(pk.data, 5, cols, bits))
+        from paper_2310_09259_b200.quik import _unpack_device
+
+        np.testing.assert_array_equal(_unpack_device(pk), v.astype(np.int8))
+        np.testing.assert_array_equal(_unpack_device(pk), o.unpack(pk.data, 5, cols, bits))
         if bits == 4:
             np.testing.assert_array_equal(m.unpack_int4(pk), v.astype(np.int8))
         else:

@@ -96,11 +96,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--only", default="")
-    ap.add_argument("--stream", default="", help="'int8' / 'int4': split-K weight-streaming GEMM for M <= 64")
     ap.add_argument("--opt-m", default="", help="comma list of OPT fc1 token counts (default: all)")
     args = ap.parse_args()
-    if args.stream:
-        q._lib.check(q.load_library().quik_set_stream_gemm(1, 1 if args.stream == "int4" else 0))
     layers = {}
     res = []
     for s in SHAPES:
