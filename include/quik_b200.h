@@ -242,6 +242,20 @@ quik_status quik_linear_forward_sharded(quik_ctx_t ctx, quik_layer_t shard, cons
                                         int64_t M, void* const* y_dst, int n_dst, int64_t ldy, int64_t col_offset,
                                         void* stream);
 
+/* CUDA IPC plumbing for the fused all-gather across processes (one process per GPU):
+ * quik_ipc_handle_get returns the IPC handle of the allocation holding `dev_ptr` and
+ * the byte offset of dev_ptr inside it (works for pointers from caching allocators);
+ * another process opens it with quik_ipc_handle_open (peer access enabled lazily) and
+ * gets the same buffer mapped at *dev_ptr (offset applied), suitable as a y_dst of
+ * quik_linear_forward_sharded; quik_ipc_handle_close unmaps it. */
+typedef struct quik_ipc_handle {
+  unsigned char bytes[64]; /* cudaIpcMemHandle_t */
+  int64_t offset;          /* byte offset of the pointer inside the allocation */
+} quik_ipc_handle;
+quik_status quik_ipc_handle_get(quik_ctx_t ctx, const void* dev_ptr, quik_ipc_handle* out);
+quik_status quik_ipc_handle_open(quik_ctx_t ctx, const quik_ipc_handle* handle, void** dev_ptr);
+quik_status quik_ipc_handle_close(quik_ctx_t ctx, void* dev_ptr, const quik_ipc_handle* handle);
+
 /* WeightOnly mode (reference LayerMode::WeightOnly, weight_only_forward,
  * runtime.cpp:115-136): activations stay floating point,
  *   y = (bias + x_o W_o^T) + x_b (q * scale)^T

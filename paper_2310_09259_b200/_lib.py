@@ -36,7 +36,8 @@ EXPORTED_SYMBOLS = (
     "quik_linear_forward_weight_only", "quik_linear_forward_sharded", "quik_set_int4_decode",
     "quik_gptq_quantize", "quik_hessian_accumulate", "quik_ctx_clear_error", "quik_ctx_reserve", "quik_layer_layout",
     "quik_linear_forward_timed", "quik_split_activations", "quik_unpack_values", "quik_compute_wreduced",
-    "quik_dequantize_weights", "quik_elementwise",
+    "quik_dequantize_weights", "quik_elementwise", "quik_ipc_handle_get", "quik_ipc_handle_open",
+    "quik_ipc_handle_close",
 )
 
 
@@ -50,6 +51,11 @@ class FormatError(RuntimeError):
 
 class QuikCudaError(RuntimeError):
     """CUDA failure inside the native library (no CPU fallback exists)."""
+
+
+class IpcHandle(C.Structure):
+    """quik_ipc_handle: a cudaIpcMemHandle_t + the pointer's offset in its allocation."""
+    _fields_ = [("bytes", C.c_ubyte * 64), ("offset", C.c_int64)]
 
 
 class WeightsDesc(C.Structure):
@@ -114,6 +120,9 @@ def load() -> C.CDLL:
             "quik_compute_wreduced": (i32, [vp, vp, i64, i64, i32, vp, vp, vp]),
             "quik_dequantize_weights": (i32, [vp, vp, i64, i64, i32, vp, vp, vp, i64, vp, vp]),
             "quik_elementwise": (i32, [vp, i32, vp, vp, vp, i64, vp]),
+            "quik_ipc_handle_get": (i32, [vp, vp, C.POINTER(IpcHandle)]),
+            "quik_ipc_handle_open": (i32, [vp, C.POINTER(IpcHandle), C.POINTER(vp)]),
+            "quik_ipc_handle_close": (i32, [vp, vp, C.POINTER(IpcHandle)]),
             "quik_set_gemm_tile": (i32, [i32, i32]),
             "quik_set_probe_mode": (i32, [i32]),
             "quik_linear_forward_host": (i32, [vp, vp, vp, i32, i64, vp, i32, i64, vp]),

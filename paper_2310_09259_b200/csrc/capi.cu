@@ -2,6 +2,7 @@
 // reference's exceptions (runtime.cpp / packed.cpp); device work is delegated
 // to the kernels in gemm.cu and quantize.cu. No CPU compute fallback exists:
 // every numerical result comes from a CUDA kernel.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1251,6 +1252,63 @@ quik_status quik_rtn_quantize_weights(quik_ctx_t ctx, const float* w, int64_t N,
       QK_CUDA(cudaStreamSynchronize(st));  // tab must outlive the copy
       return QUIK_OK;
     });
+  });
+}
+
+namespace {
+// cuMemGetAddressRange through the runtime's driver entry point (no -lcuda link)
+typedef CUresult (*AddrRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+AddrRangeFn addr_range_fn() {
+  static AddrRangeFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &f, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<AddrRangeFn>(f);
+  }();
+  return fn;
+}
+}  // namespace
+
+quik_status quik_ipc_handle_get(quik_ctx_t ctx, const void* dev_ptr, quik_ipc_handle* out) {
+  if (!ctx || !dev_ptr || !out) return fail(QUIK_ERR_INVALID_ARGUMENT, "ipc: null argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    AddrRangeFn range = addr_range_fn();
+    if (!range) return fail(QUIK_ERR_CUDA, "ipc: cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+      return fail(QUIK_ERR_INVALID_ARGUMENT, "ipc: pointer is not device memory");
+    cudaIpcMemHandle_t h;
+    QK_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    std::memcpy(out->bytes, &h, 64);
+    out->offset = static_cast<int64_t>(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+    return QUIK_OK;
+  });
+}
+
+quik_status quik_ipc_handle_open(quik_ctx_t ctx, const quik_ipc_handle* handle, void** dev_ptr) {
+  if (!ctx || !handle || !dev_ptr) return fail(QUIK_ERR_INVALID_ARGUMENT, "ipc: null argument");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle->bytes, 64);
+    void* base = nullptr;
+    QK_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *dev_ptr = static_cast<char*>(base) + handle->offset;
+    return QUIK_OK;
+  });
+}
+
+quik_status quik_ipc_handle_close(quik_ctx_t ctx, void* dev_ptr, const quik_ipc_handle* handle) {
+  if (!ctx || !dev_ptr || !handle) return fail(QUIK_ERR_INVALID_ARGUMENT, "ipc: null argument");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    QK_CUDA(cudaIpcCloseMemHandle(static_cast<char*>(dev_ptr) - handle->offset));
+    return QUIK_OK;
   });
 }
 

@@ -33,8 +33,10 @@
 // call, packed.cpp:110-111). Each CTA TMA-loads its 128 x 64-byte INT4 tile (64-byte
 // swizzle) into the stage with its own barrier; four widening warps (one per TMEM lane
 // quadrant, thread = weight row) sign-extend the nibbles and tcgen05.st the int8 row
-// into a TMEM A-operand ring (lane = row, column j = k 4j..4j+3); the MMA warp issues
-// tcgen05.mma kind::i8 with A from TMEM and the activation codes from shared memory.
+// into a TMEM A-operand ring (lane = row, column j = k 4j..4j+3) as 16 x the value (the
+// nibble in the high half of the byte: one or two logic ops per word; the epilogue
+// shifts the exact int32 sums right by 4); the MMA warp issues tcgen05.mma kind::i8
+// with A from TMEM and the activation codes from shared memory.
 // The widened operand never touches shared memory, so per stage the SM's shared
 // memory moves 8 KB of INT4 weights (TMA in + one read) instead of 16 KB twice.
 #include <cudaTypedefs.h>
@@ -484,34 +486,43 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
     int aslot = 0;
     uint32_t aphase = 0;
     const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + C::kACol;
-    auto widen = [&](int n) {
-      for (int i = 0; i < n; ++i) {
-        mbar_wait(&full4[stage], (ph4 >> stage) & 1u);
-        ph4 ^= 1u << stage;
-        const uint8_t* row = smem + stage * C::kStageBytes + r * (kKBlockBytes / 2);
-        uint4 win[4];
+    const int swz = (r >> 1) & 3;
+    // Widening as 16 x the value: the nibble moved to the HIGH half of its byte is the
+    // int8 16 * v (two's complement), one or two logic ops per word instead of a
+    // sign extension; the MMA sums 16 * (w * a) exactly (|acc| <= 16 * 64 * K_b < 2^31)
+    // and the epilogue shifts the accumulator right by 4 (exact).
+    auto load_tile = [&](uint4 (&win)[4]) {
+      mbar_wait(&full4[stage], (ph4 >> stage) & 1u);
+      ph4 ^= 1u << stage;
+      const uint8_t* row = smem + stage * C::kStageBytes + r * (kKBlockBytes / 2);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) win[c] = *reinterpret_cast<const uint4*>(row + ((c ^ ((r >> 1) & 3)) << 4));
+      for (int c = 0; c < 4; ++c) win[c] = *reinterpret_cast<const uint4*>(row + ((c ^ swz) << 4));
+      if (++stage == C::kStages) stage = 0;
+    };
+    auto widen = [&](int n) {
+      if (n <= 0) return;
+      uint4 win[4];
+      load_tile(win);
+      for (int i = 0; i < n; ++i) {
         uint32_t v[32];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
 #pragma unroll
           for (int w = 0; w < 4; ++w) {
             const uint32_t x = (&win[c].x)[w];
-            const uint32_t l = x & 0x0F0F0F0Fu, h = (x >> 4) & 0x0F0F0F0Fu;
-            v[8 * c + w] = l + (l & 0x08080808u) * 0x1Eu;  // sign-extend each nibble to a byte
-            v[8 * c + 4 + w] = h + (h & 0x08080808u) * 0x1Eu;
+            v[8 * c + w] = (x << 4) & 0xF0F0F0F0u;  // k = 32c + 4w .. +3   (low nibbles) x 16
+            v[8 * c + 4 + w] = x & 0xF0F0F0F0u;     // k = 32c + 16 + 4w .. (high nibbles) x 16
           }
         }
         mbar_wait(&aempty[aslot], aphase ^ 1);  // the MMAs that read this slot are done
         tc_fence_after();
         tmem_st32(trow + aslot * 32, v);
+        if (i + 1 < n) load_tile(win);  // next tile's shared-memory reads overlap the TMEM store
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) arrive_leader<CG>(&ready[aslot], leader_rank);
         if (++aslot == kAStages) { aslot = 0; aphase ^= 1; }
-        if (++stage == C::kStages) stage = 0;
       }
     };
     auto skip = [&](int n) { stage = (stage + n) % C::kStages; };
@@ -606,6 +617,10 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
         const float sa_l = pick(sa_pre, ci);
         const float zs_l = pick(zs_pre, ci);
         if (!kAccGlobal && kb_int > 0) tmem_ld_wait();
+        if constexpr (W4) {  // the MMAs summed 16 x the products (INT4 widening), exact
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = static_cast<uint32_t>(static_cast<int32_t>(v[j]) >> 4);
+        }
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const float sa = __shfl_sync(0xffffffffu, sa_l, j);
@@ -681,6 +696,10 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
           uint32_t v[32];
           tmem_ld32(tacc + c, v);
           tmem_ld_wait();
+          if constexpr (W4) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = static_cast<uint32_t>(static_cast<int32_t>(v[j]) >> 4);
+          }
           emit_chunk(c, v);
         }
       } else if (!two_phase) {

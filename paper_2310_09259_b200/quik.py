@@ -495,6 +495,17 @@ class QuikLinear:
             C.c_void_p(_stream_ptr(torch, x.device))))
         return outs
 
+    def forward_sharded_ptrs(self, x, dests, ldy: int, col_offset: int):
+        """forward_sharded with raw device pointers as destinations (e.g. peer outputs
+        opened through CUDA IPC, sharded.FusedAllGatherOutput); row pitch ldy elements."""
+        torch = _torch()
+        x = x.contiguous()
+        arr = (C.c_void_p * len(dests))(*dests)
+        xdt = _lib.QUIK_F16 if x.dtype == torch.float16 else _lib.QUIK_F32
+        _lib.check(self._lib.quik_linear_forward_sharded(
+            self._ctx_handle(), self.handle, _ptr(x), xdt, x.shape[0], arr, len(dests), ldy, col_offset,
+            C.c_void_p(_stream_ptr(torch, x.device))))
+
     def weight_only(self, x, out=None, out_dtype=None):
         """LayerMode::WeightOnly (reference weight_only_forward, runtime.cpp:115-136):
         activations stay floating point, y = (bias + x_o W_o^T) + x_b (q * scale)^T.

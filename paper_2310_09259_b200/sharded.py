@@ -83,3 +83,133 @@ class ShardedQuikLinear:
         return assemble(gathered.view(self.world, M, self.ns_max), self.n, self.world)
 
     __call__ = forward
+
+
+# --------------------------------------------------------------------------- fused all-gather (CUDA IPC)
+
+
+def gather_handles(mine: list, group=None) -> list:
+    """Every rank's list of serialised IPC handles (one per output buffer), rank-indexed."""
+    import torch.distributed as dist
+
+    allh = [None] * dist.get_world_size(group)
+    dist.all_gather_object(allh, mine, group=group)
+    return allh
+
+
+def peer_destinations(rank: int, world: int, own, opened: dict) -> list:
+    """Destination list of a rank's fused epilogue: its own output first, then every
+    other rank's output (opened IPC mappings) in rank order."""
+    if set(opened) != set(range(world)) - {rank}:
+        raise ValueError("fused all-gather: need the outputs of every other rank")
+    return [own] + [opened[r] for r in range(world) if r != rank]
+
+
+class FusedAllGatherOutput:
+    """[M][N] f16 output buffers shared by all ranks of a process group through CUDA IPC
+    (one process per GPU): every rank's GEMM epilogue TMA-stores its
+    shard tile by tile into EVERY rank's buffer (C ABI quik_linear_forward_sharded), so
+    the exchange rides NVLink under the next tiles' MMAs and needs no all-gather or
+    transpose. `buffers` outputs are used round robin: with two, the completion
+    barrier of step i also orders every rank's readers of step i-2's buffer (enqueued
+    before step i-1) before step i's writes into it."""
+
+    def __init__(self, M: int, N: int, group=None, device=None, buffers: int = 2):
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+        from .quik import context
+
+        self.dist, self.group = dist, group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.lib = _lib.load()
+        self.ctx = context(device)
+        dev = torch.device("cuda", self.ctx.device)
+        self.bufs = [torch.empty((M, N), dtype=torch.float16, device=dev) for _ in range(buffers)]
+        mine = []
+        for b in self.bufs:
+            h = _lib.IpcHandle()
+            _lib.check(self.lib.quik_ipc_handle_get(self.ctx.handle, C.c_void_p(b.data_ptr()), C.byref(h)))
+            mine.append(bytes(h.bytes) + int(h.offset).to_bytes(8, "little", signed=True))
+        allh = gather_handles(mine, group)
+        self._opened = []  # (ptr, handle) to close
+        self.dests = []
+        for i, b in enumerate(self.bufs):
+            opened = {}
+            for r in range(self.world):
+                if r == self.rank:
+                    continue
+                raw = allh[r][i]
+                h = _lib.IpcHandle()
+                C.memmove(h.bytes, raw[:64], 64)
+                h.offset = int.from_bytes(raw[64:72], "little", signed=True)
+                p = C.c_void_p()
+                _lib.check(self.lib.quik_ipc_handle_open(self.ctx.handle, C.byref(h), C.byref(p)))
+                opened[r] = p.value
+                self._opened.append((p.value, h))
+            self.dests.append(peer_destinations(self.rank, self.world, b.data_ptr(), opened))
+        self.flag = torch.zeros(1, dtype=torch.float32, device=dev)
+        self.step = 0
+
+    def next(self):
+        """-> (buffer index, destination pointers) of the next step."""
+        i = self.step % len(self.bufs)
+        self.step += 1
+        return i, self.dests[i]
+
+    def barrier(self):
+        """Stream-ordered completion fence: every rank's stores into every buffer are done
+        (a one-element all-reduce on the group, after the GEMM in stream order)."""
+        self.dist.all_reduce(self.flag, group=self.group)
+
+    def close(self):
+        import ctypes as C
+
+        for p, h in self._opened:
+            self.lib.quik_ipc_handle_close(self.ctx.handle, C.c_void_p(p), C.byref(h))
+        self._opened = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class FusedShardedQuikLinear:
+    """y = quik_matmul(layer, x) over a process group with the all-gather fused into the
+    GEMM epilogue (CUDA IPC peer stores, FusedAllGatherOutput). Returns this rank's copy
+    of the full [M][N] f16 output (valid on the current stream after the barrier)."""
+
+    def __init__(self, layer, max_tokens: int, group=None, device=None, local=None, n_total: int = 0,
+                 barrier: bool = True):
+        """layer: the full QuikLinearLayer (host arrays), or local = this rank's device
+        shard (QuikLinear over rows shard_bounds(n_total, world, rank)) + n_total."""
+        import torch.distributed as dist
+
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        self.n = layer.out_features() if local is None else n_total
+        self.begin, self.end = shard_bounds(self.n, world, rank)
+        if local is None:
+            from .quik import QuikLinear
+
+            local = QuikLinear(layer, device=device, row_begin=self.begin, row_end=self.end)
+        self.local = local
+        self.out = FusedAllGatherOutput(max_tokens, self.n, group=group, device=local.device)
+        self.use_barrier = barrier
+
+    def forward(self, x):
+        i, dests = self.out.next()
+        buf = self.out.bufs[i]
+        M = x.shape[0]
+        self.local.forward_sharded_ptrs(x, dests, buf.stride(0), self.begin)
+        if self.use_barrier:
+            self.out.barrier()
+        return buf[:M]
+
+    __call__ = forward

@@ -96,3 +96,46 @@ def test_sharded_forward_gloo_world2_matches_unsharded():
     for p in procs:
         p.join(30)
     assert res == {0: True, 1: True}
+
+
+def _ipc_worker(rank, world, port, out_q):
+    """Handle exchange of the fused all-gather (sharded.FusedAllGatherOutput) with
+    stand-in handles: every rank serialises one handle per output buffer, gathers all of
+    them, 'opens' the others' and builds its destination list [own, others in rank order]."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2310_09259_b200.sharded import gather_handles, peer_destinations
+
+        mine = [bytes([rank, b]) * 36 for b in range(2)]  # 72-byte stand-ins (64 handle + 8 offset)
+        allh = gather_handles(mine)
+        ok = len(allh) == world and all(allh[r][b] == bytes([r, b]) * 36 for r in range(world) for b in range(2))
+        opened_of = lambda raw: 1000 * raw[0] + raw[1]  # noqa: E731  "open" -> a fake device pointer
+        dests = [peer_destinations(rank, world, opened_of(mine[b]),
+                                   {r: opened_of(allh[r][b]) for r in range(world) if r != rank}) for b in range(2)]
+        want = [[1000 * rank + b] + [1000 * r + b for r in range(world) if r != rank] for b in range(2)]
+        out_q.put((rank, ok and dests == want))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(120)
+def test_fused_all_gather_handle_exchange_gloo_world3():
+    ctx = mp.get_context("spawn")
+    qout = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 3, port, qout)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = dict(qout.get(timeout=100) for _ in procs)
+    for p in procs:
+        p.join(30)
+    assert res == {0: True, 1: True, 2: True}
+
+
+def test_peer_destinations_rejects_missing_ranks():
+    from paper_2310_09259_b200.sharded import peer_destinations
+
+    assert peer_destinations(1, 3, "own", {0: "a", 2: "c"}) == ["own", "a", "c"]
+    with pytest.raises(ValueError):
+        peer_destinations(1, 3, "own", {0: "a"})

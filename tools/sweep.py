@@ -26,8 +26,15 @@ SHAPES = [
     ("cfg5 13B q 2:4", 2048, 5120, 5120, 256, 4, True),
     ("cfg3 70B up/gate 2:4", 4096, 8192, 28672, 256, 4, True),
     ("cfg4 OPT fc1 M=16 2:4", 16, 9216, 36864, 256, 4, True),
+    ("cfg4 OPT-66B fc2 M=2048", 2048, 36864, 9216, 256, 4),
+    # Falcon-180B (hidden 14848, FFN 59392; public model card), FC2 INT8 with the
+    # proportional outlier count 256 * 59392 / 14848 = 1024
+    ("cfg4 Falcon-180B fc1 M=2048", 2048, 14848, 59392, 256, 4),
+    ("cfg4 Falcon-180B fc2 W8A8 M=2048", 2048, 59392, 14848, 1024, 8),
+    ("cfg4 Falcon-180B qkv M=2048", 2048, 14848, 14848, 256, 4),
 ]
 OPT_FC1 = [(m, 9216, 36864, 256, 4) for m in (1, 16, 64, 128, 256, 512, 1024, 2048, 4096, 8192)]
+FALCON_FC1 = [(m, 14848, 59392, 256, 4) for m in (1, 16, 128, 512, 2048, 8192)]
 
 
 def timeit(fn, iters=20, warm=5):
@@ -97,6 +104,7 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--only", default="")
     ap.add_argument("--opt-m", default="", help="comma list of OPT fc1 token counts (default: all)")
+    ap.add_argument("--falcon", action="store_true", help="also the Falcon-180B fc1 token sweep")
     args = ap.parse_args()
     layers = {}
     res = []
@@ -109,6 +117,9 @@ def main():
         opt = [o for o in OPT_FC1 if str(o[0]) in args.opt_m.split(",")]
     for m, K, N, O, bits in ([] if args.only and not args.opt_m else opt):
         res.append(run(f"cfg4 OPT-66B fc1 M={m}", m, K, N, O, bits, layers))
+    if args.falcon:
+        for m, K, N, O, bits in FALCON_FC1:
+            res.append(run(f"cfg4 Falcon-180B fc1 M={m}", m, K, N, O, bits, layers))
     for r in res:
         print(json.dumps(r), flush=True)
 
