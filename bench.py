@@ -6,9 +6,11 @@ One step = one QUIK linear forward (K1 fused quantizer + fused tcgen05 INT/FP16
 GEMM with the dequantisation epilogue) over a synthetic activation batch of the
 workload shape, inputs resident in HBM. Default workload: BASELINE configs[2],
 the LLaMA-2-70B MLP up/gate layer 8192 -> 28672, 256 outliers, W4A4, 4096 tokens
-(fits one GPU). For N > 1 (torchrun) the output features are sharded over the
-ranks and the FP16 output is all-gathered with NCCL (strong scaling: total work
-fixed). value = whole-job TOPS = 2*M*N*K / step time (max over ranks).
+(fits one GPU). For N > 1 (torchrun, or self-launched by --gpus N) the output
+features are sharded over the ranks and every rank's GEMM epilogue stores its f16
+shard into every rank's [M][N] output through CUDA IPC (the all-gather fused into
+the GEMM; NCCL all-gather timed beside it; strong scaling: total work fixed).
+value = whole-job TOPS = 2*M*N*K / step time (max over ranks).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg3]
   python bench.py --impl reference ...   # the reference's own CPU quik_matmul
@@ -400,15 +402,37 @@ def run_ours(args, w):
             out.copy_(torch.stack(parts))
 
     y_local = torch.empty((M, ns), dtype=torch.float16, device=dev)
+    fused, fused_err = None, None
     if world > 1:
         gathered = torch.empty((world, M, ns), dtype=torch.float16, device=dev)
         y = torch.empty((M, N), dtype=torch.float16, device=dev)
+        # N > 1 exchange: the all-gather fused into the GEMM epilogue (CUDA IPC peer
+        # stores into every rank's [M][N] output + a one-element NCCL all-reduce as the
+        # completion fence); NCCL all-gather + transpose is measured beside it
+        try:
+            from paper_2310_09259_b200.sharded import FusedShardedQuikLinear
+
+            def gloo_fence():
+                torch.cuda.synchronize()
+                dist.barrier()
+
+            fused = FusedShardedQuikLinear(None, M, local=layer, n_total=N,
+                                           barrier_fn=None if backend == "nccl" else gloo_fence)
+        except Exception as exc:  # reported in the JSON line; the NCCL exchange is used instead
+            fused, fused_err = None, f"{type(exc).__name__}: {exc}"[:300]
+
+    def step_nccl(i):
+        layer.forward(xs_dev[i % nbuf], out=y_local)
+        all_gather(gathered, y_local)
+        y.view(M, world, ns).copy_(gathered.permute(1, 0, 2))
 
     def step(i, mid_event=None):
-        layer.forward(xs_dev[i % nbuf], out=y_local, mid_event=mid_event)
-        if world > 1:
-            all_gather(gathered, y_local)
-            y.view(M, world, ns).copy_(gathered.permute(1, 0, 2))
+        if world == 1:
+            layer.forward(xs_dev[i % nbuf], out=y_local, mid_event=mid_event)
+        elif fused is not None:
+            fused(xs_dev[i % nbuf])
+        else:
+            step_nccl(i)
 
     steps, warm = args.steps, args.warmup
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
@@ -465,6 +489,29 @@ def run_ours(args, w):
     torch.cuda.synchronize()
     quant_ms = [a.elapsed_time(b) for a, b, _ in ev_mid]
     gemm_ms = [b.elapsed_time(c) for _, b, c in ev_mid]
+
+    exchange = None
+    if world > 1:
+        # the same K steps with the other exchange, and compute only (no exchange)
+        def timed(fn):
+            torch.cuda.synchronize()
+            dist.barrier()
+            a, b = ev(), ev()
+            a.record()
+            for i in range(steps):
+                fn(i)
+            b.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([a.elapsed_time(b) / steps], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+
+        exchange = dict(headline="fused all-gather (CUDA IPC peer stores in the GEMM epilogue + NCCL fence)"
+                        if fused is not None else "NCCL all-gather + transpose", fused_error=fused_err,
+                        nccl_allgather_ms=timed(step_nccl),
+                        compute_only_ms=timed(lambda i: layer.forward(xs_dev[i % nbuf], out=y_local)))
+        if fused is not None:
+            exchange["fused_ms"] = timed(lambda i: fused(xs_dev[i % nbuf]))
 
     sustained = None
     if args.soak_s > 0:
@@ -583,11 +630,15 @@ def run_ours(args, w):
                 layer.forward_host(xh, yh)
                 return
             xd.copy_(xh, non_blocking=True)
-            layer.forward(xd, out=y_local)
-            all_gather(gathered, y_local)
-            y.view(M, world, ns).copy_(gathered.permute(1, 0, 2))
+            if fused is not None:
+                yy = fused(xd)
+            else:
+                layer.forward(xd, out=y_local)
+                all_gather(gathered, y_local)
+                y.view(M, world, ns).copy_(gathered.permute(1, 0, 2))
+                yy = y
             if rank == 0:
-                yh.copy_(y, non_blocking=True)
+                yh.copy_(yy, non_blocking=True)
 
         e2e_step()
         torch.cuda.synchronize()
@@ -606,7 +657,8 @@ def run_ours(args, w):
         e2e = dict(value=ops / (te * 1e-3) / 1e12, unit="TOPS", h2d_bytes_per_step=M * K * 2 * world,
                    d2h_bytes_per_step=M * N * 2, ms_per_step=te, steps=e2e_steps,
                    path=("QuikLinear.forward_host (C ABI quik_linear_forward_host: chunked, H2D/kernels/D2H overlapped)"
-                         if world == 1 else "QuikLinear.forward (C ABI quik_linear_forward_ex) + NCCL all-gather")
+                         if world == 1 else ("FusedShardedQuikLinear (C ABI quik_linear_forward_sharded, IPC peer stores)"
+                                             if fused is not None else "QuikLinear.forward + NCCL all-gather"))
                    + " with pinned host f16 x -> y")
 
     # ---- CPU reference leg (rank 0, N = 1): cpu_baseline timing and the parity check of
@@ -628,13 +680,15 @@ def run_ours(args, w):
                    ms_per_step=ms_per_step, ms_per_step_median=step_med, higher_is_better=True, scaling="strong",
                    vs_baseline=None, dtype="int8", data="synthetic",
                    config=dict(workload=args.workload, desc=w["desc"], M=M, K=K, N=N, outliers=O, bits=bits,
-                               parallelism=f"output-feature shards x{world}" + (" + NCCL all-gather" if world > 1 else ""),
+                               parallelism=f"output-feature shards x{world}" + (
+                                   "" if world == 1 else (" + all-gather fused into the GEMM epilogue (CUDA IPC)"
+                                                          if fused is not None else " + NCCL all-gather")),
                                l2=(f"L2 flushed between steps (workload {footprint / 1e6:.0f} MB < 2 x L2); value = "
                                    "sum of per-step event times" if flush else
                                    f"inputs larger than L2: x rotated over {nbuf} buffers ({nbuf * M * K * 2 / 1e6:.0f} "
                                    f"MB), int8 weights {ns * ((kb + 127) // 128 * 128) / 1e6:.0f} MB, y "
                                    f"{M * ns * 2 / 1e6:.0f} MB; no flush")),
-                   parity=parity, roofline=roofline, cpu_baseline=cpu, e2e=e2e, fp16_cublas=fp16, quantizer=quant,
+                   parity=parity, exchange=exchange, roofline=roofline, cpu_baseline=cpu, e2e=e2e, fp16_cublas=fp16, quantizer=quant,
                    sustained=sustained,
                    clocks=clocks, gpu_launches=steps * q.QuikLinear.launches(),
                    precision="W%dA%d integer codes on tcgen05 kind::i8 (s32 accumulate) + f16 outliers (f32 accumulate), f16 out"

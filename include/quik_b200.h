@@ -111,7 +111,18 @@ typedef struct quik_weights_desc {
    * group has more than two non-zero codes the layer stays dense; see
    * quik_layer_is_sparse. 0: dense. (ABI version 2; absent in version 1.) */
   int sparsity;
+  /* Device copy of 4-bit dense base weights (ABI version 3):
+   *   QUIK_WEIGHTS_SPEED (0, default): INT8 GEMM-layout weights for the prefill GEMM
+   *     (the tensor-bound regime runs at the full kind::i8 rate) and, made on the first
+   *     decode-regime forward (or quik_ctx_reserve), an INT4 copy for M <= 32;
+   *   QUIK_WEIGHTS_INT4 (1): ONLY the INT4 copy (half the weight bytes of INT8; QUIK's
+   *     memory footprint): every GEMM streams INT4 tiles and widens them into TMEM.
+   * 8-bit and 2:4-compressed layers have one device copy either way. */
+  int weight_mode;
 } quik_weights_desc;
+
+#define QUIK_WEIGHTS_SPEED 0
+#define QUIK_WEIGHTS_INT4 1
 
 /* Uploads and repacks the weights into the device GEMM layout.
  * Replaces QuikLinearLayer::validate (runtime.cpp:150-167) + per-call unpack_int4
@@ -136,6 +147,9 @@ int quik_layer_is_sparse(quik_layer_t layer);
 /* Device GEMM layout of the layer's activation operands (what quik_quantize_activations_gemm
  * writes): codes int8 [M][kpad], x_outlier16 f16 [M][opad]. */
 quik_status quik_layer_layout(quik_layer_t layer, int64_t* kpad, int64_t* opad);
+/* Device memory the layer holds (weights in every copy it keeps, per-row vectors,
+ * outlier tables), bytes; -1 for a null layer. */
+int64_t quik_layer_device_bytes(quik_layer_t layer);
 
 /*
  * Layer bundles: the reference's on-disk layer format

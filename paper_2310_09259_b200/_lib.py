@@ -23,6 +23,9 @@ QUIK_ERR_FORMAT = 7
 QUIK_F16 = 0
 QUIK_F32 = 1
 
+QUIK_WEIGHTS_SPEED = 0
+QUIK_WEIGHTS_INT4 = 1
+
 EXPORTED_SYMBOLS = (
     "quik_last_error", "quik_status_string", "quik_abi_version", "quik_ctx_create", "quik_ctx_destroy",
     "quik_ctx_sync", "quik_layer_create", "quik_layer_destroy", "quik_layer_info",
@@ -37,7 +40,7 @@ EXPORTED_SYMBOLS = (
     "quik_gptq_quantize", "quik_hessian_accumulate", "quik_ctx_clear_error", "quik_ctx_reserve", "quik_layer_layout",
     "quik_linear_forward_timed", "quik_split_activations", "quik_unpack_values", "quik_compute_wreduced",
     "quik_dequantize_weights", "quik_elementwise", "quik_ipc_handle_get", "quik_ipc_handle_open",
-    "quik_ipc_handle_close",
+    "quik_ipc_handle_close", "quik_layer_device_bytes",
 )
 
 
@@ -74,6 +77,7 @@ class WeightsDesc(C.Structure):
         ("row_begin", C.c_int64),
         ("row_end", C.c_int64),
         ("sparsity", C.c_int),
+        ("weight_mode", C.c_int),
     ]
 
 
@@ -123,6 +127,7 @@ def load() -> C.CDLL:
             "quik_ipc_handle_get": (i32, [vp, vp, C.POINTER(IpcHandle)]),
             "quik_ipc_handle_open": (i32, [vp, C.POINTER(IpcHandle), C.POINTER(vp)]),
             "quik_ipc_handle_close": (i32, [vp, vp, C.POINTER(IpcHandle)]),
+            "quik_layer_device_bytes": (i64, [vp]),
             "quik_set_gemm_tile": (i32, [i32, i32]),
             "quik_set_probe_mode": (i32, [i32]),
             "quik_linear_forward_host": (i32, [vp, vp, vp, i32, i64, vp, i32, i64, vp]),

@@ -193,11 +193,13 @@ struct quik_layer_s {
   int device = 0;
   int64_t in_features = 0, out_features = 0, n_outlier = 0, kb = 0, kpad = 0, opad = 0;
   int bits = 4;
-  int8_t* w8 = nullptr;      // [out][kpad] INT8 weights of 8-bit dense layers (null otherwise)
+  int8_t* w8 = nullptr;      // [out][kpad] INT8 weights (8-bit dense layers; 4-bit dense in speed mode)
   int sparse = 0;            // 2:4 sparse GEMM operands below are in use
   int gated = 0;             // gated MLP layer: rows interleave up / gate (32-row blocks), output width N / 2
   int8_t* w_sp = nullptr;    // [out][kpad / 2]
   uint8_t* w4 = nullptr;     // [out][kpad / 2] INT4 weights of 4-bit dense layers, device nibble layout
+                             // (INT4 mode: from create; speed mode: made for the decode regime)
+  int int4_only = 0;         // QUIK_WEIGHTS_INT4: w4 is the only base-weight copy
   uint8_t* meta = nullptr;   // metadata planes (kernels.h GemmArgs)
   __half* wo16 = nullptr;    // [out][opad]
   __half* wo16_lo = nullptr; // [out][opad] f16(w_o - f16(w_o)): weight-only forward only, uploaded on its first call
@@ -295,7 +297,7 @@ GemmArgs gemm_args(quik_ctx_t ctx, const quik_layer_s* L, int64_t M) {
   g.a_zero = static_cast<const float*>(ctx->zero.p);
   g.half_range = static_cast<float>(1 << (L->bits - 1));
   g.sparse = L->sparse;
-  g.w4 = L->w4;
+  g.w4 = L->int4_only ? L->w4 : nullptr;  // speed mode: the prefill GEMM reads the INT8 copy
   g.w_sp = L->w_sp;
   g.meta = L->meta;
   return g;
@@ -451,6 +453,8 @@ quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* d, quik_l
   if (rows > 0x7fffffffLL || kb > 0x7fffffffLL)
     return fail(QUIK_ERR_UNSUPPORTED, "layer: dimensions exceed 2^31");
   if (d->in_features > 65520) return fail(QUIK_ERR_UNSUPPORTED, "layer: in_features > 65520");
+  if (d->weight_mode != QUIK_WEIGHTS_SPEED && d->weight_mode != QUIK_WEIGHTS_INT4)
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "layer: unknown weight_mode");
 
   return guarded([&] {
     DeviceGuard g(ctx->device);
@@ -548,10 +552,11 @@ quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* d, quik_l
         const int64_t rbytes = packed_row_bytes(kb, d->bits);
         void* tmp = ctx->wtmp.ensure(static_cast<size_t>(rows * rbytes));
         QK_CUDA(cudaMemcpy(tmp, d->base + rb * rbytes, static_cast<size_t>(rows * rbytes), cudaMemcpyDefault));
-        if (d->bits == 4 && !d->sparsity) {
+        if (d->bits == 4 && !d->sparsity && d->weight_mode == QUIK_WEIGHTS_INT4) {
           QK_CUDA(cudaMalloc(&L->w4, static_cast<size_t>(rows * L->kpad / 2)));
           check_launch(launch_pack_w4_abi(static_cast<const uint8_t*>(tmp), rows, kb, L->w4, L->kpad, st),
                        "int4 weight pack");
+          L->int4_only = 1;
         } else {
           QK_CUDA(cudaMalloc(&L->w8, static_cast<size_t>(rows * L->kpad)));
           check_launch(launch_unpack_to_gemm(static_cast<const uint8_t*>(tmp), rows, kb, d->bits, L->w8, L->kpad, st),
@@ -575,12 +580,13 @@ quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* d, quik_l
             cudaFree(L->meta);
             L->w_sp = nullptr;
             L->meta = nullptr;
-            if (d->bits == 4) {  // not 2:4: a dense 4-bit layer after all -> INT4 weights
+            if (d->bits == 4 && d->weight_mode == QUIK_WEIGHTS_INT4) {  // not 2:4: dense INT4 after all
               QK_CUDA(cudaMalloc(&L->w4, static_cast<size_t>(rows * L->kpad / 2)));
               check_launch(launch_pack_w4(L->w8, rows, L->kpad, L->w4, st), "int4 weight pack");
               QK_CUDA(cudaStreamSynchronize(st));
               QK_CUDA(cudaFree(L->w8));
               L->w8 = nullptr;
+              L->int4_only = 1;
             }
           } else {
             L->sparse = 1;
@@ -862,6 +868,20 @@ quik_status quik_dequantize_epilogue(quik_ctx_t ctx, const int32_t* acc, int64_t
 }  // extern "C"
 
 namespace {
+// Speed mode: the INT4 copy of a 4-bit dense layer for the decode kernel, made on the
+// first M <= 32 forward (not under stream capture: quik_ctx_reserve makes it ahead).
+bool ensure_w4(quik_layer_s* L, cudaStream_t st) {
+  if (L->w4) return true;
+  if (L->bits != 4 || !L->w8 || L->sparse) return false;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  QK_CUDA(cudaStreamIsCapturing(st, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return false;
+  const int64_t rows = L->out_features;  // all rows (gated: up + gate)
+  QK_CUDA(cudaMalloc(&L->w4, static_cast<size_t>(rows * L->kpad / 2)));
+  check_launch(launch_pack_w4(L->w8, rows, L->kpad, L->w4, st), "int4 weight pack");
+  return true;
+}
+
 // Events recorded at the stage boundaries of one forward (StageTimes, runtime.hpp:72-80);
 // any may be null.
 struct StageMarks {
@@ -881,6 +901,7 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
   // INT8 tiles); default on (QUIK_STREAM4=0 disables).
   bool decode = variant == QUIK_V3_FUSED_EPILOGUE && M <= 32 && L->kpad && !L->sparse && !g_probe_mode &&
                 quikb200::gemm_stream4_auto;
+  if (decode && L->bits == 4) decode = ensure_w4(L, st);
   if (decode) {
     // under stream capture no workspace may be (re)allocated: use the fused path when
     // the decode workspace / counters are not sized yet (a warm-up call sizes them)
@@ -1133,6 +1154,8 @@ quik_status quik_linear_forward_weight_only(quik_ctx_t ctx, quik_layer_t L, cons
       a.out_src = L->out_src;
       a.n_out = L->n_outlier;
       a.opad = L->opad;
+      if (L->bits == 4 && !ensure_w4(L, st))
+        return fail(QUIK_ERR_INVALID_ARGUMENT, "weight_only_forward: run one call before capturing it in a graph");
       a.w4 = L->bits == 4 ? L->w4 : nullptr;
       a.w8 = L->w8;
       a.wo = L->wo16;
@@ -1312,6 +1335,21 @@ quik_status quik_ipc_handle_close(quik_ctx_t ctx, void* dev_ptr, const quik_ipc_
   });
 }
 
+int64_t quik_layer_device_bytes(quik_layer_t L) {
+  if (!L) return -1;
+  const int64_t rows = L->out_features, nch = L->kpad / 16;
+  int64_t b = 0;
+  if (L->w8) b += rows * L->kpad;
+  if (L->w4) b += rows * L->kpad / 2;
+  if (L->w_sp) b += rows * L->kpad / 2 + 2 * (L->kpad / 256) * round_up(rows, kBlockM) * 16;
+  if (L->wo16) b += rows * L->opad * 2;
+  if (L->wo16_lo) b += rows * L->opad * 2;
+  b += rows * 4 * (2 + (L->bias ? 1 : 0));
+  b += L->kb * 4 + L->n_outlier * 4 + (L->lane_mask ? round_up(L->in_features, 16) : 0);
+  if (L->kpad) b += L->kpad * 2 + nch * 16 + std::max(L->n_gen, 1) * 2;
+  return b;
+}
+
 quik_status quik_layer_layout(quik_layer_t L, int64_t* kpad, int64_t* opad) {
   if (!L) return fail(QUIK_ERR_INVALID_ARGUMENT, "null layer");
   if (kpad) *kpad = L->kpad;
@@ -1343,6 +1381,7 @@ quik_status quik_ctx_reserve(quik_ctx_t ctx, quik_layer_t L, int64_t M) {
     if (M <= 32 && L->kpad && !L->sparse) {  // decode kernel workspace + counters (zeroed)
       ctx->ensure_ws(static_cast<size_t>(M * N * 4), nullptr);
       ctx->ensure_s4_counters(quikb200::stream4_counter_count(N), nullptr);
+      if (L->bits == 4) ensure_w4(L, nullptr);
     }
     QK_CUDA(cudaDeviceSynchronize());
     return QUIK_OK;

@@ -43,6 +43,7 @@
 
 #include <cstdlib>
 #include <mutex>
+#include <string>
 #include <vector>
 #include <cstdio>
 
@@ -56,9 +57,10 @@ namespace {
 constexpr int kEpiWarp0 = 4;
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
-constexpr int kWidenWarp0 = kEpiWarp0 + kEpiWarps;  // W4: warps 12..15 widen INT4 -> TMEM
-constexpr int kThreadsW4 = kThreads + 4 * 32;
-constexpr int kAStages = 4;                         // W4: TMEM A-operand ring (32 columns each)
+constexpr int kWidenWarp0 = kEpiWarp0 + kEpiWarps;  // W4: warps 12..19 widen INT4 -> TMEM
+constexpr int kWidenGroups = 2;                     // W4: widening warp groups (4 warps = 4 lane quadrants each)
+constexpr int kThreadsW4 = kThreads + kWidenGroups * 4 * 32;
+constexpr int kAStagesMax = 8;                      // W4: TMEM A-operand ring (32 columns each)
 constexpr int kChunk = 32;                                     // tokens per epilogue step
 constexpr int kStoreBufBytes = kChunk * 32 * 2;                // [32 tokens][32 features] f16
 constexpr int kStagingBytes = kEpiWarps * 2 * kStoreBufBytes;  // double-buffered per warp
@@ -83,18 +85,33 @@ struct Cfg {
   static constexpr int kBAtomBytes = kBRows * kKBlockBytes;
   static constexpr int kBBytes = kBAtomBytes * (SP ? 2 : 1);
   static constexpr int kMetaBytes = SP ? kMetaTileBytes : 0;
-  static constexpr int kStageBytes = kABytes + kBBytes + kMetaBytes;  // W4: INT4 tile in the A region
-  static constexpr int kBudget = 227 * 1024 - 1024 - kStagingBytes - 512;
+  // W4: the main ring carries only activation tiles; the INT4 weight tiles have their own
+  // ring (released by the widening warps as soon as they have read a tile, so the HBM
+  // weight stream is not held up by the MMAs) and the f16 outlier-weight tiles a two-slot
+  // ring of their own.
+  static constexpr int kStageBytes = W4 ? kBBytes : kABytes + kBBytes + kMetaBytes;
+  static constexpr int kA4Slots = 10;
+  static constexpr int kOASlots = 2;
+  static constexpr int kRingFixed = W4 ? kOASlots * kABytes + kA4Slots * kA4Bytes : 0;
+  static constexpr int kBudget = 227 * 1024 - 1024 - kStagingBytes - 1024 - kRingFixed;
   static constexpr int kStages = (kBudget / kStageBytes) > 8 ? 8 : (kBudget / kStageBytes);
+  static constexpr int kOAOff = kStages * kStageBytes;             // W4: outlier-weight ring
+  static constexpr int kA4Off = kOAOff + kOASlots * kABytes;       // W4: INT4 weight ring
   static constexpr int kAccCols = 2 * BN;                 // two accumulator buffers
   static constexpr int kMetaCol = kAccCols;               // SP: metadata ring after the accumulators
   static constexpr int kACol = kAccCols;                  // W4: A-operand ring after the accumulators
+  // W4: as many 32-column A slots as fit next to the accumulators (up to 8): a slot is
+  // reused only after the MMAs that read it completed, so the ring depth has to cover the
+  // widen -> MMA -> commit round trip
+  static constexpr int kAStages = (512 - kAccCols) / 32 > kAStagesMax ? kAStagesMax : (512 - kAccCols) / 32;
   static constexpr int kTmemNeed = kAccCols + (SP ? 8 * kMetaSlots : 0) + (W4 ? 32 * kAStages : 0);
   static constexpr int kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128
                                  : kTmemNeed <= 256 ? 256 : 512;
   static_assert(kTmemNeed <= 512, "TMEM: accumulators + metadata / A-operand ring");
-  static constexpr int kBarBytes = (4 * kStages + 8 + 2 * kAStages) * 8 + 16;
-  static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kStagingBytes + kBarBytes;
+  static constexpr int kBarBytes = 1024;  // mbarriers + TMEM slot
+  static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kRingFixed + kStagingBytes +
+                                    kBarBytes;
+  static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
   static constexpr int kTileRows = kBlockM * CG;          // weight rows per (cluster) tile
   static constexpr int kIntStageBytes = kABytes + kBBytes + kMetaBytes;  // expect-tx per CTA (not W4)
   static constexpr int kOutStageBytes = kABytes + kBAtomBytes;
@@ -125,6 +142,8 @@ struct KParams {
   int32_t* acc_clear;
   int meta_rows;  // SP: n_pad = round_up(N, 128) rows per metadata (stage, half) plane
   int split_num;  // h_a = kb_int * split_num / 8
+  int dbg;        // diagnostics (QUIK_W4_DBG): skip W4 synchronisation steps to locate the
+                  // bottleneck; results are garbage when non-zero. Never for results.
   // gated MLP: weight rows interleave up / gate in blocks of 32
   // (combined row 64b + w: w < 32 -> up feature 32b + w, else gate feature 32b + w - 32);
   // the epilogue emits h[t][f] = silu(gate) * up into an [M][N / 2] output
@@ -137,7 +156,8 @@ struct KParams {
   CUtensorMap tm_peer[kMaxPeerOut];
 };
 constexpr int kTraceTiles = 64;
-constexpr int kTraceSlots = 12;
+__device__ long long g_wstamps[2 * 128 * 8];  // W4 MMA / widening clock64 stamps (QUIK_GEMM_TRACE)
+constexpr int kTraceSlots = 16;
 __device__ __forceinline__ long long gtime() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -145,7 +165,9 @@ __device__ __forceinline__ long long gtime() {
 }
 // slots: 0 MMA before tempty wait, 1 after it, 2 first-half int issued, 3 after tconv
 // wait, 4 all issued, 5 summed full-barrier wait (ns); 6 epi before tint wait, 7 after,
-// 8 pass 1 done, 9 after tfin wait, 10 pass 2 done
+// 8 pass 1 done, 9 after tfin wait, 10 pass 2 done; 11 MMA summed W4 ready wait (ns);
+// W4 widening warp 12 of the leader: 12 summed full4 wait, 13 summed aempty wait,
+// 14 tile start, 15 tile end
 
 // Arrive on the barrier of this CTA pair's leader (cluster rank `leader_rank`).
 template <int CG>
@@ -175,17 +197,19 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
   // 1024-byte aligned, derived by pointer arithmetic so the compiler keeps the shared
   // address space (STS / LDS instead of generic stores in the epilogue staging)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* staging = smem + C::kStages * C::kStageBytes;
+  uint8_t* staging = smem + C::kStages * C::kStageBytes + C::kRingFixed;
   uint64_t* full = reinterpret_cast<uint64_t*>(staging + kStagingBytes);
   uint64_t* empty = full + C::kStages;
   uint64_t* tint = empty + C::kStages;  // [2] int MMAs of the tile done        (MMA -> epilogue)
   uint64_t* tconv = tint + 2;           // [2] init written into TMEM          (epilogue -> MMA)
   uint64_t* tfin = tconv + 2;           // [2] outlier MMAs done, tile final   (MMA -> epilogue)
   uint64_t* tempty = tfin + 2;          // [2] accumulator buffer drained      (epilogue -> MMA)
-  uint64_t* full4 = tempty + 2;         // [kStages] W4: this CTA's INT4 tile landed (TMA -> widen)
-  uint64_t* ready = full4 + C::kStages; // [kAStages] W4: TMEM A slot widened, both CTAs (widen -> MMA)
-  uint64_t* aempty = ready + kAStages;  // [kAStages] W4: TMEM A slot consumed (MMA -> widen)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + kAStages);
+  uint64_t* full4 = tempty + 2;          // [kA4Slots] W4: this CTA's INT4 tile landed (TMA -> widen)
+  uint64_t* empty4 = full4 + C::kA4Slots; // [kA4Slots] W4: INT4 tile read (widen -> producer)
+  uint64_t* emptyo = empty4 + C::kA4Slots; // [kOASlots] W4: outlier-weight tile consumed (MMA -> producer)
+  uint64_t* ready = emptyo + C::kOASlots; // [kAStages] W4: TMEM A slot widened, both CTAs (widen -> MMA)
+  uint64_t* aempty = ready + kAStagesMax; // [kAStages] W4: TMEM A slot consumed (MMA -> widen)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + kAStagesMax);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -218,8 +242,9 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
       mbar_init(&tempty[i], kEpiWarps * CG);
     }
     if (W4) {
-      for (int i = 0; i < C::kStages; ++i) mbar_init(&full4[i], 1);
-      for (int i = 0; i < kAStages; ++i) { mbar_init(&ready[i], 4 * CG); mbar_init(&aempty[i], 1); }
+      for (int i = 0; i < C::kA4Slots; ++i) { mbar_init(&full4[i], 1); mbar_init(&empty4[i], 4); }
+      for (int i = 0; i < C::kOASlots; ++i) mbar_init(&emptyo[i], 1);
+      for (int i = 0; i < C::kAStages; ++i) { mbar_init(&ready[i], 4 * CG); mbar_init(&aempty[i], 1); }
     }
     fence_mbar_init();
   }
@@ -233,8 +258,8 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
   // producer first issues the weight loads of its first ring stages (weights do not
   // depend on K1) and waits before the token tiles; the epilogue waits before reading
   // the per-token scales; the MMA warp only reads what the producer staged.
-  constexpr bool kEarlyW = !MC;
-  if constexpr (!kEarlyW) asm volatile("griddepcontrol.wait;" ::: "memory");
+  constexpr bool kEarlyW = !MC && !W4;  // (W4: its own early-weight path in the producer)
+  if constexpr (!kEarlyW && !W4) asm volatile("griddepcontrol.wait;" ::: "memory");
 
   const int tiles_m = (p.M + BN - 1) / BN;
   const int tiles_n = (p.N + C::kTileRows - 1) / C::kTileRows;
@@ -249,7 +274,167 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
   // Tile order: consecutive tile ids share the weight block (n) so the clusters
   // that run concurrently read the same weight rows through L2.
 
-  if (warp == 0) {
+  if (W4 && warp == 3) {
+    // ---------------------------------------------------------------- W4 weight producer
+    // INT4 weight tiles stream on their own thread, paced only by the widening warps
+    // (empty4), so the HBM weight stream runs a full weight ring ahead of the widening
+    // instead of being held to the activation ring's pace by one thread's program order.
+    if (lane == 0) {
+      const uint64_t pol_w =
+          p.w_policy == 1 ? policy_evict_first() : (p.w_policy == 2 ? policy_evict_last() : policy_evict_normal());
+      int a4 = 0;
+      uint32_t aph = 0;
+      // (weights only: no griddepcontrol.wait, the loads overlap K1 under PDL)
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+        int nb, mb;
+        decode(tile, nb, mb);
+        const int wr = nb * C::kTileRows + static_cast<int>(rank) * kBlockM;
+        for (int kb = 0; kb < kb_int; ++kb) {
+          mbar_wait(&empty4[a4], aph ^ 1);
+          mbar_arrive_expect_tx(&full4[a4], kA4Bytes);
+          tma_load_2d(smem + C::kA4Off + a4 * kA4Bytes, &p.tm_w4, kb * (kKBlockBytes / 2), wr, &full4[a4], pol_w);
+          if (++a4 == C::kA4Slots) { a4 = 0; aph ^= 1; }
+        }
+      }
+    }
+  } else if (W4 && warp == 0) {
+    // ---------------------------------------------------------------- W4 activation producer
+    if (lane == 0) {
+      const uint64_t pol_w =
+          p.w_policy == 1 ? policy_evict_first() : (p.w_policy == 2 ? policy_evict_last() : policy_evict_normal());
+      const uint64_t pol_x = policy_evict_last();
+      int b = 0, o = 0;
+      uint32_t bph = 0, oph = 0;
+      // pair form for CG == 2: both CTAs' tiles complete on the leader's barrier
+      auto tma_pair = [&](void* dst, const CUtensorMap* m, int c0, int c1, uint64_t* bar, uint64_t pol) {
+        if constexpr (CG == 1) tma_load_2d(dst, m, c0, c1, bar, pol);
+        else tma_load_2d_pair(dst, m, c0, c1, bar, pol);
+      };
+      // activation codes of k-block kb -> the main ring
+      auto load_b = [&](int kb, int trow) {
+        mbar_wait(&empty[b], bph ^ 1);
+        if (leader) mbar_arrive_expect_tx(&full[b], CG * C::kBBytes);
+        tma_pair(smem + b * C::kStageBytes, &p.tm_x, kb * kKBlockBytes, trow, &full[b], pol_x);
+        if (++b == C::kStages) { b = 0; bph ^= 1; }
+      };
+      // outlier block ko: f16 weight tile -> outlier ring, f16 activations -> main ring,
+      // both on the main ring's full barrier
+      auto load_out = [&](int ko, int wrow, int trow) {
+        mbar_wait(&emptyo[o], oph ^ 1);
+        mbar_wait(&empty[b], bph ^ 1);
+        if (leader) mbar_arrive_expect_tx(&full[b], CG * (C::kABytes + C::kBBytes));
+        tma_pair(smem + C::kOAOff + o * C::kABytes, &p.tm_wo, ko * 64, wrow, &full[b], pol_w);
+        tma_pair(smem + b * C::kStageBytes, &p.tm_xo, ko * 64, trow, &full[b], pol_x);
+        if (++o == C::kOASlots) { o = 0; oph ^= 1; }
+        if (++b == C::kStages) { b = 0; bph ^= 1; }
+      };
+      auto rows_of = [&](int tile, int& wrow, int& trow) {
+        int nb, mb;
+        decode(tile, nb, mb);
+        wrow = nb * C::kTileRows + static_cast<int>(rank) * kBlockM;
+        trow = mb * BN + static_cast<int>(rank) * C::kBRows;
+      };
+      asm volatile("griddepcontrol.wait;" ::: "memory");  // K1's codes are complete
+      int prev = -1;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+        int wr, tr;
+        rows_of(tile, wr, tr);
+        if (tile + num_clusters >= num_tiles) asm volatile("griddepcontrol.launch_dependents;");
+        for (int kb = 0; kb < h_a; ++kb) load_b(kb, tr);
+        if (two_phase && prev >= 0) {
+          int pw, pt;
+          rows_of(prev, pw, pt);
+          for (int ko = 0; ko < kb_out; ++ko) load_out(ko, pw, pt);
+        }
+        for (int kb = h_a; kb < kb_int; ++kb) load_b(kb, tr);
+        prev = tile;
+      }
+      if (two_phase && prev >= 0) {
+        int pw, pt;
+        rows_of(prev, pw, pt);
+        for (int ko = 0; ko < kb_out; ++ko) load_out(ko, pw, pt);
+      }
+    }
+  } else if (W4 && warp == 1) {
+    // ---------------------------------------------------------------- W4 MMA issuer
+    // the whole (converged) warp runs the loop and one elected lane issues each MMA /
+    // commit: back-to-back UTC*MMA instead of a per-instruction ELECT / branch loop
+    // (~13 vs ~45-70 cycles per MMA, tools/ts_rate.cu), which at BN = 192 (96 cycles
+    // of tensor work per K = 32 step) decides whether the tensor pipe stays busy
+    if (leader) {
+      constexpr uint32_t id_i8 = idesc_make(2u, 1u, kBlockM * CG, BN);
+      constexpr uint32_t id_f16 = idesc_make(1u, 0u, kBlockM * CG, BN);
+      int b = 0, o = 0, aslot = 0;
+      uint32_t bph = 0, aph = 0;
+      long long full_wait = 0, ready_wait = 0;
+      int mit = 0;
+      auto int_blocks = [&](uint32_t d, int k0, int k1) {
+        for (int kb = k0; kb < k1; ++kb) {
+          long long* ms = (p.trace && cluster_id == 0 && mit < 128 && lane == 0) ? g_wstamps + mit * 8 : nullptr;
+          ++mit;
+          if (ms) ms[0] = clock64();
+          const long long t0 = p.trace ? gtime() : 0;
+          mbar_wait(&full[b], bph);
+          if (ms) ms[1] = clock64();
+          const long long t1 = p.trace ? gtime() : 0;
+          mbar_wait(&ready[aslot], aph);
+          if (ms) ms[2] = clock64();
+          if (p.trace) { full_wait += t1 - t0; ready_wait += gtime() - t1; }
+          tc_fence_after();
+          const uint64_t bd = umma_desc_sw128(smem_u32(smem + b * C::kStageBytes));
+          const uint32_t a_tm = tmem_base + C::kACol + aslot * 32;  // both CTAs widened their rows here
+#pragma unroll
+          for (int k = 0; k < 4; ++k)  // 4 x K=32 int8 = 32 TMEM columns of A, 128 bytes of B
+            mma_i8_ts_w<CG>(d, a_tm + 8 * k, bd + 2 * k, id_i8, (kb | k) != 0);
+          if (ms) ms[3] = clock64();
+          mma_commit_w<CG>(&empty[b], static_cast<uint16_t>(3));
+          mma_commit_w<CG>(&aempty[aslot], static_cast<uint16_t>(3));
+          if (ms) ms[4] = clock64();
+          if (++b == C::kStages) { b = 0; bph ^= 1; }
+          if (++aslot == C::kAStages) { aslot = 0; aph ^= 1; }
+        }
+      };
+      auto out_blocks = [&](int it_prev) {
+        const int bp = it_prev & 1;
+        mbar_wait(&tconv[bp], (it_prev >> 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + bp * BN;
+        for (int ko = 0; ko < kb_out; ++ko) {
+          mbar_wait(&full[b], bph);
+          tc_fence_after();
+          const uint64_t ad = umma_desc_sw128(smem_u32(smem + C::kOAOff + o * C::kABytes));
+          const uint64_t bd = umma_desc_sw128(smem_u32(smem + b * C::kStageBytes));
+#pragma unroll
+          for (int k = 0; k < 4; ++k)  // 4 x K=16 f16 = 128 bytes, accumulating onto init
+            mma_f16_w<CG>(d, ad + 2 * k, bd + 2 * k, id_f16, 1u);
+          mma_commit_w<CG>(&empty[b], static_cast<uint16_t>(3));
+          mma_commit_w<CG>(&emptyo[o], static_cast<uint16_t>(3));
+          if (++b == C::kStages) { b = 0; bph ^= 1; }
+          if (++o == C::kOASlots) o = 0;
+        }
+        mma_commit_w<CG>(&tfin[bp], pair_mask);
+      };
+      int it = 0;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
+        const int bb = it & 1;
+        long long* tr =
+            (p.trace && it < kTraceTiles && lane == 0) ? p.trace + (cluster_id * kTraceTiles + it) * kTraceSlots : nullptr;
+        if (tr) { tr[0] = gtime(); full_wait = 0; ready_wait = 0; }
+        mbar_wait(&tempty[bb], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        if (tr) tr[1] = gtime();
+        const uint32_t d = tmem_base + bb * BN;
+        int_blocks(d, 0, h_a);
+        if (tr) tr[2] = gtime();
+        if (two_phase && it > 0) out_blocks(it - 1);
+        if (tr) tr[3] = gtime();
+        int_blocks(d, h_a, kb_int);
+        mma_commit_w<CG>(&tint[bb], pair_mask);
+        if (tr) { tr[4] = gtime(); tr[5] = full_wait; tr[11] = ready_wait; }
+      }
+      if (two_phase && it > 0) out_blocks(it - 1);
+    }
+  } else if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol_w =
           p.w_policy == 1 ? policy_evict_first() : (p.w_policy == 2 ? policy_evict_last() : policy_evict_normal());
@@ -282,17 +467,7 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
       };
       // integer block kb: dense = load(); SP = compressed A + two B atoms + metadata tile
       auto load_int = [&](int kb, int wrow, int trow) {
-        if constexpr (W4) {
-          // INT4 tile -> this CTA's stage, on this CTA's full4 barrier (the widening warps
-          // of each CTA wait for their own tile); activation tile -> the pair's full barrier
-          mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * C::kStageBytes;
-          if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::kBBytes);
-          mbar_arrive_expect_tx(&full4[stage], kA4Bytes);
-          tma_load_2d(sa, &p.tm_w4, kb * (kKBlockBytes / 2), wrow, &full4[stage], pol_w);
-          tma_b(sa + C::kABytes, &p.tm_x, kb * kKBlockBytes, trow, pol_x);
-          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
-        } else if constexpr (!SP) {
+        if constexpr (!SP) {
           load(&p.tm_w, &p.tm_x, kb * kKBlockBytes, wrow, trow);
         } else {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -323,12 +498,6 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
           for (int kb = 0; kb < pre; ++kb) {  // fresh ring stages 0 .. pre-1
             stage = kb;
             uint8_t* sa = smem + kb * C::kStageBytes;
-            if constexpr (W4) {
-              if (leader) mbar_arrive_expect_tx(&full[kb], CG * C::kBBytes);
-              mbar_arrive_expect_tx(&full4[kb], kA4Bytes);
-              tma_load_2d(sa, &p.tm_w4, kb * (kKBlockBytes / 2), wr0, &full4[kb], pol_w);
-              continue;
-            }
             if (leader) mbar_arrive_expect_tx(&full[kb], CG * (SP ? C::kIntStageBytes : C::kOutStageBytes));
             tma(sa, &p.tm_w, kb * kKBlockBytes, wr0, pol_w);
             if constexpr (SP) {  // 2:4 metadata of the stage (a weight-side tensor too)
@@ -375,7 +544,8 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
+    // converged warp, one elected lane issues (see the W4 MMA issuer)
+    if (leader) {
       constexpr uint32_t id_i8 = idesc_make(2u, 1u, kBlockM * CG, BN);
       constexpr uint32_t id_f16 = idesc_make(1u, 0u, kBlockM * CG, BN);
       constexpr uint32_t id_sp = idesc_make(2u, 1u, kBlockM * CG, BN) | (1u << 2);  // sparse flag
@@ -383,17 +553,13 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
       int stage = 0;
       uint32_t phase = 0;
       long long full_wait = 0;
-      int aslot = 0;  // W4: TMEM A-operand ring position
-      uint32_t aphase = 0;
-      auto next_stage = [&](uint64_t& adesc, uint64_t& bdesc, bool widened = false) {
+      auto next_stage = [&](uint64_t& adesc, uint64_t& bdesc) {
         if (p.trace) {
           const long long t0 = gtime();
           mbar_wait(&full[stage], phase);
-          if (widened) mbar_wait(&ready[aslot], aphase);
           full_wait += gtime() - t0;
         } else {
           mbar_wait(&full[stage], phase);
-          if (widened) mbar_wait(&ready[aslot], aphase);
         }
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
@@ -401,37 +567,29 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
         bdesc = umma_desc_sw128(sa + C::kABytes);
       };
       auto release_stage = [&]() {
-        mma_commit<CG>(&empty[stage], MC ? static_cast<uint16_t>(0xF) : static_cast<uint16_t>(3));
+        mma_commit_w<CG>(&empty[stage], MC ? static_cast<uint16_t>(0xF) : static_cast<uint16_t>(3));
         if (++stage == C::kStages) { stage = 0; phase ^= 1; }
       };
       uint32_t meta_slot = 0;
       auto int_blocks = [&](uint32_t d, int k0, int k1) {
         for (int kb = k0; kb < k1; ++kb) {
           uint64_t ad, bd;
-          next_stage(ad, bd, W4);
-          if constexpr (W4) {
-            // A from the TMEM ring slot (both CTAs widened their rows into it)
-            const uint32_t a_tm = tmem_base + C::kACol + aslot * 32;
-#pragma unroll
-            for (int k = 0; k < 4; ++k)  // 4 x K=32 int8 = 32 TMEM columns
-              mma_i8_ts<CG>(d, a_tm + 8 * k, bd + 2 * k, id_i8, (kb | k) != 0);
-            mma_commit<CG>(&aempty[aslot], static_cast<uint16_t>(3));  // slot free in both CTAs
-            if (++aslot == kAStages) { aslot = 0; aphase ^= 1; }
-          } else if constexpr (!SP) {
+          next_stage(ad, bd);
+          if constexpr (!SP) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)  // 4 x K=32 int8 = 128 bytes
-              mma_i8<CG>(d, ad + 2 * k, bd + 2 * k, id_i8, (kb | k) != 0);
+              mma_i8_w<CG>(d, ad + 2 * k, bd + 2 * k, id_i8, (kb | k) != 0);
           } else {
             // metadata tile -> TMEM ring slot (two 128 x 128-bit copies), then 4 sparse
             // MMAs of 64 logical K: A advances 32 compressed bytes, B 64 bytes (two atoms)
             const uint32_t te = tmem_base + C::kMetaCol + meta_slot * 8;
             const uint32_t se = smem_u32(smem + stage * C::kStageBytes + C::kABytes + C::kBBytes);
-            tmem_cp_128x128b<CG>(te, smem_desc_rows16(se));
-            tmem_cp_128x128b<CG>(te + 4, smem_desc_rows16(se + kMetaTileBytes / 2));
+            tmem_cp_128x128b_w<CG>(te, smem_desc_rows16(se));
+            tmem_cp_128x128b_w<CG>(te + 4, smem_desc_rows16(se + kMetaTileBytes / 2));
             const uint64_t bd1 = bd + ((C::kBAtomBytes >> 4) & 0x3FFF);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              mma_sp_i8<CG>(d, ad + 2 * k, (k < 2 ? bd : bd1) + 4 * (k & 1), id_sp, te + 2 * k, (kb | k) != 0);
+              mma_sp_i8_w<CG>(d, ad + 2 * k, (k < 2 ? bd : bd1) + 4 * (k & 1), id_sp, te + 2 * k, (kb | k) != 0);
             if (++meta_slot == kMetaSlots) meta_slot = 0;
           }
           release_stage();
@@ -447,15 +605,16 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
           next_stage(ad, bd);
 #pragma unroll
           for (int k = 0; k < 4; ++k)  // 4 x K=16 f16 = 128 bytes, accumulating onto init
-            mma_f16<CG>(d, ad + 2 * k, bd + 2 * k, id_f16, 1u);
+            mma_f16_w<CG>(d, ad + 2 * k, bd + 2 * k, id_f16, 1u);
           release_stage();
         }
-        mma_commit<CG>(&tfin[bp], pair_mask);
+        mma_commit_w<CG>(&tfin[bp], pair_mask);
       };
       int it = 0;
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
         const int b = it & 1;
-        long long* tr = (p.trace && it < kTraceTiles) ? p.trace + (cluster_id * kTraceTiles + it) * kTraceSlots : nullptr;
+        long long* tr =
+            (p.trace && it < kTraceTiles && lane == 0) ? p.trace + (cluster_id * kTraceTiles + it) * kTraceSlots : nullptr;
         if (tr) { tr[0] = gtime(); full_wait = 0; }
         mbar_wait(&tempty[b], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -466,7 +625,7 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
         if (two_phase && it > 0) out_blocks(it - 1);
         if (tr) tr[3] = gtime();
         int_blocks(d, h_a, kb_int);
-        mma_commit<CG>(&tint[b], pair_mask);
+        mma_commit_w<CG>(&tint[b], pair_mask);
         if (tr) { tr[4] = gtime(); tr[5] = full_wait; }
       }
       if (two_phase && it > 0) out_blocks(it - 1);
@@ -479,61 +638,91 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
     // so the 8 rows of a quarter warp read 8 distinct bank groups. Byte i of chunk c
     // holds k = 32c + i (low nibble) and 32c + 16 + i (high nibble): word w of the chunk
     // widens to TMEM columns 8c + w (low) and 8c + 4 + w (high).
+    // Two groups of four warps (one per TMEM lane quadrant each) take alternate PAIRS of
+    // the CTA's integer k-blocks (one continuous sequence over its tiles): the ring
+    // positions of k-block j follow from j (INT4 slot j % kA4Slots, TMEM slot j % kAStages,
+    // parities from the wrap counts), so the groups need no shared state; each widens
+    // two k-blocks per iteration with one store wait / fence.
     const int q = warp & 3;
+    const int g = (warp - kWidenWarp0) >> 2;
     const int r = q * 32 + lane;
-    int stage = 0;
-    uint32_t ph4 = 0;  // per-stage parity of full4 (outlier stages do not use it)
-    int aslot = 0;
-    uint32_t aphase = 0;
     const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + C::kACol;
     const int swz = (r >> 1) & 3;
+    const bool tw = p.trace && leader && warp == kWidenWarp0 && lane == 0;
+    int my_tiles = 0;
+    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) ++my_tiles;
+    const long long J = static_cast<long long>(my_tiles) * kb_int;
     // Widening as 16 x the value: the nibble moved to the HIGH half of its byte is the
     // int8 16 * v (two's complement), one or two logic ops per word instead of a
     // sign extension; the MMA sums 16 * (w * a) exactly (|acc| <= 16 * 64 * K_b < 2^31)
     // and the epilogue shifts the accumulator right by 4 (exact).
-    auto load_tile = [&](uint4 (&win)[4]) {
-      mbar_wait(&full4[stage], (ph4 >> stage) & 1u);
-      ph4 ^= 1u << stage;
-      const uint8_t* row = smem + stage * C::kStageBytes + r * (kKBlockBytes / 2);
+    auto load_tile = [&](long long j, uint4 (&win)[4]) {
+      const int sl = static_cast<int>(j % C::kA4Slots);
+      mbar_wait(&full4[sl], static_cast<uint32_t>((j / C::kA4Slots) & 1));
+      const uint8_t* row = smem + C::kA4Off + sl * kA4Bytes + r * (kKBlockBytes / 2);
+      if (p.dbg & 16) {  // diagnostics: no shared-memory reads
 #pragma unroll
-      for (int c = 0; c < 4; ++c) win[c] = *reinterpret_cast<const uint4*>(row + ((c ^ swz) << 4));
-      if (++stage == C::kStages) stage = 0;
-    };
-    auto widen = [&](int n) {
-      if (n <= 0) return;
-      uint4 win[4];
-      load_tile(win);
-      for (int i = 0; i < n; ++i) {
-        uint32_t v[32];
+        for (int c = 0; c < 4; ++c) win[c] = make_uint4(r, c, 3, 4);
+      } else {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-#pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            const uint32_t x = (&win[c].x)[w];
-            v[8 * c + w] = (x << 4) & 0xF0F0F0F0u;  // k = 32c + 4w .. +3   (low nibbles) x 16
-            v[8 * c + 4 + w] = x & 0xF0F0F0F0u;     // k = 32c + 16 + 4w .. (high nibbles) x 16
-          }
-        }
-        mbar_wait(&aempty[aslot], aphase ^ 1);  // the MMAs that read this slot are done
-        tc_fence_after();
-        tmem_st32(trow + aslot * 32, v);
-        if (i + 1 < n) load_tile(win);  // next tile's shared-memory reads overlap the TMEM store
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) arrive_leader<CG>(&ready[aslot], leader_rank);
-        if (++aslot == kAStages) { aslot = 0; aphase ^= 1; }
+        for (int c = 0; c < 4; ++c) win[c] = *reinterpret_cast<const uint4*>(row + ((c ^ swz) << 4));
       }
     };
-    auto skip = [&](int n) { stage = (stage + n) % C::kStages; };
-    int it = 0;
-    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
-      widen(h_a);
-      if (two_phase && it > 0) skip(kb_out);
-      widen(kb_int - h_a);
+    // the INT4 tile is in registers (its values consumed): hand the slot back to the producer
+    auto release_tile = [&](long long j) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty4[j % C::kA4Slots]);
+    };
+    // one k-block: 16 INT4 words -> 32 TMEM columns of 16 x the int8 codes
+    auto widen_store = [&](const uint4 (&win)[4], long long j) {
+      uint32_t v[32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const uint32_t x = (&win[c].x)[w];
+          v[8 * c + w] = (x << 4) & 0xF0F0F0F0u;  // k = 32c + 4w .. +3   (low nibbles) x 16
+          v[8 * c + 4 + w] = x & 0xF0F0F0F0u;     // k = 32c + 16 + 4w .. (high nibbles) x 16
+        }
+      }
+      if (!(p.dbg & 8)) tmem_st32(trow + static_cast<uint32_t>(j % C::kAStages) * 32, v);
+    };
+    auto slot_free = [&](long long j) {  // the MMAs that read this TMEM slot are done
+      mbar_wait(&aempty[j % C::kAStages], static_cast<uint32_t>(((j / C::kAStages) & 1) ^ 1));
+    };
+    int wit = 0;
+    for (long long j0 = 2LL * g; j0 < J; j0 += 2LL * kWidenGroups) {
+      long long* ws = (tw && cluster_id == 0 && wit < 128) ? g_wstamps + 128 * 8 + wit * 8 : nullptr;
+      ++wit;
+      if (ws) ws[0] = clock64();
+      const bool two = j0 + 1 < J;
+      uint4 wa[4], wb[4];
+      load_tile(j0, wa);
+      if (two) load_tile(j0 + 1, wb);
+      if (ws) ws[1] = clock64();
+      slot_free(j0);
+      if (two) slot_free(j0 + 1);
+      if (ws) ws[2] = clock64();
+      tc_fence_after();
+      widen_store(wa, j0);
+      release_tile(j0);
+      if (two) {
+        widen_store(wb, j0 + 1);
+        release_tile(j0 + 1);
+      }
+      if (ws) ws[3] = clock64();
+      if (!(p.dbg & 2)) tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (ws) ws[4] = clock64();
+      if (lane == 0) {
+        arrive_leader<CG>(&ready[j0 % C::kAStages], leader_rank);
+        if (two) arrive_leader<CG>(&ready[(j0 + 1) % C::kAStages], leader_rank);
+      }
+      if (ws) ws[5] = clock64();
     }
   } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
-    if constexpr (kEarlyW) asm volatile("griddepcontrol.wait;" ::: "memory");  // per-token scales, acc_in
+    if constexpr (kEarlyW || W4) asm volatile("griddepcontrol.wait;" ::: "memory");  // per-token scales, acc_in
     const int e = warp - kEpiWarp0;
     const int q = warp & 3;  // TMEM lane quadrant (hardware: lanes 32*(warp%4) .. +31)
     const int h = e >> 2;
@@ -585,7 +774,8 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
                           : nullptr;
       if (tr) tr[6] = gtime();
       if (!kAccGlobal) {
-        mbar_wait(&tint[b], par);
+        if constexpr (W4) mbar_wait_sleep(&tint[b], par);  // idle epilogue warps yield their issue slots
+        else mbar_wait(&tint[b], par);
         tc_fence_after();
       }
       if (tr) tr[7] = gtime();
@@ -723,7 +913,8 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
         if (lane == 0) arrive_leader<CG>(&tconv[b], leader_rank);
         if (tr) tr[8] = gtime();
         // pass 2: outlier MMAs have accumulated onto init
-        mbar_wait(&tfin[b], par);
+        if constexpr (W4) mbar_wait_sleep(&tfin[b], par);
+        else mbar_wait(&tfin[b], par);
         tc_fence_after();
         if (tr) tr[9] = gtime();
 #pragma unroll 1
@@ -1018,6 +1209,11 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
     return e ? atoi(e) : 0;
   }();
   kp.w_policy = w_policy;
+  static const int w4_dbg = [] {
+    const char* e = getenv("QUIK_W4_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  kp.dbg = w4_dbg;
   static const int split_env = [] {  // tuning: QUIK_SPLIT_NUM in 1..7 (eighths of the int k-blocks)
     const char* e = getenv("QUIK_SPLIT_NUM");
     return e ? atoi(e) : 0;
@@ -1026,6 +1222,7 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
   kp.gated = a.gated && a.mode != kModeInt32 && a.mode != kModeProbe;  // raw accumulators stay per row
   static const char* trace_path = getenv("QUIK_GEMM_TRACE");  // diagnostics: timeline dump
   static long long* trace_buf = nullptr;
+  // per-cluster tile stamps, then (W4) per-iteration widening stamps of cluster 0
   const size_t trace_bytes = static_cast<size_t>(num_sms) * kTraceTiles * kTraceSlots * 8;
   if (trace_path && a.mode != kModeInt32 && a.mode != kModeProbe) {
     if (!trace_buf && cudaMalloc(&trace_buf, trace_bytes) != cudaSuccess) trace_buf = nullptr;
@@ -1075,6 +1272,13 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
     cudaMemcpy(h.data(), kp.trace, trace_bytes, cudaMemcpyDeviceToHost);
     if (FILE* f = fopen(trace_path, "wb")) {
       fwrite(h.data(), 8, h.size(), f);
+      fclose(f);
+    }
+    std::vector<long long> w(2 * 128 * 8);
+    cudaMemcpyFromSymbol(w.data(), g_wstamps, w.size() * 8);
+    const std::string wp = std::string(trace_path) + ".w";
+    if (FILE* f = fopen(wp.c_str(), "wb")) {
+      fwrite(w.data(), 8, w.size(), f);
       fclose(f);
     }
     return cudaSuccess;

@@ -253,7 +253,11 @@ def _dev(torch, a: np.ndarray, device: int):
     return torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{device}")
 
 
-def _host_desc(layer: QuikLinearLayer, sparse: Optional[bool] = None, row_begin: int = 0, row_end: int = 0):
+WEIGHT_MODES = {"speed": _lib.QUIK_WEIGHTS_SPEED, "int4": _lib.QUIK_WEIGHTS_INT4}
+
+
+def _host_desc(layer: QuikLinearLayer, sparse: Optional[bool] = None, row_begin: int = 0, row_end: int = 0,
+               weights: str = "speed"):
     """-> (WeightsDesc over host copies, the copies to keep alive)."""
     w = layer.weights
     n_out = layer.outliers.outlier_count()
@@ -273,7 +277,7 @@ def _host_desc(layer: QuikLinearLayer, sparse: Optional[bool] = None, row_begin:
         outlier_weights=keep["ow"].ctypes.data, outlier_indices=keep["idx"].ctypes.data if keep["idx"].size else None,
         n_outlier=n_out, bias=None if keep["bias"] is None else keep["bias"].ctypes.data,
         row_begin=row_begin, row_end=row_end,
-        sparsity=int(bool(w.mask is not None if sparse is None else sparse)))
+        sparsity=int(bool(w.mask is not None if sparse is None else sparse)), weight_mode=WEIGHT_MODES[weights])
     return d, keep
 
 
@@ -286,9 +290,13 @@ class QuikLinear:
     output-row shard (multi-GPU column sharding)."""
 
     def __init__(self, layer: QuikLinearLayer, device: Optional[int] = None, row_begin: int = 0, row_end: int = 0,
-                 sparse: Optional[bool] = None):
+                 sparse: Optional[bool] = None, weights: str = "speed"):
         """sparse: request the 2:4 sparse GEMM (default: when the weights carry a
-        SparsityMask, i.e. come from sparsegpt_joint, quantizer.cpp:299-337)."""
+        SparsityMask, i.e. come from sparsegpt_joint, quantizer.cpp:299-337).
+        weights: device copy of 4-bit dense weights, "speed" (INT8 for the prefill GEMM +
+        INT4 for decode) or "int4" (the INT4 copy only: QUIK's memory footprint)."""
+        if weights not in WEIGHT_MODES:
+            raise ValueError(f"weights must be one of {sorted(WEIGHT_MODES)}")
         torch = _torch()
         layer.validate()
         self._lib = _lib.load()
@@ -315,7 +323,7 @@ class QuikLinear:
             outlier_weights=k["ow"].ctypes.data, outlier_indices=k["idx"].ctypes.data if k["idx"].size else None,
             n_outlier=self.n_outlier, bias=None if k["bias"] is None else k["bias"].ctypes.data,
             row_begin=row_begin, row_end=row_end,
-            sparsity=int(bool(w.mask is not None if sparse is None else sparse)))
+            sparsity=int(bool(w.mask is not None if sparse is None else sparse)), weight_mode=WEIGHT_MODES[weights])
         h = C.c_void_p()
         with torch.cuda.device(self.device):
             _lib.check(self._lib.quik_layer_create(self.ctx.handle, C.byref(d), C.byref(h)))
@@ -327,7 +335,7 @@ class QuikLinear:
 
     @classmethod
     def from_device(cls, outliers: OutlierSet, base, scales, wreduced, outlier_weights, bits: int, bias=None,
-                    row_begin: int = 0, row_end: int = 0, sparse: bool = False) -> "QuikLinear":
+                    row_begin: int = 0, row_end: int = 0, sparse: bool = False, weights: str = "speed") -> "QuikLinear":
         """Builds the layer straight from device tensors in the reference formats
         (e.g. the output of rtn_quantize_weights_device) without a host round trip."""
         torch = _torch()
@@ -346,7 +354,7 @@ class QuikLinear:
             outlier_weights=None if ow is None else ow.data_ptr(),
             outlier_indices=idx.ctypes.data if idx.size else None, n_outlier=self.n_outlier,
             bias=None if bias is None else bias.data_ptr(), row_begin=row_begin, row_end=row_end,
-            sparsity=int(sparse))
+            sparsity=int(sparse), weight_mode=WEIGHT_MODES[weights])
         h = C.c_void_p()
         with torch.cuda.device(self.device):
             torch.cuda.current_stream().synchronize()
@@ -359,7 +367,7 @@ class QuikLinear:
 
     @classmethod
     def gated(cls, up: QuikLinearLayer, gate: QuikLinearLayer, device: Optional[int] = None, row_begin: int = 0,
-              row_end: int = 0) -> "QuikLinear":
+              row_end: int = 0, weights: str = "speed") -> "QuikLinear":
         """Gated MLP projection h = silu(gate(x)) * up(x) (reference forward_model with
         gated_mlp_ops, runtime.cpp:320-392) as ONE layer: shared quantizer, one GEMM
         whose epilogue forms silu(gate) * up (C ABI quik_layer_create_gated)."""
@@ -370,8 +378,8 @@ class QuikLinear:
         self._lib = _lib.load()
         self.ctx = context(device)
         self.device = self.ctx.device
-        du, ku = _host_desc(up, row_begin=row_begin, row_end=row_end)
-        dg, kg = _host_desc(gate, row_begin=row_begin, row_end=row_end)
+        du, ku = _host_desc(up, row_begin=row_begin, row_end=row_end, weights=weights)
+        dg, kg = _host_desc(gate, row_begin=row_begin, row_end=row_end, weights=weights)
         h = C.c_void_p()
         with torch.cuda.device(self.device):
             _lib.check(self._lib.quik_layer_create_gated(self.ctx.handle, C.byref(du), C.byref(dg), C.byref(h)))
@@ -408,6 +416,11 @@ class QuikLinear:
                 self.handle = None
         except Exception:
             pass
+
+    @property
+    def device_bytes(self) -> int:
+        """Device memory this layer holds (C ABI quik_layer_device_bytes)."""
+        return int(self._lib.quik_layer_device_bytes(self.handle))
 
     @property
     def is_sparse(self) -> bool:

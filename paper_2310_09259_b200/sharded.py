@@ -114,7 +114,7 @@ class FusedAllGatherOutput:
     barrier of step i also orders every rank's readers of step i-2's buffer (enqueued
     before step i-1) before step i's writes into it."""
 
-    def __init__(self, M: int, N: int, group=None, device=None, buffers: int = 2):
+    def __init__(self, M: int, N: int, group=None, device=None, buffers: int = 2, barrier_fn=None):
         import ctypes as C
 
         import torch
@@ -154,6 +154,7 @@ class FusedAllGatherOutput:
             self.dests.append(peer_destinations(self.rank, self.world, b.data_ptr(), opened))
         self.flag = torch.zeros(1, dtype=torch.float32, device=dev)
         self.step = 0
+        self._barrier_fn = barrier_fn
 
     def next(self):
         """-> (buffer index, destination pointers) of the next step."""
@@ -164,6 +165,9 @@ class FusedAllGatherOutput:
     def barrier(self):
         """Stream-ordered completion fence: every rank's stores into every buffer are done
         (a one-element all-reduce on the group, after the GEMM in stream order)."""
+        if self._barrier_fn is not None:
+            self._barrier_fn()
+            return
         self.dist.all_reduce(self.flag, group=self.group)
 
     def close(self):
@@ -186,7 +190,7 @@ class FusedShardedQuikLinear:
     of the full [M][N] f16 output (valid on the current stream after the barrier)."""
 
     def __init__(self, layer, max_tokens: int, group=None, device=None, local=None, n_total: int = 0,
-                 barrier: bool = True):
+                 barrier: bool = True, barrier_fn=None):
         """layer: the full QuikLinearLayer (host arrays), or local = this rank's device
         shard (QuikLinear over rows shard_bounds(n_total, world, rank)) + n_total."""
         import torch.distributed as dist
@@ -200,7 +204,7 @@ class FusedShardedQuikLinear:
 
             local = QuikLinear(layer, device=device, row_begin=self.begin, row_end=self.end)
         self.local = local
-        self.out = FusedAllGatherOutput(max_tokens, self.n, group=group, device=local.device)
+        self.out = FusedAllGatherOutput(max_tokens, self.n, group=group, device=local.device, barrier_fn=barrier_fn)
         self.use_barrier = barrier
 
     def forward(self, x):

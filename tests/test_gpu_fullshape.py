@@ -46,7 +46,7 @@ def q():
     return m
 
 
-def device_layer(M, K, N, O, bits, sparse, seed, bias=True):
+def device_layer(M, K, N, O, bits, sparse, seed, bias=True, weights="speed"):
     """Full-size synthetic layer on the device. Returns (QuikLinear, x16 device tensor,
     host dict of the per-row reference-format weights, outlier indices)."""
     import torch
@@ -71,7 +71,7 @@ def device_layer(M, K, N, O, bits, sparse, seed, bias=True):
     base, sc, wr, ow = m.rtn_quantize_weights_device(W, outliers, bits)
     del W
     b = torch.randn(N, generator=g, device=dev) * 0.1 if bias else None
-    layer = m.QuikLinear.from_device(outliers, base, sc, wr, ow, bits, bias=b, sparse=sparse)
+    layer = m.QuikLinear.from_device(outliers, base, sc, wr, ow, bits, bias=b, sparse=sparse, weights=weights)
     if sparse:
         assert layer.is_sparse
     host = dict(base=base.view(N, row_bytes(K - O, bits)), scales=sc, wreduced=wr,
@@ -91,13 +91,24 @@ def subset_layer(host, rows, K, O, bits, idx):
                 idx=np.asarray(idx, np.int64), bias=None if host["bias"] is None else t(host["bias"]))
 
 
-@pytest.mark.parametrize("name,M,K,N,O,bits,sparse", CONFIGS, ids=[c[0] for c in CONFIGS])
+# the INT4-only weight mode (one INT4 device copy, QuikLinear(weights="int4")) at full shape
+INT4_CONFIGS = [(n + "_int4w",) + c[1:] for n, *_ in CONFIGS for c in [next(cc for cc in CONFIGS if cc[0] == n)]
+                if n in ("cfg3_70b_up", "cfg2_7b_qkvo", "cfg4_opt66b_fc1_m256", "cfg4_opt66b_fc1_m16")]
+
+
+@pytest.mark.parametrize("name,M,K,N,O,bits,sparse", CONFIGS + INT4_CONFIGS,
+                         ids=[c[0] for c in CONFIGS + INT4_CONFIGS])
 def test_baseline_config_full_shape(name, M, K, N, O, bits, sparse):
     import torch
 
     m = q()
     o = oracle()
-    layer, x16, host, idx = device_layer(M, K, N, O, bits, sparse, seed=zlib.crc32(name.encode()) & 0xFFFF)
+    weights = "int4" if name.endswith("_int4w") else "speed"
+    layer, x16, host, idx = device_layer(M, K, N, O, bits, sparse, seed=zlib.crc32(name.encode()) & 0xFFFF,
+                                         weights=weights)
+    if weights == "int4":  # one INT4 copy of the base weights (+ f16 outliers, per-row vectors, tables)
+        kpad = (K - O + 127) // 128 * 128
+        assert layer.device_bytes < N * kpad // 2 + N * ((O + 63) // 64 * 64) * 2 + 16 * N + 64 * K
     y16 = layer(x16)                                   # the benched path: f16 in, f16 out
     y32 = layer(x16, out_dtype=torch.float32)
     torch.cuda.synchronize()

@@ -1456,3 +1456,53 @@ def test_reserve_then_capture_and_numerics_flag():
         dev.check_numerics()
     dev(xt)
     dev.check_numerics()  # cleared by the previous check
+
+
+# --------------------------------------------------------------------------- INT4-only weight mode
+
+
+@pytest.mark.parametrize("cg,bn", [(0, 0), (1, 32), (1, 64), (1, 128), (2, 128), (2, 192)])
+def test_int4_weight_mode_bit_identical(tile, cg, bn):
+    """weights="int4" (one INT4 device copy, every GEMM widens INT4 tiles into TMEM, the
+    MMAs sum 16 x the products and the epilogue shifts them back) gives the same bits as
+    the INT8-weight path for every tile, V1 / V2 / V3, f16 and f32 out, ragged shapes,
+    with and without outliers; and holds half the base-weight bytes."""
+    m = q()
+    o = oracle()
+    import torch
+
+    if cg:
+        assert tile(cg, bn) == 0
+    rng = np.random.default_rng(1300 + 10 * cg + bn)
+    for (M, K, N, O) in [(300, 1000, 520, 24), (37, 2048, 384, 0), (513, 640, 1000, 64), (129, 4100, 257, 256)]:
+        L, x, _ = make_layer(rng, M, K, N, 4, O, heavy_cols=2)
+        fast = m.QuikLinear(to_layer(L))
+        small = m.QuikLinear(to_layer(L), weights="int4")
+        xt = torch.from_numpy(x).cuda()
+        for v in m.PipelineVariant:
+            a = fast(xt, out_dtype=torch.float32, variant=v).cpu().numpy()
+            b = small(xt, out_dtype=torch.float32, variant=v).cpu().numpy()
+            np.testing.assert_array_equal(a.view(np.uint32), b.view(np.uint32), err_msg=f"{v} {M} {K} {N} {O}")
+        np.testing.assert_array_equal(fast(xt.half()).cpu().numpy().view(np.uint16),
+                                      small(xt.half()).cpu().numpy().view(np.uint16))
+        if O == 0:
+            st, want = o.quik_matmul(L, x, 2)
+            got = small(xt, out_dtype=torch.float32).cpu().numpy()
+            np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+        kpad = (K - O + 127) // 128 * 128
+        assert fast.device_bytes - small.device_bytes >= N * kpad // 2  # the INT8 copy is gone
+
+
+def test_int4_weight_mode_gated_and_decode():
+    """INT4-only layers through the gated projection and the decode kernel (M <= 32)."""
+    m = q()
+    import torch
+
+    rng = np.random.default_rng(1350)
+    up, gate, down, x = _mlp_layers(rng, 200, 512, 256, 4, 8, 32, 16)
+    a = m.QuikLinear.gated(to_layer(up), to_layer(gate))
+    b = m.QuikLinear.gated(to_layer(up), to_layer(gate), weights="int4")
+    xt = torch.from_numpy(x).cuda()
+    for M in (200, 16, 1):
+        np.testing.assert_array_equal(a(xt[:M], out_dtype=torch.float32).cpu().numpy().view(np.uint32),
+                                      b(xt[:M], out_dtype=torch.float32).cpu().numpy().view(np.uint32))

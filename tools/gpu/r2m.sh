@@ -1,0 +1,9 @@
+mkdir -p gpurun_out
+timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "every_tile or large_layer or stream_gemm or cfg1 or variants" 2>&1 | tail -3 > gpurun_out/r2m.txt
+for c in "--M 4096 --K 8192 --N 28672 --O 256" "--M 128 --K 9216 --N 36864 --O 256" "--M 2048 --K 4096 --N 4096 --O 256"; do
+  echo "== $c" >> gpurun_out/r2m.txt
+  timeout 120 python tools/gemm_case.py $c >> gpurun_out/r2m.txt 2>&1
+  QUIK_GEMM_TRACE=/tmp/tr.bin timeout 120 python tools/gemm_case.py $c --once >> gpurun_out/r2m.txt 2>&1
+  python tools/trace_view.py /tmp/tr.bin 2>&1 | grep "clk\|wait\|span" >> gpurun_out/r2m.txt
+done
+cat gpurun_out/r2m.txt

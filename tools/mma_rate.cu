@@ -12,7 +12,7 @@
 
 using namespace quikb200;
 
-template <int CG, int N, bool SP, int CP = 0>
+template <int CG, int N, bool SP, int CP = 0, bool TS = false>
 __global__ void __launch_bounds__(128, 1) rate_kernel(int iters, unsigned long long* cycles) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(128, 1) rate_kernel(int iters, unsigned long l
           }
         }
         if constexpr (SP) mma_sp_i8<CG>(tbase, ad + 2 * (k & 3), bd + 4 * (k & 1), idesc, tek + 2 * (k & 3), 1u);
+        else if constexpr (TS) mma_i8_ts<CG>(tbase, tbase + 256 + 8 * (k & 3), bd + 2 * (k & 3), idesc, 1u);
         else mma_i8<CG>(tbase, ad + 2 * (k & 3), bd + 2 * (k & 3), idesc, 1u);
       }
     }
@@ -68,9 +69,9 @@ __global__ void __launch_bounds__(128, 1) rate_kernel(int iters, unsigned long l
   }
 }
 
-template <int CG, int N, bool SP, int CP = 0>
+template <int CG, int N, bool SP, int CP = 0, bool TS = false>
 void run(int sms) {
-  auto k = rate_kernel<CG, N, SP, CP>;
+  auto k = rate_kernel<CG, N, SP, CP, TS>;
   const int smem = 64 * 1024 + 1024;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   unsigned long long* dc;
@@ -102,8 +103,8 @@ void run(int sms) {
   const double kl = SP ? 64 : 32;  // logical K per instruction
   const double macs_per_sm = double(iters) * 8 * 128 * N * kl;  // per CTA: M rows = 128 per CTA
   const double tops = 2.0 * macs_per_sm * (sms / CG * CG) / (ms * 1e-3) / 1e12;
-  printf("cta_group::%d N=%3d %-6s cp=%d : %s  %.3f ms  %.0f TOPS (dense-equivalent)  %.0f MAC/clk/SM\n", CG, N,
-         SP ? "sparse" : "dense", CP, e == cudaSuccess ? "ok " : cudaGetErrorString(e), ms, tops, macs_per_sm / cyc);
+  printf("cta_group::%d N=%3d %-6s%s cp=%d : %s  %.3f ms  %.0f TOPS (dense-equivalent)  %.0f MAC/clk/SM\n", CG, N,
+         SP ? "sparse" : "dense", TS ? " A=TMEM" : "", CP, e == cudaSuccess ? "ok " : cudaGetErrorString(e), ms, tops, macs_per_sm / cyc);
   cudaFree(dc);
 }
 
@@ -122,5 +123,13 @@ int main() {
   run<2, 192, true, 1>(sms);
   run<2, 192, true, 2>(sms);
   run<1, 128, true, 1>(sms);
+  // A operand from TMEM (the INT4-weight GEMM): kind::i8 .ts vs .ss
+  run<1, 64, false, 0, true>(sms);
+  run<1, 128, false, 0, true>(sms);
+  run<1, 256, false, 0, true>(sms);
+  run<2, 128, false, 0, true>(sms);
+  run<2, 192, false, 0, true>(sms);
+  run<2, 192, false>(sms);
+  run<2, 256, false, 0, true>(sms);
   return 0;
 }
