@@ -347,6 +347,16 @@ def run_ours(args, w):
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
+    def max_over_ranks(t):
+        """In-place max over the ranks (device tensor with NCCL, through host memory with
+        the gloo check backend)."""
+        if backend == "nccl":
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        else:
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.MAX)
+            t.copy_(h)
+
     M, K, N, O, bits = w["M"], w["K"], w["N"], w["O"], w["bits"]
     if N % world:
         raise SystemExit(f"out_features {N} not divisible by {world} GPUs")
@@ -503,7 +513,7 @@ def run_ours(args, w):
             b.record()
             torch.cuda.synchronize()
             t = torch.tensor([a.elapsed_time(b) / steps], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            max_over_ranks(t)
             return float(t.item())
 
         exchange = dict(headline="fused all-gather (CUDA IPC peer stores in the GEMM epilogue + NCCL fence)"
@@ -529,7 +539,7 @@ def run_ours(args, w):
         torch.cuda.synchronize()
         ts = torch.tensor([s0.elapsed_time(s1) / n_sus], device=dev, dtype=torch.float64)
         if world > 1:
-            dist.all_reduce(ts, op=dist.ReduceOp.MAX)
+            max_over_ranks(ts)
         ts = float(ts.item())
         sustained = dict(value=2.0 * M * N * K / (ts * 1e-3) / 1e12, unit="TOPS", ms_per_step=ts, steps=n_sus,
                          note="same step repeated back to back for --soak-s seconds after the timed region")
@@ -539,7 +549,7 @@ def run_ours(args, w):
                           statistics.median(quant_ms), statistics.mean(gemm_ms), statistics.mean(quant_ms)],
                          device=dev, dtype=torch.float64)
     if world > 1:
-        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+        max_over_ranks(stats)
     total_ms, step_med, gemm_med, quant_med, gemm_mean, quant_mean = stats.tolist()
     ms_per_step = total_ms / steps
     ops = 2.0 * M * N * K
@@ -580,7 +590,12 @@ def run_ours(args, w):
                                 f"{' x2 for 2:4 sparse' if sparse else ''} for the {kb} int columns (dense-equivalent "
                                 "ops); mixed peak = ops / (int_ops/P_i8 + f16_ops/P_f16); achieved from the median "
                                 "GEMM launch (CUDA events on the launch stream)"),
-                    int8_peak_cublaslt_tops=i8_live, int8_only_frac=achieved / p_i8)
+                    int8_peak_cublaslt_tops=i8_live, int8_only_frac=achieved / p_i8,
+                    nominal_frac=achieved / (ops_rank / (2.0 * M * ns * kb / ((9000.0 if sparse else 4500.0) * 1e12)
+                                                         + 2.0 * M * ns * O / (2250.0 * 1e12)) / 1e12),
+                    note="denominators are a cuBLAS-derived measured peak (a kernel can read a little above 1.0, "
+                         "B200_PROFILING.md); nominal_frac is against the nominal dense 4.5 POPS int8 / 2.25 PFLOPS "
+                         "f16 at the boost clock")
     # K1 algorithmic bytes per SURVEY.md §8(d): x f16 in, the codes at the reference's
     # width (INT4: ceil(K_b/2) per token), x_outlier f16, scale + zero
     bytes_q = M * K * 2 + M * a_bytes(kb) + M * O * 2 + 8 * M
@@ -609,7 +624,7 @@ def run_ours(args, w):
         t16s = [a.elapsed_time(b) for a, b in ev_step]
         t16 = torch.tensor([statistics.median(t16s)], device=dev, dtype=torch.float64)
         if world > 1:
-            dist.all_reduce(t16, op=dist.ReduceOp.MAX)
+            max_over_ranks(t16)
         t16 = float(t16.item())
         fp16 = dict(ms_median=t16, tflops=2.0 * M * ns * K / (t16 * 1e-3) / 1e12, speedup_step=t16 / step_med,
                     speedup_gemm=t16 / gemm_med,
@@ -652,7 +667,7 @@ def run_ours(args, w):
         torch.cuda.synchronize()
         te = torch.tensor([a.elapsed_time(b) / e2e_steps], device=dev, dtype=torch.float64)
         if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            max_over_ranks(te)
         te = float(te.item())
         e2e = dict(value=ops / (te * 1e-3) / 1e12, unit="TOPS", h2d_bytes_per_step=M * K * 2 * world,
                    d2h_bytes_per_step=M * N * 2, ms_per_step=te, steps=e2e_steps,
