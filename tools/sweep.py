@@ -50,6 +50,9 @@ def timeit(fn, iters=20, warm=5):
     return a.elapsed_time(b) / iters
 
 
+WEIGHTS = "speed"
+
+
 def run(name, M, K, N, O, bits, layers, sparse=False):
     dev = torch.device("cuda", 0)
     key = (K, N, O, bits, sparse)
@@ -66,7 +69,7 @@ def run(name, M, K, N, O, bits, layers, sparse=False):
             prune_24(W, torch.as_tensor(outl.permutation[: K - O], device=dev))
         base, sc, wr, ow = q.rtn_quantize_weights_device(W, outl, bits)
         del W
-        layers[key] = (q.QuikLinear.from_device(outl, base, sc, wr, ow, bits, sparse=sparse),
+        layers[key] = (q.QuikLinear.from_device(outl, base, sc, wr, ow, bits, sparse=sparse, weights=WEIGHTS),
                        torch.randn(N, K, device=dev, dtype=torch.float16))
     layer, W16 = layers[key]
     x = torch.randn(M, K, device=dev, dtype=torch.float16)
@@ -94,7 +97,8 @@ def run(name, M, K, N, O, bits, layers, sparse=False):
         torch.matmul(x, W16.t(), out=out16)
     t16 = timeit(g16.replay)
     ops = 2.0 * M * N * K
-    return dict(name=name, M=M, K=K, N=N, O=O, bits=bits, sparse=layer.is_sparse, step_ms=t_step, step_eager_ms=t_step_eager,
+    return dict(name=name, M=M, K=K, N=N, O=O, bits=bits, sparse=layer.is_sparse, weights=WEIGHTS,
+                layer_mb=layer.device_bytes / 1e6, step_ms=t_step, step_eager_ms=t_step_eager,
                 k1_ms=t_k1, gemm_ms=t_gemm,
                 tops=ops / t_step / 1e9, cublas_f16_ms=t16, speedup_vs_f16=t16 / t_step)
 
@@ -105,7 +109,11 @@ def main():
     ap.add_argument("--only", default="")
     ap.add_argument("--opt-m", default="", help="comma list of OPT fc1 token counts (default: all)")
     ap.add_argument("--falcon", action="store_true", help="also the Falcon-180B fc1 token sweep")
+    ap.add_argument("--weights", default="speed", choices=["speed", "int4"],
+                    help="device copy of 4-bit weights (QuikLinear weights=)")
     args = ap.parse_args()
+    global WEIGHTS
+    WEIGHTS = args.weights
     layers = {}
     res = []
     for s in SHAPES:
