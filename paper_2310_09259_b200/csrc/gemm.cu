@@ -571,10 +571,15 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
         if (++stage == C::kStages) { stage = 0; phase ^= 1; }
       };
       uint32_t meta_slot = 0;
+      int mit = 0;
       auto int_blocks = [&](uint32_t d, int k0, int k1) {
         for (int kb = k0; kb < k1; ++kb) {
+          long long* ms = (p.trace && cluster_id == 0 && mit < 128 && lane == 0) ? g_wstamps + mit * 8 : nullptr;
+          ++mit;
+          if (ms) ms[0] = clock64();
           uint64_t ad, bd;
           next_stage(ad, bd);
+          if (ms) { ms[1] = clock64(); ms[2] = ms[1]; }
           if constexpr (!SP) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)  // 4 x K=32 int8 = 128 bytes
@@ -592,7 +597,9 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
               mma_sp_i8_w<CG>(d, ad + 2 * k, (k < 2 ? bd : bd1) + 4 * (k & 1), id_sp, te + 2 * k, (kb | k) != 0);
             if (++meta_slot == kMetaSlots) meta_slot = 0;
           }
+          if (ms) ms[3] = clock64();
           release_stage();
+          if (ms) ms[4] = clock64();
         }
       };
       auto out_blocks = [&](int it_prev) {
