@@ -89,8 +89,8 @@ struct Cfg {
   // ring (released by the widening warps as soon as they have read a tile, so the HBM
   // weight stream is not held up by the MMAs) and the f16 outlier-weight tiles a two-slot
   // ring of their own.
-  static constexpr int kStageBytes = W4 ? kBBytes : kABytes + kBBytes + kMetaBytes;
-  static constexpr int kA4Slots = 10;
+  static constexpr int kStageBytes = W4 ? 2 * kBBytes : kABytes + kBBytes + kMetaBytes;  // W4: a k-block pair
+  static constexpr int kA4Slots = 8;
   static constexpr int kOASlots = 2;
   static constexpr int kRingFixed = W4 ? kOASlots * kABytes + kA4Slots * kA4Bytes : 0;
   static constexpr int kBudget = 227 * 1024 - 1024 - kStagingBytes - 1024 - kRingFixed;
@@ -104,6 +104,7 @@ struct Cfg {
   // reused only after the MMAs that read it completed, so the ring depth has to cover the
   // widen -> MMA -> commit round trip
   static constexpr int kAStages = (512 - kAccCols) / 32 > kAStagesMax ? kAStagesMax : (512 - kAccCols) / 32;
+  static constexpr int kAPairs = kAStages / 2;  // W4: the ring is used in 64-column k-block pairs
   static constexpr int kTmemNeed = kAccCols + (SP ? 8 * kMetaSlots : 0) + (W4 ? 32 * kAStages : 0);
   static constexpr int kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128
                                  : kTmemNeed <= 256 ? 256 : 512;
@@ -225,7 +226,8 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
   const bool two_phase = kb_out > 0;
   // int k-blocks of tile i issued before the outlier MMAs of tile i-1: the epilogue's
   // in-place dequantisation of tile i-1 must finish within them (p.split_num / 8)
-  const int h_a = (kb_int * p.split_num) >> 3;
+  // (W4: even, the integer k-blocks go in pairs)
+  const int h_a = W4 ? (((kb_int * p.split_num) >> 3) & ~1) : ((kb_int * p.split_num) >> 3);
 
   if (warp == 0 && lane == 0) {
     if (kb_int) { tma_prefetch(&p.tm_w); tma_prefetch(&p.tm_x); }
@@ -244,7 +246,7 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
     if (W4) {
       for (int i = 0; i < C::kA4Slots; ++i) { mbar_init(&full4[i], 1); mbar_init(&empty4[i], 4); }
       for (int i = 0; i < C::kOASlots; ++i) mbar_init(&emptyo[i], 1);
-      for (int i = 0; i < C::kAStages; ++i) { mbar_init(&ready[i], 4 * CG); mbar_init(&aempty[i], 1); }
+      for (int i = 0; i < C::kAPairs; ++i) { mbar_init(&ready[i], 4 * CG); mbar_init(&aempty[i], 1); }
     }
     fence_mbar_init();
   }
@@ -310,11 +312,14 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
         if constexpr (CG == 1) tma_load_2d(dst, m, c0, c1, bar, pol);
         else tma_load_2d_pair(dst, m, c0, c1, bar, pol);
       };
-      // activation codes of k-block kb -> the main ring
-      auto load_b = [&](int kb, int trow) {
+      // activation codes of the k-block pair (kb, kb + 1 < k_end) -> one main-ring stage
+      auto load_b = [&](int kb, int k_end, int trow) {
+        const int n = kb + 1 < k_end ? 2 : 1;
         mbar_wait(&empty[b], bph ^ 1);
-        if (leader) mbar_arrive_expect_tx(&full[b], CG * C::kBBytes);
-        tma_pair(smem + b * C::kStageBytes, &p.tm_x, kb * kKBlockBytes, trow, &full[b], pol_x);
+        if (leader) mbar_arrive_expect_tx(&full[b], CG * n * C::kBBytes);
+        for (int i = 0; i < n; ++i)
+          tma_pair(smem + b * C::kStageBytes + i * C::kBBytes, &p.tm_x, (kb + i) * kKBlockBytes, trow, &full[b],
+                   pol_x);
         if (++b == C::kStages) { b = 0; bph ^= 1; }
       };
       // outlier block ko: f16 weight tile -> outlier ring, f16 activations -> main ring,
@@ -340,13 +345,13 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
         int wr, tr;
         rows_of(tile, wr, tr);
         if (tile + num_clusters >= num_tiles) asm volatile("griddepcontrol.launch_dependents;");
-        for (int kb = 0; kb < h_a; ++kb) load_b(kb, tr);
+        for (int kb = 0; kb < h_a; kb += 2) load_b(kb, h_a, tr);
         if (two_phase && prev >= 0) {
           int pw, pt;
           rows_of(prev, pw, pt);
           for (int ko = 0; ko < kb_out; ++ko) load_out(ko, pw, pt);
         }
-        for (int kb = h_a; kb < kb_int; ++kb) load_b(kb, tr);
+        for (int kb = h_a; kb < kb_int; kb += 2) load_b(kb, kb_int, tr);
         prev = tile;
       }
       if (two_phase && prev >= 0) {
@@ -368,30 +373,36 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
       uint32_t bph = 0, aph = 0;
       long long full_wait = 0, ready_wait = 0;
       int mit = 0;
+      // k-block pairs: one activation-stage check, one widened-slot check, 8 MMAs and two
+      // commits per pair (the per-k-block synchronisation is what bounds the MMA warp)
       auto int_blocks = [&](uint32_t d, int k0, int k1) {
-        for (int kb = k0; kb < k1; ++kb) {
+        for (int kb = k0; kb < k1; kb += 2) {
+          const int n = kb + 1 < k1 ? 2 : 1;
           long long* ms = (p.trace && cluster_id == 0 && mit < 128 && lane == 0) ? g_wstamps + mit * 8 : nullptr;
           ++mit;
           if (ms) ms[0] = clock64();
-          const long long t0 = p.trace ? gtime() : 0;
           mbar_wait(&full[b], bph);
           if (ms) ms[1] = clock64();
-          const long long t1 = p.trace ? gtime() : 0;
           mbar_wait(&ready[aslot], aph);
           if (ms) ms[2] = clock64();
-          if (p.trace) { full_wait += t1 - t0; ready_wait += gtime() - t1; }
           tc_fence_after();
           const uint64_t bd = umma_desc_sw128(smem_u32(smem + b * C::kStageBytes));
-          const uint32_t a_tm = tmem_base + C::kACol + aslot * 32;  // both CTAs widened their rows here
+          const uint32_t a_tm = tmem_base + C::kACol + aslot * 64;  // both CTAs widened their rows here
 #pragma unroll
-          for (int k = 0; k < 4; ++k)  // 4 x K=32 int8 = 32 TMEM columns of A, 128 bytes of B
-            mma_i8_ts_w<CG>(d, a_tm + 8 * k, bd + 2 * k, id_i8, (kb | k) != 0);
+          for (int i = 0; i < 2; ++i) {
+            if (i < n) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k)  // 4 x K=32 int8 = 32 TMEM columns of A, 128 bytes of B
+                mma_i8_ts_w<CG>(d, a_tm + 32 * i + 8 * k, bd + ((i * C::kBBytes) >> 4) + 2 * k, id_i8,
+                                ((kb + i) | k) != 0);
+            }
+          }
           if (ms) ms[3] = clock64();
           mma_commit_w<CG>(&empty[b], static_cast<uint16_t>(3));
           mma_commit_w<CG>(&aempty[aslot], static_cast<uint16_t>(3));
           if (ms) ms[4] = clock64();
           if (++b == C::kStages) { b = 0; bph ^= 1; }
-          if (++aslot == C::kAStages) { aslot = 0; aph ^= 1; }
+          if (++aslot == C::kAPairs) { aslot = 0; aph ^= 1; }
         }
       };
       auto out_blocks = [&](int it_prev) {
@@ -554,13 +565,7 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
       uint32_t phase = 0;
       long long full_wait = 0;
       auto next_stage = [&](uint64_t& adesc, uint64_t& bdesc) {
-        if (p.trace) {
-          const long long t0 = gtime();
-          mbar_wait(&full[stage], phase);
-          full_wait += gtime() - t0;
-        } else {
-          mbar_wait(&full[stage], phase);
-        }
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
         adesc = umma_desc_sw128(sa);
@@ -645,20 +650,17 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
     // so the 8 rows of a quarter warp read 8 distinct bank groups. Byte i of chunk c
     // holds k = 32c + i (low nibble) and 32c + 16 + i (high nibble): word w of the chunk
     // widens to TMEM columns 8c + w (low) and 8c + 4 + w (high).
-    // Two groups of four warps (one per TMEM lane quadrant each) take alternate PAIRS of
-    // the CTA's integer k-blocks (one continuous sequence over its tiles): the ring
-    // positions of k-block j follow from j (INT4 slot j % kA4Slots, TMEM slot j % kAStages,
-    // parities from the wrap counts), so the groups need no shared state; each widens
-    // two k-blocks per iteration with one store wait / fence.
+    // Two groups of four warps (one per TMEM lane quadrant each) take alternate k-block
+    // PAIRS; ring positions follow from the pair / k-block index (INT4 slot j % kA4Slots,
+    // TMEM pair slot p % kAPairs, parities from the wrap counts), so the groups share no
+    // state; each pair is one aempty check, two widened stores, one store wait / fence
+    // and one ready arrival.
     const int q = warp & 3;
     const int g = (warp - kWidenWarp0) >> 2;
     const int r = q * 32 + lane;
     const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + C::kACol;
     const int swz = (r >> 1) & 3;
     const bool tw = p.trace && leader && warp == kWidenWarp0 && lane == 0;
-    int my_tiles = 0;
-    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) ++my_tiles;
-    const long long J = static_cast<long long>(my_tiles) * kb_int;
     // Widening as 16 x the value: the nibble moved to the HIGH half of its byte is the
     // int8 16 * v (two's complement), one or two logic ops per word instead of a
     // sign extension; the MMA sums 16 * (w * a) exactly (|acc| <= 16 * 64 * K_b < 2^31)
@@ -680,7 +682,7 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty4[j % C::kA4Slots]);
     };
-    // one k-block: 16 INT4 words -> 32 TMEM columns of 16 x the int8 codes
+    // one k-block: 16 INT4 words -> 32 TMEM columns (slot j) of 16 x the int8 codes
     auto widen_store = [&](const uint4 (&win)[4], long long j) {
       uint32_t v[32];
 #pragma unroll
@@ -692,29 +694,29 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
           v[8 * c + 4 + w] = x & 0xF0F0F0F0u;     // k = 32c + 16 + 4w .. (high nibbles) x 16
         }
       }
-      if (!(p.dbg & 8)) tmem_st32(trow + static_cast<uint32_t>(j % C::kAStages) * 32, v);
+      if (!(p.dbg & 8)) tmem_st32(trow + static_cast<uint32_t>(j) * 32, v);  // j: TMEM 32-column slot
     };
-    auto slot_free = [&](long long j) {  // the MMAs that read this TMEM slot are done
-      mbar_wait(&aempty[j % C::kAStages], static_cast<uint32_t>(((j / C::kAStages) & 1) ^ 1));
-    };
+    // the k-block pairs of each tile, in the MMA warp's order: [0, h_a) then [h_a, kb_int)
+    // (h_a even); pair p goes to group p % 2 and TMEM pair slot p % kAPairs; k-block j of
+    // the CTA's sequence sits in INT4 slot j % kA4Slots
+    long long p_idx = 0, j_base = 0;
     int wit = 0;
-    for (long long j0 = 2LL * g; j0 < J; j0 += 2LL * kWidenGroups) {
+    auto do_pair = [&](long long j0, int n, long long pp) {
       long long* ws = (tw && cluster_id == 0 && wit < 128) ? g_wstamps + 128 * 8 + wit * 8 : nullptr;
       ++wit;
       if (ws) ws[0] = clock64();
-      const bool two = j0 + 1 < J;
       uint4 wa[4], wb[4];
       load_tile(j0, wa);
-      if (two) load_tile(j0 + 1, wb);
+      if (n > 1) load_tile(j0 + 1, wb);
       if (ws) ws[1] = clock64();
-      slot_free(j0);
-      if (two) slot_free(j0 + 1);
+      const int ps = static_cast<int>(pp % C::kAPairs);
+      mbar_wait(&aempty[ps], static_cast<uint32_t>(((pp / C::kAPairs) & 1) ^ 1));  // MMAs of its last use done
       if (ws) ws[2] = clock64();
       tc_fence_after();
-      widen_store(wa, j0);
+      widen_store(wa, 2LL * ps);
       release_tile(j0);
-      if (two) {
-        widen_store(wb, j0 + 1);
+      if (n > 1) {
+        widen_store(wb, 2LL * ps + 1);
         release_tile(j0 + 1);
       }
       if (ws) ws[3] = clock64();
@@ -722,11 +724,16 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
       tc_fence_before();
       __syncwarp();
       if (ws) ws[4] = clock64();
-      if (lane == 0) {
-        arrive_leader<CG>(&ready[j0 % C::kAStages], leader_rank);
-        if (two) arrive_leader<CG>(&ready[(j0 + 1) % C::kAStages], leader_rank);
-      }
+      if (lane == 0) arrive_leader<CG>(&ready[ps], leader_rank);
       if (ws) ws[5] = clock64();
+    };
+    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+      for (int run = 0; run < 2; ++run) {
+        const int k0 = run ? h_a : 0, k1 = run ? kb_int : h_a;
+        for (int kb = k0; kb < k1; kb += 2, ++p_idx)
+          if ((p_idx & 1) == g) do_pair(j_base + kb, kb + 1 < k1 ? 2 : 1, p_idx);
+      }
+      j_base += kb_int;
     }
   } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
     if constexpr (kEarlyW || W4) asm volatile("griddepcontrol.wait;" ::: "memory");  // per-token scales, acc_in
