@@ -90,9 +90,9 @@ struct Cfg {
   // weight stream is not held up by the MMAs) and the f16 outlier-weight tiles a two-slot
   // ring of their own.
   static constexpr int kStageBytes = W4 ? 2 * kBBytes : kABytes + kBBytes + kMetaBytes;  // W4: a k-block pair
-  static constexpr int kA4Slots = 8;
+  static constexpr int kA4Slots = 4;  // W4: INT4 ring slots of one k-block PAIR (2 x 8 KB) each
   static constexpr int kOASlots = 2;
-  static constexpr int kRingFixed = W4 ? kOASlots * kABytes + kA4Slots * kA4Bytes : 0;
+  static constexpr int kRingFixed = W4 ? kOASlots * kABytes + kA4Slots * 2 * kA4Bytes : 0;
   static constexpr int kBudget = 227 * 1024 - 1024 - kStagingBytes - 1024 - kRingFixed;
   static constexpr int kStages = (kBudget / kStageBytes) > 8 ? 8 : (kBudget / kStageBytes);
   static constexpr int kOAOff = kStages * kStageBytes;             // W4: outlier-weight ring
@@ -205,8 +205,8 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
   uint64_t* tconv = tint + 2;           // [2] init written into TMEM          (epilogue -> MMA)
   uint64_t* tfin = tconv + 2;           // [2] outlier MMAs done, tile final   (MMA -> epilogue)
   uint64_t* tempty = tfin + 2;          // [2] accumulator buffer drained      (epilogue -> MMA)
-  uint64_t* full4 = tempty + 2;          // [kA4Slots] W4: this CTA's INT4 tile landed (TMA -> widen)
-  uint64_t* empty4 = full4 + C::kA4Slots; // [kA4Slots] W4: INT4 tile read (widen -> producer)
+  uint64_t* full4 = tempty + 2;          // [kA4Slots] W4: this CTA's INT4 pair landed (TMA -> widen)
+  uint64_t* empty4 = full4 + C::kA4Slots; // [kA4Slots] W4: INT4 pair read (widen -> producer)
   uint64_t* emptyo = empty4 + C::kA4Slots; // [kOASlots] W4: outlier-weight tile consumed (MMA -> producer)
   uint64_t* ready = emptyo + C::kOASlots; // [kAStages] W4: TMEM A slot widened, both CTAs (widen -> MMA)
   uint64_t* aempty = ready + kAStagesMax; // [kAStages] W4: TMEM A slot consumed (MMA -> widen)
@@ -291,11 +291,17 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
         int nb, mb;
         decode(tile, nb, mb);
         const int wr = nb * C::kTileRows + static_cast<int>(rank) * kBlockM;
-        for (int kb = 0; kb < kb_int; ++kb) {
-          mbar_wait(&empty4[a4], aph ^ 1);
-          mbar_arrive_expect_tx(&full4[a4], kA4Bytes);
-          tma_load_2d(smem + C::kA4Off + a4 * kA4Bytes, &p.tm_w4, kb * (kKBlockBytes / 2), wr, &full4[a4], pol_w);
-          if (++a4 == C::kA4Slots) { a4 = 0; aph ^= 1; }
+        for (int run = 0; run < 2; ++run) {  // the k-block pairs in the MMA warp's order
+          const int k0 = run ? h_a : 0, k1 = run ? kb_int : h_a;
+          for (int kb = k0; kb < k1; kb += 2) {
+            const int n = kb + 1 < k1 ? 2 : 1;
+            mbar_wait(&empty4[a4], aph ^ 1);
+            mbar_arrive_expect_tx(&full4[a4], n * kA4Bytes);
+            for (int i = 0; i < n; ++i)
+              tma_load_2d(smem + C::kA4Off + (2 * a4 + i) * kA4Bytes, &p.tm_w4, (kb + i) * (kKBlockBytes / 2), wr,
+                          &full4[a4], pol_w);
+            if (++a4 == C::kA4Slots) { a4 = 0; aph ^= 1; }
+          }
         }
       }
     }
@@ -651,7 +657,7 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
     // holds k = 32c + i (low nibble) and 32c + 16 + i (high nibble): word w of the chunk
     // widens to TMEM columns 8c + w (low) and 8c + 4 + w (high).
     // Two groups of four warps (one per TMEM lane quadrant each) take alternate k-block
-    // PAIRS; ring positions follow from the pair / k-block index (INT4 slot j % kA4Slots,
+    // PAIRS; ring positions follow from the pair index p (INT4 pair slot p % kA4Slots,
     // TMEM pair slot p % kAPairs, parities from the wrap counts), so the groups share no
     // state; each pair is one aempty check, two widened stores, one store wait / fence
     // and one ready arrival.
@@ -665,10 +671,9 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
     // int8 16 * v (two's complement), one or two logic ops per word instead of a
     // sign extension; the MMA sums 16 * (w * a) exactly (|acc| <= 16 * 64 * K_b < 2^31)
     // and the epilogue shifts the accumulator right by 4 (exact).
-    auto load_tile = [&](long long j, uint4 (&win)[4]) {
-      const int sl = static_cast<int>(j % C::kA4Slots);
-      mbar_wait(&full4[sl], static_cast<uint32_t>((j / C::kA4Slots) & 1));
-      const uint8_t* row = smem + C::kA4Off + sl * kA4Bytes + r * (kKBlockBytes / 2);
+    // k-block i (0 / 1) of the pair in INT4 pair slot `sl` (its full4 already waited for)
+    auto load_tile = [&](int sl, int i, uint4 (&win)[4]) {
+      const uint8_t* row = smem + C::kA4Off + (2 * sl + i) * kA4Bytes + r * (kKBlockBytes / 2);
       if (p.dbg & 16) {  // diagnostics: no shared-memory reads
 #pragma unroll
         for (int c = 0; c < 4; ++c) win[c] = make_uint4(r, c, 3, 4);
@@ -677,10 +682,10 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
         for (int c = 0; c < 4; ++c) win[c] = *reinterpret_cast<const uint4*>(row + ((c ^ swz) << 4));
       }
     };
-    // the INT4 tile is in registers (its values consumed): hand the slot back to the producer
-    auto release_tile = [&](long long j) {
+    // the INT4 pair is in registers (its values consumed): hand the slot back to the producer
+    auto release_tile = [&](int sl) {
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty4[j % C::kA4Slots]);
+      if (lane == 0) mbar_arrive(&empty4[sl]);
     };
     // one k-block: 16 INT4 words -> 32 TMEM columns (slot j) of 16 x the int8 codes
     auto widen_store = [&](const uint4 (&win)[4], long long j) {
@@ -699,26 +704,25 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
     // the k-block pairs of each tile, in the MMA warp's order: [0, h_a) then [h_a, kb_int)
     // (h_a even); pair p goes to group p % 2 and TMEM pair slot p % kAPairs; k-block j of
     // the CTA's sequence sits in INT4 slot j % kA4Slots
-    long long p_idx = 0, j_base = 0;
+    long long p_idx = 0;
     int wit = 0;
-    auto do_pair = [&](long long j0, int n, long long pp) {
+    auto do_pair = [&](int n, long long pp) {
       long long* ws = (tw && cluster_id == 0 && wit < 128) ? g_wstamps + 128 * 8 + wit * 8 : nullptr;
       ++wit;
       if (ws) ws[0] = clock64();
+      const int sl = static_cast<int>(pp % C::kA4Slots);
+      mbar_wait(&full4[sl], static_cast<uint32_t>((pp / C::kA4Slots) & 1));
       uint4 wa[4], wb[4];
-      load_tile(j0, wa);
-      if (n > 1) load_tile(j0 + 1, wb);
+      load_tile(sl, 0, wa);
+      if (n > 1) load_tile(sl, 1, wb);
       if (ws) ws[1] = clock64();
       const int ps = static_cast<int>(pp % C::kAPairs);
       mbar_wait(&aempty[ps], static_cast<uint32_t>(((pp / C::kAPairs) & 1) ^ 1));  // MMAs of its last use done
       if (ws) ws[2] = clock64();
       tc_fence_after();
       widen_store(wa, 2LL * ps);
-      release_tile(j0);
-      if (n > 1) {
-        widen_store(wb, 2LL * ps + 1);
-        release_tile(j0 + 1);
-      }
+      if (n > 1) widen_store(wb, 2LL * ps + 1);
+      release_tile(sl);
       if (ws) ws[3] = clock64();
       if (!(p.dbg & 2)) tmem_st_wait();
       tc_fence_before();
@@ -731,9 +735,8 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
       for (int run = 0; run < 2; ++run) {
         const int k0 = run ? h_a : 0, k1 = run ? kb_int : h_a;
         for (int kb = k0; kb < k1; kb += 2, ++p_idx)
-          if ((p_idx & 1) == g) do_pair(j_base + kb, kb + 1 < k1 ? 2 : 1, p_idx);
+          if ((p_idx & 1) == g) do_pair(kb + 1 < k1 ? 2 : 1, p_idx);
       }
-      j_base += kb_int;
     }
   } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
     if constexpr (kEarlyW || W4) asm volatile("griddepcontrol.wait;" ::: "memory");  // per-token scales, acc_in
