@@ -13,7 +13,7 @@ if os.path.exists(sys.argv[1] + ".w"):  # W4 clock64 stamps of cluster 0: MMA k-
     m = w[0][w[0][:, 0] > 0]
     if m.size:
         d = np.diff(m[:, :5], axis=1)
-        print("mma k-block (clk): full-wait %.0f  ready-wait %.0f  issue %.0f  commit %.0f  period %.0f (n=%d)"
+        print("mma k-block (clk): [0-1] %.0f  [1-2] %.0f  [2-3] %.0f  [3-4] %.0f  period %.0f (n=%d)"
               % (*np.median(d, axis=0), np.median(np.diff(m[:, 0])), len(m)))
     t = w[1][w[1][:, 0] > 0]
     if t.size:
