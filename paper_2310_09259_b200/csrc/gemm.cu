@@ -380,45 +380,35 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
       long long full_wait = 0, ready_wait = 0;
       int mit = 0;
       // k-block pairs: one activation-stage check, one widened-slot check, 8 MMAs and two
-      // commits per pair (the per-k-block synchronisation is what bounds the MMA warp).
-      // The next pair's two checks are made between this pair's two halves, while four
-      // MMAs are queued on the tensor pipe, so their latency does not idle it.
+      // commits per pair (the per-k-block synchronisation is what bounds the MMA warp)
       auto int_blocks = [&](uint32_t d, int k0, int k1) {
-        if (k0 >= k1) return;
-        mbar_wait(&full[b], bph);
-        mbar_wait(&ready[aslot], aph);
         for (int kb = k0; kb < k1; kb += 2) {
           const int n = kb + 1 < k1 ? 2 : 1;
           long long* ms = (p.trace && cluster_id == 0 && mit < 128 && lane == 0) ? g_wstamps + mit * 8 : nullptr;
           ++mit;
           if (ms) ms[0] = clock64();
+          mbar_wait(&full[b], bph);
+          if (ms) ms[1] = clock64();
+          mbar_wait(&ready[aslot], aph);
+          if (ms) ms[2] = clock64();
           tc_fence_after();
           const uint64_t bd = umma_desc_sw128(smem_u32(smem + b * C::kStageBytes));
           const uint32_t a_tm = tmem_base + C::kACol + aslot * 64;  // both CTAs widened their rows here
 #pragma unroll
-          for (int k = 0; k < 4; ++k)  // 4 x K=32 int8 = 32 TMEM columns of A, 128 bytes of B
-            mma_i8_ts_w<CG>(d, a_tm + 8 * k, bd + 2 * k, id_i8, (kb | k) != 0);
-          if (ms) ms[1] = clock64();
-          int nb = b + 1, na = aslot + 1;
-          uint32_t nbph = bph, naph = aph;
-          if (nb == C::kStages) { nb = 0; nbph ^= 1; }
-          if (na == C::kAPairs) { na = 0; naph ^= 1; }
-          if (kb + 2 < k1) {  // the next pair's activation stage and widened slot
-            mbar_wait(&full[nb], nbph);
-            mbar_wait(&ready[na], naph);
-          }
-          if (ms) ms[2] = clock64();
-          if (n > 1) {
+          for (int i = 0; i < 2; ++i) {
+            if (i < n) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_i8_ts_w<CG>(d, a_tm + 32 + 8 * k, bd + (C::kBBytes >> 4) + 2 * k, id_i8, 1u);
+              for (int k = 0; k < 4; ++k)  // 4 x K=32 int8 = 32 TMEM columns of A, 128 bytes of B
+                mma_i8_ts_w<CG>(d, a_tm + 32 * i + 8 * k, bd + ((i * C::kBBytes) >> 4) + 2 * k, id_i8,
+                                ((kb + i) | k) != 0);
+            }
           }
           if (ms) ms[3] = clock64();
           mma_commit_w<CG>(&empty[b], static_cast<uint16_t>(3));
           mma_commit_w<CG>(&aempty[aslot], static_cast<uint16_t>(3));
           if (ms) ms[4] = clock64();
-          b = nb; bph = nbph;
-          aslot = na; aph = naph;
+          if (++b == C::kStages) { b = 0; bph ^= 1; }
+          if (++aslot == C::kAPairs) { aslot = 0; aph ^= 1; }
         }
       };
       auto out_blocks = [&](int it_prev) {
@@ -593,51 +583,29 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
       };
       uint32_t meta_slot = 0;
       int mit = 0;
-      // The next k-block's stage check is made between this k-block's two halves, while
-      // two MMAs are queued on the tensor pipe (its latency then does not idle the pipe).
       auto int_blocks = [&](uint32_t d, int k0, int k1) {
-        if (k0 >= k1) return;
-        mbar_wait(&full[stage], phase);
         for (int kb = k0; kb < k1; ++kb) {
           long long* ms = (p.trace && cluster_id == 0 && mit < 128 && lane == 0) ? g_wstamps + mit * 8 : nullptr;
           ++mit;
           if (ms) ms[0] = clock64();
-          tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
-          const uint64_t ad = umma_desc_sw128(sa), bd = umma_desc_sw128(sa + C::kABytes);
-          auto look_ahead = [&]() {
-            if (kb + 1 < k1) {
-              const int ns = stage + 1 == C::kStages ? 0 : stage + 1;
-              mbar_wait(&full[ns], stage + 1 == C::kStages ? phase ^ 1 : phase);
-            }
-          };
+          uint64_t ad, bd;
+          next_stage(ad, bd);
+          if (ms) { ms[1] = clock64(); ms[2] = ms[1]; }
           if constexpr (!SP) {
 #pragma unroll
-            for (int k = 0; k < 2; ++k)  // 4 x K=32 int8 = 128 bytes
+            for (int k = 0; k < 4; ++k)  // 4 x K=32 int8 = 128 bytes
               mma_i8_w<CG>(d, ad + 2 * k, bd + 2 * k, id_i8, (kb | k) != 0);
-            if (ms) ms[1] = clock64();
-            look_ahead();
-            if (ms) ms[2] = clock64();
-#pragma unroll
-            for (int k = 2; k < 4; ++k)
-              mma_i8_w<CG>(d, ad + 2 * k, bd + 2 * k, id_i8, 1u);
           } else {
             // metadata tile -> TMEM ring slot (two 128 x 128-bit copies), then 4 sparse
             // MMAs of 64 logical K: A advances 32 compressed bytes, B 64 bytes (two atoms)
             const uint32_t te = tmem_base + C::kMetaCol + meta_slot * 8;
-            const uint32_t se = sa + C::kABytes + C::kBBytes;
+            const uint32_t se = smem_u32(smem + stage * C::kStageBytes + C::kABytes + C::kBBytes);
             tmem_cp_128x128b_w<CG>(te, smem_desc_rows16(se));
             tmem_cp_128x128b_w<CG>(te + 4, smem_desc_rows16(se + kMetaTileBytes / 2));
             const uint64_t bd1 = bd + ((C::kBAtomBytes >> 4) & 0x3FFF);
 #pragma unroll
-            for (int k = 0; k < 2; ++k)
-              mma_sp_i8_w<CG>(d, ad + 2 * k, bd + 4 * (k & 1), id_sp, te + 2 * k, (kb | k) != 0);
-            if (ms) ms[1] = clock64();
-            look_ahead();
-            if (ms) ms[2] = clock64();
-#pragma unroll
-            for (int k = 2; k < 4; ++k)
-              mma_sp_i8_w<CG>(d, ad + 2 * k, bd1 + 4 * (k & 1), id_sp, te + 2 * k, 1u);
+            for (int k = 0; k < 4; ++k)
+              mma_sp_i8_w<CG>(d, ad + 2 * k, (k < 2 ? bd : bd1) + 4 * (k & 1), id_sp, te + 2 * k, (kb | k) != 0);
             if (++meta_slot == kMetaSlots) meta_slot = 0;
           }
           if (ms) ms[3] = clock64();
