@@ -675,6 +675,25 @@ def run_ours(args, w):
                          if world == 1 else ("FusedShardedQuikLinear (C ABI quik_linear_forward_sharded, IPC peer stores)"
                                              if fused is not None else "QuikLinear.forward + NCCL all-gather"))
                    + " with pinned host f16 x -> y")
+        if world == 1:
+            # the reference-facing drop-in call (C++ facade quik::b200::quik_matmul on an
+            # FpMatrix): f32 host x in, f32 host y out, same C ABI entry point
+            xh32 = x16.float().cpu().pin_memory()
+            yh32 = torch.empty((M, ns), dtype=torch.float32).pin_memory()
+            layer.forward_host(xh32, yh32)
+            torch.cuda.synchronize()
+            a2, b2 = ev(), ev()
+            a2.record()
+            for _ in range(e2e_steps):
+                layer.forward_host(xh32, yh32)
+            b2.record()
+            torch.cuda.synchronize()
+            tf = a2.elapsed_time(b2) / e2e_steps
+            e2e["f32_drop_in"] = dict(value=ops / (tf * 1e-3) / 1e12, unit="TOPS", ms_per_step=tf,
+                                      h2d_bytes_per_step=M * K * 4, d2h_bytes_per_step=M * ns * 4,
+                                      path="quik_linear_forward_host with pinned host f32 x -> f32 y (the facade's "
+                                           "quik_matmul(FpMatrix) semantics)")
+            del xh32, yh32
 
     # ---- CPU reference leg (rank 0, N = 1): cpu_baseline timing and the parity check of
     # this run's y, both from the reference's own code on the same layer and tokens

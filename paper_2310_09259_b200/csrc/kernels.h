@@ -216,6 +216,7 @@ struct QuantArgs {
   int64_t kb;               // base column count K_b
   int64_t n_out;
   int bits;                 // 4 or 8
+  int hot_flags;            // hot K1 tuning (set by the launcher): bit 0 = sleep-wait on the row ring
   int8_t* q8;               // GEMM layout [M][kpad] or nullptr
   int64_t kpad;
   uint8_t* packed;          // ABI layout [M][row_bytes] (i4p / i8) or nullptr

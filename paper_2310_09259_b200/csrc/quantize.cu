@@ -500,12 +500,17 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(cons
   const uint4* cdesc = reinterpret_cast<const uint4*>(a.chunk_desc);
   const int first_base = has_out ? static_cast<int>(a.gather[0]) : 0;  // column of base position 0
 
-  // row-independent: outlier lane masks of this thread's vectors
+  // row-independent: outlier lane masks of this thread's vectors, the byte mask (lm, the
+  // rare exact paths) and its expansion to one 16-bit lane mask per f16 (lmw, pass 1:
+  // one LOP3 per word instead of a PRMT + LOP3)
   uint2 lm[VPT];
+  uint4 lmw[VPT];
 #pragma unroll
   for (int i = 0; i < VPT; ++i) {
     const int v = tid + i * nt;
     lm[i] = (has_out && in_row(v)) ? __ldg(reinterpret_cast<const uint2*>(a.lane_mask) + v) : make_uint2(0u, 0u);
+    lmw[i] = make_uint4(__byte_perm(lm[i].x, 0u, 0x1100u), __byte_perm(lm[i].x, 0u, 0x3322u),
+                        __byte_perm(lm[i].y, 0u, 0x1100u), __byte_perm(lm[i].y, 0u, 0x3322u));
   }
 
   // row-independent: this thread's outlier slots (i = tid, tid + nt) -> source column, -1 = zero pad
@@ -542,7 +547,8 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(cons
 #pragma unroll 1
   for (int t = blockIdx.x; t < M; t += gridDim.x) {
     const uint4* srow = reinterpret_cast<const uint4*>(s_ring + s * row_stride);
-    mbar_wait(&s_full[s], ph);
+    if (a.hot_flags & 1) mbar_wait_sleep(&s_full[s], ph);  // waiting threads give up their issue slots
+    else mbar_wait(&s_full[s], ph);
 
     uint4 raw[VPT];
 #pragma unroll
@@ -567,7 +573,7 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(cons
         if (!in_row(tid + i * nt)) continue;
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
-          const uint32_t mk = __byte_perm(w < 2 ? lm[i].x : lm[i].y, 0u, (w & 1) ? 0x3322u : 0x1100u);
+          const uint32_t mk = (&lmw[i].x)[w];
           const __half2 x2 = u2h2(((&raw[i].x)[w] & ~mk) | (fill & mk));
           hmin = __hmin2_nan(hmin, x2);
           hmax = __hmax2_nan(hmax, x2);
@@ -1099,6 +1105,12 @@ cudaError_t launch_quantize_hot(const QuantArgs& a, cudaStream_t stream) {
   while (stages > 1 && codes + stages * row_stride > 200 * 1024) --stages;
   const int smem = codes + stages * row_stride;
   const bool full = static_cast<int64_t>(threads) * vpt == nvec;
+  static const int wait_env = [] {  // tuning knob: QUIK_K1_WAIT=1 sleep-waits on the row ring
+    const char* e = getenv("QUIK_K1_WAIT");
+    return e ? atoi(e) : 0;
+  }();
+  QuantArgs ah = a;
+  ah.hot_flags = wait_env ? 1 : 0;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1121,7 +1133,7 @@ cudaError_t launch_quantize_hot(const QuantArgs& a, cudaStream_t stream) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;                                                \
     cfg.attrs = attr;                                                                                      \
     cfg.numAttrs = 1;                                                                                      \
-    e = cudaLaunchKernelEx(&cfg, kern, a, stages, row_stride);                                             \
+    e = cudaLaunchKernelEx(&cfg, kern, ah, stages, row_stride);                                            \
     if (e != cudaSuccess) return e;                                                                        \
   } while (0)
   if (vpt == 1) QUIK_QH_LAUNCH(1);

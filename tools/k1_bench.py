@@ -82,9 +82,13 @@ def main():
         b.record()
         torch.cuda.synchronize()
         us = a.elapsed_time(b) * 1e3 / (iters * reps)
-        nbytes = M * K * 2 + M * kpad + M * opad * 2 + 8 * M
+        nbytes = M * K * 2 + M * kpad + M * opad * 2 + 8 * M  # the kernel's own (int8 code) layout
+        alg = M * K * 2 + M * ((kb + 1) // 2 if bits == 4 else kb) + M * O * 2 + 8 * M  # SURVEY §8(d) bytes
+        peak = json.loads((Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
+            if (Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json").exists() else 6650.0
         print(json.dumps(dict(name=name, M=M, K=K, O=O, bits=bits, us=us, gbs=nbytes / us * 1e-3,
-                              frac=nbytes / us * 1e-3 / 6548.8)), flush=True)
+                              frac_device_layout=nbytes / us * 1e-3 / peak, alg_bytes=alg,
+                              frac=alg / us * 1e-3 / peak, peak_gbs=peak)), flush=True)
 
 
 if __name__ == "__main__":
