@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <numeric>
 #include <span>
@@ -365,10 +366,94 @@ class DeviceLayer {
     detail::check(quik_linear_forward(detail::ctx(), h_, x, xdt, M, y, ydt, static_cast<quik_variant>(v), stream));
   }
 
+  // Output-feature shard: this layer's f16 output columns go to column `col_offset` of
+  // every destination (own y first, then peers' mapped outputs), the all-gather fused
+  // into the GEMM epilogue (quik_linear_forward_sharded).
+  void forward_sharded(const void* x, quik_dtype xdt, int64_t M, void* const* dsts, int n_dst, int64_t ldy,
+                       int64_t col_offset, void* stream = nullptr) const {
+    detail::check(quik_linear_forward_sharded(detail::ctx(), h_, x, xdt, M, dsts, n_dst, ldy, col_offset, stream));
+  }
+
  private:
   quik_layer_t h_ = nullptr;
   int64_t in_ = 0, out_ = 0;
   LayerMode mode_ = LayerMode::Quik;
+};
+
+// ---------------------------------------------------------------- multi-GPU
+
+// Contiguous, balanced output-row range of `rank` (the first n % world ranks get one more).
+inline std::pair<int64_t, int64_t> shard_bounds(int64_t n, int world, int rank) {
+  if (world <= 0 || rank < 0 || rank >= world) throw std::invalid_argument("bad rank / world size");
+  const int64_t base = n / world, extra = n % world;
+  const int64_t b = rank * base + std::min<int64_t>(rank, extra);
+  return {b, b + base + (rank < extra ? 1 : 0)};
+}
+
+// One process per GPU: this rank's output-feature shard of a QUIK layer with the
+// all-gather fused into the GEMM epilogue. The [M][N] f16 outputs of every rank are
+// mapped into every process through CUDA IPC (quik_ipc_handle_*); `exchange` is the
+// caller's all-gather of byte blobs (MPI_Allgather, sockets, ...), used once at
+// construction. Two output buffers alternate; after forward() the caller fences the
+// ranks on `stream` (e.g. a one-element ncclAllReduce) before reading the result, which
+// also orders readers of the buffer two steps back before its next writes.
+class FusedShardedLayer {
+ public:
+  using Exchange = std::function<std::vector<std::vector<uint8_t>>(const std::vector<uint8_t>&)>;
+
+  FusedShardedLayer(const QuikLinearLayer& full, int rank, int world, int64_t max_tokens, const Exchange& exchange)
+      : rank_(rank), world_(world), n_(full.out_features()), max_tokens_(max_tokens) {
+    const auto [b, e] = shard_bounds(n_, world, rank);
+    begin_ = b;
+    local_ = std::make_unique<DeviceLayer>(full, b, e);
+    std::vector<uint8_t> mine;
+    for (int i = 0; i < 2; ++i) {
+      detail::cuda(cudaMalloc(&bufs_[i], static_cast<size_t>(max_tokens * n_ * 2)), "cudaMalloc");
+      quik_ipc_handle h{};
+      detail::check(quik_ipc_handle_get(detail::ctx(), bufs_[i], &h));
+      const auto* p = reinterpret_cast<const uint8_t*>(&h);
+      mine.insert(mine.end(), p, p + sizeof(h));
+    }
+    const std::vector<std::vector<uint8_t>> all = exchange(mine);
+    if (static_cast<int>(all.size()) != world) throw std::invalid_argument("fused all-gather: exchange size != world");
+    for (int i = 0; i < 2; ++i) {
+      dst_[i].push_back(bufs_[i]);
+      for (int r = 0; r < world; ++r) {
+        if (r == rank) continue;
+        if (all[r].size() != 2 * sizeof(quik_ipc_handle)) throw std::invalid_argument("fused all-gather: bad handle");
+        quik_ipc_handle h{};
+        std::memcpy(&h, all[r].data() + i * sizeof(h), sizeof(h));
+        void* p = nullptr;
+        detail::check(quik_ipc_handle_open(detail::ctx(), &h, &p));
+        dst_[i].push_back(p);
+        opened_.push_back({p, h});
+      }
+    }
+  }
+  ~FusedShardedLayer() {
+    for (auto& [p, h] : opened_) quik_ipc_handle_close(detail::ctx(), p, &h);
+    for (void* b : bufs_) cudaFree(b);
+  }
+  FusedShardedLayer(const FusedShardedLayer&) = delete;
+  FusedShardedLayer& operator=(const FusedShardedLayer&) = delete;
+
+  // x: device [M][in] (f16 or f32); returns this rank's copy of the full [M][N] f16 output.
+  const void* forward(const void* x, quik_dtype xdt, int64_t M, void* stream = nullptr) {
+    if (M > max_tokens_) throw std::invalid_argument("fused all-gather: more tokens than max_tokens");
+    const int i = step_++ & 1;
+    local_->forward_sharded(x, xdt, M, dst_[i].data(), world_, n_, begin_, stream);
+    return bufs_[i];
+  }
+  int64_t out_features() const { return n_; }
+
+ private:
+  int rank_, world_;
+  int64_t n_, max_tokens_, begin_ = 0;
+  int step_ = 0;
+  std::unique_ptr<DeviceLayer> local_;
+  void* bufs_[2] = {nullptr, nullptr};
+  std::vector<void*> dst_[2];
+  std::vector<std::pair<void*, quik_ipc_handle>> opened_;
 };
 
 // ---------------------------------------------------------------- reference functions

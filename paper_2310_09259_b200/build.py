@@ -118,11 +118,25 @@ def build_tests(force: bool = False) -> Path:
     return out
 
 
+def build_ipc_test(force: bool = False) -> Path:
+    """C++ two-process test of the fused all-gather through CUDA IPC (FusedShardedLayer)."""
+    src = ROOT / "tests" / "cpp" / "ipc_test.cpp"
+    out = ROOT / "build" / "tests" / "ipc_test"
+    out.parent.mkdir(parents=True, exist_ok=True)
+    deps = [src, ROOT / "include" / "quik_b200.hpp", ROOT / "include" / "quik_b200.h", LIB]
+    if force or _stale(out, deps):
+        _run(["g++", "-std=c++20", "-O2", "-Wall", "-I" + str(ROOT / "include"), "-I/usr/local/cuda/include",
+              str(src), "-o", str(out), "-L" + str(LIBDIR), "-lquik_b200", "-L/usr/local/cuda/lib64", "-lcudart",
+              "-Wl,-rpath," + str(LIBDIR), "-Wl,-rpath,$ORIGIN/../../paper_2310_09259_b200/lib"])
+    return out
+
+
 def build_all(force: bool = False) -> None:
     build_product(force)
     build_oracle(force)
     build_reference(force)
     build_tests(force)
+    build_ipc_test(force)
 
 
 if __name__ == "__main__":

@@ -71,3 +71,18 @@ def test_fused_all_gather_cuda_ipc_two_processes():
     for p in procs:
         p.join(30)
     assert res == {0: [True] * 9, 1: [True] * 9}, res
+
+
+@pytest.mark.timeout(300)
+def test_fused_all_gather_cpp_two_processes():
+    """The same exchange from C++ (quik::b200::FusedShardedLayer, tests/cpp/ipc_test.cpp):
+    two forked processes, IPC handles and barriers over pipes, every step of both ranks
+    bit-identical to the unsharded layer."""
+    import subprocess
+    from pathlib import Path
+
+    from paper_2310_09259_b200 import build
+
+    exe = build.build_ipc_test()
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=280, cwd=Path(exe).parent)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
