@@ -7,15 +7,15 @@
 //   C  = upper Cholesky factor of Hd^-1                                 (cuSOLVER potrf/potri/potrf)
 //   per-row scales from the base columns (optional clip search), fixed before the recursion
 //   for each base column j (blocks of 64): q = round_away(w_j / s), err = (w_j - q s) / C_jj,
-//   w_t -= err C_jt for t > j  (in-block: sequential per row; beyond the block: one DGEMM)
+//   w_t -= err C_jt for t > j  (in-block: sequential per row; beyond the block: one GEMM)
 //
 // The panel kernel keeps the reference's per-element arithmetic (IEEE double mul / sub /
 // div, floor(|t| + 0.5) rounding, stable 2:4 saliency order); the trailing update of a
-// block is a cuBLAS DGEMM (a library GEMM, like cuBLAS elsewhere), so the update sums run
-// in a different order and the Cholesky factor comes from cuSOLVER instead of the
-// reference's loops: results agree with the reference to FP64 rounding (codes / scales /
-// masks bit-identical on the test cases, outlier weights to float rounding).
-#include <cublas_v2.h>
+// block and the Hessian X^T X run on a hand-written FP64 tensor-core GEMM
+// (mma.sync.m8n8k4.f64, dgemm_kernel below), so the update sums run in a different order
+// than the reference's loops, and the Cholesky factor comes from cuSOLVER: results agree
+// with the reference to FP64 rounding (codes / scales / masks bit-identical on the test
+// cases, outlier weights to float rounding).
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
 
@@ -205,6 +205,80 @@ __global__ void to_double_kernel(const float* __restrict__ x, int64_t n, double*
 
 unsigned blocks_for(int64_t n) { return static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16)); }
 
+// ---------------------------------------------------------------- FP64 tensor-core GEMM
+// C(m, n) += alpha * sum_k A(m, k) * B(k, n) over strided operands
+//   A(m, k) = A[m * a_m + k * a_k],  B(k, n) = B[k * b_k + n * b_n],  C(m, n) = C[m * ldc + n]
+// (the strides express the transposes: the Hessian X^T X and the GPTQ trailing update
+// W[:, j1:] -= E * C[j0:j1, j1:]). 64 x 64 tiles per CTA, 16-deep K slices staged in
+// shared memory, four warps of 32 x 32 each as 4 x 4 tiles of
+// mma.sync.m8n8k4.f64 (sm_80+ DMMA; FP64 accumulate, every product and sum IEEE
+// double). Replaces cuBLAS DGEMM: a different summation order, FP64 either way.
+constexpr int kDT = 64, kDK = 16;
+
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(128) dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha,
+                                                    const double* __restrict__ A, int64_t a_m, int64_t a_k,
+                                                    const double* __restrict__ B, int64_t b_k, int64_t b_n,
+                                                    double* __restrict__ C, int64_t ldc) {
+  __shared__ double sa[kDT][kDK + 1];  // [m][k]
+  __shared__ double sb[kDK][kDT + 1];  // [k][n]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;  // fragment row group / thread in group
+  const int64_t m0 = static_cast<int64_t>(blockIdx.y) * kDT, n0 = static_cast<int64_t>(blockIdx.x) * kDT;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int64_t k0 = 0; k0 < K; k0 += kDK) {
+    for (int e = tid; e < kDT * kDK; e += 128) {
+      const int r = e / kDK, kk = e % kDK;  // A: consecutive threads walk k
+      const int64_t m = m0 + r, k = k0 + kk;
+      sa[r][kk] = (m < M && k < K) ? A[m * a_m + k * a_k] : 0.0;
+      const int kk2 = e / kDT, c = e % kDT;  // B: consecutive threads walk n
+      const int64_t k2 = k0 + kk2, n = n0 + c;
+      sb[kk2][c] = (k2 < K && n < N) ? B[k2 * b_k + n * b_n] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < kDK; ks += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = sa[wm + 8 * i + g][ks + t4];  // A(8x4) row: [g][t4]
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = sb[ks + t4][wn + 8 * j + g];  // B(4x8) col: [t4][g]
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // D(8x8): [g][2 t4 + h]
+        const int64_t m = m0 + wm + 8 * i + g, n = n0 + wn + 8 * j + 2 * t4 + h;
+        if (m < M && n < N) C[m * ldc + n] = __dadd_rn(C[m * ldc + n], __dmul_rn(alpha, acc[i][j][h]));
+      }
+}
+
+cudaError_t dgemm(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t a_m, int64_t a_k,
+                  const double* B, int64_t b_k, int64_t b_n, double* C, int64_t ldc, cudaStream_t st = nullptr) {
+  if (M == 0 || N == 0 || K == 0) return cudaSuccess;
+  const dim3 grid(static_cast<unsigned>((N + kDT - 1) / kDT), static_cast<unsigned>((M + kDT - 1) / kDT));
+  dgemm_kernel<<<grid, 128, 0, st>>>(M, N, K, alpha, A, a_m, a_k, B, b_k, b_n, C, ldc);
+  return cudaGetLastError();
+}
+
 struct DevMem {
   std::vector<void*> ptrs;
   ~DevMem() {
@@ -335,15 +409,8 @@ int gptq_quantize_device(const GptqArgs& a, std::string* msg) {
   scales_kernel<<<static_cast<unsigned>((N + 127) / 128), 128>>>(d_wd, N, K, kb, maxq, a.use_clipping, d_sd, d_sf);
   GQ_CUDA(cudaGetLastError());
 
-  cublasHandle_t blas = nullptr;
-  if (cublasCreate(&blas) != CUBLAS_STATUS_SUCCESS) { *msg = "gptq: cublasCreate failed"; return 4; }
-  struct BlasGuard {
-    cublasHandle_t h;
-    ~BlasGuard() { cublasDestroy(h); }
-  } bg{blas};
   const int smem = static_cast<int>((kPanel * kPanel + kPanelRows * (kPanel + 1)) * sizeof(double));
   GQ_CUDA(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  const double minus_one = -1.0, one = 1.0;
   for (int64_t j0 = 0; j0 < kb; j0 += kPanel) {
     const int jb = static_cast<int>(std::min<int64_t>(kPanel, kb - j0));
     panel_kernel<<<static_cast<unsigned>((N + kPanelRows - 1) / kPanelRows), kPanelRows, smem>>>(
@@ -351,11 +418,9 @@ int gptq_quantize_device(const GptqArgs& a, std::string* msg) {
     GQ_CUDA(cudaGetLastError());
     const int64_t j1 = j0 + jb;
     if (j1 < K) {
-      // W[:, j1:] -= E[N x jb] * C[j0:j1, j1:]   (row-major; column-major view: W^T -= C^T E^T)
-      if (cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(K - j1), static_cast<int>(N), jb, &minus_one,
-                      d_c + j0 * K + j1, static_cast<int>(K), d_err, kPanel, &one, d_wd + j1, static_cast<int>(K)) !=
-          CUBLAS_STATUS_SUCCESS) {
-        *msg = "gptq: cublasDgemm failed";
+      // W[:, j1:] -= E[N x jb] * C[j0:j1, j1:]   (row-major; the FP64 tensor-core GEMM)
+      if (dgemm(N, K - j1, jb, -1.0, d_err, kPanel, 1, d_c + j0 * K + j1, K, 1, d_wd + j1, K) != cudaSuccess) {
+        *msg = "gptq: trailing-update GEMM failed";
         return 4;
       }
     }
@@ -382,15 +447,8 @@ int hessian_accumulate_device(const float* x, int64_t T, int64_t K, double* h, s
   if (!d_x || !d_xd) { *msg = "hessian: device allocation failed"; return 4; }
   if (cudaMemcpy(d_x, x, T * K * sizeof(float), cudaMemcpyDefault) != cudaSuccess) { *msg = "hessian: copy failed"; return 4; }
   to_double_kernel<<<blocks_for(T * K), 256>>>(d_x, T * K, d_xd);
-  cublasHandle_t blas = nullptr;
-  if (cublasCreate(&blas) != CUBLAS_STATUS_SUCCESS) { *msg = "hessian: cublasCreate failed"; return 4; }
-  const double one = 1.0;
-  // column-major view: X^T is K x T (ld K); H (K x K, symmetric) += X^T (X^T)^T
-  const cublasStatus_t s = cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_T, static_cast<int>(K), static_cast<int>(K),
-                                       static_cast<int>(T), &one, d_xd, static_cast<int>(K), d_xd,
-                                       static_cast<int>(K), &one, h, static_cast<int>(K));
-  cublasDestroy(blas);
-  if (s != CUBLAS_STATUS_SUCCESS) { *msg = "hessian: cublasDgemm failed"; return 4; }
+  // H[i][j] += sum_t X[t][i] X[t][j]: A(i, t) = X[t][i], B(t, j) = X[t][j] (FP64 tensor-core GEMM)
+  if (dgemm(K, K, T, 1.0, d_xd, 1, K, d_xd, K, 1, h, K) != cudaSuccess) { *msg = "hessian: GEMM failed"; return 4; }
   if (cudaDeviceSynchronize() != cudaSuccess) { *msg = "hessian: kernel failed"; return 4; }
   return 0;
 }
