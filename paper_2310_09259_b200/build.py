@@ -61,7 +61,7 @@ def build_product(force: bool = False) -> Path:
             f.result()
     if force or jobs or _stale(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-cudart", "shared",
-              "-lcusolver", "-Xlinker", "-soname=libquik_b200.so"])
+              "-Xlinker", "-soname=libquik_b200.so"])
     return LIB
 
 

@@ -4,7 +4,7 @@
 // like the reference:
 //
 //   Hd = H[perm][perm] + lambda I,  lambda = damping * trace(H) / K     (host-summed trace)
-//   C  = upper Cholesky factor of Hd^-1                                 (cuSOLVER potrf/potri/potrf)
+//   C  = upper Cholesky factor of Hd^-1   (own blocked FP64 Cholesky / triangular inverse)
 //   per-row scales from the base columns (optional clip search), fixed before the recursion
 //   for each base column j (blocks of 64): q = round_away(w_j / s), err = (w_j - q s) / C_jj,
 //   w_t -= err C_jt for t > j  (in-block: sequential per row; beyond the block: one GEMM)
@@ -12,12 +12,12 @@
 // The panel kernel keeps the reference's per-element arithmetic (IEEE double mul / sub /
 // div, floor(|t| + 0.5) rounding, stable 2:4 saliency order); the trailing update of a
 // block and the Hessian X^T X run on a hand-written FP64 tensor-core GEMM
-// (mma.sync.m8n8k4.f64, dgemm_kernel below), so the update sums run in a different order
-// than the reference's loops, and the Cholesky factor comes from cuSOLVER: results agree
-// with the reference to FP64 rounding (codes / scales / masks bit-identical on the test
-// cases, outlier weights to float rounding).
+// (mma.sync.m8n8k4.f64, dgemm_kernel below), and so do the blocked Cholesky factorisations
+// and the triangular inverse around their diagonal-block / panel kernels: the sums run in
+// a different order than the reference's loops, so results agree with the reference to
+// FP64 rounding (codes / scales / masks bit-identical on the test cases, outlier weights
+// to float rounding). No cuBLAS / cuSOLVER.
 #include <cuda_runtime.h>
-#include <cusolverDn.h>
 
 #include <cmath>
 #include <cstdint>
@@ -271,8 +271,128 @@ __global__ void __launch_bounds__(128) dgemm_kernel(int64_t M, int64_t N, int64_
       }
 }
 
+// ---------------------------------------------------------------- Cholesky and inverse (FP64)
+// Row-major, blocks of kCb columns, right-looking: factor the diagonal block (one CTA,
+// the reference's column recursion, quantizer.cpp:33-48), solve the panel below it (one
+// thread per row), update the trailing matrix with the FP64 tensor-core GEMM.
+constexpr int kCb = 32;
+
+// Diagonal block A[j0:j0+jb, j0:j0+jb] -> its lower Cholesky factor (in place); *bad = 1
+// when a pivot is not positive and finite (the reference's "not positive definite").
+__global__ void chol_diag_kernel(double* __restrict__ a, int64_t K, int64_t j0, int jb, int* __restrict__ bad) {
+  __shared__ double s[kCb][kCb + 1];
+  const int t = threadIdx.x;  // row of the block
+  for (int c = 0; c < jb; ++c) s[t][c] = t < jb ? a[(j0 + t) * K + j0 + c] : 0.0;
+  __syncthreads();
+  for (int j = 0; j < jb; ++j) {
+    if (t == j) {
+      double v = s[j][j];
+      for (int k = 0; k < j; ++k) v = __dsub_rn(v, __dmul_rn(s[j][k], s[j][k]));
+      if (!(v > 0.0) || !isfinite(v)) {
+        *bad = 1;
+        v = 1.0;
+      }
+      s[j][j] = __dsqrt_rn(v);
+    }
+    __syncthreads();
+    if (t > j && t < jb) {
+      double v = s[t][j];
+      for (int k = 0; k < j; ++k) v = __dsub_rn(v, __dmul_rn(s[t][k], s[j][k]));
+      s[t][j] = __ddiv_rn(v, s[j][j]);
+    }
+    __syncthreads();
+  }
+  if (t < jb)
+    for (int c = 0; c < jb; ++c) a[(j0 + t) * K + j0 + c] = c <= t ? s[t][c] : 0.0;
+}
+
+// Panel below the diagonal block: row i: x = A[i, j0:j0+jb] L11^-T (forward substitution).
+__global__ void chol_panel_kernel(double* __restrict__ a, int64_t K, int64_t j0, int jb) {
+  __shared__ double l[kCb][kCb + 1];
+  for (int e = threadIdx.x; e < jb * jb; e += blockDim.x) l[e / jb][e % jb] = a[(j0 + e / jb) * K + j0 + e % jb];
+  __syncthreads();
+  const int64_t i = j0 + jb + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= K) return;
+  double x[kCb];
+#pragma unroll
+  for (int j = 0; j < kCb; ++j) {
+    if (j >= jb) break;
+    double v = a[i * K + j0 + j];
+    for (int k = 0; k < j; ++k) v = __dsub_rn(v, __dmul_rn(x[k], l[j][k]));
+    x[j] = __ddiv_rn(v, l[j][j]);
+    a[i * K + j0 + j] = x[j];
+  }
+}
+
+// One block row of Y = L^-1: Y[i0:i0+ib, :] = L_ii^-1 R, R = (rows of I) - L[i, :i0] Y[:i0, :]
+// already formed in y; one thread per column, forward substitution over the ib rows.
+__global__ void trinv_rows_kernel(const double* __restrict__ l, double* __restrict__ y, int64_t K, int64_t i0,
+                                  int ib) {
+  __shared__ double s[kCb][kCb + 1];
+  for (int e = threadIdx.x; e < ib * ib; e += blockDim.x) s[e / ib][e % ib] = l[(i0 + e / ib) * K + i0 + e % ib];
+  __syncthreads();
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= i0 + ib) return;  // Y is lower triangular: columns > the block's last row stay 0
+  double x[kCb];
+#pragma unroll
+  for (int r = 0; r < kCb; ++r) {
+    if (r >= ib) break;
+    double v = y[(i0 + r) * K + c];
+    for (int k = 0; k < r; ++k) v = __dsub_rn(v, __dmul_rn(s[r][k], x[k]));
+    x[r] = __ddiv_rn(v, s[r][r]);
+    y[(i0 + r) * K + c] = x[r];
+  }
+}
+
+__global__ void zero_upper_kernel(double* __restrict__ a, int64_t K) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < K * K;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    if (e % K > e / K) a[e] = 0.0;
+}
+
+__global__ void identity_kernel(double* __restrict__ y, int64_t K) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < K * K;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[e] = (e / K == e % K) ? 1.0 : 0.0;
+}
+
+__global__ void transpose_kernel(const double* __restrict__ x, double* __restrict__ y, int64_t K) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < K * K;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[(e % K) * K + e / K] = x[e];
+}
+
 cudaError_t dgemm(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t a_m, int64_t a_k,
-                  const double* B, int64_t b_k, int64_t b_n, double* C, int64_t ldc, cudaStream_t st = nullptr) {
+                  const double* B, int64_t b_k, int64_t b_n, double* C, int64_t ldc, cudaStream_t st);
+
+// Lower Cholesky factor of the symmetric positive definite A (row-major, in place; the
+// upper triangle is left zero). Returns 1 if A is not numerically positive definite.
+int potrf_lower(double* a, int64_t K, int* d_bad, std::string* msg) {
+  if (cudaMemset(d_bad, 0, sizeof(int)) != cudaSuccess) { *msg = "cholesky: memset failed"; return 4; }
+  for (int64_t j0 = 0; j0 < K; j0 += kCb) {
+    const int jb = static_cast<int>(std::min<int64_t>(kCb, K - j0));
+    chol_diag_kernel<<<1, kCb>>>(a, K, j0, jb, d_bad);
+    const int64_t below = K - j0 - jb;
+    if (below > 0) {
+      chol_panel_kernel<<<static_cast<unsigned>((below + 127) / 128), 128>>>(a, K, j0, jb);
+      // A22 -= L21 L21^T (the whole square; only its lower part is read later)
+      const double* l21 = a + (j0 + jb) * K + j0;
+      if (dgemm(below, below, jb, -1.0, l21, K, 1, l21, 1, K, a + (j0 + jb) * K + j0 + jb, K, nullptr) !=
+          cudaSuccess) {
+        *msg = "cholesky: trailing GEMM failed";
+        return 4;
+      }
+    }
+  }
+  // zero the strict upper triangle (the trailing updates wrote both halves)
+  zero_upper_kernel<<<blocks_for(K * K), 256>>>(a, K);
+  int bad = 0;
+  if (cudaMemcpy(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) { *msg = "cholesky: failed"; return 4; }
+  return bad ? 1 : 0;
+}
+
+cudaError_t dgemm(int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t a_m, int64_t a_k,
+                  const double* B, int64_t b_k, int64_t b_n, double* C, int64_t ldc, cudaStream_t st) {
   if (M == 0 || N == 0 || K == 0) return cudaSuccess;
   const dim3 grid(static_cast<unsigned>((N + kDT - 1) / kDT), static_cast<unsigned>((M + kDT - 1) / kDT));
   dgemm_kernel<<<grid, 128, 0, st>>>(M, N, K, alpha, A, a_m, a_k, B, b_k, b_n, C, ldc);
@@ -358,52 +478,41 @@ int gptq_quantize_device(const GptqArgs& a, std::string* msg) {
   permute_hessian_kernel<<<blocks_for(K * K), 256>>>(d_h, d_perm, lam, K, d_c);
   GQ_CUDA(cudaGetLastError());
 
-  // C: potrf (lower) -> potri (inverse, lower) -> potrf (lower) on the symmetric
-  // matrix; read row-major, the column-major lower factor of Hd^-1 is the reference's
-  // upper factor C (row j of C = column j of L), quantizer.cpp:70-99
-  cusolverDnHandle_t sol = nullptr;
-  if (cusolverDnCreate(&sol) != CUSOLVER_STATUS_SUCCESS) { *msg = "gptq: cusolverDnCreate failed"; return 4; }
-  struct SolGuard {
-    cusolverDnHandle_t h;
-    ~SolGuard() { cusolverDnDestroy(h); }
-  } sg{sol};
-  int lwork = 0, lwork2 = 0;
-  if (cusolverDnDpotrf_bufferSize(sol, CUBLAS_FILL_MODE_LOWER, static_cast<int>(K), d_c, static_cast<int>(K), &lwork) !=
-          CUSOLVER_STATUS_SUCCESS ||
-      cusolverDnDpotri_bufferSize(sol, CUBLAS_FILL_MODE_LOWER, static_cast<int>(K), d_c, static_cast<int>(K), &lwork2) !=
-          CUSOLVER_STATUS_SUCCESS) {
-    *msg = "gptq: cuSOLVER workspace query failed";
+  // C = upper Cholesky factor of Hd^-1 (quantizer.cpp:50-99): L = chol(Hd), Y = L^-1,
+  // Hd^-1 = Y^T Y, Lx = chol(Hd^-1), C = Lx^T -- every step hand-written FP64 (diagonal
+  // block / panel kernels + the FP64 tensor-core GEMM)
+  double* d_y = m.alloc<double>(K * K);
+  int* d_bad = m.alloc<int>(1);
+  if (!d_y || !d_bad) { *msg = "gptq: device allocation failed"; return 4; }
+  {
+    const int st = potrf_lower(d_c, K, d_bad, msg);
+    if (st == 1) { *msg = "Hessian is not positive definite after damping; increase the damping fraction"; return 3; }
+    if (st) return st;
+  }
+  identity_kernel<<<blocks_for(K * K), 256>>>(d_y, K);
+  for (int64_t i0 = 0; i0 < K; i0 += kCb) {
+    const int ib = static_cast<int>(std::min<int64_t>(kCb, K - i0));
+    if (i0 > 0) {  // R = I[i rows] - L[i, :i0] Y[:i0, :(i0 + ib)]
+      if (dgemm(ib, i0 + ib, i0, -1.0, d_c + i0 * K, K, 1, d_y, K, 1, d_y + i0 * K, K, nullptr) != cudaSuccess) {
+        *msg = "gptq: triangular-inverse GEMM failed";
+        return 4;
+      }
+    }
+    trinv_rows_kernel<<<static_cast<unsigned>((i0 + ib + 127) / 128), 128>>>(d_c, d_y, K, i0, ib);
+  }
+  GQ_CUDA(cudaMemset(d_c, 0, K * K * sizeof(double)));
+  if (dgemm(K, K, K, 1.0, d_y, 1, K, d_y, K, 1, d_c, K, nullptr) != cudaSuccess) {  // Y^T Y
+    *msg = "gptq: inverse GEMM failed";
     return 4;
   }
-  double* d_work = m.alloc<double>(std::max(lwork, lwork2));
-  int* d_info = m.alloc<int>(1);
-  if (!d_work || !d_info) { *msg = "gptq: device allocation failed"; return 4; }
-  auto potrf = [&](const char* what) -> int {
-    int info = 0;
-    if (cusolverDnDpotrf(sol, CUBLAS_FILL_MODE_LOWER, static_cast<int>(K), d_c, static_cast<int>(K), d_work, lwork,
-                         d_info) != CUSOLVER_STATUS_SUCCESS) {
-      *msg = std::string("gptq: cusolverDnDpotrf failed (") + what + ")";
-      return 4;
-    }
-    if (cudaMemcpy(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return 4;
-    if (info != 0) {
-      *msg = std::string(what) + ": Hessian is not positive definite after damping; increase the damping fraction";
-      return 3;
-    }
-    return 0;
-  };
-  if (int st = potrf("Hessian")) return st;
   {
-    int info = 0;
-    if (cusolverDnDpotri(sol, CUBLAS_FILL_MODE_LOWER, static_cast<int>(K), d_c, static_cast<int>(K), d_work, lwork2,
-                         d_info) != CUSOLVER_STATUS_SUCCESS) {
-      *msg = "gptq: cusolverDnDpotri failed";
-      return 4;
-    }
-    GQ_CUDA(cudaMemcpy(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost));
-    if (info != 0) { *msg = "inverse Hessian is singular"; return 3; }
+    const int st = potrf_lower(d_c, K, d_bad, msg);
+    if (st == 1) { *msg = "inverse Hessian is not positive definite"; return 3; }
+    if (st) return st;
   }
-  if (int st = potrf("inverse Hessian")) return st;
+  transpose_kernel<<<blocks_for(K * K), 256>>>(d_c, d_y, K);  // C = Lx^T (row-major upper)
+  GQ_CUDA(cudaGetLastError());
+  GQ_CUDA(cudaMemcpy(d_c, d_y, K * K * sizeof(double), cudaMemcpyDeviceToDevice));
 
   permute_w_kernel<<<blocks_for(N * K), 256>>>(d_w, d_perm, N, K, d_wd);
   scales_kernel<<<static_cast<unsigned>((N + 127) / 128), 128>>>(d_wd, N, K, kb, maxq, a.use_clipping, d_sd, d_sf);
@@ -419,7 +528,7 @@ int gptq_quantize_device(const GptqArgs& a, std::string* msg) {
     const int64_t j1 = j0 + jb;
     if (j1 < K) {
       // W[:, j1:] -= E[N x jb] * C[j0:j1, j1:]   (row-major; the FP64 tensor-core GEMM)
-      if (dgemm(N, K - j1, jb, -1.0, d_err, kPanel, 1, d_c + j0 * K + j1, K, 1, d_wd + j1, K) != cudaSuccess) {
+      if (dgemm(N, K - j1, jb, -1.0, d_err, kPanel, 1, d_c + j0 * K + j1, K, 1, d_wd + j1, K, nullptr) != cudaSuccess) {
         *msg = "gptq: trailing-update GEMM failed";
         return 4;
       }
@@ -448,7 +557,10 @@ int hessian_accumulate_device(const float* x, int64_t T, int64_t K, double* h, s
   if (cudaMemcpy(d_x, x, T * K * sizeof(float), cudaMemcpyDefault) != cudaSuccess) { *msg = "hessian: copy failed"; return 4; }
   to_double_kernel<<<blocks_for(T * K), 256>>>(d_x, T * K, d_xd);
   // H[i][j] += sum_t X[t][i] X[t][j]: A(i, t) = X[t][i], B(t, j) = X[t][j] (FP64 tensor-core GEMM)
-  if (dgemm(K, K, T, 1.0, d_xd, 1, K, d_xd, K, 1, h, K) != cudaSuccess) { *msg = "hessian: GEMM failed"; return 4; }
+  if (dgemm(K, K, T, 1.0, d_xd, 1, K, d_xd, K, 1, h, K, nullptr) != cudaSuccess) {
+    *msg = "hessian: GEMM failed";
+    return 4;
+  }
   if (cudaDeviceSynchronize() != cudaSuccess) { *msg = "hessian: kernel failed"; return 4; }
   return 0;
 }
