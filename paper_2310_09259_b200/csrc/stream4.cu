@@ -13,9 +13,11 @@
 // Same architecture as the weight-only kernel (wo.cu): the 4-bit weights never exist
 // as int8 in shared memory. A weight producer TMA-streams 16 KB INT4 tiles (128 rows x
 // 256 K) into a deep ring; G widening groups (4 warps each, one weight row per thread)
-// sign-extend the nibbles with two integer ops per four values and tcgen05.st them into
-// a TMEM A buffer (lane = weight row, column j = 4 int8 {k = 4j .. 4j+3}, pinned by
-// tools/ts_probe.cu) and release the weight slot at once; each group's converged
+// move each nibble into the high half of its byte (16 x the value, 1-2 integer ops per
+// four values; the epilogue shifts the exact sums right by 4, like the prefill GEMM),
+// tcgen05.st them into a TMEM A buffer (lane = weight row, column j = 4 int8
+// {k = 4j .. 4j+3}, pinned by tools/ts_probe.cu) and release the weight slot at once;
+// each group's converged
 // issuing warp runs 8 tcgen05.mma.kind::i8 (A from TMEM, the int8 activation-code tile
 // from shared memory) per stage into its own int32 accumulator; four epilogue warps sum
 // the G accumulators and red.add them into the workspace. Each ring stage has exactly
@@ -264,9 +266,10 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
             const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const uint32_t lo = w[q] & 0x0F0F0F0Fu, hi = (w[q] >> 4) & 0x0F0F0F0Fu;
-              o[8 * cc + q] = lo + (lo & 0x08080808u) * 0x1Eu;  // sign-extend each nibble
-              o[8 * cc + 4 + q] = hi + (hi & 0x08080808u) * 0x1Eu;
+              // 16 x the value: each nibble moved to the high half of its byte (3 ops per
+              // word instead of a sign extension); the epilogue shifts the exact sums back
+              o[8 * cc + q] = (w[q] << 4) & 0xF0F0F0F0u;
+              o[8 * cc + 4 + q] = w[q] & 0xF0F0F0F0u;
             }
           }
           tmem_st32(a_tm + 32 * h, o);
@@ -313,10 +316,11 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
           for (int j = 0; j < 32; ++j) sum[j] += static_cast<int>(x[j]);
         }
         if (n < p.N && used) {
+          const int sh = p.w8 ? 0 : 4;  // INT4: the MMAs summed 16 x the weight (exact shift)
 #pragma unroll
           for (int j = 0; j < (BN < 32 ? BN : 32); ++j) {
             const int t = c + j;
-            if (t < p.M) atomicAdd(&p.acc[static_cast<long long>(t) * p.N + n], sum[j]);
+            if (t < p.M) atomicAdd(&p.acc[static_cast<long long>(t) * p.N + n], sum[j] >> sh);
           }
         }
       }
