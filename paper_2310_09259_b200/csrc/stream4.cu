@@ -86,6 +86,7 @@ struct S4Params {
   long long ldo;
   int out_f16;
   int gated;              // rows interleave up / gate (32-row blocks): out is [M][N / 2]
+  int prefetch;           // outlier tiles load while the unit streams (QUIK_S4_PREFETCH=0: at finalisation)
   int n_dst;              // 1 + peers
   void* dst[8];           // output base pointers (dst[0] == out)
 };
@@ -288,55 +289,17 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
     const int quad = warp & 3;
     const bool lead = warp == C::kWidenEnd;  // issues the finalisation TMA loads / MMAs
     asm volatile("griddepcontrol.wait;" ::: "memory");  // K1's scales / outlier columns
-    int it = 0, bc0 = 0, fin_uses = 0;
+    int it = 0, bc0 = 0, fin_ld = 0, fin_mm = 0;
+    // one K split with BN <= 32: the unit's sums stay in registers and finalise at once
+    // (no workspace round trip, no arrival counter)
+    const bool direct = p.splits == 1 && BN <= 32;
+    constexpr uint32_t idesc_f16 = idesc_make(1u, 0u, kBlockM, BN);
     for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
       int nb, k0, k1;
       decode(u, nb, k0, k1);
       uint32_t used = 0;
       for (int k = 0; k < k1 - k0 && k < G; ++k) used |= 1u << ((bc0 + k) % G);
       bc0 += k1 - k0;
-      const int b = it & 1;
-      mbar_wait_sleep(&acc_full[b], (it >> 1) & 1);
-      tc_fence_after();
-      const int n = nb * kBlockM + quad * 32 + lane;
-      const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-      const uint32_t tacc = tmem_base + lane_off + C::kAccCol + b * C::kAccBuf;
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        int sum[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) sum[j] = 0;
-#pragma unroll 1
-        for (int g = 0; g < G; ++g) {
-          if (!(used & (1u << g))) continue;
-          uint32_t x[32];
-          tmem_ld32(tacc + g * BN + c, x);  // (BN = 16: the next accumulator's columns are ignored)
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) sum[j] += static_cast<int>(x[j]);
-        }
-        if (n < p.N && used) {
-          const int sh = p.w8 ? 0 : 4;  // INT4: the MMAs summed 16 x the weight (exact shift)
-#pragma unroll
-          for (int j = 0; j < (BN < 32 ? BN : 32); ++j) {
-            const int t = c + j;
-            if (t < p.M) atomicAdd(&p.acc[static_cast<long long>(t) * p.N + n], sum[j] >> sh);
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[b]);
-      // completion: the last of this block's splits finalises it (writes -> fence ->
-      // counter; last arriver: fence -> reads)
-      __threadfence();
-      named_barrier_sync(1, 128);
-      if (lead && lane == 0) *last_flag = atomicAdd(&p.counters[nb], 1) == p.splits - 1;
-      named_barrier_sync(1, 128);
-      if (!*last_flag) continue;
-      __threadfence();
-      // (0) the first outlier tiles start loading while init is computed
-      constexpr uint32_t idesc_f16 = idesc_make(1u, 0u, kBlockM, BN);
       auto load_blocks = [&](int j0) {
         const int nblk = p.nout - j0 < 2 ? p.nout - j0 : 2;
         if (lane == 0) {
@@ -350,7 +313,64 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
         }
         return nblk;
       };
-      if (lead && p.nout) load_blocks(0);
+      // (0) the unit's first outlier tiles load while its K range streams (the buffer is
+      // free: the previous unit's finalisation completed before this loop iteration) when
+      // this unit will (one split) or most likely will (the block's last split, which
+      // the CTAs reach last) finalise its block
+      const bool prefetched = p.nout && p.prefetch && (direct || u / tiles_n == p.splits - 1);
+      if (lead && prefetched) load_blocks(0);
+      const int b = it & 1;
+      mbar_wait_sleep(&acc_full[b], (it >> 1) & 1);
+      tc_fence_after();
+      const int n = nb * kBlockM + quad * 32 + lane;
+      const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+      const uint32_t tacc = tmem_base + lane_off + C::kAccCol + b * C::kAccBuf;
+      int sum[32];
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) sum[j] = 0;
+#pragma unroll 1
+        for (int g = 0; g < G; ++g) {
+          if (!(used & (1u << g))) continue;
+          uint32_t x[32];
+          tmem_ld32(tacc + g * BN + c, x);  // (BN = 16: the next accumulator's columns are ignored)
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sum[j] += static_cast<int>(x[j]);
+        }
+        if (direct) {
+          const int sh = p.w8 ? 0 : 4;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sum[j] >>= sh;
+        } else if (n < p.N && used) {
+          const int sh = p.w8 ? 0 : 4;  // INT4: the MMAs summed 16 x the weight (exact shift)
+#pragma unroll
+          for (int j = 0; j < (BN < 32 ? BN : 32); ++j) {
+            const int t = c + j;
+            if (t < p.M) atomicAdd(&p.acc[static_cast<long long>(t) * p.N + n], sum[j] >> sh);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[b]);
+      // completion: the last of this block's splits finalises it (writes -> fence ->
+      // counter; last arriver: fence -> reads)
+      if (!direct) {
+        __threadfence();
+        named_barrier_sync(1, 128);
+        if (lead && lane == 0) *last_flag = atomicAdd(&p.counters[nb], 1) == p.splits - 1;
+        named_barrier_sync(1, 128);
+        if (!*last_flag) {
+          if (lead && prefetched) {  // the prefetched outlier tiles are not needed: retire the phase
+            mbar_wait(fin_full, fin_ld & 1);
+            ++fin_ld;
+          }
+          continue;
+        }
+        __threadfence();
+      }
       // (1) init = bias + dequant_element(acc) -> TMEM finalisation accumulator
       const uint32_t tfin = tmem_base + lane_off + C::kFinCol;
       {
@@ -365,12 +385,17 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
           const float sa_l = tl < p.M ? __ldg(&p.a_scale[tl]) : 0.f;
           const float zs_l = tl < p.M ? __fadd_rn(__ldg(&p.a_zero[tl]), __fmul_rn(p.half_range, sa_l)) : 0.f;  // runtime.cpp:74
           int32_t accv[BN < 32 ? BN : 32];
+          if (direct) {
 #pragma unroll
-          for (int j = 0; j < (BN < 32 ? BN : 32); ++j)
-            accv[j] = (c + j < p.M && nok) ? __ldcg(&p.acc[static_cast<long long>(c + j) * p.N + n]) : 0;
+            for (int j = 0; j < (BN < 32 ? BN : 32); ++j) accv[j] = sum[j];
+          } else {
 #pragma unroll
-          for (int j = 0; j < (BN < 32 ? BN : 32); ++j)
-            if (c + j < p.M && nok) p.acc[static_cast<long long>(c + j) * p.N + n] = 0;  // zeros for the next call
+            for (int j = 0; j < (BN < 32 ? BN : 32); ++j)
+              accv[j] = (c + j < p.M && nok) ? __ldcg(&p.acc[static_cast<long long>(c + j) * p.N + n]) : 0;
+#pragma unroll
+            for (int j = 0; j < (BN < 32 ? BN : 32); ++j)
+              if (c + j < p.M && nok) p.acc[static_cast<long long>(c + j) * p.N + n] = 0;  // zeros for the next call
+          }
           uint32_t v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
@@ -395,8 +420,9 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
       if (lead && p.nout) {
         tc_fence_after();
         for (int j0 = 0; j0 < p.nout; j0 += 2) {
-          const int nblk = j0 == 0 ? (p.nout < 2 ? p.nout : 2) : load_blocks(j0);
-          mbar_wait(fin_full, fin_uses & 1);
+          const int nblk = (j0 == 0 && prefetched) ? (p.nout < 2 ? p.nout : 2) : load_blocks(j0);
+          mbar_wait(fin_full, fin_ld & 1);
+          ++fin_ld;
           tc_fence_after();
           for (int q = 0; q < nblk; ++q) {
             const uint64_t ad = umma_desc_sw128(smem_u32(fin + q * C::kFinBlk));
@@ -405,8 +431,8 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
             for (int k = 0; k < 4; ++k) mma_f16_ss_e(tmem_base + C::kFinCol, ad + 2 * k, bd + 2 * k, idesc_f16, 1u);
           }
           commit_e(fin_mma);
-          mbar_wait(fin_mma, fin_uses & 1);  // MMAs done: buffer reusable, accumulator final
-          ++fin_uses;
+          mbar_wait(fin_mma, fin_mm & 1);  // MMAs done: buffer reusable, accumulator final
+          ++fin_mm;
         }
         tc_fence_before();
       }
@@ -470,7 +496,7 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
         }
       }
       tc_fence_before();
-      if (lead && lane == 0) p.counters[nb] = 0;
+      if (lead && lane == 0 && !direct) p.counters[nb] = 0;
       named_barrier_sync(1, 128);  // the finalisation accumulator is free again
     }
   }
@@ -544,6 +570,11 @@ cudaError_t launch_stream4(const Stream4Args& a, int num_sms, cudaStream_t strea
   }();
   if (splits_env > 0) splits = std::min(splits_env, sp.nstage);
   sp.splits = splits;
+  static const int prefetch_env = [] {  // tuning: QUIK_S4_PREFETCH=0 loads the outlier tiles at finalisation
+    const char* e = getenv("QUIK_S4_PREFETCH");
+    return e ? atoi(e) : 1;
+  }();
+  sp.prefetch = prefetch_env;
   sp.acc = a.acc;
   sp.counters = a.counters;
   sp.a_scale = a.a_scale;
