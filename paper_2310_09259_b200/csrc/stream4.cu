@@ -1,7 +1,10 @@
-// Weight-streaming split-K integer GEMM on INT4 weights for small token counts
-// (M <= 64, quik mode; HBM-bound for small M, cfg1 / cfg4 small M):
+// Weight-streaming integer GEMM on INT4 weights for small token counts (M <= 64, quik
+// mode; HBM-bound for small M, cfg1 / cfg4 small M). Each CTA walks a
+// sequence of segments (a 128-row weight block's K interval: round-robin units of whole
+// blocks or K splits, or a stream-K range, host-chosen); a whole block finalises from
+// registers, a cut one accumulates
 //
-//   acc_ws[t][n] += sum_{k in split} q[n][k] * X8[t][k]      (red.global.add.s32)
+//   acc_ws[t][n] += sum_{k in segment} q[n][k] * X8[t][k]      (red.global.add.s32)
 //
 // and, in the same kernel, the rest of the layer: the CTA that completes a weight block
 // last (per-block arrival counter) finalises it exactly as the fused kernel's epilogue
@@ -72,7 +75,8 @@ struct S4Params {
   CUtensorMap tm_x;   // int8 [M][kpad], box {128 B, BN}, SW128
   CUtensorMap tm_wo;  // f16 [N][opad] as bytes, box {128 B, 128}, SW128
   CUtensorMap tm_xo;  // f16 [M][opad] as bytes, box {128 B, BN}, SW128
-  int M, N, nstage, splits, nout;  // nstage: K stages (INT4 256 K, INT8 128 K); nout: 64-column outlier blocks
+  int M, N, nstage, nout;  // nstage: K stages (INT4 256 K, INT8 128 K); nout: 64-column outlier blocks
+  int splits;              // round-robin schedule: K splits per block (0: stream-K schedule)
   int w8;                          // INT8 weights (A from the weight ring, no widening)
   int32_t* acc;                    // [M][N] int32 workspace (zero on entry and exit)
   int* counters;                   // [tiles] arrivals per weight block (zero on entry and exit)
@@ -146,14 +150,48 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
   // weight stream and its widening start while K1 is still running.
 
   const int tiles_n = (p.N + kBlockM - 1) / kBlockM;
-  const int num_units = tiles_n * p.splits;
-  // unit -> (weight block, K split); consecutive units walk the blocks of one split
-  auto decode = [&](int u, int& nb, int& k0, int& k1) {
-    nb = u % tiles_n;
-    const int s = u / tiles_n;
-    k0 = static_cast<int>((static_cast<long long>(p.nstage) * s) / p.splits);
-    k1 = static_cast<int>((static_cast<long long>(p.nstage) * (s + 1)) / p.splits);
+  // Two schedules, walked identically by every role as a sequence of segments (one
+  // weight block's K interval each):
+  //  * round robin (p.splits > 0): unit u = blockIdx.x + j * gridDim.x is block
+  //    u % tiles_n, K split u / tiles_n of p.splits (whole blocks when p.splits == 1);
+  //  * stream-K (p.splits == 0): the (block, K stage) pairs, block-major, are cut into
+  //    gridDim.x contiguous equal ranges, one per CTA (no idle tail wave when the block
+  //    count is a poor multiple of the grid).
+  // A block cut into several segments is reduced through the workspace and finalised by
+  // the last of its contributors; a whole block finalises from registers.
+  // (32-bit state: two registers per role; the rest is re-read from the parameter space)
+  const int work = tiles_n * p.nstage;
+  struct Segs {
+    int pos, end;  // stream-K: the CTA's work range; round robin: unit index and unit count
+  };
+  auto segs = [&]() {
+    if (p.splits) return Segs{static_cast<int>(blockIdx.x), tiles_n * p.splits};
+    return Segs{static_cast<int>(static_cast<long long>(work) * blockIdx.x / gridDim.x),
+                static_cast<int>(static_cast<long long>(work) * (blockIdx.x + 1) / gridDim.x)};
+  };
+  auto next = [&](Segs& sg, int& nb, int& k0, int& k1) {
+    if (sg.pos >= sg.end) return false;
+    if (p.splits) {
+      nb = sg.pos % tiles_n;
+      const int sp = sg.pos / tiles_n;
+      k0 = (p.nstage * sp) / p.splits;
+      k1 = (p.nstage * (sp + 1)) / p.splits;
+      sg.pos += gridDim.x;
+      return true;
+    }
+    nb = sg.pos / p.nstage;
+    k0 = sg.pos - nb * p.nstage;
+    k1 = k0 + (sg.end - sg.pos) < p.nstage ? k0 + (sg.end - sg.pos) : p.nstage;
+    sg.pos += k1 - k0;
     return true;
+  };
+  // after next(): that was the CTA's last segment
+  auto done = [](const Segs& sg) { return sg.pos >= sg.end; };
+  // stream-K: CTA whose range holds work item x (the largest c with floor(c * work / grid) <= x)
+  auto owner = [&](int x) { return static_cast<int>(((x + 1LL) * gridDim.x - 1) / work); };
+  auto contributors = [&](int nb) {
+    if (p.splits) return p.splits;
+    return owner((nb + 1) * p.nstage - 1) - owner(nb * p.nstage) + 1;
   };
 
   if (warp == 0 || warp == C::kIssEnd) {
@@ -162,12 +200,10 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
       const uint64_t pol_x = policy_evict_last();   // code / x_o tiles are re-read by every block
       const bool wprod = warp == 0;
       if (!wprod) asm volatile("griddepcontrol.wait;" ::: "memory");  // K1's codes are complete
-      int bc = 0;
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
-        int nb, k0, k1;
-        decode(u, nb, k0, k1);
-        if (wprod && u + static_cast<int>(gridDim.x) >= num_units)
-          asm volatile("griddepcontrol.launch_dependents;");  // last unit: the next kernel may start its prologue
+      int bc = 0, nb, k0, k1;
+      for (Segs sg = segs(); next(sg, nb, k0, k1);) {
+        if (wprod && done(sg))
+          asm volatile("griddepcontrol.launch_dependents;");  // last segment: the next kernel may start its prologue
         {
           for (int i = k0; i < k1; ++i, ++bc) {
             if (wprod) {
@@ -197,10 +233,8 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
     // acc_full once per unit
     const int g = warp - C::kEpiEnd;
     constexpr uint32_t idesc_i8 = idesc_make(2u, 1u, kBlockM, BN);
-    int bc = 0, it = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
-      int nb, k0, k1;
-      decode(u, nb, k0, k1);
+    int bc = 0, it = 0, nb, k0, k1;
+    for (Segs sg = segs(); next(sg, nb, k0, k1); ++it) {
       const int b = it & 1;
       mbar_wait_sleep(&acc_empty[b], ((it >> 1) & 1) ^ 1);
       tc_fence_after();
@@ -246,10 +280,8 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
     const int quad = warp & 3, g = (warp - 2) >> 2;
     const int r = quad * 32 + lane;
     const uint32_t a_tm = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + g * kS4TmemA;
-    int bc = 0;
-    for (int u = blockIdx.x; u < num_units && !p.w8; u += gridDim.x) {  // (INT8: nothing to widen)
-      int nb, k0, k1;
-      decode(u, nb, k0, k1);
+    int bc = 0, nb, k0, k1;
+    for (Segs sg = segs(); !p.w8 && next(sg, nb, k0, k1);) {  // (INT8: nothing to widen)
       for (int i = k0; i < k1; ++i, ++bc) {
         if (bc % G != g) continue;
         const int st = bc % C::kStagesW;
@@ -289,14 +321,13 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
     const int quad = warp & 3;
     const bool lead = warp == C::kWidenEnd;  // issues the finalisation TMA loads / MMAs
     asm volatile("griddepcontrol.wait;" ::: "memory");  // K1's scales / outlier columns
-    int it = 0, bc0 = 0, fin_ld = 0, fin_mm = 0;
-    // one K split with BN <= 32: the unit's sums stay in registers and finalise at once
-    // (no workspace round trip, no arrival counter)
-    const bool direct = p.splits == 1 && BN <= 32;
+    int it = 0, bc0 = 0, fin_ld = 0, fin_mm = 0, nb, k0, k1;
     constexpr uint32_t idesc_f16 = idesc_make(1u, 0u, kBlockM, BN);
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++it) {
-      int nb, k0, k1;
-      decode(u, nb, k0, k1);
+    for (Segs sg = segs(); next(sg, nb, k0, k1); ++it) {
+      const int ncontrib = contributors(nb);
+      // a block inside this CTA's range (BN <= 32): the sums stay in registers and
+      // finalise at once (no workspace round trip, no arrival counter)
+      const bool direct = ncontrib == 1 && BN <= 32;
       uint32_t used = 0;
       for (int k = 0; k < k1 - k0 && k < G; ++k) used |= 1u << ((bc0 + k) % G);
       bc0 += k1 - k0;
@@ -313,11 +344,14 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
         }
         return nblk;
       };
-      // (0) the unit's first outlier tiles load while its K range streams (the buffer is
-      // free: the previous unit's finalisation completed before this loop iteration) when
-      // this unit will (one split) or most likely will (the block's last split, which
-      // the CTAs reach last) finalise its block
-      const bool prefetched = p.nout && p.prefetch && (direct || u / tiles_n == p.splits - 1);
+      // (0) the segment's first outlier tiles load while its K range streams (the buffer is
+      // free: the previous segment's finalisation completed before this loop iteration)
+      // when this CTA will (a whole block) or most likely will finalise the block: round
+      // robin, the block's last split (the CTAs reach it last); stream-K, a cut block's
+      // head segment, the last one its CTA reaches (the other contributors streamed their
+      // parts at the start of their ranges)
+      const bool prefetched =
+          p.nout && p.prefetch && (direct || (p.splits ? k1 == p.nstage : (k0 == 0 && done(sg))));
       if (lead && prefetched) load_blocks(0);
       const int b = it & 1;
       mbar_wait_sleep(&acc_full[b], (it >> 1) & 1);
@@ -355,12 +389,12 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[b]);
-      // completion: the last of this block's splits finalises it (writes -> fence ->
+      // completion: the last of this block's contributors finalises it (writes -> fence ->
       // counter; last arriver: fence -> reads)
       if (!direct) {
         __threadfence();
         named_barrier_sync(1, 128);
-        if (lead && lane == 0) *last_flag = atomicAdd(&p.counters[nb], 1) == p.splits - 1;
+        if (lead && lane == 0) *last_flag = atomicAdd(&p.counters[nb], 1) == ncontrib - 1;
         named_barrier_sync(1, 128);
         if (!*last_flag) {
           if (lead && prefetched) {  // the prefetched outlier tiles are not needed: retire the phase
@@ -515,7 +549,8 @@ cudaError_t launch_s4(const S4Params& sp, int num_sms, cudaStream_t stream) {
   auto kern = stream4_gemm_kernel<BN>;
   cudaError_t e = ensure_smem_attr(kern, C::kSmemBytes);
   if (e != cudaSuccess) return e;
-  const int units = ((sp.N + kBlockM - 1) / kBlockM) * sp.splits;
+  const long long tiles = (sp.N + kBlockM - 1) / kBlockM;
+  const long long units = sp.splits ? tiles * sp.splits : tiles * sp.nstage;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(units < num_sms ? units : num_sms));
   cfg.blockDim = dim3(C::kThreads);
@@ -531,10 +566,11 @@ cudaError_t launch_s4(const S4Params& sp, int num_sms, cudaStream_t stream) {
 
 }  // namespace
 
-// Measured (profiles/r1_stream4.jsonl, K1 + this kernel, graph replay): OPT-66B fc1
-// (9216 -> 36864, 256 outliers) M = 1: 43 us, M = 16: 45.5 us (fused kernel on INT8
-// tiles: 65 us; cuBLAS f16: 110 us); cfg1 4096^2 M = 16: 14.6 us (18.6). On for 4-bit layers
-// at M <= 32 (QUIK_STREAM4=0 / quik_set_int4_decode(0) disables).
+// Measured (profiles/r2_decode_sweep.jsonl, K1 + this kernel, 10 forwards per CUDA
+// graph): OPT-66B fc1 (9216 -> 36864, 256 outliers) M = 1: 33 us, M = 16: 37 us (cuBLAS
+// f16: 108 us); LLaMA-2-70B up (8192 -> 28672) M = 1: 31 us; Falcon-180B fc1 M = 1: 79 us
+// (cuBLAS 267 us). On for 4-bit layers at M <= 32 (QUIK_STREAM4=0 /
+// quik_set_int4_decode(0) disables).
 int gemm_stream4_auto = [] {
   const char* e = getenv("QUIK_STREAM4");
   return e ? atoi(e) : 1;
@@ -555,20 +591,35 @@ cudaError_t launch_stream4(const Stream4Args& a, int num_sms, cudaStream_t strea
   sp.w8 = a.w4 ? 0 : 1;
   sp.nstage = static_cast<int>(sp.w8 ? a.kpad / 128 : (a.kpad + 255) / 256);
   sp.nout = static_cast<int>(a.opad / 64);
-  // K splits: minimise the busiest CTA's stage count (see wo.cu)
+  // Round robin with K splits minimising the busiest CTA's stage count (see wo.cu), or
+  // stream-K when that is clearly cheaper. Costs in weight stages per CTA: round robin
+  // waves x (stages per unit + 1, + 2 per reduced unit: a split block's workspace
+  // reduction, 7B up / gate M = 16 13.8 us in one split vs 18.7 us in three); stream-K the CTA's range + 8
+  // (its cut blocks finalise through the workspace at the end of the ranges), and only
+  // for ranges of >= 24 stages (shorter ranges are dominated by the per-segment
+  // epilogues). Measured: 70B up / gate (28672 x 8192) M = 1 39.6 -> 33 us and
+  // Falcon-180B fc1 M = 1 94 -> 82 us with stream-K; 7B up / gate M = 16 19.3 us round
+  // robin vs 22.8 stream-K.
   const long long tiles = (a.N + kBlockM - 1) / kBlockM;
   int splits = 1;
   long long best = -1;
   for (int s = 1; s <= 16 && s <= sp.nstage; ++s) {
     const long long waves = (tiles * s + num_sms - 1) / num_sms;
-    const long long cost = waves * ((sp.nstage + s - 1) / s + 1);
+    const long long cost = waves * ((sp.nstage + s - 1) / s + 1 + (s > 1 ? 2 : 0));
     if (best < 0 || cost < best) { best = cost; splits = s; }
   }
-  static const int splits_env = [] {  // tuning: QUIK_S4_SPLITS forces the K split count
+  {
+    const long long units = tiles * splits, waves = (units + num_sms - 1) / num_sms;
+    const long long rr = waves * ((sp.nstage + splits - 1) / splits + 1 + (splits > 1 ? 2 : 0));
+    const long long range = (tiles * sp.nstage + num_sms - 1) / num_sms;
+    if (range >= 24 && rr * 100 > 115 * (range + 8)) splits = 0;
+  }
+  static const int sched_env = [] {  // tuning: QUIK_S4_SPLITS=n forces n round-robin K splits, -1 stream-K
     const char* e = getenv("QUIK_S4_SPLITS");
     return e ? atoi(e) : 0;
   }();
-  if (splits_env > 0) splits = std::min(splits_env, sp.nstage);
+  if (sched_env > 0) splits = std::min(sched_env, sp.nstage);
+  if (sched_env < 0) splits = 0;
   sp.splits = splits;
   static const int prefetch_env = [] {  // tuning: QUIK_S4_PREFETCH=0 loads the outlier tiles at finalisation
     const char* e = getenv("QUIK_S4_PREFETCH");

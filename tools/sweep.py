@@ -32,6 +32,14 @@ SHAPES = [
     ("cfg4 Falcon-180B fc1 M=2048", 2048, 14848, 59392, 256, 4),
     ("cfg4 Falcon-180B fc2 W8A8 M=2048", 2048, 59392, 14848, 1024, 8),
     ("cfg4 Falcon-180B qkv M=2048", 2048, 14848, 14848, 256, 4),
+    # decode regime (M <= 32): the INT4 decode kernel
+    ("decode cfg1 M=32", 32, 4096, 4096, 128, 4),
+    ("decode 70B up/gate M=1", 1, 8192, 28672, 256, 4),
+    ("decode 70B up/gate M=16", 16, 8192, 28672, 256, 4),
+    ("decode 70B up/gate M=32", 32, 8192, 28672, 256, 4),
+    ("decode OPT-66B fc1 M=32", 32, 9216, 36864, 256, 4),
+    ("decode 7B up/gate M=16", 16, 4096, 11008, 256, 4),
+    ("decode 70B down W8A8 M=16", 16, 28672, 8192, 896, 8),
 ]
 OPT_FC1 = [(m, 9216, 36864, 256, 4) for m in (1, 16, 64, 128, 256, 512, 1024, 2048, 4096, 8192)]
 FALCON_FC1 = [(m, 14848, 59392, 256, 4) for m in (1, 16, 128, 512, 2048, 8192)]
@@ -51,6 +59,7 @@ def timeit(fn, iters=20, warm=5):
 
 
 WEIGHTS = "speed"
+REPS = 10  # forwards per CUDA graph
 
 
 def run(name, M, K, N, O, bits, layers, sparse=False):
@@ -78,11 +87,13 @@ def run(name, M, K, N, O, bits, layers, sparse=False):
     for e in mid:  # materialise the raw cudaEvent handles
         e.record()
     t_step_eager = timeit(lambda: layer.forward(x, out=y))
-    # CUDA graph of the forward (removes host launch overhead, visible at small M)
+    # CUDA graph of REPS back-to-back forwards (removes host launch overhead; a graph of
+    # one small forward is timed at the graph-launch granularity, ~2 us steps, instead)
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
-        layer.forward(x, out=y)
-    t_step = timeit(g.replay)
+        for _ in range(REPS):
+            layer.forward(x, out=y)
+    t_step = timeit(g.replay) / REPS
     # kernel split from one instrumented call
     for _ in range(3):
         mid[0].record()
@@ -94,8 +105,9 @@ def run(name, M, K, N, O, bits, layers, sparse=False):
     g16 = torch.cuda.CUDAGraph()
     torch.matmul(x, W16.t(), out=out16)
     with torch.cuda.graph(g16):
-        torch.matmul(x, W16.t(), out=out16)
-    t16 = timeit(g16.replay)
+        for _ in range(REPS):
+            torch.matmul(x, W16.t(), out=out16)
+    t16 = timeit(g16.replay) / REPS
     ops = 2.0 * M * N * K
     return dict(name=name, M=M, K=K, N=N, O=O, bits=bits, sparse=layer.is_sparse, weights=WEIGHTS,
                 layer_mb=layer.device_bytes / 1e6, step_ms=t_step, step_eager_ms=t_step_eager,
