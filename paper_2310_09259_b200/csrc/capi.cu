@@ -214,6 +214,9 @@ struct quik_layer_s {
   uint32_t* chunk_desc = nullptr;  // [kpad / 16] x uint4 hot-quantizer compaction descriptors
   uint16_t* gen_chunk = nullptr;   // [n_gen] chunks gathered per byte
   int n_gen = 0;
+  // wide-row K1 slices (kernels.h QuantArgs::slice_desc), n_slice == 0: one CTA per row
+  int32_t* slice_desc = nullptr;
+  int n_slice = 0, slice_cols_max = 0, slice_chunks_max = 0, slice_code_bytes = 0;
 };
 
 namespace {
@@ -252,6 +255,96 @@ quik_status on_stream(quik_ctx_t ctx, cudaStream_t st, F&& f) {
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Wide rows: split each row of K1 over a cluster of CTAs (quantize.cu
+// quantize_wide_kernel). Slice boundaries sit at output-chunk boundaries near c * K / C;
+// a slice loads the columns from its first base column (rounded down to a 16-byte
+// vector) to the next slice's start or its last base column (rounded up), whichever is
+// later, so every column is loaded by some slice and neighbours overlap by < 8 columns.
+// Outlier slots go to the slice whose [start, next start) holds their column.
+// Used where one CTA per row cannot hold a row (K > 32768: OPT-66B fc2, Falcon-180B fc2);
+// the per-row cluster exchange makes it slower than the one-CTA kernel below that
+// (70B down 28672: 128 us in 2 slices vs 110 us). QUIK_K1_WIDE_MIN_K (default 32769) /
+// QUIK_K1_SLICE_COLS (8192) tune it.
+void build_k1_slices(quik_layer_s* L, const std::vector<int32_t>& base_src, const std::vector<int32_t>& out_src,
+                     const std::vector<uint16_t>& gen, int64_t kr16) {
+  static const int64_t min_k = [] {
+    const char* e = getenv("QUIK_K1_WIDE_MIN_K");
+    return e ? atoll(e) : 32769LL;
+  }();
+  static const int64_t slice_cols = [] {
+    const char* e = getenv("QUIK_K1_SLICE_COLS");
+    return e ? std::max(1024LL, atoll(e)) : 8192LL;
+  }();
+  const int64_t K = L->in_features, kb = L->kb, nch = L->kpad / 16;
+  if (K < min_k || kb < 64 || K % 8) return;
+  const int64_t nch_base = (kb + 15) / 16;  // chunks holding base positions
+  int C = static_cast<int>(std::min<int64_t>(8, (K + slice_cols - 1) / slice_cols));
+  if (C < 2) return;
+  std::vector<int64_t> ch_lo;
+  for (;; --C) {
+    ch_lo.assign(1, 0);
+    bool ok = true;
+    for (int c = 1; c < C && ok; ++c) {
+      const int64_t T = c * K / C;
+      const int64_t pos = std::lower_bound(base_src.begin(), base_src.end(), static_cast<int32_t>(T)) - base_src.begin();
+      const int64_t ch = pos / 16;
+      ok = ch > ch_lo.back() && ch < nch_base;
+      ch_lo.push_back(ch);
+    }
+    if (ok) break;
+    if (C == 2) return;
+  }
+  ch_lo.push_back(nch);
+  std::vector<int64_t> in_lo(C + 1);
+  for (int c = 0; c < C; ++c) in_lo[c] = c == 0 ? 0 : (base_src[16 * ch_lo[c]] & ~int64_t{7});
+  in_lo[C] = K;
+  std::vector<int32_t> desc(static_cast<size_t>(8 * C));
+  int64_t cols_max = 0, chunks_max = 0, code_bytes = 0;
+  for (int c = 0; c < C; ++c) {
+    const int64_t last_pos = std::min<int64_t>(16 * ch_lo[c + 1], kb) - 1;
+    int64_t hi = c == C - 1 ? K : std::max(in_lo[c + 1], (static_cast<int64_t>(base_src[last_pos]) + 8) & ~int64_t{7});
+    hi = std::min(hi, K);
+    const int64_t n = hi - in_lo[c];
+    auto first_out = [&](int64_t col) {
+      return static_cast<int64_t>(std::lower_bound(out_src.begin(), out_src.end(), static_cast<int32_t>(col)) - out_src.begin());
+    };
+    const int64_t o_lo = c == 0 ? 0 : first_out(in_lo[c]);
+    const int64_t o_hi = c == C - 1 ? L->opad : first_out(in_lo[c + 1]);
+    auto first_gen = [&](int64_t ch) {
+      return static_cast<int64_t>(std::lower_bound(gen.begin(), gen.end(), static_cast<uint16_t>(ch)) - gen.begin());
+    };
+    const int64_t g_lo = first_gen(ch_lo[c]), g_hi = c == C - 1 ? static_cast<int64_t>(gen.size()) : first_gen(ch_lo[c + 1]);
+    int32_t* d = &desc[static_cast<size_t>(8 * c)];
+    d[0] = static_cast<int32_t>(in_lo[c]);
+    d[1] = static_cast<int32_t>(n);
+    d[2] = static_cast<int32_t>(ch_lo[c]);
+    d[3] = static_cast<int32_t>(ch_lo[c + 1]);
+    d[4] = static_cast<int32_t>(o_lo);
+    d[5] = static_cast<int32_t>(o_hi);
+    d[6] = static_cast<int32_t>(g_lo);
+    d[7] = static_cast<int32_t>(g_hi);
+    cols_max = std::max(cols_max, n);
+    chunks_max = std::max(chunks_max, ch_lo[c + 1] - ch_lo[c]);
+    // window reads run up to 20 bytes past a chunk's source; the last slice also holds
+    // the pad positions' zero codes at kr16
+    code_bytes = std::max(code_bytes, std::max(n, c == C - 1 ? kr16 - in_lo[c] : 0) + 32);
+  }
+  QK_CUDA(cudaMalloc(&L->slice_desc, desc.size() * 4));
+  QK_CUDA(cudaMemcpy(L->slice_desc, desc.data(), desc.size() * 4, cudaMemcpyHostToDevice));
+  L->n_slice = C;
+  L->slice_cols_max = static_cast<int>(cols_max);
+  L->slice_chunks_max = static_cast<int>(chunks_max);
+  L->slice_code_bytes = static_cast<int>(round_up(code_bytes, 128));
+}
+
+void set_slices(QuantArgs& q, const quik_layer_s* L) {
+  q.slice_desc = L->slice_desc;
+  q.n_slice = L->n_slice;
+  q.slice_cols_max = L->slice_cols_max;
+  q.slice_chunks_max = L->slice_chunks_max;
+  q.slice_code_bytes = L->slice_code_bytes;
+}
+
 // Runs K1 into the context scratch (GEMM layout) for the hot path.
 void run_k1(quik_ctx_t ctx, const quik_layer_s* L, const void* x, quik_dtype xdt, int64_t M, cudaStream_t st) {
   QuantArgs q{};
@@ -265,6 +358,7 @@ void run_k1(quik_ctx_t ctx, const quik_layer_s* L, const void* x, quik_dtype xdt
   q.chunk_desc = L->chunk_desc;
   q.gen_chunk = L->gen_chunk;
   q.n_gen = L->n_gen;
+  set_slices(q, L);
   q.out_src = L->out_src;
   q.kb = L->kb;
   q.n_out = L->n_outlier;
@@ -535,6 +629,7 @@ quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* d, quik_l
       QK_CUDA(cudaMemcpy(L->chunk_desc, desc.data(), nch * 16, cudaMemcpyHostToDevice));
       QK_CUDA(cudaMalloc(&L->gen_chunk, std::max<size_t>(gen.size(), 1) * 2));
       if (!gen.empty()) QK_CUDA(cudaMemcpy(L->gen_chunk, gen.data(), gen.size() * 2, cudaMemcpyHostToDevice));
+      build_k1_slices(L, base_src, out_src, gen, kr16);
     }
     if (rows > 0) {
       QK_CUDA(cudaMalloc(&L->w_scale, rows * 4));
@@ -694,6 +789,7 @@ quik_status quik_layer_destroy(quik_layer_t L) {
   cudaFree(L->gather);
   cudaFree(L->chunk_desc);
   cudaFree(L->gen_chunk);
+  cudaFree(L->slice_desc);
   delete L;
   return QUIK_OK;
 }
@@ -763,6 +859,7 @@ quik_status quik_quantize_activations_gemm(quik_ctx_t ctx, quik_layer_t L, const
       q.chunk_desc = L->chunk_desc;
       q.gen_chunk = L->gen_chunk;
       q.n_gen = L->n_gen;
+      set_slices(q, L);
       q.out_src = L->out_src;
       q.kb = L->kb;
       q.n_out = L->n_outlier;

@@ -226,6 +226,15 @@ struct QuantArgs {
   int64_t opad;
   float* xo32;              // [M][n_out] fp32 outliers (ABI) or nullptr
   int* err;                 // device flag, set to 1 on non-finite base input
+  // Row slices of the wide hot quantizer (K1 over a thread-block cluster, one CTA per
+  // slice; n_slice >= 2): slice_desc [n_slice] x int32[8] = {first column (multiple of
+  // 8), columns, first / end output chunk, first / end outlier slot, first / end index
+  // into gen_chunk}; the sizes below are maxima over the slices.
+  const int32_t* slice_desc;
+  int n_slice;
+  int slice_cols_max;       // columns of the widest slice
+  int slice_chunks_max;     // output chunks of the busiest slice
+  int slice_code_bytes;     // shared code-row bytes (window reads and the zero tail included)
 };
 cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t stream);
 

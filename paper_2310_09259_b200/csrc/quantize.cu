@@ -13,6 +13,8 @@
 #include <cfloat>
 #include <cstdlib>
 
+#include <cstdio>
+
 #include "kernels.h"
 #include "sm100.cuh"
 
@@ -779,6 +781,321 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(cons
   }
 }
 
+// Wide rows (K beyond one CTA's ring: OPT-66B fc2 36864, Falcon-180B fc2 59392, the
+// 28672-wide down projections): the hot kernel's algorithm with each row split over a
+// thread-block cluster, one CTA per slice (quik_layer_create builds the slices: a
+// contiguous column range covering a contiguous range of output chunks and outlier
+// slots, neighbouring slices overlapping by < 8 columns). Each CTA streams its slice of
+// every row through its own TMA ring, reduces min / max over its base columns, and the
+// cluster exchanges the partials through distributed shared memory (every CTA stores
+// its partial into every peer's slot [row parity][rank] with st.async, which completes
+// transaction bytes on the peer's mbarrier; min / max are order independent, so all CTAs reach the same row
+// scale). Codes, compaction (window offsets rebased to the slice) and the outlier copy
+// then stay inside the CTA. The rare exact paths (near-tie quotients; the sign of a zero
+// minimum, which takes a second cluster exchange of the first zero's key) match the hot
+// kernel's, so the codes are bit-identical to it and to the reference.
+template <int BITS, int VPT>
+__global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_wide_kernel(const QuantArgs a, int stages, int row_stride) {
+  extern __shared__ __align__(128) uint8_t s_dyn[];
+  __shared__ float s_min[16], s_max[16];
+  __shared__ int s_nf[16];
+  __shared__ unsigned s_key[16];
+  __shared__ __align__(8) uint64_t s_full[8];
+  __shared__ __align__(16) uint4 s_x[2][8];  // [row parity][rank]: min, max, non-finite (bits)
+  __shared__ __align__(16) uint4 s_k[2][8];  // zero-minimum key exchange
+  __shared__ __align__(8) uint64_t s_xbar[2], s_kbar[2];
+  constexpr int kHr = 1 << (BITS - 1);
+  constexpr float kLevels = static_cast<float>((1 << BITS) - 1);
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int tid = threadIdx.x;
+  const int nt = blockDim.x;
+  const int nwarps = (nt + 31) >> 5;
+  const uint32_t rank = cluster_ctarank();
+  const int C = a.n_slice;
+  const int4 sd0 = __ldg(reinterpret_cast<const int4*>(a.slice_desc) + 2 * rank);
+  const int4 sd1 = __ldg(reinterpret_cast<const int4*>(a.slice_desc) + 2 * rank + 1);
+  const int in_lo = sd0.x, in_n = sd0.y, ch_lo = sd0.z, ch_hi = sd0.w;
+  const int o_lo = sd1.x, o_hi = sd1.y, g_lo = sd1.z, g_hi = sd1.w;
+  const int K = static_cast<int>(a.K);
+  const int M = static_cast<int>(a.M);
+  const int nvec = in_n >> 3;
+  auto in_row = [&](int v) { return v < nvec; };
+  const int kr16 = (K + 15) & ~15;
+  const uint32_t row_bytes = static_cast<uint32_t>(in_n) * 2u;
+  const int code_stride = a.slice_code_bytes;
+  uint8_t* s_codes = s_dyn;                // [code_stride]: codes by local column, zero tail
+  uint8_t* s_ring = s_dyn + code_stride;   // [stages][row_stride]
+  const bool has_out = a.lane_mask != nullptr;
+  const __half* xg = reinterpret_cast<const __half*>(a.x) + in_lo;
+  const uint4* cdesc = reinterpret_cast<const uint4*>(a.chunk_desc);
+  const int first_base = static_cast<int>(a.gather[16 * ch_lo]) - in_lo;  // a base column of the slice
+  const int cl = blockIdx.x / C, ncl = gridDim.x / C;
+
+  uint2 lm[VPT];
+  uint4 lmw[VPT];
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int v = tid + i * nt;
+    lm[i] = (has_out && in_row(v)) ? __ldg(reinterpret_cast<const uint2*>(a.lane_mask + in_lo) + v) : make_uint2(0u, 0u);
+    lmw[i] = make_uint4(__byte_perm(lm[i].x, 0u, 0x1100u), __byte_perm(lm[i].x, 0u, 0x3322u),
+                        __byte_perm(lm[i].y, 0u, 0x1100u), __byte_perm(lm[i].y, 0u, 0x3322u));
+  }
+  // this CTA's outlier slots i = o_lo + tid (+ nt): source column in the slice, -1 = zero pad
+  int osrc[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int i = o_lo + tid + j * nt;
+    osrc[j] = (has_out && i < o_hi && i < a.n_out) ? __ldg(&a.out_src[i]) - in_lo : -1;
+  }
+  const int opad = static_cast<int>(a.opad);
+  const bool xo_hoisted = o_hi - o_lo <= 2 * nt;
+
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&s_full[s], 1);
+    // exchange barriers: this CTA's arrive (with C x 16 bytes expected) + the C peers'
+    // st.async completions
+    for (int s = 0; s < 2; ++s) { mbar_init(&s_xbar[s], 1); mbar_init(&s_kbar[s], 1); }
+    fence_mbar_init();
+  }
+  if (rank == static_cast<uint32_t>(C - 1) && tid < 8)  // zero codes of the pad positions (kr16 + q)
+    reinterpret_cast<uint32_t*>(s_codes + (kr16 - in_lo))[tid] = 0u;
+  __syncthreads();
+  cluster_sync();  // every peer's exchange barriers are initialised before the first remote arrive
+  if (tid == 0) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (int s = 0; s < stages; ++s) {
+      const int r = cl + s * ncl;
+      if (r >= M) break;
+      mbar_arrive_expect_tx(&s_full[s], row_bytes);
+      bulk_load_1d(s_ring + s * row_stride, xg + static_cast<int64_t>(r) * a.ldx, row_bytes, &s_full[s]);
+    }
+  }
+
+  int s = 0, it = 0, kround = 0;
+  uint32_t ph = 0;
+#pragma unroll 1
+  for (int t = cl; t < M; t += ncl, ++it) {
+    const uint4* srow = reinterpret_cast<const uint4*>(s_ring + s * row_stride);
+    mbar_wait(&s_full[s], ph);
+    uint4 raw[VPT];
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int v = tid + i * nt;
+      raw[i] = in_row(v) ? srow[v] : make_uint4(0, 0, 0, 0);
+    }
+    uint16_t xov[2] = {0, 0};
+    if (a.xo16 && xo_hoisted) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (osrc[j] >= 0) xov[j] = reinterpret_cast<const uint16_t*>(srow)[osrc[j]];
+    }
+    // ---- pass 1: packed min / max over the slice's base columns
+    __half2 hmin = u2h2(0x7C007C00u), hmax = u2h2(0xFC00FC00u);
+    {
+      const uint32_t h0 = reinterpret_cast<const uint16_t*>(srow)[first_base];
+      const uint32_t fill = h0 | (h0 << 16);
+#pragma unroll
+      for (int i = 0; i < VPT; ++i) {
+        if (!in_row(tid + i * nt)) continue;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const uint32_t mk = (&lmw[i].x)[w];
+          const __half2 x2 = u2h2(((&raw[i].x)[w] & ~mk) | (fill & mk));
+          hmin = __hmin2_nan(hmin, x2);
+          hmax = __hmax2_nan(hmax, x2);
+        }
+      }
+    }
+    float vmin, vmax;
+    int nonfinite;
+    {
+      const float2 fmn = __half22float2(hmin);
+      const float2 fmx = __half22float2(hmax);
+      nonfinite = isnan(fmn.x) || isnan(fmn.y) || isnan(fmx.x) || isnan(fmx.y) || fmx.x == INFINITY ||
+                  fmx.y == INFINITY || fmn.x == -INFINITY || fmn.y == -INFINITY;
+      vmin = fminf(fmn.x, fmn.y);
+      vmax = fmaxf(fmx.x, fmx.y);
+    }
+    vmin = redux_min(vmin);
+    vmax = redux_max(vmax);
+    nonfinite = __reduce_or_sync(0xffffffffu, nonfinite);
+    if ((tid & 31) == 0) { s_min[tid >> 5] = vmin; s_max[tid >> 5] = vmax; s_nf[tid >> 5] = nonfinite; }
+    __syncthreads();  // (A)
+    const int xp = it & 1;
+    if (tid == 0) {
+      const int rn = t + stages * ncl;
+      if (rn < M) {
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&s_full[s], row_bytes);
+        bulk_load_1d(s_ring + s * row_stride, xg + static_cast<int64_t>(rn) * a.ldx, row_bytes, &s_full[s]);
+      }
+    }
+    if (tid < 32) {
+      // the CTA's partial -> every CTA of the cluster
+      const int l = tid;
+      float m0 = redux_min(l < nwarps ? s_min[l] : INFINITY);
+      float m1 = redux_max(l < nwarps ? s_max[l] : -INFINITY);
+      const int nf = __reduce_or_sync(0xffffffffu, l < nwarps ? s_nf[l] : 0);
+      if (l == 0) mbar_arrive_expect_tx(&s_xbar[xp], 16u * C);
+      if (l < C)
+        st_async_cluster_v4(&s_x[xp][rank], static_cast<uint32_t>(l),
+                            make_uint4(__float_as_uint(m0), __float_as_uint(m1), static_cast<uint32_t>(nf), 0u),
+                            &s_xbar[xp]);
+    }
+    mbar_wait(&s_xbar[xp], (it >> 1) & 1);
+    {
+      const int l = tid & 31;
+      const uint4 px = l < C ? s_x[xp][l] : make_uint4(__float_as_uint(INFINITY), __float_as_uint(-INFINITY), 0u, 0u);
+      vmin = redux_min(__uint_as_float(px.x));
+      vmax = redux_max(__uint_as_float(px.y));
+      nonfinite = __reduce_or_sync(0xffffffffu, static_cast<int>(px.z));
+    }
+    if (vmin == 0.0f) {
+      // rare: the sign of a zero minimum is the first-seen zero's (cluster-uniform branch)
+      unsigned key = 0xFFFFFFFFu;
+#pragma unroll
+      for (int i = 0; i < VPT; ++i) {
+        const int v = tid + i * nt;
+        if (!in_row(v)) continue;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float x = elem<__half>(raw[i], e);
+          const uint32_t mbyte = ((e < 4 ? lm[i].x : lm[i].y) >> (8 * (e & 3))) & 0xFFu;
+          if (mbyte == 0 && x == 0.0f) {
+            const unsigned k = (static_cast<unsigned>(in_lo + v * 8 + e) << 1) | (__float_as_uint(x) >> 31);
+            key = k < key ? k : key;
+          }
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const unsigned o = __shfl_xor_sync(0xffffffffu, key, off);
+        key = o < key ? o : key;
+      }
+      if ((tid & 31) == 0) s_key[tid >> 5] = key;
+      __syncthreads();
+      const int kp = kround & 1;
+      if (tid < 32) {
+        unsigned k = 0xFFFFFFFFu;
+        for (int w = 0; w < nwarps; ++w) k = s_key[w] < k ? s_key[w] : k;
+        if (tid == 0) mbar_arrive_expect_tx(&s_kbar[kp], 16u * C);
+        if (tid < C)
+          st_async_cluster_v4(&s_k[kp][rank], static_cast<uint32_t>(tid), make_uint4(k, 0u, 0u, 0u), &s_kbar[kp]);
+      }
+      mbar_wait(&s_kbar[kp], (kround >> 1) & 1);
+      ++kround;
+      key = 0xFFFFFFFFu;
+      for (int r = 0; r < C; ++r) key = s_k[kp][r].x < key ? s_k[kp][r].x : key;
+      vmin = (key & 1u) ? -0.0f : 0.0f;
+    }
+    const float range = __fsub_rn(vmax, vmin);
+    const float scale = range == 0.0f ? 1.0f : __fdiv_rn(range, kLevels);
+    const float rcp = __frcp_rn(scale);
+    if (tid == 0 && rank == 0) {
+      if (nonfinite && a.err) atomicExch(a.err, 1);
+      a.scale[t] = scale;
+      a.zero[t] = vmin;
+    }
+    const float rcp_lo = __fmul_rd(rcp, 1.0f - 0x1p-20f), rcp_hi = __fmul_ru(rcp, 1.0f + 0x1p-20f);
+    const unsigned long long rlo2 = f32x2_pack(rcp_lo, rcp_lo), rhi2 = f32x2_pack(rcp_hi, rcp_hi);
+    constexpr float kMagic = 12582912.0f - static_cast<float>(kHr);
+    const unsigned long long magic2 = f32x2_pack(kMagic, kMagic);
+
+    // ---- pass 2: codes for every column of the slice
+    uint32_t near_vec = 0;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int v = tid + i * nt;
+      if (!in_row(v)) continue;
+      uint32_t tb[8];
+      uint32_t diff = 0;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const uint32_t xw = (&raw[i].x)[w];
+        const unsigned long long d2 = f32x2_pack(sub_f16_f32(xw & 0xFFFFu, vmin), sub_f16_f32(xw >> 16, vmin));
+        unsigned long long tl2, th2;
+        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(tl2) : "l"(d2), "l"(rlo2), "l"(magic2));
+        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(th2) : "l"(d2), "l"(rhi2), "l"(magic2));
+        const uint32_t l0 = static_cast<uint32_t>(tl2), l1 = static_cast<uint32_t>(tl2 >> 32);
+        diff |= (l0 ^ static_cast<uint32_t>(th2)) | (l1 ^ static_cast<uint32_t>(th2 >> 32));
+        tb[2 * w] = l0;
+        tb[2 * w + 1] = l1;
+      }
+      near_vec |= (diff != 0u ? 1u : 0u) << i;
+      const uint32_t w0 = __byte_perm(__byte_perm(tb[0], tb[1], 0x0040), __byte_perm(tb[2], tb[3], 0x0040), 0x5410);
+      const uint32_t w1 = __byte_perm(__byte_perm(tb[4], tb[5], 0x0040), __byte_perm(tb[6], tb[7], 0x0040), 0x5410);
+      *reinterpret_cast<uint2*>(s_codes + v * 8) = make_uint2(w0, w1);
+    }
+    if (near_vec) {
+#pragma unroll 1
+      for (uint32_t nv = near_vec; nv; nv &= nv - 1) {
+        const int iv = __ffs(nv) - 1;
+        const int v = tid + iv * nt;
+        uint4 rv = raw[0];
+#pragma unroll
+        for (int i = 1; i < VPT; ++i)
+          if (i == iv) rv = raw[i];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int c = v * 8 + e;
+          const uint32_t hw = (&rv.x)[e >> 1];
+          const float d = __fsub_rn(__half2float(__ushort_as_half(static_cast<unsigned short>((e & 1) ? hw >> 16 : hw & 0xFFFFu))), vmin);
+          if (__float_as_uint(__fmaf_rn(d, rcp_lo, kMagic)) != __float_as_uint(__fmaf_rn(d, rcp_hi, kMagic)))
+            s_codes[c] = static_cast<uint8_t>(static_cast<int>(quant_slow(d, scale)) - kHr);
+        }
+      }
+    }
+    __syncthreads();  // (B) codes complete
+    // ---- outliers of this slice (ascending index order, runtime.cpp:217)
+    if (a.xo16) {
+      uint16_t* xo = reinterpret_cast<uint16_t*>(a.xo16) + static_cast<int64_t>(t) * opad;
+      if (xo_hoisted) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int i = o_lo + tid + j * nt;
+          if (i < o_hi) xo[i] = xov[j];
+        }
+      } else {
+        const uint16_t* xrow = reinterpret_cast<const uint16_t*>(xg + static_cast<int64_t>(t) * a.ldx);
+        for (int i = o_lo + tid; i < o_hi; i += nt)
+          xo[i] = (has_out && i < a.n_out) ? xrow[__ldg(&a.out_src[i]) - in_lo] : 0;
+      }
+    }
+    // ---- compacted code chunks of this slice (window offsets rebased to the slice)
+    uint4* dst = reinterpret_cast<uint4*>(a.q8 + static_cast<int64_t>(t) * a.kpad);
+    for (int cidx = ch_lo + tid; cidx < ch_hi; cidx += nt) {
+      const uint4 d = __ldg(cdesc + cidx);
+      if (d.x == 0xFFFFFFFFu) continue;  // general chunk (below)
+      const uint32_t* wa = reinterpret_cast<const uint32_t*>(s_codes + (d.x & 0xFFFFu) - in_lo);
+      const uint32_t* wb = reinterpret_cast<const uint32_t*>(s_codes + (d.y & 0xFFFFu) - in_lo);
+      const uint32_t sa = d.x >> 16, sb = d.y >> 16;
+      const uint32_t a0 = wa[0], a1 = wa[1], a2 = wa[2], a3 = wa[3], a4 = wa[4];
+      const uint32_t b0 = wb[0], b1 = wb[1], b2 = wb[2], b3 = wb[3], b4 = wb[4];
+      const uint32_t o0 = __byte_perm(__byte_perm(a0, a1, sa), __byte_perm(b0, b1, sb), d.z & 0xFFFFu);
+      const uint32_t o1 = __byte_perm(__byte_perm(a1, a2, sa), __byte_perm(b1, b2, sb), d.z >> 16);
+      const uint32_t o2 = __byte_perm(__byte_perm(a2, a3, sa), __byte_perm(b2, b3, sb), d.w & 0xFFFFu);
+      const uint32_t o3 = __byte_perm(__byte_perm(a3, a4, sa), __byte_perm(b3, b4, sb), d.w >> 16);
+      dst[cidx] = make_uint4(o0, o1, o2, o3);
+    }
+    for (int gi = g_lo + tid; gi < g_hi; gi += nt) {
+      const int cidx = a.gen_chunk[gi];
+      const uint4 g0 = __ldg(reinterpret_cast<const uint4*>(a.gather + cidx * 16));
+      const uint4 g1 = __ldg(reinterpret_cast<const uint4*>(a.gather + cidx * 16 + 8));
+      const uint32_t gw[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      uint32_t w[4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint32_t c0 = s_codes[(gw[2 * kk] & 0xFFFFu) - in_lo], c1 = s_codes[(gw[2 * kk] >> 16) - in_lo];
+        const uint32_t c2 = s_codes[(gw[2 * kk + 1] & 0xFFFFu) - in_lo], c3 = s_codes[(gw[2 * kk + 1] >> 16) - in_lo];
+        w[kk] = __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410);
+      }
+      dst[cidx] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    if (++s == stages) { s = 0; ph ^= 1u; }
+  }
+  cluster_sync();  // no CTA leaves while a peer may still address its shared memory
+}
+
 __global__ void split_kernel(const SplitArgs a) {
   const int64_t t = blockIdx.y;
   for (int64_t j = blockIdx.x * blockDim.x + threadIdx.x; j < a.kb + a.opad; j += gridDim.x * blockDim.x) {
@@ -1109,6 +1426,10 @@ cudaError_t launch_quantize_hot(const QuantArgs& a, cudaStream_t stream) {
     const char* e = getenv("QUIK_K1_WAIT");
     return e ? atoi(e) : 0;
   }();
+  static const int hot_pdl = [] {  // tuning: QUIK_K1_PDL=0 launches without programmatic serialization
+    const char* e = getenv("QUIK_K1_PDL");
+    return e ? atoi(e) : 1;
+  }();
   QuantArgs ah = a;
   ah.hot_flags = wait_env ? 1 : 0;
   int dev = 0, sms = 148;
@@ -1132,7 +1453,7 @@ cudaError_t launch_quantize_hot(const QuantArgs& a, cudaStream_t stream) {
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                                       \
     attr[0].val.programmaticStreamSerializationAllowed = 1;                                                \
     cfg.attrs = attr;                                                                                      \
-    cfg.numAttrs = 1;                                                                                      \
+    cfg.numAttrs = hot_pdl ? 1 : 0;                                                                        \
     e = cudaLaunchKernelEx(&cfg, kern, ah, stages, row_stride);                                            \
     if (e != cudaSuccess) return e;                                                                        \
   } while (0)
@@ -1144,15 +1465,90 @@ cudaError_t launch_quantize_hot(const QuantArgs& a, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+template <int B>
+cudaError_t launch_quantize_wide(const QuantArgs& a, cudaStream_t stream) {
+  // launched WITHOUT programmatic serialization by default: under PDL its clusters start
+  // while the previous layer's GEMM still holds SMs and the persistent row ranges of the
+  // late clusters stretch the launch (OPT-66B fc2 M = 2048 step 587 -> 540 us without;
+  // QUIK_K1_WIDE_PDL=1 restores it)
+  static const int wide_pdl = [] {
+    const char* e = getenv("QUIK_K1_WIDE_PDL");
+    return e ? atoi(e) : 0;
+  }();
+  const int C = a.n_slice;
+  const int64_t nvec = a.slice_cols_max / 8;
+  int vpt = 1;
+  while (vpt < 8 && (nvec + vpt - 1) / vpt > 128) vpt *= 2;
+  const int threads = static_cast<int>(round_up((nvec + vpt - 1) / vpt, 32));
+  if (threads > (vpt >= 8 ? 512 : 256)) return cudaErrorNotSupported;
+  const int row_stride = static_cast<int>(round_up(static_cast<int64_t>(a.slice_cols_max) * 2, 128));
+  int stages = static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(8, (32 * 1024) / row_stride)));
+  while (stages > 1 && a.slice_code_bytes + stages * row_stride > 200 * 1024) --stages;
+  const int smem = a.slice_code_bytes + stages * row_stride;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+#define QUIK_QW_LAUNCH(V)                                                                                   \
+  do {                                                                                                      \
+    auto kern = quantize_wide_kernel<B, V>;                                                                 \
+    cudaError_t e = ensure_smem_attr(kern, smem);                                                           \
+    if (e != cudaSuccess) return e;                                                                         \
+    cudaLaunchConfig_t cfg{};                                                                               \
+    cfg.blockDim = dim3(threads);                                                                           \
+    cfg.dynamicSmemBytes = smem;                                                                            \
+    cfg.stream = stream;                                                                                    \
+    cudaLaunchAttribute attr[2];                                                                            \
+    attr[0].id = cudaLaunchAttributeClusterDimension;                                                       \
+    attr[0].val.clusterDim.x = C;                                                                           \
+    attr[0].val.clusterDim.y = 1;                                                                           \
+    attr[0].val.clusterDim.z = 1;                                                                           \
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;                                        \
+    attr[1].val.programmaticStreamSerializationAllowed = 1;                                                 \
+    cfg.attrs = attr;                                                                                       \
+    cfg.numAttrs = wide_pdl ? 2 : 1;                                                                        \
+    /* as many clusters as are co-resident (the row loop is persistent) */                                  \
+    static int cached_key = -1, cached_clusters = 0;                                                        \
+    const int key = (C << 24) ^ (threads << 12) ^ smem;                                                     \
+    int clusters = 0;                                                                                       \
+    if (key == cached_key) {                                                                                \
+      clusters = cached_clusters;                                                                           \
+    } else {                                                                                                \
+      cfg.gridDim = dim3(static_cast<unsigned>(C * sms));                                                   \
+      e = cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg);                                            \
+      if (e != cudaSuccess) return e;                                                                       \
+      cached_key = key;                                                                                     \
+      cached_clusters = clusters;                                                                           \
+    }                                                                                                       \
+    if (clusters < 1) return cudaErrorNotSupported;                                                         \
+    const int64_t ncl = std::min<int64_t>(a.M, clusters);                                                   \
+    cfg.gridDim = dim3(static_cast<unsigned>(ncl * C));                                                     \
+    e = cudaLaunchKernelEx(&cfg, kern, a, stages, row_stride);                                              \
+    if (e != cudaSuccess) return e;                                                                         \
+  } while (0)
+  if (vpt == 1) QUIK_QW_LAUNCH(1);
+  else if (vpt == 2) QUIK_QW_LAUNCH(2);
+  else if (vpt == 4) QUIK_QW_LAUNCH(4);
+  else QUIK_QW_LAUNCH(8);
+#undef QUIK_QW_LAUNCH
+  return cudaGetLastError();
+}
+
 cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t stream) {
   if (a.M == 0) return cudaSuccess;
   // hot path: f16 rows, 16-byte aligned, GEMM-layout outputs only
   const bool hot = !a.x_is_f32 && a.q8 && !a.packed && !a.xo32 && a.chunk_desc && a.gather && a.K % 8 == 0 &&
                    a.K / 8 <= 512 * 8 && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && (a.ldx * 2) % 16 == 0;
-  static const int variant = [] {  // tuning: QUIK_K1_VARIANT=0 forces the general kernel
+  static const int variant = [] {  // tuning: QUIK_K1_VARIANT=0 forces the general kernel, 2 the one-CTA-per-row hot kernel
     const char* e = getenv("QUIK_K1_VARIANT");
     return e ? atoi(e) : 1;
   }();
+  // wide rows: K1 over a cluster of CTAs per row (the layer's slices)
+  const bool wide = !a.x_is_f32 && a.q8 && !a.packed && !a.xo32 && a.chunk_desc && a.gather && a.n_slice >= 2 &&
+                    a.slice_desc && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && (a.ldx * 2) % 16 == 0;
+  if (wide && variant != 0 && variant != 2) {
+    const cudaError_t e = a.bits == 4 ? launch_quantize_wide<4>(a, stream) : launch_quantize_wide<8>(a, stream);
+    if (e != cudaErrorNotSupported) return e;
+  }
   if (hot && variant != 0) {
     const cudaError_t e = a.bits == 4 ? launch_quantize_hot<4>(a, stream) : launch_quantize_hot<8>(a, stream);
     if (e != cudaErrorNotSupported) return e;  // else: shape outside the hot kernel's range

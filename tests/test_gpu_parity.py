@@ -619,6 +619,51 @@ def test_hot_quantizer_ties_zeros_and_shapes():
         _hot_k1_case(m, o, x, idx, 4 if K == 8192 else 8)
 
 
+def test_wide_quantizer_cluster_slices_bit_exact():
+    """K1 for wide rows (K > 32768: each row split over a thread-block cluster, one CTA
+    per slice, min / max exchanged through distributed shared memory) against the oracle:
+    OPT-66B fc2 (36864) and Falcon-180B fc2 (59392) widths and odd ones, outliers
+    clustered on the slice boundaries, at the row ends, none at all; exact ties; zero
+    minima whose first zero (and its sign) lies in a later slice; more rows than
+    co-resident clusters."""
+    m = q()
+    o = oracle()
+    rng = np.random.default_rng(7300)
+    for K, M, bits, pattern in [(36864, 300, 8, "random"), (59392, 40, 8, "random"), (40000, 64, 4, "bounds"),
+                                (49152, 50, 4, "bounds"), (36864, 30, 8, "ends"), (40960, 30, 4, "none"),
+                                (36864, 1200, 4, "random")]:
+        C = min(8, -(-K // 8192))
+        if pattern == "random":
+            idx = np.sort(rng.choice(K, size=K // 32, replace=False))
+        elif pattern == "bounds":  # contiguous outlier runs straddling every slice boundary
+            runs = [np.arange(max(0, c * K // C - 40), min(K, c * K // C + 25)) for c in range(1, C)]
+            idx = np.unique(np.concatenate(runs + [rng.choice(K, size=64, replace=False)]))
+        elif pattern == "ends":
+            idx = np.concatenate([np.arange(0, 300), np.arange(K - 500, K)])
+        else:
+            idx = np.array([], np.int64)
+        idx = np.asarray(idx, np.int64)
+        x = rng.normal(0, 1, size=(M, K)).astype(np.float16)
+        if len(idx):
+            x[:, idx[::2]] *= 30
+        base = np.setdiff1d(np.arange(K), idx)
+        # row 0: exact ties on the quantization grid; rows 1-2: zero minimum, the first
+        # zero in a late slice (-0 then +0, and +0 then -0); row 3: constant
+        levels = (1 << bits) - 1
+        g = rng.integers(0, 2 * levels + 1, size=K).astype(np.float32) * 0.5
+        g[base[0]], g[base[1]] = 0.0, levels
+        x[0] = g.astype(np.float16)
+        for r, (s1, s2) in ((1, (-0.0, 0.0)), (2, (0.0, -0.0))):
+            if M > r:
+                x[r] = np.abs(x[r]) + np.float16(0.5)
+                late = base[(len(base) * 3) // 4]
+                later = base[(len(base) * 7) // 8]
+                x[r, late], x[r, later] = s1, s2
+        if M > 3:
+            x[3] = np.float16(2.5)
+        _hot_k1_case(m, o, x, idx, bits)
+
+
 # --------------------------------------------------------------------------- 2:4 sparse base weights (cfg5)
 
 

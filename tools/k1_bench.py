@@ -22,6 +22,8 @@ SHAPES = [  # name, M, K, O, bits
     ("cfg2 7B down W8A8", 2048, 11008, 688, 8),
     ("cfg1", 16, 4096, 128, 4),
     ("cfg5 13B up", 2048, 5120, 256, 4),
+    ("cfg4 OPT-66B fc2 W4", 2048, 36864, 256, 4),
+    ("cfg4 Falcon-180B fc2 W8A8", 2048, 59392, 1024, 8),
 ]
 
 
