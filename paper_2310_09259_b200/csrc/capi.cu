@@ -1042,9 +1042,20 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
     return QUIK_OK;
   }
   if (variant == QUIK_V3_FUSED_EPILOGUE) {
+    // speed mode, mid token counts: the GEMM streams the weights more than it computes,
+    // so it reads the INT4 copy (half the bytes; the decode regime makes it anyway):
+    // OPT-66B fc1 M = 64 61.9 -> 46.2 us, M = 128 66.5 -> 54.8 us; from M = 256 the
+    // INT8 copy is faster again (84 vs 127 us). QUIK_W4_MID_M sets the bound (0: off).
+    static const int64_t w4_mid_m = [] {
+      const char* e = getenv("QUIK_W4_MID_M");
+      return e ? atoll(e) : 128LL;
+    }();
+    const bool mid_w4 = !L->int4_only && L->bits == 4 && !L->sparse && !g_probe_mode && M <= w4_mid_m &&
+                        ensure_w4(L, st);
     run_k1(ctx, L, x, xdt, M, st);
     mark(sm.after_quant, st);
     GemmArgs gm = gemm_args(ctx, L, M);
+    if (mid_w4) gm.w4 = L->w4;
     gm.out = y;
     gm.ldo = ldy;
     gm.mode = ydt == QUIK_F16 ? kModeF16 : kModeF32;
