@@ -993,10 +993,14 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
                          void* const* peers = nullptr, int n_peer = 0) {
   if (M == 0 || L->out_features == 0) return QUIK_OK;
   const int64_t N = L->out_features;
-  // Decode regime (M <= 32, dense layers): the split-K stream kernel (stream4.cu)
-  // spreads small layers over every SM (4-bit: INT4 weights widened into TMEM; 8-bit:
-  // INT8 tiles); default on (QUIK_STREAM4=0 disables).
-  bool decode = variant == QUIK_V3_FUSED_EPILOGUE && M <= 32 && L->kpad && !L->sparse && !g_probe_mode &&
+  // Decode regime (M <= 16, or M <= 32 for layers of >= 128 M weights, dense layers):
+  // the weight-streaming kernel (stream4.cu) spreads small layers over every SM (4-bit:
+  // INT4 weights widened into TMEM; 8-bit: INT8 tiles); default on (QUIK_STREAM4=0
+  // disables). At 17-32 tokens the fused kernel (on the INT4 copy, QUIK_W4_MID_M) is as
+  // fast or faster except for the largest layers (M = 32: cfg1 4096^2 12.7 us fused vs
+  // 13.1 decode, 7B up 13.5 vs 15.9, 70B up 38.6 vs 38.7, OPT-66B fc1 44.2 vs 37.2).
+  const bool decode_m = M <= 16 || (M <= 32 && N * L->kpad >= (int64_t{128} << 20));
+  bool decode = variant == QUIK_V3_FUSED_EPILOGUE && decode_m && L->kpad && !L->sparse && !g_probe_mode &&
                 quikb200::gemm_stream4_auto;
   if (decode && L->bits == 4) decode = ensure_w4(L, st);
   if (decode) {

@@ -39,6 +39,8 @@ SHAPES = [
     ("decode 70B up/gate M=32", 32, 8192, 28672, 256, 4),
     ("decode OPT-66B fc1 M=32", 32, 9216, 36864, 256, 4),
     ("decode 7B up/gate M=16", 16, 4096, 11008, 256, 4),
+    ("decode 7B up/gate M=32", 32, 4096, 11008, 256, 4),
+    ("decode 7B qkvo M=32", 32, 4096, 4096, 256, 4),
     ("decode 70B down W8A8 M=16", 16, 28672, 8192, 896, 8),
 ]
 OPT_FC1 = [(m, 9216, 36864, 256, 4) for m in (1, 16, 64, 128, 256, 512, 1024, 2048, 4096, 8192)]
