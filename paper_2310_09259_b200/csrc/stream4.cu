@@ -31,6 +31,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 
@@ -57,10 +58,13 @@ struct S4Cfg {
   static constexpr int kOffT = kStagesW * kS4WBytes;
   static constexpr int kOffF = kOffT + kStagesT * kSlotT;
   static constexpr int kRingBytes = kOffF + 2 * kFinBlk;
-  static constexpr int kBarBytes = (2 * (kStagesW + kStagesT) + 2 * G + 6) * 8 + 32;
+  // TMEM A buffers per widening group: two at BN = 16 (the group widens its next stage
+  // while its MMAs still read the previous one), one where TMEM is short
+  static constexpr int NB = BN == 16 ? 2 : 1;
+  static constexpr int kBarBytes = (2 * (kStagesW + kStagesT) + 2 * G * NB + 6) * 8 + 32;
   static constexpr int kSmemBytes = 1024 + kRingBytes + kBarBytes;
   static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
-  static constexpr int kAccCol = G * kS4TmemA;
+  static constexpr int kAccCol = NB * G * kS4TmemA;
   static constexpr int kAccBuf = G * BN;             // G int32 accumulators, double-buffered
   static constexpr int kFinCol = kAccCol + 2 * kAccBuf;  // f32 finalisation accumulator (BN)
   static_assert(kFinCol + BN <= 512, "TMEM budget");
@@ -110,9 +114,10 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
   uint64_t* empty_t = full_t + C::kStagesT;
   uint64_t* fin_full = empty_t + C::kStagesT;  // finalisation: outlier tiles landed
   uint64_t* fin_mma = fin_full + 1;            // finalisation: outlier MMAs done
-  uint64_t* a_full = fin_mma + 1;              // [G] widening group g -> issuer g
-  uint64_t* a_empty = a_full + G;            // [G] issuer g -> widening group g
-  uint64_t* acc_full = a_empty + G;          // [2] the G issuers -> epilogue
+  constexpr int NB = C::NB;
+  uint64_t* a_full = fin_mma + 1;              // [G][NB] widening group g, A buffer b -> issuer g
+  uint64_t* a_empty = a_full + G * NB;       // [G][NB] issuer g -> widening group g
+  uint64_t* acc_full = a_empty + G * NB;     // [2] the G issuers -> epilogue
   uint64_t* acc_empty = acc_full + 2;        // [2] epilogue -> issuers
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
@@ -134,7 +139,7 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
       for (int i = 0; i < C::kStagesT; ++i) { mbar_init(&full_t[i], 1); mbar_init(&empty_t[i], 1); }
       mbar_init(fin_full, 1);
       mbar_init(fin_mma, 1);
-      for (int i = 0; i < G; ++i) { mbar_init(&a_full[i], 4); mbar_init(&a_empty[i], 1); }
+      for (int i = 0; i < G * NB; ++i) { mbar_init(&a_full[i], 4); mbar_init(&a_empty[i], 1); }
       for (int i = 0; i < 2; ++i) { mbar_init(&acc_full[i], G); mbar_init(&acc_empty[i], 4); }
       fence_mbar_init();
     }
@@ -259,16 +264,18 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
           commit_e(&empty_t[st]);
           continue;
         }
-        mbar_wait_spin(&a_full[g], (bc / G) & 1);          // A widened into TMEM
+        // the group's n-th stage uses A buffer n % NB
+        const int n = bc / G, ab = n % NB;
+        mbar_wait_spin(&a_full[g * NB + ab], (n / NB) & 1);  // A widened into TMEM
         mbar_wait(&full_t[st], (bc / C::kStagesT) & 1);    // code tile landed
         tc_fence_after();
-        const uint32_t a_tm = tmem_base + g * kS4TmemA;
+        const uint32_t a_tm = tmem_base + (ab * G + g) * kS4TmemA;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           mma_i8_ts_e(d, a_tm + 8 * j, bd0 + (j >> 2) * (C::kTAtom >> 4) + 2 * (j & 3), idesc_i8,
                       (first && j == 0) ? 0u : 1u);
         first = false;
-        commit_e(&a_empty[g]);
+        commit_e(&a_empty[g * NB + ab]);
         commit_e(&empty_t[st]);
       }
       commit_e(&acc_full[b]);
@@ -279,14 +286,16 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
     // (low nibbles of word q) and 8c + 4 + q (high nibbles)
     const int quad = warp & 3, g = (warp - 2) >> 2;
     const int r = quad * 32 + lane;
-    const uint32_t a_tm = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + g * kS4TmemA;
+    const uint32_t a_lane = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
     int bc = 0, nb, k0, k1;
     for (Segs sg = segs(); !p.w8 && next(sg, nb, k0, k1);) {  // (INT8: nothing to widen)
       for (int i = k0; i < k1; ++i, ++bc) {
         if (bc % G != g) continue;
         const int st = bc % C::kStagesW;
+        const int n = bc / G, ab = n % NB;
+        const uint32_t a_tm = a_lane + (ab * G + g) * kS4TmemA;
         mbar_wait_sleep(&full_w[st], (bc / C::kStagesW) & 1);
-        mbar_wait_spin(&a_empty[g], ((bc / G) & 1) ^ 1);
+        mbar_wait_spin(&a_empty[g * NB + ab], ((n / NB) & 1) ^ 1);
         tc_fence_after();
         const uint8_t* wrow = ring_w + st * kS4WBytes + r * kKBlockBytes;
 #pragma unroll 1
@@ -312,7 +321,7 @@ __global__ void __launch_bounds__(S4Cfg<BN>::kThreads, 1) stream4_gemm_kernel(co
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&empty_w[st]);  // weight tile consumed (the MMAs read TMEM)
-          mbar_arrive(&a_full[g]);
+          mbar_arrive(&a_full[g * NB + ab]);
         }
       }
     }
@@ -591,28 +600,27 @@ cudaError_t launch_stream4(const Stream4Args& a, int num_sms, cudaStream_t strea
   sp.w8 = a.w4 ? 0 : 1;
   sp.nstage = static_cast<int>(sp.w8 ? a.kpad / 128 : (a.kpad + 255) / 256);
   sp.nout = static_cast<int>(a.opad / 64);
-  // Round robin with K splits minimising the busiest CTA's stage count (see wo.cu), or
-  // stream-K when that is clearly cheaper. Costs in weight stages per CTA: round robin
-  // waves x (stages per unit + 1, + 2 per reduced unit: a split block's workspace
-  // reduction, 7B up / gate M = 16 13.8 us in one split vs 18.7 us in three); stream-K the CTA's range + 8
-  // (its cut blocks finalise through the workspace at the end of the ranges), and only
-  // for ranges of >= 24 stages (shorter ranges are dominated by the per-segment
-  // epilogues). Measured: 70B up / gate (28672 x 8192) M = 1 39.6 -> 33 us and
-  // Falcon-180B fc1 M = 1 94 -> 82 us with stream-K; 7B up / gate M = 16 19.3 us round
-  // robin vs 22.8 stream-K.
+  // Schedule from a cost model in weight stages per CTA. Round robin with s K splits:
+  // (full waves + the last wave's fill, counted as at least 0.75 of a wave: a partly
+  // filled wave streams faster per CTA, the kernel being HBM-bound) x (stages per unit
+  // + 1, + 4 per split unit for its workspace reduction). Stream-K: the CTA's range + 8
+  // (its cut blocks finalise through the workspace at the end of the ranges), only for
+  // ranges of >= 24 stages and when 15 % cheaper. Measured, M = 1: 70B up / gate
+  // (224 blocks) whole blocks 27.1 us vs stream-K 30.1; Falcon-180B fc1 (464 blocks,
+  // a 20-CTA last wave) stream-K 76.8 vs whole blocks 82.8 vs 3 splits 90; 7B up / gate
+  // M = 16 13.8 us whole blocks vs 18.7 in 3 splits.
   const long long tiles = (a.N + kBlockM - 1) / kBlockM;
   int splits = 1;
-  long long best = -1;
+  double best = -1.0;
   for (int s = 1; s <= 16 && s <= sp.nstage; ++s) {
-    const long long waves = (tiles * s + num_sms - 1) / num_sms;
-    const long long cost = waves * ((sp.nstage + s - 1) / s + 1 + (s > 1 ? 2 : 0));
+    const long long units = tiles * s, full = units / num_sms, rest = units - full * num_sms;
+    const double waves = static_cast<double>(full) + (rest ? std::max(0.75, static_cast<double>(rest) / num_sms) : 0.0);
+    const double cost = waves * ((sp.nstage + s - 1) / s + 1 + (s > 1 ? 4 : 0));
     if (best < 0 || cost < best) { best = cost; splits = s; }
   }
   {
-    const long long units = tiles * splits, waves = (units + num_sms - 1) / num_sms;
-    const long long rr = waves * ((sp.nstage + splits - 1) / splits + 1 + (splits > 1 ? 2 : 0));
-    const long long range = (tiles * sp.nstage + num_sms - 1) / num_sms;
-    if (range >= 24 && rr * 100 > 115 * (range + 8)) splits = 0;
+    const double range = std::ceil(static_cast<double>(tiles * sp.nstage) / num_sms);
+    if (range >= 24 && best > 1.15 * (range + 8)) splits = 0;
   }
   static const int sched_env = [] {  // tuning: QUIK_S4_SPLITS=n forces n round-robin K splits, -1 stream-K
     const char* e = getenv("QUIK_S4_SPLITS");
