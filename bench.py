@@ -629,7 +629,10 @@ def run_ours(args, w):
         fp16 = dict(ms_median=t16, tflops=2.0 * M * ns * K / (t16 * 1e-3) / 1e12, speedup_step=t16 / step_med,
                     speedup_gemm=t16 / gemm_med,
                     note="torch.matmul f16 (cuBLAS) of the per-rank shape, same x; medians of per-step events")
+        decode = decode_regime(torch, layer, xs_dev[0], Wf, ns, K, kb, O, bits, pk) if world == 1 else None
         del Wf, out16
+    else:
+        decode = None
 
     # ---- e2e: host (pinned) buffers through the public API, copies inside the timed region
     e2e = None
@@ -723,13 +726,52 @@ def run_ours(args, w):
                                    f"MB), int8 weights {ns * ((kb + 127) // 128 * 128) / 1e6:.0f} MB, y "
                                    f"{M * ns * 2 / 1e6:.0f} MB; no flush")),
                    parity=parity, exchange=exchange, roofline=roofline, cpu_baseline=cpu, e2e=e2e, fp16_cublas=fp16, quantizer=quant,
-                   sustained=sustained,
+                   sustained=sustained, decode=decode,
                    clocks=clocks, gpu_launches=steps * q.QuikLinear.launches(),
                    precision="W%dA%d integer codes on tcgen05 kind::i8 (s32 accumulate) + f16 outliers (f32 accumulate), f16 out"
                              % (bits, bits))
         emit(out)
     if world > 1:
         dist.destroy_process_group()
+
+
+def decode_regime(torch, layer, x, Wf, ns, K, kb, O, bits, pk):
+    """The same layer in the decode regime (1 and 16 tokens: K1 + the weight-streaming
+    decode kernel, stream4.cu) against cuBLAS f16 of the same shape: 10 forwards per
+    CUDA graph, median of 5 replays. HBM fraction over the bytes a forward must stream:
+    the INT4 weights and the f16 outlier weights (x and y are < 1 MB)."""
+    out = {}
+    wbytes = ns * ((kb + 127) // 128 * 128) // (2 if bits == 4 else 1) + ns * ((O + 63) // 64 * 64) * 2
+
+    def graph_us(fn):
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(10):
+                fn()
+        ts = []
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            g.replay()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) * 1e3 / 10)
+        return statistics.median(ts)
+
+    for t in (1, 16):
+        xt = x[:t].contiguous()
+        yt = torch.empty((t, ns), device=x.device, dtype=torch.float16)
+        o16 = torch.empty((t, ns), device=x.device, dtype=torch.float16)
+        us = graph_us(lambda: layer.forward(xt, out=yt))
+        us16 = graph_us(lambda: torch.matmul(xt, Wf.t(), out=o16))
+        out[f"tokens_{t}"] = dict(us=us, hbm_gbs=wbytes / (us * 1e-6) / 1e9, hbm_frac=wbytes / (us * 1e-6) / 1e9 / pk["hbm_gbs"],
+                                  cublas_f16_us=us16, speedup=us16 / us)
+    out["weight_bytes"] = wbytes
+    out["note"] = ("same layer, first 1 / 16 tokens of x: K1 + the INT4 decode kernel; 10 forwards per CUDA graph, "
+                   "median of 5 replays; HBM fraction of the INT4 + f16 outlier weight bytes")
+    return out
 
 
 def spawn_ranks(args) -> int:
