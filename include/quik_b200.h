@@ -140,6 +140,20 @@ quik_status quik_layer_destroy(quik_layer_t layer);
  * plain layer applied to h. quik_layer_info reports out_features = F. */
 quik_status quik_layer_create_gated(quik_ctx_t ctx, const quik_weights_desc* up, const quik_weights_desc* gate,
                                    quik_layer_t* out);
+/* Gated MLP block (reference forward_model with gated_mlp_ops,
+ * runtime.cpp:373-388): y = down(silu(gate(x)) * up(x)). gated: a
+ * quik_layer_create_gated layer, down: a plain layer with in_features = F.
+ * h: device f16 [M][ldh] hidden state (written; ldh >= F); y: [M][ldy] of ydt.
+ * Above the decode regime the gated GEMM's epilogue also reduces the down projection's
+ * per-token min / max over the base (non-outlier) columns of the f16 h it stores, and
+ * the down projection's quantizer consumes them instead of its own reduction pass
+ * (runtime.cpp:36-50 split across the two kernels). h, the down codes / scales and y
+ * are bit-identical to quik_linear_forward(gated) followed by quik_linear_forward(down)
+ * on h. Non-finite base values of h raise the context's numerical flag
+ * (quik_ctx_sync -> QUIK_ERR_NUMERICAL), as the down quantizer would. Asynchronous. */
+quik_status quik_gated_mlp_forward(quik_ctx_t ctx, quik_layer_t gated, quik_layer_t down, const void* x,
+                                   quik_dtype xdt, int64_t M, void* h, int64_t ldh, void* y, quik_dtype ydt,
+                                   int64_t ldy, void* stream);
 quik_status quik_layer_info(quik_layer_t layer, int64_t* in_features, int64_t* out_features,
                             int64_t* n_outlier, int* bits);
 /* 1 if the layer runs the 2:4 sparse GEMM (sparsity requested and compressible). */

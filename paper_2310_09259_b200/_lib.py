@@ -40,7 +40,7 @@ EXPORTED_SYMBOLS = (
     "quik_gptq_quantize", "quik_hessian_accumulate", "quik_ctx_clear_error", "quik_ctx_reserve", "quik_layer_layout",
     "quik_linear_forward_timed", "quik_split_activations", "quik_unpack_values", "quik_compute_wreduced",
     "quik_dequantize_weights", "quik_elementwise", "quik_ipc_handle_get", "quik_ipc_handle_open",
-    "quik_ipc_handle_close", "quik_layer_device_bytes",
+    "quik_ipc_handle_close", "quik_layer_device_bytes", "quik_gated_mlp_forward",
 )
 
 
@@ -114,6 +114,7 @@ def load() -> C.CDLL:
             "quik_linear_forward_strided": (i32, [vp, vp, vp, i32, i64, vp, i32, i64, i32, vp]),
             "quik_linear_forward_launches": (i32, [i32]),
             "quik_linear_forward_ex": (i32, [vp, vp, vp, i32, i64, vp, i32, i64, i32, vp, vp]),
+            "quik_gated_mlp_forward": (i32, [vp, vp, vp, vp, i32, i64, vp, i64, vp, i32, i64, vp]),
             "quik_rtn_quantize_weights": (i32, [vp, vp, i64, i64, vp, i64, i32, i32, vp, vp, vp, vp, vp]),
             "quik_ctx_clear_error": (i32, [vp, vp]),
             "quik_ctx_reserve": (i32, [vp, vp, i64]),

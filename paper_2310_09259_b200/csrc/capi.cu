@@ -131,6 +131,18 @@ struct quik_ctx_s {
   int num_sms = 148;
   int* d_err = nullptr;
   DevBuf q8, scale, zero, xo16, acc, fp, xbase, xo32, wtmp, wo_ws, s4_out, s4_cnt, aux;
+  // gated MLP block: the down projection's per-token min / max keys (kernels.h), kept at
+  // their initial values between calls (the down K1 restores what it reads)
+  DevBuf hstat;
+  uint4* ensure_hstat(int64_t M, cudaStream_t st) {
+    const size_t before = hstat.cap;
+    void* p = hstat.ensure(static_cast<size_t>(M) * 16);
+    if (hstat.cap != before) check_hstat(launch_hstat_init(static_cast<uint4*>(p), hstat.cap / 16, st));
+    return static_cast<uint4*>(p);
+  }
+  static void check_hstat(cudaError_t e) {
+    if (e != cudaSuccess) throw CudaFail{e, "hstat init"};
+  }
   // per-weight-block arrival counters of the INT4 decode kernel (zero between calls)
   int* ensure_s4_counters(size_t n, cudaStream_t st) {
     const size_t before = s4_cnt.cap;
@@ -217,6 +229,10 @@ struct quik_layer_s {
   // wide-row K1 slices (kernels.h QuantArgs::slice_desc), n_slice == 0: one CTA per row
   int32_t* slice_desc = nullptr;
   int n_slice = 0, slice_cols_max = 0, slice_chunks_max = 0, slice_code_bytes = 0;
+  // [ceil(in / 32) + 1] words, bit f = input feature f is an outlier column (bits past
+  // in_features set): the base-column mask a gated projection's epilogue reduces this
+  // layer's K1 min / max over (quik_gated_mlp_forward)
+  uint32_t* fmask = nullptr;
 };
 
 namespace {
@@ -346,7 +362,8 @@ void set_slices(QuantArgs& q, const quik_layer_s* L) {
 }
 
 // Runs K1 into the context scratch (GEMM layout) for the hot path.
-void run_k1(quik_ctx_t ctx, const quik_layer_s* L, const void* x, quik_dtype xdt, int64_t M, cudaStream_t st) {
+void run_k1(quik_ctx_t ctx, const quik_layer_s* L, const void* x, quik_dtype xdt, int64_t M, cudaStream_t st,
+            uint4* pre_stat = nullptr) {
   QuantArgs q{};
   q.x = x;
   q.x_is_f32 = xdt == QUIK_F32;
@@ -370,6 +387,7 @@ void run_k1(quik_ctx_t ctx, const quik_layer_s* L, const void* x, quik_dtype xdt
   q.xo16 = L->opad ? static_cast<__half*>(ctx->xo16.ensure(static_cast<size_t>(M * L->opad * 2))) : nullptr;
   q.opad = L->opad;
   q.err = ctx->d_err;
+  q.pre_stat = pre_stat;
   check_launch(launch_quantize(q, st), "quantize kernel");
 }
 
@@ -488,7 +506,8 @@ quik_status quik_ctx_destroy(quik_ctx_t ctx) {
   DeviceGuard g(ctx->device);
   cudaDeviceSynchronize();
   for (DevBuf* b : {&ctx->q8, &ctx->scale, &ctx->zero, &ctx->xo16, &ctx->acc, &ctx->fp, &ctx->xbase, &ctx->xo32,
-                    &ctx->wtmp, &ctx->xdev, &ctx->ydev, &ctx->ws, &ctx->wo_ws, &ctx->s4_out, &ctx->s4_cnt, &ctx->aux})
+                    &ctx->wtmp, &ctx->xdev, &ctx->ydev, &ctx->ws, &ctx->wo_ws, &ctx->s4_out, &ctx->s4_cnt, &ctx->aux,
+                    &ctx->hstat})
     b->release();
   if (ctx->s_in) {
     cudaStreamDestroy(ctx->s_in);
@@ -576,6 +595,14 @@ quik_status quik_layer_create(quik_ctx_t ctx, const quik_weights_desc* d, quik_l
     for (int64_t i = 0; i < d->n_outlier; ++i) lane_mask[d->outlier_indices[i]] = 0xFF;
     std::vector<uint16_t> gather(static_cast<size_t>(L->kpad), static_cast<uint16_t>(kr16));
     for (int64_t j = 0; j < kb; ++j) gather[j] = static_cast<uint16_t>(base_src[j]);
+    {
+      const int64_t nw = d->in_features / 32 + 1;
+      std::vector<uint32_t> fm(static_cast<size_t>(nw), 0u);
+      for (int64_t f = 0; f < nw * 32; ++f)
+        if (f >= d->in_features || is_out[f]) fm[f >> 5] |= 1u << (f & 31);
+      QK_CUDA(cudaMalloc(&L->fmask, nw * 4));
+      QK_CUDA(cudaMemcpy(L->fmask, fm.data(), nw * 4, cudaMemcpyHostToDevice));
+    }
 
     cudaStream_t st = nullptr;
     if (kb) {
@@ -790,6 +817,7 @@ quik_status quik_layer_destroy(quik_layer_t L) {
   cudaFree(L->chunk_desc);
   cudaFree(L->gen_chunk);
   cudaFree(L->slice_desc);
+  cudaFree(L->fmask);
   delete L;
   return QUIK_OK;
 }
@@ -988,9 +1016,21 @@ void mark(cudaEvent_t e, cudaStream_t st) {
   if (e) QK_CUDA(cudaEventRecord(e, st));
 }
 
+// Gated MLP block link (quik_gated_mlp_forward): the gated projection's GEMM epilogue
+// emits the down projection's per-token min / max keys (emit: hmask = the down layer's
+// outlier mask; *emitted = whether the fused GEMM ran, i.e. the keys are complete), the
+// down projection's K1 consumes them (consume).
+struct MlpLink {
+  uint4* hstat = nullptr;
+  const uint32_t* hmask = nullptr;
+  bool* emitted = nullptr;
+  bool consume = false;
+};
+
 quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M, void* y,
                          quik_dtype ydt, int64_t ldy, quik_variant variant, cudaStream_t st, const StageMarks& sm,
-                         void* const* peers = nullptr, int n_peer = 0) {
+                         void* const* peers = nullptr, int n_peer = 0, const MlpLink& link = MlpLink{}) {
+  uint4* const pre = link.consume ? link.hstat : nullptr;
   if (M == 0 || L->out_features == 0) return QUIK_OK;
   const int64_t N = L->out_features;
   // Decode regime (M <= 16, or M <= 32 for layers of >= 128 M weights, dense layers):
@@ -1015,7 +1055,7 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
   if (decode) {
     // decode regime: K1 -> one kernel for the INT4 split-K GEMM and the fused epilogue
     // (dequant + outlier MMAs, stream4.cu); workspace / counters stay zeroed between calls
-    run_k1(ctx, L, x, xdt, M, st);
+    run_k1(ctx, L, x, xdt, M, st, pre);
     mark(sm.after_quant, st);
     Stream4Args a{};
     a.w4 = L->bits == 4 ? L->w4 : nullptr;
@@ -1056,10 +1096,17 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
     }();
     const bool mid_w4 = !L->int4_only && L->bits == 4 && !L->sparse && !g_probe_mode && M <= w4_mid_m &&
                         ensure_w4(L, st);
-    run_k1(ctx, L, x, xdt, M, st);
+    run_k1(ctx, L, x, xdt, M, st, pre);
     mark(sm.after_quant, st);
     GemmArgs gm = gemm_args(ctx, L, M);
     if (mid_w4) gm.w4 = L->w4;
+    if (link.hmask && L->gated && !L->sparse && ydt == QUIK_F16 && !g_probe_mode &&
+        (reinterpret_cast<uintptr_t>(y) & 15) == 0 && (ldy * 2) % 16 == 0) {  // TMA-store tiles
+      gm.hstat = link.hstat;
+      gm.hmask = link.hmask;
+      gm.herr = ctx->d_err;
+      if (link.emitted) *link.emitted = true;
+    }
     gm.out = y;
     gm.ldo = ldy;
     gm.mode = ydt == QUIK_F16 ? kModeF16 : kModeF32;
@@ -1106,7 +1153,7 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
     q.err = ctx->d_err;
     check_launch(launch_quantize(q, st), "quantize kernel");
   } else {
-    run_k1(ctx, L, x, xdt, M, st);
+    run_k1(ctx, L, x, xdt, M, st, pre);
   }
   mark(sm.after_quant, st);
   // V1/V2 tail: the int32 accumulator through global memory, then the same
@@ -1150,6 +1197,54 @@ quik_status quik_linear_forward_ex(quik_ctx_t ctx, quik_layer_t L, const void* x
     sm.after_quant = reinterpret_cast<cudaEvent_t>(mid_event);
     return on_stream(ctx, as_stream(stream),
                      [&] { return forward_impl(ctx, L, x, xdt, M, y, ydt, ldy, variant, as_stream(stream), sm); });
+  });
+}
+
+quik_status quik_gated_mlp_forward(quik_ctx_t ctx, quik_layer_t gated, quik_layer_t down, const void* x,
+                                   quik_dtype xdt, int64_t M, void* h, int64_t ldh, void* y, quik_dtype ydt,
+                                   int64_t ldy, void* stream) {
+  if (!ctx || !gated || !down) return fail(QUIK_ERR_INVALID_ARGUMENT, "null context or layer");
+  if (!gated->gated) return fail(QUIK_ERR_INVALID_ARGUMENT, "gated MLP: first layer is not a gated projection");
+  const int64_t F = gated->out_features / 2;
+  if (down->in_features != F)
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "gated MLP: down projection input != up/gate output features");
+  if (down->gated) return fail(QUIK_ERR_INVALID_ARGUMENT, "gated MLP: down projection is gated");
+  if (M < 0) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_matmul: negative token count");
+  if (M > 0 && (!x || !h || !y)) return fail(QUIK_ERR_INVALID_ARGUMENT, "gated MLP: null input, hidden or output");
+  if (M > 0x7fffffffLL) return fail(QUIK_ERR_UNSUPPORTED, "quik_matmul: token count exceeds 2^31");
+  if (ldh < F) return fail(QUIK_ERR_INVALID_ARGUMENT, "gated MLP: hidden pitch < hidden features");
+  if (ldy < down->out_features) return fail(QUIK_ERR_INVALID_ARGUMENT, "quik_matmul: output pitch < out_features");
+  if (gated->in_features * (xdt == QUIK_F32 ? 4 : 2) > 128 * 1024 || F * 2 > 128 * 1024)
+    return fail(QUIK_ERR_UNSUPPORTED, "quik_matmul: row wider than 128 KiB (register-resident quantizer limit)");
+  if (ctx->device != gated->device || ctx->device != down->device)
+    return fail(QUIK_ERR_INVALID_ARGUMENT, "context and layers live on different devices");
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = as_stream(stream);
+    return on_stream(ctx, st, [&] {
+      if (M == 0) return QUIK_OK;
+      static const int fuse_env = [] {  // QUIK_MLP_FUSE=0: no statistics link (two plain forwards)
+        const char* e = getenv("QUIK_MLP_FUSE");
+        return e ? atoi(e) : 1;
+      }();
+      MlpLink up_link, down_link;
+      bool emitted = false;
+      if (fuse_env && down->kpad) {
+        up_link.hstat = ctx->ensure_hstat(M, st);
+        up_link.hmask = down->fmask;
+        up_link.emitted = &emitted;
+      }
+      StageMarks none;
+      quik_status s1 = forward_impl(ctx, gated, x, xdt, M, h, QUIK_F16, ldh, QUIK_V3_FUSED_EPILOGUE, st, none, nullptr,
+                                    0, up_link);
+      if (s1 != QUIK_OK) return s1;
+      if (emitted) {
+        down_link.hstat = up_link.hstat;
+        down_link.consume = true;
+      }
+      return forward_impl(ctx, down, h, QUIK_F16, M, y, ydt, ldy, QUIK_V3_FUSED_EPILOGUE, st, none, nullptr, 0,
+                          down_link);
+    });
   });
 }
 

@@ -155,7 +155,16 @@ struct KParams {
   // fused all-gather: each output tile is also stored through these maps (peer outputs)
   int n_peer;
   CUtensorMap tm_peer[kMaxPeerOut];
+  // gated MLP block: the down projection's per-token base min / max keys (GemmArgs::hstat)
+  uint4* hstat;
+  const uint32_t* hmask;
+  int* herr;
 };
+__device__ __forceinline__ __half2 u2h2(uint32_t u) {
+  __half2 h;
+  memcpy(&h, &u, 4);
+  return h;
+}
 constexpr int kTraceTiles = 64;
 __device__ long long g_wstamps[2 * 128 * 8];  // W4 MMA / widening clock64 stamps (QUIK_GEMM_TRACE)
 constexpr int kTraceSlots = 16;
@@ -190,7 +199,8 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
   static_assert(!(W4 && (SP || MC)), "W4 is a dense-weight variant");
   constexpr int CL = MC ? 4 : CG;  // CTAs per cluster
   constexpr bool kAccGlobal = MODE == kModeAccInitF32 || MODE == kModeAccInitF16;
-  constexpr bool kF16Out = MODE == kModeF16 || MODE == kModeAccInitF16;
+  constexpr bool kF16Out = MODE == kModeF16 || MODE == kModeAccInitF16 || MODE == kModeF16Stats;
+  constexpr bool kStats = MODE == kModeF16Stats;  // gated MLP block: down K1 statistics
   constexpr bool kInt32Out = MODE == kModeInt32;
   constexpr bool kProbe = MODE == kModeProbe;
 
@@ -883,6 +893,61 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
             for (int i = 0; i < p.n_peer; ++i) tma_store_2d(&p.tm_peer[i], buf, n0_out, mb * BN + c, pol_y);
             bulk_commit();
           }
+          if constexpr (kStats) {
+            // gated MLP block: the down projection's K1 reduction (runtime.cpp:36-50 over
+            // the base columns of h) on the staged f16 tile, transposed: lane j reads token
+            // j's 32 features (16-byte pieces rotated by lane pair: conflict-free), outlier
+            // features of the down layer (fm) replaced by a base value of the same token,
+            // packed f16 min / max (K1's pass 1), one atomic pair per token and chunk on
+            // order-preserving keys (kernels.h). Signed zeros: a chunk whose minimum is a
+            // zero reports its first base zero's column and sign (the row minimum is zero
+            // only if every zero-holding chunk's minimum is). Non-finite: error flag.
+            const uint32_t fm = __ldg(&p.hmask[n0_out >> 5]);
+            const int t = mb * BN + c + lane;
+            if (fm != 0xFFFFFFFFu && t < p.M) {
+              const uint16_t* rowh = reinterpret_cast<const uint16_t*>(buf) + lane * 32;
+              const uint4* row4 = reinterpret_cast<const uint4*>(rowh);
+              const uint32_t f0 = rowh[__ffs(~fm) - 1];
+              const uint32_t fill = f0 | (f0 << 16);
+              __half2 mn = u2h2(0x7C007C00u), mx = u2h2(0xFC00FC00u);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const int kk = (k + (lane >> 1)) & 3;
+                const uint4 q4 = row4[kk];
+                const uint32_t byte = (fm >> (8 * kk)) & 0xFFu;
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                  const uint32_t i2 = (byte >> (2 * w)) & 3u;
+                  const uint32_t mk = (i2 & 1u ? 0x0000FFFFu : 0u) | (i2 & 2u ? 0xFFFF0000u : 0u);
+                  const __half2 x2 = u2h2(((&q4.x)[w] & ~mk) | (fill & mk));
+                  mn = __hmin2_nan(mn, x2);
+                  mx = __hmax2_nan(mx, x2);
+                }
+              }
+              const float2 fmn = __half22float2(mn), fmx = __half22float2(mx);
+              const bool bad = isnan(fmn.x) || isnan(fmn.y) || isnan(fmx.x) || isnan(fmx.y) || fmx.x == INFINITY ||
+                               fmx.y == INFINITY || fmn.x == -INFINITY || fmn.y == -INFINITY;
+              if (bad) atomicExch(p.herr, 1);
+              const float vmn = fminf(fmn.x, fmn.y), vmx = fmaxf(fmx.x, fmx.y);
+              auto key = [](float v) {  // f16-exact value -> order-preserving key (+-0 -> +0)
+                const uint32_t u = __half_as_ushort(__float2half_rn(v));
+                const uint32_t mag = u & 0x7FFFu;
+                return ((u & 0x8000u) && mag) ? 0x7FFFu - mag : (mag | 0x8000u);
+              };
+              atomicMin(&p.hstat[t].x, key(vmn));
+              atomicMax(&p.hstat[t].y, key(vmx));
+              if (vmn == 0.0f) {  // rare: this chunk's first base zero (column, sign)
+#pragma unroll 1
+                for (int f = 0; f < 32; ++f) {
+                  const uint32_t u = rowh[f];
+                  if (!((fm >> f) & 1u) && (u & 0x7FFFu) == 0u) {
+                    atomicMin(&p.hstat[t].z, (static_cast<uint32_t>(n0_out + f) << 1) | (u >> 15));
+                    break;
+                  }
+                }
+              }
+            }
+          }
           sbuf ^= 1;
           return;
         }
@@ -1054,6 +1119,7 @@ cudaError_t launch_mode(const KParams& kp, int mode, int num_sms, cudaStream_t s
     case kModeAccInitF16: return launch_cfg<CG, BN, kModeAccInitF16, false, MC>(kp, num_sms, stream);
     case kModeF32: return launch_cfg<CG, BN, kModeF32, false, MC>(kp, num_sms, stream);
     case kModeProbe: return launch_cfg<CG, BN, kModeProbe, false, MC>(kp, num_sms, stream);
+    case kModeF16Stats: return launch_cfg<CG, BN, kModeF16Stats, false, MC>(kp, num_sms, stream);
     default: return launch_cfg<CG, BN, kModeF16, false, MC>(kp, num_sms, stream);
   }
 }
@@ -1066,6 +1132,7 @@ cudaError_t launch_mode_w4(const KParams& kp, int mode, int num_sms, cudaStream_
     case kModeF32: return launch_cfg<CG, BN, kModeF32, false, false, true>(kp, num_sms, stream);
     case kModeProbe: return launch_cfg<CG, BN, kModeProbe, false, false, true>(kp, num_sms, stream);
     case kModeF16: return launch_cfg<CG, BN, kModeF16, false, false, true>(kp, num_sms, stream);
+    case kModeF16Stats: return launch_cfg<CG, BN, kModeF16Stats, false, false, true>(kp, num_sms, stream);
     default: return cudaErrorInvalidValue;  // AccInit tails read int32 accumulators, no weights
   }
 }
@@ -1237,6 +1304,9 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
   }();
   kp.split_num = (split_env >= 1 && split_env <= 7) ? split_env : (sp ? 6 : 4);
   kp.gated = a.gated && a.mode != kModeInt32 && a.mode != kModeProbe;  // raw accumulators stay per row
+  kp.hstat = (kp.gated && a.mode == kModeF16 && !sp) ? a.hstat : nullptr;  // 2:4 tiles: no statistics
+  kp.hmask = a.hmask;
+  kp.herr = a.herr;
   static const char* trace_path = getenv("QUIK_GEMM_TRACE");  // diagnostics: timeline dump
   static long long* trace_buf = nullptr;
   // per-cluster tile stamps, then (W4) per-iteration widening stamps of cluster 0
@@ -1280,9 +1350,14 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
   kp.out = a.out;
   kp.ldo = a.ldo;
   const int key = ((cg << 16) | bn) | (mc ? kKeyMC : 0) | (w4 ? kKeyW4 : 0);
+  const int mode = kp.hstat ? kModeF16Stats : a.mode;
+  if (kp.hstat && !kp.tma_store) {  // the statistics read the staged TMA-store tile
+    *err_msg = "gated MLP statistics need a 16-byte aligned f16 hidden state";
+    return cudaErrorInvalidValue;
+  }
   if (kp.trace) {
     // launch, then dump the timeline of this call (overwrites the file each call)
-    cudaError_t e = sp ? launch_sp_key(key, kp, a.mode, num_sms, stream) : launch_dense_key(key, kp, a.mode, num_sms, stream);
+    cudaError_t e = sp ? launch_sp_key(key, kp, mode, num_sms, stream) : launch_dense_key(key, kp, mode, num_sms, stream);
     if (e != cudaSuccess) return e;
     std::vector<long long> h(trace_bytes / 8);
     cudaStreamSynchronize(stream);
@@ -1301,11 +1376,11 @@ cudaError_t launch_quik_gemm(const GemmArgs& a, int num_sms, cudaStream_t stream
     return cudaSuccess;
   }
   if (sp) {
-    const cudaError_t e = launch_sp_key(key, kp, a.mode, num_sms, stream);
+    const cudaError_t e = launch_sp_key(key, kp, mode, num_sms, stream);
     if (e == cudaErrorInvalidConfiguration) *err_msg = "unsupported sparse tile configuration";
     return e;
   }
-  const cudaError_t e = launch_dense_key(key, kp, a.mode, num_sms, stream);
+  const cudaError_t e = launch_dense_key(key, kp, mode, num_sms, stream);
   if (e == cudaErrorInvalidConfiguration) *err_msg = "unsupported tile configuration";
   return e;
 }

@@ -42,6 +42,8 @@ enum GemmMode : int {
   kModeF16 = 3,         // same, out f16 (hot path)
   kModeProbe = 4,       // diagnostics: mainloop + TMEM traffic, no global stores
   kModeAccInitF16 = 5,  // acc read from global int32 (V1/V2 tail), out f16
+  kModeF16Stats = 6,    // kModeF16 + the gated epilogue's down-projection statistics
+                        // (GemmArgs::hstat; set by the launcher, dense / W4 tiles)
 };
 
 struct GemmArgs {
@@ -85,6 +87,16 @@ struct GemmArgs {
   // process), f16 TMA-store outputs only
   void* const* peer_out;
   int n_peer;
+  // gated MLP block (second half): the epilogue also reduces the next
+  // (down) projection's per-token base min / max over the f16 h it stores, so the down
+  // layer's K1 skips its reduction pass (QuantArgs::pre_stat). hstat [M] x uint4 =
+  // {min key, max key, first-zero key, 0} (order-preserving u32 keys of the f16 values,
+  // atomics; quik_gated_mlp_forward); hmask [ceil(N / 2 / 32)] words, bit f set =
+  // feature f is a down-projection outlier column (or past the row); herr: non-finite
+  // base h flag. hstat == nullptr: no statistics.
+  uint4* hstat;
+  const uint32_t* hmask;
+  int* herr;
 };
 constexpr int kMaxPeerOut = 7;
 
@@ -235,7 +247,14 @@ struct QuantArgs {
   int slice_cols_max;       // columns of the widest slice
   int slice_chunks_max;     // output chunks of the busiest slice
   int slice_code_bytes;     // shared code-row bytes (window reads and the zero tail included)
+  // Prescaled rows (hot kernel only): the per-token base min / max were reduced by the
+  // producing GEMM's epilogue (GemmArgs::hstat); the kernel reads them instead of its own
+  // reduction pass and restores the keys to their initial values for the next forward.
+  uint4* pre_stat;
 };
+// hstat / pre_stat keys: f16 bits u (signed zeros canonicalised to +0) ->
+// u >= 0 ? u | 0x8000 : 0x7FFF - (u & 0x7FFF); initial {0xFFFFFFFF, 0, 0xFFFFFFFF, 0}
+cudaError_t launch_hstat_init(uint4* stat, int64_t M, cudaStream_t stream);
 cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t stream);
 
 // V1 split (runtime.cpp:169-186): base columns in permutation order as f32

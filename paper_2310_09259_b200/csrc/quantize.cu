@@ -470,6 +470,12 @@ __device__ __forceinline__ float sub_f16_f32(uint32_t h, float c) {
   return d;
 }
 
+// hstat / pre_stat key (kernels.h) -> the f16 value it encodes
+__device__ __forceinline__ float hkey_to_float(uint32_t k) {
+  const uint32_t u = k >= 0x8000u ? k - 0x8000u : (0x8000u | (0x7FFFu - k));
+  return __half2float(__ushort_as_half(static_cast<unsigned short>(u)));
+}
+
 template <int BITS, int VPT, bool FULL>
 __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(const QuantArgs a, int stages, int row_stride) {
   extern __shared__ __align__(128) uint8_t s_dyn[];
@@ -494,8 +500,12 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(cons
   // one code row (written after barrier A of row t+1, read before it for row t), then
   // the ring
   const int code_stride = (kr16 + 32 + 127) & ~127;
+  // prescaled rows (a.pre_stat: min / max from the producing GEMM's epilogue): no
+  // reduction barrier, so the code row is double-buffered (row t+1's codes may be
+  // written while row t's are still being compacted) and the ring slot is refilled at (B)
+  uint4* const pre = a.pre_stat;
   uint8_t* s_codes = s_dyn;                          // [code_stride]: codes by column, zero tail
-  uint8_t* s_ring = s_dyn + code_stride;             // [stages][row_stride]
+  uint8_t* s_ring = s_dyn + code_stride * (pre ? 2 : 1);  // [stages][row_stride]
   const bool has_out = a.lane_mask != nullptr;
   const int nchunk = static_cast<int>(a.kpad >> 4);
   const __half* xg = reinterpret_cast<const __half*>(a.x);
@@ -530,6 +540,7 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(cons
     fence_mbar_init();
   }
   if (tid < 8) reinterpret_cast<uint32_t*>(s_codes + kr16)[tid] = 0u;  // zero tail
+  if (pre && tid >= 8 && tid < 16) reinterpret_cast<uint32_t*>(s_codes + code_stride + kr16)[tid - 8] = 0u;
   __syncthreads();
   if (tid == 0) {
     // PDL: everything above (tables, barriers) overlapped the previous kernel; its
@@ -551,6 +562,8 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(cons
     const uint4* srow = reinterpret_cast<const uint4*>(s_ring + s * row_stride);
     if (a.hot_flags & 1) mbar_wait_sleep(&s_full[s], ph);  // waiting threads give up their issue slots
     else mbar_wait(&s_full[s], ph);
+    uint4 pst = make_uint4(0u, 0u, 0u, 0u);
+    if (pre) pst = __ldcg(pre + t);  // issued early: its latency overlaps the row loads
 
     uint4 raw[VPT];
 #pragma unroll
@@ -565,6 +578,17 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(cons
       for (int j = 0; j < 2; ++j)
         if (osrc[j] >= 0) xov[j] = reinterpret_cast<const uint16_t*>(srow)[osrc[j]];
     }
+    float vmin, vmax;
+    int nonfinite = 0;
+    if (pre) {
+      // the epilogue's keys (kernels.h): exact f16 values; a zero minimum takes the sign
+      // of the first zero (its column in the key's upper bits); non-finite values were
+      // flagged by the epilogue
+      vmin = hkey_to_float(pst.x);
+      vmax = hkey_to_float(pst.y);
+      if (kb == 0) { vmin = 0.f; vmax = 0.f; }
+      if (vmin == 0.0f && kb > 0 && pst.z != 0xFFFFFFFFu) vmin = (pst.z & 1u) ? -0.0f : 0.0f;
+    } else {
     // ---- pass 1: packed min / max over the base columns
     __half2 hmin = u2h2(0x7C007C00u), hmax = u2h2(0xFC00FC00u);
     if (has_out) {
@@ -593,8 +617,6 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(cons
         }
       }
     }
-    float vmin, vmax;
-    int nonfinite;
     {
       const float2 fmn = __half22float2(hmin);
       const float2 fmx = __half22float2(hmax);
@@ -653,6 +675,7 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(cons
       for (int w = 1; w < nwarps; ++w) key = s_key[w] < key ? s_key[w] : key;
       vmin = (key & 1u) ? -0.0f : 0.0f;
     }
+    }  // !pre
     const float range = __fsub_rn(vmax, vmin);
     const float scale = range == 0.0f ? 1.0f : __fdiv_rn(range, kLevels);
     const float rcp = __frcp_rn(scale);
@@ -721,6 +744,16 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(cons
       }
     }
     __syncthreads();  // (B) codes complete
+    if (pre && tid == 0) {
+      // prescaled: every thread holds the row (and its outlier values) since before (B)
+      const int rn = t + stages * gridDim.x;
+      if (rn < M) {
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&s_full[s], row_bytes);
+        bulk_load_1d(s_ring + s * row_stride, xg + static_cast<int64_t>(rn) * a.ldx, row_bytes, &s_full[s]);
+      }
+      pre[t] = make_uint4(0xFFFFFFFFu, 0u, 0xFFFFFFFFu, 0u);  // initial keys for the next forward
+    }
     // this row's compaction descriptors (row-independent, L1-resident): all loads in
     // flight before the outlier gather instead of one at a time in the copy-out loop
     constexpr int kCk = VPT > 1 ? VPT / 2 : 1;
@@ -778,6 +811,7 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_hot_kernel(cons
       dst[cidx] = make_uint4(w[0], w[1], w[2], w[3]);
     }
     if (++s == stages) { s = 0; ph ^= 1u; }
+    if (pre) s_codes = s_dyn + (s_codes == s_dyn ? code_stride : 0);
   }
 }
 
@@ -1419,8 +1453,9 @@ cudaError_t launch_quantize_hot(const QuantArgs& a, cudaStream_t stream) {
     return e ? atoi(e) : 32;
   }();
   int stages = static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(8, (ring_kb * 1024) / row_stride)));
-  while (stages > 1 && codes + stages * row_stride > 200 * 1024) --stages;
-  const int smem = codes + stages * row_stride;
+  const int code_bufs = a.pre_stat ? 2 : 1;  // prescaled rows: double-buffered code row
+  while (stages > 1 && code_bufs * codes + stages * row_stride > 200 * 1024) --stages;
+  const int smem = code_bufs * codes + stages * row_stride;
   const bool full = static_cast<int64_t>(threads) * vpt == nvec;
   static const int wait_env = [] {  // tuning knob: QUIK_K1_WAIT=1 sleep-waits on the row ring
     const char* e = getenv("QUIK_K1_WAIT");
@@ -1545,6 +1580,19 @@ cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t stream) {
   // wide rows: K1 over a cluster of CTAs per row (the layer's slices)
   const bool wide = !a.x_is_f32 && a.q8 && !a.packed && !a.xo32 && a.chunk_desc && a.gather && a.n_slice >= 2 &&
                     a.slice_desc && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && (a.ldx * 2) % 16 == 0;
+  if (a.pre_stat) {
+    // prescaled rows: the hot kernel consumes and resets the keys; any other kernel
+    // reduces the rows itself, then the keys are reset for the next forward
+    if (hot && variant != 0) {
+      const cudaError_t e = a.bits == 4 ? launch_quantize_hot<4>(a, stream) : launch_quantize_hot<8>(a, stream);
+      if (e != cudaErrorNotSupported) return e;
+    }
+    QuantArgs b = a;
+    b.pre_stat = nullptr;
+    const cudaError_t e = launch_quantize(b, stream);
+    if (e != cudaSuccess) return e;
+    return launch_hstat_init(a.pre_stat, a.M, stream);
+  }
   if (wide && variant != 0 && variant != 2) {
     const cudaError_t e = a.bits == 4 ? launch_quantize_wide<4>(a, stream) : launch_quantize_wide<8>(a, stream);
     if (e != cudaErrorNotSupported) return e;
@@ -1555,6 +1603,17 @@ cudaError_t launch_quantize(const QuantArgs& a, cudaStream_t stream) {
   }
   if (a.x_is_f32) return a.bits == 4 ? launch_quantize_t<float, 4>(a, stream) : launch_quantize_t<float, 8>(a, stream);
   return a.bits == 4 ? launch_quantize_t<__half, 4>(a, stream) : launch_quantize_t<__half, 8>(a, stream);
+}
+
+__global__ void hstat_init_kernel(uint4* stat, int64_t M) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < M) stat[i] = make_uint4(0xFFFFFFFFu, 0u, 0xFFFFFFFFu, 0u);
+}
+
+cudaError_t launch_hstat_init(uint4* stat, int64_t M, cudaStream_t stream) {
+  if (M == 0) return cudaSuccess;
+  hstat_init_kernel<<<static_cast<unsigned>((M + 255) / 256), 256, 0, stream>>>(stat, M);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_split(const SplitArgs& a, cudaStream_t stream) {

@@ -710,10 +710,35 @@ class QuikGatedMLP:
         if self.down.in_features != self.proj.out_features:
             raise ValueError("gated MLP: down projection input != up/gate output features")
 
-    def forward(self, x, out=None, out_dtype=None, hidden_dtype=None):
-        """hidden_dtype: dtype of h between the projections (default: x's dtype)."""
-        h = self.proj(x, out_dtype=hidden_dtype or x.dtype)
-        return self.down(h, out=out, out_dtype=out_dtype)
+    def forward(self, x, out=None, out_dtype=None, hidden_dtype=None, fused: bool = True):
+        """hidden_dtype: dtype of h between the projections (default: x's dtype).
+        With an f16 hidden state the block runs through quik_gated_mlp_forward: the
+        gated GEMM's epilogue also reduces the down projection's per-token min / max, so
+        the down quantizer skips its reduction pass (bit-identical to the two forwards;
+        fused=False runs them separately)."""
+        return self.forward_with_hidden(x, out, out_dtype, hidden_dtype, fused)[0]
+
+    def forward_with_hidden(self, x, out=None, out_dtype=None, hidden_dtype=None, fused: bool = True):
+        """forward() that also returns the hidden state h: (y, h)."""
+        torch = _torch()
+        hd = hidden_dtype or x.dtype
+        if hd != torch.float16 or not fused:
+            h = self.proj(x, out_dtype=hd)
+            return self.down(h, out=out, out_dtype=out_dtype), h
+        if x.dim() != 2 or x.shape[1] != self.proj.in_features:
+            raise ValueError(f"quik_matmul: input has {x.shape[-1]} features, layer expects {self.proj.in_features}")
+        if x.dtype not in (torch.float16, torch.float32):
+            raise ValueError("quik_matmul: input must be float16 or float32")
+        x = x.contiguous()
+        M = x.shape[0]
+        h = self.proj._check_out(torch, x, None, torch.float16, "gated MLP")
+        out = self.down._check_out(torch, x, out, out_dtype, "gated MLP")
+        ydt = _lib.QUIK_F16 if out.dtype == torch.float16 else _lib.QUIK_F32
+        xdt = _lib.QUIK_F16 if x.dtype == torch.float16 else _lib.QUIK_F32
+        _lib.check(self.proj._lib.quik_gated_mlp_forward(
+            self.proj._ctx_handle(), self.proj.handle, self.down.handle, _ptr(x), xdt, M, _ptr(h), h.stride(0),
+            _ptr(out), ydt, out.stride(0), C.c_void_p(_stream_ptr(torch, x.device))))
+        return out, h
 
     __call__ = forward
 
