@@ -1131,7 +1131,7 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_wide_kernel(con
 }
 
 __global__ void split_kernel(const SplitArgs a) {
-  const int64_t t = blockIdx.y;
+  for (int64_t t = blockIdx.y; t < a.M; t += gridDim.y)  // rows beyond grid.y's 65535 limit
   for (int64_t j = blockIdx.x * blockDim.x + threadIdx.x; j < a.kb + a.opad; j += gridDim.x * blockDim.x) {
     if (j < a.kb) {
       const int64_t c = a.base_src[j];
@@ -1159,15 +1159,14 @@ __global__ void split_kernel(const SplitArgs a) {
 
 __global__ void unpack_kernel(const uint8_t* __restrict__ packed, int64_t rows, int64_t cols, int bits,
                               int8_t* __restrict__ dst, int64_t kpad) {
-  const int64_t r = blockIdx.y;
   const int64_t rb = bits == 4 ? (cols + 1) / 2 : cols;
-  const uint8_t* src = packed + r * rb;
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
   for (int64_t c = blockIdx.x * blockDim.x + threadIdx.x; c < kpad; c += gridDim.x * blockDim.x) {
     int8_t v = 0;
     if (c < cols) {
-      if (bits == 8) v = static_cast<int8_t>(src[c]);
+      if (bits == 8) v = static_cast<int8_t>(packed[r * rb + c]);
       else {
-        const uint8_t b = src[c / 2];
+        const uint8_t b = packed[r * rb + c / 2];
         v = static_cast<int8_t>(static_cast<int>((c & 1) ? (b >> 4) : (b & 0xF)) - 8);
       }
     }
@@ -1177,7 +1176,7 @@ __global__ void unpack_kernel(const uint8_t* __restrict__ packed, int64_t rows, 
 
 __global__ void f32_to_f16_kernel(const float* __restrict__ src, int64_t rows, int64_t cols,
                                   __half* __restrict__ dst, int64_t pitch) {
-  const int64_t r = blockIdx.y;
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
   for (int64_t c = blockIdx.x * blockDim.x + threadIdx.x; c < pitch; c += gridDim.x * blockDim.x)
     dst[r * pitch + c] = __float2half_rn(c < cols ? src[r * cols + c] : 0.0f);
 }
@@ -1194,7 +1193,7 @@ __global__ void dequant_kernel(const int32_t* __restrict__ acc, int64_t M, int64
                                const float* __restrict__ za, float hr, const float* __restrict__ sw,
                                const float* __restrict__ wr, const float* __restrict__ fp_part, void* out,
                                int out_kind /*0 f32 deq only, 1 f32 add, 2 f16 add*/) {
-  const int64_t t = blockIdx.y;
+  for (int64_t t = blockIdx.y; t < M; t += gridDim.y)
   for (int64_t r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
     const int64_t i = t * N + r;
     const float d = dequant_element(acc[i], sa[t], sw[r], za[t], hr, wr[r]);
@@ -1365,7 +1364,8 @@ dim3 grid2(int64_t cols, int64_t rows) {
   int64_t gx = (cols + 255) / 256;
   if (gx > 64) gx = 64;
   if (gx < 1) gx = 1;
-  return dim3(static_cast<unsigned>(gx), static_cast<unsigned>(rows));
+  // rows past grid.y's limit are walked by the kernels' row loops
+  return dim3(static_cast<unsigned>(gx), static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(rows, 65535))));
 }
 
 }  // namespace

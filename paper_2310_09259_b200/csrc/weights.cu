@@ -8,6 +8,8 @@
 // Every floating-point operation is the reference's, as an explicit _rn intrinsic.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace quikb200 {
@@ -112,9 +114,9 @@ __global__ void wreduced_kernel(const uint8_t* __restrict__ base, int64_t N, int
 __global__ void dequant_weights_kernel(const uint8_t* __restrict__ base, int64_t N, int64_t K, int64_t kb, int bits,
                                        const float* __restrict__ scales, const int32_t* __restrict__ perm,
                                        const float* __restrict__ ow, float* __restrict__ out) {
-  const int64_t r = blockIdx.y;
   const int64_t rb = bits == 4 ? (kb + 1) / 2 : kb;
   const int64_t no = K - kb;
+  for (int64_t r = blockIdx.y; r < N; r += gridDim.y)
   for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < K;
        j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     float v;
@@ -171,7 +173,7 @@ cudaError_t launch_dequantize_weights(const uint8_t* base, int64_t N, int64_t K,
                                       cudaStream_t stream) {
   if (N == 0 || K == 0) return cudaSuccess;
   const unsigned gx = blocks_for(K, 256) > 64 ? 64 : blocks_for(K, 256);
-  dequant_weights_kernel<<<dim3(gx, static_cast<unsigned>(N)), 256, 0, stream>>>(base, N, K, kb, bits, scales, perm,
+  dequant_weights_kernel<<<dim3(gx, static_cast<unsigned>(std::min<int64_t>(N, 65535))), 256, 0, stream>>>(base, N, K, kb, bits, scales, perm,
                                                                                  ow, out);
   return cudaGetLastError();
 }

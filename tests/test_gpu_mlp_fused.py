@@ -43,7 +43,8 @@ def test_fused_mlp_bit_identical_to_unfused(bits_ud, bits_down):
 
     rng = np.random.default_rng(1100 + 10 * bits_ud + bits_down)
     for (M, K, F, O, Od) in [(40, 256, 160, 32, 16), (300, 512, 384, 64, 32), (130, 384, 96, 0, 0),
-                             (517, 640, 1024, 64, 0), (64, 256, 2048, 32, 96)]:
+                             (517, 640, 1024, 64, 0), (64, 256, 2048, 32, 96), (200, 256, 9216, 32, 300),
+                             (48, 128, 36864, 0, 512)]:  # > 65535 gated rows; wide down rows: plain K1
         up, gate, down, x = _mlp_layers(rng, M, K, F, bits_ud, bits_down, O, Od)
         mlp = _blocks(up, gate, down)
         xt = torch.from_numpy(x).cuda()
@@ -129,7 +130,7 @@ def test_fused_mlp_nonfinite_hidden_raises():
 
 def test_fused_mlp_llama7b_shape():
     """LLaMA-2-7B MLP (4096 -> 11008 -> 4096, W4A4 up / gate, W8A8 down with 688 outliers)
-    at 512 tokens: the hot down K1 at its 11008-wide rows."""
+    at 512 tokens: the prescaled hot down K1 at its 11008-wide rows."""
     import torch
 
     rng = np.random.default_rng(1500)
