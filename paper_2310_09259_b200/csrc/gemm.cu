@@ -758,6 +758,70 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
     const int c_end = (c_begin + kHalf) < BN ? (c_begin + kHalf) : BN;
     uint8_t* my_stage = staging + e * 2 * kStoreBufBytes;
     int sbuf = 0;
+    // kStats gate warps: the previous chunk's staged h tile, reduced while the up warp
+    // works on the current one (pend_t0 < 0: none)
+    const __half* pend_hb = nullptr;
+    int pend_n0s = 0, pend_t0 = -1;
+    // gated MLP block (kStats): the down projection's K1 reduction (runtime.cpp:36-50
+    // over the base columns of h), run by the gate warp on the up warp's staged f16 tile
+    // hb (features n0s .. n0s + 31, tokens t0 ..) while the up warp goes on with its
+    // next chunk
+    auto down_stats = [&](const __half* hb, int n0s, int t0) {
+      // Transposed: lane j reads token j's 32 features (16-byte pieces rotated by lane
+      // pair: conflict-free), outlier features of the down layer (fm) replaced by a
+      // base value of the same token,
+      // packed f16 min / max (K1's pass 1), one atomic pair per token and chunk on
+      // order-preserving keys (kernels.h). Signed zeros: a chunk whose minimum is a
+      // zero reports its first base zero's column and sign (the row minimum is zero
+      // only if every zero-holding chunk's minimum is). Non-finite: error flag.
+      const uint32_t fm = __ldg(&p.hmask[n0s >> 5]);
+      const int t = t0 + lane;
+      if (fm != 0xFFFFFFFFu && t < p.M && !(p.dbg & 512)) {
+        const uint16_t* rowh = reinterpret_cast<const uint16_t*>(hb) + lane * 32;
+        const uint4* row4 = reinterpret_cast<const uint4*>(rowh);
+        const uint32_t f0 = rowh[__ffs(~fm) - 1];
+        const uint32_t fill = f0 | (f0 << 16);
+        __half2 mn = u2h2(0x7C007C00u), mx = u2h2(0xFC00FC00u);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int kk = (k + (lane >> 1)) & 3;
+          const uint4 q4 = row4[kk];
+          const uint32_t byte = (fm >> (8 * kk)) & 0xFFu;
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const uint32_t i2 = (byte >> (2 * w)) & 3u;
+            const uint32_t mk = (i2 & 1u ? 0x0000FFFFu : 0u) | (i2 & 2u ? 0xFFFF0000u : 0u);
+            const __half2 x2 = u2h2(((&q4.x)[w] & ~mk) | (fill & mk));
+            mn = __hmin2_nan(mn, x2);
+            mx = __hmax2_nan(mx, x2);
+          }
+        }
+        const float2 fmn = __half22float2(mn), fmx = __half22float2(mx);
+        const bool bad = isnan(fmn.x) || isnan(fmn.y) || isnan(fmx.x) || isnan(fmx.y) || fmx.x == INFINITY ||
+                         fmx.y == INFINITY || fmn.x == -INFINITY || fmn.y == -INFINITY;
+        if (bad) atomicExch(p.herr, 1);
+        const float vmn = fminf(fmn.x, fmn.y), vmx = fmaxf(fmx.x, fmx.y);
+        auto key = [](float v) {  // f16-exact value -> order-preserving key (+-0 -> +0)
+          const uint32_t u = __half_as_ushort(__float2half_rn(v));
+          const uint32_t mag = u & 0x7FFFu;
+          return ((u & 0x8000u) && mag) ? 0x7FFFu - mag : (mag | 0x8000u);
+        };
+        if (!(p.dbg & 256)) {
+          atomicMin(&p.hstat[t].x, key(vmn));
+          atomicMax(&p.hstat[t].y, key(vmx));
+        }
+        if (vmn == 0.0f) {  // rare: this chunk's first base zero (column, sign)
+#pragma unroll 1
+          for (int f = 0; f < 32; ++f) {
+            const uint32_t u = rowh[f];
+            if (!((fm >> f) & 1u) && (u & 0x7FFFu) == 0u) {
+              atomicMin(&p.hstat[t].z, (static_cast<uint32_t>(n0s + f) << 1) | (u >> 15));
+              break;
+            }
+          }
+        }
+      }
+    };
     const bool tma_out = kF16Out && p.tma_store;
     const uint64_t pol_y = policy_evict_first();  // the output is not re-read by this kernel
     int it = 0;
@@ -861,6 +925,22 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
         if constexpr (kProbe) return;
         if (p.gated) {
           if (gate_warp) {
+            if constexpr (kStats) {
+              // barrier pair_bar + 4 (up -> gate): the up warp has read the exchange
+              // buffer and staged its h tile; pair_bar (gate -> up): exchange buffer full.
+              // The gate warp reduces the previous chunk's h tile while the up warp forms
+              // and stores the current one.
+              if (pend_t0 >= 0) named_barrier_sync(pair_bar + 4, 64);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) xch[j * 32 + lane] = __uint_as_float(v[j]);
+              named_barrier_arrive(pair_bar, 64);
+              if (pend_t0 >= 0 && tma_out) down_stats(pend_hb, pend_n0s, pend_t0);
+              pend_hb = reinterpret_cast<const __half*>(staging + (e - 1) * 2 * kStoreBufBytes + sbuf * kStoreBufBytes);
+              pend_n0s = (n0 - 32) / 2;
+              pend_t0 = mb * BN + c;
+              sbuf ^= 1;  // mirrors the up warp's staging buffer
+              return;
+            }
 #pragma unroll
             for (int j = 0; j < 32; ++j) xch[j * 32 + lane] = __uint_as_float(v[j]);
             named_barrier_sync(pair_bar, 64);
@@ -876,7 +956,7 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
             const float silu = __fdividef(g, 1.0f + __expf(-g));
             v[j] = __float_as_uint(__fmul_rn(silu, __uint_as_float(v[j])));
           }
-          named_barrier_sync(pair_bar, 64);
+          if constexpr (!kStats) named_barrier_sync(pair_bar, 64);
         }
         if (tma_out) {
           __half* buf = reinterpret_cast<__half*>(my_stage + sbuf * kStoreBufBytes);
@@ -894,62 +974,13 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
             bulk_commit();
           }
           if constexpr (kStats) {
-            // gated MLP block: the down projection's K1 reduction (runtime.cpp:36-50 over
-            // the base columns of h) on the staged f16 tile, transposed: lane j reads token
-            // j's 32 features (16-byte pieces rotated by lane pair: conflict-free), outlier
-            // features of the down layer (fm) replaced by a base value of the same token,
-            // packed f16 min / max (K1's pass 1), one atomic pair per token and chunk on
-            // order-preserving keys (kernels.h). Signed zeros: a chunk whose minimum is a
-            // zero reports its first base zero's column and sign (the row minimum is zero
-            // only if every zero-holding chunk's minimum is). Non-finite: error flag.
-            const uint32_t fm = __ldg(&p.hmask[n0_out >> 5]);
-            const int t = mb * BN + c + lane;
-            if (fm != 0xFFFFFFFFu && t < p.M) {
-              const uint16_t* rowh = reinterpret_cast<const uint16_t*>(buf) + lane * 32;
-              const uint4* row4 = reinterpret_cast<const uint4*>(rowh);
-              const uint32_t f0 = rowh[__ffs(~fm) - 1];
-              const uint32_t fill = f0 | (f0 << 16);
-              __half2 mn = u2h2(0x7C007C00u), mx = u2h2(0xFC00FC00u);
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int kk = (k + (lane >> 1)) & 3;
-                const uint4 q4 = row4[kk];
-                const uint32_t byte = (fm >> (8 * kk)) & 0xFFu;
-#pragma unroll
-                for (int w = 0; w < 4; ++w) {
-                  const uint32_t i2 = (byte >> (2 * w)) & 3u;
-                  const uint32_t mk = (i2 & 1u ? 0x0000FFFFu : 0u) | (i2 & 2u ? 0xFFFF0000u : 0u);
-                  const __half2 x2 = u2h2(((&q4.x)[w] & ~mk) | (fill & mk));
-                  mn = __hmin2_nan(mn, x2);
-                  mx = __hmax2_nan(mx, x2);
-                }
-              }
-              const float2 fmn = __half22float2(mn), fmx = __half22float2(mx);
-              const bool bad = isnan(fmn.x) || isnan(fmn.y) || isnan(fmx.x) || isnan(fmx.y) || fmx.x == INFINITY ||
-                               fmx.y == INFINITY || fmn.x == -INFINITY || fmn.y == -INFINITY;
-              if (bad) atomicExch(p.herr, 1);
-              const float vmn = fminf(fmn.x, fmn.y), vmx = fmaxf(fmx.x, fmx.y);
-              auto key = [](float v) {  // f16-exact value -> order-preserving key (+-0 -> +0)
-                const uint32_t u = __half_as_ushort(__float2half_rn(v));
-                const uint32_t mag = u & 0x7FFFu;
-                return ((u & 0x8000u) && mag) ? 0x7FFFu - mag : (mag | 0x8000u);
-              };
-              atomicMin(&p.hstat[t].x, key(vmn));
-              atomicMax(&p.hstat[t].y, key(vmx));
-              if (vmn == 0.0f) {  // rare: this chunk's first base zero (column, sign)
-#pragma unroll 1
-                for (int f = 0; f < 32; ++f) {
-                  const uint32_t u = rowh[f];
-                  if (!((fm >> f) & 1u) && (u & 0x7FFFu) == 0u) {
-                    atomicMin(&p.hstat[t].z, (static_cast<uint32_t>(n0_out + f) << 1) | (u >> 15));
-                    break;
-                  }
-                }
-              }
-            }
+            if (p.gated) named_barrier_arrive(pair_bar + 4, 64);  // the gate warp reduces the staged tile
           }
           sbuf ^= 1;
           return;
+        }
+        if constexpr (kStats) {
+          if (p.gated) named_barrier_arrive(pair_bar + 4, 64);  // (no statistics without TMA tiles: host-checked)
         }
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -1011,6 +1042,12 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
       __syncwarp();
       if (lane == 0) arrive_leader<CG>(&tempty[b], leader_rank);
       if (tr) tr[10] = gtime();
+    }
+    if constexpr (kStats) {
+      if (p.gated && (q & 1) && pend_t0 >= 0) {  // the last chunk's statistics
+        named_barrier_sync(1 + (e >> 1) + 4, 64);
+        if (tma_out) down_stats(pend_hb, pend_n0s, pend_t0);
+      }
     }
     if (lane == 0) bulk_wait_all();
   }

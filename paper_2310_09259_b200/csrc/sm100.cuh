@@ -193,6 +193,10 @@ __device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const CUtensorMap
 __device__ __forceinline__ void named_barrier_sync(int id, int count) {
   asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
+// Producer side of a named barrier: arrives without waiting (the consumers bar.sync).
+__device__ __forceinline__ void named_barrier_arrive(int id, int count) {
+  asm volatile("barrier.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 
 // ------------------------------------------------------------------ clusters
 __device__ __forceinline__ uint32_t cluster_ctarank() {

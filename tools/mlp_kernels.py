@@ -1,5 +1,5 @@
 """Per-kernel launch list of the gated MLP block (for ncu --metrics gpu__time_duration.sum):
-LLaMA-2-70B (4096 tokens) through quik_gated_mlp_forward (statistics fused) and through
+LLaMA-2-70B (4096 tokens; argv[1] picks another SHAPES entry, e.g. 7B) through quik_gated_mlp_forward (statistics fused) and through
 two plain forwards, 3 calls each after a warm-up."""
 import sys
 
@@ -9,7 +9,8 @@ import torch  # noqa: E402
 import paper_2310_09259_b200 as q  # noqa: E402
 from mlp_bench import SHAPES, device_layer, host_layer  # noqa: E402
 
-name, M, H, F, O, Od, b_ud, b_d = [s for s in SHAPES if "70B" in s[0]][0]
+which = sys.argv[1] if len(sys.argv) > 1 else "70B"
+name, M, H, F, O, Od, b_ud, b_d = [s for s in SHAPES if which in s[0]][0]
 dev = torch.device("cuda", 0)
 g = torch.Generator(device=dev).manual_seed(5)
 outl, tu = device_layer(dev, H, F, O, b_ud, g)
