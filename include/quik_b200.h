@@ -70,7 +70,9 @@ quik_status quik_ctx_sync(quik_ctx_t ctx, void* stream);
 /* Clears the non-finite-input flag (asynchronously, on `stream`). */
 quik_status quik_ctx_clear_error(quik_ctx_t ctx, void* stream);
 /* Sizes the context's scratch for forwards of `layer` with up to M tokens (codes,
- * scales, outlier operands, the decode workspace and the INT4 weight copy at M <= 32),
+ * scales, outlier operands, the decode workspace and the INT4 weight copy at M <= 32;
+ * for a gated layer also the quik_gated_mlp_forward statistics — reserve the block's
+ * gated layer and its down projection),
  * so that later forwards can be captured into a CUDA graph: scratch cannot grow during
  * capture (those calls return QUIK_ERR_INVALID_ARGUMENT). Synchronous. */
 quik_status quik_ctx_reserve(quik_ctx_t ctx, quik_layer_t layer, int64_t M);

@@ -1242,8 +1242,14 @@ quik_status quik_gated_mlp_forward(quik_ctx_t ctx, quik_layer_t gated, quik_laye
         down_link.hstat = up_link.hstat;
         down_link.consume = true;
       }
-      return forward_impl(ctx, down, h, QUIK_F16, M, y, ydt, ldy, QUIK_V3_FUSED_EPILOGUE, st, none, nullptr, 0,
-                          down_link);
+      try {
+        return forward_impl(ctx, down, h, QUIK_F16, M, y, ydt, ldy, QUIK_V3_FUSED_EPILOGUE, st, none, nullptr, 0,
+                            down_link);
+      } catch (...) {
+        // the keys the gated epilogue posted were not consumed: restore them
+        if (emitted) launch_hstat_init(up_link.hstat, M, st);
+        throw;
+      }
     });
   });
 }
@@ -1585,6 +1591,7 @@ quik_status quik_ctx_reserve(quik_ctx_t ctx, quik_layer_t L, int64_t M) {
     ctx->scale.ensure(M * 4);
     ctx->zero.ensure(M * 4);
     if (L->opad) ctx->xo16.ensure(static_cast<size_t>(M * L->opad * 2));
+    if (L->gated) ctx->ensure_hstat(M, nullptr);  // quik_gated_mlp_forward statistics
     if (M <= 32 && L->kpad && !L->sparse) {  // decode kernel workspace + counters (zeroed)
       ctx->ensure_ws(static_cast<size_t>(M * N * 4), nullptr);
       ctx->ensure_s4_counters(quikb200::stream4_counter_count(N), nullptr);

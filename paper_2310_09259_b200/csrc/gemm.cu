@@ -776,7 +776,7 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
       // only if every zero-holding chunk's minimum is). Non-finite: error flag.
       const uint32_t fm = __ldg(&p.hmask[n0s >> 5]);
       const int t = t0 + lane;
-      if (fm != 0xFFFFFFFFu && t < p.M && !(p.dbg & 512)) {
+      if (fm != 0xFFFFFFFFu && t < p.M) {
         const uint16_t* rowh = reinterpret_cast<const uint16_t*>(hb) + lane * 32;
         const uint4* row4 = reinterpret_cast<const uint4*>(rowh);
         const uint32_t f0 = rowh[__ffs(~fm) - 1];
@@ -806,10 +806,8 @@ __global__ void __launch_bounds__(W4 ? kThreadsW4 : kThreads, 1) quik_gemm_kerne
           const uint32_t mag = u & 0x7FFFu;
           return ((u & 0x8000u) && mag) ? 0x7FFFu - mag : (mag | 0x8000u);
         };
-        if (!(p.dbg & 256)) {
-          atomicMin(&p.hstat[t].x, key(vmn));
-          atomicMax(&p.hstat[t].y, key(vmx));
-        }
+        atomicMin(&p.hstat[t].x, key(vmn));
+        atomicMax(&p.hstat[t].y, key(vmx));
         if (vmn == 0.0f) {  // rare: this chunk's first base zero (column, sign)
 #pragma unroll 1
           for (int f = 0; f < 32; ++f) {

@@ -137,3 +137,33 @@ def test_fused_mlp_llama7b_shape():
     up, gate, down, x = _mlp_layers(rng, 512, 4096, 11008, 4, 8, 256, 688)
     mlp = _blocks(up, gate, down)
     _check_block(mlp, torch.from_numpy(x).cuda().half(), torch)
+
+
+def test_fused_mlp_cuda_graph_replay():
+    """The block captured into a CUDA graph after quik_ctx_reserve (gated layer + down):
+    every replay consumes and restores the statistics keys, so replays with new inputs in
+    the captured buffer equal the unfused block."""
+    import torch
+
+    rng = np.random.default_rng(1600)
+    up, gate, down, x = _mlp_layers(rng, 192, 512, 640, 4, 8, 32, 48)
+    mlp = _blocks(up, gate, down)
+    xt = torch.from_numpy(x).cuda().half()
+    mlp.proj.reserve(xt.shape[0])
+    mlp.down.reserve(xt.shape[0])
+    y = torch.empty(xt.shape[0], down["out_features"], device="cuda", dtype=torch.float16)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        mlp.forward(xt, out=y)  # warm-up on the capture stream
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        mlp.forward(xt, out=y)
+    for k in range(3):
+        xt.copy_(torch.from_numpy(rng.normal(0, 1 + k, size=x.shape).astype(np.float16)).cuda())
+        g.replay()
+        torch.cuda.synchronize()
+        want = mlp.forward(xt, hidden_dtype=torch.float16, fused=False)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(y.cpu().numpy().view(np.uint16), want.cpu().numpy().view(np.uint16))
