@@ -385,6 +385,10 @@ def run_ours(args, w):
     layer = q.QuikLinear.from_device(outliers, base, sc, wr, ow, bits, sparse=sparse)
     if sparse and not layer.is_sparse:
         raise SystemExit("2:4 workload: layer did not compress")
+    # the same layer with ONE INT4 weight copy in HBM (weights="int4": every GEMM tile
+    # widens the INT4 tiles into TMEM), reported beside the headline's speed mode
+    layer4 = (q.QuikLinear.from_device(outliers, base, sc, wr, ow, bits, weights="int4")
+              if bits == 4 and not sparse and world == 1 and not args.no_cublas else None)
     check_cpu = rank == 0 and world == 1 and not args.no_cpu
     host = None
     if check_cpu:  # reference-format copy of the layer for the CPU reference leg (cpu_baseline + parity)
@@ -607,6 +611,7 @@ def run_ours(args, w):
 
     # ---- FP16 cuBLAS GEMM of the same (sharded) shape, same x
     fp16 = None
+    int4_weights = None
     if not args.no_cublas:
         Wf = torch.randn((ns, K), device=dev, dtype=torch.float16)
         out16 = torch.empty((M, ns), device=dev, dtype=torch.float16)
@@ -631,8 +636,28 @@ def run_ours(args, w):
                     note="torch.matmul f16 (cuBLAS) of the per-rank shape, same x; medians of per-step events")
         decode = decode_regime(torch, layer, xs_dev[0], Wf, ns, K, kb, O, bits, pk) if world == 1 else None
         del Wf, out16
+        if layer4 is not None:
+            for i in range(3):
+                layer4.forward(xs_dev[i % nbuf], out=y_local)
+            torch.cuda.synchronize()
+            for i in range(steps):
+                if flush:
+                    flush_buf.fill_(float(i))
+                ev_step[i][0].record()
+                layer4.forward(xs_dev[i % nbuf], out=y_local)
+                ev_step[i][1].record()
+            torch.cuda.synchronize()
+            t4 = statistics.median(a.elapsed_time(b) for a, b in ev_step)
+            int4_weights = dict(ms_median=t4, tops=ops_rank / (t4 * 1e-3) / 1e12, speedup_vs_cublas_f16=t16 / t4,
+                                device_bytes=layer4.device_bytes, speed_mode_device_bytes=layer.device_bytes,
+                                note="the same layer built with weights='int4' (one INT4 weight copy in HBM, widened "
+                                     "into TMEM inside every GEMM tile; quik_layer_create QUIK_WEIGHTS_INT4): "
+                                     "K1 + GEMM per step, median of per-step events; the headline runs speed mode "
+                                     "(an INT8 copy for prefill GEMMs)")
+        del layer4
     else:
         decode = None
+        del layer4
 
     # ---- e2e: host (pinned) buffers through the public API, copies inside the timed region
     e2e = None
@@ -726,7 +751,7 @@ def run_ours(args, w):
                                    f"MB), int8 weights {ns * ((kb + 127) // 128 * 128) / 1e6:.0f} MB, y "
                                    f"{M * ns * 2 / 1e6:.0f} MB; no flush")),
                    parity=parity, exchange=exchange, roofline=roofline, cpu_baseline=cpu, e2e=e2e, fp16_cublas=fp16, quantizer=quant,
-                   sustained=sustained, decode=decode,
+                   sustained=sustained, decode=decode, int4_weights=int4_weights,
                    clocks=clocks, gpu_launches=steps * q.QuikLinear.launches(),
                    precision="W%dA%d integer codes on tcgen05 kind::i8 (s32 accumulate) + f16 outliers (f32 accumulate), f16 out"
                              % (bits, bits))
