@@ -704,9 +704,10 @@ class QuikGatedMLP:
     one GEMM) followed by the down projection (its own K1 + GEMM)."""
 
     def __init__(self, up: QuikLinearLayer, gate: QuikLinearLayer, down: QuikLinearLayer,
-                 device: Optional[int] = None):
-        self.proj = QuikLinear.gated(up, gate, device)
-        self.down = QuikLinear(down, device)
+                 device: Optional[int] = None, weights: str = "speed"):
+        """weights: "speed" or "int4" for both projections (QuikLinear)."""
+        self.proj = QuikLinear.gated(up, gate, device, weights=weights)
+        self.down = QuikLinear(down, device, weights=weights)
         if self.down.in_features != self.proj.out_features:
             raise ValueError("gated MLP: down projection input != up/gate output features")
 

@@ -73,6 +73,23 @@ def test_fused_mlp_decode_regime_and_every_tile(tile):
         _check_block(mlp, xt, torch)
 
 
+def test_fused_mlp_int4_weights_mode():
+    """Both projections with one INT4 weight copy (weights="int4": the W4 GEMM tiles emit
+    the statistics) equal the speed-mode block bit for bit."""
+    m = q()
+    import torch
+
+    rng = np.random.default_rng(1700)
+    up, gate, down, x = _mlp_layers(rng, 300, 512, 384, 4, 4, 64, 32)
+    xt = torch.from_numpy(x).cuda().half()
+    a = _blocks(up, gate, down)
+    b = m.QuikGatedMLP(to_layer(up), to_layer(gate), to_layer(down), weights="int4")
+    _check_block(b, xt, torch)
+    ya, yb = a(xt), b(xt)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(ya.cpu().numpy().view(np.uint16), yb.cpu().numpy().view(np.uint16))
+
+
 def test_fused_mlp_signed_zero_minimum():
     """h == +-0 everywhere (zero up weights and bias): the down quantizer's minimum is a
     zero whose sign is the first base column's (runtime.cpp:44-48 strict comparisons),
