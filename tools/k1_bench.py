@@ -24,6 +24,8 @@ SHAPES = [  # name, M, K, O, bits
     ("cfg5 13B up", 2048, 5120, 256, 4),
     ("cfg4 OPT-66B fc2 W4", 2048, 36864, 256, 4),
     ("cfg4 Falcon-180B fc2 W8A8", 2048, 59392, 1024, 8),
+    ("cfg4 OPT-66B fc1", 2048, 9216, 256, 4),
+    ("cfg4 Falcon-180B fc1 / qkv", 2048, 14848, 256, 4),
 ]
 
 
