@@ -145,7 +145,7 @@ quik_status quik_layer_create_gated(quik_ctx_t ctx, const quik_weights_desc* up,
 /* Gated MLP block (reference forward_model with gated_mlp_ops,
  * runtime.cpp:373-388): y = down(silu(gate(x)) * up(x)). gated: a
  * quik_layer_create_gated layer, down: a plain layer with in_features = F.
- * h: device f16 [M][ldh] hidden state (written; ldh >= F); y: [M][ldy] of ydt.
+ * h: device f16 [M][ldh] hidden state (written; ldh >= F, any pitch); y: [M][ldy] of ydt.
  * Above the decode regime the gated GEMM's epilogue also reduces the down projection's
  * per-token min / max over the base (non-outlier) columns of the f16 h it stores, and
  * the down projection's quantizer consumes them instead of its own reduction pass

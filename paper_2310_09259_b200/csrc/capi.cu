@@ -363,13 +363,13 @@ void set_slices(QuantArgs& q, const quik_layer_s* L) {
 
 // Runs K1 into the context scratch (GEMM layout) for the hot path.
 void run_k1(quik_ctx_t ctx, const quik_layer_s* L, const void* x, quik_dtype xdt, int64_t M, cudaStream_t st,
-            uint4* pre_stat = nullptr) {
+            uint4* pre_stat = nullptr, int64_t ldx = 0) {
   QuantArgs q{};
   q.x = x;
   q.x_is_f32 = xdt == QUIK_F32;
   q.M = M;
   q.K = L->in_features;
-  q.ldx = L->in_features;
+  q.ldx = ldx ? ldx : L->in_features;  // x row pitch (elements)
   q.lane_mask = L->lane_mask;
   q.gather = L->gather;
   q.chunk_desc = L->chunk_desc;
@@ -1025,6 +1025,7 @@ struct MlpLink {
   const uint32_t* hmask = nullptr;
   bool* emitted = nullptr;
   bool consume = false;
+  int64_t ldx = 0;  // input row pitch (0: in_features), V3 / decode paths
 };
 
 quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dtype xdt, int64_t M, void* y,
@@ -1055,7 +1056,7 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
   if (decode) {
     // decode regime: K1 -> one kernel for the INT4 split-K GEMM and the fused epilogue
     // (dequant + outlier MMAs, stream4.cu); workspace / counters stay zeroed between calls
-    run_k1(ctx, L, x, xdt, M, st, pre);
+    run_k1(ctx, L, x, xdt, M, st, pre, link.ldx);
     mark(sm.after_quant, st);
     Stream4Args a{};
     a.w4 = L->bits == 4 ? L->w4 : nullptr;
@@ -1096,7 +1097,7 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
     }();
     const bool mid_w4 = !L->int4_only && L->bits == 4 && !L->sparse && !g_probe_mode && M <= w4_mid_m &&
                         ensure_w4(L, st);
-    run_k1(ctx, L, x, xdt, M, st, pre);
+    run_k1(ctx, L, x, xdt, M, st, pre, link.ldx);
     mark(sm.after_quant, st);
     GemmArgs gm = gemm_args(ctx, L, M);
     if (mid_w4) gm.w4 = L->w4;
@@ -1153,7 +1154,7 @@ quik_status forward_impl(quik_ctx_t ctx, quik_layer_t L, const void* x, quik_dty
     q.err = ctx->d_err;
     check_launch(launch_quantize(q, st), "quantize kernel");
   } else {
-    run_k1(ctx, L, x, xdt, M, st, pre);
+    run_k1(ctx, L, x, xdt, M, st, pre, link.ldx);
   }
   mark(sm.after_quant, st);
   // V1/V2 tail: the int32 accumulator through global memory, then the same
@@ -1242,6 +1243,7 @@ quik_status quik_gated_mlp_forward(quik_ctx_t ctx, quik_layer_t gated, quik_laye
         down_link.hstat = up_link.hstat;
         down_link.consume = true;
       }
+      down_link.ldx = ldh;
       try {
         return forward_impl(ctx, down, h, QUIK_F16, M, y, ydt, ldy, QUIK_V3_FUSED_EPILOGUE, st, none, nullptr, 0,
                             down_link);

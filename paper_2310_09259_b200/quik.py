@@ -719,8 +719,10 @@ class QuikGatedMLP:
         fused=False runs them separately)."""
         return self.forward_with_hidden(x, out, out_dtype, hidden_dtype, fused)[0]
 
-    def forward_with_hidden(self, x, out=None, out_dtype=None, hidden_dtype=None, fused: bool = True):
-        """forward() that also returns the hidden state h: (y, h)."""
+    def forward_with_hidden(self, x, out=None, out_dtype=None, hidden_dtype=None, fused: bool = True,
+                            hidden=None):
+        """forward() that also returns the hidden state h: (y, h). hidden: optional f16
+        [M][>= F] row-major buffer for h (any row pitch >= F; the fused path)."""
         torch = _torch()
         hd = hidden_dtype or x.dtype
         if hd != torch.float16 or not fused:
@@ -732,7 +734,9 @@ class QuikGatedMLP:
             raise ValueError("quik_matmul: input must be float16 or float32")
         x = x.contiguous()
         M = x.shape[0]
-        h = self.proj._check_out(torch, x, None, torch.float16, "gated MLP")
+        h = self.proj._check_out(torch, x, hidden, torch.float16, "gated MLP")
+        if h.dtype != torch.float16:
+            raise ValueError("gated MLP: the hidden state must be float16")
         out = self.down._check_out(torch, x, out, out_dtype, "gated MLP")
         ydt = _lib.QUIK_F16 if out.dtype == torch.float16 else _lib.QUIK_F32
         xdt = _lib.QUIK_F16 if x.dtype == torch.float16 else _lib.QUIK_F32

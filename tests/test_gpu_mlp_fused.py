@@ -184,3 +184,23 @@ def test_fused_mlp_cuda_graph_replay():
         want = mlp.forward(xt, hidden_dtype=torch.float16, fused=False)
         torch.cuda.synchronize()
         np.testing.assert_array_equal(y.cpu().numpy().view(np.uint16), want.cpu().numpy().view(np.uint16))
+
+
+def test_fused_mlp_hidden_row_pitch():
+    """h in a caller buffer with a row pitch > F (16-byte multiple: the statistics and the
+    prescaled down K1 at that pitch; not a multiple: the plain path)."""
+    import torch
+
+    rng = np.random.default_rng(1800)
+    up, gate, down, x = _mlp_layers(rng, 200, 512, 384, 4, 8, 64, 32)
+    mlp = _blocks(up, gate, down)
+    xt = torch.from_numpy(x).cuda().half()
+    want, hw = mlp.forward_with_hidden(xt, fused=False)
+    for pad in (40, 4):
+        buf = torch.full((xt.shape[0], 384 + pad), 7.0, device="cuda", dtype=torch.float16)
+        y, h = mlp.forward_with_hidden(xt, hidden=buf[:, :384])
+        torch.cuda.synchronize()
+        assert h.stride(0) == 384 + pad
+        np.testing.assert_array_equal(h.cpu().numpy().view(np.uint16), hw.cpu().numpy().view(np.uint16))
+        np.testing.assert_array_equal(y.cpu().numpy().view(np.uint16), want.cpu().numpy().view(np.uint16))
+        assert torch.all(buf[:, 384:] == 7.0)
