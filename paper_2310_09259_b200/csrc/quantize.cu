@@ -555,6 +555,9 @@ __global__ void __launch_bounds__(VPT >= 4 ? 512 : 256) quantize_hot_kernel(cons
     }
   }
 
+  // prescaled: every thread that reads the keys (written by the previous kernel) waits on
+  // the programmatic dependency itself (the others only consume TMA data issued after it)
+  if (pre) asm volatile("griddepcontrol.wait;" ::: "memory");
   int s = 0;
   uint32_t ph = 0;
 #pragma unroll 1
