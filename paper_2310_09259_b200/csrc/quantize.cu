@@ -476,8 +476,12 @@ __device__ __forceinline__ float hkey_to_float(uint32_t k) {
   return __half2float(__ushort_as_half(static_cast<unsigned short>(u)));
 }
 
-template <int BITS, int VPT, bool FULL>
-__global__ void __launch_bounds__(VPT >= 4 ? 512 : 256) quantize_hot_kernel(const QuantArgs a, int stages, int row_stride) {
+// FILL: no per-thread lane masks (48 registers at VPT 8): each row's outlier columns are
+// overwritten in the ring slot by the row's first base value (a value of the base set,
+// so it cannot move the base min / max, and a zero there carries the first base zero's
+// sign) behind one more block barrier, so the kernel fits two CTAs per SM.
+template <int BITS, int VPT, bool FULL, bool FILL>
+__device__ __forceinline__ void quantize_hot_body(const QuantArgs& a, int stages, int row_stride) {
   extern __shared__ __align__(128) uint8_t s_dyn[];
   __shared__ float s_min[16], s_max[16];
   __shared__ int s_nf[16];
@@ -501,11 +505,11 @@ __global__ void __launch_bounds__(VPT >= 4 ? 512 : 256) quantize_hot_kernel(cons
   // the ring
   const int code_stride = (kr16 + 32 + 127) & ~127;
   // prescaled rows (a.pre_stat: min / max from the producing GEMM's epilogue): no
-  // reduction barrier, so the code row is double-buffered (row t+1's codes may be
-  // written while row t's are still being compacted) and the ring slot is refilled at (B)
+  // reduction pass; barrier A stays (it orders row t's compaction reads before row
+  // t+1's code writes and frees the ring slot)
   uint4* const pre = a.pre_stat;
   uint8_t* s_codes = s_dyn;                          // [code_stride]: codes by column, zero tail
-  uint8_t* s_ring = s_dyn + code_stride * (pre ? 2 : 1);  // [stages][row_stride]
+  uint8_t* s_ring = s_dyn + code_stride;             // [stages][row_stride]
   const bool has_out = a.lane_mask != nullptr;
   const int nchunk = static_cast<int>(a.kpad >> 4);
   const __half* xg = reinterpret_cast<const __half*>(a.x);
@@ -515,12 +519,13 @@ __global__ void __launch_bounds__(VPT >= 4 ? 512 : 256) quantize_hot_kernel(cons
   // row-independent: outlier lane masks of this thread's vectors, the byte mask (lm, the
   // rare exact paths) and its expansion to one 16-bit lane mask per f16 (lmw, pass 1:
   // one LOP3 per word instead of a PRMT + LOP3)
-  uint2 lm[VPT];
-  uint4 lmw[VPT];
+  constexpr int kLm = FILL ? 1 : VPT;
+  uint2 lm[kLm];
+  uint4 lmw[kLm];
 #pragma unroll
-  for (int i = 0; i < VPT; ++i) {
+  for (int i = 0; i < kLm; ++i) {
     const int v = tid + i * nt;
-    lm[i] = (has_out && in_row(v)) ? __ldg(reinterpret_cast<const uint2*>(a.lane_mask) + v) : make_uint2(0u, 0u);
+    lm[i] = (!FILL && has_out && in_row(v)) ? __ldg(reinterpret_cast<const uint2*>(a.lane_mask) + v) : make_uint2(0u, 0u);
     lmw[i] = make_uint4(__byte_perm(lm[i].x, 0u, 0x1100u), __byte_perm(lm[i].x, 0u, 0x3322u),
                         __byte_perm(lm[i].y, 0u, 0x1100u), __byte_perm(lm[i].y, 0u, 0x3322u));
   }
@@ -540,7 +545,6 @@ __global__ void __launch_bounds__(VPT >= 4 ? 512 : 256) quantize_hot_kernel(cons
     fence_mbar_init();
   }
   if (tid < 8) reinterpret_cast<uint32_t*>(s_codes + kr16)[tid] = 0u;  // zero tail
-  if (pre && tid >= 8 && tid < 16) reinterpret_cast<uint32_t*>(s_codes + code_stride + kr16)[tid - 8] = 0u;
   __syncthreads();
   if (tid == 0) {
     // PDL: everything above (tables, barriers) overlapped the previous kernel; its
@@ -569,10 +573,12 @@ __global__ void __launch_bounds__(VPT >= 4 ? 512 : 256) quantize_hot_kernel(cons
     if (pre) pst = __ldcg(pre + t);  // issued early: its latency overlaps the row loads
 
     uint4 raw[VPT];
+    if constexpr (!FILL) {
 #pragma unroll
-    for (int i = 0; i < VPT; ++i) {
-      const int v = tid + i * nt;
-      raw[i] = in_row(v) ? srow[v] : make_uint4(0, 0, 0, 0);
+      for (int i = 0; i < VPT; ++i) {
+        const int v = tid + i * nt;
+        raw[i] = in_row(v) ? srow[v] : make_uint4(0, 0, 0, 0);
+      }
     }
     // this row's outlier values (the ring slot is refilled at barrier A)
     uint16_t xov[2] = {0, 0};
@@ -581,20 +587,27 @@ __global__ void __launch_bounds__(VPT >= 4 ? 512 : 256) quantize_hot_kernel(cons
       for (int j = 0; j < 2; ++j)
         if (osrc[j] >= 0) xov[j] = reinterpret_cast<const uint16_t*>(srow)[osrc[j]];
     }
-    float vmin, vmax;
+    if constexpr (FILL) {
+      // outlier columns := the first base value (each thread its own slots, after reading
+      // them above; the non-hoisted outlier copy reads x from global memory)
+      if (has_out && !pre) {
+        uint16_t* hrow = reinterpret_cast<uint16_t*>(s_ring + s * row_stride);
+        const uint16_t h0 = hrow[first_base];  // a base column: never overwritten
+        for (int i = tid; i < a.n_out; i += nt) hrow[__ldg(&a.out_src[i])] = h0;
+        __syncthreads();  // (F)
+      }
+#pragma unroll
+      for (int i = 0; i < VPT; ++i) {
+        const int v = tid + i * nt;
+        raw[i] = in_row(v) ? srow[v] : make_uint4(0, 0, 0, 0);
+      }
+    }
+    float vmin = 0.f, vmax = 0.f;
     int nonfinite = 0;
-    if (pre) {
-      // the epilogue's keys (kernels.h): exact f16 values; a zero minimum takes the sign
-      // of the first zero (its column in the key's upper bits); non-finite values were
-      // flagged by the epilogue
-      vmin = hkey_to_float(pst.x);
-      vmax = hkey_to_float(pst.y);
-      if (kb == 0) { vmin = 0.f; vmax = 0.f; }
-      if (vmin == 0.0f && kb > 0 && pst.z != 0xFFFFFFFFu) vmin = (pst.z & 1u) ? -0.0f : 0.0f;
-    } else {
+    if (!pre) {
     // ---- pass 1: packed min / max over the base columns
     __half2 hmin = u2h2(0x7C007C00u), hmax = u2h2(0xFC00FC00u);
-    if (has_out) {
+    if (has_out && !FILL) {
       const uint32_t h0 = reinterpret_cast<const uint16_t*>(srow)[first_base];
       const uint32_t fill = h0 | (h0 << 16);  // a base value of this row, in both halves
 #pragma unroll
@@ -602,7 +615,7 @@ __global__ void __launch_bounds__(VPT >= 4 ? 512 : 256) quantize_hot_kernel(cons
         if (!in_row(tid + i * nt)) continue;
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
-          const uint32_t mk = (&lmw[i].x)[w];
+          const uint32_t mk = (&lmw[FILL ? 0 : i].x)[w];
           const __half2 x2 = u2h2(((&raw[i].x)[w] & ~mk) | (fill & mk));
           hmin = __hmin2_nan(hmin, x2);
           hmax = __hmax2_nan(hmax, x2);
@@ -632,6 +645,7 @@ __global__ void __launch_bounds__(VPT >= 4 ? 512 : 256) quantize_hot_kernel(cons
     vmax = redux_max(vmax);
     nonfinite = __reduce_or_sync(0xffffffffu, nonfinite);
     if ((tid & 31) == 0) { s_min[tid >> 5] = vmin; s_max[tid >> 5] = vmax; s_nf[tid >> 5] = nonfinite; }
+    }
     __syncthreads();  // (A): every thread is done with the previous row and holds this one in registers
     if (tid == 0) {
       // refill this row's ring slot: after A nothing reads it (row in registers,
@@ -643,6 +657,15 @@ __global__ void __launch_bounds__(VPT >= 4 ? 512 : 256) quantize_hot_kernel(cons
         bulk_load_1d(s_ring + s * row_stride, xg + static_cast<int64_t>(rn) * a.ldx, row_bytes, &s_full[s]);
       }
     }
+    if (pre) {
+      // the epilogue's keys (kernels.h): exact f16 values; a zero minimum takes the sign
+      // of the first zero (its column in the key's upper bits); non-finite values were
+      // flagged by the epilogue
+      vmin = hkey_to_float(pst.x);
+      vmax = hkey_to_float(pst.y);
+      if (kb == 0) { vmin = 0.f; vmax = 0.f; }
+      if (vmin == 0.0f && kb > 0 && pst.z != 0xFFFFFFFFu) vmin = (pst.z & 1u) ? -0.0f : 0.0f;
+    } else {
     {
       const int l = tid & 31;
       vmin = redux_min(l < nwarps ? s_min[l] : INFINITY);
@@ -660,7 +683,8 @@ __global__ void __launch_bounds__(VPT >= 4 ? 512 : 256) quantize_hot_kernel(cons
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const float x = elem<__half>(raw[i], e);
-          const uint32_t mbyte = ((e < 4 ? lm[i].x : lm[i].y) >> (8 * (e & 3))) & 0xFFu;
+          uint32_t mbyte = 0u;
+          if constexpr (!FILL) mbyte = ((e < 4 ? lm[i].x : lm[i].y) >> (8 * (e & 3))) & 0xFFu;
           if (mbyte == 0 && x == 0.0f) {
             const unsigned k = (static_cast<unsigned>(v * 8 + e) << 1) | (__float_as_uint(x) >> 31);
             key = k < key ? k : key;
@@ -747,16 +771,7 @@ __global__ void __launch_bounds__(VPT >= 4 ? 512 : 256) quantize_hot_kernel(cons
       }
     }
     __syncthreads();  // (B) codes complete
-    if (pre && tid == 0) {
-      // prescaled: every thread holds the row (and its outlier values) since before (B)
-      const int rn = t + stages * gridDim.x;
-      if (rn < M) {
-        fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&s_full[s], row_bytes);
-        bulk_load_1d(s_ring + s * row_stride, xg + static_cast<int64_t>(rn) * a.ldx, row_bytes, &s_full[s]);
-      }
-      pre[t] = make_uint4(0xFFFFFFFFu, 0u, 0xFFFFFFFFu, 0u);  // initial keys for the next forward
-    }
+    if (pre && tid == 0) pre[t] = make_uint4(0xFFFFFFFFu, 0u, 0xFFFFFFFFu, 0u);  // initial keys, next forward
     // this row's compaction descriptors (row-independent, L1-resident): all loads in
     // flight before the outlier gather instead of one at a time in the copy-out loop
     constexpr int kCk = VPT > 1 ? VPT / 2 : 1;
@@ -814,8 +829,17 @@ __global__ void __launch_bounds__(VPT >= 4 ? 512 : 256) quantize_hot_kernel(cons
       dst[cidx] = make_uint4(w[0], w[1], w[2], w[3]);
     }
     if (++s == stages) { s = 0; ph ^= 1u; }
-    if (pre) s_codes = s_dyn + (s_codes == s_dyn ? code_stride : 0);
   }
+}
+
+template <int BITS, int VPT, bool FULL>
+__global__ void __launch_bounds__(VPT >= 4 ? 512 : 256) quantize_hot_kernel(const QuantArgs a, int stages, int row_stride) {
+  quantize_hot_body<BITS, VPT, FULL, false>(a, stages, row_stride);
+}
+template <int BITS, int VPT, bool FULL>
+__global__ void __launch_bounds__(VPT >= 4 ? 512 : 256, 2) quantize_hot_fill_kernel(const QuantArgs a, int stages,
+                                                                                      int row_stride) {
+  quantize_hot_body<BITS, VPT, FULL, true>(a, stages, row_stride);
 }
 
 // Wide rows (K beyond one CTA's ring: OPT-66B fc2 36864, Falcon-180B fc2 59392, the
@@ -1426,8 +1450,8 @@ cudaError_t launch_quantize_hot(const QuantArgs& a, cudaStream_t stream) {
   while (vpt < 8 && (nvec + vpt - 1) / vpt > 128) vpt *= 2;
   // an exact fit (FULL: no bounds checks, fewer registers) wins over the 4-warp target:
   // the exact fit with the fewest threads >= 128, else the one with the most threads
-  // (4-vector rows up to 512 threads: K = 9216 / 11008 / 14848 fit exactly at 288 / 344 /
-  // 464 threads; OPT-66B fc1 K1 20.7 -> 19.8 us, the others unchanged)
+  // (4-vector rows up to 512 threads: K = 9216 fits exactly at 288 threads, OPT-66B fc1
+  // K1 20.7 -> 19.8 us)
   int best = 0;
   int64_t best_thr = 0;
   for (int v = 1; v <= 8; v *= 2) {
@@ -1457,10 +1481,26 @@ cudaError_t launch_quantize_hot(const QuantArgs& a, cudaStream_t stream) {
     const char* e = getenv("QUIK_K1_RING_KB");
     return e ? atoi(e) : 32;
   }();
+  // One ring stage by default: a slot is refilled at barrier A of its own row, so one
+  // stage still overlaps the next row's load with this row's codes, and the smaller CTA
+  // fits more CTAs per SM (measured, k1_bench: 70B down 110.7 -> 96.6 us with FILL below,
+  // 7B down 33.9 -> 27.6, cfg3 28.0 -> 27.4, 7B q/k/v/o 10.9 -> 10.4). QUIK_K1_STAGES=n
+  // forces n stages, QUIK_K1_STAGES=0 the ring_kb rule above.
   int stages = static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(8, (ring_kb * 1024) / row_stride)));
-  const int code_bufs = a.pre_stat ? 2 : 1;  // prescaled rows: double-buffered code row
-  while (stages > 1 && code_bufs * codes + stages * row_stride > 200 * 1024) --stages;
-  const int smem = code_bufs * codes + stages * row_stride;
+  static const int stages_env = [] {
+    const char* e = getenv("QUIK_K1_STAGES");
+    return e ? atoi(e) : 1;
+  }();
+  if (stages_env >= 1 && stages_env <= 8) stages = stages_env;
+  // VPT 8 rows run the FILL kernel (no lane-mask registers: 64 instead of 106-121, two
+  // CTAs per SM); QUIK_K1_FILL=0 keeps the masks in registers
+  static const int fill_env = [] {
+    const char* e = getenv("QUIK_K1_FILL");
+    return e ? atoi(e) : 1;
+  }();
+  const bool fill = fill_env != 0 && vpt == 8;
+  while (stages > 1 && codes + stages * row_stride > 200 * 1024) --stages;
+  const int smem = codes + stages * row_stride;
   const bool full = static_cast<int64_t>(threads) * vpt == nvec;
   static const int wait_env = [] {  // tuning knob: QUIK_K1_WAIT=1 sleep-waits on the row ring
     const char* e = getenv("QUIK_K1_WAIT");
@@ -1477,7 +1517,8 @@ cudaError_t launch_quantize_hot(const QuantArgs& a, cudaStream_t stream) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
 #define QUIK_QH_LAUNCH(V)                                                                                  \
   do {                                                                                                     \
-    auto kern = full ? quantize_hot_kernel<B, V, true> : quantize_hot_kernel<B, V, false>;                  \
+    auto kern = fill ? (full ? quantize_hot_fill_kernel<B, V, true> : quantize_hot_fill_kernel<B, V, false>)      \
+                     : (full ? quantize_hot_kernel<B, V, true> : quantize_hot_kernel<B, V, false>);             \
     cudaError_t e = ensure_smem_attr(kern, smem);                                                          \
     if (e != cudaSuccess) return e;                                                                        \
     int per_sm = 0;                                                                                        \
