@@ -855,7 +855,11 @@ __global__ void __launch_bounds__(VPT >= 4 ? 512 : 256, 2) quantize_hot_fill_ker
 // then stay inside the CTA. The rare exact paths (near-tie quotients; the sign of a zero
 // minimum, which takes a second cluster exchange of the first zero's key) match the hot
 // kernel's, so the codes are bit-identical to it and to the reference.
-template <int BITS, int VPT>
+// FILL (as the hot kernel's): no lane-mask registers; the slice's outlier columns (its
+// own slots and the < 8 overlap columns past them) are overwritten in the ring slot by
+// the slice's first base value, and the rare first-zero scan skips the columns before
+// it (outliers or the previous slice's base columns, which that slice scans).
+template <int BITS, int VPT, bool FILL>
 __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_wide_kernel(const QuantArgs a, int stages, int row_stride) {
   extern __shared__ __align__(128) uint8_t s_dyn[];
   __shared__ float s_min[16], s_max[16];
@@ -892,12 +896,14 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_wide_kernel(con
   const int first_base = static_cast<int>(a.gather[16 * ch_lo]) - in_lo;  // a base column of the slice
   const int cl = blockIdx.x / C, ncl = gridDim.x / C;
 
-  uint2 lm[VPT];
-  uint4 lmw[VPT];
+  constexpr int kLm = FILL ? 1 : VPT;
+  uint2 lm[kLm];
+  uint4 lmw[kLm];
 #pragma unroll
-  for (int i = 0; i < VPT; ++i) {
+  for (int i = 0; i < kLm; ++i) {
     const int v = tid + i * nt;
-    lm[i] = (has_out && in_row(v)) ? __ldg(reinterpret_cast<const uint2*>(a.lane_mask + in_lo) + v) : make_uint2(0u, 0u);
+    lm[i] = (!FILL && has_out && in_row(v)) ? __ldg(reinterpret_cast<const uint2*>(a.lane_mask + in_lo) + v)
+                                             : make_uint2(0u, 0u);
     lmw[i] = make_uint4(__byte_perm(lm[i].x, 0u, 0x1100u), __byte_perm(lm[i].x, 0u, 0x3322u),
                         __byte_perm(lm[i].y, 0u, 0x1100u), __byte_perm(lm[i].y, 0u, 0x3322u));
   }
@@ -939,16 +945,35 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_wide_kernel(con
     const uint4* srow = reinterpret_cast<const uint4*>(s_ring + s * row_stride);
     mbar_wait(&s_full[s], ph);
     uint4 raw[VPT];
+    if constexpr (!FILL) {
 #pragma unroll
-    for (int i = 0; i < VPT; ++i) {
-      const int v = tid + i * nt;
-      raw[i] = in_row(v) ? srow[v] : make_uint4(0, 0, 0, 0);
+      for (int i = 0; i < VPT; ++i) {
+        const int v = tid + i * nt;
+        raw[i] = in_row(v) ? srow[v] : make_uint4(0, 0, 0, 0);
+      }
     }
     uint16_t xov[2] = {0, 0};
     if (a.xo16 && xo_hoisted) {
 #pragma unroll
       for (int j = 0; j < 2; ++j)
         if (osrc[j] >= 0) xov[j] = reinterpret_cast<const uint16_t*>(srow)[osrc[j]];
+    }
+    if constexpr (FILL) {
+      if (has_out) {
+        uint16_t* hrow = reinterpret_cast<uint16_t*>(s_ring + s * row_stride);
+        const uint16_t h0 = hrow[first_base];  // a base column: never overwritten
+        const int i_end = o_hi + 8 < static_cast<int>(a.n_out) ? o_hi + 8 : static_cast<int>(a.n_out);
+        for (int i = o_lo + tid; i < i_end; i += nt) {
+          const int col = __ldg(&a.out_src[i]) - in_lo;
+          if (col >= 0 && col < in_n) hrow[col] = h0;
+        }
+        __syncthreads();  // (F)
+      }
+#pragma unroll
+      for (int i = 0; i < VPT; ++i) {
+        const int v = tid + i * nt;
+        raw[i] = in_row(v) ? srow[v] : make_uint4(0, 0, 0, 0);
+      }
     }
     // ---- pass 1: packed min / max over the slice's base columns
     __half2 hmin = u2h2(0x7C007C00u), hmax = u2h2(0xFC00FC00u);
@@ -960,7 +985,7 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_wide_kernel(con
         if (!in_row(tid + i * nt)) continue;
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
-          const uint32_t mk = (&lmw[i].x)[w];
+          const uint32_t mk = FILL ? 0u : (&lmw[FILL ? 0 : i].x)[w];
           const __half2 x2 = u2h2(((&raw[i].x)[w] & ~mk) | (fill & mk));
           hmin = __hmin2_nan(hmin, x2);
           hmax = __hmax2_nan(hmax, x2);
@@ -1021,7 +1046,9 @@ __global__ void __launch_bounds__(VPT >= 8 ? 512 : 256) quantize_wide_kernel(con
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const float x = elem<__half>(raw[i], e);
-          const uint32_t mbyte = ((e < 4 ? lm[i].x : lm[i].y) >> (8 * (e & 3))) & 0xFFu;
+          uint32_t mbyte = 0u;
+          if constexpr (!FILL) mbyte = ((e < 4 ? lm[i].x : lm[i].y) >> (8 * (e & 3))) & 0xFFu;
+          else mbyte = (v * 8 + e < first_base) ? 1u : 0u;
           if (mbyte == 0 && x == 0.0f) {
             const unsigned k = (static_cast<unsigned>(in_lo + v * 8 + e) << 1) | (__float_as_uint(x) >> 31);
             key = k < key ? k : key;
@@ -1565,14 +1592,28 @@ cudaError_t launch_quantize_wide(const QuantArgs& a, cudaStream_t stream) {
   if (threads > (vpt >= 8 ? 512 : 256)) return cudaErrorNotSupported;
   const int row_stride = static_cast<int>(round_up(static_cast<int64_t>(a.slice_cols_max) * 2, 128));
   int stages = static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(8, (32 * 1024) / row_stride)));
+  // one ring stage by default (as the hot kernel; with the FILL kernel below: OPT-66B
+  // fc2 82.4 -> 70.0 us, Falcon-180B fc2 139.0 -> 117.4); QUIK_K1_WIDE_STAGES=n forces n,
+  // =0 the 32 KB rule above
+  static const int wstages_env = [] {
+    const char* e = getenv("QUIK_K1_WIDE_STAGES");
+    return e ? atoi(e) : 1;
+  }();
+  if (wstages_env >= 1 && wstages_env <= 8) stages = wstages_env;
   while (stages > 1 && a.slice_code_bytes + stages * row_stride > 200 * 1024) --stages;
   const int smem = a.slice_code_bytes + stages * row_stride;
+  // FILL kernel for eight-vector slices (no lane-mask registers; QUIK_K1_WIDE_FILL=0 off)
+  static const int wfill_env = [] {
+    const char* e = getenv("QUIK_K1_WIDE_FILL");
+    return e ? atoi(e) : 1;
+  }();
+  const bool wfill = wfill_env != 0 && vpt == 8;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
 #define QUIK_QW_LAUNCH(V)                                                                                   \
   do {                                                                                                      \
-    auto kern = quantize_wide_kernel<B, V>;                                                                 \
+    auto kern = wfill ? quantize_wide_kernel<B, V, true> : quantize_wide_kernel<B, V, false>;               \
     cudaError_t e = ensure_smem_attr(kern, smem);                                                           \
     if (e != cudaSuccess) return e;                                                                         \
     cudaLaunchConfig_t cfg{};                                                                               \
