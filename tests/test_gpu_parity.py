@@ -619,6 +619,33 @@ def test_hot_quantizer_ties_zeros_and_shapes():
         _hot_k1_case(m, o, x, idx, 4 if K == 8192 else 8)
 
 
+def test_hot_quantizer_eight_vector_rows_outlier_fill():
+    """Rows of eight 16-byte vectors per thread (K = 8192 / 11008 / 28672: the kernel that
+    overwrites a row's outlier columns in shared memory with its first base value
+    instead of holding lane masks in registers): outliers holding the row's extreme
+    values, outliers before the first base column, zero minima whose first base zero is
+    the first base column (-0 / +0) with zeros of the other sign at outlier columns and
+    later base columns, constant rows, many rows per CTA."""
+    m = q()
+    o = oracle()
+    rng = np.random.default_rng(7400)
+    for K, O, bits, M in [(8192, 256, 4, 600), (11008, 688, 8, 300), (28672, 896, 8, 400)]:
+        idx = np.sort(np.concatenate([np.arange(0, 5), rng.choice(np.arange(5, K), size=O - 5, replace=False)]))
+        base = np.setdiff1d(np.arange(K), idx)
+        x = rng.normal(0, 1, size=(M, K)).astype(np.float16)
+        x[0, idx[7]] = -1000.0   # an outlier below every base value
+        x[1, idx[9]] = 1000.0    # an outlier above every base value
+        for r, (first, other) in ((2, (-0.0, 0.0)), (3, (0.0, -0.0))):
+            x[r] = np.abs(x[r]) + np.float16(0.25)
+            x[r, base[0]] = first                      # the first base column is the zero minimum
+            x[r, base[len(base) // 2]] = other         # a later base zero of the other sign
+            x[r, idx[:5]] = other                      # outlier zeros before it, other sign
+        x[4] = np.float16(1.5)                         # constant row
+        x[5, base] = np.float16(-0.0)                  # all-zero base row, -0 first
+        x[5, idx] = np.float16(3.0)
+        _hot_k1_case(m, o, x, idx.astype(np.int64), bits)
+
+
 def test_wide_quantizer_cluster_slices_bit_exact():
     """K1 for wide rows (K > 32768: each row split over a thread-block cluster, one CTA
     per slice, min / max exchanged through distributed shared memory) against the oracle:
