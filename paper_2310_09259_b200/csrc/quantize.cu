@@ -564,6 +564,11 @@ __device__ __forceinline__ void quantize_hot_body(const QuantArgs& a, int stages
   if (pre) asm volatile("griddepcontrol.wait;" ::: "memory");
   int s = 0;
   uint32_t ph = 0;
+  // FILL: the next row's outlier overwrite is done before barrier B of the current row
+  // (once its load has landed), so B doubles as its barrier F; `prepared` marks a row
+  // whose slot is already overwritten, xov_next holds its outlier values
+  bool prepared = false;
+  uint16_t xov_next[2] = {0, 0};
 #pragma unroll 1
   for (int t = blockIdx.x; t < M; t += gridDim.x) {
     const uint4* srow = reinterpret_cast<const uint4*>(s_ring + s * row_stride);
@@ -582,7 +587,10 @@ __device__ __forceinline__ void quantize_hot_body(const QuantArgs& a, int stages
     }
     // this row's outlier values (the ring slot is refilled at barrier A)
     uint16_t xov[2] = {0, 0};
-    if (a.xo16 && xo_hoisted) {
+    if (prepared) {
+      xov[0] = xov_next[0];
+      xov[1] = xov_next[1];
+    } else if (a.xo16 && xo_hoisted) {
 #pragma unroll
       for (int j = 0; j < 2; ++j)
         if (osrc[j] >= 0) xov[j] = reinterpret_cast<const uint16_t*>(srow)[osrc[j]];
@@ -590,7 +598,7 @@ __device__ __forceinline__ void quantize_hot_body(const QuantArgs& a, int stages
     if constexpr (FILL) {
       // outlier columns := the first base value (each thread its own slots, after reading
       // them above; the non-hoisted outlier copy reads x from global memory)
-      if (has_out && !pre) {
+      if (has_out && !pre && !prepared) {
         uint16_t* hrow = reinterpret_cast<uint16_t*>(s_ring + s * row_stride);
         const uint16_t h0 = hrow[first_base];  // a base column: never overwritten
         for (int i = tid; i < a.n_out; i += nt) hrow[__ldg(&a.out_src[i])] = h0;
@@ -770,7 +778,28 @@ __device__ __forceinline__ void quantize_hot_body(const QuantArgs& a, int stages
         }
       }
     }
-    __syncthreads();  // (B) codes complete
+    if constexpr (FILL) {
+      // the next row of this CTA: wait for its slot, take its outlier values, overwrite
+      // its outlier columns; barrier B below then orders these stores before its raw loads
+      const int tn = t + static_cast<int>(gridDim.x);
+      prepared = false;
+      if (has_out && !pre && tn < M) {
+        const int sn = s + 1 == stages ? 0 : s + 1;
+        const uint32_t phn = s + 1 == stages ? ph ^ 1u : ph;
+        if (a.hot_flags & 1) mbar_wait_sleep(&s_full[sn], phn);
+        else mbar_wait(&s_full[sn], phn);
+        uint16_t* hn = reinterpret_cast<uint16_t*>(s_ring + sn * row_stride);
+        if (a.xo16 && xo_hoisted) {
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+            if (osrc[j] >= 0) xov_next[j] = hn[osrc[j]];
+        }
+        const uint16_t h0n = hn[first_base];
+        for (int i = tid; i < a.n_out; i += nt) hn[__ldg(&a.out_src[i])] = h0n;
+        prepared = true;
+      }
+    }
+    __syncthreads();  // (B) codes complete (FILL: and the next row's outlier columns overwritten)
     if (pre && tid == 0) pre[t] = make_uint4(0xFFFFFFFFu, 0u, 0xFFFFFFFFu, 0u);  // initial keys, next forward
     // this row's compaction descriptors (row-independent, L1-resident): all loads in
     // flight before the outlier gather instead of one at a time in the copy-out loop
